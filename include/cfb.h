@@ -1,0 +1,126 @@
+/*
+ * cfb.h — C ABI of libcfb.so, the B200 (sm_100a) ClusterFusion decode-step library.
+ *
+ * Plain pointers and sizes only; no torch types.  All device pointers are
+ * caller-owned CUDA device memory; `stream` is a cudaStream_t passed as void*.
+ * Every entry point is stream-ordered, allocates nothing on the hot path and
+ * returns CFB_OK or a negative status; cfb_last_error() holds the message of
+ * the calling thread's last failure.  Status codes map onto the reference's
+ * exception hierarchy (pkg/src/clusterdec/errors.py:4-33), see cfb_status.
+ *
+ * Reference interfaces replaced (paths relative to /root/reference/pkg/src/clusterdec):
+ *   cfb_mha_decode         <- dataflows.py:235-313  run_fused_mha_decode  (split_token, Alg. 3)
+ *   cfb_mla_decode         <- dataflows.py:316-429  run_fused_mla_decode  (fused_mla, App. B.1)
+ *   cfb_splithead_decode   <- dataflows.py:432-502  run_splithead_decode  (split_head, App. B.2)
+ *   cfb_ffn_decode         <- oracle.py:112-131     ffn_reference(..., "silu") fused into one launch
+ *   cfb_cluster_collective <- collectives.py:110-203 cluster_reduce / cluster_gather (DSMEM KAT kernel)
+ *   cfb_lm_head_argmax, cfb_embed, cfb_llama_*  <- no reference counterpart (SPEC.md:298 non-goals);
+ *                            the north-star decode loop around the fused modules.
+ */
+#ifndef CFB_H_
+#define CFB_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (errors.py) ------------------------------------------- */
+enum cfb_status {
+  CFB_OK = 0,
+  CFB_ERR_DIMENSION = -1,      /* DimensionError: partitioning / kernel domain */
+  CFB_ERR_CLUSTER_SIZE = -2,   /* InvalidClusterSize: N not a power of two in [1,16] */
+  CFB_ERR_SHAPE = -3,          /* ShapeMismatch */
+  CFB_ERR_SMEM = -4,           /* SmemOverflow: schedule needs more than 227 KB per CTA */
+  CFB_ERR_CUDA = -5,           /* SimulationError: CUDA launch/runtime failure */
+  CFB_ERR_ARGUMENT = -6        /* ValueError: null pointer / bad enum */
+};
+
+enum cfb_dtype { CFB_F16 = 2, CFB_F32 = 4 }; /* value = storage bytes (dims.dtype_bytes) */
+
+/* cfb_mha_args.flags */
+enum cfb_flags {
+  CFB_APPEND = 1 << 0,       /* new token's K/V join rank N-1's segment (append_new_token) */
+  CFB_WRITE_KV = 1 << 1,     /* also store the new K/V rows into the cache at position S+b */
+  CFB_ROPE = 1 << 2,         /* rotate q and k_new (rotate-half convention) at position S+b */
+  CFB_NORM = 1 << 3,         /* x = f16(rmsnorm(resid) * norm_w) instead of reading x */
+  CFB_RESID = 1 << 4,        /* out = resid + sum_heads(...) (residual add in the epilogue) */
+  CFB_STATS_MERGED = 1 << 5  /* stats_mode="merged": one SOFTMAX_MERGE pair reduce */
+};
+
+/* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
+enum cfb_stage {
+  CFB_STAGE_QKV_GATHER = 0,
+  CFB_STAGE_STATS_MAX = 1,
+  CFB_STAGE_STATS_SUM = 2,
+  CFB_STAGE_STATS_MERGE = 3,
+  CFB_STAGE_ATTN_OUT = 4,
+  CFB_STAGE_Q_PROJ_GATHER = 5,
+  CFB_STAGE_LATENT_GATHER = 6,
+  CFB_STAGE_ABSORBED_Q_GATHER = 7,
+  CFB_STAGE_DOWN_PROJ = 8,
+  CFB_STAGE_SCORE_REDUCE = 9,
+  CFB_STAGE_OUT_PROJ_REDUCE = 10,
+  CFB_STAGE_COUNT = 11
+};
+
+/*
+ * split_token fused attention module: one thread-block cluster of N CTAs
+ * per head (grid = N x n_heads).  Layouts (T = fp16 or fp32 per dtype):
+ *   x        [B][D]                      T     (unless CFB_NORM)
+ *   resid    [B][D]                      fp32  (CFB_NORM / CFB_RESID)
+ *   norm_w   [D]                         T
+ *   w_qkv    [n_heads][N][3*Hp/N][D]     T     rank r's rows: q,k,v head-dim slices
+ *   w_out    [n_heads][D][Hp]            T     (W_out[head])^T, rank r owns rows r*D/N..
+ *   k_cache, v_cache [n_heads][cache_cap][Hp] T
+ *   rope_cs  [cache_cap][Hp/2][2]        fp32  (cos, sin)
+ *   out      [B][D]                      fp32  sum over heads in head order (+resid)
+ *   out_partial [n_heads][B][D]          fp32  workspace
+ *   tickets  [cfb_mha_ticket_count()]    u32   workspace, zero before first use
+ *   stats    [n_heads][2][B]             fp32  (score_max, score_sum) of rank 0
+ * D must be a multiple of 8*N/(gcd) (16-byte rows); Hp (head_pad) a power of
+ * two >= 8 holding head_dim logical dims (rest zero-padded by the caller).
+ */
+typedef struct cfb_mha_args {
+  int dtype;
+  int batch, hidden, n_heads, head_dim, head_pad;
+  int cluster;
+  int seq_len;          /* cached positions; ignored when step_pos != NULL */
+  int cache_cap;
+  int flags;
+  const void* x;
+  const float* resid;
+  const void* norm_w;
+  float eps;
+  const void* w_qkv;
+  const void* w_out;
+  void* k_cache;
+  void* v_cache;
+  const float* rope_cs;
+  const int* step_pos;  /* device int: S for this launch (graph-friendly) */
+  float* out;
+  float* out_partial;
+  unsigned* tickets;
+  float* stats;
+  unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
+} cfb_mha_args;
+
+int cfb_mha_decode(const cfb_mha_args* args, void* stream);
+size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
+
+/* One ClusterReduce (op 0=sum,1=max,2=softmax_merge) or ClusterGather (op 3)
+ * over N CTAs of one cluster; in/out [N][n] T.  Test kernel for the DSMEM
+ * primitives (reference KATs). */
+int cfb_cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
+                           unsigned long long* traffic, void* stream);
+
+const char* cfb_last_error(void);
+const char* cfb_version(void);
+int cfb_device_sm_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CFB_H_ */

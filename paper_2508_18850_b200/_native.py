@@ -1,0 +1,94 @@
+"""ctypes binding of ``libcfb.so`` (the C ABI declared in ``include/cfb.h``).
+
+The library is built in-tree by ``__graft_entry__.build()`` (``make`` in
+``csrc/``).  There is no fallback: if the library or a CUDA device is
+missing, every entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from .exceptions import (DimensionError, InvalidClusterSize, ShapeMismatch, SimulationError,
+                         SmemOverflow)
+
+LIB_PATH = Path(__file__).resolve().parent / "libcfb.so"
+
+CFB_F16, CFB_F32 = 2, 4
+APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED = 1, 2, 4, 8, 16, 32
+STAGE_NAMES = ("qkv_gather", "stats_max_reduce", "stats_sum_reduce", "stats_merge_reduce",
+               "attn_out_reduce", "q_proj_gather", "latent_kv_gather", "absorbed_q_gather",
+               "down_proj_reduce", "score_reduce", "out_proj_reduce")
+
+_vp = ctypes.c_void_p
+
+
+class MhaArgs(ctypes.Structure):
+    """Mirror of ``cfb_mha_args``."""
+
+    _fields_ = [
+        ("dtype", ctypes.c_int), ("batch", ctypes.c_int), ("hidden", ctypes.c_int),
+        ("n_heads", ctypes.c_int), ("head_dim", ctypes.c_int), ("head_pad", ctypes.c_int),
+        ("cluster", ctypes.c_int), ("seq_len", ctypes.c_int), ("cache_cap", ctypes.c_int),
+        ("flags", ctypes.c_int),
+        ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("eps", ctypes.c_float),
+        ("w_qkv", _vp), ("w_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
+        ("rope_cs", _vp), ("step_pos", _vp), ("out", _vp), ("out_partial", _vp),
+        ("tickets", _vp), ("stats", _vp), ("traffic", _vp),
+    ]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libcfb.so once; raise loudly when it is absent."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise SimulationError(
+                f"{LIB_PATH} not built; run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
+        L.cfb_mha_decode.argtypes = [ctypes.POINTER(MhaArgs), _vp]
+        L.cfb_mha_decode.restype = ctypes.c_int
+        L.cfb_mha_ticket_count.argtypes = [ctypes.c_int] * 4
+        L.cfb_mha_ticket_count.restype = ctypes.c_size_t
+        L.cfb_cluster_collective.argtypes = [ctypes.c_int] * 4 + [_vp, _vp, _vp, _vp]
+        L.cfb_cluster_collective.restype = ctypes.c_int
+        L.cfb_last_error.restype = ctypes.c_char_p
+        L.cfb_version.restype = ctypes.c_char_p
+        L.cfb_device_sm_count.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+_STATUS = {-1: DimensionError, -2: InvalidClusterSize, -3: ShapeMismatch, -4: SmemOverflow,
+           -5: SimulationError, -6: ValueError}
+
+
+def check(status: int) -> None:
+    """Translate a cfb_status into the reference's exception classes."""
+    if status != 0:
+        msg = lib().cfb_last_error().decode(errors="replace")
+        raise _STATUS.get(status, SimulationError)(msg)
+
+
+def ptr(t) -> int | None:
+    """Device pointer of a torch tensor (or None)."""
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def require_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        raise SimulationError("paper_2508_18850_b200 needs a CUDA (sm_100a) device; "
+                              "there is no CPU fallback")
+    return torch.device("cuda")

@@ -1,0 +1,46 @@
+// extern "C" surface of libcfb.so (declared in include/cfb.h).
+#include <cstdio>
+#include <cstring>
+
+#include "common.h"
+
+namespace cfb {
+static thread_local char g_err[1024] = "";
+
+int set_error(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+}  // namespace cfb
+
+extern "C" {
+
+int cfb_mha_decode(const cfb_mha_args* args, void* stream) {
+  return cfb::mha_decode(args, static_cast<cudaStream_t>(stream));
+}
+
+size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype) {
+  return cfb::mha_ticket_count(hidden, head_pad, cluster, dtype);
+}
+
+int cfb_cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
+                           unsigned long long* traffic, void* stream) {
+  return cfb::cluster_collective(dtype, op, cluster, n, in, out, traffic,
+                                 static_cast<cudaStream_t>(stream));
+}
+
+const char* cfb_last_error(void) { return cfb::g_err; }
+
+const char* cfb_version(void) { return "cfb 0.1.0 sm_100a"; }
+
+int cfb_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return -1;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return -1;
+  return n;
+}
+
+}  // extern "C"

@@ -1,0 +1,655 @@
+// split_token fused attention module (ClusterFusion Alg. 3) for sm_100a.
+//
+// Mirrors reference dataflows.py:235-313 (run_fused_mha_decode):
+//   one cluster of N CTAs per head (grid N x n_heads), CTA rank r:
+//   1. QKV GEMV over its head-dim slice [r*h, (r+1)*h) of q, k and v
+//      (rows stream from HBM by TMA bulk copies)            dataflows.py:256-267
+//   2. ClusterGather of the 3h-slices (DSMEM), canonical order  :268-279
+//   3. (model mode) RoPE + KV-cache append of the new token
+//   4. flash-decoding over KV segment [r*ceil(S/N), ...); the new token's
+//      K/V join rank N-1's segment only                       :283-295
+//   5. softmax-stat merge: MAX reduce, rescaled SUM reduce (or one
+//      SOFTMAX_MERGE pair reduce)                             :187-227
+//   6. rescale A by exp(m_b - m*)/l*, SUM reduce of A (DSMEM) :298-300
+//   7. O-proj over output columns [r*D/N, (r+1)*D/N)         :302-310
+//   8. cross-head sum: per-head fp32 partials, the last CTA to finish a
+//      column chunk (ticket) sums the heads in head order (+ residual).
+//      Deterministic replacement of the reference's atomic_accumulate.
+// Storage rounding follows simcore.py: every buffer store is rounded to T.
+#include <cuda_runtime.h>
+
+#include "collectives.cuh"
+#include "common.h"
+#include "stream.cuh"
+
+namespace cfb {
+
+struct MhaParams {
+  int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags;
+  float sqrt_h, eps;
+  const void* x;
+  const float* resid;
+  const void* norm_w;
+  const void* w_qkv;
+  const void* w_out;
+  void* k_cache;
+  void* v_cache;
+  const float* rope_cs;
+  const int* step_pos;
+  float* out;
+  float* out_partial;
+  unsigned* tickets;
+  float* stats;
+  unsigned long long* traffic;
+};
+
+struct MhaLayout {
+  int bars, x, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, total;
+  int seg_bytes, a_bytes, st_bytes;
+};
+
+__host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
+
+__host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int tb) {
+  MhaLayout L;
+  const int h = Hp / N;
+  int rounds = 0;
+  while ((1 << rounds) < N) ++rounds;
+  L.seg_bytes = round16(B * 3 * h * tb);
+  L.a_bytes = round16(B * Hp * tb);
+  L.st_bytes = round16(2 * B * tb);
+  int o = kRingBytes;
+  L.bars = o;       o += (2 * kNumSlots + 16) * 8;
+  L.x = o;          o += round16(B * D * tb);
+  L.gbuf = o;       o += N * L.seg_bytes;
+  L.qf = o;         o += 3 * B * Hp * 4;
+  L.ws_acc = o;     o += kNumConsumerWarps * B * Hp * 4;
+  L.ws_ml = o;      o += kNumConsumerWarps * B * 2 * 4;
+  L.loc = o;        o += round16(4 * B * 4);  // m_loc, l_loc, m_star, l_star
+  L.fw = o;         o += round16(kNumConsumerWarps * B * 4);
+  L.abuf = o;       o += L.a_bytes;
+  L.arx = o;        o += 4 * L.a_bytes;
+  L.st = o;         o += 2 * L.st_bytes;
+  L.strx = o;       o += 8 * L.st_bytes;
+  L.red = o;        o += round16(kNumConsumerWarps * B * 4);
+  L.total = o;
+  return L;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// RMSNorm of fp32 residual rows into T activations (all consumer threads).
+// x = f16((resid * (1/sqrt(mean(resid^2) + eps))) * w)
+template <typename T, int QB>
+__device__ void rmsnorm_rows(T* xs, const float* resid, const T* w, int B, int D, float eps,
+                             float* red, int tid) {
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int b = 0; b < B; ++b) {
+    float ss = 0.f;
+    for (int d = tid; d < D; d += kConsumerThreads) {
+      const float v = resid[(size_t)b * D + d];
+      ss = fmaf(v, v, ss);
+    }
+    ss = warp_sum(ss);
+    if (lane == 0) red[b * kNumConsumerWarps + warp] = ss;
+  }
+  consumer_sync();
+  for (int b = 0; b < B; ++b) {
+    float tot = 0.f;
+    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) tot += red[b * kNumConsumerWarps + w2];
+    const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
+    for (int d = tid; d < D; d += kConsumerThreads) {
+      const float v = __fmul_rn(__fmul_rn(resid[(size_t)b * D + d], inv), Elem<T>::to_f(w[d]));
+      xs[b * D + d] = Elem<T>::from_f(v);
+    }
+  }
+  consumer_sync();
+}
+
+template <typename T, int EPL, int QB>
+__global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaParams p) {
+  extern __shared__ __align__(128) char smem[];
+  constexpr int tb = sizeof(T);
+  const int B = p.B, D = p.D, Hp = p.Hp;
+  const uint32_t N = p.N;
+  const int h = Hp / N;
+  const MhaLayout L = mha_layout(B, D, Hp, N, tb);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
+  const Ring ring{smem, bars, bars + kNumSlots};
+  uint64_t* cbar = bars + 2 * kNumSlots;  // [0,4) gather, [4,8) max/merge, [8,12) sum, [12,16) attn
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int head = blockIdx.y;
+  int rounds = 0;
+  while ((1u << rounds) < N) ++rounds;
+  const int S = p.step_pos ? *p.step_pos : p.S_static;
+  const int seg = S == 0 ? 0 : (S + (int)N - 1) / (int)N;
+  const int lo = min((int)rank * seg, S), hi = min(lo + seg, S);
+  const bool merged = p.flags & 32;
+
+  if (tid == 0) {
+    ring_init(ring);
+    for (int r = 0; r < rounds; ++r) {
+      mbar_init(&cbar[r], 1);
+      mbar_arrive_expect_tx(&cbar[r], (1u << r) * L.seg_bytes);
+      mbar_init(&cbar[4 + r], 1);
+      mbar_arrive_expect_tx(&cbar[4 + r], L.st_bytes);
+      mbar_init(&cbar[8 + r], 1);
+      mbar_arrive_expect_tx(&cbar[8 + r], L.st_bytes);
+      mbar_init(&cbar[12 + r], 1);
+      mbar_arrive_expect_tx(&cbar[12 + r], L.a_bytes);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  cluster_arrive();
+
+  const size_t cache_head = (size_t)head * p.cache_cap * Hp;
+  const Phase P0 = make_phase(static_cast<const T*>(p.w_qkv) + ((size_t)head * N + rank) * 3 * h * D,
+                              nullptr, 3 * h, D * tb);
+  const Phase P1 = make_phase(static_cast<const T*>(p.k_cache) + cache_head + (size_t)lo * Hp,
+                              static_cast<const T*>(p.v_cache) + cache_head + (size_t)lo * Hp,
+                              hi - lo, Hp * tb);
+  const int cols = D / (int)N;
+  const Phase P2 = make_phase(static_cast<const T*>(p.w_out) + (size_t)head * D * Hp +
+                                  (size_t)rank * cols * Hp,
+                              nullptr, cols, Hp * tb);
+
+  if (warp == kNumConsumerWarps) {  // ------------------------------ producer
+    if (lane == 0) {
+      int cnt[kNumConsumerWarps] = {};
+      const uint64_t pol = policy_evict_first();
+      produce_phase(P0, ring, cnt, pol);
+      produce_phase(P1, ring, cnt, pol);
+      produce_phase(P2, ring, cnt, pol);
+    }
+    __syncwarp();
+    cluster_wait();
+    cluster_arrive();
+    cluster_wait();
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumers
+  T* xs = reinterpret_cast<T*>(smem + L.x);
+  T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
+  float* qf = reinterpret_cast<float*>(smem + L.qf);
+  float* kf = qf + B * Hp;
+  float* vf = kf + B * Hp;
+  float* ws_acc = reinterpret_cast<float*>(smem + L.ws_acc);
+  float* ws_m = reinterpret_cast<float*>(smem + L.ws_ml);
+  float* ws_l = ws_m + kNumConsumerWarps * B;
+  float* m_loc = reinterpret_cast<float*>(smem + L.loc);
+  float* l_loc = m_loc + B;
+  float* m_st = l_loc + B;
+  float* l_st = m_st + B;
+  float* fw = reinterpret_cast<float*>(smem + L.fw);
+  T* abuf = reinterpret_cast<T*>(smem + L.abuf);
+  float* red = reinterpret_cast<float*>(smem + L.red);
+  unsigned long long sent[5] = {0, 0, 0, 0, 0};  // gather, max, sum, merge, attn
+
+  // 1. activations
+  if (p.flags & 8) {
+    rmsnorm_rows<T, QB>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  } else {
+    const char* src = static_cast<const char*>(p.x);
+    for (int v = tid; v < B * D * tb / 16; v += kConsumerThreads)
+      reinterpret_cast<uint4*>(xs)[v] = reinterpret_cast<const uint4*>(src)[v];
+    consumer_sync();
+  }
+
+  // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
+  int cnt = 0;
+  {
+    float acc[QB];
+    constexpr int epv = Elem<T>::kPerVec;
+    consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+      const int row_b = (P0.pieces == 1) ? P0.row_bytes : it.bytes;
+      const int col0 = it.byte0 / tb;
+      for (int rr = 0; rr < it.nrows; ++rr) {
+        const char* row = slot + rr * row_b;
+        if (it.piece == 0) {
+#pragma unroll
+          for (int b = 0; b < QB; ++b) acc[b] = 0.f;
+        }
+        for (int v = lane; v < row_b / 16; v += 32) {
+          float w[epv];
+          Elem<T>::unpack(lds128(row + 16 * v), w);
+#pragma unroll
+          for (int b = 0; b < QB; ++b) {
+            if (b < B) {
+              float xv[epv];
+              Elem<T>::unpack(lds128(xs + (size_t)b * D + col0 + v * epv), xv);
+#pragma unroll
+              for (int e = 0; e < epv; ++e) acc[b] = fmaf(w[e], xv[e], acc[b]);
+            }
+          }
+        }
+        if (it.piece == P0.pieces - 1) {
+#pragma unroll
+          for (int b = 0; b < QB; ++b) {
+            if (b < B) {
+              const float s = warp_sum(acc[b]);
+              if (lane == 0) gseg[b * 3 * h + it.row0 + rr] = Elem<T>::from_f(s);
+            }
+          }
+        }
+      }
+    });
+  }
+  consumer_sync();
+  cluster_wait();  // peers' mbarriers are initialised from here on
+
+  // 3. ClusterGather of the qkv slices
+  const int seg_elems = L.seg_bytes / tb;
+  if (warp == 0 && N > 1) {
+    uint64_t* gb[4] = {&cbar[0], &cbar[1], &cbar[2], &cbar[3]};
+    warp_cluster_gather(reinterpret_cast<char*>(gseg), L.seg_bytes, gb, rank, N, lane);
+    for (uint32_t s = 1; s < N; s <<= 1) sent[0] += (unsigned long long)s * B * 3 * (p.H / N) * tb;
+  }
+  consumer_sync();
+  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+    const int b = idx / Hp, d = idx % Hp;
+    const int r = d / h, i = d % h;
+    const T* sg = gseg + ((rank - r + N) % N) * seg_elems + b * 3 * h;
+    qf[idx] = Elem<T>::to_f(sg[i]);
+    kf[idx] = Elem<T>::to_f(sg[h + i]);
+    vf[idx] = Elem<T>::to_f(sg[2 * h + i]);
+  }
+  consumer_sync();
+  if (p.flags & 4) {  // RoPE (rotate-half) at position S + b
+    const int half = Hp / 2;
+    for (int idx = tid; idx < B * half; idx += kConsumerThreads) {
+      const int b = idx / half, i = idx % half;
+      const float c = p.rope_cs[((size_t)(S + b) * half + i) * 2];
+      const float sn = p.rope_cs[((size_t)(S + b) * half + i) * 2 + 1];
+      float* qb = qf + b * Hp;
+      float* kb = kf + b * Hp;
+      const float q1 = qb[i], q2 = qb[i + half], k1 = kb[i], k2 = kb[i + half];
+      qb[i] = round_to<T>(__fsub_rn(__fmul_rn(q1, c), __fmul_rn(q2, sn)));
+      qb[i + half] = round_to<T>(__fadd_rn(__fmul_rn(q2, c), __fmul_rn(q1, sn)));
+      kb[i] = round_to<T>(__fsub_rn(__fmul_rn(k1, c), __fmul_rn(k2, sn)));
+      kb[i + half] = round_to<T>(__fadd_rn(__fmul_rn(k2, c), __fmul_rn(k1, sn)));
+    }
+    consumer_sync();
+  }
+  if ((p.flags & 2) && rank == N - 1) {  // KV-cache append at rows S..S+B-1
+    T* kc = static_cast<T*>(p.k_cache) + cache_head;
+    T* vc = static_cast<T*>(p.v_cache) + cache_head;
+    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+      kc[(size_t)S * Hp + idx] = Elem<T>::from_f(kf[idx]);
+      vc[(size_t)S * Hp + idx] = Elem<T>::from_f(vf[idx]);
+    }
+  }
+
+  // 4. split-KV flash decoding over this rank's segment (online softmax per warp)
+  const int LPK = Hp / EPL, KPP = 32 / LPK, g = lane / LPK, li = lane % LPK;
+  float q[QB][EPL], acc[QB][EPL], m[QB], l[QB];
+#pragma unroll
+  for (int b = 0; b < QB; ++b) {
+    m[b] = -INFINITY;
+    l[b] = 0.f;
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) {
+      q[b][e] = (b < B) ? qf[b * Hp + li * EPL + e] : 0.f;
+      acc[b][e] = 0.f;
+    }
+  }
+  const float sqrt_h = p.sqrt_h;
+  auto attend = [&](auto&& load_k, auto&& load_v, int nkeys) {
+    for (int k0 = 0; k0 < nkeys; k0 += KPP) {
+      const int key = k0 + g;
+      const bool valid = key < nkeys;
+      const int kk = valid ? key : 0;
+      float kv[EPL], vv[EPL], s[QB];
+      load_k(kk, kv);
+#pragma unroll
+      for (int b = 0; b < QB; ++b) {
+        float t = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) t = fmaf(q[b][e], kv[e], t);
+        s[b] = t;
+      }
+      for (int o = 1; o < LPK; o <<= 1) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
+      }
+      load_v(kk, vv);
+#pragma unroll
+      for (int b = 0; b < QB; ++b) {
+        if (b >= B) continue;
+        const float sb = valid ? __fdiv_rn(s[b], sqrt_h) : -INFINITY;
+        float mx = sb;
+        for (int o = LPK; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float mn = fmaxf(m[b], mx);
+        if (mn == -INFINITY) continue;
+        const float alpha = (m[b] == -INFINITY) ? 0.f : expf(m[b] - mn);
+        const float pr = valid ? expf(sb - mn) : 0.f;
+        l[b] = fmaf(l[b], alpha, pr);
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[b][e] = fmaf(pr, vv[e], acc[b][e] * alpha);
+        m[b] = mn;
+      }
+    }
+  };
+  consume_phase(P1, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+    const T* K = reinterpret_cast<const T*>(slot);
+    const T* V = reinterpret_cast<const T*>(slot + kSlotBytes / 2);
+    attend([&](int k, float* o) { load_elems<T, EPL>(K + k * Hp + li * EPL, o); },
+           [&](int k, float* o) { load_elems<T, EPL>(V + k * Hp + li * EPL, o); }, it.nrows);
+  });
+  if ((p.flags & 1) && rank == N - 1 && warp == 0) {  // new token(s): counted exactly once
+    attend([&](int k, float* o) {
+             for (int e = 0; e < EPL; ++e) o[e] = kf[k * Hp + li * EPL + e];
+           },
+           [&](int k, float* o) {
+             for (int e = 0; e < EPL; ++e) o[e] = vf[k * Hp + li * EPL + e];
+           },
+           B);
+  }
+  // fold the KPP key groups of the warp (same lane-in-group = same dims)
+#pragma unroll
+  for (int b = 0; b < QB; ++b) {
+    for (int o = LPK; o < 32; o <<= 1) {
+      l[b] += __shfl_xor_sync(0xffffffffu, l[b], o);
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[b][e] += __shfl_xor_sync(0xffffffffu, acc[b][e], o);
+    }
+    if (b < B) {
+      if (g == 0) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ws_acc[(warp * B + b) * Hp + li * EPL + e] = acc[b][e];
+      }
+      if (lane == 0) {
+        ws_m[warp * B + b] = m[b];
+        ws_l[warp * B + b] = l[b];
+      }
+    }
+  }
+  consumer_sync();
+  // merge the 8 warp states in warp order -> (A_loc, m_loc, l_loc)
+  if (tid < B) {
+    const int b = tid;
+    float mm = -INFINITY;
+    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) mm = fmaxf(mm, ws_m[w2 * B + b]);
+    float ll = 0.f;
+    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) {
+      const float mw = ws_m[w2 * B + b];
+      const float f = (mw == -INFINITY) ? 0.f : expf(mw - mm);
+      fw[w2 * B + b] = f;
+      ll = fmaf(ws_l[w2 * B + b], f, ll);
+    }
+    m_loc[b] = mm;
+    l_loc[b] = ll;
+  }
+  consumer_sync();
+  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+    const int b = idx / Hp;
+    float a = 0.f;
+    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
+      a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
+    abuf[idx] = Elem<T>::from_f(a);  // block.store("attn_out", a_part)
+  }
+  for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
+    abuf[idx] = Elem<T>::from_f(0.f);
+
+  // 5. softmax statistics
+  T* st0 = reinterpret_cast<T*>(smem + L.st);
+  T* st1 = reinterpret_cast<T*>(smem + L.st + L.st_bytes);
+  if (warp == 0) {
+    T* rx[4];
+    uint64_t* rb[4];
+    for (int i = 0; i < L.st_bytes / tb; i += 1)
+      if (i % 32 == lane) {
+        st0[i] = Elem<T>::from_f(0.f);
+        st1[i] = Elem<T>::from_f(0.f);
+      }
+    __syncwarp();
+    if (merged) {
+      for (int b = lane; b < B; b += 32) {
+        st0[b] = Elem<T>::from_f(m_loc[b]);
+        st0[B + b] = Elem<T>::from_f(l_loc[b]);
+      }
+      __syncwarp();
+      for (int r = 0; r < 4; ++r) {
+        rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
+        rb[r] = &cbar[4 + r];
+      }
+      warp_cluster_reduce<T>(st0, 2 * B, L.st_bytes, rx, rb, kSoftmaxMerge, rank, N, lane);
+      for (int r = 0; r < rounds; ++r) sent[3] += 2ull * B * tb;
+      for (int b = lane; b < B; b += 32) {
+        m_st[b] = Elem<T>::to_f(st0[b]);
+        l_st[b] = Elem<T>::to_f(st0[B + b]);
+      }
+    } else {
+      for (int b = lane; b < B; b += 32) st0[b] = Elem<T>::from_f(m_loc[b]);
+      __syncwarp();
+      for (int r = 0; r < 4; ++r) {
+        rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
+        rb[r] = &cbar[4 + r];
+      }
+      warp_cluster_reduce<T>(st0, B, L.st_bytes, rx, rb, kMax, rank, N, lane);
+      for (int b = lane; b < B; b += 32) {
+        const float ms = Elem<T>::to_f(st0[b]);
+        m_st[b] = ms;
+        const float f = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - ms);
+        st1[b] = Elem<T>::from_f(__fmul_rn(l_loc[b], f));
+      }
+      __syncwarp();
+      for (int r = 0; r < 4; ++r) {
+        rx[r] = reinterpret_cast<T*>(smem + L.strx + (4 + r) * L.st_bytes);
+        rb[r] = &cbar[8 + r];
+      }
+      warp_cluster_reduce<T>(st1, B, L.st_bytes, rx, rb, kSum, rank, N, lane);
+      for (int b = lane; b < B; b += 32) l_st[b] = Elem<T>::to_f(st1[b]);
+      for (int r = 0; r < rounds; ++r) {
+        sent[1] += (unsigned long long)B * tb;
+        sent[2] += (unsigned long long)B * tb;
+      }
+    }
+  }
+  consumer_sync();
+  // 6. rescale and reduce the attention output
+  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+    const int b = idx / Hp;
+    const float e = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - m_st[b]);
+    const float f = __fdiv_rn(e, l_st[b]);
+    abuf[idx] = Elem<T>::from_f(__fmul_rn(Elem<T>::to_f(abuf[idx]), f));
+  }
+  consumer_sync();
+  if (warp == 0) {
+    T* rx[4];
+    uint64_t* rb[4];
+    for (int r = 0; r < 4; ++r) {
+      rx[r] = reinterpret_cast<T*>(smem + L.arx + r * L.a_bytes);
+      rb[r] = &cbar[12 + r];
+    }
+    warp_cluster_reduce<T>(abuf, B * Hp, L.a_bytes, rx, rb, kSum, rank, N, lane);
+    for (int r = 0; r < rounds; ++r) sent[4] += (unsigned long long)B * p.H * tb;
+    if (rank == 0 && p.stats)
+      for (int b = lane; b < B; b += 32) {
+        p.stats[((size_t)head * 2) * B + b] = m_st[b];
+        p.stats[((size_t)head * 2 + 1) * B + b] = l_st[b];
+      }
+    if (lane == 0 && p.traffic) {
+      atomicAdd(&p.traffic[0], sent[0]);
+      if (merged) {
+        atomicAdd(&p.traffic[3], sent[3]);
+      } else {
+        atomicAdd(&p.traffic[1], sent[1]);
+        atomicAdd(&p.traffic[2], sent[2]);
+      }
+      atomicAdd(&p.traffic[4], sent[4]);
+    }
+  }
+  consumer_sync();
+
+  // 7. O-projection over this rank's output columns + 8. cross-head sum
+  float a[QB][EPL];
+#pragma unroll
+  for (int b = 0; b < QB; ++b)
+#pragma unroll
+    for (int e = 0; e < EPL; ++e) a[b][e] = (b < B) ? Elem<T>::to_f(abuf[b * Hp + li * EPL + e]) : 0.f;
+  const int c_base = (int)rank * cols;
+  const int items_per_rank = (cols + P2.rows_per_item - 1) / P2.rows_per_item;
+  consume_phase(P2, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+    const T* W = reinterpret_cast<const T*>(slot);
+    for (int k0 = 0; k0 < it.nrows; k0 += KPP) {
+      const int row = k0 + g;
+      const bool valid = row < it.nrows;
+      float w[EPL], s[QB];
+      load_elems<T, EPL>(W + (valid ? row : 0) * Hp + li * EPL, w);
+#pragma unroll
+      for (int b = 0; b < QB; ++b) {
+        float t = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) t = fmaf(a[b][e], w[e], t);
+        s[b] = t;
+      }
+      for (int o = 1; o < LPK; o <<= 1) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
+      }
+      if (valid && li == 0) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b)
+          if (b < B) p.out_partial[((size_t)head * B + b) * D + c_base + it.row0 + row] = s[b];
+      }
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned old = 0;
+    const int chunk = (int)rank * items_per_rank + it.row0 / P2.rows_per_item;
+    if (lane == 0) old = atomicAdd(&p.tickets[chunk], 1u);
+    old = __shfl_sync(0xffffffffu, old, 0);
+    if (old == (unsigned)p.n_heads - 1) {  // last head for this chunk: sum heads in order
+      __threadfence();
+      for (int idx = lane; idx < B * it.nrows; idx += 32) {
+        const int b = idx / it.nrows;
+        const int c = c_base + it.row0 + idx % it.nrows;
+        float s = 0.f;
+        for (int hh = 0; hh < p.n_heads; ++hh) s += __ldcg(&p.out_partial[((size_t)hh * B + b) * D + c]);
+        if (p.flags & 16) s = p.resid[(size_t)b * D + c] + s;
+        p.out[(size_t)b * D + c] = s;
+      }
+      if (lane == 0) p.tickets[chunk] = 0;  // re-arm for the next launch
+    }
+  });
+  cluster_arrive();
+  cluster_wait();
+}
+
+// ---------------------------------------------------------------- host side
+
+template <typename T, int EPL, int QB>
+static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st) {
+  auto kern = mha_split_token_kernel<T, EPL, QB>;
+  static bool configured = false;
+  if (!configured) {
+    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.N, p.n_heads, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.N;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+  return CFB_OK;
+}
+
+template <typename T>
+static int launch_mha_t(const MhaParams& p, size_t smem, cudaStream_t st) {
+  if (p.B > 4) return launch_mha_inst<T, 4, 16>(p, smem, st);
+  if (p.Hp == 8) {
+    if (p.B == 1) return launch_mha_inst<T, 8, 1>(p, smem, st);
+    if (p.B == 2) return launch_mha_inst<T, 8, 2>(p, smem, st);
+    return launch_mha_inst<T, 8, 4>(p, smem, st);
+  }
+  if (p.B == 1) return launch_mha_inst<T, 16, 1>(p, smem, st);
+  if (p.B == 2) return launch_mha_inst<T, 16, 2>(p, smem, st);
+  return launch_mha_inst<T, 16, 4>(p, smem, st);
+}
+
+int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
+  if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
+  if (a->dtype != CFB_F16 && a->dtype != CFB_F32)
+    return set_error(CFB_ERR_ARGUMENT, "dtype must be CFB_F16 (2) or CFB_F32 (4)");
+  const int N = a->cluster, tb = a->dtype;
+  if (N < 1 || N > 16 || (N & (N - 1)))
+    return set_error(CFB_ERR_CLUSTER_SIZE, "cluster size must be a power of two in [1, 16], got %d", N);
+  if (a->batch < 1 || a->batch > 16) return set_error(CFB_ERR_DIMENSION, "batch must be in [1, 16]");
+  const int Hp = a->head_pad;
+  if (Hp < 8 || (Hp & (Hp - 1)) || Hp < a->head_dim || Hp > 512)
+    return set_error(CFB_ERR_DIMENSION, "head_pad must be a power of two in [8, 512] >= head_dim");
+  if (a->batch > 4 && Hp > 128)
+    return set_error(CFB_ERR_DIMENSION, "batch > 4 requires head_pad <= 128");
+  if (Hp % N || a->head_dim % N)
+    return set_error(CFB_ERR_DIMENSION, "head_dim %d not divisible by cluster size %d", a->head_dim, N);
+  if (a->hidden % N || (a->hidden * tb) % 16 || ((a->hidden / N) < 1))
+    return set_error(CFB_ERR_DIMENSION, "hidden %d must be divisible by cluster size and 16-byte rows",
+                     a->hidden);
+  if (!a->step_pos && a->seq_len < 0) return set_error(CFB_ERR_DIMENSION, "seq_len must be >= 0");
+  if (!a->step_pos && a->seq_len == 0 && !(a->flags & CFB_APPEND))
+    return set_error(CFB_ERR_DIMENSION, "no attended positions: empty cache and no appended token");
+  if ((a->flags & CFB_ROPE) && (!a->rope_cs || Hp != a->head_dim))
+    return set_error(CFB_ERR_ARGUMENT, "CFB_ROPE needs rope_cs and head_pad == head_dim");
+  if ((a->flags & (CFB_NORM | CFB_RESID)) && !a->resid)
+    return set_error(CFB_ERR_ARGUMENT, "CFB_NORM/CFB_RESID need resid");
+  if ((a->flags & CFB_NORM) && !a->norm_w) return set_error(CFB_ERR_ARGUMENT, "CFB_NORM needs norm_w");
+  if (!(a->flags & CFB_NORM) && !a->x) return set_error(CFB_ERR_ARGUMENT, "x is null");
+  if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->out || !a->out_partial ||
+      !a->tickets)
+    return set_error(CFB_ERR_ARGUMENT, "null weight / cache / workspace pointer");
+  const MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb);
+  if (L.total > kMaxSmem)
+    return set_error(CFB_ERR_SMEM, "split_token schedule needs %d B of shared memory per CTA (max %d)",
+                     L.total, kMaxSmem);
+  MhaParams p;
+  p.B = a->batch;
+  p.D = a->hidden;
+  p.H = a->head_dim;
+  p.Hp = Hp;
+  p.N = N;
+  p.n_heads = a->n_heads;
+  p.S_static = a->seq_len;
+  p.cache_cap = a->cache_cap;
+  p.flags = a->flags;
+  p.sqrt_h = (float)std::sqrt((double)a->head_dim);
+  p.eps = a->eps;
+  p.x = a->x;
+  p.resid = a->resid;
+  p.norm_w = a->norm_w;
+  p.w_qkv = a->w_qkv;
+  p.w_out = a->w_out;
+  p.k_cache = a->k_cache;
+  p.v_cache = a->v_cache;
+  p.rope_cs = a->rope_cs;
+  p.step_pos = a->step_pos;
+  p.out = a->out;
+  p.out_partial = a->out_partial;
+  p.tickets = a->tickets;
+  p.stats = a->stats;
+  p.traffic = a->traffic;
+  return tb == 2 ? launch_mha_t<__half>(p, L.total, st) : launch_mha_t<float>(p, L.total, st);
+}
+
+size_t mha_ticket_count(int hidden, int head_pad, int cluster, int dtype) {
+  const int cols = hidden / cluster;
+  const int rpi = kSlotBytes / (head_pad * dtype);
+  return (size_t)cluster * ((cols + rpi - 1) / rpi);
+}
+
+}  // namespace cfb

@@ -1,0 +1,31 @@
+// Host-side helpers shared by the cfb translation units: error state and
+// status codes of the C ABI (include/cfb.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstddef>
+
+#include "../../include/cfb.h"
+
+namespace cfb {
+
+constexpr int kMaxSmem = 227 * 1024;
+
+int set_error(int code, const char* fmt, ...);
+
+#define CFB_CUDA(expr)                                                              \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return ::cfb::set_error(CFB_ERR_CUDA, "%s failed: %s (%s:%d)", #expr,         \
+                              cudaGetErrorString(e_), __FILE__, __LINE__);          \
+  } while (0)
+
+int mha_decode(const cfb_mha_args* a, cudaStream_t st);
+size_t mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
+int cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
+                       unsigned long long* traffic, cudaStream_t st);
+
+}  // namespace cfb

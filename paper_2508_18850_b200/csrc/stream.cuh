@@ -1,0 +1,167 @@
+// Weight/KV streaming engine shared by every cfb kernel.
+//
+// One producer warp (warp kNumConsumerWarps) streams a CTA's whole schedule of
+// contiguous global rows into a ring of shared-memory slots with
+// cp.async.bulk (TMA bulk copies) completing on per-slot mbarriers.  Each
+// consumer warp owns kSlotsPerWarp private slots, so a slot is consumed by
+// exactly one warp and no CTA-wide barrier is needed to recycle it.
+//
+// A schedule is a list of Phases.  Weights and the KV cache never depend on
+// the activations, so the producer runs ahead across phase boundaries (and
+// across the DSMEM collectives the consumers wait on in between): the next
+// phase's bytes are already in flight while the cluster exchanges partials.
+#pragma once
+#include "ptx.cuh"
+
+namespace cfb {
+
+constexpr int kNumConsumerWarps = 8;
+constexpr int kThreads = (kNumConsumerWarps + 1) * 32;
+constexpr int kConsumerThreads = kNumConsumerWarps * 32;
+constexpr int kSlotsPerWarp = 2;
+constexpr int kNumSlots = kNumConsumerWarps * kSlotsPerWarp;
+constexpr int kSlotBytes = 8192;
+constexpr int kRingBytes = kNumSlots * kSlotBytes;
+constexpr uint32_t kConsumerBar = 1;  // named barrier id for consumer-only sync
+
+__device__ __forceinline__ void consumer_sync() { named_bar_sync(kConsumerBar, kConsumerThreads); }
+
+// `n_rows` rows of `row_bytes` each, contiguous from src0.  When src1 is set
+// ("paired"), item k carries the same rows of src0 and src1 in the two halves
+// of a slot (K and V cache rows).  Rows that do not fit a slot are split into
+// pieces that all go to the same consumer warp, in order.
+struct Phase {
+  const char* src0;
+  const char* src1;
+  int n_rows;
+  int row_bytes;
+  int rows_per_item;
+  int pieces;
+  int piece_bytes;
+};
+
+__device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, int n_rows,
+                                            int row_bytes) {
+  Phase p;
+  p.src0 = static_cast<const char*>(src0);
+  p.src1 = static_cast<const char*>(src1);
+  p.n_rows = n_rows < 0 ? 0 : n_rows;
+  p.row_bytes = row_bytes;
+  const int cap = src1 ? kSlotBytes / 2 : kSlotBytes;
+  if (row_bytes <= cap) {
+    p.rows_per_item = cap / row_bytes;
+    p.pieces = 1;
+    p.piece_bytes = row_bytes;
+  } else {  // paired phases never need pieces (row <= 4 KB checked on host)
+    p.rows_per_item = 1;
+    p.pieces = (row_bytes + cap - 1) / cap;
+    p.piece_bytes = cap;
+  }
+  return p;
+}
+
+struct Item {
+  int row0;     // first row
+  int nrows;    // rows in this item (1 for pieces)
+  int piece;    // piece index within the row
+  int byte0;    // byte offset of the piece within its row
+  int bytes;    // bytes per source
+};
+
+__device__ __forceinline__ int items_for_warp(const Phase& p, int w) {
+  if (p.pieces == 1) {
+    const int n_items = (p.n_rows + p.rows_per_item - 1) / p.rows_per_item;
+    return n_items > w ? (n_items - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
+  }
+  const int rows_w = p.n_rows > w ? (p.n_rows - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
+  return rows_w * p.pieces;
+}
+
+__device__ __forceinline__ Item item_of(const Phase& p, int w, int j) {
+  Item it;
+  if (p.pieces == 1) {
+    const int i = j * kNumConsumerWarps + w;
+    it.row0 = i * p.rows_per_item;
+    it.nrows = min(p.rows_per_item, p.n_rows - it.row0);
+    it.piece = 0;
+    it.byte0 = 0;
+    it.bytes = it.nrows * p.row_bytes;
+  } else {
+    it.row0 = (j / p.pieces) * kNumConsumerWarps + w;
+    it.nrows = 1;
+    it.piece = j % p.pieces;
+    it.byte0 = it.piece * p.piece_bytes;
+    it.bytes = min(p.piece_bytes, p.row_bytes - it.byte0);
+  }
+  return it;
+}
+
+struct Ring {
+  char* slots;
+  uint64_t* full;
+  uint64_t* empty;
+  __device__ __forceinline__ char* slot(int s) const { return slots + s * kSlotBytes; }
+};
+
+__device__ __forceinline__ void ring_init(const Ring& r) {
+  for (int s = 0; s < kNumSlots; ++s) {
+    mbar_init(&r.full[s], 1);
+    mbar_init(&r.empty[s], 1);
+  }
+}
+
+// Producer side: called by one elected thread; `cnt` = per-warp item counters.
+__device__ __forceinline__ void produce_phase(const Phase& p, const Ring& r,
+                                              int (&cnt)[kNumConsumerWarps], uint64_t policy) {
+  const int jmax = items_for_warp(p, 0);
+  for (int j = 0; j < jmax; ++j) {
+#pragma unroll
+    for (int w = 0; w < kNumConsumerWarps; ++w) {
+      if (j >= items_for_warp(p, w)) continue;
+      const Item it = item_of(p, w, j);
+      const int c = cnt[w]++;
+      const int s = w * kSlotsPerWarp + (c % kSlotsPerWarp);
+      const uint32_t par = (c / kSlotsPerWarp) & 1;
+      mbar_wait(&r.empty[s], par ^ 1);
+      const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
+      mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
+      bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
+      if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
+    }
+  }
+}
+
+// Consumer side: warp `w` walks its items; f(item, slot_ptr) runs warp-wide.
+template <class F>
+__device__ __forceinline__ void consume_phase(const Phase& p, const Ring& r, int w, int lane,
+                                              int& cnt, F&& f) {
+  const int n = items_for_warp(p, w);
+  for (int j = 0; j < n; ++j) {
+    const Item it = item_of(p, w, j);
+    const int c = cnt++;
+    const int s = w * kSlotsPerWarp + (c % kSlotsPerWarp);
+    mbar_wait(&r.full[s], (c / kSlotsPerWarp) & 1);
+    f(it, r.slot(s));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&r.empty[s]);
+  }
+}
+
+// Load `n` consecutive elements of type T starting at p (16-byte aligned
+// when n*sizeof(T) >= 16) into floats.
+template <typename T, int n>
+__device__ __forceinline__ void load_elems(const T* p, float* out) {
+  constexpr int bytes = n * static_cast<int>(sizeof(T));
+  if constexpr (bytes >= 16) {
+#pragma unroll
+    for (int i = 0; i < bytes / 16; ++i) {
+      const uint4 v = lds128(reinterpret_cast<const char*>(p) + 16 * i);
+      Elem<T>::unpack(v, out + i * Elem<T>::kPerVec);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < n; ++i) out[i] = Elem<T>::to_f(p[i]);
+  }
+}
+
+}  // namespace cfb

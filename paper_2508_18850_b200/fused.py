@@ -1,0 +1,226 @@
+"""Drop-in fused decode dataflows backed by the sm_100a kernels in libcfb.so.
+
+Same names, arguments, results and errors as the reference's
+``dataflows.py`` (``run_fused_mha_decode`` :235-313, ``run_dataflow``
+:505-514, ``DecodeResult`` :55-68).  The numerics run on the GPU: the
+scenario's arrays are packed once per call into the kernels' HBM layouts
+(fp16 when ``dtype_bytes == 2``), the kernel is launched through the C ABI,
+and the result carries the device output plus the DSMEM ledger of the
+kernel's static collective schedule, cross-checked against the byte counters
+the kernel itself kept.
+
+Deliberate, documented deviation: heads are summed in
+fp32 in head order by a deterministic ticketed reduction instead of the
+reference's f16-rounded atomic accumulation, so ``output`` is closer to the
+dense fp32 oracle than the reference simulator's own f16 output.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError, SimulationError
+from .ledger import GLOBAL, StageTrace, TrafficLedger, emit_gather, emit_reduce
+from .scenario import MHA, MLA, validate_scenario
+
+SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD = "split_token", "fused_mla", "split_head"
+DATAFLOW_KINDS = (SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD)
+TWO_PASS, MERGED = "two_pass", "merged"
+
+
+@dataclass
+class DecodeResult:
+    output: np.ndarray
+    ledger: TrafficLedger
+    stage_traffic: dict
+    score_max: np.ndarray
+    score_sum: np.ndarray
+    collectives: list = field(default_factory=list)
+    n_clusters: int = 0
+    n_blocks: int = 1
+    device_traffic: dict = field(default_factory=dict)  # bytes the kernel counted
+
+    @property
+    def dsmem_bytes(self) -> int:
+        return self.ledger.channel_bytes("dsmem")
+
+
+def sequence_segments(seq_len: int, n_blocks: int) -> list[tuple[int, int]]:
+    """Contiguous ceil(S/N) KV segments per CTA (dataflows.py:109-114)."""
+    if seq_len == 0:
+        return [(0, 0)] * n_blocks
+    step = -(-seq_len // n_blocks)
+    return [(min(b * step, seq_len), min((b + 1) * step, seq_len)) for b in range(n_blocks)]
+
+
+def validate_partitioning(scenario, kind: str, append_new_token: bool = True) -> None:
+    """Partitioning rules and error types of dataflows.py:117-137."""
+    n = scenario.cluster.n_blocks
+    d = scenario.dims
+    if kind not in DATAFLOW_KINDS:
+        raise DimensionError(f"unknown dataflow kind {kind!r}")
+    if d.seq_len == 0 and not append_new_token:
+        raise DimensionError("no attended positions: empty cache and no appended token")
+    if d.head_dim % n:
+        raise DimensionError(f"head_dim {d.head_dim} not divisible by cluster size {n}")
+    if kind in (SPLIT_TOKEN, FUSED_MLA) and d.hidden_dim % n:
+        raise DimensionError(f"hidden_dim {d.hidden_dim} not divisible by cluster size {n}")
+    if kind == FUSED_MLA:
+        if scenario.kind != MLA:
+            raise DimensionError("fused_mla requires an mla scenario")
+        if d.kv_lora_rank is None or d.kv_lora_rank % n:
+            raise DimensionError(f"kv_lora_rank {d.kv_lora_rank} not divisible by cluster size {n}")
+    elif scenario.kind != MHA:
+        raise DimensionError(f"{kind} requires an mha scenario")
+
+
+def pow2_at_least(x: int, lo: int = 8) -> int:
+    p = lo
+    while p < x:
+        p *= 2
+    return p
+
+
+def padded_hidden(D: int, n: int, dtype_bytes: int) -> int:
+    """Smallest D' >= D with 16-byte rows and D' % n == 0 (zero padding)."""
+    q = max(n, 16 // dtype_bytes)
+    return -(-D // q) * q
+
+
+def _emit_global(ledger, n, batch, out_slice, nbytes):
+    for b in range(n):
+        for _ in range(batch):
+            ledger.record(-1, b, -1, out_slice * nbytes, GLOBAL)
+
+
+def _finish_output(out: np.ndarray) -> np.ndarray:
+    if not np.all(np.isfinite(out)):
+        raise SimulationError("decode produced a non-finite output")
+    return out
+
+
+def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
+                         append_new_token: bool = True) -> DecodeResult:
+    """split_token fused attention module on the GPU (one cluster per head)."""
+    import torch
+
+    validate_partitioning(scenario, SPLIT_TOKEN, append_new_token)
+    validate_scenario(scenario)
+    if stats_mode not in (TWO_PASS, MERGED):
+        raise ValueError(f"unknown stats_mode {stats_mode!r}")
+    dev = _native.require_cuda()
+    d = scenario.dims
+    n, nb = scenario.cluster.n_blocks, d.dtype_bytes
+    B, D, nh, H, S = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.seq_len
+    dt = torch.float16 if nb == 2 else torch.float32
+    Hp = pow2_at_least(H)
+    Dp = padded_hidden(D, n, nb)
+    hp = Hp // n
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+
+    with torch.no_grad():
+        x = torch.zeros(B, Dp, device=dev, dtype=dt)
+        x[:, :D] = up(scenario.hidden).to(dt)
+        # w_qkv (nh, D, 3H) -> rows [head][rank][q|k|v slice][D']
+        w = up(scenario.w_qkv).reshape(nh, D, 3, H).permute(0, 2, 3, 1)  # (nh, 3, H, D)
+        wp = torch.zeros(nh, 3, Hp, Dp, device=dev, dtype=dt)
+        wp[:, :, :H, :D] = w.to(dt)
+        w_qkv = wp.reshape(nh, 3, n, hp, Dp).permute(0, 2, 1, 3, 4).contiguous()
+        wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
+        wo[:, :D, :H] = up(scenario.w_out).transpose(1, 2).to(dt)
+        cap = max(S, 1)
+        kc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)
+        vc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)
+        if S:
+            kc[:, :S, :H] = up(scenario.k_cache).to(dt)
+            vc[:, :S, :H] = up(scenario.v_cache).to(dt)
+        out = torch.empty(B, Dp, device=dev, dtype=torch.float32)
+        part = torch.empty(nh, B, Dp, device=dev, dtype=torch.float32)
+        L = _native.lib()
+        tickets = torch.zeros(int(L.cfb_mha_ticket_count(Dp, Hp, n, nb)), device=dev,
+                              dtype=torch.int32)
+        stats = torch.zeros(nh, 2, B, device=dev, dtype=torch.float32)
+        traffic = torch.zeros(16, device=dev, dtype=torch.int64)
+        flags = (_native.APPEND if append_new_token else 0) | (
+            _native.STATS_MERGED if stats_mode == MERGED else 0)
+        args = _native.MhaArgs(
+            dtype=nb, batch=B, hidden=Dp, n_heads=nh, head_dim=H, head_pad=Hp, cluster=n,
+            seq_len=S, cache_cap=cap, flags=flags, x=x.data_ptr(), eps=0.0,
+            w_qkv=w_qkv.data_ptr(), w_out=wo.data_ptr(), k_cache=kc.data_ptr(),
+            v_cache=vc.data_ptr(), out=out.data_ptr(), out_partial=part.data_ptr(),
+            tickets=tickets.data_ptr(), stats=stats.data_ptr(), traffic=traffic.data_ptr())
+        _native.check(L.cfb_mha_decode(args, _native.stream_ptr()))
+        torch.cuda.synchronize()
+        out_np = out[:, :D].cpu().numpy()
+        st = stats.cpu().numpy()
+        dev_traffic = traffic.cpu().numpy()
+
+    # ledger of the static schedule, in the reference's event order
+    ledger = TrafficLedger()
+    stage_traffic: dict[str, int] = {}
+    traces = []
+    names = ["qkv_gather"] + (["stats_merge_reduce"] if stats_mode == MERGED
+                              else ["stats_max_reduce", "stats_sum_reduce"]) + ["attn_out_reduce"]
+    h = H // n
+    for head in range(nh):
+        tr = [("qkv_gather", emit_gather(ledger, n, B * 3 * h * nb))]
+        if stats_mode == MERGED:
+            tr.append(("stats_merge_reduce", emit_reduce(ledger, n, 2 * B * nb)))
+        else:
+            tr.append(("stats_max_reduce", emit_reduce(ledger, n, B * nb)))
+            tr.append(("stats_sum_reduce", emit_reduce(ledger, n, B * nb)))
+        tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * H * nb)))
+        for stage, t in tr:
+            stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
+            traces.append(StageTrace(stage, head, t))
+        _emit_global(ledger, n, B, D // n, nb)
+    device_traffic = {_native.STAGE_NAMES[i]: int(dev_traffic[i]) for i in range(5)
+                      if _native.STAGE_NAMES[i] in names}
+    if device_traffic != stage_traffic:
+        raise SimulationError(f"kernel DSMEM byte counters {device_traffic} disagree with the "
+                              f"schedule {stage_traffic}")
+    return DecodeResult(output=_finish_output(out_np), ledger=ledger, stage_traffic=stage_traffic,
+                        score_max=np.ascontiguousarray(st[:, 0, :]),
+                        score_sum=np.ascontiguousarray(st[:, 1, :]), collectives=traces,
+                        n_clusters=nh, n_blocks=n, device_traffic=device_traffic)
+
+
+def run_dataflow(kind: str, scenario, **kwargs) -> DecodeResult:
+    """Dispatch by dataflow kind (dataflows.py:505-514)."""
+    if kind == SPLIT_TOKEN:
+        return run_fused_mha_decode(scenario, **kwargs)
+    if kind == FUSED_MLA:
+        from .mla import run_fused_mla_decode
+        return run_fused_mla_decode(scenario, **kwargs)
+    if kind == SPLIT_HEAD:
+        from .mla import run_splithead_decode
+        kwargs.pop("stats_mode", None)
+        return run_splithead_decode(scenario, **kwargs)
+    raise DimensionError(f"unknown dataflow kind {kind!r}")
+
+
+def cluster_collective(payloads: np.ndarray, op: str, dtype_bytes: int = 4):
+    """Run one DSMEM ClusterReduce ("sum"/"max"/"softmax_merge") or
+    ClusterGather ("gather") on the GPU.  payloads: (N, n).  Returns
+    (per-CTA buffers, dsmem bytes counted by the kernel)."""
+    import torch
+    dev = _native.require_cuda()
+    ops = {"sum": 0, "max": 1, "softmax_merge": 2, "softmax-merge": 2, "gather": 3}
+    if op not in ops:
+        raise ValueError(f"unknown collective {op!r}")
+    p = np.ascontiguousarray(payloads, dtype=np.float32)
+    N, n = p.shape
+    dt = torch.float16 if dtype_bytes == 2 else torch.float32
+    inp = torch.from_numpy(p).to(dev).to(dt)
+    out = torch.zeros((N, N * n) if op == "gather" else (N, n), device=dev, dtype=dt)
+    traffic = torch.zeros(1, device=dev, dtype=torch.int64)
+    _native.check(_native.lib().cfb_cluster_collective(dtype_bytes, ops[op], N, n, inp.data_ptr(),
+                                                       out.data_ptr(), traffic.data_ptr(),
+                                                       _native.stream_ptr()))
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy(), int(traffic.item())
