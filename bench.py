@@ -1,0 +1,382 @@
+"""Benchmark: Llama2-7B batch-1 greedy decode TPOT on B200 (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--contexts 1024,2048,4096,8192,16384]
+
+One "step" = one decode token through the whole model (embed, 32 x
+[split_token attention module + fused SwiGLU FFN], LM head + argmax),
+replayed from a CUDA graph with weights and KV cache resident in HBM.
+`value` is the mean TPOT (µs/token) over the context sweep; the per-context
+numbers are in `sweep`.  Inputs (13.5 GB of weights) are far larger than the
+126 MB L2, so no L2 flush is needed between steps.
+
+--impl reference times the CPU oracle restatement of the reference path
+(oracle/, numpy, all host threads) on a bounded sample: one decoder block per
+context, extrapolated to 32 layers plus the LM head.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "TPOT µs/token, Llama2-7B bs1 decode 1K–16K ctx; achieved HBM GB/s vs peak"
+FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return d, "measured"
+    return dict(FALLBACK_PEAKS), "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int = 0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except (ValueError, IndexError):
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------- GPU arm
+def run_ours(args, rank, world):
+    import torch
+    import paper_2508_18850_b200 as cfb  # noqa: F401
+    from paper_2508_18850_b200 import _native
+    from paper_2508_18850_b200.llama import LLAMA2_7B, LlamaDecoder
+    import ctypes
+
+    dev = torch.device("cuda", rank % max(torch.cuda.device_count(), 1))
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = LLAMA2_7B
+    ctxs = [int(c) for c in args.contexts.split(",")]
+    cap = max(ctxs) + args.warmup + args.steps + 8
+    model = LlamaDecoder.random(cfg, cache_cap=cap, seed=1234 + rank)
+    L = _native.lib()
+    st = torch.cuda.current_stream()
+
+    # configure kernels outside capture, then capture one step
+    model.set_state(ctxs[0], 1)
+    model.step()
+    torch.cuda.synchronize()
+    model.set_state(ctxs[0], 1)
+    model.capture()
+
+    pk, pk_kind = peaks()
+    sweep = []
+    sampler = ClockSampler(dev.index or 0)
+    launches = 0
+    with sampler:
+        for ctx in ctxs:
+            model.set_state(ctx, 1)
+            for _ in range(args.warmup):
+                model.replay()
+            model.set_state(ctx, 1)
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            for _ in range(args.steps):
+                model.replay()
+            e1.record(st)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            if world > 1:
+                t = torch.tensor([ms], device=dev)
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+                ms = float(t.item())
+            launches += model.launches_per_step * args.steps
+            tpot_us = ms * 1e3 / args.steps
+            mean_ctx = ctx + (args.steps - 1) / 2
+            gbs = cfg.step_bytes(int(mean_ctx)) / (tpot_us * 1e-6) / 1e9
+            sweep.append({"ctx": ctx, "tpot_us": round(tpot_us, 2), "hbm_gbs": round(gbs, 1),
+                          "frac_of_peak": round(gbs / pk["hbm_gbs"], 4)})
+
+        # e2e: host token -> device (pinned H2D), graph, token -> host (pinned D2H), per step
+        host_in = torch.ones(1, dtype=torch.int32).pin_memory()
+        host_out = torch.zeros(1, dtype=torch.int32).pin_memory()
+        e2e = []
+        for ctx in ctxs:
+            model.set_state(ctx, 1)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                _native.check(L.cfb_llama_write_token(model._h, ctypes.c_void_p(host_in.data_ptr()),
+                                                      _native.stream_ptr()))
+                model.replay()
+                _native.check(L.cfb_llama_read(model._h, ctypes.c_void_p(host_out.data_ptr()),
+                                               None, _native.stream_ptr()))
+                st.synchronize()
+                host_in[0] = host_out[0]
+            dt = time.perf_counter() - t0
+            e2e.append(dt * 1e6 / args.steps)
+            launches += model.launches_per_step * args.steps
+    clocks = sampler.summary()
+
+    # dominant kernel (fused FFN, 64% of weight bytes): avg launch duration with
+    # CUDA events on its stream, cycling through the 32 layers' weights
+    ffn_bytes = 3 * cfg.hidden * cfg.inter * 2 + cfg.hidden * 2
+    resid = torch.randn(1, cfg.hidden, device=dev)
+    out = torch.empty(1, cfg.hidden, device=dev)
+    act = torch.empty(cfg.inter, device=dev, dtype=torch.float16)
+    bar = torch.zeros(1, device=dev, dtype=torch.int64)
+    fargs = []
+    for lyr in model.layers:
+        fargs.append(_native.FfnArgs(
+            dtype=2, batch=1, hidden=cfg.hidden, inter=cfg.inter,
+            flags=_native.NORM | _native.RESID, grid=0, eps=cfg.eps, x=None,
+            resid=resid.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
+            w_dn=lyr["w_dn"].data_ptr(), act=act.data_ptr(), out=out.data_ptr(),
+            barrier=bar.data_ptr()))
+    for a in fargs[:4]:
+        _native.check(L.cfb_ffn_decode(a, _native.stream_ptr()))
+    reps = 4 * len(fargs)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for i in range(reps):
+        _native.check(L.cfb_ffn_decode(fargs[i % len(fargs)], _native.stream_ptr()))
+    e1.record(st)
+    torch.cuda.synchronize()
+    ffn_us = e0.elapsed_time(e1) * 1e3 / reps
+    launches += reps
+    ffn_gbs = ffn_bytes / (ffn_us * 1e-6) / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "ffn_dram_bytes.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    tpot = float(np.mean([s["tpot_us"] for s in sweep]))
+    e2e_tpot = float(np.mean(e2e))
+    line = {
+        "metric": METRIC, "value": round(tpot, 2), "unit": "us/token", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tpot / 1e3, 4),
+        "higher_is_better": False, "scaling": "replicas" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f16", "data": "synthetic (random fp16 weights + KV cache, device-drawn)",
+        "config": {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
+                               + "/".join(str(c) for c in ctxs) + ", cluster size 4 (configs[1]); "
+                               "value = mean TPOT over the sweep",
+                   "model": "llama2-7b", "global_batch": world, "contexts": ctxs,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "cluster_size": cfg.cluster,
+                   "l2": "inputs larger than L2 (13.5 GB weights streamed per token), no flush"},
+        "sweep": sweep,
+        "achieved_hbm_gbs_mean": round(float(np.mean([s["hbm_gbs"] for s in sweep])), 1),
+        "e2e": {"value": round(e2e_tpot, 2), "unit": "us/token", "h2d_bytes_per_step": 4,
+                "d2h_bytes_per_step": 4,
+                "path": "cfb_llama_write_token (pinned H2D) + cfb_llama_replay + cfb_llama_read "
+                        "(pinned D2H) + stream sync, every step"},
+        "roofline": {"kernel": "ffn_swiglu_kernel (fused gate/up + SiLU*mul + down)",
+                     "bound": "hbm", "achieved": round(ffn_gbs, 1), "peak": pk["hbm_gbs"],
+                     "peak_kind": pk_kind, "unit": "GB/s", "frac": round(ffn_gbs / pk["hbm_gbs"], 4),
+                     "traffic": traffic, "bytes_per_launch": ffn_bytes,
+                     "avg_launch_us": round(ffn_us, 2)},
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+    return line
+
+
+# --------------------------------------------------------------------- CPU arm
+def _block_sample(cfg, ctx, rng):
+    """fp32 numpy weights of ONE decoder block + a ctx-long cache (oracle inputs)."""
+    from oracle import clusterdec_port as cp  # noqa: F401
+    D, F, nh, H = cfg.hidden, cfg.inter, cfg.n_heads, cfg.head_dim
+
+    def f16(shape, scale):
+        return (rng.standard_normal(shape, dtype=np.float32) * scale).astype(np.float16).astype(np.float32)
+
+    return dict(x=f16((1, D), 1.0), g1=np.ones(D, np.float32), g2=np.ones(D, np.float32),
+                w_qkv=f16((nh, D, 3 * H), D ** -0.5), w_out=f16((nh, H, D), H ** -0.5),
+                w1=f16((F, D), D ** -0.5), w2=f16((F, D), D ** -0.5), w3=f16((D, F), F ** -0.5),
+                k=f16((nh, ctx, H), 1.0), v=f16((nh, ctx, H), 1.0))
+
+
+def _block_once(cfg, s):
+    from oracle import clusterdec_port as cp
+    from oracle import llama_port as lp
+    h = lp.rmsnorm_f16(s["x"], s["g1"], cfg.eps)
+    x = s["x"] + cp.dense_mha(h, s["w_qkv"], s["w_out"], s["k"], s["v"])
+    return x + lp.ffn_block(x, s["g2"], s["w1"], s["w2"], s["w3"], cfg.eps)
+
+
+def _lm_head_once(cfg, w, x):
+    from oracle import llama_port as lp
+    return int(np.argmax(lp.rmsnorm_f16(x, np.ones(cfg.hidden, np.float32), cfg.eps) @ w.T))
+
+
+def cpu_baseline(ctxs, cfg, threads, reps=1):
+    """Oracle (numpy port of the reference path) timed on the host: one block
+    per context x 32 layers + the LM head = TPOT estimate."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:  # pragma: no cover
+        threadpool_limits = None
+    rng = np.random.default_rng(0)
+    w_lm = (rng.standard_normal((cfg.vocab, cfg.hidden), dtype=np.float32)
+            * cfg.hidden ** -0.5).astype(np.float16).astype(np.float32)
+    vals = []
+    ctx_ = contextlib_null() if threadpool_limits is None else threadpool_limits(threads)
+    with ctx_:
+        for ctx in ctxs:
+            s = _block_sample(cfg, ctx, rng)
+            _block_once(cfg, s)  # warm
+            t = []
+            for _ in range(reps):
+                t0 = time.perf_counter()
+                _block_once(cfg, s)
+                t.append(time.perf_counter() - t0)
+            t0 = time.perf_counter()
+            _lm_head_once(cfg, w_lm, s["x"])
+            lm = time.perf_counter() - t0
+            vals.append((min(t) * cfg.n_layers + lm) * 1e6)
+            del s
+    return {"value": round(float(np.mean(vals)), 1), "unit": "us/token", "cores": threads,
+            "kind": "port",
+            "sample": f"oracle numpy block (RMSNorm + dense_mha_decode + residual + RMSNorm + "
+                      f"SwiGLU ffn_reference + residual) at ctx {','.join(map(str, ctxs))}, B=1, "
+                      f"best of {reps}, x{cfg.n_layers} layers + LM head; OpenBLAS, {threads} threads"}
+
+
+class contextlib_null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
+def run_reference(args, rank, world):
+    from paper_2508_18850_b200.llama import LLAMA2_7B
+    cfg = LLAMA2_7B
+    ctxs = [int(c) for c in args.contexts.split(",")]
+    threads = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_limits
+        lim = threadpool_limits(threads)
+    except ImportError:
+        lim = contextlib_null()
+    rng = np.random.default_rng(0)
+    samples = {c: _block_sample(cfg, c, rng) for c in ctxs}
+    w_lm = (rng.standard_normal((cfg.vocab, cfg.hidden), dtype=np.float32)
+            * cfg.hidden ** -0.5).astype(np.float16).astype(np.float32)
+    with lim:
+        def one_step():
+            per = []
+            for c in ctxs:
+                t0 = time.perf_counter()
+                _block_once(cfg, samples[c])
+                blk = time.perf_counter() - t0
+                t0 = time.perf_counter()
+                _lm_head_once(cfg, w_lm, samples[c]["x"])
+                per.append((blk * cfg.n_layers + (time.perf_counter() - t0)) * 1e6)
+            return float(np.mean(per))
+        for _ in range(args.warmup):
+            one_step()
+        vals = [one_step() for _ in range(args.steps)]
+    tpot = float(np.mean(vals))
+    sample = (f"per step: one oracle decoder block (numpy port of dense_mha_decode + "
+              f"ffn_reference silu + RMSNorm/residual) at each ctx {ctxs}, x{cfg.n_layers} layers "
+              f"+ LM head, mean over contexts; {threads} threads")
+    return {"metric": METRIC, "impl": "reference", "value": round(tpot, 1), "unit": "us/token",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(tpot / 1e3, 3), "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp16-valued inputs)", "data": "synthetic",
+            "config": {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
+                                   + "/".join(map(str, ctxs)) + " (configs[1]); value = mean TPOT",
+                       "model": "llama2-7b", "global_batch": 1, "contexts": ctxs,
+                       "parallelism": "cpu"},
+            "cpu_baseline": {"value": round(tpot, 1), "unit": "us/token", "cores": threads,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(tpot, 1), "unit": "us/token", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--contexts", default="1024,2048,4096,8192,16384")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", args.gpus if args.gpus else 1))
+    if "RANK" not in os.environ:
+        world = 1
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        line = run_reference(args, rank, world)
+    else:
+        line = run_ours(args, rank, world)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

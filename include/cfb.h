@@ -110,6 +110,90 @@ typedef struct cfb_mha_args {
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);
 size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
 
+
+/*
+ * Fused SwiGLU FFN (one launch, persistent grid, one CTA per SM):
+ *   out = [resid +] (silu(h w1^T) * (h w2^T)) w3^T,  h = x or f16(rmsnorm(resid) * norm_w)
+ *   w_gu  [F][2][D]  T   row 2f = w1[f] (gate), row 2f+1 = w2[f] (up)
+ *   w_dn  [D][F]     T   = w3
+ *   act   [B][F]     T   workspace;  barrier: one u64, zero before first use
+ */
+typedef struct cfb_ffn_args {
+  int dtype, batch, hidden, inter, flags, grid; /* grid <= 0: one CTA per SM */
+  float eps;
+  const void* x;
+  const float* resid;
+  const void* norm_w;
+  const void* w_gu;
+  const void* w_dn;
+  void* act;
+  float* out;
+  unsigned long long* barrier;
+} cfb_ffn_args;
+int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
+
+/* Final RMSNorm + LM head + greedy argmax (first index of the max, numpy
+ * semantics).  w [V][D] T; logits [B][V] fp32 (nullable); cand_* [grid][B]
+ * workspace; ticket one u32 (zero); token_out [B]; step_pos (nullable) is
+ * incremented once the token is written. */
+typedef struct cfb_lm_args {
+  int dtype, batch, hidden, vocab, grid;
+  float eps;
+  const float* resid;
+  const void* norm_w;
+  const void* w;
+  float* logits;
+  float* cand_val;
+  int* cand_idx;
+  unsigned* ticket;
+  int* token_out;
+  int* step_pos;
+} cfb_lm_args;
+int cfb_lm_head_argmax(const cfb_lm_args* args, void* stream);
+
+/* out[b][:] = float(table[tokens[b]][:]) */
+int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,
+              void* stream);
+
+/*
+ * Whole-model greedy decode step (Llama2 family, batch 1):
+ *   embed -> n_layers x (split_token attention module [norm, rope, kv append,
+ *   residual] -> fused FFN [norm, residual]) -> final norm + LM head + argmax.
+ * Per-layer weight pointers are in the layouts above; rope_cs [cache_cap][H/2][2].
+ * The engine owns its small workspace; the CUDA graph of one step advances
+ * the device-side position, so replays decode consecutive tokens.
+ */
+typedef struct cfb_llama_config {
+  int dtype, n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster;
+  float eps;
+} cfb_llama_config;
+typedef struct cfb_llama_weights {
+  const void* embed;
+  const void* final_norm;
+  const void* lm_head;
+  const float* rope_cs;
+  const void* const* attn_norm;
+  const void* const* w_qkv;
+  const void* const* w_out;
+  const void* const* ffn_norm;
+  const void* const* w_gu;
+  const void* const* w_dn;
+  void* const* k_cache;
+  void* const* v_cache;
+} cfb_llama_weights;
+typedef struct cfb_llama cfb_llama;
+int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cfb_llama** out);
+int cfb_llama_destroy(cfb_llama* m);
+int cfb_llama_set_state(cfb_llama* m, int pos, int token, void* stream);
+int cfb_llama_step(cfb_llama* m, void* stream);
+int cfb_llama_capture(cfb_llama* m, void* stream);
+int cfb_llama_replay(cfb_llama* m, void* stream);
+int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, float** resid);
+int cfb_llama_launches_per_step(const cfb_llama* m);
+/* stream-ordered copies between the engine and host memory (either may be NULL) */
+int cfb_llama_read(cfb_llama* m, int* token_host, float* logits_host, void* stream);
+int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
+
 /* One ClusterReduce (op 0=sum,1=max,2=softmax_merge) or ClusterGather (op 3)
  * over N CTAs of one cluster; in/out [N][n] T.  Test kernel for the DSMEM
  * primitives (reference KATs). */

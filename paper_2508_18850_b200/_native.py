@@ -60,6 +60,7 @@ def lib() -> ctypes.CDLL:
         L.cfb_last_error.restype = ctypes.c_char_p
         L.cfb_version.restype = ctypes.c_char_p
         L.cfb_device_sm_count.restype = ctypes.c_int
+        bind_extra(L)
         _lib = L
     return _lib
 
@@ -92,3 +93,27 @@ def require_cuda():
         raise SimulationError("paper_2508_18850_b200 needs a CUDA (sm_100a) device; "
                               "there is no CPU fallback")
     return torch.device("cuda")
+
+
+class FfnArgs(ctypes.Structure):
+    """Mirror of ``cfb_ffn_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "inter", "flags", "grid")] + [
+        ("eps", ctypes.c_float), ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("w_gu", _vp),
+        ("w_dn", _vp), ("act", _vp), ("out", _vp), ("barrier", _vp)]
+
+
+class LmArgs(ctypes.Structure):
+    """Mirror of ``cfb_lm_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "vocab", "grid")] + [
+        ("eps", ctypes.c_float), ("resid", _vp), ("norm_w", _vp), ("w", _vp), ("logits", _vp),
+        ("cand_val", _vp), ("cand_idx", _vp), ("ticket", _vp), ("token_out", _vp),
+        ("step_pos", _vp)]
+
+
+def bind_extra(L) -> None:
+    L.cfb_ffn_decode.argtypes = [ctypes.POINTER(FfnArgs), _vp]
+    L.cfb_ffn_decode.restype = ctypes.c_int
+    L.cfb_lm_head_argmax.argtypes = [ctypes.POINTER(LmArgs), _vp]
+    L.cfb_lm_head_argmax.restype = ctypes.c_int

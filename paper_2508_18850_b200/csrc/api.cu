@@ -26,6 +26,19 @@ size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype) {
   return cfb::mha_ticket_count(hidden, head_pad, cluster, dtype);
 }
 
+int cfb_ffn_decode(const cfb_ffn_args* args, void* stream) {
+  return cfb::ffn_decode(args, static_cast<cudaStream_t>(stream));
+}
+
+int cfb_lm_head_argmax(const cfb_lm_args* args, void* stream) {
+  return cfb::lm_head_argmax(args, static_cast<cudaStream_t>(stream));
+}
+
+int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,
+              void* stream) {
+  return cfb::embed(dtype, table, tokens, out, batch, hidden, static_cast<cudaStream_t>(stream));
+}
+
 int cfb_cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
                            unsigned long long* traffic, void* stream) {
   return cfb::cluster_collective(dtype, op, cluster, n, in, out, traffic,

@@ -20,7 +20,7 @@
 
 #include "collectives.cuh"
 #include "common.h"
-#include "stream.cuh"
+#include "gemv.cuh"
 
 namespace cfb {
 
@@ -74,40 +74,6 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.red = o;        o += round16(kNumConsumerWarps * B * 4);
   L.total = o;
   return L;
-}
-
-__device__ __forceinline__ float warp_sum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  return v;
-}
-
-// RMSNorm of fp32 residual rows into T activations (all consumer threads).
-// x = f16((resid * (1/sqrt(mean(resid^2) + eps))) * w)
-template <typename T, int QB>
-__device__ void rmsnorm_rows(T* xs, const float* resid, const T* w, int B, int D, float eps,
-                             float* red, int tid) {
-  const int warp = tid >> 5, lane = tid & 31;
-  for (int b = 0; b < B; ++b) {
-    float ss = 0.f;
-    for (int d = tid; d < D; d += kConsumerThreads) {
-      const float v = resid[(size_t)b * D + d];
-      ss = fmaf(v, v, ss);
-    }
-    ss = warp_sum(ss);
-    if (lane == 0) red[b * kNumConsumerWarps + warp] = ss;
-  }
-  consumer_sync();
-  for (int b = 0; b < B; ++b) {
-    float tot = 0.f;
-    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) tot += red[b * kNumConsumerWarps + w2];
-    const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
-    for (int d = tid; d < D; d += kConsumerThreads) {
-      const float v = __fmul_rn(__fmul_rn(resid[(size_t)b * D + d], inv), Elem<T>::to_f(w[d]));
-      xs[b * D + d] = Elem<T>::from_f(v);
-    }
-  }
-  consumer_sync();
 }
 
 template <typename T, int EPL, int QB>
@@ -194,7 +160,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // 1. activations
   if (p.flags & 8) {
-    rmsnorm_rows<T, QB>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
     const char* src = static_cast<const char*>(p.x);
     for (int v = tid; v < B * D * tb / 16; v += kConsumerThreads)
@@ -205,40 +171,15 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
   int cnt = 0;
   {
-    float acc[QB];
-    constexpr int epv = Elem<T>::kPerVec;
+    RowDot<T, QB> rd;
     consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-      const int row_b = (P0.pieces == 1) ? P0.row_bytes : it.bytes;
-      const int col0 = it.byte0 / tb;
-      for (int rr = 0; rr < it.nrows; ++rr) {
-        const char* row = slot + rr * row_b;
-        if (it.piece == 0) {
+      rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
+        if (lane == 0) {
 #pragma unroll
-          for (int b = 0; b < QB; ++b) acc[b] = 0.f;
+          for (int b = 0; b < QB; ++b)
+            if (b < B) gseg[b * 3 * h + row] = Elem<T>::from_f(s[b]);
         }
-        for (int v = lane; v < row_b / 16; v += 32) {
-          float w[epv];
-          Elem<T>::unpack(lds128(row + 16 * v), w);
-#pragma unroll
-          for (int b = 0; b < QB; ++b) {
-            if (b < B) {
-              float xv[epv];
-              Elem<T>::unpack(lds128(xs + (size_t)b * D + col0 + v * epv), xv);
-#pragma unroll
-              for (int e = 0; e < epv; ++e) acc[b] = fmaf(w[e], xv[e], acc[b]);
-            }
-          }
-        }
-        if (it.piece == P0.pieces - 1) {
-#pragma unroll
-          for (int b = 0; b < QB; ++b) {
-            if (b < B) {
-              const float s = warp_sum(acc[b]);
-              if (lane == 0) gseg[b * 3 * h + it.row0 + rr] = Elem<T>::from_f(s);
-            }
-          }
-        }
-      }
+      });
     });
   }
   consumer_sync();

@@ -25,6 +25,10 @@ int set_error(int code, const char* fmt, ...);
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
 size_t mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
+int ffn_decode(const cfb_ffn_args* a, cudaStream_t st);
+int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st);
+int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
+          cudaStream_t st);
 int cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
                        unsigned long long* traffic, cudaStream_t st);
 

@@ -1,0 +1,243 @@
+// Whole-model greedy decode engine (Llama2 family, batch 1): the native
+// runtime around the fused kernels.  One step = embed -> n_layers x
+// (split_token attention module, fused SwiGLU FFN) -> LM head + argmax; the
+// step is captured once into a CUDA graph and replayed, and the device-side
+// position/token it advances make consecutive replays decode consecutive
+// tokens without any host work.
+#include <vector>
+
+#include "common.h"
+
+struct cfb_llama {
+  cfb_llama_config cfg;
+  std::vector<const void*> attn_norm, w_qkv, w_out, ffn_norm, w_gu, w_dn;
+  std::vector<void*> k_cache, v_cache;
+  const void* embed = nullptr;
+  const void* final_norm = nullptr;
+  const void* lm_head = nullptr;
+  const float* rope_cs = nullptr;
+  // workspace (engine-owned)
+  float* resid[2] = {nullptr, nullptr};
+  void* act = nullptr;
+  float* out_partial = nullptr;
+  unsigned* tickets = nullptr;
+  unsigned long long* barrier = nullptr;
+  float* logits = nullptr;
+  float* cand_val = nullptr;
+  int* cand_idx = nullptr;
+  unsigned* lm_ticket = nullptr;
+  int* token = nullptr;
+  int* pos = nullptr;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+namespace {
+
+int alloc_zero(void** p, size_t bytes) {
+  CFB_CUDA(cudaMalloc(p, bytes));
+  CFB_CUDA(cudaMemset(*p, 0, bytes));
+  return CFB_OK;
+}
+
+int enqueue_step(cfb_llama* m, cudaStream_t st) {
+  const cfb_llama_config& c = m->cfg;
+  int rc = cfb::embed(c.dtype, m->embed, m->token, m->resid[0], 1, c.hidden, st);
+  if (rc) return rc;
+  for (int l = 0; l < c.n_layers; ++l) {
+    cfb_mha_args a = {};
+    a.dtype = c.dtype;
+    a.batch = 1;
+    a.hidden = c.hidden;
+    a.n_heads = c.n_heads;
+    a.head_dim = c.head_dim;
+    a.head_pad = c.head_dim;
+    a.cluster = c.cluster;
+    a.cache_cap = c.cache_cap;
+    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_RESID;
+    a.resid = m->resid[0];
+    a.norm_w = m->attn_norm[l];
+    a.eps = c.eps;
+    a.w_qkv = m->w_qkv[l];
+    a.w_out = m->w_out[l];
+    a.k_cache = m->k_cache[l];
+    a.v_cache = m->v_cache[l];
+    a.rope_cs = m->rope_cs;
+    a.step_pos = m->pos;
+    a.out = m->resid[1];
+    a.out_partial = m->out_partial;
+    a.tickets = m->tickets;
+    if ((rc = cfb::mha_decode(&a, st))) return rc;
+    cfb_ffn_args f = {};
+    f.dtype = c.dtype;
+    f.batch = 1;
+    f.hidden = c.hidden;
+    f.inter = c.inter;
+    f.flags = CFB_NORM | CFB_RESID;
+    f.eps = c.eps;
+    f.resid = m->resid[1];
+    f.norm_w = m->ffn_norm[l];
+    f.w_gu = m->w_gu[l];
+    f.w_dn = m->w_dn[l];
+    f.act = m->act;
+    f.out = m->resid[0];
+    f.barrier = m->barrier;
+    if ((rc = cfb::ffn_decode(&f, st))) return rc;
+  }
+  cfb_lm_args h = {};
+  h.dtype = c.dtype;
+  h.batch = 1;
+  h.hidden = c.hidden;
+  h.vocab = c.vocab;
+  h.eps = c.eps;
+  h.resid = m->resid[0];
+  h.norm_w = m->final_norm;
+  h.w = m->lm_head;
+  h.logits = m->logits;
+  h.cand_val = m->cand_val;
+  h.cand_idx = m->cand_idx;
+  h.ticket = m->lm_ticket;
+  h.token_out = m->token;
+  h.step_pos = m->pos;
+  return cfb::lm_head_argmax(&h, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cfb_llama** out) {
+  using cfb::set_error;
+  if (!cfg || !w || !out) return set_error(CFB_ERR_ARGUMENT, "null argument");
+  if (cfg->n_layers < 1 || !w->attn_norm || !w->w_qkv || !w->w_out || !w->ffn_norm || !w->w_gu ||
+      !w->w_dn || !w->k_cache || !w->v_cache || !w->embed || !w->final_norm || !w->lm_head ||
+      !w->rope_cs)
+    return set_error(CFB_ERR_ARGUMENT, "missing weight pointers");
+  cfb_llama* m = new cfb_llama();
+  m->cfg = *cfg;
+  const int L = cfg->n_layers;
+  m->attn_norm.assign(w->attn_norm, w->attn_norm + L);
+  m->w_qkv.assign(w->w_qkv, w->w_qkv + L);
+  m->w_out.assign(w->w_out, w->w_out + L);
+  m->ffn_norm.assign(w->ffn_norm, w->ffn_norm + L);
+  m->w_gu.assign(w->w_gu, w->w_gu + L);
+  m->w_dn.assign(w->w_dn, w->w_dn + L);
+  m->k_cache.assign(w->k_cache, w->k_cache + L);
+  m->v_cache.assign(w->v_cache, w->v_cache + L);
+  m->embed = w->embed;
+  m->final_norm = w->final_norm;
+  m->lm_head = w->lm_head;
+  m->rope_cs = w->rope_cs;
+  const size_t D = cfg->hidden;
+  int rc = 0;
+  int sms = cfb_device_sm_count();
+  if (sms <= 0) sms = 148;
+  const size_t tickets = cfb::mha_ticket_count(cfg->hidden, cfg->head_dim, cfg->cluster, cfg->dtype);
+  if ((rc = alloc_zero((void**)&m->resid[0], D * 4)) || (rc = alloc_zero((void**)&m->resid[1], D * 4)) ||
+      (rc = alloc_zero(&m->act, (size_t)cfg->inter * cfg->dtype)) ||
+      (rc = alloc_zero((void**)&m->out_partial, (size_t)cfg->n_heads * D * 4)) ||
+      (rc = alloc_zero((void**)&m->tickets, tickets * 4)) ||
+      (rc = alloc_zero((void**)&m->barrier, 8)) ||
+      (rc = alloc_zero((void**)&m->logits, (size_t)cfg->vocab * 4)) ||
+      (rc = alloc_zero((void**)&m->cand_val, (size_t)sms * 4)) ||
+      (rc = alloc_zero((void**)&m->cand_idx, (size_t)sms * 4)) ||
+      (rc = alloc_zero((void**)&m->lm_ticket, 4)) || (rc = alloc_zero((void**)&m->token, 4)) ||
+      (rc = alloc_zero((void**)&m->pos, 4))) {
+    cfb_llama_destroy(m);
+    return rc;
+  }
+  *out = m;
+  return CFB_OK;
+}
+
+int cfb_llama_destroy(cfb_llama* m) {
+  if (!m) return CFB_OK;
+  if (m->exec) cudaGraphExecDestroy(m->exec);
+  if (m->graph) cudaGraphDestroy(m->graph);
+  void* bufs[] = {m->resid[0], m->resid[1], m->act,      m->out_partial, m->tickets, m->barrier,
+                  m->logits,   m->cand_val, m->cand_idx, m->lm_ticket,   m->token,   m->pos};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  delete m;
+  return CFB_OK;
+}
+
+int cfb_llama_set_state(cfb_llama* m, int pos, int token, void* stream) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (pos < 0 || pos >= m->cfg.cache_cap)
+    return cfb::set_error(CFB_ERR_DIMENSION, "pos %d outside cache capacity %d", pos, m->cfg.cache_cap);
+  if (token < 0 || token >= m->cfg.vocab) return cfb::set_error(CFB_ERR_DIMENSION, "token out of range");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  static thread_local int host[2];
+  host[0] = pos;
+  host[1] = token;
+  CFB_CUDA(cudaMemcpyAsync(m->pos, &host[0], 4, cudaMemcpyHostToDevice, st));
+  CFB_CUDA(cudaMemcpyAsync(m->token, &host[1], 4, cudaMemcpyHostToDevice, st));
+  CFB_CUDA(cudaStreamSynchronize(st));
+  return CFB_OK;
+}
+
+int cfb_llama_step(cfb_llama* m, void* stream) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  return enqueue_step(m, static_cast<cudaStream_t>(stream));
+}
+
+int cfb_llama_capture(cfb_llama* m, void* stream) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (m->exec) {
+    cudaGraphExecDestroy(m->exec);
+    m->exec = nullptr;
+  }
+  if (m->graph) {
+    cudaGraphDestroy(m->graph);
+    m->graph = nullptr;
+  }
+  CFB_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+  const int rc = enqueue_step(m, st);
+  cudaGraph_t g = nullptr;
+  const cudaError_t e = cudaStreamEndCapture(st, &g);
+  if (rc) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  CFB_CUDA(e);
+  m->graph = g;
+  CFB_CUDA(cudaGraphInstantiate(&m->exec, g, 0));
+  return CFB_OK;
+}
+
+int cfb_llama_replay(cfb_llama* m, void* stream) {
+  if (!m || !m->exec) return cfb::set_error(CFB_ERR_ARGUMENT, "engine has no captured graph");
+  CFB_CUDA(cudaGraphLaunch(m->exec, static_cast<cudaStream_t>(stream)));
+  return CFB_OK;
+}
+
+int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, float** resid) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (logits) *logits = m->logits;
+  if (token) *token = m->token;
+  if (pos) *pos = m->pos;
+  if (resid) *resid = m->resid[0];
+  return CFB_OK;
+}
+
+int cfb_llama_launches_per_step(const cfb_llama* m) { return m ? 2 + 2 * m->cfg.n_layers : 0; }
+
+int cfb_llama_read(cfb_llama* m, int* token_host, float* logits_host, void* stream) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (token_host) CFB_CUDA(cudaMemcpyAsync(token_host, m->token, 4, cudaMemcpyDeviceToHost, st));
+  if (logits_host)
+    CFB_CUDA(cudaMemcpyAsync(logits_host, m->logits, (size_t)m->cfg.vocab * 4, cudaMemcpyDeviceToHost, st));
+  return CFB_OK;
+}
+
+int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream) {
+  if (!m || !token_host) return cfb::set_error(CFB_ERR_ARGUMENT, "null argument");
+  CFB_CUDA(cudaMemcpyAsync(m->token, token_host, 4, cudaMemcpyHostToDevice,
+                           static_cast<cudaStream_t>(stream)));
+  return CFB_OK;
+}
+
+}  // extern "C"

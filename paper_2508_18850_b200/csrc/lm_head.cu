@@ -1,0 +1,201 @@
+// Final RMSNorm + LM-head GEMV + greedy argmax (one launch), and the
+// token-embedding gather that starts a decode step.  No reference
+// counterpart (SPEC.md:298 lists the LM head as a non-goal); these close the
+// north-star decode loop around the fused attention / FFN modules.
+//
+// Argmax semantics = numpy.argmax: first index of the maximum.  Each CTA
+// reduces its vocabulary slice; the last CTA to finish (ticket) reduces the
+// per-CTA candidates in CTA order, writes the token and advances the step
+// position, so a captured CUDA graph can be replayed step after step.
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "gemv.cuh"
+
+namespace cfb {
+
+struct LmParams {
+  int B, D, V, flags;
+  float eps;
+  const float* resid;
+  const void* norm_w;
+  const void* w;        // [V][D] T
+  float* logits;        // [B][V] fp32 (nullable)
+  float* cand_val;      // [G][B]
+  int* cand_idx;        // [G][B]
+  unsigned* ticket;     // 1 counter
+  int* token_out;       // [B]
+  int* step_pos;        // advanced by 1 when non-null
+};
+
+__device__ __forceinline__ bool better(float v, int i, float bv, int bi) {
+  return v > bv || (v == bv && i < bi) || (bv != bv);  // NaN-free inputs assumed
+}
+
+template <typename T, int QB>
+__global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) {
+  extern __shared__ __align__(128) char smem[];
+  constexpr int tb = sizeof(T);
+  const int B = p.B, D = p.D, V = p.V, G = gridDim.x, i = blockIdx.x;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRingBytes);
+  const Ring ring{smem, bars, bars + kNumSlots};
+  T* xs = reinterpret_cast<T*>(smem + kRingBytes + 2 * kNumSlots * 8);
+  float* red = reinterpret_cast<float*>(reinterpret_cast<char*>(xs) + ((B * D * tb + 15) & ~15));
+  float* wv = red + kNumConsumerWarps * B;
+  int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int v0 = (int)((long long)i * V / G), v1 = (int)((long long)(i + 1) * V / G);
+  if (tid == 0) {
+    ring_init(ring);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)v0 * D, nullptr, v1 - v0, D * tb);
+  if (warp == kNumConsumerWarps) {
+    if (lane == 0) {
+      int cnt[kNumConsumerWarps] = {};
+      produce_phase(P0, ring, cnt, policy_evict_first());
+    }
+    return;
+  }
+  rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  float bv[QB];
+  int bi[QB];
+#pragma unroll
+  for (int b = 0; b < QB; ++b) {
+    bv[b] = -INFINITY;
+    bi[b] = 0x7fffffff;
+  }
+  int cnt = 0;
+  RowDot<T, QB> rd;
+  consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+    rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
+      const int v = v0 + row;
+#pragma unroll
+      for (int b = 0; b < QB; ++b)
+        if (b < B) {
+          if (lane == 0 && p.logits) p.logits[(size_t)b * V + v] = s[b];
+          if (better(s[b], v, bv[b], bi[b])) {
+            bv[b] = s[b];
+            bi[b] = v;
+          }
+        }
+    });
+  });
+  if (lane == 0)
+    for (int b = 0; b < B; ++b) {
+      wv[warp * B + b] = bv[b < QB ? b : 0];
+      wi[warp * B + b] = bi[b < QB ? b : 0];
+    }
+  consumer_sync();
+  if (tid < B) {
+    float v = -INFINITY;
+    int ix = 0x7fffffff;
+    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
+      if (better(wv[w2 * B + tid], wi[w2 * B + tid], v, ix)) {
+        v = wv[w2 * B + tid];
+        ix = wi[w2 * B + tid];
+      }
+    p.cand_val[(size_t)i * B + tid] = v;
+    p.cand_idx[(size_t)i * B + tid] = ix;
+  }
+  __threadfence();
+  consumer_sync();
+  __shared__ unsigned last;
+  if (tid == 0) last = (atomicAdd(p.ticket, 1u) == (unsigned)G - 1);
+  consumer_sync();
+  if (last) {
+    __threadfence();
+    if (tid < B) {
+      float v = -INFINITY;
+      int ix = 0x7fffffff;
+      for (int c = 0; c < G; ++c) {
+        const float cv = __ldcg(&p.cand_val[(size_t)c * B + tid]);
+        const int ci = __ldcg(&p.cand_idx[(size_t)c * B + tid]);
+        if (better(cv, ci, v, ix)) {
+          v = cv;
+          ix = ci;
+        }
+      }
+      p.token_out[tid] = ix;
+    }
+    if (tid == 0) {
+      *p.ticket = 0;
+      if (p.step_pos) *p.step_pos += 1;
+    }
+  }
+}
+
+template <typename T>
+__global__ void embed_kernel(const T* table, const int* tokens, float* out, int B, int D) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < B * D; idx += gridDim.x * blockDim.x) {
+    const int b = idx / D, d = idx % D;
+    out[idx] = Elem<T>::to_f(table[(size_t)tokens[b] * D + d]);
+  }
+}
+
+template <typename T, int QB>
+static int launch_lm_inst(const LmParams& p, int grid, size_t smem, cudaStream_t st) {
+  auto kern = lm_head_kernel<T, QB>;
+  static bool configured = false;
+  if (!configured) {
+    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+    configured = true;
+  }
+  kern<<<grid, kThreads, smem, st>>>(p);
+  CFB_CUDA(cudaGetLastError());
+  return CFB_OK;
+}
+
+int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
+  if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
+  const int tb = a->dtype;
+  if (tb != CFB_F16 && tb != CFB_F32) return set_error(CFB_ERR_ARGUMENT, "bad dtype");
+  if (a->batch < 1 || a->batch > 8) return set_error(CFB_ERR_DIMENSION, "lm batch must be in [1, 8]");
+  if ((a->hidden * tb) % 16) return set_error(CFB_ERR_DIMENSION, "hidden must give 16-byte rows");
+  if (!a->resid || !a->norm_w || !a->w || !a->cand_val || !a->cand_idx || !a->ticket || !a->token_out)
+    return set_error(CFB_ERR_ARGUMENT, "null pointer");
+  int dev = 0, sms = 0;
+  CFB_CUDA(cudaGetDevice(&dev));
+  CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int grid = a->grid > 0 ? a->grid : sms;
+  if (grid > a->vocab) grid = a->vocab;
+  const size_t smem = kRingBytes + 2 * kNumSlots * 8 + ((a->batch * a->hidden * tb + 15) & ~15) +
+                      3 * kNumConsumerWarps * a->batch * 4;
+  if (smem > (size_t)kMaxSmem) return set_error(CFB_ERR_SMEM, "lm head needs too much smem");
+  LmParams p;
+  p.B = a->batch;
+  p.D = a->hidden;
+  p.V = a->vocab;
+  p.flags = 0;
+  p.eps = a->eps;
+  p.resid = a->resid;
+  p.norm_w = a->norm_w;
+  p.w = a->w;
+  p.logits = a->logits;
+  p.cand_val = a->cand_val;
+  p.cand_idx = a->cand_idx;
+  p.ticket = a->ticket;
+  p.token_out = a->token_out;
+  p.step_pos = a->step_pos;
+  if (tb == 2) {
+    if (p.B == 1) return launch_lm_inst<__half, 1>(p, grid, smem, st);
+    return launch_lm_inst<__half, 8>(p, grid, smem, st);
+  }
+  if (p.B == 1) return launch_lm_inst<float, 1>(p, grid, smem, st);
+  return launch_lm_inst<float, 8>(p, grid, smem, st);
+}
+
+int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
+          cudaStream_t st) {
+  if (!table || !tokens || !out) return set_error(CFB_ERR_ARGUMENT, "null pointer");
+  const int threads = 256, blocks = (B * D + threads - 1) / threads;
+  if (dtype == CFB_F16)
+    embed_kernel<__half><<<blocks, threads, 0, st>>>(static_cast<const __half*>(table), tokens, out, B, D);
+  else
+    embed_kernel<float><<<blocks, threads, 0, st>>>(static_cast<const float*>(table), tokens, out, B, D);
+  CFB_CUDA(cudaGetLastError());
+  return CFB_OK;
+}
+
+}  // namespace cfb

@@ -224,3 +224,70 @@ def cluster_collective(payloads: np.ndarray, op: str, dtype_bytes: int = 4):
                                                        _native.stream_ptr()))
     torch.cuda.synchronize()
     return out.float().cpu().numpy(), int(traffic.item())
+
+
+def run_fused_ffn(z, w1, w2, w3, activation: str = "silu", dtype_bytes: int = 2,
+                  resid=None, norm_w=None, eps: float = 1e-5) -> np.ndarray:
+    """Fused gate/up -> SiLU*mul -> down in one launch; the reference's
+    ``ffn_reference(z, w1, w2, w3, "silu")`` (oracle.py:112-131).
+
+    With ``resid``/``norm_w`` the kernel computes z = f16(rmsnorm(resid)*norm_w)
+    itself and returns resid + FFN(z) (the decoder-block form).  The
+    activation vector is stored at ``dtype_bytes`` precision between the two
+    GEMVs (it crosses CTAs through HBM)."""
+    import torch
+    if activation != "silu":
+        raise DimensionError("the fused FFN kernel implements the SwiGLU ('silu') gate only")
+    dev = _native.require_cuda()
+    w1, w2, w3 = (np.asarray(a, np.float32) for a in (w1, w2, w3))
+    F, D = w1.shape
+    if w2.shape != (F, D) or w3.shape != (D, F):
+        from .exceptions import ShapeMismatch
+        raise ShapeMismatch(f"ffn shapes inconsistent: w1 {w1.shape}, w2 {w2.shape}, w3 {w3.shape}")
+    dt = torch.float16 if dtype_bytes == 2 else torch.float32
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).to(dt)
+
+    flags = 0
+    B = (np.asarray(resid) if resid is not None else np.asarray(z)).shape[0]
+    x = up(z) if resid is None else None
+    r = torch.from_numpy(np.ascontiguousarray(resid, np.float32)).to(dev) if resid is not None else None
+    g = up(norm_w) if norm_w is not None else None
+    if resid is not None:
+        flags |= _native.NORM | _native.RESID
+    w_gu = torch.stack([up(w1), up(w2)], 1).contiguous()
+    w_dn = up(w3)
+    act = torch.empty(B, F, device=dev, dtype=dt)
+    out = torch.empty(B, D, device=dev, dtype=torch.float32)
+    bar = torch.zeros(1, device=dev, dtype=torch.int64)
+    a = _native.FfnArgs(dtype=dtype_bytes, batch=B, hidden=D, inter=F, flags=flags, grid=0,
+                        eps=eps, x=_native.ptr(x), resid=_native.ptr(r), norm_w=_native.ptr(g),
+                        w_gu=w_gu.data_ptr(), w_dn=w_dn.data_ptr(), act=act.data_ptr(),
+                        out=out.data_ptr(), barrier=bar.data_ptr())
+    _native.check(_native.lib().cfb_ffn_decode(a, _native.stream_ptr()))
+    return out.cpu().numpy()
+
+
+def lm_head_argmax(resid, norm_w, w_lm, eps: float = 1e-5, dtype_bytes: int = 2):
+    """Final RMSNorm + LM head + greedy argmax on the GPU.  Returns
+    (logits (B, V) fp32, tokens (B,))."""
+    import torch
+    dev = _native.require_cuda()
+    dt = torch.float16 if dtype_bytes == 2 else torch.float32
+    r = torch.from_numpy(np.ascontiguousarray(resid, np.float32)).to(dev)
+    B, D = r.shape
+    w = torch.from_numpy(np.ascontiguousarray(w_lm, np.float32)).to(dev).to(dt)
+    V = w.shape[0]
+    g = torch.from_numpy(np.ascontiguousarray(norm_w, np.float32)).to(dev).to(dt)
+    logits = torch.empty(B, V, device=dev, dtype=torch.float32)
+    cv = torch.empty(1024 * B, device=dev, dtype=torch.float32)
+    ci = torch.empty(1024 * B, device=dev, dtype=torch.int32)
+    ticket = torch.zeros(1, device=dev, dtype=torch.int32)
+    tok = torch.empty(B, device=dev, dtype=torch.int32)
+    a = _native.LmArgs(dtype=dtype_bytes, batch=B, hidden=D, vocab=V, grid=0, eps=eps,
+                       resid=r.data_ptr(), norm_w=g.data_ptr(), w=w.data_ptr(),
+                       logits=logits.data_ptr(), cand_val=cv.data_ptr(), cand_idx=ci.data_ptr(),
+                       ticket=ticket.data_ptr(), token_out=tok.data_ptr(), step_pos=None)
+    _native.check(_native.lib().cfb_lm_head_argmax(a, _native.stream_ptr()))
+    return logits.cpu().numpy(), tok.cpu().numpy()

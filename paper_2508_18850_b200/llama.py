@@ -1,0 +1,297 @@
+"""Llama2-family greedy decode on the B200 kernels (north-star config #2).
+
+``LlamaDecoder`` holds the weights and KV cache in HBM in the kernels'
+layouts and drives the native engine (``cfb_llama_*`` in ``csrc/llama.cu``):
+one step = embed -> n_layers x (split_token attention module with RMSNorm,
+RoPE, KV append and residual -> fused SwiGLU FFN with RMSNorm and residual)
+-> final RMSNorm + LM head + argmax, captured once into a CUDA graph.
+
+Weights come either from ``random_llama_params`` (numpy, reference draw
+conventions of ``scenarios.py:108-137``; used for parity against the CPU
+oracle) or are drawn directly on the device in the packed layouts
+(``LlamaDecoder.random``; used by the benchmark, where generating 6.7 B
+parameters on the host would dominate the run).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError
+
+
+@dataclass(frozen=True)
+class LlamaConfig:
+    n_layers: int = 32
+    hidden: int = 4096
+    n_heads: int = 32
+    head_dim: int = 128
+    inter: int = 11008
+    vocab: int = 32000
+    eps: float = 1e-5
+    rope_theta: float = 10000.0
+    cluster: int = 4
+    dtype_bytes: int = 2
+
+    def weight_bytes(self) -> int:
+        """Bytes of every weight a decode step streams (attention + FFN + norms,
+        LM head, one embedding row) — SURVEY.md §8(d)."""
+        D, F, nb = self.hidden, self.inter, self.dtype_bytes
+        per_layer = (D * 3 * self.n_heads * self.head_dim + self.n_heads * self.head_dim * D
+                     + 3 * D * F) * nb + 2 * D * nb
+        return self.n_layers * per_layer + self.vocab * D * nb + D * nb + D * nb
+
+    def kv_bytes_per_position(self) -> int:
+        return self.n_layers * 2 * self.n_heads * self.head_dim * self.dtype_bytes
+
+    def step_bytes(self, ctx: int) -> int:
+        """Algorithmic HBM bytes of one decode step at `ctx` cached positions:
+        weights + KV read of ctx positions + KV write of the new one."""
+        return self.weight_bytes() + self.kv_bytes_per_position() * (ctx + 1)
+
+
+LLAMA2_7B = LlamaConfig()
+
+
+class _LlamaConfigC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "n_layers", "hidden", "n_heads", "head_dim",
+                                             "inter", "vocab", "cache_cap", "cluster")] + [
+        ("eps", ctypes.c_float)]
+
+
+_PP = ctypes.POINTER(ctypes.c_void_p)
+
+
+class _LlamaWeightsC(ctypes.Structure):
+    _fields_ = [("embed", ctypes.c_void_p), ("final_norm", ctypes.c_void_p),
+                ("lm_head", ctypes.c_void_p), ("rope_cs", ctypes.c_void_p)] + [
+        (n, _PP) for n in ("attn_norm", "w_qkv", "w_out", "ffn_norm", "w_gu", "w_dn",
+                           "k_cache", "v_cache")]
+
+
+def rope_table(max_pos: int, head_dim: int, theta: float) -> np.ndarray:
+    """(max_pos, H/2, 2) fp32 (cos, sin) of rotate-half RoPE; angles in fp64."""
+    half = head_dim // 2
+    inv_freq = theta ** (-(np.arange(half, dtype=np.float64) * 2.0) / head_dim)
+    ang = np.outer(np.arange(max_pos, dtype=np.float64), inv_freq)
+    return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
+
+
+def random_llama_params(cfg: LlamaConfig, seed: int = 0, prefill: int = 0) -> dict:
+    """Seeded numpy parameters in the reference's logical layouts.
+
+    Per layer l: default_rng(seed*1000 + l) draws attn_norm (1 + 0.1 N),
+    w_qkv (nh, D, 3H)*D^-1/2, w_out (nh, H, D)*H^-1/2, ffn_norm,
+    w1 (F, D)*D^-1/2, w2 (F, D)*D^-1/2, w3 (D, F)*F^-1/2, then the prefilled
+    K and V caches (nh, prefill, H) ~ N(0, 1); globals from seed*1000 + 999:
+    embed (V, D) ~ N(0, 1), final_norm, lm_head (V, D)*D^-1/2.  All values are
+    rounded to fp16."""
+    def draw(rng, shape, scale, shift=0.0):
+        x = (rng.standard_normal(shape) * scale + shift).astype(np.float32)
+        return x.astype(np.float16).astype(np.float32)
+
+    D, F, nh, H = cfg.hidden, cfg.inter, cfg.n_heads, cfg.head_dim
+    layers = []
+    for l in range(cfg.n_layers):
+        rng = np.random.default_rng(seed * 1000 + l)
+        layers.append(dict(
+            attn_norm=draw(rng, (D,), 0.1, 1.0),
+            w_qkv=draw(rng, (nh, D, 3 * H), D ** -0.5),
+            w_out=draw(rng, (nh, H, D), H ** -0.5),
+            ffn_norm=draw(rng, (D,), 0.1, 1.0),
+            w1=draw(rng, (F, D), D ** -0.5),
+            w2=draw(rng, (F, D), D ** -0.5),
+            w3=draw(rng, (D, F), F ** -0.5),
+            k_cache=draw(rng, (nh, prefill, H), 1.0),
+            v_cache=draw(rng, (nh, prefill, H), 1.0)))
+    rng = np.random.default_rng(seed * 1000 + 999)
+    return dict(layers=layers, embed=draw(rng, (cfg.vocab, D), 1.0),
+                final_norm=draw(rng, (D,), 0.1, 1.0), lm_head=draw(rng, (cfg.vocab, D), D ** -0.5))
+
+
+class LlamaDecoder:
+    """Device-resident Llama model + KV cache driving the native engine."""
+
+    def __init__(self, cfg: LlamaConfig, cache_cap: int):
+        import torch
+        if cfg.dtype_bytes != 2:
+            raise DimensionError("the decode engine runs fp16 storage only")
+        if cfg.head_dim % cfg.cluster or cfg.hidden % cfg.cluster:
+            raise DimensionError("head_dim and hidden must be divisible by the cluster size")
+        self.cfg = cfg
+        self.cache_cap = cache_cap
+        self.dev = _native.require_cuda()
+        self.torch = torch
+        self.layers: list[dict] = []
+        self._h = None
+        self._keep = []
+
+    # ------------------------------------------------------------ packing
+    def _pack_layer(self, lp: dict) -> dict:
+        """Logical numpy layer -> kernel layouts on device (see include/cfb.h)."""
+        torch, cfg, dev = self.torch, self.cfg, self.dev
+        D, nh, H, F, N = cfg.hidden, cfg.n_heads, cfg.head_dim, cfg.inter, cfg.cluster
+
+        def t(a):
+            return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).half()
+
+        w = t(lp["w_qkv"]).reshape(nh, D, 3, N, H // N)          # (nh, D, 3, N, h)
+        w_qkv = w.permute(0, 3, 2, 4, 1).contiguous()             # (nh, N, 3, h, D)
+        w_out = t(lp["w_out"]).transpose(1, 2).contiguous()       # (nh, D, H)
+        w_gu = torch.stack([t(lp["w1"]), t(lp["w2"])], 1).contiguous()  # (F, 2, D)
+        kc = torch.zeros(nh, self.cache_cap, H, device=dev, dtype=torch.float16)
+        vc = torch.zeros_like(kc)
+        S0 = lp["k_cache"].shape[1]
+        if S0:
+            kc[:, :S0] = t(lp["k_cache"])
+            vc[:, :S0] = t(lp["v_cache"])
+        return dict(attn_norm=t(lp["attn_norm"]), w_qkv=w_qkv, w_out=w_out,
+                    ffn_norm=t(lp["ffn_norm"]), w_gu=w_gu, w_dn=t(lp["w3"]), k_cache=kc,
+                    v_cache=vc)
+
+    @classmethod
+    def from_params(cls, cfg: LlamaConfig, params: dict, cache_cap: int) -> "LlamaDecoder":
+        m = cls(cfg, cache_cap)
+        torch = m.torch
+        m.layers = [m._pack_layer(lp) for lp in params["layers"]]
+
+        def t(a):
+            return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(m.dev).half()
+
+        m.embed, m.final_norm, m.lm_head = t(params["embed"]), t(params["final_norm"]), t(
+            params["lm_head"])
+        m._finish()
+        return m
+
+    @classmethod
+    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0) -> "LlamaDecoder":
+        """Weights and a full KV cache drawn on the device (torch Philox), packed
+        layouts directly.  Scales as random_llama_params."""
+        m = cls(cfg, cache_cap)
+        torch, dev = m.torch, m.dev
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        D, nh, H, F, N = cfg.hidden, cfg.n_heads, cfg.head_dim, cfg.inter, cfg.cluster
+
+        def rnd(shape, scale, shift=0.0):
+            x = torch.empty(shape, device=dev, dtype=torch.float16)
+            x.normal_(mean=shift, std=scale, generator=g)
+            return x
+
+        for _ in range(cfg.n_layers):
+            m.layers.append(dict(
+                attn_norm=rnd((D,), 0.1, 1.0), w_qkv=rnd((nh, N, 3, H // N, D), D ** -0.5),
+                w_out=rnd((nh, D, H), H ** -0.5), ffn_norm=rnd((D,), 0.1, 1.0),
+                w_gu=rnd((F, 2, D), D ** -0.5), w_dn=rnd((D, F), F ** -0.5),
+                k_cache=rnd((nh, cache_cap, H), 1.0), v_cache=rnd((nh, cache_cap, H), 1.0)))
+        m.embed = rnd((cfg.vocab, D), 1.0)
+        m.final_norm = rnd((D,), 0.1, 1.0)
+        m.lm_head = rnd((cfg.vocab, D), D ** -0.5)
+        m._finish()
+        return m
+
+    def _finish(self):
+        cfg, torch = self.cfg, self.torch
+        self.rope = torch.from_numpy(rope_table(self.cache_cap, cfg.head_dim, cfg.rope_theta)).to(
+            self.dev)
+        L = cfg.n_layers
+
+        def arr(key):
+            a = (ctypes.c_void_p * L)(*[self.layers[i][key].data_ptr() for i in range(L)])
+            self._keep.append(a)
+            return ctypes.cast(a, _PP)
+
+        c = _LlamaConfigC(dtype=2, n_layers=L, hidden=cfg.hidden, n_heads=cfg.n_heads,
+                          head_dim=cfg.head_dim, inter=cfg.inter, vocab=cfg.vocab,
+                          cache_cap=self.cache_cap, cluster=cfg.cluster, eps=cfg.eps)
+        w = _LlamaWeightsC(embed=self.embed.data_ptr(), final_norm=self.final_norm.data_ptr(),
+                           lm_head=self.lm_head.data_ptr(), rope_cs=self.rope.data_ptr(),
+                           attn_norm=arr("attn_norm"), w_qkv=arr("w_qkv"), w_out=arr("w_out"),
+                           ffn_norm=arr("ffn_norm"), w_gu=arr("w_gu"), w_dn=arr("w_dn"),
+                           k_cache=arr("k_cache"), v_cache=arr("v_cache"))
+        L_ = _native.lib()
+        L_.cfb_llama_create.argtypes = [ctypes.POINTER(_LlamaConfigC),
+                                        ctypes.POINTER(_LlamaWeightsC),
+                                        ctypes.POINTER(ctypes.c_void_p)]
+        h = ctypes.c_void_p()
+        _native.check(L_.cfb_llama_create(c, w, ctypes.byref(h)))
+        self._h = h
+        for name in ("cfb_llama_step", "cfb_llama_capture", "cfb_llama_replay",
+                     "cfb_llama_destroy", "cfb_llama_launches_per_step"):
+            getattr(L_, name).argtypes = [ctypes.c_void_p] + ([ctypes.c_void_p]
+                                                              if name not in ("cfb_llama_destroy",
+                                                                              "cfb_llama_launches_per_step")
+                                                              else [])
+        L_.cfb_llama_set_state.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                           ctypes.c_void_p]
+        L_.cfb_llama_read.argtypes = [ctypes.c_void_p] * 4
+        L_.cfb_llama_write_token.argtypes = [ctypes.c_void_p] * 3
+        self._lib = L_
+
+    # ------------------------------------------------------------ driving
+    @property
+    def launches_per_step(self) -> int:
+        return int(self._lib.cfb_llama_launches_per_step(self._h))
+
+    def set_state(self, pos: int, token: int) -> None:
+        _native.check(self._lib.cfb_llama_set_state(self._h, pos, token, _native.stream_ptr()))
+
+    def step(self) -> None:
+        """Eager launches of one decode step (no graph)."""
+        _native.check(self._lib.cfb_llama_step(self._h, _native.stream_ptr()))
+
+    def capture(self) -> None:
+        """Capture one step into a CUDA graph (call step() once before, so
+        kernel attributes are configured outside capture)."""
+        _native.check(self._lib.cfb_llama_capture(self._h, _native.stream_ptr()))
+
+    def replay(self) -> None:
+        _native.check(self._lib.cfb_llama_replay(self._h, _native.stream_ptr()))
+
+    def read_token_async(self, host_int32_ptr: int) -> None:
+        """Stream-ordered D2H copy of the current token into host memory."""
+        _native.check(self._lib.cfb_llama_read(self._h, ctypes.c_void_p(host_int32_ptr), None,
+                                               _native.stream_ptr()))
+
+    def write_token_async(self, host_int32_ptr: int) -> None:
+        """Stream-ordered H2D copy of the next input token from host memory."""
+        _native.check(self._lib.cfb_llama_write_token(self._h, ctypes.c_void_p(host_int32_ptr),
+                                                      _native.stream_ptr()))
+
+    def token(self) -> int:
+        buf = np.zeros(1, np.int32)
+        self.read_token_async(buf.ctypes.data)
+        self.torch.cuda.synchronize()
+        return int(buf[0])
+
+    def logits(self) -> np.ndarray:
+        buf = np.zeros(self.cfg.vocab, np.float32)
+        _native.check(self._lib.cfb_llama_read(self._h, None, ctypes.c_void_p(buf.ctypes.data),
+                                               _native.stream_ptr()))
+        self.torch.cuda.synchronize()
+        return buf
+
+    def generate(self, first_token: int, pos: int, n_tokens: int, use_graph: bool = True) -> list:
+        """Greedy decode n_tokens starting at cache position pos."""
+        self.set_state(pos, first_token)
+        out = []
+        if use_graph:
+            self.step()
+            self.set_state(pos, first_token)
+            self.capture()
+        for _ in range(n_tokens):
+            self.replay() if use_graph else self.step()
+            out.append(self.token())
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None:
+            try:
+                self._lib.cfb_llama_destroy(self._h)
+            except Exception:
+                pass
+            self._h = None
