@@ -42,9 +42,9 @@ __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int 
   int o = kRingBytes;
   L.bars = o;  o += 2 * kNumSlots * 8;
   L.x = o;     o += ((B * D * tb + 15) & ~15);
-  L.gu = o;    o += 2 * B * fmax * 4;
+  L.gu = o;    o += (2 * B * fmax * 4 + 15) & ~15;
   L.act = o;   o += ((B * F * tb + 15) & ~15);
-  L.red = o;   o += kNumConsumerWarps * B * 4;
+  L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
   L.total = o;
   return L;
 }

@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   float* red = reinterpret_cast<float*>(reinterpret_cast<char*>(xs) + ((B * D * tb + 15) & ~15));
   float* wv = red + kNumConsumerWarps * B;
   int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
+  unsigned& last = *reinterpret_cast<unsigned*>(wi + kNumConsumerWarps * B);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int v0 = (int)((long long)i * V / G), v1 = (int)((long long)(i + 1) * V / G);
   if (tid == 0) {
@@ -101,7 +102,6 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   }
   __threadfence();
   consumer_sync();
-  __shared__ unsigned last;
   if (tid == 0) last = (atomicAdd(p.ticket, 1u) == (unsigned)G - 1);
   consumer_sync();
   if (last) {
@@ -161,7 +161,7 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   int grid = a->grid > 0 ? a->grid : sms;
   if (grid > a->vocab) grid = a->vocab;
   const size_t smem = kRingBytes + 2 * kNumSlots * 8 + ((a->batch * a->hidden * tb + 15) & ~15) +
-                      3 * kNumConsumerWarps * a->batch * 4;
+                      3 * kNumConsumerWarps * a->batch * 4 + 16;
   if (smem > (size_t)kMaxSmem) return set_error(CFB_ERR_SMEM, "lm head needs too much smem");
   LmParams p;
   p.B = a->batch;
