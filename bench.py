@@ -109,7 +109,7 @@ def run_ours(args, rank, world):
     cap = max(ctxs) + args.warmup + args.steps + 8
     model = LlamaDecoder.random(cfg, cache_cap=cap, seed=1234 + rank)
     L = _native.lib()
-    st = torch.cuda.current_stream()
+    st = model.stream
 
     # configure kernels outside capture, then capture one step
     model.set_state(ctxs[0], 1)
@@ -128,7 +128,7 @@ def run_ours(args, rank, world):
             for _ in range(args.warmup):
                 model.replay()
             model.set_state(ctx, 1)
-            torch.cuda.synchronize()
+            st.synchronize()
             if world > 1:
                 torch.distributed.barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -159,10 +159,10 @@ def run_ours(args, rank, world):
             t0 = time.perf_counter()
             for _ in range(args.steps):
                 _native.check(L.cfb_llama_write_token(model._h, ctypes.c_void_p(host_in.data_ptr()),
-                                                      _native.stream_ptr()))
+                                                      model._sp()))
                 model.replay()
                 _native.check(L.cfb_llama_read(model._h, ctypes.c_void_p(host_out.data_ptr()),
-                                               None, _native.stream_ptr()))
+                                               None, model._sp()))
                 st.synchronize()
                 host_in[0] = host_out[0]
             dt = time.perf_counter() - t0
@@ -185,13 +185,14 @@ def run_ours(args, rank, world):
             resid=resid.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
             w_dn=lyr["w_dn"].data_ptr(), act=act.data_ptr(), out=out.data_ptr(),
             barrier=bar.data_ptr()))
+    torch.cuda.synchronize()
     for a in fargs[:4]:
-        _native.check(L.cfb_ffn_decode(a, _native.stream_ptr()))
+        _native.check(L.cfb_ffn_decode(a, model._sp()))
     reps = 4 * len(fargs)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     for i in range(reps):
-        _native.check(L.cfb_ffn_decode(fargs[i % len(fargs)], _native.stream_ptr()))
+        _native.check(L.cfb_ffn_decode(fargs[i % len(fargs)], model._sp()))
     e1.record(st)
     torch.cuda.synchronize()
     ffn_us = e0.elapsed_time(e1) * 1e3 / reps

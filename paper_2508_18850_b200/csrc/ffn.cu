@@ -32,6 +32,8 @@ struct FfnParams {
   unsigned long long* barrier;
 };
 
+// x (phase 0 input, B x D) and act (phase 1 input, B x F) are never live at
+// the same time and share one region.
 struct FfnLayout {
   int bars, x, gu, act, red, total;
 };
@@ -41,9 +43,9 @@ __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int 
   const int fmax = F / G + 1;
   int o = kRingBytes;
   L.bars = o;  o += 2 * kNumSlots * 8;
-  L.x = o;     o += ((B * D * tb + 15) & ~15);
+  L.x = o;
+  L.act = o;   o += ((B * (D > F ? D : F) * tb + 15) & ~15);
   L.gu = o;    o += (2 * B * fmax * 4 + 15) & ~15;
-  L.act = o;   o += ((B * F * tb + 15) & ~15);
   L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
   L.total = o;
   return L;

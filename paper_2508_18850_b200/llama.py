@@ -129,6 +129,7 @@ class LlamaDecoder:
         self.layers: list[dict] = []
         self._h = None
         self._keep = []
+        self.stream = torch.cuda.Stream(device=self.dev)  # capture needs a non-default stream
 
     # ------------------------------------------------------------ packing
     def _pack_layer(self, lp: dict) -> dict:
@@ -233,46 +234,49 @@ class LlamaDecoder:
         self._lib = L_
 
     # ------------------------------------------------------------ driving
+    def _sp(self) -> int:
+        return self.stream.cuda_stream
+
     @property
     def launches_per_step(self) -> int:
         return int(self._lib.cfb_llama_launches_per_step(self._h))
 
     def set_state(self, pos: int, token: int) -> None:
-        _native.check(self._lib.cfb_llama_set_state(self._h, pos, token, _native.stream_ptr()))
+        _native.check(self._lib.cfb_llama_set_state(self._h, pos, token, self._sp()))
 
     def step(self) -> None:
         """Eager launches of one decode step (no graph)."""
-        _native.check(self._lib.cfb_llama_step(self._h, _native.stream_ptr()))
+        _native.check(self._lib.cfb_llama_step(self._h, self._sp()))
 
     def capture(self) -> None:
         """Capture one step into a CUDA graph (call step() once before, so
         kernel attributes are configured outside capture)."""
-        _native.check(self._lib.cfb_llama_capture(self._h, _native.stream_ptr()))
+        _native.check(self._lib.cfb_llama_capture(self._h, self._sp()))
 
     def replay(self) -> None:
-        _native.check(self._lib.cfb_llama_replay(self._h, _native.stream_ptr()))
+        _native.check(self._lib.cfb_llama_replay(self._h, self._sp()))
 
     def read_token_async(self, host_int32_ptr: int) -> None:
         """Stream-ordered D2H copy of the current token into host memory."""
         _native.check(self._lib.cfb_llama_read(self._h, ctypes.c_void_p(host_int32_ptr), None,
-                                               _native.stream_ptr()))
+                                               self._sp()))
 
     def write_token_async(self, host_int32_ptr: int) -> None:
         """Stream-ordered H2D copy of the next input token from host memory."""
         _native.check(self._lib.cfb_llama_write_token(self._h, ctypes.c_void_p(host_int32_ptr),
-                                                      _native.stream_ptr()))
+                                                      self._sp()))
 
     def token(self) -> int:
         buf = np.zeros(1, np.int32)
         self.read_token_async(buf.ctypes.data)
-        self.torch.cuda.synchronize()
+        self.stream.synchronize()
         return int(buf[0])
 
     def logits(self) -> np.ndarray:
         buf = np.zeros(self.cfg.vocab, np.float32)
         _native.check(self._lib.cfb_llama_read(self._h, None, ctypes.c_void_p(buf.ctypes.data),
-                                               _native.stream_ptr()))
-        self.torch.cuda.synchronize()
+                                               self._sp()))
+        self.stream.synchronize()
         return buf
 
     def generate(self, first_token: int, pos: int, n_tokens: int, use_graph: bool = True) -> list:
