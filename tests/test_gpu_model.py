@@ -107,14 +107,14 @@ def _teacher_forced(cfg, prefill, steps, seed, atol):
 def test_llama_small_teacher_forced_greedy():
     cfg = LlamaConfig(n_layers=3, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
                       cluster=4)
-    _teacher_forced(cfg, prefill=37, steps=6, seed=1, atol=2e-3)
+    _teacher_forced(cfg, prefill=37, steps=6, seed=1, atol=2e-2)
 
 
 @pytest.mark.parametrize("cluster", [2, 8, 16])
 def test_llama_small_cluster_sizes(cluster):
     cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
                       cluster=cluster)
-    _teacher_forced(cfg, prefill=50, steps=3, seed=2, atol=2e-3)
+    _teacher_forced(cfg, prefill=50, steps=3, seed=2, atol=2e-2)
 
 
 def test_llama_full_width_two_layers():
