@@ -25,7 +25,7 @@
 namespace cfb {
 
 struct MhaParams {
-  int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags;
+  int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags, spw;
   float sqrt_h, eps;
   const void* x;
   const float* resid;
@@ -50,7 +50,7 @@ struct MhaLayout {
 
 __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int tb) {
+__host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int tb, int spw) {
   MhaLayout L;
   const int h = Hp / N;
   int rounds = 0;
@@ -58,9 +58,9 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.seg_bytes = round16(B * 3 * h * tb);
   L.a_bytes = round16(B * Hp * tb);
   L.st_bytes = round16(2 * B * tb);
-  int o = kRingBytes;
+  int o = ring_bytes(spw);
   L.bars = o;       o += (2 * kNumSlots + 16) * 8;
-  L.x = o;          o += round16(B * D * tb);
+  L.x = o;          o += round16(B * D * 4);  // fp32 activations
   L.gbuf = o;       o += N * L.seg_bytes;
   L.qf = o;         o += 3 * B * Hp * 4;
   L.ws_acc = o;     o += kNumConsumerWarps * B * Hp * 4;
@@ -83,9 +83,9 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   const int B = p.B, D = p.D, Hp = p.Hp;
   const uint32_t N = p.N;
   const int h = Hp / N;
-  const MhaLayout L = mha_layout(B, D, Hp, N, tb);
+  const MhaLayout L = mha_layout(B, D, Hp, N, tb, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  const Ring ring{smem, bars, bars + kNumSlots};
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
   uint64_t* cbar = bars + 2 * kNumSlots;  // [0,4) gather, [4,8) max/merge, [8,12) sum, [12,16) attn
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -126,12 +126,12 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
                               nullptr, cols, Hp * tb);
 
   if (warp == kNumConsumerWarps) {  // ------------------------------ producer
-    if (lane == 0) {
-      int cnt[kNumConsumerWarps] = {};
+    if (lane < kNumConsumerWarps) {
+      int c = 0;
       const uint64_t pol = policy_evict_first();
-      produce_phase(P0, ring, cnt, pol);
-      produce_phase(P1, ring, cnt, pol);
-      produce_phase(P2, ring, cnt, pol);
+      produce_phase(P0, ring, lane, c, pol);
+      produce_phase(P1, ring, lane, c, pol);
+      produce_phase(P2, ring, lane, c, pol);
     }
     __syncwarp();
     cluster_wait();
@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   // ---------------------------------------------------------------- consumers
-  T* xs = reinterpret_cast<T*>(smem + L.x);
+  float* xs = reinterpret_cast<float*>(smem + L.x);
   T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   float* kf = qf + B * Hp;
@@ -160,18 +160,15 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // 1. activations
   if (p.flags & 8) {
-    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
-    const char* src = static_cast<const char*>(p.x);
-    for (int v = tid; v < B * D * tb / 16; v += kConsumerThreads)
-      reinterpret_cast<uint4*>(xs)[v] = reinterpret_cast<const uint4*>(src)[v];
-    consumer_sync();
+    copy_to_smem<T, float>(xs, static_cast<const T*>(p.x), B * D, tid);
   }
 
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
   int cnt = 0;
   {
-    RowDot<T, QB> rd;
+    RowDot<T, float, QB> rd;
     consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
       rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
         if (lane == 0) {
@@ -554,7 +551,9 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->out || !a->out_partial ||
       !a->tickets)
     return set_error(CFB_ERR_ARGUMENT, "null weight / cache / workspace pointer");
-  const MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb);
+  int spw = kMaxSlotsPerWarp;
+  MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb, spw);
+  while (L.total > kMaxSmem && spw > 1) L = mha_layout(a->batch, a->hidden, Hp, N, tb, --spw);
   if (L.total > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "split_token schedule needs %d B of shared memory per CTA (max %d)",
                      L.total, kMaxSmem);
@@ -568,6 +567,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.S_static = a->seq_len;
   p.cache_cap = a->cache_cap;
   p.flags = a->flags;
+  p.spw = spw;
   p.sqrt_h = (float)std::sqrt((double)a->head_dim);
   p.eps = a->eps;
   p.x = a->x;

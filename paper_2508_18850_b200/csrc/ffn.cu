@@ -20,7 +20,7 @@
 namespace cfb {
 
 struct FfnParams {
-  int B, D, F, flags;
+  int B, D, F, flags, spw;
   float eps;
   const void* x;          // [B][D] T (no CFB_NORM)
   const float* resid;     // [B][D] fp32
@@ -38,13 +38,14 @@ struct FfnLayout {
   int bars, x, gu, act, red, total;
 };
 
-__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int tb) {
+__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int tb, int spw) {
   FfnLayout L;
   const int fmax = F / G + 1;
-  int o = kRingBytes;
+  const int xb = B * D * 4, ab = B * F * tb;  // fp32 x, T act
+  int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
   L.x = o;
-  L.act = o;   o += ((B * (D > F ? D : F) * tb + 15) & ~15);
+  L.act = o;   o += (((xb > ab) ? xb : ab) + 15) & ~15;
   L.gu = o;    o += (2 * B * fmax * 4 + 15) & ~15;
   L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
   L.total = o;
@@ -56,9 +57,9 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
   const int B = p.B, D = p.D, F = p.F, G = gridDim.x, i = blockIdx.x;
-  const FfnLayout L = ffn_layout(B, D, F, G, tb);
+  const FfnLayout L = ffn_layout(B, D, F, G, tb, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  const Ring ring{smem, bars, bars + kNumSlots};
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int f0 = (int)((long long)i * F / G), f1 = (int)((long long)(i + 1) * F / G);
   const int c0 = (int)((long long)i * D / G), c1 = (int)((long long)(i + 1) * D / G);
@@ -72,27 +73,27 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)c0 * F, nullptr, c1 - c0,
                               F * tb);
   if (warp == kNumConsumerWarps) {
-    if (lane == 0) {
-      int cnt[kNumConsumerWarps] = {};
+    if (lane < kNumConsumerWarps) {
+      int c = 0;
       const uint64_t pol = policy_evict_first();
-      produce_phase(P0, ring, cnt, pol);
-      produce_phase(P1, ring, cnt, pol);
+      produce_phase(P0, ring, lane, c, pol);
+      produce_phase(P1, ring, lane, c, pol);
     }
     return;
   }
-  T* xs = reinterpret_cast<T*>(smem + L.x);
+  float* xs = reinterpret_cast<float*>(smem + L.x);
   float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][2*(f1-f0)]
   T* acts = reinterpret_cast<T*>(smem + L.act);
   float* red = reinterpret_cast<float*>(smem + L.red);
   const int nloc = 2 * (f1 - f0);
 
   if (p.flags & CFB_NORM)
-    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   else
-    copy_to_smem<T>(xs, static_cast<const T*>(p.x), B * D, tid);
+    copy_to_smem<T, float>(xs, static_cast<const T*>(p.x), B * D, tid);
 
   int cnt = 0;
-  RowDot<T, QB> rd;
+  RowDot<T, float, QB> rd;
   consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
       if (lane == 0) {
@@ -111,10 +112,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
     act_g[(size_t)b * F + f0 + j] = Elem<T>::from_f(__fmul_rn(sl, u));
   }
   grid_barrier(p.barrier, tid);
-  copy_to_smem<T>(acts, act_g, B * F, tid);
+  copy_to_smem<T, T>(acts, act_g, B * F, tid);
 
+  RowDot<T, T, QB> rd1;
   consume_phase(P1, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-    rd.item(P1, it, slot, acts, F, B, lane, [&](int row, const float (&s)[QB]) {
+    rd1.item(P1, it, slot, acts, F, B, lane, [&](int row, const float (&s)[QB]) {
       if (lane == 0) {
         const int c = c0 + row;
 #pragma unroll
@@ -159,7 +161,9 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   int grid = a->grid > 0 ? a->grid : sms;
   grid = grid > sms ? sms : grid;  // grid barrier: every CTA must be co-resident
   if (grid > a->inter) grid = a->inter;
-  const FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb);
+  int spw = kMaxSlotsPerWarp;
+  FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, spw);
+  while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, --spw);
   if (L.total > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "ffn schedule needs %d B of shared memory (max %d)", L.total,
                      kMaxSmem);
@@ -168,6 +172,7 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.D = a->hidden;
   p.F = a->inter;
   p.flags = a->flags;
+  p.spw = spw;
   p.eps = a->eps;
   p.x = a->x;
   p.resid = a->resid;

@@ -15,7 +15,7 @@
 namespace cfb {
 
 struct LmParams {
-  int B, D, V, flags;
+  int B, D, V, flags, spw;
   float eps;
   const float* resid;
   const void* norm_w;
@@ -37,10 +37,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
   const int B = p.B, D = p.D, V = p.V, G = gridDim.x, i = blockIdx.x;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kRingBytes);
-  const Ring ring{smem, bars, bars + kNumSlots};
-  T* xs = reinterpret_cast<T*>(smem + kRingBytes + 2 * kNumSlots * 8);
-  float* red = reinterpret_cast<float*>(reinterpret_cast<char*>(xs) + ((B * D * tb + 15) & ~15));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(p.spw));
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
+  float* xs = reinterpret_cast<float*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
+  float* red = xs + B * D;
   float* wv = red + kNumConsumerWarps * B;
   int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
   unsigned& last = *reinterpret_cast<unsigned*>(wi + kNumConsumerWarps * B);
@@ -53,13 +53,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   __syncthreads();
   const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)v0 * D, nullptr, v1 - v0, D * tb);
   if (warp == kNumConsumerWarps) {
-    if (lane == 0) {
-      int cnt[kNumConsumerWarps] = {};
-      produce_phase(P0, ring, cnt, policy_evict_first());
+    if (lane < kNumConsumerWarps) {
+      int c = 0;
+      produce_phase(P0, ring, lane, c, policy_evict_first());
     }
     return;
   }
-  rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   float bv[QB];
   int bi[QB];
 #pragma unroll
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     bi[b] = 0x7fffffff;
   }
   int cnt = 0;
-  RowDot<T, QB> rd;
+  RowDot<T, float, QB> rd;
   consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
       const int v = v0 + row;
@@ -160,14 +160,20 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int grid = a->grid > 0 ? a->grid : sms;
   if (grid > a->vocab) grid = a->vocab;
-  const size_t smem = kRingBytes + 2 * kNumSlots * 8 + ((a->batch * a->hidden * tb + 15) & ~15) +
-                      3 * kNumConsumerWarps * a->batch * 4 + 16;
+  int spw = kMaxSlotsPerWarp;
+  auto need = [&](int s) {
+    return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)a->batch * a->hidden * 4 +
+           3 * kNumConsumerWarps * a->batch * 4 + 16;
+  };
+  while (need(spw) > (size_t)kMaxSmem && spw > 1) --spw;
+  const size_t smem = need(spw);
   if (smem > (size_t)kMaxSmem) return set_error(CFB_ERR_SMEM, "lm head needs too much smem");
   LmParams p;
   p.B = a->batch;
   p.D = a->hidden;
   p.V = a->vocab;
   p.flags = 0;
+  p.spw = spw;
   p.eps = a->eps;
   p.resid = a->resid;
   p.norm_w = a->norm_w;

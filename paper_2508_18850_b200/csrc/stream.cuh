@@ -3,8 +3,10 @@
 // One producer warp (warp kNumConsumerWarps) streams a CTA's whole schedule of
 // contiguous global rows into a ring of shared-memory slots with
 // cp.async.bulk (TMA bulk copies) completing on per-slot mbarriers.  Each
-// consumer warp owns kSlotsPerWarp private slots, so a slot is consumed by
-// exactly one warp and no CTA-wide barrier is needed to recycle it.
+// consumer warp owns `spw` private slots, so a slot is consumed by exactly
+// one warp and no CTA-wide barrier is needed to recycle it.  Producer lane w
+// feeds consumer warp w: the eight sub-rings refill independently (no
+// head-of-line blocking behind a slow warp) and eight threads issue copies.
 //
 // A schedule is a list of Phases.  Weights and the KV cache never depend on
 // the activations, so the producer runs ahead across phase boundaries (and
@@ -18,10 +20,10 @@ namespace cfb {
 constexpr int kNumConsumerWarps = 8;
 constexpr int kThreads = (kNumConsumerWarps + 1) * 32;
 constexpr int kConsumerThreads = kNumConsumerWarps * 32;
-constexpr int kSlotsPerWarp = 2;
-constexpr int kNumSlots = kNumConsumerWarps * kSlotsPerWarp;
+constexpr int kMaxSlotsPerWarp = 3;
+constexpr int kNumSlots = kNumConsumerWarps * kMaxSlotsPerWarp;  // barrier storage
 constexpr int kSlotBytes = 8192;
-constexpr int kRingBytes = kNumSlots * kSlotBytes;
+__host__ __device__ constexpr int ring_bytes(int spw) { return kNumConsumerWarps * spw * kSlotBytes; }
 constexpr uint32_t kConsumerBar = 1;  // named barrier id for consumer-only sync
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(kConsumerBar, kConsumerThreads); }
@@ -100,6 +102,7 @@ struct Ring {
   char* slots;
   uint64_t* full;
   uint64_t* empty;
+  int spw;  // slots per consumer warp
   __device__ __forceinline__ char* slot(int s) const { return slots + s * kSlotBytes; }
 };
 
@@ -110,24 +113,20 @@ __device__ __forceinline__ void ring_init(const Ring& r) {
   }
 }
 
-// Producer side: called by one elected thread; `cnt` = per-warp item counters.
-__device__ __forceinline__ void produce_phase(const Phase& p, const Ring& r,
-                                              int (&cnt)[kNumConsumerWarps], uint64_t policy) {
-  const int jmax = items_for_warp(p, 0);
-  for (int j = 0; j < jmax; ++j) {
-#pragma unroll
-    for (int w = 0; w < kNumConsumerWarps; ++w) {
-      if (j >= items_for_warp(p, w)) continue;
-      const Item it = item_of(p, w, j);
-      const int c = cnt[w]++;
-      const int s = w * kSlotsPerWarp + (c % kSlotsPerWarp);
-      const uint32_t par = (c / kSlotsPerWarp) & 1;
-      mbar_wait(&r.empty[s], par ^ 1);
-      const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
-      mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
-      bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
-      if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
-    }
+// Producer side: lane w of the producer warp feeds consumer warp w;
+// `cnt` = that warp's running item counter (continues across phases).
+__device__ __forceinline__ void produce_phase(const Phase& p, const Ring& r, int w, int& cnt,
+                                              uint64_t policy) {
+  const int n = items_for_warp(p, w);
+  for (int j = 0; j < n; ++j) {
+    const Item it = item_of(p, w, j);
+    const int c = cnt++;
+    const int s = w * r.spw + (c % r.spw);
+    mbar_wait(&r.empty[s], ((c / r.spw) & 1) ^ 1);
+    const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
+    mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
+    bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
+    if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
   }
 }
 
@@ -139,8 +138,8 @@ __device__ __forceinline__ void consume_phase(const Phase& p, const Ring& r, int
   for (int j = 0; j < n; ++j) {
     const Item it = item_of(p, w, j);
     const int c = cnt++;
-    const int s = w * kSlotsPerWarp + (c % kSlotsPerWarp);
-    mbar_wait(&r.full[s], (c / kSlotsPerWarp) & 1);
+    const int s = w * r.spw + (c % r.spw);
+    mbar_wait(&r.full[s], (c / r.spw) & 1);
     f(it, r.slot(s));
     __syncwarp();
     if (lane == 0) mbar_arrive(&r.empty[s]);
