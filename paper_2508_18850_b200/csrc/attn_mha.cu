@@ -126,13 +126,8 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
                               nullptr, cols, Hp * tb);
 
   if (warp == kNumConsumerWarps) {  // ------------------------------ producer
-    if (lane < kNumConsumerWarps) {
-      int c = 0;
-      const uint64_t pol = policy_evict_first();
-      produce_phase(P0, ring, lane, c, pol);
-      produce_phase(P1, ring, lane, c, pol);
-      produce_phase(P2, ring, lane, c, pol);
-    }
+    const Phase ph[3] = {P0, P1, P2};
+    produce_all(ph, ring, lane, policy_evict_first());
     __syncwarp();
     cluster_wait();
     cluster_arrive();

@@ -73,12 +73,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)c0 * F, nullptr, c1 - c0,
                               F * tb);
   if (warp == kNumConsumerWarps) {
-    if (lane < kNumConsumerWarps) {
-      int c = 0;
-      const uint64_t pol = policy_evict_first();
-      produce_phase(P0, ring, lane, c, pol);
-      produce_phase(P1, ring, lane, c, pol);
-    }
+    const Phase ph[2] = {P0, P1};
+    produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
   float* xs = reinterpret_cast<float*>(smem + L.x);

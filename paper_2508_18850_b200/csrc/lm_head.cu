@@ -53,10 +53,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   __syncthreads();
   const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)v0 * D, nullptr, v1 - v0, D * tb);
   if (warp == kNumConsumerWarps) {
-    if (lane < kNumConsumerWarps) {
-      int c = 0;
-      produce_phase(P0, ring, lane, c, policy_evict_first());
-    }
+    const Phase ph[1] = {P0};
+    produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
   rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);

@@ -113,20 +113,46 @@ __device__ __forceinline__ void ring_init(const Ring& r) {
   }
 }
 
-// Producer side: lane w of the producer warp feeds consumer warp w;
-// `cnt` = that warp's running item counter (continues across phases).
-__device__ __forceinline__ void produce_phase(const Phase& p, const Ring& r, int w, int& cnt,
-                                              uint64_t policy) {
-  const int n = items_for_warp(p, w);
-  for (int j = 0; j < n; ++j) {
-    const Item it = item_of(p, w, j);
-    const int c = cnt++;
-    const int s = w * r.spw + (c % r.spw);
-    mbar_wait(&r.empty[s], ((c / r.spw) & 1) ^ 1);
-    const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
-    mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
-    bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
-    if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
+__device__ __forceinline__ void issue_item(const Phase& p, const Item& it, const Ring& r, int s,
+                                           uint64_t policy) {
+  const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
+  mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
+  bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
+  if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
+}
+
+// Producer warp: lane w < kNumConsumerWarps feeds consumer warp w through
+// its sub-ring, walking the phases in order.  The loop is warp-uniform and
+// only probes slots with the non-blocking test_wait, so one lane waiting for
+// a busy slot never stalls the others (a blocking try_wait in divergent
+// lanes would serialise the warp).
+template <int NP>
+__device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r, int lane,
+                                            uint64_t policy) {
+  const int w = lane;
+  int ph = 0, j = 0, c = 0;
+  bool done = w >= kNumConsumerWarps;
+  while (true) {
+    bool issued = false;
+    if (!done) {
+      while (ph < NP && j >= items_for_warp(P[ph], w)) {
+        ++ph;
+        j = 0;
+      }
+      if (ph == NP) {
+        done = true;
+      } else {
+        const int s = w * r.spw + (c % r.spw);
+        if (mbar_test(&r.empty[s], ((c / r.spw) & 1) ^ 1)) {
+          issue_item(P[ph], item_of(P[ph], w, j), r, s, policy);
+          ++c;
+          ++j;
+          issued = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (!__any_sync(0xffffffffu, issued)) __nanosleep(32);
   }
 }
 
