@@ -1,5 +1,6 @@
 // extern "C" surface of libcfb.so (declared in include/cfb.h).
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.h"
@@ -13,6 +14,14 @@ int set_error(int code, const char* fmt, ...) {
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
   return code;
+}
+int tuned_spw() {
+  static int v = [] {
+    const char* e = getenv("CFB_SPW");
+    const int x = e ? atoi(e) : kMaxSlotsPerWarpHost;
+    return (x < 1 || x > kMaxSlotsPerWarpHost) ? kMaxSlotsPerWarpHost : x;
+  }();
+  return v;
 }
 }  // namespace cfb
 

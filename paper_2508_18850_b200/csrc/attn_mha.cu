@@ -546,7 +546,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->out || !a->out_partial ||
       !a->tickets)
     return set_error(CFB_ERR_ARGUMENT, "null weight / cache / workspace pointer");
-  int spw = kMaxSlotsPerWarp;
+  int spw = tuned_spw();
   MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb, spw);
   while (L.total > kMaxSmem && spw > 1) L = mha_layout(a->batch, a->hidden, Hp, N, tb, --spw);
   if (L.total > kMaxSmem)

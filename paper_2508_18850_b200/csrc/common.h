@@ -12,8 +12,12 @@
 namespace cfb {
 
 constexpr int kMaxSmem = 227 * 1024;
+constexpr int kMaxSlotsPerWarpHost = 3;  // == kMaxSlotsPerWarp (stream.cuh)
 
 int set_error(int code, const char* fmt, ...);
+
+// Ring depth (slots per consumer warp); CFB_SPW overrides it for tuning runs.
+int tuned_spw();
 
 #define CFB_CUDA(expr)                                                              \
   do {                                                                              \

@@ -157,7 +157,7 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   int grid = a->grid > 0 ? a->grid : sms;
   grid = grid > sms ? sms : grid;  // grid barrier: every CTA must be co-resident
   if (grid > a->inter) grid = a->inter;
-  int spw = kMaxSlotsPerWarp;
+  int spw = tuned_spw();
   FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, spw);
   while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, --spw);
   if (L.total > kMaxSmem)

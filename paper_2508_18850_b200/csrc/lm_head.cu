@@ -158,7 +158,7 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int grid = a->grid > 0 ? a->grid : sms;
   if (grid > a->vocab) grid = a->vocab;
-  int spw = kMaxSlotsPerWarp;
+  int spw = tuned_spw();
   auto need = [&](int s) {
     return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)a->batch * a->hidden * 4 +
            3 * kNumConsumerWarps * a->batch * 4 + 16;
