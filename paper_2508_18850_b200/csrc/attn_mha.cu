@@ -60,7 +60,7 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.st_bytes = round16(2 * B * tb);
   int o = ring_bytes(spw);
   L.bars = o;       o += (2 * kNumSlots + 16) * 8;
-  L.x = o;          o += round16(B * D * 4);  // fp32 activations
+  L.x = o;          o += round16(B * D * tb);
   L.gbuf = o;       o += N * L.seg_bytes;
   L.qf = o;         o += 3 * B * Hp * 4;
   L.ws_acc = o;     o += kNumConsumerWarps * B * Hp * 4;
@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   // ---------------------------------------------------------------- consumers
-  float* xs = reinterpret_cast<float*>(smem + L.x);
+  T* xs = reinterpret_cast<T*>(smem + L.x);
   T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   float* kf = qf + B * Hp;
@@ -155,15 +155,15 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // 1. activations
   if (p.flags & 8) {
-    rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
-    copy_to_smem<T, float>(xs, static_cast<const T*>(p.x), B * D, tid);
+    copy_to_smem<T, T>(xs, static_cast<const T*>(p.x), B * D, tid);
   }
 
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
   int cnt = 0;
   {
-    RowDot<T, float, QB> rd;
+    RowDot<T, T, QB> rd;
     consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
       rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
         if (lane == 0) {

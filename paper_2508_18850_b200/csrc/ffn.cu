@@ -41,7 +41,7 @@ struct FfnLayout {
 __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int tb, int spw) {
   FfnLayout L;
   const int fmax = F / G + 1;
-  const int xb = B * D * 4, ab = B * F * tb;  // fp32 x, T act
+  const int xb = B * D * tb, ab = B * F * tb;
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
   L.x = o;
@@ -77,19 +77,19 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
-  float* xs = reinterpret_cast<float*>(smem + L.x);
+  T* xs = reinterpret_cast<T*>(smem + L.x);
   float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][2*(f1-f0)]
   T* acts = reinterpret_cast<T*>(smem + L.act);
   float* red = reinterpret_cast<float*>(smem + L.red);
   const int nloc = 2 * (f1 - f0);
 
   if (p.flags & CFB_NORM)
-    rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   else
-    copy_to_smem<T, float>(xs, static_cast<const T*>(p.x), B * D, tid);
+    copy_to_smem<T, T>(xs, static_cast<const T*>(p.x), B * D, tid);
 
   int cnt = 0;
-  RowDot<T, float, QB> rd;
+  RowDot<T, T, QB> rd;
   consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
       if (lane == 0) {

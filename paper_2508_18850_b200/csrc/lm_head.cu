@@ -39,8 +39,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   const int B = p.B, D = p.D, V = p.V, G = gridDim.x, i = blockIdx.x;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(p.spw));
   const Ring ring{smem, bars, bars + kNumSlots, p.spw};
-  float* xs = reinterpret_cast<float*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
-  float* red = xs + B * D;
+  T* xs = reinterpret_cast<T*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
+  float* red = reinterpret_cast<float*>(reinterpret_cast<char*>(xs) + ((B * D * tb + 15) & ~15));
   float* wv = red + kNumConsumerWarps * B;
   int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
   unsigned& last = *reinterpret_cast<unsigned*>(wi + kNumConsumerWarps * B);
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
-  rmsnorm_to_smem<T, float>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   float bv[QB];
   int bi[QB];
 #pragma unroll
@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     bi[b] = 0x7fffffff;
   }
   int cnt = 0;
-  RowDot<T, float, QB> rd;
+  RowDot<T, T, QB> rd;
   consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
       const int v = v0 + row;
@@ -160,7 +160,7 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   if (grid > a->vocab) grid = a->vocab;
   int spw = tuned_spw();
   auto need = [&](int s) {
-    return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)a->batch * a->hidden * 4 +
+    return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)((a->batch * a->hidden * tb + 15) & ~15) +
            3 * kNumConsumerWarps * a->batch * 4 + 16;
   };
   while (need(spw) > (size_t)kMaxSmem && spw > 1) --spw;
