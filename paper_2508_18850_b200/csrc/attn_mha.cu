@@ -44,7 +44,7 @@ struct MhaParams {
 };
 
 struct MhaLayout {
-  int bars, x, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, total;
+  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, total;
   int seg_bytes, a_bytes, st_bytes;
 };
 
@@ -60,7 +60,8 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.st_bytes = round16(2 * B * tb);
   int o = ring_bytes(spw);
   L.bars = o;       o += (2 * kNumSlots + 16) * 8;
-  L.x = o;          o += round16(B * D * tb);
+  L.x = o;          o += round16(B * D * 4);  // fp32, tile-GEMV layout
+  L.part = o;       o += round16(kNumConsumerWarps * B * 3 * h * 4);
   L.gbuf = o;       o += N * L.seg_bytes;
   L.qf = o;         o += 3 * B * Hp * 4;
   L.ws_acc = o;     o += kNumConsumerWarps * B * Hp * 4;
@@ -115,8 +116,10 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   cluster_arrive();
 
   const size_t cache_head = (size_t)head * p.cache_cap * Hp;
-  const Phase P0 = make_phase(static_cast<const T*>(p.w_qkv) + ((size_t)head * N + rank) * 3 * h * D,
-                              nullptr, 3 * h, D * tb);
+  const int qkv_rows = 3 * h, qkv_tiles = (qkv_rows + kTileRows - 1) / kTileRows;
+  const Phase P0 = make_phase(static_cast<const T*>(p.w_qkv) +
+                                  ((size_t)head * N + rank) * qkv_tiles * kTileRows * D,
+                              nullptr, qkv_tiles, kTileRows * D * tb, true);
   const Phase P1 = make_phase(static_cast<const T*>(p.k_cache) + cache_head + (size_t)lo * Hp,
                               static_cast<const T*>(p.v_cache) + cache_head + (size_t)lo * Hp,
                               hi - lo, Hp * tb);
@@ -136,7 +139,8 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   // ---------------------------------------------------------------- consumers
-  T* xs = reinterpret_cast<T*>(smem + L.x);
+  float* xs = reinterpret_cast<float*>(smem + L.x);
+  float* part = reinterpret_cast<float*>(smem + L.part);
   T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
   float* qf = reinterpret_cast<float*>(smem + L.qf);
   float* kf = qf + B * Hp;
@@ -155,25 +159,15 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // 1. activations
   if (p.flags & 8) {
-    rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
-    copy_to_smem<T, T>(xs, static_cast<const T*>(p.x), B * D, tid);
+    load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
   }
 
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
   int cnt = 0;
-  {
-    RowDot<T, T, QB> rd;
-    consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-      rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
-        if (lane == 0) {
-#pragma unroll
-          for (int b = 0; b < QB; ++b)
-            if (b < B) gseg[b * 3 * h + row] = Elem<T>::from_f(s[b]);
-        }
-      });
-    });
-  }
+  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
+                          [&](int row, int b, float v) { gseg[b * 3 * h + row] = Elem<T>::from_f(v); });
   consumer_sync();
   cluster_wait();  // peers' mbarriers are initialised from here on
 
@@ -273,7 +267,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     const T* K = reinterpret_cast<const T*>(slot);
     const T* V = reinterpret_cast<const T*>(slot + kSlotBytes / 2);
     attend([&](int k, float* o) { load_elems<T, EPL>(K + k * Hp + li * EPL, o); },
-           [&](int k, float* o) { load_elems<T, EPL>(V + k * Hp + li * EPL, o); }, it.nrows);
+           [&](int k, float* o) { load_elems<T, EPL>(V + k * Hp + li * EPL, o); }, it.nunits);
   });
   if ((p.flags & 1) && rank == N - 1 && warp == 0) {  // new token(s): counted exactly once
     attend([&](int k, float* o) {
@@ -428,12 +422,12 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 #pragma unroll
     for (int e = 0; e < EPL; ++e) a[b][e] = (b < B) ? Elem<T>::to_f(abuf[b * Hp + li * EPL + e]) : 0.f;
   const int c_base = (int)rank * cols;
-  const int items_per_rank = (cols + P2.rows_per_item - 1) / P2.rows_per_item;
+  const int items_per_rank = (cols + P2.per_item - 1) / P2.per_item;
   consume_phase(P2, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     const T* W = reinterpret_cast<const T*>(slot);
-    for (int k0 = 0; k0 < it.nrows; k0 += KPP) {
+    for (int k0 = 0; k0 < it.nunits; k0 += KPP) {
       const int row = k0 + g;
-      const bool valid = row < it.nrows;
+      const bool valid = row < it.nunits;
       float w[EPL], s[QB];
       load_elems<T, EPL>(W + (valid ? row : 0) * Hp + li * EPL, w);
 #pragma unroll
@@ -450,20 +444,20 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
       if (valid && li == 0) {
 #pragma unroll
         for (int b = 0; b < QB; ++b)
-          if (b < B) p.out_partial[((size_t)head * B + b) * D + c_base + it.row0 + row] = s[b];
+          if (b < B) p.out_partial[((size_t)head * B + b) * D + c_base + it.unit0 + row] = s[b];
       }
     }
     __threadfence();
     __syncwarp();
     unsigned old = 0;
-    const int chunk = (int)rank * items_per_rank + it.row0 / P2.rows_per_item;
+    const int chunk = (int)rank * items_per_rank + it.unit0 / P2.per_item;
     if (lane == 0) old = atomicAdd(&p.tickets[chunk], 1u);
     old = __shfl_sync(0xffffffffu, old, 0);
     if (old == (unsigned)p.n_heads - 1) {  // last head for this chunk: sum heads in order
       __threadfence();
-      for (int idx = lane; idx < B * it.nrows; idx += 32) {
-        const int b = idx / it.nrows;
-        const int c = c_base + it.row0 + idx % it.nrows;
+      for (int idx = lane; idx < B * it.nunits; idx += 32) {
+        const int b = idx / it.nunits;
+        const int c = c_base + it.unit0 + idx % it.nunits;
         float s = 0.f;
         for (int hh = 0; hh < p.n_heads; ++hh) s += __ldcg(&p.out_partial[((size_t)hh * B + b) * D + c]);
         if (p.flags & 16) s = p.resid[(size_t)b * D + c] + s;
@@ -506,7 +500,7 @@ static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st) {
 template <typename T>
 static int launch_mha_t(const MhaParams& p, size_t smem, cudaStream_t st) {
   if (p.B > 4) return launch_mha_inst<T, 4, 16>(p, smem, st);
-  if (p.Hp == 8) {
+  if (p.Hp == 8) {  // EPL: attention elements per lane
     if (p.B == 1) return launch_mha_inst<T, 8, 1>(p, smem, st);
     if (p.B == 2) return launch_mha_inst<T, 8, 2>(p, smem, st);
     return launch_mha_inst<T, 8, 4>(p, smem, st);

@@ -6,12 +6,14 @@
 // The reference has no fused counterpart; this kernel is the
 // north-star "gate/up GEMV, SiLU*mul and down GEMV in one launch".
 //
-// Persistent grid of one CTA per SM.  CTA i owns intermediate rows
-// [i*F/G, (i+1)*F/G) (gate and up interleaved: packed row 2f = w1[f],
-// 2f+1 = w2[f]) and output rows [i*D/G, (i+1)*D/G) of w3.  The activation
-// vector crosses CTAs once, through global memory and a grid barrier; the
-// producer warp keeps streaming this CTA's w3 rows into the ring while the
-// barrier is pending, so HBM never idles at the phase boundary.
+// Persistent grid of one CTA per SM.  Weights are row-tiled (gemv.cuh):
+//   w_gu tile t = rows (w1[2t], w1[2t+1], w2[2t], w2[2t+1])   F/2 tiles of D
+//   w_dn tile u = rows 4u..4u+3 of w3                          D/4 tiles of F
+// CTA i owns gate/up tiles [i*T1/G, (i+1)*T1/G) and down tiles
+// [i*T2/G, (i+1)*T2/G).  The activation vector crosses CTAs once, through
+// global memory and a grid barrier; the producer warp keeps streaming this
+// CTA's w3 tiles into the ring while the barrier is pending, so HBM never
+// idles at the phase boundary.
 #include <cuda_runtime.h>
 
 #include "common.h"
@@ -25,28 +27,28 @@ struct FfnParams {
   const void* x;          // [B][D] T (no CFB_NORM)
   const float* resid;     // [B][D] fp32
   const void* norm_w;     // [D] T
-  const void* w_gu;       // [F][2][D] T
-  const void* w_dn;       // [D][F] T
+  const void* w_gu;       // row-tiled, F/2 tiles of D
+  const void* w_dn;       // row-tiled, D/4 tiles of F
   void* act;              // [B][F] T workspace
   float* out;             // [B][D] fp32
   unsigned long long* barrier;
 };
 
 // x (phase 0 input, B x D) and act (phase 1 input, B x F) are never live at
-// the same time and share one region.
+// the same time and share one fp32 region.
 struct FfnLayout {
-  int bars, x, gu, act, red, total;
+  int bars, x, gu, part, red, total;
 };
 
-__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int tb, int spw) {
+__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int spw) {
   FfnLayout L;
-  const int fmax = F / G + 1;
-  const int xb = B * D * tb, ab = B * F * tb;
+  const int t1 = (F / 2 + G - 1) / G, t2 = (D / 4 + G - 1) / G;  // max tiles per CTA
+  const int rows = 4 * (t1 > t2 ? t1 : t2);
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
-  L.x = o;
-  L.act = o;   o += (((xb > ab) ? xb : ab) + 15) & ~15;
-  L.gu = o;    o += (2 * B * fmax * 4 + 15) & ~15;
+  L.x = o;     o += ((B * (D > F ? D : F) * 4 + 15) & ~15);
+  L.gu = o;    o += ((B * 4 * t1 * 4 + 15) & ~15);
+  L.part = o;  o += ((kNumConsumerWarps * B * rows * 4 + 15) & ~15);
   L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
   L.total = o;
   return L;
@@ -57,73 +59,61 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
   const int B = p.B, D = p.D, F = p.F, G = gridDim.x, i = blockIdx.x;
-  const FfnLayout L = ffn_layout(B, D, F, G, tb, p.spw);
+  const FfnLayout L = ffn_layout(B, D, F, G, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int f0 = (int)((long long)i * F / G), f1 = (int)((long long)(i + 1) * F / G);
-  const int c0 = (int)((long long)i * D / G), c1 = (int)((long long)(i + 1) * D / G);
+  const int T1 = F / 2, T2 = D / 4;
+  const int a0 = (int)((long long)i * T1 / G), a1 = (int)((long long)(i + 1) * T1 / G);
+  const int u0 = (int)((long long)i * T2 / G), u1 = (int)((long long)(i + 1) * T2 / G);
   if (tid == 0) {
     ring_init(ring);
     fence_mbar_init();
   }
   __syncthreads();
-  const Phase P0 = make_phase(static_cast<const T*>(p.w_gu) + (size_t)2 * f0 * D, nullptr,
-                              2 * (f1 - f0), D * tb);
-  const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)c0 * F, nullptr, c1 - c0,
-                              F * tb);
+  const Phase P0 = make_phase(static_cast<const T*>(p.w_gu) + (size_t)a0 * 4 * D, nullptr, a1 - a0,
+                              4 * D * tb, true);
+  const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)u0 * 4 * F, nullptr, u1 - u0,
+                              4 * F * tb, true);
   if (warp == kNumConsumerWarps) {
     const Phase ph[2] = {P0, P1};
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
-  T* xs = reinterpret_cast<T*>(smem + L.x);
-  float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][2*(f1-f0)]
-  T* acts = reinterpret_cast<T*>(smem + L.act);
+  float* xs = reinterpret_cast<float*>(smem + L.x);
+  float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][4*(a1-a0)]
+  float* part = reinterpret_cast<float*>(smem + L.part);
   float* red = reinterpret_cast<float*>(smem + L.red);
-  const int nloc = 2 * (f1 - f0);
+  const int rows0 = 4 * (a1 - a0);
 
   if (p.flags & CFB_NORM)
-    rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   else
-    copy_to_smem<T, T>(xs, static_cast<const T*>(p.x), B * D, tid);
+    load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
 
   int cnt = 0;
-  RowDot<T, T, QB> rd;
-  consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-    rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
-      if (lane == 0) {
-#pragma unroll
-        for (int b = 0; b < QB; ++b)
-          if (b < B) gu[b * nloc + row] = s[b];
-      }
-    });
-  });
+  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows0, part,
+                          [&](int row, int b, float v) { gu[b * rows0 + row] = v; });
   consumer_sync();
   T* act_g = static_cast<T*>(p.act);
-  for (int idx = tid; idx < B * (f1 - f0); idx += kConsumerThreads) {
-    const int b = idx / (f1 - f0), j = idx % (f1 - f0);
-    const float g = gu[b * nloc + 2 * j], u = gu[b * nloc + 2 * j + 1];
+  const int nf = 2 * (a1 - a0);
+  for (int idx = tid; idx < B * nf; idx += kConsumerThreads) {
+    const int b = idx / nf, j = idx % nf;           // f = 2*a0 + j
+    const int t = j >> 1, e = j & 1;                // tile rows: g0 g1 u0 u1
+    const float g = gu[b * rows0 + 4 * t + e], u = gu[b * rows0 + 4 * t + 2 + e];
     const float sl = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    act_g[(size_t)b * F + f0 + j] = Elem<T>::from_f(__fmul_rn(sl, u));
+    act_g[(size_t)b * F + 2 * a0 + j] = Elem<T>::from_f(__fmul_rn(sl, u));
   }
   grid_barrier(p.barrier, tid);
-  copy_to_smem<T, T>(acts, act_g, B * F, tid);
+  load_act_to_smem<T>(xs, act_g, B, F, tid);
 
-  RowDot<T, T, QB> rd1;
-  consume_phase(P1, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-    rd1.item(P1, it, slot, acts, F, B, lane, [&](int row, const float (&s)[QB]) {
-      if (lane == 0) {
-        const int c = c0 + row;
-#pragma unroll
-        for (int b = 0; b < QB; ++b)
-          if (b < B) {
-            const float r = (p.flags & CFB_RESID) ? p.resid[(size_t)b * D + c] : 0.f;
-            p.out[(size_t)b * D + c] = (p.flags & CFB_RESID) ? __fadd_rn(r, s[b]) : s[b];
-          }
-      }
-    });
-  });
+  const int rows1 = 4 * (u1 - u0);
+  tiled_gemv_phase<T, QB>(P1, ring, warp, lane, tid, cnt, xs, F, B, rows1, part,
+                          [&](int row, int b, float v) {
+                            const int c = 4 * u0 + row;
+                            if (p.flags & CFB_RESID) v = __fadd_rn(p.resid[(size_t)b * D + c], v);
+                            p.out[(size_t)b * D + c] = v;
+                          });
 }
 
 template <typename T, int QB>
@@ -144,8 +134,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   const int tb = a->dtype;
   if (tb != CFB_F16 && tb != CFB_F32) return set_error(CFB_ERR_ARGUMENT, "bad dtype");
   if (a->batch < 1 || a->batch > 8) return set_error(CFB_ERR_DIMENSION, "ffn batch must be in [1, 8]");
-  if ((a->hidden * tb) % 16 || (a->inter * tb) % 16)
-    return set_error(CFB_ERR_DIMENSION, "hidden and inter must give 16-byte rows");
+  if (a->hidden % 8 || a->inter % 8)
+    return set_error(CFB_ERR_DIMENSION, "hidden and inter must be multiples of 8");
   if (!a->w_gu || !a->w_dn || !a->act || !a->out || !a->barrier)
     return set_error(CFB_ERR_ARGUMENT, "null weight / workspace pointer");
   if ((a->flags & CFB_NORM) ? (!a->resid || !a->norm_w) : !a->x)
@@ -156,10 +146,11 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int grid = a->grid > 0 ? a->grid : sms;
   grid = grid > sms ? sms : grid;  // grid barrier: every CTA must be co-resident
-  if (grid > a->inter) grid = a->inter;
+  if (grid > a->hidden / 4) grid = a->hidden / 4;
+  if (grid > a->inter / 2) grid = a->inter / 2;
   int spw = tuned_spw();
-  FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, spw);
-  while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, tb, --spw);
+  FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, spw);
+  while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, --spw);
   if (L.total > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "ffn schedule needs %d B of shared memory (max %d)", L.total,
                      kMaxSmem);

@@ -1,12 +1,25 @@
-// Row-GEMV consumer shared by the attention, FFN and LM-head kernels:
-// dot products of streamed weight rows (K-major, in a ring slot) with B
-// activation rows held in shared memory.  Lanes stride over 16-byte vectors
-// of a row; a row that spans several slot pieces keeps its partial sums in
-// registers until its last piece, then a warp butterfly finishes the sum.
+// Row-tiled GEMV consumer shared by the attention (QKV), FFN and LM-head kernels.
+//
+// Weight layout ("row tiles"): rows are grouped in tiles of 4 consecutive
+// rows stored chunk-major, [tile][chunk][4 rows][16 B], where a chunk is 16
+// bytes of one row (8 fp16 or 4 fp32 weights).  A warp covers 8 chunks x 4
+// rows per step: lane = 4*q + r reads chunk q+8k of row r, so the 32 lanes
+// read 512 contiguous bytes (conflict-free LDS.128) and only 8 distinct
+// activation chunks, which live in shared memory as fp32 in a lo/hi split
+// layout (8 consecutive chunks = 128 contiguous bytes: one wavefront, no
+// conversion).  Per 16-byte weight vector a lane issues one weight LDS, two
+// activation LDS, the fp16->fp32 unpack and four packed FFMA2s; no per-row
+// shuffles except a 3-step butterfly across the 8 chunk groups per tile.
+//
+// Activation layout for fp16 weights, row of C elements: element d at
+//   (d%8 < 4 ? 0 : C/2) + (d/8)*4 + d%4        (lo half | hi half)
+// and plain contiguous for fp32 weights.
 #pragma once
 #include "stream.cuh"
 
 namespace cfb {
+
+constexpr int kTileRows = 4;
 
 __device__ __forceinline__ float warp_allsum(float v) {
 #pragma unroll
@@ -27,87 +40,111 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
 __device__ __forceinline__ float f2_sum(unsigned long long v) {
   return __uint_as_float(static_cast<unsigned>(v)) + __uint_as_float(static_cast<unsigned>(v >> 32));
 }
-
-// Load 8 activations (elements [k, k+8) of an XT row in smem) as 4 fp32 pairs.
-template <typename XT>
-__device__ __forceinline__ void load_x8(const XT* x, unsigned long long (&xp)[4]) {
-  if constexpr (sizeof(XT) == 4) {
-    const uint4 a = lds128(x), b = lds128(x + 4);
-    xp[0] = (static_cast<unsigned long long>(a.y) << 32) | a.x;
-    xp[1] = (static_cast<unsigned long long>(a.w) << 32) | a.z;
-    xp[2] = (static_cast<unsigned long long>(b.y) << 32) | b.x;
-    xp[3] = (static_cast<unsigned long long>(b.w) << 32) | b.z;
-  } else {
-    float f[8];
-    Elem<XT>::unpack(lds128(x), f);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) xp[i] = f2_pack(f[2 * i], f[2 * i + 1]);
-  }
+__device__ __forceinline__ unsigned long long u2_lo(const uint4& v) {
+  return (static_cast<unsigned long long>(v.y) << 32) | v.x;
+}
+__device__ __forceinline__ unsigned long long u2_hi(const uint4& v) {
+  return (static_cast<unsigned long long>(v.w) << 32) | v.z;
 }
 
-// Weights T (fp16 or fp32) streamed in slots; activations XT (fp32 or T) in
-// smem rows of stride `xstride`.  Per 16-byte weight vector: one LDS.128,
-// the fp16->fp32 unpack, and packed FFMA2s into two interleaved partial sums.
-template <typename T, typename XT, int QB>
-struct RowDot {
-  unsigned long long acc[QB];
+// position of activation element d in the smem layout of a C-long row
+template <typename T>
+__device__ __forceinline__ int xpos(int d, int C) {
+  if constexpr (sizeof(T) == 2) return ((d & 7) < 4 ? 0 : C / 2) + (d >> 3) * 4 + (d & 3);
+  return d;
+}
 
-  // done(row_index, sums) runs on all lanes with warp-reduced sums[QB].
-  template <class Done>
-  __device__ __forceinline__ void item(const Phase& P, const Item& it, const char* slot,
-                                       const XT* xs, int xstride, int B, int lane, Done&& done) {
-    constexpr int epv = Elem<T>::kPerVec;
-    const int row_b = (P.pieces == 1) ? P.row_bytes : it.bytes;
-    const int col0 = it.byte0 / static_cast<int>(sizeof(T));
-    for (int rr = 0; rr < it.nrows; ++rr) {
-      const char* row = slot + rr * row_b;
-      if (it.piece == 0) {
+// One tiles-mode item: for every tile in the item, the lanes' partial dot
+// products of the tile's 4 rows (over the item's chunks) with B activation
+// rows, reduced across the 8 chunk groups.  emit(row, sums) runs on all
+// lanes; lanes 0..3 (chunk group 0) hold row (4*tile + lane)'s sums.
+template <typename T, int QB, class Emit>
+__device__ __forceinline__ void tile_item(const Phase& P, const Item& it, const char* slot,
+                                          const float* xs, int C, int B, int lane, Emit&& emit) {
+  const int q = lane >> 2, r = lane & 3;
+  const int nch = it.bytes / (it.nunits * 64);  // chunks per tile in this item
+  const int ch0 = it.byte0 / 64;
+  for (int t = 0; t < it.nunits; ++t) {
+    const char* tile = slot + t * nch * 64;
+    unsigned long long acc[QB];
 #pragma unroll
-        for (int b = 0; b < QB; ++b) acc[b] = 0ull;
-      }
-      const int nvec = row_b / 16;
+    for (int b = 0; b < QB; ++b) acc[b] = 0ull;
 #pragma unroll 4
-      for (int v = lane; v < nvec; v += 32) {
-        float w[epv];
-        Elem<T>::unpack(lds128(row + 16 * v), w);
+    for (int c = q; c < nch; c += 8) {
+      const uint4 wv = lds128(tile + (c * 4 + r) * 16);
+      const int gc = ch0 + c;
+      if constexpr (sizeof(T) == 2) {
+        const __half2* h = reinterpret_cast<const __half2*>(&wv);
+        const float2 w0 = __half22float2(h[0]), w1 = __half22float2(h[1]);
+        const float2 w2 = __half22float2(h[2]), w3 = __half22float2(h[3]);
 #pragma unroll
         for (int b = 0; b < QB; ++b) {
           if (b < B) {
-            const XT* xb = xs + (size_t)b * xstride + col0 + v * epv;
+            const float* xb = xs + (size_t)b * C;
+            const uint4 lo = lds128(xb + gc * 4), hi = lds128(xb + C / 2 + gc * 4);
+            acc[b] = ffma2(f2_pack(w0.x, w0.y), u2_lo(lo), acc[b]);
+            acc[b] = ffma2(f2_pack(w1.x, w1.y), u2_hi(lo), acc[b]);
+            acc[b] = ffma2(f2_pack(w2.x, w2.y), u2_lo(hi), acc[b]);
+            acc[b] = ffma2(f2_pack(w3.x, w3.y), u2_hi(hi), acc[b]);
+          }
+        }
+      } else {
 #pragma unroll
-            for (int h8 = 0; h8 < epv / 8 + (epv < 8 ? 1 : 0); ++h8) {
-              if constexpr (epv >= 8) {
-                unsigned long long xp[4];
-                load_x8<XT>(xb + 8 * h8, xp);
-#pragma unroll
-                for (int i = 0; i < 4; ++i)
-                  acc[b] = ffma2(f2_pack(w[8 * h8 + 2 * i], w[8 * h8 + 2 * i + 1]), xp[i], acc[b]);
-              } else {  // fp32 weights: 4 per vector
-                float xv[4];
-#pragma unroll
-                for (int i = 0; i < 4; ++i) xv[i] = Elem<XT>::to_f(xb[i]);
-                acc[b] = ffma2(f2_pack(w[0], w[1]), f2_pack(xv[0], xv[1]), acc[b]);
-                acc[b] = ffma2(f2_pack(w[2], w[3]), f2_pack(xv[2], xv[3]), acc[b]);
-              }
-            }
+        for (int b = 0; b < QB; ++b) {
+          if (b < B) {
+            const uint4 xv = lds128(xs + (size_t)b * C + gc * 4);
+            acc[b] = ffma2(u2_lo(wv), u2_lo(xv), acc[b]);
+            acc[b] = ffma2(u2_hi(wv), u2_hi(xv), acc[b]);
           }
         }
       }
-      if (it.piece == P.pieces - 1) {
-        float s[QB];
-#pragma unroll
-        for (int b = 0; b < QB; ++b) s[b] = (b < B) ? warp_allsum(f2_sum(acc[b])) : 0.f;
-        done(it.row0 + rr, s);
-      }
     }
+    float s[QB];
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      float v = f2_sum(acc[b]);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 16);
+      s[b] = v;
+    }
+    emit((it.unit0 + t) * kTileRows + r, s);
   }
-};
+}
 
-// x[b][d] = T((resid[b][d] * (1/sqrt(mean_d(resid^2) + eps))) * w[d]) for all
-// consumer threads, stored as XT (the fp16-rounded value, widened when XT is
-// float); `red` holds kNumConsumerWarps * B floats.
-template <typename T, typename XT>
-__device__ void rmsnorm_to_smem(XT* xs, const float* resid, const T* w, int B, int D, float eps,
+// Tiles-mode GEMV phase with a deterministic cross-warp reduction: every
+// warp adds its items' row partials into its private slice of `part`
+// ([kNumConsumerWarps][B][rows]); finish(row, b, value) then runs for each
+// (row < rows) with the warp slices summed in warp order.
+template <typename T, int QB, class Finish>
+__device__ __forceinline__ void tiled_gemv_phase(const Phase& P, const Ring& ring, int warp,
+                                                 int lane, int tid, int& cnt, const float* xs,
+                                                 int C, int B, int rows, float* part,
+                                                 Finish&& finish) {
+  for (int i = tid; i < kNumConsumerWarps * B * rows; i += kConsumerThreads) part[i] = 0.f;
+  consumer_sync();
+  float* mine = part + (size_t)warp * B * rows;
+  consume_phase(P, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+    tile_item<T, QB>(P, it, slot, xs, C, B, lane, [&](int row, const float (&s)[QB]) {
+      if (lane < kTileRows && row < rows) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b)
+          if (b < B) mine[b * rows + row] += s[b];
+      }
+    });
+  });
+  consumer_sync();
+  for (int i = tid; i < B * rows; i += kConsumerThreads) {
+    float v = 0.f;
+    for (int w = 0; w < kNumConsumerWarps; ++w) v += part[(size_t)w * B * rows + i];
+    finish(i % rows, i / rows, v);
+  }
+}
+
+// x[b][d] = T((resid[b][d] * (1/sqrt(mean_d(resid^2) + eps))) * w[d]) as fp32
+// in the tile-GEMV activation layout; `red` holds kNumConsumerWarps * B floats.
+template <typename T>
+__device__ void rmsnorm_to_smem(float* xs, const float* resid, const T* w, int B, int D, float eps,
                                 float* red, int tid) {
   const int warp = tid >> 5, lane = tid & 31;
   for (int b = 0; b < B; ++b) {
@@ -126,27 +163,29 @@ __device__ void rmsnorm_to_smem(XT* xs, const float* resid, const T* w, int B, i
     const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
     for (int d = tid; d < D; d += kConsumerThreads) {
       const float v = __fmul_rn(__fmul_rn(resid[(size_t)b * D + d], inv), Elem<T>::to_f(w[d]));
-      xs[(size_t)b * D + d] = static_cast<XT>(round_to<T>(v));
+      xs[(size_t)b * D + xpos<T>(d, D)] = round_to<T>(v);
     }
   }
   consumer_sync();
 }
 
-// Copy n T activations (16-byte aligned) from global into shared memory as XT.
-template <typename T, typename XT>
-__device__ __forceinline__ void copy_to_smem(XT* xs, const T* x, int n_elems, int tid) {
-  if constexpr (sizeof(T) == sizeof(XT)) {
-    const uint4* s = reinterpret_cast<const uint4*>(x);
-    uint4* d = reinterpret_cast<uint4*>(xs);
-    for (int v = tid; v < n_elems * (int)sizeof(T) / 16; v += kConsumerThreads) d[v] = __ldcg(s + v);
-  } else {
-    constexpr int epv = Elem<T>::kPerVec;
-    const uint4* s = reinterpret_cast<const uint4*>(x);
-    for (int v = tid; v < n_elems / epv; v += kConsumerThreads) {
-      float f[epv];
-      Elem<T>::unpack(__ldcg(s + v), f);
-#pragma unroll
-      for (int e = 0; e < epv; ++e) xs[v * epv + e] = f[e];
+// n_rows rows of C T-activations (16-byte aligned) from global memory into
+// the fp32 tile-GEMV layout.
+template <typename T>
+__device__ __forceinline__ void load_act_to_smem(float* xs, const T* x, int n_rows, int C, int tid) {
+  constexpr int epv = Elem<T>::kPerVec;
+  const uint4* s = reinterpret_cast<const uint4*>(x);
+  const int vpr = C / epv;
+  for (int v = tid; v < n_rows * vpr; v += kConsumerThreads) {
+    const int b = v / vpr, k = v % vpr;
+    float f[epv];
+    Elem<T>::unpack(__ldcg(s + v), f);
+    float* xb = xs + (size_t)b * C;
+    if constexpr (epv == 8) {
+      *reinterpret_cast<float4*>(xb + k * 4) = make_float4(f[0], f[1], f[2], f[3]);
+      *reinterpret_cast<float4*>(xb + C / 2 + k * 4) = make_float4(f[4], f[5], f[6], f[7]);
+    } else {
+      *reinterpret_cast<float4*>(xb + k * 4) = make_float4(f[0], f[1], f[2], f[3]);
     }
   }
   consumer_sync();

@@ -37,27 +37,32 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
   const int B = p.B, D = p.D, V = p.V, G = gridDim.x, i = blockIdx.x;
+  const int TV = (V + kTileRows - 1) / kTileRows;
+  const int t0 = (int)((long long)i * TV / G), t1 = (int)((long long)(i + 1) * TV / G);
+  const int rows = kTileRows * (t1 - t0);
+  const int rows_max = kTileRows * ((TV + G - 1) / G);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(p.spw));
   const Ring ring{smem, bars, bars + kNumSlots, p.spw};
-  T* xs = reinterpret_cast<T*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
-  float* red = reinterpret_cast<float*>(reinterpret_cast<char*>(xs) + ((B * D * tb + 15) & ~15));
+  float* xs = reinterpret_cast<float*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
+  float* part = xs + B * D;
+  float* red = part + kNumConsumerWarps * B * rows_max;
   float* wv = red + kNumConsumerWarps * B;
   int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
   unsigned& last = *reinterpret_cast<unsigned*>(wi + kNumConsumerWarps * B);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int v0 = (int)((long long)i * V / G), v1 = (int)((long long)(i + 1) * V / G);
   if (tid == 0) {
     ring_init(ring);
     fence_mbar_init();
   }
   __syncthreads();
-  const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)v0 * D, nullptr, v1 - v0, D * tb);
+  const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)t0 * kTileRows * D, nullptr,
+                              t1 - t0, kTileRows * D * tb, true);
   if (warp == kNumConsumerWarps) {
     const Phase ph[1] = {P0};
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
-  rmsnorm_to_smem<T, T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   float bv[QB];
   int bi[QB];
 #pragma unroll
@@ -66,26 +71,34 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     bi[b] = 0x7fffffff;
   }
   int cnt = 0;
-  RowDot<T, T, QB> rd;
-  consume_phase(P0, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-    rd.item(P0, it, slot, xs, D, B, lane, [&](int row, const float (&s)[QB]) {
-      const int v = v0 + row;
+  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows, part,
+                          [&](int row, int b, float s) {
+                            const int v = kTileRows * t0 + row;
+                            if (v >= V) return;
+                            if (p.logits) p.logits[(size_t)b * V + v] = s;
 #pragma unroll
-      for (int b = 0; b < QB; ++b)
-        if (b < B) {
-          if (lane == 0 && p.logits) p.logits[(size_t)b * V + v] = s[b];
-          if (better(s[b], v, bv[b], bi[b])) {
-            bv[b] = s[b];
-            bi[b] = v;
-          }
-        }
-    });
-  });
-  if (lane == 0)
-    for (int b = 0; b < B; ++b) {
-      wv[warp * B + b] = bv[b < QB ? b : 0];
-      wi[warp * B + b] = bi[b < QB ? b : 0];
+                            for (int bb = 0; bb < QB; ++bb)
+                              if (bb == b && better(s, v, bv[bb], bi[bb])) {
+                                bv[bb] = s;
+                                bi[bb] = v;
+                              }
+                          });
+  // per-thread best -> warp best -> CTA candidate
+#pragma unroll
+  for (int b = 0; b < QB; ++b) {
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, bv[b], o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi[b], o);
+      if (better(ov, oi, bv[b], bi[b])) {
+        bv[b] = ov;
+        bi[b] = oi;
+      }
     }
+    if (lane == 0 && b < B) {
+      wv[warp * B + b] = bv[b];
+      wi[warp * B + b] = bi[b];
+    }
+  }
   consumer_sync();
   if (tid < B) {
     float v = -INFINITY;
@@ -150,18 +163,21 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   const int tb = a->dtype;
   if (tb != CFB_F16 && tb != CFB_F32) return set_error(CFB_ERR_ARGUMENT, "bad dtype");
   if (a->batch < 1 || a->batch > 8) return set_error(CFB_ERR_DIMENSION, "lm batch must be in [1, 8]");
-  if ((a->hidden * tb) % 16) return set_error(CFB_ERR_DIMENSION, "hidden must give 16-byte rows");
+  if (a->hidden % 8) return set_error(CFB_ERR_DIMENSION, "hidden must be a multiple of 8");
   if (!a->resid || !a->norm_w || !a->w || !a->cand_val || !a->cand_idx || !a->ticket || !a->token_out)
     return set_error(CFB_ERR_ARGUMENT, "null pointer");
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int grid = a->grid > 0 ? a->grid : sms;
-  if (grid > a->vocab) grid = a->vocab;
+  if (grid > a->vocab / kTileRows) grid = a->vocab / kTileRows;
+  if (grid < 1) grid = 1;
   int spw = tuned_spw();
+  const int TV = (a->vocab + kTileRows - 1) / kTileRows;
+  const int rows_max = kTileRows * ((TV + grid - 1) / grid);
   auto need = [&](int s) {
-    return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)((a->batch * a->hidden * tb + 15) & ~15) +
-           3 * kNumConsumerWarps * a->batch * 4 + 16;
+    return (size_t)ring_bytes(s) + 2 * kNumSlots * 8 + (size_t)a->batch * a->hidden * 4 +
+           (size_t)kNumConsumerWarps * a->batch * rows_max * 4 + 3 * kNumConsumerWarps * a->batch * 4 + 16;
   };
   while (need(spw) > (size_t)kMaxSmem && spw > 1) --spw;
   const size_t smem = need(spw);

@@ -28,72 +28,76 @@ constexpr uint32_t kConsumerBar = 1;  // named barrier id for consumer-only sync
 
 __device__ __forceinline__ void consumer_sync() { named_bar_sync(kConsumerBar, kConsumerThreads); }
 
-// `n_rows` rows of `row_bytes` each, contiguous from src0.  When src1 is set
-// ("paired"), item k carries the same rows of src0 and src1 in the two halves
-// of a slot (K and V cache rows).  Rows that do not fit a slot are split into
-// pieces that all go to the same consumer warp, in order.
+// A phase streams `n_units` contiguous units of `unit_bytes` each from src0.
+//   rows mode  (tiles == false): a unit is one K-major row (KV-cache rows,
+//              W_out^T rows); paired phases carry the same rows of src0 and
+//              src1 in the two halves of a slot (K and V).
+//   tiles mode (tiles == true):  a unit is a 4-row tile of a row-tiled weight
+//              matrix, [chunk][4 rows][16 B] (see gemv.cuh); a tile larger
+//              than a slot is split into column pieces.
+// Items (<= one slot) are dealt round-robin: item i goes to consumer warp i % 8.
 struct Phase {
   const char* src0;
   const char* src1;
-  int n_rows;
-  int row_bytes;
-  int rows_per_item;
-  int pieces;
+  int n_units;
+  int unit_bytes;
+  int per_item;     // units per item (pieces == 1)
+  int pieces;       // pieces per unit (> 1 only in tiles mode)
   int piece_bytes;
+  int n_items;
+  bool tiles;
 };
 
-__device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, int n_rows,
-                                            int row_bytes) {
+__device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, int n_units,
+                                            int unit_bytes, bool tiles = false) {
   Phase p;
   p.src0 = static_cast<const char*>(src0);
   p.src1 = static_cast<const char*>(src1);
-  p.n_rows = n_rows < 0 ? 0 : n_rows;
-  p.row_bytes = row_bytes;
+  p.n_units = n_units < 0 ? 0 : n_units;
+  p.unit_bytes = unit_bytes;
+  p.tiles = tiles;
   const int cap = src1 ? kSlotBytes / 2 : kSlotBytes;
-  if (row_bytes <= cap) {
-    p.rows_per_item = cap / row_bytes;
+  if (unit_bytes <= cap) {
+    p.per_item = cap / unit_bytes;
     p.pieces = 1;
-    p.piece_bytes = row_bytes;
-  } else {  // paired phases never need pieces (row <= 4 KB checked on host)
-    p.rows_per_item = 1;
-    p.pieces = (row_bytes + cap - 1) / cap;
+    p.piece_bytes = unit_bytes;
+    p.n_items = (p.n_units + p.per_item - 1) / p.per_item;
+  } else {  // tiles mode only (checked on the host)
+    p.per_item = 1;
+    p.pieces = (unit_bytes + cap - 1) / cap;
     p.piece_bytes = cap;
+    p.n_items = p.n_units * p.pieces;
   }
   return p;
 }
 
 struct Item {
-  int row0;     // first row
-  int nrows;    // rows in this item (1 for pieces)
-  int piece;    // piece index within the row
-  int byte0;    // byte offset of the piece within its row
-  int bytes;    // bytes per source
+  int unit0;   // first unit (row or tile)
+  int nunits;  // units in this item (1 for pieces)
+  int piece;   // piece index within the unit
+  int byte0;   // byte offset of the piece within its unit
+  int bytes;   // bytes per source
 };
 
 __device__ __forceinline__ int items_for_warp(const Phase& p, int w) {
-  if (p.pieces == 1) {
-    const int n_items = (p.n_rows + p.rows_per_item - 1) / p.rows_per_item;
-    return n_items > w ? (n_items - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
-  }
-  const int rows_w = p.n_rows > w ? (p.n_rows - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
-  return rows_w * p.pieces;
+  return p.n_items > w ? (p.n_items - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
 }
 
 __device__ __forceinline__ Item item_of(const Phase& p, int w, int j) {
+  const int i = j * kNumConsumerWarps + w;
   Item it;
   if (p.pieces == 1) {
-    const int i = j * kNumConsumerWarps + w;
-    it.row0 = i * p.rows_per_item;
-    it.nrows = min(p.rows_per_item, p.n_rows - it.row0);
+    it.unit0 = i * p.per_item;
+    it.nunits = min(p.per_item, p.n_units - it.unit0);
     it.piece = 0;
     it.byte0 = 0;
-    it.bytes = it.nrows * p.row_bytes;
+    it.bytes = it.nunits * p.unit_bytes;
   } else {
-    it.row0 = (j / p.pieces) * kNumConsumerWarps + w;
-    it.nrows = 1;
-    it.piece = j % p.pieces;
+    it.unit0 = i / p.pieces;
+    it.nunits = 1;
+    it.piece = i % p.pieces;
     it.byte0 = it.piece * p.piece_bytes;
-    it.bytes = min(p.piece_bytes, p.row_bytes - it.byte0);
+    it.bytes = min(p.piece_bytes, p.unit_bytes - it.byte0);
   }
   return it;
 }
@@ -115,7 +119,7 @@ __device__ __forceinline__ void ring_init(const Ring& r) {
 
 __device__ __forceinline__ void issue_item(const Phase& p, const Item& it, const Ring& r, int s,
                                            uint64_t policy) {
-  const size_t off = static_cast<size_t>(it.row0) * p.row_bytes + it.byte0;
+  const size_t off = static_cast<size_t>(it.unit0) * p.unit_bytes + it.byte0;
   mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
   bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
   if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);

@@ -24,6 +24,7 @@ import numpy as np
 from . import _native
 from .exceptions import DimensionError, SimulationError
 from .ledger import GLOBAL, StageTrace, TrafficLedger, emit_gather, emit_reduce
+from .layouts import gate_up_tiles, qkv_tiles, row_tiles
 from .scenario import MHA, MLA, validate_scenario
 
 SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD = "split_token", "fused_mla", "split_head"
@@ -126,11 +127,8 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
     with torch.no_grad():
         x = torch.zeros(B, Dp, device=dev, dtype=dt)
         x[:, :D] = up(scenario.hidden).to(dt)
-        # w_qkv (nh, D, 3H) -> rows [head][rank][q|k|v slice][D']
-        w = up(scenario.w_qkv).reshape(nh, D, 3, H).permute(0, 2, 3, 1)  # (nh, 3, H, D)
-        wp = torch.zeros(nh, 3, Hp, Dp, device=dev, dtype=dt)
-        wp[:, :, :H, :D] = w.to(dt)
-        w_qkv = wp.reshape(nh, 3, n, hp, Dp).permute(0, 2, 1, 3, 4).contiguous()
+        # w_qkv (nh, D, 3H) -> row tiles [head][rank][q|k|v slice][D']
+        w_qkv = qkv_tiles(up(scenario.w_qkv).to(dt), n, Hp, Dp)
         wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
         wo[:, :D, :H] = up(scenario.w_out).transpose(1, 2).to(dt)
         cap = max(S, 1)
@@ -256,8 +254,10 @@ def run_fused_ffn(z, w1, w2, w3, activation: str = "silu", dtype_bytes: int = 2,
     g = up(norm_w) if norm_w is not None else None
     if resid is not None:
         flags |= _native.NORM | _native.RESID
-    w_gu = torch.stack([up(w1), up(w2)], 1).contiguous()
-    w_dn = up(w3)
+    if F % 2 or D % 4:
+        raise DimensionError("fused FFN needs an even intermediate size and hidden % 4 == 0")
+    w_gu = gate_up_tiles(up(w1), up(w2))
+    w_dn = row_tiles(up(w3))
     act = torch.empty(B, F, device=dev, dtype=dt)
     out = torch.empty(B, D, device=dev, dtype=torch.float32)
     bar = torch.zeros(1, device=dev, dtype=torch.int64)
@@ -279,6 +279,7 @@ def lm_head_argmax(resid, norm_w, w_lm, eps: float = 1e-5, dtype_bytes: int = 2)
     B, D = r.shape
     w = torch.from_numpy(np.ascontiguousarray(w_lm, np.float32)).to(dev).to(dt)
     V = w.shape[0]
+    w = row_tiles(w)
     g = torch.from_numpy(np.ascontiguousarray(norm_w, np.float32)).to(dev).to(dt)
     logits = torch.empty(B, V, device=dev, dtype=torch.float32)
     cv = torch.empty(1024 * B, device=dev, dtype=torch.float32)

@@ -1,0 +1,51 @@
+"""HBM weight layouts of the cfb kernels (torch, on device; see include/cfb.h).
+
+Row tiles (csrc/gemv.cuh): rows grouped 4 at a time and stored chunk-major,
+[tile][16-byte chunk][4 rows][chunk elements], so a warp's weight load is 512
+contiguous bytes and the streaming unit is a contiguous byte range.
+"""
+
+from __future__ import annotations
+
+TILE_ROWS = 4
+
+
+def _epc(t) -> int:
+    """elements per 16-byte chunk"""
+    return 16 // t.element_size()
+
+
+def row_tiles(w, rows_pad: int | None = None):
+    """(..., R, C) -> (..., R_pad/4, C/epc, 4, epc), zero rows appended."""
+    import torch
+    *lead, R, C = w.shape
+    rp = rows_pad if rows_pad is not None else -(-R // TILE_ROWS) * TILE_ROWS
+    if rp != R:
+        pad = torch.zeros(*lead, rp - R, C, device=w.device, dtype=w.dtype)
+        w = torch.cat([w, pad], dim=-2)
+    e = _epc(w)
+    return w.reshape(*lead, rp // TILE_ROWS, TILE_ROWS, C // e, e).transpose(-3, -2).contiguous()
+
+
+def gate_up_tiles(w1, w2):
+    """w1, w2 (F, D) -> tiles of rows (w1[2t], w1[2t+1], w2[2t], w2[2t+1])."""
+    import torch
+    F, D = w1.shape
+    inter = torch.cat([w1.reshape(F // 2, 2, D), w2.reshape(F // 2, 2, D)], dim=1)  # (F/2, 4, D)
+    e = _epc(w1)
+    return inter.reshape(F // 2, TILE_ROWS, D // e, e).transpose(1, 2).contiguous()
+
+
+def qkv_tiles(w_qkv, n_blocks: int, head_pad: int, hidden_pad: int):
+    """(nh, D, 3H) -> [nh][N][tiles of rows (q slice | k slice | v slice) of
+    head_pad/N dims each][D']: rank r's rows are q[r*h:(r+1)*h], k[...], v[...]."""
+    import torch
+    nh, D, threeH = w_qkv.shape
+    H = threeH // 3
+    hp = head_pad // n_blocks
+    w = w_qkv.reshape(nh, D, 3, H).permute(0, 2, 3, 1)  # (nh, 3, H, D)
+    wp = torch.zeros(nh, 3, head_pad, hidden_pad, device=w.device, dtype=w.dtype)
+    wp[:, :, :H, :D] = w
+    rows = wp.reshape(nh, 3, n_blocks, hp, hidden_pad).permute(0, 2, 1, 3, 4)  # (nh, N, 3, h, D')
+    rows = rows.reshape(nh, n_blocks, 3 * hp, hidden_pad)
+    return row_tiles(rows)

@@ -22,6 +22,7 @@ import numpy as np
 
 from . import _native
 from .exceptions import DimensionError
+from .layouts import gate_up_tiles, qkv_tiles, row_tiles
 
 
 @dataclass(frozen=True)
@@ -140,10 +141,9 @@ class LlamaDecoder:
         def t(a):
             return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).half()
 
-        w = t(lp["w_qkv"]).reshape(nh, D, 3, N, H // N)          # (nh, D, 3, N, h)
-        w_qkv = w.permute(0, 3, 2, 4, 1).contiguous()             # (nh, N, 3, h, D)
+        w_qkv = qkv_tiles(t(lp["w_qkv"]), N, H, D)               # row tiles per (head, rank)
         w_out = t(lp["w_out"]).transpose(1, 2).contiguous()       # (nh, D, H)
-        w_gu = torch.stack([t(lp["w1"]), t(lp["w2"])], 1).contiguous()  # (F, 2, D)
+        w_gu = gate_up_tiles(t(lp["w1"]), t(lp["w2"]))            # row tiles (g g u u)
         kc = torch.zeros(nh, self.cache_cap, H, device=dev, dtype=torch.float16)
         vc = torch.zeros_like(kc)
         S0 = lp["k_cache"].shape[1]
@@ -151,7 +151,7 @@ class LlamaDecoder:
             kc[:, :S0] = t(lp["k_cache"])
             vc[:, :S0] = t(lp["v_cache"])
         return dict(attn_norm=t(lp["attn_norm"]), w_qkv=w_qkv, w_out=w_out,
-                    ffn_norm=t(lp["ffn_norm"]), w_gu=w_gu, w_dn=t(lp["w3"]), k_cache=kc,
+                    ffn_norm=t(lp["ffn_norm"]), w_gu=w_gu, w_dn=row_tiles(t(lp["w3"])), k_cache=kc,
                     v_cache=vc)
 
     @classmethod
@@ -163,8 +163,8 @@ class LlamaDecoder:
         def t(a):
             return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(m.dev).half()
 
-        m.embed, m.final_norm, m.lm_head = t(params["embed"]), t(params["final_norm"]), t(
-            params["lm_head"])
+        m.embed, m.final_norm = t(params["embed"]), t(params["final_norm"])
+        m.lm_head = row_tiles(t(params["lm_head"]))
         m._finish()
         return m
 
@@ -185,13 +185,14 @@ class LlamaDecoder:
 
         for _ in range(cfg.n_layers):
             m.layers.append(dict(
-                attn_norm=rnd((D,), 0.1, 1.0), w_qkv=rnd((nh, N, 3, H // N, D), D ** -0.5),
+                attn_norm=rnd((D,), 0.1, 1.0),
+                w_qkv=rnd((nh, N, 3 * H // N // 4, D // 8, 4, 8), D ** -0.5),
                 w_out=rnd((nh, D, H), H ** -0.5), ffn_norm=rnd((D,), 0.1, 1.0),
-                w_gu=rnd((F, 2, D), D ** -0.5), w_dn=rnd((D, F), F ** -0.5),
+                w_gu=rnd((F // 2, D // 8, 4, 8), D ** -0.5), w_dn=rnd((D // 4, F // 8, 4, 8), F ** -0.5),
                 k_cache=rnd((nh, cache_cap, H), 1.0), v_cache=rnd((nh, cache_cap, H), 1.0)))
         m.embed = rnd((cfg.vocab, D), 1.0)
         m.final_norm = rnd((D,), 0.1, 1.0)
-        m.lm_head = rnd((cfg.vocab, D), D ** -0.5)
+        m.lm_head = rnd((cfg.vocab // 4, D // 8, 4, 8), D ** -0.5)
         m._finish()
         return m
 
