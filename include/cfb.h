@@ -105,6 +105,7 @@ typedef struct cfb_mha_args {
   unsigned* tickets;
   float* stats;
   unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
+  unsigned long long* trace;   /* [grid CTAs][8] %globaltimer phase stamps (profiling), or NULL */
 } cfb_mha_args;
 
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);
@@ -129,6 +130,7 @@ typedef struct cfb_ffn_args {
   void* act;
   float* out;
   unsigned long long* barrier;
+  unsigned long long* trace;   /* [grid CTAs][8] %globaltimer phase stamps (profiling), or NULL */
 } cfb_ffn_args;
 int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
 

@@ -36,7 +36,7 @@ class MhaArgs(ctypes.Structure):
         ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("eps", ctypes.c_float),
         ("w_qkv", _vp), ("w_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
         ("rope_cs", _vp), ("step_pos", _vp), ("out", _vp), ("out_partial", _vp),
-        ("tickets", _vp), ("stats", _vp), ("traffic", _vp),
+        ("tickets", _vp), ("stats", _vp), ("traffic", _vp), ("trace", _vp),
     ]
 
 
@@ -100,7 +100,7 @@ class FfnArgs(ctypes.Structure):
 
     _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "inter", "flags", "grid")] + [
         ("eps", ctypes.c_float), ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("w_gu", _vp),
-        ("w_dn", _vp), ("act", _vp), ("out", _vp), ("barrier", _vp)]
+        ("w_dn", _vp), ("act", _vp), ("out", _vp), ("barrier", _vp), ("trace", _vp)]
 
 
 class LmArgs(ctypes.Structure):

@@ -41,6 +41,7 @@ struct MhaParams {
   unsigned* tickets;
   float* stats;
   unsigned long long* traffic;
+  unsigned long long* trace;
 };
 
 struct MhaLayout {
@@ -139,6 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   // ---------------------------------------------------------------- consumers
+  unsigned long long* tr =
+      p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 : nullptr;
+  if (tr && tid == 0) tr[0] = globaltimer();
   float* xs = reinterpret_cast<float*>(smem + L.x);
   float* part = reinterpret_cast<float*>(smem + L.part);
   T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
@@ -165,10 +169,12 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
+  if (tr && tid == 0) tr[1] = globaltimer();
   int cnt = 0;
   tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
                           [&](int row, int b, float v) { gseg[b * 3 * h + row] = Elem<T>::from_f(v); });
   consumer_sync();
+  if (tr && tid == 0) tr[2] = globaltimer();
   cluster_wait();  // peers' mbarriers are initialised from here on
 
   // 3. ClusterGather of the qkv slices
@@ -213,6 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     }
   }
 
+  if (tr && tid == 0) tr[3] = globaltimer();
   // 4. split-KV flash decoding over this rank's segment (online softmax per warp)
   const int LPK = Hp / EPL, KPP = 32 / LPK, g = lane / LPK, li = lane % LPK;
   float q[QB][EPL], acc[QB][EPL], m[QB], l[QB];
@@ -324,6 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
     abuf[idx] = Elem<T>::from_f(0.f);
 
+  if (tr && tid == 0) tr[4] = globaltimer();
   // 5. softmax statistics
   T* st0 = reinterpret_cast<T*>(smem + L.st);
   T* st1 = reinterpret_cast<T*>(smem + L.st + L.st_bytes);
@@ -415,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
   consumer_sync();
 
+  if (tr && tid == 0) tr[5] = globaltimer();
   // 7. O-projection over this rank's output columns + 8. cross-head sum
   float a[QB][EPL];
 #pragma unroll
@@ -466,8 +475,10 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
       if (lane == 0) p.tickets[chunk] = 0;  // re-arm for the next launch
     }
   });
+  if (tr && tid == 0) tr[6] = globaltimer();
   cluster_arrive();
   cluster_wait();
+  if (tr && tid == 0) tr[7] = globaltimer();
 }
 
 // ---------------------------------------------------------------- host side
@@ -573,6 +584,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.tickets = a->tickets;
   p.stats = a->stats;
   p.traffic = a->traffic;
+  p.trace = a->trace;
   return tb == 2 ? launch_mha_t<__half>(p, L.total, st) : launch_mha_t<float>(p, L.total, st);
 }
 

@@ -32,6 +32,7 @@ struct FfnParams {
   void* act;              // [B][F] T workspace
   float* out;             // [B][D] fp32
   unsigned long long* barrier;
+  unsigned long long* trace;
 };
 
 // x (phase 0 input, B x D) and act (phase 1 input, B x F) are never live at
@@ -80,6 +81,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
+  unsigned long long* tr = p.trace ? p.trace + (size_t)i * 8 : nullptr;
+  if (tr && tid == 0) tr[0] = globaltimer();
   float* xs = reinterpret_cast<float*>(smem + L.x);
   float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][4*(a1-a0)]
   float* part = reinterpret_cast<float*>(smem + L.part);
@@ -91,6 +94,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   else
     load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
 
+  if (tr && tid == 0) tr[1] = globaltimer();
   int cnt = 0;
   tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows0, part,
                           [&](int row, int b, float v) { gu[b * rows0 + row] = v; });
@@ -104,8 +108,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
     const float sl = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
     act_g[(size_t)b * F + 2 * a0 + j] = Elem<T>::from_f(__fmul_rn(sl, u));
   }
+  if (tr && tid == 0) tr[2] = globaltimer();
   grid_barrier(p.barrier, tid);
+  if (tr && tid == 0) tr[3] = globaltimer();
   load_act_to_smem<T>(xs, act_g, B, F, tid);
+  if (tr && tid == 0) tr[4] = globaltimer();
 
   const int rows1 = 4 * (u1 - u0);
   tiled_gemv_phase<T, QB>(P1, ring, warp, lane, tid, cnt, xs, F, B, rows1, part,
@@ -114,6 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
                             if (p.flags & CFB_RESID) v = __fadd_rn(p.resid[(size_t)b * D + c], v);
                             p.out[(size_t)b * D + c] = v;
                           });
+  if (tr && tid == 0) tr[5] = globaltimer();
 }
 
 template <typename T, int QB>
@@ -169,6 +177,7 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.act = a->act;
   p.out = a->out;
   p.barrier = a->barrier;
+  p.trace = a->trace;
   const size_t smem = L.total;
   if (tb == 2) {
     if (p.B == 1) return launch_ffn_inst<__half, 1>(p, grid, smem, st);

@@ -124,6 +124,12 @@ __device__ __forceinline__ int ld_acquire_s32(const int* p) {
   return v;
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 // Programmatic dependent launch (PDL) controls; no-ops when the launch
 // did not opt in.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

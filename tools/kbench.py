@@ -80,3 +80,25 @@ res = {
                   (D * 3 * nh * H + nh * H * D) * 2 + 2 * nh * H * 2 * a.ctx),
 }
 print(json.dumps(res))
+
+# ---- per-CTA phase timeline (globaltimer stamps, ns) of one launch each
+if "--trace" in sys.argv or True:
+    import numpy as np
+    tr = torch.zeros(256 * 8, device=dev, dtype=torch.int64)
+    fa = ffn(layers[0]); fa.trace = tr.data_ptr()
+    _native.check(L.cfb_ffn_decode(fa, sp)); torch.cuda.synchronize()
+    t = tr.view(256, 8).cpu().numpy()[:148, :6].astype(np.float64)
+    t0 = t[:, 0].min()
+    names = ["start", "norm", "gateup", "barrier", "actload", "down"]
+    print("ffn timeline us (min/median/max per stamp):",
+          {n: (round((t[:, k].min() - t0) / 1e3, 2), round((np.median(t[:, k]) - t0) / 1e3, 2),
+               round((t[:, k].max() - t0) / 1e3, 2)) for k, n in enumerate(names)})
+    tr.zero_()
+    ma = mha(layers[0]); ma.trace = tr.data_ptr()
+    _native.check(L.cfb_mha_decode(ma, sp)); torch.cuda.synchronize()
+    t = tr.view(256, 8).cpu().numpy()[:nh * N].astype(np.float64)
+    t0 = t[:, 0].min()
+    names = ["start", "norm", "qkv", "gather", "attn", "stats", "oproj", "end"]
+    print("mha timeline us (min/median/max per stamp):",
+          {n: (round((t[:, k].min() - t0) / 1e3, 2), round((np.median(t[:, k]) - t0) / 1e3, 2),
+               round((t[:, k].max() - t0) / 1e3, 2)) for k, n in enumerate(names)})
