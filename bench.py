@@ -177,12 +177,13 @@ def run_ours(args, rank, world):
     out = torch.empty(1, cfg.hidden, device=dev)
     act = torch.empty(cfg.inter, device=dev, dtype=torch.float16)
     bar = torch.zeros(1, device=dev, dtype=torch.int64)
+    accum = torch.zeros(1, cfg.hidden, device=dev, dtype=torch.int64)
     fargs = []
     for lyr in model.layers:
         fargs.append(_native.FfnArgs(
             dtype=2, batch=1, hidden=cfg.hidden, inter=cfg.inter,
-            flags=_native.NORM | _native.RESID, grid=0, eps=cfg.eps, x=None,
-            resid=resid.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
+            flags=_native.NORM | _native.RESID | _native.PDL, grid=0, eps=cfg.eps, x=None,
+            resid=resid.data_ptr(), accum=accum.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
             w_dn=lyr["w_dn"].data_ptr(), act=act.data_ptr(), out=out.data_ptr(),
             barrier=bar.data_ptr()))
     torch.cuda.synchronize()

@@ -47,7 +47,9 @@ enum cfb_flags {
   CFB_ROPE = 1 << 2,         /* rotate q and k_new (rotate-half convention) at position S+b */
   CFB_NORM = 1 << 3,         /* x = f16(rmsnorm(resid) * norm_w) instead of reading x */
   CFB_RESID = 1 << 4,        /* out = resid + sum_heads(...) (residual add in the epilogue) */
-  CFB_STATS_MERGED = 1 << 5  /* stats_mode="merged": one SOFTMAX_MERGE pair reduce */
+  CFB_STATS_MERGED = 1 << 5, /* stats_mode="merged": one SOFTMAX_MERGE pair reduce */
+  CFB_PDL = 1 << 6           /* programmatic dependent launch: the kernel may start while its
+                                stream predecessor finishes (weights stream before the wait) */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
@@ -76,9 +78,14 @@ enum cfb_stage {
  *   w_out    [n_heads][D][Hp]            T     (W_out[head])^T, rank r owns rows r*D/N..
  *   k_cache, v_cache [n_heads][cache_cap][Hp] T
  *   rope_cs  [cache_cap][Hp/2][2]        fp32  (cos, sin)
- *   out      [B][D]                      fp32  sum over heads in head order (+resid)
- *   out_partial [n_heads][B][D]          fp32  workspace
- *   tickets  [cfb_mha_ticket_count()]    u32   workspace, zero before first use
+ *   accum    [B][D]                      u64   cross-head sum in 64-bit fixed point
+ *                                              (value * 2^32, two's complement), zero
+ *                                              before first use; every CTA adds its
+ *                                              O-proj columns with red.global.add, so
+ *                                              the sum is order-independent (deterministic)
+ *   out      [B][D]                      fp32  (nullable) out = [resid +] accum * 2^-32,
+ *                                              after which accum is re-zeroed; NULL leaves
+ *                                              the sum in accum for cfb_ffn_decode
  *   stats    [n_heads][2][B]             fp32  (score_max, score_sum) of rank 0
  * D must be a multiple of 8*N/(gcd) (16-byte rows); Hp (head_pad) a power of
  * two >= 8 holding head_dim logical dims (rest zero-padded by the caller).
@@ -101,20 +108,20 @@ typedef struct cfb_mha_args {
   const float* rope_cs;
   const int* step_pos;  /* device int: S for this launch (graph-friendly) */
   float* out;
-  float* out_partial;
-  unsigned* tickets;
+  unsigned long long* accum;
   float* stats;
   unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
   unsigned long long* trace;   /* [grid CTAs][8] %globaltimer phase stamps (profiling), or NULL */
 } cfb_mha_args;
 
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);
-size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
 
 
 /*
  * Fused SwiGLU FFN (one launch, persistent grid, one CTA per SM):
- *   out = [resid +] (silu(h w1^T) * (h w2^T)) w3^T,  h = x or f16(rmsnorm(resid) * norm_w)
+ *   out = [r +] (silu(h w1^T) * (h w2^T)) w3^T,  h = x or f16(rmsnorm(r) * norm_w),
+ *   r = resid [+ accum * 2^-32]  (accum: the attention module's fixed-point head
+ *   sum, nullable; re-zeroed by this kernel).  out may alias resid.
  *   w_gu  [F][2][D]  T   row 2f = w1[f] (gate), row 2f+1 = w2[f] (up)
  *   w_dn  [D][F]     T   = w3
  *   act   [B][F]     T   workspace;  barrier: one u64, zero before first use
@@ -124,6 +131,7 @@ typedef struct cfb_ffn_args {
   float eps;
   const void* x;
   const float* resid;
+  unsigned long long* accum;
   const void* norm_w;
   const void* w_gu;
   const void* w_dn;
@@ -139,7 +147,7 @@ int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
  * workspace; ticket one u32 (zero); token_out [B]; step_pos (nullable) is
  * incremented once the token is written. */
 typedef struct cfb_lm_args {
-  int dtype, batch, hidden, vocab, grid;
+  int dtype, batch, hidden, vocab, grid, flags; /* flags: CFB_PDL */
   float eps;
   const float* resid;
   const void* norm_w;
@@ -160,7 +168,8 @@ int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int b
 /*
  * Whole-model greedy decode step (Llama2 family, batch 1):
  *   embed -> n_layers x (split_token attention module [norm, rope, kv append,
- *   residual] -> fused FFN [norm, residual]) -> final norm + LM head + argmax.
+ *   fixed-point head sum] -> fused FFN [residual + head sum, norm, residual])
+ *   -> final norm + LM head + argmax, every launch with CFB_PDL.
  * Per-layer weight pointers are in the layouts above; rope_cs [cache_cap][H/2][2].
  * The engine owns its small workspace; the CUDA graph of one step advances
  * the device-side position, so replays decode consecutive tokens.

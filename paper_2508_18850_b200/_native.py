@@ -17,7 +17,7 @@ from .exceptions import (DimensionError, InvalidClusterSize, ShapeMismatch, Simu
 LIB_PATH = Path(__file__).resolve().parent / "libcfb.so"
 
 CFB_F16, CFB_F32 = 2, 4
-APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED = 1, 2, 4, 8, 16, 32
+APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED, PDL = 1, 2, 4, 8, 16, 32, 64
 STAGE_NAMES = ("qkv_gather", "stats_max_reduce", "stats_sum_reduce", "stats_merge_reduce",
                "attn_out_reduce", "q_proj_gather", "latent_kv_gather", "absorbed_q_gather",
                "down_proj_reduce", "score_reduce", "out_proj_reduce")
@@ -35,8 +35,8 @@ class MhaArgs(ctypes.Structure):
         ("flags", ctypes.c_int),
         ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("eps", ctypes.c_float),
         ("w_qkv", _vp), ("w_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
-        ("rope_cs", _vp), ("step_pos", _vp), ("out", _vp), ("out_partial", _vp),
-        ("tickets", _vp), ("stats", _vp), ("traffic", _vp), ("trace", _vp),
+        ("rope_cs", _vp), ("step_pos", _vp), ("out", _vp), ("accum", _vp),
+        ("stats", _vp), ("traffic", _vp), ("trace", _vp),
     ]
 
 
@@ -53,8 +53,6 @@ def lib() -> ctypes.CDLL:
         L = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | ctypes.RTLD_GLOBAL)
         L.cfb_mha_decode.argtypes = [ctypes.POINTER(MhaArgs), _vp]
         L.cfb_mha_decode.restype = ctypes.c_int
-        L.cfb_mha_ticket_count.argtypes = [ctypes.c_int] * 4
-        L.cfb_mha_ticket_count.restype = ctypes.c_size_t
         L.cfb_cluster_collective.argtypes = [ctypes.c_int] * 4 + [_vp, _vp, _vp, _vp]
         L.cfb_cluster_collective.restype = ctypes.c_int
         L.cfb_last_error.restype = ctypes.c_char_p
@@ -99,14 +97,14 @@ class FfnArgs(ctypes.Structure):
     """Mirror of ``cfb_ffn_args``."""
 
     _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "inter", "flags", "grid")] + [
-        ("eps", ctypes.c_float), ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("w_gu", _vp),
+        ("eps", ctypes.c_float), ("x", _vp), ("resid", _vp), ("accum", _vp), ("norm_w", _vp), ("w_gu", _vp),
         ("w_dn", _vp), ("act", _vp), ("out", _vp), ("barrier", _vp), ("trace", _vp)]
 
 
 class LmArgs(ctypes.Structure):
     """Mirror of ``cfb_lm_args``."""
 
-    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "vocab", "grid")] + [
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "vocab", "grid", "flags")] + [
         ("eps", ctypes.c_float), ("resid", _vp), ("norm_w", _vp), ("w", _vp), ("logits", _vp),
         ("cand_val", _vp), ("cand_idx", _vp), ("ticket", _vp), ("token_out", _vp),
         ("step_pos", _vp)]

@@ -31,10 +31,6 @@ int cfb_mha_decode(const cfb_mha_args* args, void* stream) {
   return cfb::mha_decode(args, static_cast<cudaStream_t>(stream));
 }
 
-size_t cfb_mha_ticket_count(int hidden, int head_pad, int cluster, int dtype) {
-  return cfb::mha_ticket_count(hidden, head_pad, cluster, dtype);
-}
-
 int cfb_ffn_decode(const cfb_ffn_args* args, void* stream) {
   return cfb::ffn_decode(args, static_cast<cudaStream_t>(stream));
 }

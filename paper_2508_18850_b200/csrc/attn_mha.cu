@@ -12,10 +12,19 @@
 //      SOFTMAX_MERGE pair reduce)                             :187-227
 //   6. rescale A by exp(m_b - m*)/l*, SUM reduce of A (DSMEM) :298-300
 //   7. O-proj over output columns [r*D/N, (r+1)*D/N)         :302-310
-//   8. cross-head sum: per-head fp32 partials, the last CTA to finish a
-//      column chunk (ticket) sums the heads in head order (+ residual).
-//      Deterministic replacement of the reference's atomic_accumulate.
+//   8. cross-head sum: every CTA adds its O-proj columns into a 64-bit
+//      fixed-point accumulator (value * 2^32, red.global.add.u64).  Integer
+//      addition is associative, so the sum is bit-identical whatever order
+//      the 32 heads' CTAs arrive in: a deterministic replacement of the
+//      reference's atomic_accumulate (dataflows.py:302-310) with no tickets,
+//      fences or serial tail.  The consumer (the FFN prologue in the decode
+//      engine, or mha_finalize_kernel for the API) converts it back to fp32.
 // Storage rounding follows simcore.py: every buffer store is rounded to T.
+//
+// Programmatic dependent launch: the producer warp streams this CTA's W_qkv
+// rows before griddepcontrol.wait, i.e. while the previous kernel is still
+// finishing; everything that reads activations, the step position or the KV
+// cache happens after the wait.
 #include <cuda_runtime.h>
 
 #include "collectives.cuh"
@@ -26,7 +35,7 @@ namespace cfb {
 
 struct MhaParams {
   int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags, spw;
-  float sqrt_h, eps;
+  float inv_sqrt_h, eps;
   const void* x;
   const float* resid;
   const void* norm_w;
@@ -36,16 +45,14 @@ struct MhaParams {
   void* v_cache;
   const float* rope_cs;
   const int* step_pos;
-  float* out;
-  float* out_partial;
-  unsigned* tickets;
+  unsigned long long* accum;  // [B][D] fixed-point head sum (2^-32 units)
   float* stats;
   unsigned long long* traffic;
   unsigned long long* trace;
 };
 
 struct MhaLayout {
-  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, total;
+  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, misc, total;
   int seg_bytes, a_bytes, st_bytes;
 };
 
@@ -74,6 +81,7 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.st = o;         o += 2 * L.st_bytes;
   L.strx = o;       o += 8 * L.st_bytes;
   L.red = o;        o += round16(kNumConsumerWarps * B * 4);
+  L.misc = o;       o += 16;
   L.total = o;
   return L;
 }
@@ -82,6 +90,11 @@ template <typename T, int EPL, int QB>
 __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaParams p) {
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
+  // keys (rows) per online-softmax / O-proj chunk: a chunk's dot products,
+  // shuffle reductions and exponentials are independent, which is the ILP
+  // that hides shuffle/MUFU latency with only 8 consumer warps per SM
+  constexpr int RC = QB == 1 ? 4 : (QB <= 4 ? 2 : 1);
+  constexpr int RO = QB == 1 ? 8 : (QB <= 4 ? 4 : 1);
   const int B = p.B, D = p.D, Hp = p.Hp;
   const uint32_t N = p.N;
   const int h = Hp / N;
@@ -94,10 +107,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   const int head = blockIdx.y;
   int rounds = 0;
   while ((1u << rounds) < N) ++rounds;
-  const int S = p.step_pos ? *p.step_pos : p.S_static;
-  const int seg = S == 0 ? 0 : (S + (int)N - 1) / (int)N;
-  const int lo = min((int)rank * seg, S), hi = min(lo + seg, S);
-  const bool merged = p.flags & 32;
+  const bool merged = p.flags & CFB_STATS_MERGED;
 
   if (tid == 0) {
     ring_init(ring);
@@ -115,23 +125,33 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
   __syncthreads();
   cluster_arrive();
+  pdl_launch_dependents();
 
   const size_t cache_head = (size_t)head * p.cache_cap * Hp;
   const int qkv_rows = 3 * h, qkv_tiles = (qkv_rows + kTileRows - 1) / kTileRows;
   const Phase P0 = make_phase(static_cast<const T*>(p.w_qkv) +
                                   ((size_t)head * N + rank) * qkv_tiles * kTileRows * D,
                               nullptr, qkv_tiles, kTileRows * D * tb, true);
-  const Phase P1 = make_phase(static_cast<const T*>(p.k_cache) + cache_head + (size_t)lo * Hp,
-                              static_cast<const T*>(p.v_cache) + cache_head + (size_t)lo * Hp,
-                              hi - lo, Hp * tb);
   const int cols = D / (int)N;
   const Phase P2 = make_phase(static_cast<const T*>(p.w_out) + (size_t)head * D * Hp +
                                   (size_t)rank * cols * Hp,
                               nullptr, cols, Hp * tb);
+  auto kv_phase = [&](int S) {
+    const int seg = S == 0 ? 0 : (S + (int)N - 1) / (int)N;
+    const int lo = min((int)rank * seg, S), hi = min(lo + seg, S);
+    return make_phase(static_cast<const T*>(p.k_cache) + cache_head + (size_t)lo * Hp,
+                      static_cast<const T*>(p.v_cache) + cache_head + (size_t)lo * Hp, hi - lo,
+                      Hp * tb);
+  };
 
   if (warp == kNumConsumerWarps) {  // ------------------------------ producer
-    const Phase ph[3] = {P0, P1, P2};
-    produce_all(ph, ring, lane, policy_evict_first());
+    int c = 0;
+    const Phase ph0[1] = {P0};
+    produce_all(ph0, ring, lane, policy_evict_first(), c);  // weights: before the PDL wait
+    pdl_wait();
+    const int S = p.step_pos ? *p.step_pos : p.S_static;
+    const Phase ph1[2] = {kv_phase(S), P2};
+    produce_all(ph1, ring, lane, policy_evict_first(), c);
     __syncwarp();
     cluster_wait();
     cluster_arrive();
@@ -161,8 +181,12 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   float* red = reinterpret_cast<float*>(smem + L.red);
   unsigned long long sent[5] = {0, 0, 0, 0, 0};  // gather, max, sum, merge, attn
 
+  pdl_wait();  // activations / step position / KV cache of the previous kernel
+  const int S = p.step_pos ? *p.step_pos : p.S_static;
+  const Phase P1 = kv_phase(S);
+
   // 1. activations
-  if (p.flags & 8) {
+  if (p.flags & CFB_NORM) {
     rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
     load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
@@ -194,7 +218,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     vf[idx] = Elem<T>::to_f(sg[2 * h + i]);
   }
   consumer_sync();
-  if (p.flags & 4) {  // RoPE (rotate-half) at position S + b
+  if (p.flags & CFB_ROPE) {  // RoPE (rotate-half) at position S + b
     const int half = Hp / 2;
     for (int idx = tid; idx < B * half; idx += kConsumerThreads) {
       const int b = idx / half, i = idx % half;
@@ -210,7 +234,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     }
     consumer_sync();
   }
-  if ((p.flags & 2) && rank == N - 1) {  // KV-cache append at rows S..S+B-1
+  if ((p.flags & CFB_WRITE_KV) && rank == N - 1) {  // KV-cache append at rows S..S+B-1
     T* kc = static_cast<T*>(p.k_cache) + cache_head;
     T* vc = static_cast<T*>(p.v_cache) + cache_head;
     for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
@@ -220,8 +244,11 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
 
   if (tr && tid == 0) tr[3] = globaltimer();
-  // 4. split-KV flash decoding over this rank's segment (online softmax per warp)
+  // 4. split-KV flash decoding over this rank's segment.  A warp covers KPP
+  //    keys per step (LPK lanes x EPL dims each); RC steps form one chunk
+  //    whose scores share one max/rescale (online softmax per chunk).
   const int LPK = Hp / EPL, KPP = 32 / LPK, g = lane / LPK, li = lane % LPK;
+  const float inv_sqrt_h = p.inv_sqrt_h;
   float q[QB][EPL], acc[QB][EPL], m[QB], l[QB];
 #pragma unroll
   for (int b = 0; b < QB; ++b) {
@@ -233,39 +260,56 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
       acc[b][e] = 0.f;
     }
   }
-  const float sqrt_h = p.sqrt_h;
   auto attend = [&](auto&& load_k, auto&& load_v, int nkeys) {
-    for (int k0 = 0; k0 < nkeys; k0 += KPP) {
-      const int key = k0 + g;
-      const bool valid = key < nkeys;
-      const int kk = valid ? key : 0;
-      float kv[EPL], vv[EPL], s[QB];
-      load_k(kk, kv);
+    for (int k0 = 0; k0 < nkeys; k0 += RC * KPP) {
+      float s[RC][QB];
+      bool valid[RC];
 #pragma unroll
-      for (int b = 0; b < QB; ++b) {
-        float t = 0.f;
+      for (int j = 0; j < RC; ++j) {
+        const int key = k0 + j * KPP + g;
+        valid[j] = key < nkeys;
+        float kv[EPL];
+        load_k(valid[j] ? key : 0, kv);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) t = fmaf(q[b][e], kv[e], t);
-        s[b] = t;
+        for (int b = 0; b < QB; ++b) {
+          float t = 0.f;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) t = fmaf(q[b][e], kv[e], t);
+          s[j][b] = t;
+        }
       }
       for (int o = 1; o < LPK; o <<= 1) {
 #pragma unroll
-        for (int b = 0; b < QB; ++b) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
+        for (int j = 0; j < RC; ++j)
+#pragma unroll
+          for (int b = 0; b < QB; ++b) s[j][b] += __shfl_xor_sync(0xffffffffu, s[j][b], o);
       }
-      load_v(kk, vv);
+      float vv[RC][EPL];
+#pragma unroll
+      for (int j = 0; j < RC; ++j) load_v(valid[j] ? k0 + j * KPP + g : 0, vv[j]);
 #pragma unroll
       for (int b = 0; b < QB; ++b) {
         if (b >= B) continue;
-        const float sb = valid ? __fdiv_rn(s[b], sqrt_h) : -INFINITY;
-        float mx = sb;
-        for (int o = LPK; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        const float mn = fmaxf(m[b], mx);
-        if (mn == -INFINITY) continue;
-        const float alpha = (m[b] == -INFINITY) ? 0.f : expf(m[b] - mn);
-        const float pr = valid ? expf(sb - mn) : 0.f;
-        l[b] = fmaf(l[b], alpha, pr);
+        float mx = -INFINITY;
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) acc[b][e] = fmaf(pr, vv[e], acc[b][e] * alpha);
+        for (int j = 0; j < RC; ++j) {
+          s[j][b] = valid[j] ? __fmul_rn(s[j][b], inv_sqrt_h) : -INFINITY;
+          mx = fmaxf(mx, s[j][b]);
+        }
+        for (int o = LPK; o < 32; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        const float mn = fmaxf(m[b], mx);  // finite: the chunk has >= 1 valid key
+        const float alpha = __expf(m[b] - mn);  // m = -inf -> 0
+        float ps = 0.f;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[b][e] *= alpha;
+#pragma unroll
+        for (int j = 0; j < RC; ++j) {
+          const float pr = __expf(s[j][b] - mn);  // invalid: exp(-inf) = 0
+          ps += pr;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) acc[b][e] = fmaf(pr, vv[j][e], acc[b][e]);
+        }
+        l[b] = fmaf(l[b], alpha, ps);
         m[b] = mn;
       }
     }
@@ -276,7 +320,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     attend([&](int k, float* o) { load_elems<T, EPL>(K + k * Hp + li * EPL, o); },
            [&](int k, float* o) { load_elems<T, EPL>(V + k * Hp + li * EPL, o); }, it.nunits);
   });
-  if ((p.flags & 1) && rank == N - 1 && warp == 0) {  // new token(s): counted exactly once
+  if ((p.flags & CFB_APPEND) && rank == N - 1 && warp == 0) {  // new token(s): counted once
     attend([&](int k, float* o) {
              for (int e = 0; e < EPL; ++e) o[e] = kf[k * Hp + li * EPL + e];
            },
@@ -285,7 +329,8 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
            },
            B);
   }
-  // fold the KPP key groups of the warp (same lane-in-group = same dims)
+  // fold the KPP key groups of the warp (same lane-in-group = same dims);
+  // the groups share m (warp-uniform), so l and acc simply add
 #pragma unroll
   for (int b = 0; b < QB; ++b) {
     for (int o = LPK; o < 32; o <<= 1) {
@@ -338,11 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   if (warp == 0) {
     T* rx[4];
     uint64_t* rb[4];
-    for (int i = 0; i < L.st_bytes / tb; i += 1)
-      if (i % 32 == lane) {
-        st0[i] = Elem<T>::from_f(0.f);
-        st1[i] = Elem<T>::from_f(0.f);
-      }
+    for (int i = lane; i < L.st_bytes / tb; i += 32) {
+      st0[i] = Elem<T>::from_f(0.f);
+      st1[i] = Elem<T>::from_f(0.f);
+    }
     __syncwarp();
     if (merged) {
       for (int b = lane; b < B; b += 32) {
@@ -424,55 +468,48 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   consumer_sync();
 
   if (tr && tid == 0) tr[5] = globaltimer();
-  // 7. O-projection over this rank's output columns + 8. cross-head sum
+  // 7. O-projection over this rank's output columns, RO rows per chunk, and
+  // 8. the cross-head sum into the fixed-point accumulator
   float a[QB][EPL];
 #pragma unroll
   for (int b = 0; b < QB; ++b)
 #pragma unroll
     for (int e = 0; e < EPL; ++e) a[b][e] = (b < B) ? Elem<T>::to_f(abuf[b * Hp + li * EPL + e]) : 0.f;
   const int c_base = (int)rank * cols;
-  const int items_per_rank = (cols + P2.per_item - 1) / P2.per_item;
   consume_phase(P2, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     const T* W = reinterpret_cast<const T*>(slot);
-    for (int k0 = 0; k0 < it.nunits; k0 += KPP) {
-      const int row = k0 + g;
-      const bool valid = row < it.nunits;
-      float w[EPL], s[QB];
-      load_elems<T, EPL>(W + (valid ? row : 0) * Hp + li * EPL, w);
+    for (int k0 = 0; k0 < it.nunits; k0 += RO * KPP) {
+      float s[RO][QB];
 #pragma unroll
-      for (int b = 0; b < QB; ++b) {
-        float t = 0.f;
+      for (int j = 0; j < RO; ++j) {
+        const int row = k0 + j * KPP + g;
+        float w[EPL];
+        load_elems<T, EPL>(W + (row < it.nunits ? row : 0) * Hp + li * EPL, w);
 #pragma unroll
-        for (int e = 0; e < EPL; ++e) t = fmaf(a[b][e], w[e], t);
-        s[b] = t;
+        for (int b = 0; b < QB; ++b) {
+          float t = 0.f;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e) t = fmaf(a[b][e], w[e], t);
+          s[j][b] = t;
+        }
       }
       for (int o = 1; o < LPK; o <<= 1) {
 #pragma unroll
-        for (int b = 0; b < QB; ++b) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
-      }
-      if (valid && li == 0) {
+        for (int j = 0; j < RO; ++j)
 #pragma unroll
-        for (int b = 0; b < QB; ++b)
-          if (b < B) p.out_partial[((size_t)head * B + b) * D + c_base + it.unit0 + row] = s[b];
+          for (int b = 0; b < QB; ++b) s[j][b] += __shfl_xor_sync(0xffffffffu, s[j][b], o);
       }
-    }
-    __threadfence();
-    __syncwarp();
-    unsigned old = 0;
-    const int chunk = (int)rank * items_per_rank + it.unit0 / P2.per_item;
-    if (lane == 0) old = atomicAdd(&p.tickets[chunk], 1u);
-    old = __shfl_sync(0xffffffffu, old, 0);
-    if (old == (unsigned)p.n_heads - 1) {  // last head for this chunk: sum heads in order
-      __threadfence();
-      for (int idx = lane; idx < B * it.nunits; idx += 32) {
-        const int b = idx / it.nunits;
-        const int c = c_base + it.unit0 + idx % it.nunits;
-        float s = 0.f;
-        for (int hh = 0; hh < p.n_heads; ++hh) s += __ldcg(&p.out_partial[((size_t)hh * B + b) * D + c]);
-        if (p.flags & 16) s = p.resid[(size_t)b * D + c] + s;
-        p.out[(size_t)b * D + c] = s;
+      if (li == 0) {
+#pragma unroll
+        for (int j = 0; j < RO; ++j) {
+          const int row = k0 + j * KPP + g;
+          if (row < it.nunits) {
+#pragma unroll
+            for (int b = 0; b < QB; ++b)
+              if (b < B) red_add_fixed(&p.accum[(size_t)b * D + c_base + it.unit0 + row], s[j][b]);
+          }
+        }
       }
-      if (lane == 0) p.tickets[chunk] = 0;  // re-arm for the next launch
     }
   });
   if (tr && tid == 0) tr[6] = globaltimer();
@@ -481,10 +518,21 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   if (tr && tid == 0) tr[7] = globaltimer();
 }
 
+// API epilogue: out = [resid +] accum * 2^-32, then re-zero the accumulator.
+__global__ void mha_finalize_kernel(float* out, const float* resid,
+                                    unsigned long long* accum, int n) {
+  pdl_wait();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const float v = fixed_to_float(accum[i]);
+    out[i] = resid ? __fadd_rn(resid[i], v) : v;
+    accum[i] = 0ull;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 
 template <typename T, int EPL, int QB>
-static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st) {
+static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st, bool pdl) {
   auto kern = mha_split_token_kernel<T, EPL, QB>;
   static bool configured = false;
   if (!configured) {
@@ -497,28 +545,24 @@ static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = p.N;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  LaunchAttrs at(p.N, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
   CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return CFB_OK;
 }
 
 template <typename T>
-static int launch_mha_t(const MhaParams& p, size_t smem, cudaStream_t st) {
-  if (p.B > 4) return launch_mha_inst<T, 4, 16>(p, smem, st);
+static int launch_mha_t(const MhaParams& p, size_t smem, cudaStream_t st, bool pdl) {
+  if (p.B > 4) return launch_mha_inst<T, 4, 16>(p, smem, st, pdl);
   if (p.Hp == 8) {  // EPL: attention elements per lane
-    if (p.B == 1) return launch_mha_inst<T, 8, 1>(p, smem, st);
-    if (p.B == 2) return launch_mha_inst<T, 8, 2>(p, smem, st);
-    return launch_mha_inst<T, 8, 4>(p, smem, st);
+    if (p.B == 1) return launch_mha_inst<T, 8, 1>(p, smem, st, pdl);
+    if (p.B == 2) return launch_mha_inst<T, 8, 2>(p, smem, st, pdl);
+    return launch_mha_inst<T, 8, 4>(p, smem, st, pdl);
   }
-  if (p.B == 1) return launch_mha_inst<T, 16, 1>(p, smem, st);
-  if (p.B == 2) return launch_mha_inst<T, 16, 2>(p, smem, st);
-  return launch_mha_inst<T, 16, 4>(p, smem, st);
+  if (p.B == 1) return launch_mha_inst<T, 16, 1>(p, smem, st, pdl);
+  if (p.B == 2) return launch_mha_inst<T, 16, 2>(p, smem, st, pdl);
+  return launch_mha_inst<T, 16, 4>(p, smem, st, pdl);
 }
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
@@ -548,9 +592,8 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
     return set_error(CFB_ERR_ARGUMENT, "CFB_NORM/CFB_RESID need resid");
   if ((a->flags & CFB_NORM) && !a->norm_w) return set_error(CFB_ERR_ARGUMENT, "CFB_NORM needs norm_w");
   if (!(a->flags & CFB_NORM) && !a->x) return set_error(CFB_ERR_ARGUMENT, "x is null");
-  if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->out || !a->out_partial ||
-      !a->tickets)
-    return set_error(CFB_ERR_ARGUMENT, "null weight / cache / workspace pointer");
+  if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->accum)
+    return set_error(CFB_ERR_ARGUMENT, "null weight / cache / accumulator pointer");
   int spw = tuned_spw();
   MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb, spw);
   while (L.total > kMaxSmem && spw > 1) L = mha_layout(a->batch, a->hidden, Hp, N, tb, --spw);
@@ -568,7 +611,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.cache_cap = a->cache_cap;
   p.flags = a->flags;
   p.spw = spw;
-  p.sqrt_h = (float)std::sqrt((double)a->head_dim);
+  p.inv_sqrt_h = (float)(1.0 / std::sqrt((double)a->head_dim));
   p.eps = a->eps;
   p.x = a->x;
   p.resid = a->resid;
@@ -579,19 +622,18 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.v_cache = a->v_cache;
   p.rope_cs = a->rope_cs;
   p.step_pos = a->step_pos;
-  p.out = a->out;
-  p.out_partial = a->out_partial;
-  p.tickets = a->tickets;
+  p.accum = a->accum;
   p.stats = a->stats;
   p.traffic = a->traffic;
   p.trace = a->trace;
-  return tb == 2 ? launch_mha_t<__half>(p, L.total, st) : launch_mha_t<float>(p, L.total, st);
-}
-
-size_t mha_ticket_count(int hidden, int head_pad, int cluster, int dtype) {
-  const int cols = hidden / cluster;
-  const int rpi = kSlotBytes / (head_pad * dtype);
-  return (size_t)cluster * ((cols + rpi - 1) / rpi);
+  const bool pdl = a->flags & CFB_PDL;
+  int rc = tb == 2 ? launch_mha_t<__half>(p, L.total, st, pdl) : launch_mha_t<float>(p, L.total, st, pdl);
+  if (rc || !a->out) return rc;
+  const int n = a->batch * a->hidden;
+  mha_finalize_kernel<<<(n + 255) / 256, 256, 0, st>>>(
+      a->out, (a->flags & CFB_RESID) ? a->resid : nullptr, a->accum, n);
+  CFB_CUDA(cudaGetLastError());
+  return CFB_OK;
 }
 
 }  // namespace cfb

@@ -14,6 +14,28 @@ namespace cfb {
 constexpr int kMaxSmem = 227 * 1024;
 constexpr int kMaxSlotsPerWarpHost = 3;  // == kMaxSlotsPerWarp (stream.cuh)
 
+// Launch attributes shared by the cfb kernels: optional cluster shape and
+// programmatic dependent launch (the kernel may start while its predecessor
+// in the stream finishes; it orders itself with griddepcontrol.wait).
+struct LaunchAttrs {
+  cudaLaunchAttribute a[2];
+  int n = 0;
+  LaunchAttrs(int cluster, bool pdl) {
+    if (cluster > 0) {
+      a[n].id = cudaLaunchAttributeClusterDimension;
+      a[n].val.clusterDim.x = cluster;
+      a[n].val.clusterDim.y = 1;
+      a[n].val.clusterDim.z = 1;
+      ++n;
+    }
+    if (pdl) {
+      a[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      a[n].val.programmaticStreamSerializationAllowed = 1;
+      ++n;
+    }
+  }
+};
+
 int set_error(int code, const char* fmt, ...);
 
 // Ring depth (slots per consumer warp); CFB_SPW overrides it for tuning runs.
@@ -28,11 +50,10 @@ int tuned_spw();
   } while (0)
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
-size_t mha_ticket_count(int hidden, int head_pad, int cluster, int dtype);
 int ffn_decode(const cfb_ffn_args* a, cudaStream_t st);
 int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st);
 int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
-          cudaStream_t st);
+          cudaStream_t st, bool pdl = false);
 int cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
                        unsigned long long* traffic, cudaStream_t st);
 

@@ -14,6 +14,12 @@
 // global memory and a grid barrier; the producer warp keeps streaming this
 // CTA's w3 tiles into the ring while the barrier is pending, so HBM never
 // idles at the phase boundary.
+//
+// Decoder-block form: the residual entering the block is r = resid + the
+// attention module's fixed-point head sum (accum), folded into the RMSNorm
+// prologue; after the grid barrier every CTA re-zeroes accum for the output
+// rows it owns, and writes out = r + FFN for those rows (out may alias
+// resid).  With PDL the producer streams w_gu before griddepcontrol.wait.
 #include <cuda_runtime.h>
 
 #include "common.h"
@@ -26,6 +32,7 @@ struct FfnParams {
   float eps;
   const void* x;          // [B][D] T (no CFB_NORM)
   const float* resid;     // [B][D] fp32
+  unsigned long long* accum;  // [B][D] fixed-point attention head sum (nullable)
   const void* norm_w;     // [D] T
   const void* w_gu;       // row-tiled, F/2 tiles of D
   const void* w_dn;       // row-tiled, D/4 tiles of F
@@ -41,13 +48,13 @@ struct FfnLayout {
   int bars, x, gu, part, red, total;
 };
 
-__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int spw) {
+__host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int spw, bool xh) {
   FfnLayout L;
   const int t1 = (F / 2 + G - 1) / G, t2 = (D / 4 + G - 1) / G;  // max tiles per CTA
   const int rows = 4 * (t1 > t2 ? t1 : t2);
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
-  L.x = o;     o += ((B * (D > F ? D : F) * 4 + 15) & ~15);
+  L.x = o;     o += ((B * (D > F ? D : F) * (xh ? 2 : 4) + 15) & ~15);
   L.gu = o;    o += ((B * 4 * t1 * 4 + 15) & ~15);
   L.part = o;  o += ((kNumConsumerWarps * B * rows * 4 + 15) & ~15);
   L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
@@ -55,12 +62,12 @@ __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int 
   return L;
 }
 
-template <typename T, int QB>
+template <typename T, int QB, bool XH>
 __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams p) {
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
   const int B = p.B, D = p.D, F = p.F, G = gridDim.x, i = blockIdx.x;
-  const FfnLayout L = ffn_layout(B, D, F, G, p.spw);
+  const FfnLayout L = ffn_layout(B, D, F, G, p.spw, XH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -76,27 +83,42 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
                               4 * D * tb, true);
   const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)u0 * 4 * F, nullptr, u1 - u0,
                               4 * F * tb, true);
+  pdl_launch_dependents();
   if (warp == kNumConsumerWarps) {
     const Phase ph[2] = {P0, P1};
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
+  pdl_wait();
   unsigned long long* tr = p.trace ? p.trace + (size_t)i * 8 : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer();
-  float* xs = reinterpret_cast<float*>(smem + L.x);
+  XElem<XH>* xs = reinterpret_cast<XElem<XH>*>(smem + L.x);
   float* gu = reinterpret_cast<float*>(smem + L.gu);  // [B][4*(a1-a0)]
   float* part = reinterpret_cast<float*>(smem + L.part);
   float* red = reinterpret_cast<float*>(smem + L.red);
   const int rows0 = 4 * (a1 - a0);
 
-  if (p.flags & CFB_NORM)
-    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
-  else
-    load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
+  if ((p.flags & CFB_NORM) && p.accum) {
+    const float* resid = p.resid;
+    const unsigned long long* acc = p.accum;
+    rmsnorm_to_smem_ld<T, XH>(
+        xs,
+        [&](int b, int v) {
+          const float4 r = reinterpret_cast<const float4*>(resid + (size_t)b * D)[v];
+          const ulonglong2 a0 = __ldcg(reinterpret_cast<const ulonglong2*>(acc + (size_t)b * D) + 2 * v);
+          const ulonglong2 a1 = __ldcg(reinterpret_cast<const ulonglong2*>(acc + (size_t)b * D) + 2 * v + 1);
+          return make_float4(__fadd_rn(r.x, fixed_to_float(a0.x)), __fadd_rn(r.y, fixed_to_float(a0.y)),
+                             __fadd_rn(r.z, fixed_to_float(a1.x)), __fadd_rn(r.w, fixed_to_float(a1.y)));
+        },
+        static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  } else if (p.flags & CFB_NORM) {
+    rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  } else
+    load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
 
   if (tr && tid == 0) tr[1] = globaltimer();
   int cnt = 0;
-  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows0, part,
+  tiled_gemv_phase<T, QB, XH>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows0, part,
                           [&](int row, int b, float v) { gu[b * rows0 + row] = v; });
   consumer_sync();
   T* act_g = static_cast<T*>(p.act);
@@ -111,29 +133,43 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   if (tr && tid == 0) tr[2] = globaltimer();
   grid_barrier(p.barrier, tid);
   if (tr && tid == 0) tr[3] = globaltimer();
-  load_act_to_smem<T>(xs, act_g, B, F, tid);
+  load_act_to_smem<T, XH>(xs, act_g, B, F, tid);
   if (tr && tid == 0) tr[4] = globaltimer();
 
   const int rows1 = 4 * (u1 - u0);
-  tiled_gemv_phase<T, QB>(P1, ring, warp, lane, tid, cnt, xs, F, B, rows1, part,
+  tiled_gemv_phase<T, QB, XH>(P1, ring, warp, lane, tid, cnt, xs, F, B, rows1, part,
                           [&](int row, int b, float v) {
-                            const int c = 4 * u0 + row;
-                            if (p.flags & CFB_RESID) v = __fadd_rn(p.resid[(size_t)b * D + c], v);
-                            p.out[(size_t)b * D + c] = v;
+                            const size_t c = (size_t)b * D + 4 * u0 + row;
+                            if (p.flags & CFB_RESID) {
+                              float r = p.resid[c];
+                              if (p.accum) {
+                                r = __fadd_rn(r, fixed_to_float(__ldcg(p.accum + c)));
+                                p.accum[c] = 0ull;  // every CTA read it before the barrier
+                              }
+                              v = __fadd_rn(r, v);
+                            }
+                            p.out[c] = v;
                           });
   if (tr && tid == 0) tr[5] = globaltimer();
 }
 
-template <typename T, int QB>
+template <typename T, int QB, bool XH>
 static int launch_ffn_inst(const FfnParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = ffn_swiglu_kernel<T, QB>;
+  auto kern = ffn_swiglu_kernel<T, QB, XH>;
   static bool configured = false;
   if (!configured) {
     CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     configured = true;
   }
-  kern<<<grid, kThreads, smem, st>>>(p);
-  CFB_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  LaunchAttrs at(0, p.flags & CFB_PDL);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return CFB_OK;
 }
 
@@ -149,6 +185,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   if ((a->flags & CFB_NORM) ? (!a->resid || !a->norm_w) : !a->x)
     return set_error(CFB_ERR_ARGUMENT, "missing activation input");
   if ((a->flags & CFB_RESID) && !a->resid) return set_error(CFB_ERR_ARGUMENT, "CFB_RESID needs resid");
+  if (a->accum && (a->flags & (CFB_NORM | CFB_RESID)) != (CFB_NORM | CFB_RESID))
+    return set_error(CFB_ERR_ARGUMENT, "accum needs CFB_NORM | CFB_RESID");
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
@@ -156,9 +194,11 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   grid = grid > sms ? sms : grid;  // grid barrier: every CTA must be co-resident
   if (grid > a->hidden / 4) grid = a->hidden / 4;
   if (grid > a->inter / 2) grid = a->inter / 2;
+  // fp16 activations in smem when the fp32 layout cannot fit (batch > 2)
+  const bool xh = tb == 2 && a->batch > 2;
   int spw = tuned_spw();
-  FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, spw);
-  while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, --spw);
+  FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, spw, xh);
+  while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, --spw, xh);
   if (L.total > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "ffn schedule needs %d B of shared memory (max %d)", L.total,
                      kMaxSmem);
@@ -171,6 +211,7 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.eps = a->eps;
   p.x = a->x;
   p.resid = a->resid;
+  p.accum = a->accum;
   p.norm_w = a->norm_w;
   p.w_gu = a->w_gu;
   p.w_dn = a->w_dn;
@@ -180,14 +221,14 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.trace = a->trace;
   const size_t smem = L.total;
   if (tb == 2) {
-    if (p.B == 1) return launch_ffn_inst<__half, 1>(p, grid, smem, st);
-    if (p.B == 2) return launch_ffn_inst<__half, 2>(p, grid, smem, st);
-    if (p.B <= 4) return launch_ffn_inst<__half, 4>(p, grid, smem, st);
-    return launch_ffn_inst<__half, 8>(p, grid, smem, st);
+    if (p.B == 1) return launch_ffn_inst<__half, 1, false>(p, grid, smem, st);
+    if (p.B == 2) return launch_ffn_inst<__half, 2, false>(p, grid, smem, st);
+    if (p.B <= 4) return launch_ffn_inst<__half, 4, true>(p, grid, smem, st);
+    return launch_ffn_inst<__half, 8, true>(p, grid, smem, st);
   }
-  if (p.B == 1) return launch_ffn_inst<float, 1>(p, grid, smem, st);
-  if (p.B <= 4) return launch_ffn_inst<float, 4>(p, grid, smem, st);
-  return launch_ffn_inst<float, 8>(p, grid, smem, st);
+  if (p.B == 1) return launch_ffn_inst<float, 1, false>(p, grid, smem, st);
+  if (p.B <= 4) return launch_ffn_inst<float, 4, false>(p, grid, smem, st);
+  return launch_ffn_inst<float, 8, false>(p, grid, smem, st);
 }
 
 }  // namespace cfb

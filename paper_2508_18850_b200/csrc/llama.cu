@@ -17,10 +17,9 @@ struct cfb_llama {
   const void* lm_head = nullptr;
   const float* rope_cs = nullptr;
   // workspace (engine-owned)
-  float* resid[2] = {nullptr, nullptr};
+  float* resid = nullptr;             // fp32 residual stream [D]
+  unsigned long long* accum = nullptr; // attention head sum, fixed point [D]
   void* act = nullptr;
-  float* out_partial = nullptr;
-  unsigned* tickets = nullptr;
   unsigned long long* barrier = nullptr;
   float* logits = nullptr;
   float* cand_val = nullptr;
@@ -42,7 +41,7 @@ int alloc_zero(void** p, size_t bytes) {
 
 int enqueue_step(cfb_llama* m, cudaStream_t st) {
   const cfb_llama_config& c = m->cfg;
-  int rc = cfb::embed(c.dtype, m->embed, m->token, m->resid[0], 1, c.hidden, st);
+  int rc = cfb::embed(c.dtype, m->embed, m->token, m->resid, 1, c.hidden, st, true);
   if (rc) return rc;
   for (int l = 0; l < c.n_layers; ++l) {
     cfb_mha_args a = {};
@@ -54,8 +53,8 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
     a.head_pad = c.head_dim;
     a.cluster = c.cluster;
     a.cache_cap = c.cache_cap;
-    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_RESID;
-    a.resid = m->resid[0];
+    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_STATS_MERGED | CFB_PDL;
+    a.resid = m->resid;
     a.norm_w = m->attn_norm[l];
     a.eps = c.eps;
     a.w_qkv = m->w_qkv[l];
@@ -64,23 +63,23 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
     a.v_cache = m->v_cache[l];
     a.rope_cs = m->rope_cs;
     a.step_pos = m->pos;
-    a.out = m->resid[1];
-    a.out_partial = m->out_partial;
-    a.tickets = m->tickets;
+    a.out = nullptr;  // the head sum stays in accum for the FFN prologue
+    a.accum = m->accum;
     if ((rc = cfb::mha_decode(&a, st))) return rc;
     cfb_ffn_args f = {};
     f.dtype = c.dtype;
     f.batch = 1;
     f.hidden = c.hidden;
     f.inter = c.inter;
-    f.flags = CFB_NORM | CFB_RESID;
+    f.flags = CFB_NORM | CFB_RESID | CFB_PDL;
     f.eps = c.eps;
-    f.resid = m->resid[1];
+    f.resid = m->resid;
+    f.accum = m->accum;
     f.norm_w = m->ffn_norm[l];
     f.w_gu = m->w_gu[l];
     f.w_dn = m->w_dn[l];
     f.act = m->act;
-    f.out = m->resid[0];
+    f.out = m->resid;
     f.barrier = m->barrier;
     if ((rc = cfb::ffn_decode(&f, st))) return rc;
   }
@@ -90,7 +89,8 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
   h.hidden = c.hidden;
   h.vocab = c.vocab;
   h.eps = c.eps;
-  h.resid = m->resid[0];
+  h.flags = CFB_PDL;
+  h.resid = m->resid;
   h.norm_w = m->final_norm;
   h.w = m->lm_head;
   h.logits = m->logits;
@@ -132,11 +132,8 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
   int rc = 0;
   int sms = cfb_device_sm_count();
   if (sms <= 0) sms = 148;
-  const size_t tickets = cfb::mha_ticket_count(cfg->hidden, cfg->head_dim, cfg->cluster, cfg->dtype);
-  if ((rc = alloc_zero((void**)&m->resid[0], D * 4)) || (rc = alloc_zero((void**)&m->resid[1], D * 4)) ||
+  if ((rc = alloc_zero((void**)&m->resid, D * 4)) || (rc = alloc_zero((void**)&m->accum, D * 8)) ||
       (rc = alloc_zero(&m->act, (size_t)cfg->inter * cfg->dtype)) ||
-      (rc = alloc_zero((void**)&m->out_partial, (size_t)cfg->n_heads * D * 4)) ||
-      (rc = alloc_zero((void**)&m->tickets, tickets * 4)) ||
       (rc = alloc_zero((void**)&m->barrier, 8)) ||
       (rc = alloc_zero((void**)&m->logits, (size_t)cfg->vocab * 4)) ||
       (rc = alloc_zero((void**)&m->cand_val, (size_t)sms * 4)) ||
@@ -154,8 +151,8 @@ int cfb_llama_destroy(cfb_llama* m) {
   if (!m) return CFB_OK;
   if (m->exec) cudaGraphExecDestroy(m->exec);
   if (m->graph) cudaGraphDestroy(m->graph);
-  void* bufs[] = {m->resid[0], m->resid[1], m->act,      m->out_partial, m->tickets, m->barrier,
-                  m->logits,   m->cand_val, m->cand_idx, m->lm_ticket,   m->token,   m->pos};
+  void* bufs[] = {m->resid,  m->accum,    m->act,      m->barrier, m->logits,
+                  m->cand_val, m->cand_idx, m->lm_ticket, m->token,   m->pos};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -218,7 +215,7 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
   if (logits) *logits = m->logits;
   if (token) *token = m->token;
   if (pos) *pos = m->pos;
-  if (resid) *resid = m->resid[0];
+  if (resid) *resid = m->resid;
   return CFB_OK;
 }
 

@@ -57,11 +57,13 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   __syncthreads();
   const Phase P0 = make_phase(static_cast<const T*>(p.w) + (size_t)t0 * kTileRows * D, nullptr,
                               t1 - t0, kTileRows * D * tb, true);
+  pdl_launch_dependents();
   if (warp == kNumConsumerWarps) {
     const Phase ph[1] = {P0};
     produce_all(ph, ring, lane, policy_evict_first());
     return;
   }
+  pdl_wait();
   rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   float bv[QB];
   int bi[QB];
@@ -139,6 +141,8 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
 
 template <typename T>
 __global__ void embed_kernel(const T* table, const int* tokens, float* out, int B, int D) {
+  pdl_launch_dependents();
+  pdl_wait();
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < B * D; idx += gridDim.x * blockDim.x) {
     const int b = idx / D, d = idx % D;
     out[idx] = Elem<T>::to_f(table[(size_t)tokens[b] * D + d]);
@@ -153,8 +157,15 @@ static int launch_lm_inst(const LmParams& p, int grid, size_t smem, cudaStream_t
     CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
     configured = true;
   }
-  kern<<<grid, kThreads, smem, st>>>(p);
-  CFB_CUDA(cudaGetLastError());
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  LaunchAttrs at(0, p.flags & CFB_PDL);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return CFB_OK;
 }
 
@@ -186,7 +197,7 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   p.B = a->batch;
   p.D = a->hidden;
   p.V = a->vocab;
-  p.flags = 0;
+  p.flags = a->flags;
   p.spw = spw;
   p.eps = a->eps;
   p.resid = a->resid;
@@ -207,14 +218,22 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
 }
 
 int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
-          cudaStream_t st) {
+          cudaStream_t st, bool pdl) {
   if (!table || !tokens || !out) return set_error(CFB_ERR_ARGUMENT, "null pointer");
   const int threads = 256, blocks = (B * D + threads - 1) / threads;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.stream = st;
+  LaunchAttrs at(0, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
   if (dtype == CFB_F16)
-    embed_kernel<__half><<<blocks, threads, 0, st>>>(static_cast<const __half*>(table), tokens, out, B, D);
+    CFB_CUDA(cudaLaunchKernelEx(&cfg, embed_kernel<__half>, static_cast<const __half*>(table), tokens,
+                                out, B, D));
   else
-    embed_kernel<float><<<blocks, threads, 0, st>>>(static_cast<const float*>(table), tokens, out, B, D);
-  CFB_CUDA(cudaGetLastError());
+    CFB_CUDA(cudaLaunchKernelEx(&cfg, embed_kernel<float>, static_cast<const float*>(table), tokens,
+                                out, B, D));
   return CFB_OK;
 }
 

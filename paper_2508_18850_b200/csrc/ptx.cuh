@@ -137,6 +137,14 @@ __device__ __forceinline__ void pdl_launch_dependents() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
+// fixed-point (2^-32) encoding of the cross-head accumulator
+__device__ __forceinline__ void red_add_fixed(unsigned long long* p, float v) {
+  atomicAdd(p, static_cast<unsigned long long>(__float2ll_rn(v * 4294967296.0f)));
+}
+__device__ __forceinline__ float fixed_to_float(unsigned long long v) {
+  return __ll2float_rn(static_cast<long long>(v)) * 2.3283064365386963e-10f;  // 2^-32
+}
+
 // ---------------------------------------------------------------- numerics
 template <typename T>
 struct Elem;

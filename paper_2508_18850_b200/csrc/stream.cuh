@@ -126,15 +126,17 @@ __device__ __forceinline__ void issue_item(const Phase& p, const Item& it, const
 }
 
 // Producer warp: lane w < kNumConsumerWarps feeds consumer warp w through
-// its sub-ring, walking the phases in order.  The loop is warp-uniform and
+// its sub-ring, walking the phases in order.  `c` (per lane) counts the
+// items issued so far, so a schedule may be produced in several calls (e.g.
+// weights first, then - after a PDL wait - activation-dependent KV rows).  The loop is warp-uniform and
 // only probes slots with the non-blocking test_wait, so one lane waiting for
 // a busy slot never stalls the others (a blocking try_wait in divergent
 // lanes would serialise the warp).
 template <int NP>
 __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r, int lane,
-                                            uint64_t policy) {
+                                            uint64_t policy, int& c) {
   const int w = lane;
-  int ph = 0, j = 0, c = 0;
+  int ph = 0, j = 0;
   bool done = w >= kNumConsumerWarps;
   while (true) {
     bool issued = false;
@@ -158,6 +160,12 @@ __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r,
     if (__all_sync(0xffffffffu, done)) break;
     if (!__any_sync(0xffffffffu, issued)) __nanosleep(32);
   }
+}
+template <int NP>
+__device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r, int lane,
+                                            uint64_t policy) {
+  int c = 0;
+  produce_all(P, r, lane, policy, c);
 }
 
 // Consumer side: warp `w` walks its items; f(item, slot_ptr) runs warp-wide.

@@ -141,26 +141,26 @@ def test_library_exports_every_declared_symbol():
     assert L.cfb_version().startswith(b"cfb")
 
 
-def test_abi_struct_layout_matches_header():
-    """ctypes mirror must have the field order of cfb_mha_args."""
-    text = (ROOT / "include" / "cfb.h").read_text()
-    body = text.split("typedef struct cfb_mha_args {")[1].split("} cfb_mha_args;")[0]
+def _struct_fields(text, name):
+    body = text.split(f"typedef struct {name} {{")[1].split(f"}} {name};")[0]
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     names = []
     for decl in body.split(";"):
         decl = decl.strip()
         if not decl:
             continue
-        parts = decl.replace("*", " ").split()
-        # "int batch, hidden" -> several names
-        tail = decl.split(None, 1)[1] if not decl.startswith("const") else decl.split(None, 2)[2]
-        for nm in tail.replace("*", " ").split(","):
+        # "int batch, hidden" -> several names; drop the type words
+        words = decl.replace("*", " ").replace(",", " , ").split()
+        while words and words[0] in ("const", "unsigned", "long", "int", "float", "void", "char"):
+            words.pop(0)
+        for nm in " ".join(words).split(","):
             names.append(nm.strip().split()[-1])
-        del parts
-    assert names == [f[0] for f in _native.MhaArgs._fields_]
+    return names
 
 
-def test_ticket_count_is_host_computable():
-    L = _native.lib()
-    assert L.cfb_mha_ticket_count(4096, 128, 4, 2) == 4 * (1024 // 32)
-    assert ctypes.sizeof(_native.MhaArgs) > 0
+@pytest.mark.parametrize("cname,pyname", [("cfb_mha_args", "MhaArgs"), ("cfb_ffn_args", "FfnArgs"),
+                                          ("cfb_lm_args", "LmArgs")])
+def test_abi_struct_layout_matches_header(cname, pyname):
+    """ctypes mirrors must have the field order of the C structs."""
+    text = (ROOT / "include" / "cfb.h").read_text()
+    assert _struct_fields(text, cname) == [f[0] for f in getattr(_native, pyname)._fields_]

@@ -19,7 +19,9 @@ ap.add_argument("--ctx", type=int, default=1024)
 ap.add_argument("--reps", type=int, default=64)
 ap.add_argument("--layers", type=int, default=16)
 ap.add_argument("--cluster", type=int, default=4)
+ap.add_argument("--no-pdl", action="store_true")
 a = ap.parse_args()
+a.pdl = 0 if a.no_pdl else _native.PDL
 dev = torch.device("cuda")
 D, F, nh, H, N = 4096, 11008, 32, 128, a.cluster
 L = _native.lib()
@@ -38,14 +40,14 @@ resid = torch.randn(1, D, device=dev)
 out = torch.empty(1, D, device=dev)
 act = torch.empty(F, device=dev, dtype=torch.float16)
 bar = torch.zeros(1, device=dev, dtype=torch.int64)
-part = torch.empty(nh, 1, D, device=dev)
-tick = torch.zeros(4096, device=dev, dtype=torch.int32)
+accum = torch.zeros(1, D, device=dev, dtype=torch.int64)
 pos = torch.tensor([a.ctx], device=dev, dtype=torch.int32)
 torch.cuda.synchronize()
 
 
 def ffn(l):
-    return _native.FfnArgs(dtype=2, batch=1, hidden=D, inter=F, flags=_native.NORM | _native.RESID,
+    return _native.FfnArgs(dtype=2, batch=1, hidden=D, inter=F,
+                           flags=_native.NORM | _native.RESID | a.pdl, accum=accum.data_ptr(),
                            grid=0, eps=1e-5, resid=resid.data_ptr(), norm_w=l["g"].data_ptr(),
                            w_gu=l["w_gu"].data_ptr(), w_dn=l["w_dn"].data_ptr(), act=act.data_ptr(),
                            out=out.data_ptr(), barrier=bar.data_ptr())
@@ -54,11 +56,11 @@ def ffn(l):
 def mha(l):
     return _native.MhaArgs(dtype=2, batch=1, hidden=D, n_heads=nh, head_dim=H, head_pad=H, cluster=N,
                            seq_len=a.ctx, cache_cap=a.ctx + 8,
-                           flags=_native.APPEND | _native.NORM | _native.RESID, resid=resid.data_ptr(),
+                           flags=_native.APPEND | _native.NORM | _native.STATS_MERGED | a.pdl,
+                           resid=resid.data_ptr(),
                            norm_w=l["g"].data_ptr(), eps=1e-5, w_qkv=l["w_qkv"].data_ptr(),
                            w_out=l["w_out"].data_ptr(), k_cache=l["kc"].data_ptr(),
-                           v_cache=l["vc"].data_ptr(), out=out.data_ptr(), out_partial=part.data_ptr(),
-                           tickets=tick.data_ptr())
+                           v_cache=l["vc"].data_ptr(), out=None, accum=accum.data_ptr())
 
 
 def timeit(fn, args, nbytes):
