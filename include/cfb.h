@@ -48,8 +48,11 @@ enum cfb_flags {
   CFB_NORM = 1 << 3,         /* x = f16(rmsnorm(resid) * norm_w) instead of reading x */
   CFB_RESID = 1 << 4,        /* out = resid + sum_heads(...) (residual add in the epilogue) */
   CFB_STATS_MERGED = 1 << 5, /* stats_mode="merged": one SOFTMAX_MERGE pair reduce */
-  CFB_PDL = 1 << 6           /* programmatic dependent launch: the kernel may start while its
+  CFB_PDL = 1 << 6,          /* programmatic dependent launch: the kernel may start while its
                                 stream predecessor finishes (weights stream before the wait) */
+  CFB_ONESHOT = 1 << 7       /* latency-optimal cluster exchange (decode engine): one-round
+                                all-to-all DSMEM gather, and ONE fused softmax-merge reduce of
+                                fp32 (m, l, A) in place of the stats + attn_out reduces */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
@@ -111,7 +114,7 @@ typedef struct cfb_mha_args {
   unsigned long long* accum;
   float* stats;
   unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
-  unsigned long long* trace;   /* [grid CTAs][8] %globaltimer phase stamps (profiling), or NULL */
+  unsigned long long* trace;   /* [grid CTAs][16] %globaltimer phase stamps (profiling), or NULL */
 } cfb_mha_args;
 
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);

@@ -52,13 +52,14 @@ struct MhaParams {
 };
 
 struct MhaLayout {
-  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, misc, total;
-  int seg_bytes, a_bytes, st_bytes;
+  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, pay, total;
+  int seg_bytes, a_bytes, st_bytes, pay_bytes;
 };
 
 __host__ __device__ inline int round16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int tb, int spw) {
+__host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int tb, int spw,
+                                                bool oneshot) {
   MhaLayout L;
   const int h = Hp / N;
   int rounds = 0;
@@ -66,6 +67,7 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.seg_bytes = round16(B * 3 * h * tb);
   L.a_bytes = round16(B * Hp * tb);
   L.st_bytes = round16(2 * B * tb);
+  L.pay_bytes = oneshot ? round16((2 * B + B * Hp) * 4) : 0;  // fp32 [m | l | A]
   int o = ring_bytes(spw);
   L.bars = o;       o += (2 * kNumSlots + 16) * 8;
   L.x = o;          o += round16(B * D * 4);  // fp32, tile-GEMV layout
@@ -81,7 +83,7 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.st = o;         o += 2 * L.st_bytes;
   L.strx = o;       o += 8 * L.st_bytes;
   L.red = o;        o += round16(kNumConsumerWarps * B * 4);
-  L.misc = o;       o += 16;
+  L.pay = o;        o += N * L.pay_bytes;
   L.total = o;
   return L;
 }
@@ -98,7 +100,8 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   const int B = p.B, D = p.D, Hp = p.Hp;
   const uint32_t N = p.N;
   const int h = Hp / N;
-  const MhaLayout L = mha_layout(B, D, Hp, N, tb, p.spw);
+  const bool oneshot = p.flags & CFB_ONESHOT;
+  const MhaLayout L = mha_layout(B, D, Hp, N, tb, p.spw, oneshot);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw};
   uint64_t* cbar = bars + 2 * kNumSlots;  // [0,4) gather, [4,8) max/merge, [8,12) sum, [12,16) attn
@@ -109,7 +112,14 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   while ((1u << rounds) < N) ++rounds;
   const bool merged = p.flags & CFB_STATS_MERGED;
 
-  if (tid == 0) {
+  if (tid == 0 && oneshot) {
+    ring_init(ring);
+    mbar_init(&cbar[0], 1);
+    mbar_arrive_expect_tx(&cbar[0], (N - 1) * L.seg_bytes);
+    mbar_init(&cbar[4], 1);
+    mbar_arrive_expect_tx(&cbar[4], (N - 1) * L.pay_bytes);
+    fence_mbar_init();
+  } else if (tid == 0) {
     ring_init(ring);
     for (int r = 0; r < rounds; ++r) {
       mbar_init(&cbar[r], 1);
@@ -161,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // ---------------------------------------------------------------- consumers
   unsigned long long* tr =
-      p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 8 : nullptr;
+      p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer();
   float* xs = reinterpret_cast<float*>(smem + L.x);
   float* part = reinterpret_cast<float*>(smem + L.part);
@@ -200,10 +210,22 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   consumer_sync();
   if (tr && tid == 0) tr[2] = globaltimer();
   cluster_wait();  // peers' mbarriers are initialised from here on
+  if (tr && tid == 0) tr[8] = globaltimer();
 
   // 3. ClusterGather of the qkv slices
   const int seg_elems = L.seg_bytes / tb;
-  if (warp == 0 && N > 1) {
+  if (warp == 0 && N > 1 && oneshot) {
+    // one round: push the local segment into slot (peer - rank) mod N of every
+    // peer (the same rank-rotated layout the log2(N)-round schedule leaves)
+    for (uint32_t d = 1; d < N; ++d) {
+      const uint32_t peer = (rank + d) % N;
+      dsmem_push(gseg, reinterpret_cast<char*>(gseg) + d * L.seg_bytes, &cbar[0], L.seg_bytes, peer,
+                 lane);
+    }
+    sent[0] += (unsigned long long)(N - 1) * B * 3 * (p.H / N) * tb;
+    __syncwarp();
+    mbar_wait(&cbar[0], 0);
+  } else if (warp == 0 && N > 1) {
     uint64_t* gb[4] = {&cbar[0], &cbar[1], &cbar[2], &cbar[3]};
     warp_cluster_gather(reinterpret_cast<char*>(gseg), L.seg_bytes, gb, rank, N, lane);
     for (uint32_t s = 1; s < N; s <<= 1) sent[0] += (unsigned long long)s * B * 3 * (p.H / N) * tb;
@@ -314,12 +336,14 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
       }
     }
   };
+  if (tr && tid == 0) tr[11] = globaltimer();
   consume_phase(P1, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
     const T* K = reinterpret_cast<const T*>(slot);
     const T* V = reinterpret_cast<const T*>(slot + kSlotBytes / 2);
     attend([&](int k, float* o) { load_elems<T, EPL>(K + k * Hp + li * EPL, o); },
            [&](int k, float* o) { load_elems<T, EPL>(V + k * Hp + li * EPL, o); }, it.nunits);
   });
+  if (tr && tid == 0) tr[12] = globaltimer();
   if ((p.flags & CFB_APPEND) && rank == N - 1 && warp == 0) {  // new token(s): counted once
     attend([&](int k, float* o) {
              for (int e = 0; e < EPL; ++e) o[e] = kf[k * Hp + li * EPL + e];
@@ -350,6 +374,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     }
   }
   consumer_sync();
+  if (tr && tid == 0) tr[13] = globaltimer();
   // merge the 8 warp states in warp order -> (A_loc, m_loc, l_loc)
   if (tid < B) {
     const int b = tid;
@@ -366,107 +391,169 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     l_loc[b] = ll;
   }
   consumer_sync();
-  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
-    const int b = idx / Hp;
-    float a = 0.f;
-    for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
-      a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
-    abuf[idx] = Elem<T>::from_f(a);  // block.store("attn_out", a_part)
-  }
-  for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
-    abuf[idx] = Elem<T>::from_f(0.f);
-
-  if (tr && tid == 0) tr[4] = globaltimer();
-  // 5. softmax statistics
-  T* st0 = reinterpret_cast<T*>(smem + L.st);
-  T* st1 = reinterpret_cast<T*>(smem + L.st + L.st_bytes);
-  if (warp == 0) {
-    T* rx[4];
-    uint64_t* rb[4];
-    for (int i = lane; i < L.st_bytes / tb; i += 32) {
-      st0[i] = Elem<T>::from_f(0.f);
-      st1[i] = Elem<T>::from_f(0.f);
+  if (oneshot) {
+    // Fused statistics + attention-output exchange in ONE round: every CTA
+    // pushes its fp32 partial state (m_loc, l_loc, unnormalised A_loc) into
+    // slot `rank` of every peer, then all CTAs merge the N states in rank
+    // order (identical, deterministic result everywhere):
+    //   m* = max_r m_r,  l* = sum_r l_r e^{m_r - m*},  A* = sum_r A_r e^{m_r - m*} / l*
+    // = the reference's MAX-reduce / rescale / SUM-reduce / rescale / SUM-reduce
+    // sequence (dataflows.py:187-232, :297-300) with all partial stores in fp32.
+    const int pw = L.pay_bytes / 4;
+    float* pay = reinterpret_cast<float*>(smem + L.pay);
+    float* mine = pay + rank * pw;
+    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+      const int b = idx / Hp;
+      float a = 0.f;
+      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
+        a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
+      mine[2 * B + idx] = a;
     }
-    __syncwarp();
-    if (merged) {
-      for (int b = lane; b < B; b += 32) {
-        st0[b] = Elem<T>::from_f(m_loc[b]);
-        st0[B + b] = Elem<T>::from_f(l_loc[b]);
+    if (tid < B) {
+      mine[tid] = m_loc[tid];
+      mine[B + tid] = l_loc[tid];
+    }
+    consumer_sync();
+    if (tr && tid == 0) tr[4] = globaltimer();
+    if (warp == 0 && N > 1) {
+      for (uint32_t d = 1; d < N; ++d)
+        dsmem_push(mine, mine, &cbar[4], L.pay_bytes, (rank + d) % N, lane);
+      sent[4] += (unsigned long long)(N - 1) * (2 * B + B * p.H) * 4;
+    }
+    if (tr && tid == 0) tr[9] = globaltimer();
+    if (N > 1) mbar_wait(&cbar[4], 0);
+    if (tr && tid == 0) tr[10] = globaltimer();
+    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+      const int b = idx / Hp;
+      float ms = -INFINITY;
+      for (uint32_t r = 0; r < N; ++r) ms = fmaxf(ms, pay[r * pw + b]);
+      float ls = 0.f, a = 0.f;
+      for (uint32_t r = 0; r < N; ++r) {
+        const float mr = pay[r * pw + b];
+        const float f = (mr == -INFINITY) ? 0.f : expf(mr - ms);
+        ls = fmaf(pay[r * pw + B + b], f, ls);
+        a = fmaf(pay[r * pw + 2 * B + idx], f, a);
       }
-      __syncwarp();
-      for (int r = 0; r < 4; ++r) {
-        rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
-        rb[r] = &cbar[4 + r];
-      }
-      warp_cluster_reduce<T>(st0, 2 * B, L.st_bytes, rx, rb, kSoftmaxMerge, rank, N, lane);
-      for (int r = 0; r < rounds; ++r) sent[3] += 2ull * B * tb;
-      for (int b = lane; b < B; b += 32) {
-        m_st[b] = Elem<T>::to_f(st0[b]);
-        l_st[b] = Elem<T>::to_f(st0[B + b]);
-      }
-    } else {
-      for (int b = lane; b < B; b += 32) st0[b] = Elem<T>::from_f(m_loc[b]);
-      __syncwarp();
-      for (int r = 0; r < 4; ++r) {
-        rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
-        rb[r] = &cbar[4 + r];
-      }
-      warp_cluster_reduce<T>(st0, B, L.st_bytes, rx, rb, kMax, rank, N, lane);
-      for (int b = lane; b < B; b += 32) {
-        const float ms = Elem<T>::to_f(st0[b]);
+      abuf[idx] = Elem<T>::from_f(__fdiv_rn(a, ls));
+      if (idx % Hp == 0) {
         m_st[b] = ms;
-        const float f = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - ms);
-        st1[b] = Elem<T>::from_f(__fmul_rn(l_loc[b], f));
+        l_st[b] = ls;
+      }
+    }
+    consumer_sync();
+    if (warp == 0) {
+      if (rank == 0 && p.stats)
+        for (int b = lane; b < B; b += 32) {
+          p.stats[((size_t)head * 2) * B + b] = m_st[b];
+          p.stats[((size_t)head * 2 + 1) * B + b] = l_st[b];
+        }
+      if (lane == 0 && p.traffic) {
+        atomicAdd(&p.traffic[0], sent[0]);
+        atomicAdd(&p.traffic[4], sent[4]);
+      }
+    }
+  } else {
+    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+      const int b = idx / Hp;
+      float a = 0.f;
+      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
+        a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
+      abuf[idx] = Elem<T>::from_f(a);  // block.store("attn_out", a_part)
+    }
+    for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
+      abuf[idx] = Elem<T>::from_f(0.f);
+
+    if (tr && tid == 0) tr[4] = globaltimer();
+    // 5. softmax statistics
+    T* st0 = reinterpret_cast<T*>(smem + L.st);
+    T* st1 = reinterpret_cast<T*>(smem + L.st + L.st_bytes);
+    if (warp == 0) {
+      T* rx[4];
+      uint64_t* rb[4];
+      for (int i = lane; i < L.st_bytes / tb; i += 32) {
+        st0[i] = Elem<T>::from_f(0.f);
+        st1[i] = Elem<T>::from_f(0.f);
       }
       __syncwarp();
-      for (int r = 0; r < 4; ++r) {
-        rx[r] = reinterpret_cast<T*>(smem + L.strx + (4 + r) * L.st_bytes);
-        rb[r] = &cbar[8 + r];
-      }
-      warp_cluster_reduce<T>(st1, B, L.st_bytes, rx, rb, kSum, rank, N, lane);
-      for (int b = lane; b < B; b += 32) l_st[b] = Elem<T>::to_f(st1[b]);
-      for (int r = 0; r < rounds; ++r) {
-        sent[1] += (unsigned long long)B * tb;
-        sent[2] += (unsigned long long)B * tb;
-      }
-    }
-  }
-  consumer_sync();
-  // 6. rescale and reduce the attention output
-  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
-    const int b = idx / Hp;
-    const float e = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - m_st[b]);
-    const float f = __fdiv_rn(e, l_st[b]);
-    abuf[idx] = Elem<T>::from_f(__fmul_rn(Elem<T>::to_f(abuf[idx]), f));
-  }
-  consumer_sync();
-  if (warp == 0) {
-    T* rx[4];
-    uint64_t* rb[4];
-    for (int r = 0; r < 4; ++r) {
-      rx[r] = reinterpret_cast<T*>(smem + L.arx + r * L.a_bytes);
-      rb[r] = &cbar[12 + r];
-    }
-    warp_cluster_reduce<T>(abuf, B * Hp, L.a_bytes, rx, rb, kSum, rank, N, lane);
-    for (int r = 0; r < rounds; ++r) sent[4] += (unsigned long long)B * p.H * tb;
-    if (rank == 0 && p.stats)
-      for (int b = lane; b < B; b += 32) {
-        p.stats[((size_t)head * 2) * B + b] = m_st[b];
-        p.stats[((size_t)head * 2 + 1) * B + b] = l_st[b];
-      }
-    if (lane == 0 && p.traffic) {
-      atomicAdd(&p.traffic[0], sent[0]);
       if (merged) {
-        atomicAdd(&p.traffic[3], sent[3]);
+        for (int b = lane; b < B; b += 32) {
+          st0[b] = Elem<T>::from_f(m_loc[b]);
+          st0[B + b] = Elem<T>::from_f(l_loc[b]);
+        }
+        __syncwarp();
+        for (int r = 0; r < 4; ++r) {
+          rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
+          rb[r] = &cbar[4 + r];
+        }
+        warp_cluster_reduce<T>(st0, 2 * B, L.st_bytes, rx, rb, kSoftmaxMerge, rank, N, lane);
+        for (int r = 0; r < rounds; ++r) sent[3] += 2ull * B * tb;
+        for (int b = lane; b < B; b += 32) {
+          m_st[b] = Elem<T>::to_f(st0[b]);
+          l_st[b] = Elem<T>::to_f(st0[B + b]);
+        }
       } else {
-        atomicAdd(&p.traffic[1], sent[1]);
-        atomicAdd(&p.traffic[2], sent[2]);
+        for (int b = lane; b < B; b += 32) st0[b] = Elem<T>::from_f(m_loc[b]);
+        __syncwarp();
+        for (int r = 0; r < 4; ++r) {
+          rx[r] = reinterpret_cast<T*>(smem + L.strx + r * L.st_bytes);
+          rb[r] = &cbar[4 + r];
+        }
+        warp_cluster_reduce<T>(st0, B, L.st_bytes, rx, rb, kMax, rank, N, lane);
+        for (int b = lane; b < B; b += 32) {
+          const float ms = Elem<T>::to_f(st0[b]);
+          m_st[b] = ms;
+          const float f = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - ms);
+          st1[b] = Elem<T>::from_f(__fmul_rn(l_loc[b], f));
+        }
+        __syncwarp();
+        for (int r = 0; r < 4; ++r) {
+          rx[r] = reinterpret_cast<T*>(smem + L.strx + (4 + r) * L.st_bytes);
+          rb[r] = &cbar[8 + r];
+        }
+        warp_cluster_reduce<T>(st1, B, L.st_bytes, rx, rb, kSum, rank, N, lane);
+        for (int b = lane; b < B; b += 32) l_st[b] = Elem<T>::to_f(st1[b]);
+        for (int r = 0; r < rounds; ++r) {
+          sent[1] += (unsigned long long)B * tb;
+          sent[2] += (unsigned long long)B * tb;
+        }
       }
-      atomicAdd(&p.traffic[4], sent[4]);
     }
+    consumer_sync();
+    // 6. rescale and reduce the attention output
+    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+      const int b = idx / Hp;
+      const float e = (m_loc[b] == -INFINITY) ? 0.f : expf(m_loc[b] - m_st[b]);
+      const float f = __fdiv_rn(e, l_st[b]);
+      abuf[idx] = Elem<T>::from_f(__fmul_rn(Elem<T>::to_f(abuf[idx]), f));
+    }
+    consumer_sync();
+    if (warp == 0) {
+      T* rx[4];
+      uint64_t* rb[4];
+      for (int r = 0; r < 4; ++r) {
+        rx[r] = reinterpret_cast<T*>(smem + L.arx + r * L.a_bytes);
+        rb[r] = &cbar[12 + r];
+      }
+      warp_cluster_reduce<T>(abuf, B * Hp, L.a_bytes, rx, rb, kSum, rank, N, lane);
+      for (int r = 0; r < rounds; ++r) sent[4] += (unsigned long long)B * p.H * tb;
+      if (rank == 0 && p.stats)
+        for (int b = lane; b < B; b += 32) {
+          p.stats[((size_t)head * 2) * B + b] = m_st[b];
+          p.stats[((size_t)head * 2 + 1) * B + b] = l_st[b];
+        }
+      if (lane == 0 && p.traffic) {
+        atomicAdd(&p.traffic[0], sent[0]);
+        if (merged) {
+          atomicAdd(&p.traffic[3], sent[3]);
+        } else {
+          atomicAdd(&p.traffic[1], sent[1]);
+          atomicAdd(&p.traffic[2], sent[2]);
+        }
+        atomicAdd(&p.traffic[4], sent[4]);
+      }
+    }
+    consumer_sync();
   }
-  consumer_sync();
-
   if (tr && tid == 0) tr[5] = globaltimer();
   // 7. O-projection over this rank's output columns, RO rows per chunk, and
   // 8. the cross-head sum into the fixed-point accumulator
@@ -595,8 +682,9 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->accum)
     return set_error(CFB_ERR_ARGUMENT, "null weight / cache / accumulator pointer");
   int spw = tuned_spw();
-  MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb, spw);
-  while (L.total > kMaxSmem && spw > 1) L = mha_layout(a->batch, a->hidden, Hp, N, tb, --spw);
+  const bool oneshot = a->flags & CFB_ONESHOT;
+  MhaLayout L = mha_layout(a->batch, a->hidden, Hp, N, tb, spw, oneshot);
+  while (L.total > kMaxSmem && spw > 1) L = mha_layout(a->batch, a->hidden, Hp, N, tb, --spw, oneshot);
   if (L.total > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "split_token schedule needs %d B of shared memory per CTA (max %d)",
                      L.total, kMaxSmem);

@@ -53,7 +53,7 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
     a.head_pad = c.head_dim;
     a.cluster = c.cluster;
     a.cache_cap = c.cache_cap;
-    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_STATS_MERGED | CFB_PDL;
+    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_ONESHOT | CFB_PDL;
     a.resid = m->resid;
     a.norm_w = m->attn_norm[l];
     a.eps = c.eps;

@@ -24,13 +24,17 @@ import numpy as np
 
 from . import _native
 from .exceptions import DimensionError, SimulationError
-from .ledger import GLOBAL, StageTrace, TrafficLedger, emit_gather, emit_reduce
+from .ledger import (GLOBAL, ONESHOT_MERGE, StageTrace, TrafficLedger, emit_gather, emit_oneshot,
+                     emit_reduce)
 from .layouts import gate_up_tiles, qkv_tiles, row_tiles
 from .scenario import MHA, MLA, validate_scenario
 
 SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD = "split_token", "fused_mla", "split_head"
 DATAFLOW_KINDS = (SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD)
-TWO_PASS, MERGED = "two_pass", "merged"
+# "oneshot" extends the reference's stats modes (dataflows.py:187-227): the
+# decode engine's single-round all-to-all gather + one fused fp32 (m, l, A)
+# softmax-merge in place of the stats and attn_out reduces (CFB_ONESHOT).
+TWO_PASS, MERGED, ONESHOT = "two_pass", "merged", "oneshot"
 
 
 @dataclass
@@ -111,7 +115,7 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
 
     validate_partitioning(scenario, SPLIT_TOKEN, append_new_token)
     validate_scenario(scenario)
-    if stats_mode not in (TWO_PASS, MERGED):
+    if stats_mode not in (TWO_PASS, MERGED, ONESHOT):
         raise ValueError(f"unknown stats_mode {stats_mode!r}")
     dev = _native.require_cuda()
     d = scenario.dims
@@ -143,8 +147,8 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
         accum = torch.zeros(B, Dp, device=dev, dtype=torch.int64)
         stats = torch.zeros(nh, 2, B, device=dev, dtype=torch.float32)
         traffic = torch.zeros(16, device=dev, dtype=torch.int64)
-        flags = (_native.APPEND if append_new_token else 0) | (
-            _native.STATS_MERGED if stats_mode == MERGED else 0)
+        flags = (_native.APPEND if append_new_token else 0) | {
+            TWO_PASS: 0, MERGED: _native.STATS_MERGED, ONESHOT: _native.ONESHOT}[stats_mode]
         args = _native.MhaArgs(
             dtype=nb, batch=B, hidden=Dp, n_heads=nh, head_dim=H, head_pad=Hp, cluster=n,
             seq_len=S, cache_cap=cap, flags=flags, x=x.data_ptr(), eps=0.0,
@@ -165,19 +169,29 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
                               else ["stats_max_reduce", "stats_sum_reduce"]) + ["attn_out_reduce"]
     h = H // n
     for head in range(nh):
-        tr = [("qkv_gather", emit_gather(ledger, n, B * 3 * h * nb))]
-        if stats_mode == MERGED:
+        if stats_mode == ONESHOT:
+            tr = [("qkv_gather", emit_oneshot(ledger, n, B * 3 * h * nb, "gather")),
+                  ("attn_state_merge", emit_oneshot(ledger, n, (2 * B + B * H) * 4, ONESHOT_MERGE))]
+        else:
+            tr = [("qkv_gather", emit_gather(ledger, n, B * 3 * h * nb))]
+        if stats_mode == ONESHOT:
+            pass  # statistics travel inside attn_state_merge
+        elif stats_mode == MERGED:
             tr.append(("stats_merge_reduce", emit_reduce(ledger, n, 2 * B * nb)))
         else:
             tr.append(("stats_max_reduce", emit_reduce(ledger, n, B * nb)))
             tr.append(("stats_sum_reduce", emit_reduce(ledger, n, B * nb)))
-        tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * H * nb)))
+        if stats_mode != ONESHOT:
+            tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * H * nb)))
         for stage, t in tr:
             stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
             traces.append(StageTrace(stage, head, t))
         _emit_global(ledger, n, B, D // n, nb)
-    device_traffic = {_native.STAGE_NAMES[i]: int(dev_traffic[i]) for i in range(5)
-                      if _native.STAGE_NAMES[i] in names}
+    if stats_mode == ONESHOT:
+        device_traffic = {"qkv_gather": int(dev_traffic[0]), "attn_state_merge": int(dev_traffic[4])}
+    else:
+        device_traffic = {_native.STAGE_NAMES[i]: int(dev_traffic[i]) for i in range(5)
+                          if _native.STAGE_NAMES[i] in names}
     if device_traffic != stage_traffic:
         raise SimulationError(f"kernel DSMEM byte counters {device_traffic} disagree with the "
                               f"schedule {stage_traffic}")

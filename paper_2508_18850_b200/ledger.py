@@ -111,6 +111,21 @@ def emit_gather(ledger: TrafficLedger, n: int, seg: int) -> CollectiveTrace:
     return CollectiveTrace(GATHER, seg, rounds, total)
 
 
+def emit_oneshot(ledger: TrafficLedger, n: int, payload: int, primitive: str) -> CollectiveTrace:
+    """Events of one single-round all-to-all push (the decode engine's
+    latency-optimal ClusterGather / fused softmax-merge, CFB_ONESHOT): every
+    block sends its payload to each of the N-1 peers in round 0.  A gather
+    moves the same total bytes as the doubling schedule, N(N-1)*payload."""
+    log2_exact(n)
+    for b in range(n):
+        for d in range(1, n):
+            ledger.record(0, b, (b + d) % n, payload, DSMEM)
+    return CollectiveTrace(primitive, payload, 1 if n > 1 else 0, payload * (n - 1) * n)
+
+
+ONESHOT_MERGE = "oneshot_merge"
+
+
 @dataclass(frozen=True)
 class TrafficEntry:
     stage: str
@@ -155,7 +170,7 @@ class TrafficBreakdown:
 
 
 def _entry(stage, prim, payload, n, is_stats=False) -> TrafficEntry:
-    f = traffic_reduce if prim == REDUCE else traffic_gather
+    f = traffic_reduce if prim == REDUCE else traffic_gather  # one-shot merge: N(N-1)*payload
     return TrafficEntry(stage, prim, payload, f(payload, n), is_stats)
 
 
@@ -170,6 +185,13 @@ def dataflow_traffic(kind: str, dims, n_blocks: int, stats_mode: str = "two_pass
     if dims.head_dim % n_blocks:
         raise DimensionError(f"head_dim {dims.head_dim} not divisible by {n_blocks}")
     h = dims.head_dim // n_blocks
+    if stats_mode == "oneshot":
+        if kind != "split_token":
+            raise DimensionError("stats_mode='oneshot' is implemented for split_token")
+        h = dims.head_dim // n_blocks
+        return TrafficBreakdown(kind, n_blocks, dims.n_heads, [
+            _entry("qkv_gather", GATHER, B * 3 * h * nb, n_blocks),
+            _entry("attn_state_merge", ONESHOT_MERGE, (2 * B + B * dims.head_dim) * 4, n_blocks)])
     if stats_mode == "merged":
         stats = [_entry("stats_merge_reduce", REDUCE, 2 * B * nb, n_blocks, True)]
     else:

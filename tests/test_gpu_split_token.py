@@ -236,3 +236,23 @@ def test_kernel_domain_errors():
     dims = cfb.ModelDims(1, 8, 1, 6, 2)
     with pytest.raises(cfb.DimensionError):
         cfb.run_fused_mha_decode(cfb.random_mha_scenario(dims, n_blocks=4, seed=0))
+
+
+@pytest.mark.parametrize("n", [1, 2, 4, 8, 16])
+def test_oneshot_exchange_matches_reference_schedule(n):
+    """The engine's one-round DSMEM exchange (CFB_ONESHOT) computes the same
+    module output and statistics as the reference's log2(N)-round schedule,
+    and its device byte counters match its own ledger."""
+    for dtype_bytes, tol in ((4, 1e-5), (2, 2e-3)):
+        dims = cfb.ModelDims(1, 512, 4, 128, 333, dtype_bytes=dtype_bytes)
+        sc = cfb.random_mha_scenario(dims, n_blocks=n, seed=40 + n)
+        ref = cfb.run_fused_mha_decode(sc, stats_mode="two_pass")
+        one = cfb.run_fused_mha_decode(sc, stats_mode="oneshot")
+        assert float(np.max(np.abs(one.output - ref.output))) <= tol
+        np.testing.assert_allclose(one.score_max, ref.score_max, atol=tol)
+        np.testing.assert_allclose(one.score_sum, ref.score_sum, rtol=tol)
+        dense = cp.dense_mha(sc.hidden, sc.w_qkv, sc.w_out, sc.k_cache, sc.v_cache)
+        assert float(np.max(np.abs(one.output - dense))) <= (1e-5 if dtype_bytes == 4 else 2e-2)
+        bd = cfb.reconcile_traffic("split_token", one, sc.dims, "oneshot")
+        assert bd.reconciled
+        assert one.device_traffic == one.stage_traffic

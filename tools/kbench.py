@@ -20,8 +20,10 @@ ap.add_argument("--reps", type=int, default=64)
 ap.add_argument("--layers", type=int, default=16)
 ap.add_argument("--cluster", type=int, default=4)
 ap.add_argument("--no-pdl", action="store_true")
+ap.add_argument("--mode", default="oneshot", choices=["oneshot", "merged", "two_pass"])
 a = ap.parse_args()
 a.pdl = 0 if a.no_pdl else _native.PDL
+a.mode = {"oneshot": _native.ONESHOT, "merged": _native.STATS_MERGED, "two_pass": 0}[a.mode]
 dev = torch.device("cuda")
 D, F, nh, H, N = 4096, 11008, 32, 128, a.cluster
 L = _native.lib()
@@ -56,7 +58,7 @@ def ffn(l):
 def mha(l):
     return _native.MhaArgs(dtype=2, batch=1, hidden=D, n_heads=nh, head_dim=H, head_pad=H, cluster=N,
                            seq_len=a.ctx, cache_cap=a.ctx + 8,
-                           flags=_native.APPEND | _native.NORM | _native.STATS_MERGED | a.pdl,
+                           flags=_native.APPEND | _native.NORM | a.mode | a.pdl,
                            resid=resid.data_ptr(),
                            norm_w=l["g"].data_ptr(), eps=1e-5, w_qkv=l["w_qkv"].data_ptr(),
                            w_out=l["w_out"].data_ptr(), k_cache=l["kc"].data_ptr(),
@@ -95,12 +97,16 @@ if "--trace" in sys.argv or True:
     print("ffn timeline us (min/median/max per stamp):",
           {n: (round((t[:, k].min() - t0) / 1e3, 2), round((np.median(t[:, k]) - t0) / 1e3, 2),
                round((t[:, k].max() - t0) / 1e3, 2)) for k, n in enumerate(names)})
-    tr.zero_()
+    tr = torch.zeros(256 * 16, device=dev, dtype=torch.int64)
     ma = mha(layers[0]); ma.trace = tr.data_ptr()
     _native.check(L.cfb_mha_decode(ma, sp)); torch.cuda.synchronize()
-    t = tr.view(256, 8).cpu().numpy()[:nh * N].astype(np.float64)
+    t = tr.view(256, 16).cpu().numpy()[:nh * N].astype(np.float64)
     t0 = t[:, 0].min()
-    names = ["start", "norm", "qkv", "gather", "attn", "stats", "oproj", "end"]
+    names = ["start", "norm", "qkv", "gather", "attn", "stats", "oproj", "end", "cwait", "push",
+             "xchg", "attn0", "kvdone", "newtok"]
     print("mha timeline us (min/median/max per stamp):",
           {n: (round((t[:, k].min() - t0) / 1e3, 2), round((np.median(t[:, k]) - t0) / 1e3, 2),
                round((t[:, k].max() - t0) / 1e3, 2)) for k, n in enumerate(names)})
+    import os
+    os.makedirs("gpurun_out", exist_ok=True)
+    np.save(f"gpurun_out/mha_trace_ctx{a.ctx}.npy", (t - t0) / 1e3)
