@@ -78,7 +78,10 @@ enum cfb_stage {
  *   resid    [B][D]                      fp32  (CFB_NORM / CFB_RESID)
  *   norm_w   [D]                         T
  *   w_qkv    [n_heads][N][3*Hp/N][D]     T     rank r's rows: q,k,v head-dim slices
- *   w_out    [n_heads][D][Hp]            T     (W_out[head])^T, rank r owns rows r*D/N..
+ *   w_out    [n_heads][N][D/N][Hp]       T     rank r's rows r*D/N.. of (W_out[head])^T,
+ *                                              each row chunk-rotated: logical 16-byte
+ *                                              chunk k of slice row g stored at chunk
+ *                                              (k + g) mod (Hp*T/16)
  *   k_cache, v_cache [n_heads][cache_cap][Hp] T
  *   rope_cs  [cache_cap][Hp/2][2]        fp32  (cos, sin)
  *   accum    [B][D]                      u64   cross-head sum in 64-bit fixed point

@@ -23,6 +23,14 @@ int tuned_spw() {
   }();
   return v;
 }
+int tuned_sleep() {
+  static int v = [] {
+    const char* e = getenv("CFB_SLEEP");
+    const int x = e ? atoi(e) : 32;
+    return x < 32 ? 32 : (x > 100000 ? 100000 : x);
+  }();
+  return v;
+}
 }  // namespace cfb
 
 extern "C" {

@@ -34,7 +34,7 @@
 namespace cfb {
 
 struct MhaParams {
-  int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags, spw;
+  int B, D, H, Hp, N, n_heads, S_static, cache_cap, flags, spw, sleep_max;
   float inv_sqrt_h, eps;
   const void* x;
   const float* resid;
@@ -52,7 +52,7 @@ struct MhaParams {
 };
 
 struct MhaLayout {
-  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, fw, abuf, arx, st, strx, red, pay, total;
+  int bars, x, part, gbuf, qf, ws_acc, ws_ml, loc, abuf, arx, st, strx, red, pay, total;
   int seg_bytes, a_bytes, st_bytes, pay_bytes;
 };
 
@@ -70,14 +70,13 @@ __host__ __device__ inline MhaLayout mha_layout(int B, int D, int Hp, int N, int
   L.pay_bytes = oneshot ? round16((2 * B + B * Hp) * 4) : 0;  // fp32 [m | l | A]
   int o = ring_bytes(spw);
   L.bars = o;       o += (2 * kNumSlots + 16) * 8;
-  L.x = o;          o += round16(B * D * 4);  // fp32, tile-GEMV layout
+  L.x = o;          o += round16(B * (D > Hp ? D : Hp) * 4);  // fp32, tile-GEMV layout
   L.part = o;       o += round16(kNumConsumerWarps * B * 3 * h * 4);
   L.gbuf = o;       o += N * L.seg_bytes;
   L.qf = o;         o += 3 * B * Hp * 4;
   L.ws_acc = o;     o += kNumConsumerWarps * B * Hp * 4;
   L.ws_ml = o;      o += kNumConsumerWarps * B * 2 * 4;
   L.loc = o;        o += round16(4 * B * 4);  // m_loc, l_loc, m_star, l_star
-  L.fw = o;         o += round16(kNumConsumerWarps * B * 4);
   L.abuf = o;       o += L.a_bytes;
   L.arx = o;        o += 4 * L.a_bytes;
   L.st = o;         o += 2 * L.st_bytes;
@@ -92,18 +91,18 @@ template <typename T, int EPL, int QB>
 __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaParams p) {
   extern __shared__ __align__(128) char smem[];
   constexpr int tb = sizeof(T);
-  // keys (rows) per online-softmax / O-proj chunk: a chunk's dot products,
+  constexpr bool XH = sizeof(T) == 2;  // GEMV activations as fp16 in smem (FHFMA path)
+  // keys per online-softmax chunk: a chunk's dot products,
   // shuffle reductions and exponentials are independent, which is the ILP
   // that hides shuffle/MUFU latency with only 8 consumer warps per SM
   constexpr int RC = QB == 1 ? 4 : (QB <= 4 ? 2 : 1);
-  constexpr int RO = QB == 1 ? 8 : (QB <= 4 ? 4 : 1);
   const int B = p.B, D = p.D, Hp = p.Hp;
   const uint32_t N = p.N;
   const int h = Hp / N;
   const bool oneshot = p.flags & CFB_ONESHOT;
   const MhaLayout L = mha_layout(B, D, Hp, N, tb, p.spw, oneshot);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   uint64_t* cbar = bars + 2 * kNumSlots;  // [0,4) gather, [4,8) max/merge, [8,12) sum, [12,16) attn
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
@@ -143,8 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
                                   ((size_t)head * N + rank) * qkv_tiles * kTileRows * D,
                               nullptr, qkv_tiles, kTileRows * D * tb, true);
   const int cols = D / (int)N;
-  const Phase P2 = make_phase(static_cast<const T*>(p.w_out) + (size_t)head * D * Hp +
-                                  (size_t)rank * cols * Hp,
+  const Phase P2 = make_phase(static_cast<const T*>(p.w_out) + ((size_t)head * N + rank) * cols * Hp,
                               nullptr, cols, Hp * tb);
   auto kv_phase = [&](int S) {
     const int seg = S == 0 ? 0 : (S + (int)N - 1) / (int)N;
@@ -173,7 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   unsigned long long* tr =
       p.trace ? p.trace + ((size_t)blockIdx.y * gridDim.x + blockIdx.x) * 16 : nullptr;
   if (tr && tid == 0) tr[0] = globaltimer();
-  float* xs = reinterpret_cast<float*>(smem + L.x);
+  XElem<XH>* xs = reinterpret_cast<XElem<XH>*>(smem + L.x);
   float* part = reinterpret_cast<float*>(smem + L.part);
   T* gseg = reinterpret_cast<T*>(smem + L.gbuf);
   float* qf = reinterpret_cast<float*>(smem + L.qf);
@@ -186,7 +184,6 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   float* l_loc = m_loc + B;
   float* m_st = l_loc + B;
   float* l_st = m_st + B;
-  float* fw = reinterpret_cast<float*>(smem + L.fw);
   T* abuf = reinterpret_cast<T*>(smem + L.abuf);
   float* red = reinterpret_cast<float*>(smem + L.red);
   unsigned long long sent[5] = {0, 0, 0, 0, 0};  // gather, max, sum, merge, attn
@@ -197,15 +194,15 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   // 1. activations
   if (p.flags & CFB_NORM) {
-    rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+    rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
-    load_act_to_smem<T>(xs, static_cast<const T*>(p.x), B, D, tid);
+    load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
   }
 
   // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
   if (tr && tid == 0) tr[1] = globaltimer();
   int cnt = 0;
-  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
+  tiled_gemv_phase<T, QB, XH>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
                           [&](int row, int b, float v) { gseg[b * 3 * h + row] = Elem<T>::from_f(v); });
   consumer_sync();
   if (tr && tid == 0) tr[2] = globaltimer();
@@ -375,21 +372,42 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   }
   consumer_sync();
   if (tr && tid == 0) tr[13] = globaltimer();
-  // merge the 8 warp states in warp order -> (A_loc, m_loc, l_loc)
-  if (tid < B) {
-    const int b = tid;
+  // merge the 8 warp states in warp order -> (A_loc, m_loc, l_loc); every
+  // thread recomputes the (cheap) per-warp factors of its batch row, so the
+  // merge is one parallel pass with no serial section
+  const int pw = L.pay_bytes / 4;
+  float* pay = reinterpret_cast<float*>(smem + L.pay);
+  float* mine = pay + rank * pw;  // oneshot: fp32 exchange payload [m | l | A]
+  for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
+    const int b = idx / Hp;
     float mm = -INFINITY;
+#pragma unroll
     for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) mm = fmaxf(mm, ws_m[w2 * B + b]);
-    float ll = 0.f;
+    float ll = 0.f, a = 0.f;
+#pragma unroll
     for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) {
       const float mw = ws_m[w2 * B + b];
       const float f = (mw == -INFINITY) ? 0.f : expf(mw - mm);
-      fw[w2 * B + b] = f;
       ll = fmaf(ws_l[w2 * B + b], f, ll);
+      a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], f, a);
     }
-    m_loc[b] = mm;
-    l_loc[b] = ll;
+    if (oneshot) {
+      mine[2 * B + idx] = a;
+    } else {
+      abuf[idx] = Elem<T>::from_f(a);  // block.store("attn_out", a_part)
+    }
+    if (idx % Hp == 0) {
+      m_loc[b] = mm;
+      l_loc[b] = ll;
+      if (oneshot) {
+        mine[b] = mm;
+        mine[B + b] = ll;
+      }
+    }
   }
+  if (!oneshot)
+    for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
+      abuf[idx] = Elem<T>::from_f(0.f);
   consumer_sync();
   if (oneshot) {
     // Fused statistics + attention-output exchange in ONE round: every CTA
@@ -399,21 +417,6 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     //   m* = max_r m_r,  l* = sum_r l_r e^{m_r - m*},  A* = sum_r A_r e^{m_r - m*} / l*
     // = the reference's MAX-reduce / rescale / SUM-reduce / rescale / SUM-reduce
     // sequence (dataflows.py:187-232, :297-300) with all partial stores in fp32.
-    const int pw = L.pay_bytes / 4;
-    float* pay = reinterpret_cast<float*>(smem + L.pay);
-    float* mine = pay + rank * pw;
-    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
-      const int b = idx / Hp;
-      float a = 0.f;
-      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
-        a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
-      mine[2 * B + idx] = a;
-    }
-    if (tid < B) {
-      mine[tid] = m_loc[tid];
-      mine[B + tid] = l_loc[tid];
-    }
-    consumer_sync();
     if (tr && tid == 0) tr[4] = globaltimer();
     if (warp == 0 && N > 1) {
       for (uint32_t d = 1; d < N; ++d)
@@ -453,15 +456,6 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
       }
     }
   } else {
-    for (int idx = tid; idx < B * Hp; idx += kConsumerThreads) {
-      const int b = idx / Hp;
-      float a = 0.f;
-      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
-        a = fmaf(ws_acc[(w2 * B + b) * Hp + idx % Hp], fw[w2 * B + b], a);
-      abuf[idx] = Elem<T>::from_f(a);  // block.store("attn_out", a_part)
-    }
-    for (int idx = B * Hp + tid; idx < L.a_bytes / tb; idx += kConsumerThreads)
-      abuf[idx] = Elem<T>::from_f(0.f);
 
     if (tr && tid == 0) tr[4] = globaltimer();
     // 5. softmax statistics
@@ -555,51 +549,26 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
     consumer_sync();
   }
   if (tr && tid == 0) tr[5] = globaltimer();
-  // 7. O-projection over this rank's output columns, RO rows per chunk, and
+  // 7. O-projection over this rank's output columns (row-tiled W_out^T slice,
+  //    the same conflict-free tile GEMV as the QKV phase, K = head_pad) and
   // 8. the cross-head sum into the fixed-point accumulator
-  float a[QB][EPL];
-#pragma unroll
-  for (int b = 0; b < QB; ++b)
-#pragma unroll
-    for (int e = 0; e < EPL; ++e) a[b][e] = (b < B) ? Elem<T>::to_f(abuf[b * Hp + li * EPL + e]) : 0.f;
   const int c_base = (int)rank * cols;
+  long long cyc_math = 0, nitems = 0;
   consume_phase(P2, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-    const T* W = reinterpret_cast<const T*>(slot);
-    for (int k0 = 0; k0 < it.nunits; k0 += RO * KPP) {
-      float s[RO][QB];
+    const long long c0 = clock64();
+    ++nitems;
+    rowlane_item<T, QB>(it, slot, abuf, Hp, B, lane, [&](int row, const float (&s)[QB]) {
 #pragma unroll
-      for (int j = 0; j < RO; ++j) {
-        const int row = k0 + j * KPP + g;
-        float w[EPL];
-        load_elems<T, EPL>(W + (row < it.nunits ? row : 0) * Hp + li * EPL, w);
-#pragma unroll
-        for (int b = 0; b < QB; ++b) {
-          float t = 0.f;
-#pragma unroll
-          for (int e = 0; e < EPL; ++e) t = fmaf(a[b][e], w[e], t);
-          s[j][b] = t;
-        }
-      }
-      for (int o = 1; o < LPK; o <<= 1) {
-#pragma unroll
-        for (int j = 0; j < RO; ++j)
-#pragma unroll
-          for (int b = 0; b < QB; ++b) s[j][b] += __shfl_xor_sync(0xffffffffu, s[j][b], o);
-      }
-      if (li == 0) {
-#pragma unroll
-        for (int j = 0; j < RO; ++j) {
-          const int row = k0 + j * KPP + g;
-          if (row < it.nunits) {
-#pragma unroll
-            for (int b = 0; b < QB; ++b)
-              if (b < B) red_add_fixed(&p.accum[(size_t)b * D + c_base + it.unit0 + row], s[j][b]);
-          }
-        }
-      }
-    }
+      for (int b = 0; b < QB; ++b)
+        if (b < B) red_add_fixed(&p.accum[(size_t)b * D + c_base + row], s[b]);
+    });
+    cyc_math += clock64() - c0;
   });
-  if (tr && tid == 0) tr[6] = globaltimer();
+  if (tr && tid == 0) {
+    tr[6] = globaltimer();
+    tr[14] = cyc_math;
+    tr[15] = nitems;
+  }
   cluster_arrive();
   cluster_wait();
   if (tr && tid == 0) tr[7] = globaltimer();
@@ -699,6 +668,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.cache_cap = a->cache_cap;
   p.flags = a->flags;
   p.spw = spw;
+  p.sleep_max = tuned_sleep();
   p.inv_sqrt_h = (float)(1.0 / std::sqrt((double)a->head_dim));
   p.eps = a->eps;
   p.x = a->x;

@@ -40,6 +40,8 @@ int set_error(int code, const char* fmt, ...);
 
 // Ring depth (slots per consumer warp); CFB_SPW overrides it for tuning runs.
 int tuned_spw();
+// Producer idle back-off cap in ns; CFB_SLEEP overrides it.
+int tuned_sleep();
 
 #define CFB_CUDA(expr)                                                              \
   do {                                                                              \

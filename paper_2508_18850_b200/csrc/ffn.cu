@@ -28,7 +28,7 @@
 namespace cfb {
 
 struct FfnParams {
-  int B, D, F, flags, spw;
+  int B, D, F, flags, spw, sleep_max;
   float eps;
   const void* x;          // [B][D] T (no CFB_NORM)
   const float* resid;     // [B][D] fp32
@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   const int B = p.B, D = p.D, F = p.F, G = gridDim.x, i = blockIdx.x;
   const FfnLayout L = ffn_layout(B, D, F, G, p.spw, XH);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
-  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int T1 = F / 2, T2 = D / 4;
   const int a0 = (int)((long long)i * T1 / G), a1 = (int)((long long)(i + 1) * T1 / G);
@@ -194,8 +194,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   grid = grid > sms ? sms : grid;  // grid barrier: every CTA must be co-resident
   if (grid > a->hidden / 4) grid = a->hidden / 4;
   if (grid > a->inter / 2) grid = a->inter / 2;
-  // fp16 activations in smem when the fp32 layout cannot fit (batch > 2)
-  const bool xh = tb == 2 && a->batch > 2;
+  // fp16 activations in smem for fp16 weights (FHFMA GEMV path)
+  const bool xh = tb == 2;
   int spw = tuned_spw();
   FfnLayout L = ffn_layout(a->batch, a->hidden, a->inter, grid, spw, xh);
   while (L.total > kMaxSmem && spw > 1) L = ffn_layout(a->batch, a->hidden, a->inter, grid, --spw, xh);
@@ -208,6 +208,7 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.F = a->inter;
   p.flags = a->flags;
   p.spw = spw;
+  p.sleep_max = tuned_sleep();
   p.eps = a->eps;
   p.x = a->x;
   p.resid = a->resid;
@@ -221,8 +222,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.trace = a->trace;
   const size_t smem = L.total;
   if (tb == 2) {
-    if (p.B == 1) return launch_ffn_inst<__half, 1, false>(p, grid, smem, st);
-    if (p.B == 2) return launch_ffn_inst<__half, 2, false>(p, grid, smem, st);
+    if (p.B == 1) return launch_ffn_inst<__half, 1, true>(p, grid, smem, st);
+    if (p.B == 2) return launch_ffn_inst<__half, 2, true>(p, grid, smem, st);
     if (p.B <= 4) return launch_ffn_inst<__half, 4, true>(p, grid, smem, st);
     return launch_ffn_inst<__half, 8, true>(p, grid, smem, st);
   }

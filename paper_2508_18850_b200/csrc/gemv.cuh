@@ -39,6 +39,23 @@ __device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsign
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
   return r;
 }
+// d = float(lo/hi half of a) * float(lo/hi half of b) + c   (sm_100 FHFMA)
+__device__ __forceinline__ float fma_f16_lo(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{\n\t.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.f16 %0, al, bl, %3;\n\t}"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fma_f16_hi(uint32_t a, uint32_t b, float c) {
+  float d;
+  asm("{\n\t.reg .b16 al, ah, bl, bh;\n\t"
+      "mov.b32 {al, ah}, %1;\n\tmov.b32 {bl, bh}, %2;\n\t"
+      "fma.rn.f32.f16 %0, ah, bh, %3;\n\t}"
+      : "=f"(d) : "r"(a), "r"(b), "f"(c));
+  return d;
+}
 __device__ __forceinline__ float f2_sum(unsigned long long v) {
   return __uint_as_float(static_cast<unsigned>(v)) + __uint_as_float(static_cast<unsigned>(v >> 32));
 }
@@ -64,64 +81,131 @@ using XElem = typename std::conditional<XH, __half, float>::type;
 // products of the tile's 4 rows (over the item's chunks) with B activation
 // rows, reduced across the 8 chunk groups.  emit(row, sums) runs on all
 // lanes; lanes 0..3 (chunk group 0) hold row (4*tile + lane)'s sums.
+// Multiply-accumulate of one 16-byte weight chunk (global chunk index gc)
+// with the B activation rows.
+template <typename T, int QB, bool XH>
+__device__ __forceinline__ void chunk_mac(unsigned long long (&acc)[QB], const uint4& wv, int gc,
+                                          const XElem<XH>* xs, int C, int B) {
+  if constexpr (sizeof(T) == 2 && XH) {
+    // fp16 weights x fp16 activations, fp32 accumulate: one FHFMA per weight
+    // (fma.rn.f32.f16 - the f16 x f16 product is exact in fp32, so this is
+    // bit-identical to converting both operands first), no conversions
+    const uint32_t wr[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      if (b < B) {
+        const uint4 xv = lds128(xs + (size_t)b * C + gc * 8);
+        const uint32_t xr[4] = {xv.x, xv.y, xv.z, xv.w};
+        float lo = __uint_as_float(static_cast<uint32_t>(acc[b]));
+        float hi = __uint_as_float(static_cast<uint32_t>(acc[b] >> 32));
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          lo = fma_f16_lo(wr[j], xr[j], lo);
+          hi = fma_f16_hi(wr[j], xr[j], hi);
+        }
+        acc[b] = f2_pack(lo, hi);
+      }
+    }
+  } else if constexpr (sizeof(T) == 2) {
+    const __half2* h = reinterpret_cast<const __half2*>(&wv);
+    const float2 w0 = __half22float2(h[0]), w1 = __half22float2(h[1]);
+    const float2 w2 = __half22float2(h[2]), w3 = __half22float2(h[3]);
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      if (b < B) {
+        const float* xb = xs + (size_t)b * C;
+        const uint4 lo = lds128(xb + gc * 4), hi = lds128(xb + C / 2 + gc * 4);
+        acc[b] = ffma2(f2_pack(w0.x, w0.y), u2_lo(lo), acc[b]);
+        acc[b] = ffma2(f2_pack(w1.x, w1.y), u2_hi(lo), acc[b]);
+        acc[b] = ffma2(f2_pack(w2.x, w2.y), u2_lo(hi), acc[b]);
+        acc[b] = ffma2(f2_pack(w3.x, w3.y), u2_hi(hi), acc[b]);
+      }
+    }
+  } else {
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      if (b < B) {
+        const uint4 xv = lds128(xs + (size_t)b * C + gc * 4);
+        acc[b] = ffma2(u2_lo(wv), u2_lo(xv), acc[b]);
+        acc[b] = ffma2(u2_hi(wv), u2_hi(xv), acc[b]);
+      }
+    }
+  }
+}
+
+// One tiles-mode item: for every tile in the item, the lanes' partial dot
+// products of the tile's 4 rows (over the item's chunks) with B activation
+// rows, reduced across the 8 chunk groups.  emit(row, sums) runs on all
+// lanes; lanes 0..3 (chunk group 0) hold row (4*tile + lane)'s sums.  Short
+// rows (K = head_dim in the O-projection: 2 chunks per lane per tile) are
+// processed TG tiles at a time so the butterflies of TG tiles interleave
+// instead of serialising on shuffle latency.
 template <typename T, int QB, bool XH, class Emit>
 __device__ __forceinline__ void tile_item(const Phase& P, const Item& it, const char* slot,
                                           const XElem<XH>* xs, int C, int B, int lane, Emit&& emit) {
+  constexpr int TG = QB == 1 ? 8 : (QB <= 2 ? 4 : (QB <= 4 ? 2 : 1));
   const int q = lane >> 2, r = lane & 3;
   const int nch = it.bytes / (it.nunits * 64);  // chunks per tile in this item
   const int ch0 = it.byte0 / 64;
+  if (TG > 1 && nch <= 16) {
+    // short rows: TG tiles per group, at most 2 chunks per lane per tile
+    for (int t0 = 0; t0 < it.nunits; t0 += TG) {
+      unsigned long long acc[TG][QB];
+#pragma unroll
+      for (int u = 0; u < TG; ++u)
+#pragma unroll
+        for (int b = 0; b < QB; ++b) acc[u][b] = 0ull;
+      if (t0 + TG <= it.nunits) {  // full group: straight-line, loads hoisted
+        uint4 wv[TG][2];
+#pragma unroll
+        for (int u = 0; u < TG; ++u)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            wv[u][k] = (q + 8 * k < nch) ? lds128(slot + (((t0 + u) * nch + q + 8 * k) * 4 + r) * 16)
+                                         : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (int u = 0; u < TG; ++u)
+#pragma unroll
+          for (int k = 0; k < 2; ++k)
+            if (q + 8 * k < nch) chunk_mac<T, QB, XH>(acc[u], wv[u][k], ch0 + q + 8 * k, xs, C, B);
+      } else {
+#pragma unroll
+        for (int u = 0; u < TG; ++u) {
+          if (t0 + u < it.nunits) {
+            const char* tile = slot + (t0 + u) * nch * 64;
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+              if (q + 8 * k < nch)
+                chunk_mac<T, QB, XH>(acc[u], lds128(tile + ((q + 8 * k) * 4 + r) * 16),
+                                     ch0 + q + 8 * k, xs, C, B);
+          }
+        }
+      }
+      float s[TG][QB];
+#pragma unroll
+      for (int u = 0; u < TG; ++u)
+#pragma unroll
+        for (int b = 0; b < QB; ++b) s[u][b] = f2_sum(acc[u][b]);
+#pragma unroll
+      for (int o = 4; o <= 16; o <<= 1)
+#pragma unroll
+        for (int u = 0; u < TG; ++u)
+#pragma unroll
+          for (int b = 0; b < QB; ++b) s[u][b] += __shfl_xor_sync(0xffffffffu, s[u][b], o);
+#pragma unroll
+      for (int u = 0; u < TG; ++u)
+        if (t0 + u < it.nunits) emit((it.unit0 + t0 + u) * kTileRows + r, s[u]);
+    }
+    return;
+  }
   for (int t = 0; t < it.nunits; ++t) {
     const char* tile = slot + t * nch * 64;
     unsigned long long acc[QB];
 #pragma unroll
     for (int b = 0; b < QB; ++b) acc[b] = 0ull;
 #pragma unroll 4
-    for (int c = q; c < nch; c += 8) {
-      const uint4 wv = lds128(tile + (c * 4 + r) * 16);
-      const int gc = ch0 + c;
-      if constexpr (sizeof(T) == 2 && XH) {
-        const __half2* h = reinterpret_cast<const __half2*>(&wv);
-        const float2 w0 = __half22float2(h[0]), w1 = __half22float2(h[1]);
-        const float2 w2 = __half22float2(h[2]), w3 = __half22float2(h[3]);
-#pragma unroll
-        for (int b = 0; b < QB; ++b) {
-          if (b < B) {
-            const uint4 xv = lds128(xs + (size_t)b * C + gc * 8);
-            const __half2* xh = reinterpret_cast<const __half2*>(&xv);
-            const float2 x0 = __half22float2(xh[0]), x1 = __half22float2(xh[1]);
-            const float2 x2 = __half22float2(xh[2]), x3 = __half22float2(xh[3]);
-            acc[b] = ffma2(f2_pack(w0.x, w0.y), f2_pack(x0.x, x0.y), acc[b]);
-            acc[b] = ffma2(f2_pack(w1.x, w1.y), f2_pack(x1.x, x1.y), acc[b]);
-            acc[b] = ffma2(f2_pack(w2.x, w2.y), f2_pack(x2.x, x2.y), acc[b]);
-            acc[b] = ffma2(f2_pack(w3.x, w3.y), f2_pack(x3.x, x3.y), acc[b]);
-          }
-        }
-      } else if constexpr (sizeof(T) == 2) {
-        const __half2* h = reinterpret_cast<const __half2*>(&wv);
-        const float2 w0 = __half22float2(h[0]), w1 = __half22float2(h[1]);
-        const float2 w2 = __half22float2(h[2]), w3 = __half22float2(h[3]);
-#pragma unroll
-        for (int b = 0; b < QB; ++b) {
-          if (b < B) {
-            const float* xb = xs + (size_t)b * C;
-            const uint4 lo = lds128(xb + gc * 4), hi = lds128(xb + C / 2 + gc * 4);
-            acc[b] = ffma2(f2_pack(w0.x, w0.y), u2_lo(lo), acc[b]);
-            acc[b] = ffma2(f2_pack(w1.x, w1.y), u2_hi(lo), acc[b]);
-            acc[b] = ffma2(f2_pack(w2.x, w2.y), u2_lo(hi), acc[b]);
-            acc[b] = ffma2(f2_pack(w3.x, w3.y), u2_hi(hi), acc[b]);
-          }
-        }
-      } else {
-#pragma unroll
-        for (int b = 0; b < QB; ++b) {
-          if (b < B) {
-            const uint4 xv = lds128(xs + (size_t)b * C + gc * 4);
-            acc[b] = ffma2(u2_lo(wv), u2_lo(xv), acc[b]);
-            acc[b] = ffma2(u2_hi(wv), u2_hi(xv), acc[b]);
-          }
-        }
-      }
-    }
+    for (int c = q; c < nch; c += 8)
+      chunk_mac<T, QB, XH>(acc, lds128(tile + (c * 4 + r) * 16), ch0 + c, xs, C, B);
     float s[QB];
 #pragma unroll
     for (int b = 0; b < QB; ++b) {
@@ -132,6 +216,118 @@ __device__ __forceinline__ void tile_item(const Phase& P, const Item& it, const 
       s[b] = v;
     }
     emit((it.unit0 + t) * kTileRows + r, s);
+  }
+}
+
+// Short-row GEMV item (rows mode, K = C elements, C*sizeof(T) small: the
+// O-projection's K = head_dim): one lane per row (L lanes per row when a row
+// exceeds 16 chunks), so there are no cross-lane reductions at all.  Rows are
+// stored chunk-rotated - logical chunk k of slice row g sits at physical chunk
+// (k + g) mod nch - so the 32 lanes of a warp, each reading "its" row, hit all
+// eight 16-byte bank groups (conflict-free LDS.128).  The activation chunk is
+// the same for every lane (broadcast).  emit(g, sums) runs on the row's lane 0.
+template <typename T, int QB, int NCH, class Emit>
+__device__ __forceinline__ void rowlane_item_fixed(const Item& it, const char* slot, const T* a,
+                                                   int B, int lane, Emit&& emit) {
+  // NCH chunks per row, one lane per row, no runtime conditions in the row body
+  constexpr int tb = sizeof(T), epc = 16 / tb, C = NCH * epc, rb = C * tb;
+  for (int r0 = 0; r0 < it.nunits; r0 += 32) {
+    const int row = r0 + lane;
+    const bool valid = row < it.nunits;
+    const int g = it.unit0 + row;
+    const char* rp = slot + (size_t)(valid ? row : 0) * rb;
+    uint4 wv[NCH];
+#pragma unroll
+    for (int k = 0; k < NCH; ++k) wv[k] = lds128(rp + ((k + g) & (NCH - 1)) * 16);
+    float s[QB];
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      if (b < B) {
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          const uint4 av = lds128(a + (size_t)b * C + k * epc);
+          if constexpr (tb == 2) {
+            acc[0] = fma_f16_lo(wv[k].x, av.x, acc[0]);
+            acc[1] = fma_f16_hi(wv[k].x, av.x, acc[1]);
+            acc[2] = fma_f16_lo(wv[k].y, av.y, acc[2]);
+            acc[3] = fma_f16_hi(wv[k].y, av.y, acc[3]);
+            acc[0] = fma_f16_lo(wv[k].z, av.z, acc[0]);
+            acc[1] = fma_f16_hi(wv[k].z, av.z, acc[1]);
+            acc[2] = fma_f16_lo(wv[k].w, av.w, acc[2]);
+            acc[3] = fma_f16_hi(wv[k].w, av.w, acc[3]);
+          } else {
+            acc[0] = fmaf(__uint_as_float(wv[k].x), __uint_as_float(av.x), acc[0]);
+            acc[1] = fmaf(__uint_as_float(wv[k].y), __uint_as_float(av.y), acc[1]);
+            acc[2] = fmaf(__uint_as_float(wv[k].z), __uint_as_float(av.z), acc[2]);
+            acc[3] = fmaf(__uint_as_float(wv[k].w), __uint_as_float(av.w), acc[3]);
+          }
+        }
+      }
+      s[b] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    }
+    if (valid) emit(g, s);
+  }
+}
+
+template <typename T, int QB, class Emit>
+__device__ __forceinline__ void rowlane_item(const Item& it, const char* slot, const T* a, int C,
+                                             int B, int lane, Emit&& emit) {
+  constexpr int tb = sizeof(T);
+  constexpr int epc = 16 / tb;
+  constexpr int kMaxChunks = 16;  // chunks per lane
+  const int nch = C * tb / 16, rb = C * tb;
+  if (nch == 16) return rowlane_item_fixed<T, QB, 16>(it, slot, a, B, lane, emit);
+  if (nch == 8) return rowlane_item_fixed<T, QB, 8>(it, slot, a, B, lane, emit);
+  const int L = nch > kMaxChunks ? nch / kMaxChunks : 1;
+  const int sub = lane % L, lr = lane / L, step = 32 / L;
+  for (int r0 = 0; r0 < it.nunits; r0 += step) {
+    const int row = r0 + lr;
+    const bool valid = row < it.nunits;
+    const int g = it.unit0 + row;
+    const char* rp = slot + (size_t)(valid ? row : 0) * rb;
+    float acc[QB][2];
+#pragma unroll
+    for (int b = 0; b < QB; ++b) acc[b][0] = acc[b][1] = 0.f;
+    uint4 wv[kMaxChunks];
+#pragma unroll
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int k = sub + L * i;
+      if (k < nch) wv[i] = lds128(rp + ((k + g) & (nch - 1)) * 16);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxChunks; ++i) {
+      const int k = sub + L * i;
+      if (k < nch) {
+#pragma unroll
+        for (int b = 0; b < QB; ++b) {
+          if (b < B) {
+            const uint4 av = lds128(a + (size_t)b * C + k * epc);
+            if constexpr (tb == 2) {
+              const uint32_t wr[4] = {wv[i].x, wv[i].y, wv[i].z, wv[i].w};
+              const uint32_t ar[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                acc[b][0] = fma_f16_lo(wr[j], ar[j], acc[b][0]);
+                acc[b][1] = fma_f16_hi(wr[j], ar[j], acc[b][1]);
+              }
+            } else {
+              acc[b][0] = fmaf(__uint_as_float(wv[i].x), __uint_as_float(av.x), acc[b][0]);
+              acc[b][1] = fmaf(__uint_as_float(wv[i].y), __uint_as_float(av.y), acc[b][1]);
+              acc[b][0] = fmaf(__uint_as_float(wv[i].z), __uint_as_float(av.z), acc[b][0]);
+              acc[b][1] = fmaf(__uint_as_float(wv[i].w), __uint_as_float(av.w), acc[b][1]);
+            }
+          }
+        }
+      }
+    }
+    float s[QB];
+#pragma unroll
+    for (int b = 0; b < QB; ++b) {
+      s[b] = acc[b][0] + acc[b][1];
+      for (int o = 1; o < L; o <<= 1) s[b] += __shfl_xor_sync(0xffffffffu, s[b], o);
+    }
+    if (valid && sub == 0) emit(g, s);
   }
 }
 

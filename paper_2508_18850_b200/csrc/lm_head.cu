@@ -15,7 +15,7 @@
 namespace cfb {
 
 struct LmParams {
-  int B, D, V, flags, spw;
+  int B, D, V, flags, spw, sleep_max;
   float eps;
   const float* resid;
   const void* norm_w;
@@ -42,9 +42,10 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   const int rows = kTileRows * (t1 - t0);
   const int rows_max = kTileRows * ((TV + G - 1) / G);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(p.spw));
-  const Ring ring{smem, bars, bars + kNumSlots, p.spw};
-  float* xs = reinterpret_cast<float*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
-  float* part = xs + B * D;
+  const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
+  constexpr bool XH = sizeof(T) == 2;  // fp16 activations (FHFMA GEMV path)
+  XElem<XH>* xs = reinterpret_cast<XElem<XH>*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8);
+  float* part = reinterpret_cast<float*>(smem + ring_bytes(p.spw) + 2 * kNumSlots * 8) + B * D;
   float* red = part + kNumConsumerWarps * B * rows_max;
   float* wv = red + kNumConsumerWarps * B;
   int* wi = reinterpret_cast<int*>(wv + kNumConsumerWarps * B);
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     return;
   }
   pdl_wait();
-  rmsnorm_to_smem<T>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
+  rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   float bv[QB];
   int bi[QB];
 #pragma unroll
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
     bi[b] = 0x7fffffff;
   }
   int cnt = 0;
-  tiled_gemv_phase<T, QB>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows, part,
+  tiled_gemv_phase<T, QB, XH>(P0, ring, warp, lane, tid, cnt, xs, D, B, rows, part,
                           [&](int row, int b, float s) {
                             const int v = kTileRows * t0 + row;
                             if (v >= V) return;
@@ -199,6 +200,7 @@ int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st) {
   p.V = a->vocab;
   p.flags = a->flags;
   p.spw = spw;
+  p.sleep_max = tuned_sleep();
   p.eps = a->eps;
   p.resid = a->resid;
   p.norm_w = a->norm_w;

@@ -106,7 +106,8 @@ struct Ring {
   char* slots;
   uint64_t* full;
   uint64_t* empty;
-  int spw;  // slots per consumer warp
+  int spw;        // slots per consumer warp
+  int sleep_max;  // producer idle back-off cap (ns)
   __device__ __forceinline__ char* slot(int s) const { return slots + s * kSlotBytes; }
 };
 
@@ -138,6 +139,7 @@ __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r,
   const int w = lane;
   int ph = 0, j = 0;
   bool done = w >= kNumConsumerWarps;
+  int nap = 32;
   while (true) {
     bool issued = false;
     if (!done) {
@@ -158,7 +160,14 @@ __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r,
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
-    if (!__any_sync(0xffffffffu, issued)) __nanosleep(32);
+    // idle: exponential back-off, so a producer waiting on full sub-rings does
+    // not steal issue slots from the consumer warps sharing its SM sub-partition
+    if (__any_sync(0xffffffffu, issued)) {
+      nap = 32;
+    } else {
+      __nanosleep(nap);
+      nap = min(2 * nap, r.sleep_max);
+    }
   }
 }
 template <int NP>

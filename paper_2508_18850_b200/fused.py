@@ -26,7 +26,7 @@ from . import _native
 from .exceptions import DimensionError, SimulationError
 from .ledger import (GLOBAL, ONESHOT_MERGE, StageTrace, TrafficLedger, emit_gather, emit_oneshot,
                      emit_reduce)
-from .layouts import gate_up_tiles, qkv_tiles, row_tiles
+from .layouts import gate_up_tiles, qkv_tiles, row_tiles, wo_rows
 from .scenario import MHA, MLA, validate_scenario
 
 SPLIT_TOKEN, FUSED_MLA, SPLIT_HEAD = "split_token", "fused_mla", "split_head"
@@ -136,6 +136,7 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
         w_qkv = qkv_tiles(up(scenario.w_qkv).to(dt), n, Hp, Dp)
         wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
         wo[:, :D, :H] = up(scenario.w_out).transpose(1, 2).to(dt)
+        wo = wo_rows(wo, n)
         cap = max(S, 1)
         kc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)
         vc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)

@@ -49,3 +49,21 @@ def qkv_tiles(w_qkv, n_blocks: int, head_pad: int, hidden_pad: int):
     rows = wp.reshape(nh, 3, n_blocks, hp, hidden_pad).permute(0, 2, 1, 3, 4)  # (nh, N, 3, h, D')
     rows = rows.reshape(nh, n_blocks, 3 * hp, hidden_pad)
     return row_tiles(rows)
+
+
+def wo_rows(w_out_t, n_blocks: int):
+    """(nh, D, Hp) = (W_out[head])^T -> [nh][N][D/N][Hp]: rank r's rows
+    r*D/N .. (r+1)*D/N, each row chunk-rotated for the row-per-lane O-proj
+    (csrc/gemv.cuh rowlane_item): logical 16-byte chunk k of slice row g is
+    stored at chunk (k + g) mod nch."""
+    import torch
+    nh, D, Hp = w_out_t.shape
+    cols = D // n_blocks
+    e = _epc(w_out_t)
+    nch = Hp // e
+    w = w_out_t.reshape(nh, n_blocks, cols, nch, e)
+    g = torch.arange(cols, device=w.device).view(cols, 1)
+    p = torch.arange(nch, device=w.device).view(1, nch)
+    logical = (p - g) % nch  # physical chunk p holds logical chunk (p - g) mod nch
+    idx = logical.view(1, 1, cols, nch, 1).expand(nh, n_blocks, cols, nch, e)
+    return torch.gather(w, 3, idx).reshape(nh, n_blocks, cols, Hp).contiguous()

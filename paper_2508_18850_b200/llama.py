@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from .exceptions import DimensionError
-from .layouts import gate_up_tiles, qkv_tiles, row_tiles
+from .layouts import gate_up_tiles, qkv_tiles, row_tiles, wo_rows
 
 
 @dataclass(frozen=True)
@@ -142,7 +142,7 @@ class LlamaDecoder:
             return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).half()
 
         w_qkv = qkv_tiles(t(lp["w_qkv"]), N, H, D)               # row tiles per (head, rank)
-        w_out = t(lp["w_out"]).transpose(1, 2).contiguous()       # (nh, D, H)
+        w_out = wo_rows(t(lp["w_out"]).transpose(1, 2).contiguous(), N)  # row tiles per rank
         w_gu = gate_up_tiles(t(lp["w1"]), t(lp["w2"]))            # row tiles (g g u u)
         kc = torch.zeros(nh, self.cache_cap, H, device=dev, dtype=torch.float16)
         vc = torch.zeros_like(kc)
@@ -187,7 +187,7 @@ class LlamaDecoder:
             m.layers.append(dict(
                 attn_norm=rnd((D,), 0.1, 1.0),
                 w_qkv=rnd((nh, N, 3 * H // N // 4, D // 8, 4, 8), D ** -0.5),
-                w_out=rnd((nh, D, H), H ** -0.5), ffn_norm=rnd((D,), 0.1, 1.0),
+                w_out=rnd((nh, N, D // N, H), H ** -0.5), ffn_norm=rnd((D,), 0.1, 1.0),
                 w_gu=rnd((F // 2, D // 8, 4, 8), D ** -0.5), w_dn=rnd((D // 4, F // 8, 4, 8), F ** -0.5),
                 k_cache=rnd((nh, cache_cap, H), 1.0), v_cache=rnd((nh, cache_cap, H), 1.0)))
         m.embed = rnd((cfg.vocab, D), 1.0)

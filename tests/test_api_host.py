@@ -164,3 +164,20 @@ def test_abi_struct_layout_matches_header(cname, pyname):
     """ctypes mirrors must have the field order of the C structs."""
     text = (ROOT / "include" / "cfb.h").read_text()
     assert _struct_fields(text, cname) == [f[0] for f in getattr(_native, pyname)._fields_]
+
+
+def test_wo_rows_layout():
+    """W_out^T rank slices with per-row chunk rotation (logical chunk k of slice
+    row g at physical chunk (k + g) mod nch)."""
+    import torch
+    from paper_2508_18850_b200.layouts import wo_rows
+    nh, D, Hp, N = 2, 24, 32, 4  # cols = 6, nch = 4 (fp16)
+    w = torch.arange(nh * D * Hp, dtype=torch.float32).reshape(nh, D, Hp).half()
+    t = wo_rows(w, N)
+    assert t.shape == (nh, N, 6, Hp)
+    for h in range(nh):
+        for r in range(N):
+            for g in range(6):
+                for k in range(4):
+                    p = (k + g) % 4
+                    assert torch.equal(t[h, r, g, p * 8:(p + 1) * 8], w[h, r * 6 + g, k * 8:(k + 1) * 8])

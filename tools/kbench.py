@@ -20,6 +20,7 @@ ap.add_argument("--reps", type=int, default=64)
 ap.add_argument("--layers", type=int, default=16)
 ap.add_argument("--cluster", type=int, default=4)
 ap.add_argument("--no-pdl", action="store_true")
+ap.add_argument("--dbg", type=int, default=0)
 ap.add_argument("--mode", default="oneshot", choices=["oneshot", "merged", "two_pass"])
 a = ap.parse_args()
 a.pdl = 0 if a.no_pdl else _native.PDL
@@ -36,7 +37,7 @@ def rnd(*shape, s=0.02):
 
 
 layers = [dict(g=rnd(D, s=1.0), w_gu=rnd(F, 2, D), w_dn=rnd(D, F), w_qkv=rnd(nh, N, 3, H // N, D),
-               w_out=rnd(nh, D, H), kc=rnd(nh, a.ctx + 8, H, s=1.0), vc=rnd(nh, a.ctx + 8, H, s=1.0))
+               w_out=rnd(nh, N, D // N, H), kc=rnd(nh, a.ctx + 8, H, s=1.0), vc=rnd(nh, a.ctx + 8, H, s=1.0))
           for _ in range(a.layers)]
 resid = torch.randn(1, D, device=dev)
 out = torch.empty(1, D, device=dev)
@@ -58,7 +59,7 @@ def ffn(l):
 def mha(l):
     return _native.MhaArgs(dtype=2, batch=1, hidden=D, n_heads=nh, head_dim=H, head_pad=H, cluster=N,
                            seq_len=a.ctx, cache_cap=a.ctx + 8,
-                           flags=_native.APPEND | _native.NORM | a.mode | a.pdl,
+                           flags=_native.APPEND | _native.NORM | a.mode | a.pdl | a.dbg,
                            resid=resid.data_ptr(),
                            norm_w=l["g"].data_ptr(), eps=1e-5, w_qkv=l["w_qkv"].data_ptr(),
                            w_out=l["w_out"].data_ptr(), k_cache=l["kc"].data_ptr(),
@@ -99,6 +100,9 @@ if "--trace" in sys.argv or True:
                round((t[:, k].max() - t0) / 1e3, 2)) for k, n in enumerate(names)})
     tr = torch.zeros(256 * 16, device=dev, dtype=torch.int64)
     ma = mha(layers[0]); ma.trace = tr.data_ptr()
+    torch.cuda.synchronize()
+    for i in range(1, 4):  # traced launch inside a warm PDL chain, like the engine
+        _native.check(L.cfb_mha_decode(mha(layers[i]), sp))
     _native.check(L.cfb_mha_decode(ma, sp)); torch.cuda.synchronize()
     t = tr.view(256, 16).cpu().numpy()[:nh * N].astype(np.float64)
     t0 = t[:, 0].min()
@@ -110,3 +114,4 @@ if "--trace" in sys.argv or True:
     import os
     os.makedirs("gpurun_out", exist_ok=True)
     np.save(f"gpurun_out/mha_trace_ctx{a.ctx}.npy", (t - t0) / 1e3)
+    print("oproj math cycles (warp 0) median", np.median(t[:, 14]), "items", np.median(t[:, 15]))
