@@ -124,6 +124,39 @@ int cfb_mha_decode(const cfb_mha_args* args, void* stream);
 
 
 /*
+ * fused_mla latent-attention module (dataflows.py:316-429): one cluster of N
+ * CTAs per head.  H = head_dim, R = kv_lora_rank, Hp/Rp power-of-two pads,
+ * h = H/N, rs = R/N, rsp = pow2 >= max(rs, 16/T), D % N == 0.  Layouts (T):
+ *   x       [B][D]
+ *   w_q     [n_heads][N][ceil(h/4)][D*T/16][4][16/T]  row tiles of W_q[head][:, r*h..]^T
+ *   w_kv    [N][ceil(rs/4)][D*T/16][4][16/T]          row tiles of W_kv[:, r*rs..]^T (shared)
+ *   w_up    [n_heads][N][rs][Hp]     rows j of W_up[head][:, r*rs + j]^T, chunk-rotated
+ *   w_down  [n_heads][N][Hp][rsp]    rows j of W_down[head][r*rs.., j]^T, chunk-rotated
+ *   w_out   [n_heads][N][D/N][Hp]    as cfb_mha_args.w_out
+ *   cache   [seq_len][Rp]            latent rows (shared by all heads)
+ *   accum / out / stats / traffic as cfb_mha_args; flags: CFB_APPEND,
+ *   CFB_STATS_MERGED, CFB_PDL.  Batch <= 4.
+ * "Chunk-rotated": logical 16-byte chunk k of row g stored at (k + g) mod nch.
+ */
+typedef struct cfb_mla_args {
+  int dtype;
+  int batch, hidden, n_heads, head_dim, head_pad, kv_rank, rank_pad;
+  int cluster, seq_len, flags;
+  const void* x;
+  const void* w_q;
+  const void* w_kv;
+  const void* w_up;
+  const void* w_down;
+  const void* w_out;
+  const void* cache;
+  float* out;
+  unsigned long long* accum;
+  float* stats;
+  unsigned long long* traffic;
+} cfb_mla_args;
+int cfb_mla_decode(const cfb_mla_args* args, void* stream);
+
+/*
  * Fused SwiGLU FFN (one launch, persistent grid, one CTA per SM):
  *   out = [r +] (silu(h w1^T) * (h w2^T)) w3^T,  h = x or f16(rmsnorm(r) * norm_w),
  *   r = resid [+ accum * 2^-32]  (accum: the attention module's fixed-point head

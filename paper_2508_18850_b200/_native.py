@@ -93,6 +93,16 @@ def require_cuda():
     return torch.device("cuda")
 
 
+class MlaArgs(ctypes.Structure):
+    """Mirror of ``cfb_mla_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "n_heads", "head_dim",
+                                             "head_pad", "kv_rank", "rank_pad", "cluster",
+                                             "seq_len", "flags")] + [
+        (n, _vp) for n in ("x", "w_q", "w_kv", "w_up", "w_down", "w_out", "cache", "out", "accum",
+                           "stats", "traffic")]
+
+
 class FfnArgs(ctypes.Structure):
     """Mirror of ``cfb_ffn_args``."""
 
@@ -111,6 +121,8 @@ class LmArgs(ctypes.Structure):
 
 
 def bind_extra(L) -> None:
+    L.cfb_mla_decode.argtypes = [ctypes.POINTER(MlaArgs), _vp]
+    L.cfb_mla_decode.restype = ctypes.c_int
     L.cfb_ffn_decode.argtypes = [ctypes.POINTER(FfnArgs), _vp]
     L.cfb_ffn_decode.restype = ctypes.c_int
     L.cfb_lm_head_argmax.argtypes = [ctypes.POINTER(LmArgs), _vp]

@@ -39,6 +39,10 @@ int cfb_mha_decode(const cfb_mha_args* args, void* stream) {
   return cfb::mha_decode(args, static_cast<cudaStream_t>(stream));
 }
 
+int cfb_mla_decode(const cfb_mla_args* args, void* stream) {
+  return cfb::mla_decode(args, static_cast<cudaStream_t>(stream));
+}
+
 int cfb_ffn_decode(const cfb_ffn_args* args, void* stream) {
   return cfb::ffn_decode(args, static_cast<cudaStream_t>(stream));
 }

@@ -687,9 +687,12 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   const bool pdl = a->flags & CFB_PDL;
   int rc = tb == 2 ? launch_mha_t<__half>(p, L.total, st, pdl) : launch_mha_t<float>(p, L.total, st, pdl);
   if (rc || !a->out) return rc;
-  const int n = a->batch * a->hidden;
-  mha_finalize_kernel<<<(n + 255) / 256, 256, 0, st>>>(
-      a->out, (a->flags & CFB_RESID) ? a->resid : nullptr, a->accum, n);
+  return mha_finalize(a->out, (a->flags & CFB_RESID) ? a->resid : nullptr, a->accum,
+                      a->batch * a->hidden, st);
+}
+
+int mha_finalize(float* out, const float* resid, unsigned long long* accum, int n, cudaStream_t st) {
+  mha_finalize_kernel<<<(n + 255) / 256, 256, 0, st>>>(out, resid, accum, n);
   CFB_CUDA(cudaGetLastError());
   return CFB_OK;
 }

@@ -67,3 +67,18 @@ def wo_rows(w_out_t, n_blocks: int):
     logical = (p - g) % nch  # physical chunk p holds logical chunk (p - g) mod nch
     idx = logical.view(1, 1, cols, nch, 1).expand(nh, n_blocks, cols, nch, e)
     return torch.gather(w, 3, idx).reshape(nh, n_blocks, cols, Hp).contiguous()
+
+
+def rotated_rows(t):
+    """(..., rows, C) -> same shape with every row chunk-rotated by its index
+    g within the rows dim: logical 16-byte chunk k stored at (k + g) mod nch
+    (the row-per-lane GEMV layout, csrc/gemv.cuh rowlane_item)."""
+    import torch
+    *lead, rows, C = t.shape
+    e = _epc(t)
+    nch = C // e
+    w = t.reshape(*lead, rows, nch, e)
+    g = torch.arange(rows, device=t.device).view(rows, 1)
+    p = torch.arange(nch, device=t.device).view(1, nch)
+    logical = ((p - g) % nch).view(*([1] * len(lead)), rows, nch, 1).expand(*lead, rows, nch, e)
+    return torch.gather(w, len(lead) + 1, logical).reshape(*lead, rows, C).contiguous()

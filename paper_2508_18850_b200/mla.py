@@ -1,0 +1,128 @@
+"""fused_mla (and split_head) dataflows on the GPU: drop-ins for the
+reference's ``run_fused_mla_decode`` (``dataflows.py:316-429``) and
+``run_splithead_decode`` (``dataflows.py:432-502``).
+
+The scenario's arrays are packed once per call into the kernel layouts of
+``include/cfb.h`` (``cfb_mla_args``), the kernel runs through the C ABI, and
+the result carries the output, the statistics of rank 0 and the DSMEM ledger
+of the kernel's static schedule, cross-checked against the byte counters the
+kernel kept.  Same deliberate deviation as split_token: heads are summed in
+64-bit fixed point (exact, order-free) instead of f16-rounded atomics.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError, SimulationError
+from .fused import (FUSED_MLA, MERGED, TWO_PASS, DecodeResult, _emit_global, _finish_output,
+                    padded_hidden, pow2_at_least, validate_partitioning)
+from .layouts import rotated_rows, row_tiles, wo_rows
+from .ledger import StageTrace, TrafficLedger, emit_gather, emit_reduce
+from .scenario import validate_scenario
+
+
+def pack_mla(sc, dev, dt):
+    """DecodeScenario (MLA) -> dict of device tensors in cfb_mla_args layouts."""
+    import torch
+    d = sc.dims
+    n, nb = sc.cluster.n_blocks, d.dtype_bytes
+    B, D, nh, H, R = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.kv_lora_rank
+    S = d.seq_len
+    Hp, Rp = pow2_at_least(H), pow2_at_least(R)
+    Dp = padded_hidden(D, n, nb)
+    h, rs = H // n, R // n
+    rsp = pow2_at_least(rs, 16 // nb)
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+
+    x = torch.zeros(B, Dp, device=dev, dtype=dt)
+    x[:, :D] = up(sc.hidden).to(dt)
+    wq = torch.zeros(nh, Dp, H, device=dev, dtype=dt)
+    wq[:, :D, :] = up(sc.w_q).to(dt)                        # (nh, Dp, H)
+    wq = wq.reshape(nh, Dp, n, h).permute(0, 2, 3, 1)         # (nh, N, h, Dp)
+    wkv = torch.zeros(Dp, R, device=dev, dtype=dt)
+    wkv[:D] = up(sc.w_kv).to(dt)
+    wkv = wkv.reshape(Dp, n, rs).permute(1, 2, 0)              # (N, rs, Dp)
+    wup = torch.zeros(nh, Hp, R, device=dev, dtype=dt)
+    wup[:, :H] = up(sc.w_up).to(dt)
+    wup = wup.reshape(nh, Hp, n, rs).permute(0, 2, 3, 1)      # (nh, N, rs, Hp)
+    wdn = torch.zeros(nh, n, rsp, Hp, device=dev, dtype=dt)
+    wdn[:, :, :rs, :H] = up(sc.w_down).to(dt).reshape(nh, n, rs, H)
+    wdn = wdn.transpose(2, 3)                                  # (nh, N, Hp, rsp)
+    wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
+    wo[:, :D, :H] = up(sc.w_out).transpose(1, 2).to(dt)
+    cache = torch.zeros(max(S, 1), Rp, device=dev, dtype=dt)
+    if S:
+        cache[:S, :R] = up(sc.kv_cache).to(dt)
+    return dict(x=x, w_q=row_tiles(wq.contiguous()), w_kv=row_tiles(wkv.contiguous()),
+                w_up=rotated_rows(wup.contiguous()), w_down=rotated_rows(wdn.contiguous()),
+                w_out=wo_rows(wo, n), cache=cache, Dp=Dp, Hp=Hp, Rp=Rp)
+
+
+def run_fused_mla_decode(scenario, stats_mode: str = TWO_PASS,
+                         append_new_token: bool = True) -> DecodeResult:
+    """fused_mla latent attention on the GPU (one cluster per head)."""
+    import torch
+    validate_partitioning(scenario, FUSED_MLA, append_new_token)
+    validate_scenario(scenario)
+    if stats_mode not in (TWO_PASS, MERGED):
+        raise ValueError(f"unknown stats_mode {stats_mode!r}")
+    dev = _native.require_cuda()
+    d = scenario.dims
+    n, nb = scenario.cluster.n_blocks, d.dtype_bytes
+    B, D, nh, H, R = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.kv_lora_rank
+    if B > 4:
+        raise DimensionError("the fused_mla kernel supports batch <= 4")
+    dt = torch.float16 if nb == 2 else torch.float32
+    with torch.no_grad():
+        pk = pack_mla(scenario, dev, dt)
+        out = torch.empty(B, pk["Dp"], device=dev, dtype=torch.float32)
+        accum = torch.zeros(B, pk["Dp"], device=dev, dtype=torch.int64)
+        stats = torch.zeros(nh, 2, B, device=dev, dtype=torch.float32)
+        traffic = torch.zeros(16, device=dev, dtype=torch.int64)
+        flags = (_native.APPEND if append_new_token else 0) | (
+            _native.STATS_MERGED if stats_mode == MERGED else 0)
+        args = _native.MlaArgs(
+            dtype=nb, batch=B, hidden=pk["Dp"], n_heads=nh, head_dim=H, head_pad=pk["Hp"],
+            kv_rank=R, rank_pad=pk["Rp"], cluster=n, seq_len=d.seq_len, flags=flags,
+            x=pk["x"].data_ptr(), w_q=pk["w_q"].data_ptr(), w_kv=pk["w_kv"].data_ptr(),
+            w_up=pk["w_up"].data_ptr(), w_down=pk["w_down"].data_ptr(),
+            w_out=pk["w_out"].data_ptr(), cache=pk["cache"].data_ptr(), out=out.data_ptr(),
+            accum=accum.data_ptr(), stats=stats.data_ptr(), traffic=traffic.data_ptr())
+        _native.check(_native.lib().cfb_mla_decode(args, _native.stream_ptr()))
+        torch.cuda.synchronize()
+        out_np = out[:, :D].cpu().numpy()
+        st = stats.cpu().numpy()
+        dev_traffic = traffic.cpu().numpy()
+
+    ledger = TrafficLedger()
+    stage_traffic: dict[str, int] = {}
+    traces = []
+    h, rs = H // n, R // n
+    for head in range(nh):
+        tr = [("q_proj_gather", emit_gather(ledger, n, B * h * nb)),
+              ("latent_kv_gather", emit_gather(ledger, n, B * rs * nb)),
+              ("absorbed_q_gather", emit_gather(ledger, n, B * rs * nb))]
+        if stats_mode == MERGED:
+            tr.append(("stats_merge_reduce", emit_reduce(ledger, n, 2 * B * nb)))
+        else:
+            tr.append(("stats_max_reduce", emit_reduce(ledger, n, B * nb)))
+            tr.append(("stats_sum_reduce", emit_reduce(ledger, n, B * nb)))
+        tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * R * nb)))
+        tr.append(("down_proj_reduce", emit_reduce(ledger, n, B * H * nb)))
+        for stage, t in tr:
+            stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
+            traces.append(StageTrace(stage, head, t))
+        _emit_global(ledger, n, B, D // n, nb)
+    device_traffic = {_native.STAGE_NAMES[i]: int(dev_traffic[i]) for i in range(11)
+                      if _native.STAGE_NAMES[i] in stage_traffic}
+    if device_traffic != stage_traffic:
+        raise SimulationError(f"kernel DSMEM byte counters {device_traffic} disagree with the "
+                              f"schedule {stage_traffic}")
+    return DecodeResult(output=_finish_output(out_np), ledger=ledger, stage_traffic=stage_traffic,
+                        score_max=np.ascontiguousarray(st[:, 0, :]),
+                        score_sum=np.ascontiguousarray(st[:, 1, :]), collectives=traces,
+                        n_clusters=nh, n_blocks=n, device_traffic=device_traffic)

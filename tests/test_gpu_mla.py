@@ -1,0 +1,114 @@
+"""GPU parity of the fused_mla latent-attention kernel against the reference
+golden vectors (produced by the real ``clusterdec.run_fused_mla_decode``) and
+the CPU oracle.
+
+Tolerances: fp32 storage reproduces the reference's own bound (<= 1e-5,
+test_dataflows.py:111-117); fp16 storage: <= 3e-2 vs the reference
+simulator's f16 output (test_acceptance.py:176-180), <= 2e-3 vs the oracle
+restated with the kernel's fp32 head accumulation, and the north-star
+max-abs 2e-2 / max-rel 1e-2 vs the dense fp32 oracle.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import paper_2508_18850_b200 as cfb
+from oracle import clusterdec_port as cp
+
+pytestmark = pytest.mark.gpu
+
+MLA_KEYS = ("hidden", "w_q", "w_up", "w_kv", "w_down", "w_out", "kv_cache")
+
+
+def _scenario(case):
+    d = case["dims"]
+    dims = cfb.ModelDims(d["B"], d["D"], d["n_heads"], d["H"], d["S"], d["rank"], d["dtype_bytes"])
+    return cfb.random_mla_scenario(dims, case["n_blocks"], case["seed"])
+
+
+def _rel(a, b):
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-30))
+
+
+def test_fused_mla_matches_reference_golden(golden):
+    meta, g = golden
+    n_checked = 0
+    for case in meta["cases"]:
+        if case["kind"] != "fused_mla":
+            continue
+        sc = _scenario(case)
+        mode = case.get("stats_mode", "two_pass")
+        append = case.get("append_new_token", True)
+        res = cfb.run_fused_mla_decode(sc, stats_mode=mode, append_new_token=append)
+        name = case["name"]
+        ref = g[f"{name}/output"]
+        arrs = {k: getattr(sc, k) for k in MLA_KEYS}
+        if case["dims"]["dtype_bytes"] == 4:
+            assert float(np.max(np.abs(res.output - ref))) <= 1e-5, name
+            np.testing.assert_allclose(res.score_max, g[f"{name}/score_max"], atol=1e-5)
+            np.testing.assert_allclose(res.score_sum, g[f"{name}/score_sum"], rtol=1e-5)
+        else:
+            assert float(np.max(np.abs(res.output - ref))) <= 3e-2, name
+            o32, sm, ss = cp.fused_mla(arrs, case["n_blocks"], 2, mode, append, head_accum="f32")
+            assert float(np.max(np.abs(res.output - o32))) <= 2e-3, name
+            np.testing.assert_allclose(res.score_max, sm, atol=2e-3)
+            np.testing.assert_allclose(res.score_sum, ss, rtol=2e-3)
+        if f"{name}/dense" in g.files:
+            dense = g[f"{name}/dense"]
+            tol = 1e-5 if case["dims"]["dtype_bytes"] == 4 else 2e-2
+            assert float(np.max(np.abs(res.output - dense))) <= tol, name
+            if case["dims"]["dtype_bytes"] == 2:
+                assert _rel(res.output, dense) <= 1e-2, name
+        assert res.stage_traffic == case["stage_traffic"], name
+        assert res.dsmem_bytes == case["dsmem_bytes"], name
+        assert len(res.ledger) == case["n_events"], name
+        assert res.ledger.channel_bytes("global") == case["global_bytes"], name
+        assert cfb.reconcile_traffic("fused_mla", res, sc.dims, mode).reconciled, name
+        n_checked += 1
+    assert n_checked >= 40
+
+
+def test_fused_mla_merged_equals_two_pass():
+    dims = cfb.ModelDims(2, 64, 4, 16, 37, 32, dtype_bytes=4)
+    sc = cfb.random_mla_scenario(dims, n_blocks=4, seed=5)
+    a = cfb.run_fused_mla_decode(sc, stats_mode="two_pass")
+    b = cfb.run_fused_mla_decode(sc, stats_mode="merged")
+    assert np.array_equal(a.score_max, b.score_max)
+    assert float(np.max(np.abs(a.output - b.output))) <= 1e-5
+
+
+def test_fused_mla_cluster_size_invariance_and_empty_cache():
+    outs = []
+    for n in (1, 2, 4, 8):
+        dims = cfb.ModelDims(1, 64, 2, 16, 29, 32, dtype_bytes=4)
+        outs.append(cfb.run_fused_mla_decode(cfb.random_mla_scenario(dims, n, seed=9)).output)
+    for o in outs:
+        assert float(np.max(np.abs(o - outs[0]))) <= 1e-4
+    dims = cfb.ModelDims(1, 32, 2, 8, 0, 16, dtype_bytes=4)
+    sc = cfb.random_mla_scenario(dims, n_blocks=2, seed=1)
+    res = cfb.run_fused_mla_decode(sc)
+    dense = cp.dense_mla(sc.hidden, sc.w_q, sc.w_up, sc.w_kv, sc.w_down, sc.w_out, sc.kv_cache)
+    assert float(np.max(np.abs(res.output - dense))) <= 1e-5
+
+
+def test_fused_mla_deepseek_preset_dims(golden):
+    """Reference preset (cli.py:47-54): D=2048, 16 heads, H=128, R=512, S=1K, fp16, N=4."""
+    meta, g = golden
+    case = next(c for c in meta["cases"] if c["name"] == "dsv2_full_s1k_n4")
+    sc = _scenario(case)
+    res = cfb.run_fused_mla_decode(sc)
+    ref = g["dsv2_full_s1k_n4/output"]
+    assert float(np.max(np.abs(res.output - ref))) <= 3e-2
+    if "dsv2_full_s1k_n4/dense" in g.files:
+        dense = g["dsv2_full_s1k_n4/dense"]
+        assert float(np.max(np.abs(res.output - dense))) <= 2e-2 and _rel(res.output, dense) <= 1e-2
+    assert res.stage_traffic == case["stage_traffic"]
+
+
+def test_fused_mla_bit_identical_replay():
+    dims = cfb.ModelDims(1, 256, 4, 64, 100, 128, dtype_bytes=2)
+    a = cfb.run_fused_mla_decode(cfb.random_mla_scenario(dims, 4, seed=3))
+    b = cfb.run_fused_mla_decode(cfb.random_mla_scenario(dims, 4, seed=3))
+    assert np.array_equal(a.output, b.output)
