@@ -157,6 +157,29 @@ typedef struct cfb_mla_args {
 int cfb_mla_decode(const cfb_mla_args* args, void* stream);
 
 /*
+ * split_head attention module (dataflows.py:432-502): one cluster of N CTAs
+ * per head, head-dim partition throughout; reduce payloads B x (S+B) scores
+ * and B x D projections (CFB_ERR_SMEM when they exceed shared memory).
+ * Reference layouts (T): x [B][D], w_qkv [n_heads][D][3H], w_out
+ * [n_heads][H][D], k/v_cache [n_heads][S][H].  accum/out/stats/traffic as
+ * cfb_mha_args; flags: CFB_APPEND.
+ */
+typedef struct cfb_splithead_args {
+  int dtype;
+  int batch, hidden, n_heads, head_dim, cluster, seq_len, flags;
+  const void* x;
+  const void* w_qkv;
+  const void* w_out;
+  const void* k_cache;
+  const void* v_cache;
+  float* out;
+  unsigned long long* accum;
+  float* stats;
+  unsigned long long* traffic;
+} cfb_splithead_args;
+int cfb_splithead_decode(const cfb_splithead_args* args, void* stream);
+
+/*
  * Fused SwiGLU FFN (one launch, persistent grid, one CTA per SM):
  *   out = [r +] (silu(h w1^T) * (h w2^T)) w3^T,  h = x or f16(rmsnorm(r) * norm_w),
  *   r = resid [+ accum * 2^-32]  (accum: the attention module's fixed-point head

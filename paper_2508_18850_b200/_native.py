@@ -103,6 +103,15 @@ class MlaArgs(ctypes.Structure):
                            "stats", "traffic")]
 
 
+class SplitHeadArgs(ctypes.Structure):
+    """Mirror of ``cfb_splithead_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "n_heads", "head_dim",
+                                             "cluster", "seq_len", "flags")] + [
+        (n, _vp) for n in ("x", "w_qkv", "w_out", "k_cache", "v_cache", "out", "accum", "stats",
+                           "traffic")]
+
+
 class FfnArgs(ctypes.Structure):
     """Mirror of ``cfb_ffn_args``."""
 
@@ -123,6 +132,8 @@ class LmArgs(ctypes.Structure):
 def bind_extra(L) -> None:
     L.cfb_mla_decode.argtypes = [ctypes.POINTER(MlaArgs), _vp]
     L.cfb_mla_decode.restype = ctypes.c_int
+    L.cfb_splithead_decode.argtypes = [ctypes.POINTER(SplitHeadArgs), _vp]
+    L.cfb_splithead_decode.restype = ctypes.c_int
     L.cfb_ffn_decode.argtypes = [ctypes.POINTER(FfnArgs), _vp]
     L.cfb_ffn_decode.restype = ctypes.c_int
     L.cfb_lm_head_argmax.argtypes = [ctypes.POINTER(LmArgs), _vp]

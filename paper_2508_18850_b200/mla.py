@@ -126,3 +126,60 @@ def run_fused_mla_decode(scenario, stats_mode: str = TWO_PASS,
                         score_max=np.ascontiguousarray(st[:, 0, :]),
                         score_sum=np.ascontiguousarray(st[:, 1, :]), collectives=traces,
                         n_clusters=nh, n_blocks=n, device_traffic=device_traffic)
+
+
+def run_splithead_decode(scenario, append_new_token: bool = True) -> DecodeResult:
+    """split_head dataflow on the GPU (``dataflows.py:432-502``)."""
+    import torch
+    from .fused import SPLIT_HEAD
+    validate_partitioning(scenario, SPLIT_HEAD, append_new_token)
+    validate_scenario(scenario)
+    dev = _native.require_cuda()
+    d = scenario.dims
+    n, nb = scenario.cluster.n_blocks, d.dtype_bytes
+    B, D, nh, H, S = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.seq_len
+    dt = torch.float16 if nb == 2 else torch.float32
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev).to(dt)
+
+    with torch.no_grad():
+        x, wqkv, wo = up(scenario.hidden), up(scenario.w_qkv), up(scenario.w_out)
+        kc = up(scenario.k_cache) if S else torch.zeros(1, device=dev, dtype=dt)
+        vc = up(scenario.v_cache) if S else torch.zeros(1, device=dev, dtype=dt)
+        out = torch.empty(B, D, device=dev, dtype=torch.float32)
+        accum = torch.zeros(B, D, device=dev, dtype=torch.int64)
+        stats = torch.zeros(nh, 2, B, device=dev, dtype=torch.float32)
+        traffic = torch.zeros(16, device=dev, dtype=torch.int64)
+        args = _native.SplitHeadArgs(
+            dtype=nb, batch=B, hidden=D, n_heads=nh, head_dim=H, cluster=n, seq_len=S,
+            flags=_native.APPEND if append_new_token else 0, x=x.data_ptr(),
+            w_qkv=wqkv.data_ptr(), w_out=wo.data_ptr(), k_cache=kc.data_ptr(),
+            v_cache=vc.data_ptr(), out=out.data_ptr(), accum=accum.data_ptr(),
+            stats=stats.data_ptr(), traffic=traffic.data_ptr())
+        _native.check(_native.lib().cfb_splithead_decode(args, _native.stream_ptr()))
+        torch.cuda.synchronize()
+        out_np = out.cpu().numpy()
+        st = stats.cpu().numpy()
+        dev_traffic = traffic.cpu().numpy()
+
+    ledger = TrafficLedger()
+    stage_traffic: dict[str, int] = {}
+    traces = []
+    att = S + (B if append_new_token else 0)
+    for head in range(nh):
+        tr = [("score_reduce", emit_reduce(ledger, n, B * att * nb)),
+              ("out_proj_reduce", emit_reduce(ledger, n, B * D * nb))]
+        for stage, t in tr:
+            stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
+            traces.append(StageTrace(stage, head, t))
+        for _ in range(B):  # rank 0 writes the full head output once per row
+            ledger.record(-1, 0, -1, D * nb, "global")
+    device_traffic = {"score_reduce": int(dev_traffic[9]), "out_proj_reduce": int(dev_traffic[10])}
+    if device_traffic != stage_traffic:
+        raise SimulationError(f"kernel DSMEM byte counters {device_traffic} disagree with the "
+                              f"schedule {stage_traffic}")
+    return DecodeResult(output=_finish_output(out_np), ledger=ledger, stage_traffic=stage_traffic,
+                        score_max=np.ascontiguousarray(st[:, 0, :]),
+                        score_sum=np.ascontiguousarray(st[:, 1, :]), collectives=traces,
+                        n_clusters=nh, n_blocks=n, device_traffic=device_traffic)

@@ -112,3 +112,39 @@ def test_fused_mla_bit_identical_replay():
     a = cfb.run_fused_mla_decode(cfb.random_mla_scenario(dims, 4, seed=3))
     b = cfb.run_fused_mla_decode(cfb.random_mla_scenario(dims, 4, seed=3))
     assert np.array_equal(a.output, b.output)
+
+
+# ----------------------------------------------------------------- split_head
+def _mha_scenario(case):
+    d = case["dims"]
+    dims = cfb.ModelDims(d["B"], d["D"], d["n_heads"], d["H"], d["S"], d.get("rank"), d["dtype_bytes"])
+    return cfb.random_mha_scenario(dims, case["n_blocks"], case["seed"])
+
+
+def test_split_head_matches_reference_golden(golden):
+    meta, g = golden
+    n_checked = 0
+    for case in meta["cases"]:
+        if case["kind"] != "split_head":
+            continue
+        sc = _mha_scenario(case)
+        append = case.get("append_new_token", True)
+        res = cfb.run_dataflow("split_head", sc, append_new_token=append)
+        name = case["name"]
+        ref = g[f"{name}/output"]
+        if case["dims"]["dtype_bytes"] == 4:
+            assert float(np.max(np.abs(res.output - ref))) <= 1e-5, name
+            np.testing.assert_allclose(res.score_max, g[f"{name}/score_max"], atol=1e-5)
+            np.testing.assert_allclose(res.score_sum, g[f"{name}/score_sum"], rtol=1e-5)
+        else:
+            assert float(np.max(np.abs(res.output - ref))) <= 3e-2, name
+            arrs = {k: getattr(sc, k) for k in ("hidden", "w_qkv", "w_out", "k_cache", "v_cache")}
+            o32, sm, ss = cp.split_head(arrs, case["n_blocks"], 2, append, head_accum="f32")
+            assert float(np.max(np.abs(res.output - o32))) <= 2e-3, name
+            np.testing.assert_allclose(res.score_max, sm, atol=2e-3)
+        assert res.stage_traffic == case["stage_traffic"], name
+        assert res.dsmem_bytes == case["dsmem_bytes"], name
+        assert res.ledger.channel_bytes("global") == case["global_bytes"], name
+        assert cfb.reconcile_traffic("split_head", res, sc.dims).reconciled, name
+        n_checked += 1
+    assert n_checked >= 40
