@@ -13,6 +13,8 @@
  *   cfb_mla_decode         <- dataflows.py:316-429  run_fused_mla_decode  (fused_mla, App. B.1)
  *   cfb_splithead_decode   <- dataflows.py:432-502  run_splithead_decode  (split_head, App. B.2)
  *   cfb_ffn_decode         <- oracle.py:112-131     ffn_reference(..., "silu") fused into one launch
+ *   cfb_moe_decode         <- no reference counterpart: DeepSeek-V2 MoE
+ *                            (transformers DeepseekV2Moe semantics, oracle/deepseek_port.py)
  *   cfb_cluster_collective <- collectives.py:110-203 cluster_reduce / cluster_gather (DSMEM KAT kernel)
  *   cfb_lm_head_argmax, cfb_embed, cfb_llama_*  <- no reference counterpart (SPEC.md:298 non-goals);
  *                            the north-star decode loop around the fused modules.
@@ -135,7 +137,8 @@ int cfb_mha_decode(const cfb_mha_args* args, void* stream);
  *   w_out   [n_heads][N][D/N][Hp]    as cfb_mha_args.w_out
  *   cache   [seq_len][Rp]            latent rows (shared by all heads)
  *   accum / out / stats / traffic as cfb_mha_args; flags: CFB_APPEND,
- *   CFB_STATS_MERGED, CFB_PDL.  Batch <= 4.
+ *   CFB_STATS_MERGED, CFB_PDL, CFB_NORM (x = f16(rmsnorm(resid) * norm_w),
+ *   resid [B][D] fp32, norm_w [D] T; x unused).  Batch <= 4.
  * "Chunk-rotated": logical 16-byte chunk k of row g stored at (k + g) mod nch.
  */
 typedef struct cfb_mla_args {
@@ -153,6 +156,9 @@ typedef struct cfb_mla_args {
   unsigned long long* accum;
   float* stats;
   unsigned long long* traffic;
+  const float* resid;
+  const void* norm_w;
+  float eps;
 } cfb_mla_args;
 int cfb_mla_decode(const cfb_mla_args* args, void* stream);
 
@@ -203,6 +209,41 @@ typedef struct cfb_ffn_args {
   unsigned long long* trace;   /* [grid CTAs][8] %globaltimer phase stamps (profiling), or NULL */
 } cfb_ffn_args;
 int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
+
+/*
+ * Fused DeepSeek-V2 MoE (one launch, persistent grid, one CTA per SM):
+ *   h = x or f16(rmsnorm(r) * norm_w), r = resid [+ accum_in * 2^-32]
+ *   p = softmax(h W_r^T); top_k experts by p (ties: lower id), w = p * routed_scale
+ *   y = sum_k w_k down_k(f16(silu(gate_k h) * up_k h)) + shared(h)
+ *   out = [r +] y          (CFB_RESID; out may alias resid; accum_in re-zeroed)
+ * fp16 only, batch <= 4, n_experts <= 256, top_k <= 16, hidden a multiple of 8
+ * up to 512 or one of 1024/2048/4096.  Layouts (fp16), Q = max(1, hidden/512):
+ *   w_router [E][D]
+ *   w_gu     [E][inter/2][D/8][4][8]   row tiles (gate 2t, gate 2t+1, up 2t, up 2t+1)
+ *   w_dn     [E][inter/8][Q][8][D/Q]   blocks of W_down^T: 8 intermediate rows x D/Q
+ *   s_gu / s_dn: shared experts (width shared_inter = n_shared * inter), same layouts
+ *   accum    [B][D] u64 workspace, zero before first use (re-zeroed)
+ *   barrier  one u64, zero before first use; route_idx/route_w [B][top_k] (nullable)
+ */
+typedef struct cfb_moe_args {
+  int dtype, batch, hidden, n_experts, top_k, inter, shared_inter, flags, grid;
+  float eps, routed_scale;
+  const void* x;
+  const float* resid;
+  unsigned long long* accum_in;
+  const void* norm_w;
+  const void* w_router;
+  const void* w_gu;
+  const void* w_dn;
+  const void* s_gu;
+  const void* s_dn;
+  unsigned long long* accum;
+  float* out;
+  int* route_idx;
+  float* route_w;
+  unsigned long long* barrier;
+} cfb_moe_args;
+int cfb_moe_decode(const cfb_moe_args* args, void* stream);
 
 /* Final RMSNorm + LM head + greedy argmax (first index of the max, numpy
  * semantics).  w [V][D] T; logits [B][V] fp32 (nullable); cand_* [grid][B]

@@ -14,6 +14,7 @@ from .fused import (DATAFLOW_KINDS, FUSED_MLA, MERGED, SPLIT_HEAD, SPLIT_TOKEN, 
                     TWO_PASS, DecodeResult, cluster_collective, run_dataflow,
                     run_fused_mha_decode, sequence_segments, validate_partitioning)
 from .mla import run_fused_mla_decode, run_splithead_decode  # noqa: F401
+from .moe import MoeWeights, pack_moe, run_moe_decode  # noqa: F401
 from .ledger import (CollectiveTrace, StageTrace, TrafficBreakdown, TrafficEntry,  # noqa: F401
                      TrafficEvent, TrafficLedger, dataflow_traffic, reconcile_traffic,
                      traffic_gather, traffic_reduce)

@@ -100,7 +100,7 @@ class MlaArgs(ctypes.Structure):
                                              "head_pad", "kv_rank", "rank_pad", "cluster",
                                              "seq_len", "flags")] + [
         (n, _vp) for n in ("x", "w_q", "w_kv", "w_up", "w_down", "w_out", "cache", "out", "accum",
-                           "stats", "traffic")]
+                           "stats", "traffic", "resid", "norm_w")] + [("eps", ctypes.c_float)]
 
 
 class SplitHeadArgs(ctypes.Structure):
@@ -129,7 +129,19 @@ class LmArgs(ctypes.Structure):
         ("step_pos", _vp)]
 
 
+class MoeArgs(ctypes.Structure):
+    """Mirror of ``cfb_moe_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("dtype", "batch", "hidden", "n_experts", "top_k",
+                                             "inter", "shared_inter", "flags", "grid")] + [
+        ("eps", ctypes.c_float), ("routed_scale", ctypes.c_float)] + [
+        (n, _vp) for n in ("x", "resid", "accum_in", "norm_w", "w_router", "w_gu", "w_dn", "s_gu",
+                           "s_dn", "accum", "out", "route_idx", "route_w", "barrier")]
+
+
 def bind_extra(L) -> None:
+    L.cfb_moe_decode.argtypes = [ctypes.POINTER(MoeArgs), _vp]
+    L.cfb_moe_decode.restype = ctypes.c_int
     L.cfb_mla_decode.argtypes = [ctypes.POINTER(MlaArgs), _vp]
     L.cfb_mla_decode.restype = ctypes.c_int
     L.cfb_splithead_decode.argtypes = [ctypes.POINTER(SplitHeadArgs), _vp]

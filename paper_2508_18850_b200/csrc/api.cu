@@ -51,6 +51,10 @@ int cfb_ffn_decode(const cfb_ffn_args* args, void* stream) {
   return cfb::ffn_decode(args, static_cast<cudaStream_t>(stream));
 }
 
+int cfb_moe_decode(const cfb_moe_args* args, void* stream) {
+  return cfb::moe_decode(args, static_cast<cudaStream_t>(stream));
+}
+
 int cfb_lm_head_argmax(const cfb_lm_args* args, void* stream) {
   return cfb::lm_head_argmax(args, static_cast<cudaStream_t>(stream));
 }

@@ -30,8 +30,10 @@ namespace cfb {
 
 struct MlaParams {
   int B, D, H, Hp, R, Rp, rsp, N, n_heads, S, flags, spw, sleep_max;
-  float inv_sqrt_r;
+  float inv_sqrt_r, eps;
   const void* x;
+  const float* resid;   // [B][D] fp32 (CFB_NORM)
+  const void* norm_w;   // [D] T (CFB_NORM)
   const void* w_q;    // [head][rank][tiles of h rows][D] row tiles
   const void* w_kv;   // [rank][tiles of rs rows][D] row tiles
   const void* w_up;   // [head][rank][rs rows][Hp] chunk-rotated (W_up^T slice)
@@ -129,6 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_fused_kernel(const MlaParams 
   }
   __syncthreads();
   cluster_arrive();
+  pdl_launch_dependents();
 
   const int S = p.S;
   const int seg = S == 0 ? 0 : (S + (int)N - 1) / (int)N;
@@ -177,7 +180,12 @@ __global__ void __launch_bounds__(kThreads, 1) mla_fused_kernel(const MlaParams 
   T* dbuf = reinterpret_cast<T*>(smem + L.dbuf);
   unsigned long long sent[CFB_STAGE_COUNT] = {};  // logical DSMEM bytes per cfb_stage
 
-  load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
+  pdl_wait();  // activations come from the stream predecessor (PDL)
+  if (p.flags & CFB_NORM)
+    rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps,
+                           reinterpret_cast<float*>(smem + L.red), tid);
+  else
+    load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
 
   // 1. q-proj and latent down-projection slices
   int cnt = 0;
@@ -539,7 +547,9 @@ int mla_decode(const cfb_mla_args* a, cudaStream_t st) {
   if (a->seq_len < 0) return set_error(CFB_ERR_DIMENSION, "seq_len must be >= 0");
   if (a->seq_len == 0 && !(a->flags & CFB_APPEND))
     return set_error(CFB_ERR_DIMENSION, "no attended positions: empty cache and no appended token");
-  if (!a->x || !a->w_q || !a->w_kv || !a->w_up || !a->w_down || !a->w_out || !a->cache || !a->accum)
+  if ((a->flags & CFB_NORM) && (!a->resid || !a->norm_w))
+    return set_error(CFB_ERR_ARGUMENT, "CFB_NORM needs resid and norm_w");
+  if ((!(a->flags & CFB_NORM) && !a->x) || !a->w_q || !a->w_kv || !a->w_up || !a->w_down || !a->w_out || !a->cache || !a->accum)
     return set_error(CFB_ERR_ARGUMENT, "null input / weight / accumulator pointer");
   const int rs = a->kv_rank / N, h = a->head_dim / N;
   const int rsp = pow2_ge(rs, 16 / tb);
@@ -566,6 +576,9 @@ int mla_decode(const cfb_mla_args* a, cudaStream_t st) {
   p.sleep_max = tuned_sleep();
   p.inv_sqrt_r = (float)(1.0 / std::sqrt((double)a->kv_rank));
   p.x = a->x;
+  p.resid = a->resid;
+  p.norm_w = a->norm_w;
+  p.eps = a->eps;
   p.w_q = a->w_q;
   p.w_kv = a->w_kv;
   p.w_up = a->w_up;

@@ -56,6 +56,7 @@ int mha_finalize(float* out, const float* resid, unsigned long long* accum, int 
 int mla_decode(const cfb_mla_args* a, cudaStream_t st);
 int splithead_decode(const cfb_splithead_args* a, cudaStream_t st);
 int ffn_decode(const cfb_ffn_args* a, cudaStream_t st);
+int moe_decode(const cfb_moe_args* a, cudaStream_t st);
 int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st);
 int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
           cudaStream_t st, bool pdl = false);

@@ -160,7 +160,8 @@ def _struct_fields(text, name):
 
 @pytest.mark.parametrize("cname,pyname", [("cfb_mha_args", "MhaArgs"), ("cfb_ffn_args", "FfnArgs"),
                                           ("cfb_lm_args", "LmArgs"), ("cfb_mla_args", "MlaArgs"),
-                                          ("cfb_splithead_args", "SplitHeadArgs")])
+                                          ("cfb_splithead_args", "SplitHeadArgs"),
+                                          ("cfb_moe_args", "MoeArgs")])
 def test_abi_struct_layout_matches_header(cname, pyname):
     """ctypes mirrors must have the field order of the C structs."""
     text = (ROOT / "include" / "cfb.h").read_text()
@@ -182,3 +183,19 @@ def test_wo_rows_layout():
                 for k in range(4):
                     p = (k + g) % 4
                     assert torch.equal(t[h, r, g, p * 8:(p + 1) * 8], w[h, r * 6 + g, k * 8:(k + 1) * 8])
+
+
+def test_moe_down_blocks_layout():
+    """W_down (D, F) -> [F/8][Q][8][D/Q]: block (g, q) row r = W_down^T row
+    8g + r, columns q*D/Q .. (q+1)*D/Q."""
+    import torch
+    from paper_2508_18850_b200.moe import down_blocks, moe_segments
+    for D, F in ((64, 16), (1024, 24), (2048, 16)):
+        Q = moe_segments(D)
+        w = torch.arange(D * F, dtype=torch.float32).reshape(D, F)
+        t = down_blocks(w)
+        assert t.shape == (F // 8, Q, 8, D // Q)
+        for g in range(F // 8):
+            for q in range(Q):
+                for r in range(8):
+                    assert torch.equal(t[g, q, r], w[q * D // Q:(q + 1) * D // Q, 8 * g + r])
