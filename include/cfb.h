@@ -223,7 +223,10 @@ int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
  *   w_dn     [E][inter/8][Q][8][D/Q]   blocks of W_down^T: 8 intermediate rows x D/Q
  *   s_gu / s_dn: shared experts (width shared_inter = n_shared * inter), same layouts
  *   accum    [B][D] u64 workspace, zero before first use (re-zeroed)
- *   barrier  one u64, zero before first use; route_idx/route_w [B][top_k] (nullable)
+ *   barrier  two u64 (grid barrier, route counter), zero before first use; both are
+ *            monotonic, so a workspace must always be used with the same grid
+ *   logits   [B][E] fp32 workspace: router logits of the last launch
+ *   route_idx/route_w [B][top_k] (nullable): selected experts / gate weights
  */
 typedef struct cfb_moe_args {
   int dtype, batch, hidden, n_experts, top_k, inter, shared_inter, flags, grid;
@@ -242,6 +245,8 @@ typedef struct cfb_moe_args {
   int* route_idx;
   float* route_w;
   unsigned long long* barrier;
+  float* logits;
+  unsigned long long* trace;   /* [grid CTAs][16] clock64 phase stamps (profiling), or NULL */
 } cfb_moe_args;
 int cfb_moe_decode(const cfb_moe_args* args, void* stream);
 

@@ -19,8 +19,8 @@
 // down-projection contribution of those 8 columns to all D outputs
 // (split-K), which it adds into a 64-bit fixed-point accumulator with
 // red.global.add - integer adds, so the result is independent of CTA order.
-// A final grid barrier lets every CTA finish its slice of the output
-// (out = resid + attention sum + MoE sum) and re-zero the accumulators.
+// The last CTA to finish (a ticket on a monotonic counter) writes the output
+// (out = resid + attention sum + MoE sum) and re-zeroes the accumulators.
 //
 // Router: every CTA computes all E logits itself from the (L2-resident)
 // router matrix while its producer warp already streams the shared experts,
@@ -46,6 +46,7 @@ namespace cfb {
 constexpr int kMoeMaxExperts = 256;
 constexpr int kMoeMaxTopK = 16;
 constexpr int kMoeMaxBatch = 4;
+constexpr int kMoeChunk = 16;  // gate/up groups per GEMV phase (bounds the partial buffer)
 
 struct MoeParams {
   int B, D, E, K, Fe, Fs, Q, flags, spw, sleep_max;
@@ -63,12 +64,14 @@ struct MoeParams {
   float* out;
   int* route_idx;
   float* route_w;
-  unsigned long long* barrier;
+  unsigned long long* barrier;  // [0] finished CTAs, [1] published router rows (monotonic)
+  float* logits;               // [B][E] router logits (workspace)
+  unsigned long long* trace;  // [grid][16] %globaltimer phase stamps (profiling) or null
 };
 
 struct MoeLayout {
-  int bars, xs, logit, sel, slot, gw, tk, gu, part, act, dpart, red, total;
-  int max_groups, umax;
+  int bars, rrow, xs, logit, slot, gw, tk, gu, part, act, dpart, red, total;
+  int max_groups, umax, rrows;  // rrows: router rows prefetched into smem (0: read via L2)
 };
 
 __host__ __device__ inline int moe_r16(int x) { return (x + 15) & ~15; }
@@ -81,18 +84,20 @@ __host__ __device__ inline MoeLayout moe_layout(int B, int D, int E, int K, int 
   const int Tt = Gs + L.umax * Ge;
   L.max_groups = (Tt + G - 1) / G + 1;
   int o = ring_bytes(spw);
-  L.bars = o;  o += moe_r16((2 * kNumSlots + 1) * 8);
+  L.bars = o;  o += moe_r16((2 * kNumSlots + 2) * 8);
+  const int rows = (E + G - 1) / G;
+  L.rrows = rows * D * 2 <= 16384 ? rows : 0;
+  L.rrow = o;  o += moe_r16(L.rrows * D * 2);
   L.xs = o;    o += moe_r16(B * D * 2);
-  L.logit = o; o += moe_r16(B * E * 4);
-  L.sel = o;   o += moe_r16(E);
+  L.logit = o; o += moe_r16(2 * B * E * 4);
   L.slot = o;  o += moe_r16((L.umax + 1) * 4);
   L.gw = o;    o += moe_r16(B * L.umax * 4);
   L.tk = o;    o += moe_r16(2 * B * K * 4);
-  L.gu = o;    o += moe_r16(B * 16 * L.max_groups * 4);
-  L.part = o;  o += moe_r16(kNumConsumerWarps * B * 16 * L.max_groups * 4);
-  L.act = o;   o += moe_r16(2 * B * 8 * L.max_groups * 4);
+  L.gu = o;    o += moe_r16(B * 16 * kMoeChunk * 4);
+  L.part = o;  o += moe_r16(kNumConsumerWarps * B * 16 * kMoeChunk * 4);
+  L.act = o;   o += moe_r16(2 * B * 8 * L.max_groups * 2);
   L.dpart = o; o += moe_r16((8 / Q) * B * D * 4);
-  L.red = o;   o += moe_r16(kNumConsumerWarps * B * 4);
+  L.red = o;   o += moe_r16(kNumConsumerWarps * (B > 2 ? B : 2) * 4);
   L.total = o;
   return L;
 }
@@ -113,55 +118,6 @@ __device__ __forceinline__ MoeRange moe_range(int i, int G, int Gs, int Tr) {
   return m;
 }
 
-// top-k (descending logit, ties to the lower expert index) and the softmax
-// probability of each selected expert, for one token row; warp-wide.
-__device__ __forceinline__ void topk_row(const float* lg, int E, int K, float scale, int lane,
-                                         int* idx_out, float* w_out) {
-  constexpr int kPer = kMoeMaxExperts / 32;
-  float v[kPer];
-  float m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k) {
-    const int e = lane + 32 * k;
-    v[k] = e < E ? lg[e] : -INFINITY;
-    m = fmaxf(m, v[k]);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-  float s = 0.f;
-#pragma unroll
-  for (int k = 0; k < kPer; ++k)
-    if (lane + 32 * k < E) s += expf(v[k] - m);
-  s = warp_allsum(s);
-  unsigned taken = 0;
-  for (int j = 0; j < K; ++j) {
-    float bv = -INFINITY;
-    int bi = 0x7fffffff;
-#pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = lane + 32 * k;
-      if (e < E && !(taken >> k & 1u) && (v[k] > bv || (v[k] == bv && e < bi))) {
-        bv = v[k];
-        bi = e;
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > bv || (ov == bv && oi < bi)) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if ((bi & 31) == lane) taken |= 1u << (bi >> 5);
-    if (lane == 0) {
-      idx_out[j] = bi;
-      w_out[j] = __fmul_rn(__fdiv_rn(expf(bv - m), s), scale);
-    }
-  }
-}
-
 template <int QB>
 __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   extern __shared__ __align__(128) char smem[];
@@ -169,59 +125,103 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   const MoeLayout L = moe_layout(B, D, E, K, p.Fe, p.Fs, Q, G, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* route_bar = bars + 2 * kNumSlots;
+  uint64_t* rrow_bar = route_bar + 1;  // router rows landed in smem
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Gs = p.Fs / 8, Ge = p.Fe / 8;
   const int Wd = D / Q;                        // columns per down segment
   const int tileB = 4 * D * 2;                 // gate/up tile: 4 rows x D fp16
   const int blkB = 16 * Wd;                    // down block: 8 rows x Wd fp16
-  const size_t eGu = (size_t)(p.Fe / 2) * 4 * D, eDn = (size_t)Ge * 8 * D;  // elements per expert
+  const size_t eGu = (size_t)Ge * 16 * D, eDn = (size_t)Ge * 8 * D;  // elements per expert
   int* slot_e = reinterpret_cast<int*>(smem + L.slot);  // [umax] expert ids, [umax] = U
   if (tid == 0) {
     ring_init(ring);
     mbar_init(route_bar, 1);
+    mbar_init(rrow_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   const MoeRange rs = moe_range(i, G, Gs, 0);  // shared part is routing-independent
-  const Phase GUs = make_phase(p.s_gu + (size_t)rs.s0 * 4 * 4 * D, nullptr, 4 * (rs.s1 - rs.s0),
-                               tileB, true);
-  const Phase DNs = make_phase(p.s_dn + (size_t)rs.s0 * 8 * D, nullptr, Q * (rs.s1 - rs.s0), blkB);
-  auto routed_phase = [&](const MoeRange& m, int u, bool down) {
-    const int ga = max(m.r0, u * Ge) - u * Ge, gb = min(m.r1, (u + 1) * Ge) - u * Ge;
-    const int e = slot_e[u];
-    if (down)
-      return make_phase(p.w_dn + e * eDn + (size_t)ga * 8 * D, nullptr, Q * (gb - ga), blkB);
-    return make_phase(p.w_gu + e * eGu + (size_t)ga * 4 * 4 * D, nullptr, 4 * (gb - ga), tileB, true);
+  // phases: gate/up tiles of groups [g0, g0 + ng) (<= kMoeChunk groups per
+  // phase, so the cross-warp partial buffer stays small), down blocks
+  auto gu_phase = [&](const __half* base, int g0, int ng) {
+    return make_phase(base + (size_t)g0 * 16 * D, nullptr, 4 * ng, tileB, true);
+  };
+  auto dn_phase = [&](const __half* base, int g0, int ng) {
+    return make_phase(base + (size_t)g0 * 8 * D, nullptr, Q * ng, blkB);
+  };
+  // routed segment u of this CTA's range: expert slot_e[u], groups [ga, gb) of it
+  auto seg = [&](const MoeRange& m, int u, int& ga, int& gb) {
+    ga = max(m.r0, u * Ge) - u * Ge;
+    gb = min(m.r1, (u + 1) * Ge) - u * Ge;
+    return slot_e[u];
   };
   pdl_launch_dependents();
 
-  if (warp == kNumConsumerWarps) {  // producer
+  if (warp == kNumConsumerWarps) {  // ------------------------------ producer
     const uint64_t pol = policy_evict_first();
     int c = 0;
-    const Phase ps[2] = {GUs, DNs};
-    produce_all(ps, ring, lane, pol, c);
-    mbar_wait(route_bar, 0);
+    if (lane == 0 && L.rrows) {  // this CTA's router rows e = i, i + G, ... first
+      int n = 0;
+      for (int e = i; e < E; e += G) ++n;
+      mbar_arrive_expect_tx(rrow_bar, (uint32_t)(n * D * 2));
+      n = 0;
+      for (int e = i; e < E; e += G, ++n)
+        bulk_g2s(smem + L.rrow + (size_t)n * D * 2, p.w_router + (size_t)e * D, D * 2, rrow_bar,
+                 policy_evict_last());  // router rows stay L2-resident across steps
+    }
+    for (int g = rs.s0; g < rs.s1; g += kMoeChunk) {
+      const Phase ph[1] = {gu_phase(p.s_gu, g, min(kMoeChunk, rs.s1 - g))};
+      produce_all(ph, ring, lane, pol, c);
+    }
+    {
+      const Phase ph[1] = {dn_phase(p.s_dn, rs.s0, rs.s1 - rs.s0)};
+      produce_all(ph, ring, lane, pol, c);
+    }
+    if (lane == 0)  // routing (consumer warps) -> expert list in smem
+      while (!mbar_test(route_bar, 0)) __nanosleep(64);
+    __syncwarp();
     const int U = slot_e[L.umax];
     const MoeRange m = moe_range(i, G, Gs, U * Ge);
-    for (int pass = 0; pass < 2; ++pass)
-      for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
-        const Phase ph[1] = {routed_phase(m, u, pass == 1)};
+    for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
+      int ga, gb;
+      const int e = seg(m, u, ga, gb);
+      for (int g = ga; g < gb; g += kMoeChunk) {
+        const Phase ph[1] = {gu_phase(p.w_gu + e * eGu, g, min(kMoeChunk, gb - g))};
         produce_all(ph, ring, lane, pol, c);
       }
+    }
+    for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
+      int ga, gb;
+      const int e = seg(m, u, ga, gb);
+      const Phase ph[1] = {dn_phase(p.w_dn + e * eDn, ga, gb - ga)};
+      produce_all(ph, ring, lane, pol, c);
+    }
     return;
   }
 
+  // ---------------------------------------------------------------- consumers
   pdl_wait();
+  unsigned long long* tr = p.trace ? p.trace + (size_t)i * 16 : nullptr;
+  auto stamp = [&](int k) {  // SM cycle counter (globaltimer is too coarse on B200)
+    if (tr && tid == 0) tr[k] = clock64();
+  };
+  stamp(0);
+  // launch epoch: barrier[0] counts finished CTAs (G per launch); no CTA of
+  // this launch can finish before every CTA has published its router rows
+  const unsigned long long epoch =
+      tid == 0 ? ld_acquire_u64(p.barrier) / (unsigned long long)G : 0ull;
   __half* xs = reinterpret_cast<__half*>(smem + L.xs);
-  float* logit = reinterpret_cast<float*>(smem + L.logit);
-  unsigned char* sel = reinterpret_cast<unsigned char*>(smem + L.sel);
-  float* gw = reinterpret_cast<float*>(smem + L.gw);     // [B][umax]
-  float* gu = reinterpret_cast<float*>(smem + L.gu);     // [B][16 * groups]
+  float* lg = reinterpret_cast<float*>(smem + L.logit);   // [2][B][E]: logits, gate weights
+  float* gw = reinterpret_cast<float*>(smem + L.gw);      // [B][umax]
+  float* gu = reinterpret_cast<float*>(smem + L.gu);      // [B][16 * kMoeChunk]
   float* part = reinterpret_cast<float*>(smem + L.part);
-  float* act = reinterpret_cast<float*>(smem + L.act);   // [B][8 * groups] (x2: shared, routed)
+  __half* act = reinterpret_cast<__half*>(smem + L.act);  // [2][B][8 * max_groups] fp16
   float* dpart = reinterpret_cast<float*>(smem + L.dpart);
   float* red = reinterpret_cast<float*>(smem + L.red);
+  const int act_ld = 8 * L.max_groups;
+  __half* act_s = act;
+  __half* act_r = act + B * act_ld;
 
   // 0. activations: x = f16(rmsnorm(resid [+ attention sum]) * g), or x
   if ((p.flags & CFB_NORM) && p.accum_in) {
@@ -242,101 +242,58 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   } else {
     load_act_to_smem<__half, true>(xs, p.x, B, D, tid);
   }
+  stamp(1);
 
-  // 1. router logits (fp32), every CTA: warp w takes experts w, w+8, ...
+  // 1. router rows e = i, i + G, ... of this CTA (fp32 logits, all 8 warps
+  //    split D), published to global memory + the launch's route counter
   {
     const int nch = D / 8;
-    for (int e0 = warp; e0 < E; e0 += 2 * kNumConsumerWarps) {
-      const int e1 = e0 + kNumConsumerWarps;
-      float a0[QB], a1[QB];
+    int rows = 0;
+    if (L.rrows && i < E) mbar_wait(rrow_bar, 0);
+    for (int e = i; e < E; e += G, ++rows) {
+      const uint4* wr = reinterpret_cast<const uint4*>(p.w_router + (size_t)e * D);
+      const uint4* ws = reinterpret_cast<const uint4*>(smem + L.rrow + (size_t)rows * D * 2);
+      float a[QB];
 #pragma unroll
-      for (int b = 0; b < QB; ++b) a0[b] = a1[b] = 0.f;
-      const uint4* r0 = reinterpret_cast<const uint4*>(p.w_router + (size_t)e0 * D);
-      const uint4* r1 = reinterpret_cast<const uint4*>(p.w_router + (size_t)(e1 < E ? e1 : e0) * D);
-      for (int c0 = 0; c0 < nch; c0 += 32 * 4) {
-        uint4 w0[4], w1[4];
+      for (int b = 0; b < QB; ++b) a[b] = 0.f;
+      for (int c = tid; c < nch; c += kConsumerThreads) {
+        const uint4 wv = L.rrows ? ws[c] : __ldg(wr + c);
+        const uint32_t q[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = c0 + lane + 32 * k;
-          w0[k] = c < nch ? __ldg(r0 + c) : make_uint4(0, 0, 0, 0);
-          w1[k] = c < nch ? __ldg(r1 + c) : make_uint4(0, 0, 0, 0);
-        }
+        for (int b = 0; b < QB; ++b) {
+          if (b < B) {
+            const uint4 xv = lds128(xs + (size_t)b * D + c * 8);
+            const uint32_t xr[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = c0 + lane + 32 * k;
-          if (c < nch) {
-#pragma unroll
-            for (int b = 0; b < QB; ++b) {
-              if (b < B) {
-                const uint4 xv = lds128(xs + (size_t)b * D + c * 8);
-                const uint32_t xr[4] = {xv.x, xv.y, xv.z, xv.w};
-                const uint32_t q0[4] = {w0[k].x, w0[k].y, w0[k].z, w0[k].w};
-                const uint32_t q1[4] = {w1[k].x, w1[k].y, w1[k].z, w1[k].w};
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  a0[b] = fma_f16_hi(q0[j], xr[j], fma_f16_lo(q0[j], xr[j], a0[b]));
-                  a1[b] = fma_f16_hi(q1[j], xr[j], fma_f16_lo(q1[j], xr[j], a1[b]));
-                }
-              }
-            }
+            for (int j = 0; j < 4; ++j) a[b] = fma_f16_hi(q[j], xr[j], fma_f16_lo(q[j], xr[j], a[b]));
           }
         }
       }
 #pragma unroll
       for (int b = 0; b < QB; ++b) {
         if (b < B) {
-          const float s0 = warp_allsum(a0[b]), s1 = warp_allsum(a1[b]);
-          if (lane == 0) {
-            logit[b * E + e0] = s0;
-            if (e1 < E) logit[b * E + e1] = s1;
-          }
+          const float sw = warp_allsum(a[b]);
+          if (lane == 0) red[b * kNumConsumerWarps + warp] = sw;
         }
       }
-    }
-  }
-  for (int e = tid; e < E; e += kConsumerThreads) sel[e] = 0;
-  consumer_sync();
-
-  // 2. top-k per token, union of the selected experts (ascending id), gate weights
-  if (warp == 0) {
-    int* s_idx = reinterpret_cast<int*>(smem + L.tk);
-    float* s_w = reinterpret_cast<float*>(s_idx + B * K);
-    for (int b = 0; b < B; ++b) topk_row(logit + b * E, E, K, p.scale, lane, s_idx + b * K, s_w + b * K);
-    __syncwarp();
-    for (int t = lane; t < B * K; t += 32) sel[s_idx[t]] = 1;
-    __syncwarp();
-    int U = 0;
-    for (int base = 0; base < E; base += 32) {
-      const bool f = base + lane < E && sel[base + lane];
-      const unsigned bal = __ballot_sync(0xffffffffu, f);
-      if (f) slot_e[U + __popc(bal & ((1u << lane) - 1u))] = base + lane;
-      U += __popc(bal);
-    }
-    __syncwarp();
-    for (int t = lane; t < B * U; t += 32) gw[(t / U) * L.umax + t % U] = 0.f;
-    __syncwarp();
-    for (int t = lane; t < B * K; t += 32) {
-      const int b = t / K, e = s_idx[t];
-      int u = 0;
-      while (slot_e[u] != e) ++u;
-      gw[b * L.umax + u] = s_w[t];
-    }
-    if (lane == 0) slot_e[L.umax] = U;
-    if (i == 0 && p.route_idx)
-      for (int t = lane; t < B * K; t += 32) {
-        p.route_idx[t] = s_idx[t];
-        if (p.route_w) p.route_w[t] = s_w[t];
+      consumer_sync();
+      if (tid < B) {
+        float v = 0.f;
+        for (int w = 0; w < kNumConsumerWarps; ++w) v += red[tid * kNumConsumerWarps + w];
+        p.logits[tid * E + e] = v;
       }
+      consumer_sync();
+    }
+    if (rows && tid == 0) {
+      __threadfence();
+      atomicAdd(p.barrier + 1, (unsigned long long)rows);
+    }
   }
-  consumer_sync();
-  if (tid == 0) mbar_arrive(route_bar);
-  const int U = slot_e[L.umax];
-  const MoeRange m = moe_range(i, G, Gs, U * Ge);
+  stamp(2);
 
-  // 3. gate/up GEMV over a phase, SwiGLU, scaled activations into act_dst
+  // 2. gate/up GEMV of one chunk, SwiGLU, fp16 activations into act_dst
   int cnt = 0;
-  auto gate_up = [&](const Phase& P, int n_groups, float* act_dst, int act_ld, int f_off,
-                     const float* wgt /* [B] or null: weight 1 */) {
+  auto gate_up = [&](const Phase& P, int n_groups, __half* act_dst) {
     const int rows = 16 * n_groups;
     tiled_gemv_phase<__half, QB, true>(P, ring, warp, lane, tid, cnt, xs, D, B, rows, part,
                                        [&](int row, int b, float v) { gu[b * rows + row] = v; });
@@ -345,13 +302,102 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
       const int b = t / (8 * n_groups), j = t % (8 * n_groups);  // f = 2*tile + e
       const int tl = j >> 1, e = j & 1;
       const float g = gu[b * rows + 4 * tl + e], uu = gu[b * rows + 4 * tl + 2 + e];
-      const float a = __half2float(__float2half_rn(__fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), uu)));
-      act_dst[b * act_ld + f_off + j] = wgt ? __fmul_rn(wgt[b * L.umax], a) : a;
+      act_dst[b * act_ld + j] = __float2half_rn(__fmul_rn(__fdiv_rn(g, __fadd_rn(1.0f, expf(-g))), uu));
     }
     consumer_sync();
   };
 
-  // 4. split-K down projection of a phase's blocks: warp w owns segment w % Q
+  // 3. routing, all consumer threads: rank_b(e) = #{e' : l_e' > l_e or
+  //    (l_e' == l_e and e' < e)}; row b selects e iff rank < K (ties toward
+  //    the lower id) and e lands at top-k position rank.  The union of the
+  //    rows' experts is compacted in ascending id; gw[b][slot] = row b's gate
+  //    weight (softmax probability * scale) or 0.  No dynamically indexed
+  //    register arrays anywhere: with 227 KB of shared memory there is little
+  //    L1 left, and local memory would round-trip to L2.
+  auto route = [&]() {
+    int* s_idx = reinterpret_cast<int*>(smem + L.tk);
+    float* s_w = reinterpret_cast<float*>(s_idx + B * K);
+    float* st = red;  // [B][2] row max, row sum
+    if (tid == 0) {
+      const unsigned long long target = (epoch + 1ull) * (unsigned long long)E;
+      while (ld_acquire_u64(p.barrier + 1) < target) __nanosleep(32);
+    }
+    consumer_sync();
+    stamp(11);
+    for (int t = tid; t < B * E; t += kConsumerThreads) lg[t] = __ldcg(p.logits + t);
+    consumer_sync();
+    stamp(12);
+    if (warp < B) {  // row statistics: warp b
+      const float* l = lg + warp * E;
+      float m = -INFINITY;
+      for (int e = lane; e < E; e += 32) m = fmaxf(m, l[e]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+      float sum = 0.f;
+      for (int e = lane; e < E; e += 32) sum += expf(l[e] - m);
+      sum = warp_allsum(sum);
+      if (lane == 0) {
+        st[2 * warp] = m;
+        st[2 * warp + 1] = sum;
+      }
+    }
+    consumer_sync();
+    // ranks: 4 threads per (row, expert) pair, each comparing a quarter of the row
+    for (int t0 = 0; t0 < 4 * B * E; t0 += kConsumerThreads) {
+      const int t = t0 + tid;
+      const bool valid = t < 4 * B * E;
+      const int pr = valid ? t >> 2 : 0, qt = t & 3;
+      const int b = pr / E, e = pr % E;
+      const float* l = lg + b * E;
+      const float v = l[e];
+      int r = 0;
+      for (int e2 = qt; e2 < E; e2 += 4) {
+        const float o = l[e2];
+        r += (o > v || (o == v && e2 < e)) ? 1 : 0;
+      }
+      r += __shfl_xor_sync(0xffffffffu, r, 1);
+      r += __shfl_xor_sync(0xffffffffu, r, 2);
+      if (valid && qt == 0) {
+        float w = -1.0f;  // marker: not selected by row b
+        if (r < K) {
+          w = __fmul_rn(__fdiv_rn(expf(v - st[2 * b]), st[2 * b + 1]), p.scale);
+          s_idx[b * K + r] = e;
+          s_w[b * K + r] = w;
+        }
+        lg[(B + b) * E + e] = w;
+      }
+    }
+    consumer_sync();
+    stamp(13);
+    if (warp == 0) {
+      int U = 0;
+      for (int base = 0; base < E; base += 32) {
+        const int e = base + lane;
+        bool f = false;
+        for (int b = 0; b < B; ++b) f |= e < E && lg[(B + b) * E + e] >= 0.f;
+        const unsigned bal = __ballot_sync(0xffffffffu, f);
+        if (f) {
+          const int pos = U + __popc(bal & ((1u << lane) - 1u));
+          slot_e[pos] = e;
+          for (int b = 0; b < B; ++b) gw[b * L.umax + pos] = fmaxf(lg[(B + b) * E + e], 0.f);
+        }
+        U += __popc(bal);
+      }
+      if (lane == 0) slot_e[L.umax] = U;
+      if (i == 0 && p.route_idx)
+        for (int t = lane; t < B * K; t += 32) {
+          p.route_idx[t] = s_idx[t];
+          if (p.route_w) p.route_w[t] = s_w[t];
+        }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(route_bar);  // release the expert list to the producer
+    }
+    consumer_sync();
+  };
+
+  // 4. split-K down projection: warp w owns column segment w % Q, lanes own
+  //    fixed columns; fp16 weights x fp16 activations (FHFMA, exact products,
+  //    fp32 sums) per expert segment, then scaled by the gate weight
   constexpr int kCpl = 2;  // 16-byte chunks per lane per block row (Wd <= 512)
   float acc[QB][kCpl][8];
   auto zero_acc = [&] {
@@ -362,106 +408,148 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
 #pragma unroll
         for (int e = 0; e < 8; ++e) acc[b][j][e] = 0.f;
   };
-  auto down = [&](const Phase& P, const float* a_src, int act_ld, int g_off) {
+  auto down = [&](const Phase& P, const __half* a_src, int g_off) {
     const int nch = Wd / 8;
+    const unsigned short* a16 = reinterpret_cast<const unsigned short*>(a_src);
     consume_phase(P, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
       for (int uu = 0; uu < it.nunits; ++uu) {
-        const int unit = it.unit0 + uu;
-        const int gl = unit / Q + g_off;  // local group (seg = unit % Q == warp % Q)
+        const int gl = (it.unit0 + uu) / Q + g_off;  // local group (segment = warp % Q)
         const char* blk = slot + (size_t)uu * blkB;
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
-          float av[QB];
+          uint32_t a2[QB];
 #pragma unroll
-          for (int b = 0; b < QB; ++b) av[b] = b < B ? a_src[b * act_ld + 8 * gl + r] : 0.f;
+          for (int b = 0; b < QB; ++b) {
+            const uint32_t h = b < B ? a16[b * act_ld + 8 * gl + r] : 0u;
+            a2[b] = h | (h << 16);
+          }
 #pragma unroll
           for (int j = 0; j < kCpl; ++j) {
             const int c = lane + 32 * j;
             if (c < nch) {
               const uint4 wv = lds128(blk + ((size_t)r * nch + c) * 16);
-              float wf[8];
-              Elem<__half>::unpack(wv, wf);
+              const uint32_t wr[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
               for (int b = 0; b < QB; ++b)
 #pragma unroll
-                for (int e = 0; e < 8; ++e) acc[b][j][e] = fmaf(wf[e], av[b], acc[b][j][e]);
+                for (int q = 0; q < 4; ++q) {
+                  acc[b][j][2 * q] = fma_f16_lo(wr[q], a2[b], acc[b][j][2 * q]);
+                  acc[b][j][2 * q + 1] = fma_f16_hi(wr[q], a2[b], acc[b][j][2 * q + 1]);
+                }
             }
           }
         }
       }
     });
   };
-  auto flush = [&](bool add) {  // registers -> dpart[warp / Q][b][segment columns]
+  auto flush = [&](const float* wgt, bool add) {  // dpart[warp / Q][b][seg cols] (+)= w_b * acc
     float* dst = dpart + (size_t)(warp / Q) * B * D + (warp % Q) * Wd;
     const int nch = Wd / 8;
 #pragma unroll
     for (int b = 0; b < QB; ++b) {
       if (b < B) {
+        const float w = wgt ? wgt[b * L.umax] : 1.0f;
 #pragma unroll
         for (int j = 0; j < kCpl; ++j) {
           const int c = lane + 32 * j;
           if (c < nch) {
             float4* d4 = reinterpret_cast<float4*>(dst + (size_t)b * D + c * 8);
-            float4 v0 = make_float4(acc[b][j][0], acc[b][j][1], acc[b][j][2], acc[b][j][3]);
-            float4 v1 = make_float4(acc[b][j][4], acc[b][j][5], acc[b][j][6], acc[b][j][7]);
+            float o[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
             if (add) {
               const float4 o0 = d4[0], o1 = d4[1];
-              v0 = make_float4(o0.x + v0.x, o0.y + v0.y, o0.z + v0.z, o0.w + v0.w);
-              v1 = make_float4(o1.x + v1.x, o1.y + v1.y, o1.z + v1.z, o1.w + v1.w);
+              o[0] = o0.x; o[1] = o0.y; o[2] = o0.z; o[3] = o0.w;
+              o[4] = o1.x; o[5] = o1.y; o[6] = o1.z; o[7] = o1.w;
             }
-            d4[0] = v0;
-            d4[1] = v1;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = fmaf(w, acc[b][j][e], o[e]);
+            d4[0] = make_float4(o[0], o[1], o[2], o[3]);
+            d4[1] = make_float4(o[4], o[5], o[6], o[7]);
           }
         }
       }
     }
   };
 
-  float* act_s = act;
-  float* act_r = act + B * 8 * L.max_groups;
-  const int ns = rs.s1 - rs.s0, nr = m.r1 - m.r0;
-  // shared experts
-  gate_up(GUs, ns, act_s, 8 * L.max_groups, 0, nullptr);
+  // routing first (the producer streams the shared experts meanwhile and
+  // needs the expert list before its ring is full), then shared gate/up and
+  // down, routed gate/up and down
+  route();
+  stamp(3);
+  for (int g = rs.s0; g < rs.s1; g += kMoeChunk)
+    gate_up(gu_phase(p.s_gu, g, min(kMoeChunk, rs.s1 - g)), min(kMoeChunk, rs.s1 - g),
+            act_s + 8 * (g - rs.s0));
+  stamp(4);
   zero_acc();
-  down(DNs, act_s, 8 * L.max_groups, 0);
-  flush(false);
-  // routed experts (this CTA's slice of the selected experts' concatenation)
+  down(dn_phase(p.s_dn, rs.s0, rs.s1 - rs.s0), act_s, 0);
+  flush(nullptr, false);
+  stamp(5);
+  const int U = slot_e[L.umax];
+  const MoeRange m = moe_range(i, G, Gs, U * Ge);
   for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
-    const int ga = max(m.r0, u * Ge);
-    gate_up(routed_phase(m, u, false), min(m.r1, (u + 1) * Ge) - ga, act_r, 8 * L.max_groups,
-            8 * (ga - m.r0), gw + u);
+    int ga, gb;
+    const int e = seg(m, u, ga, gb);
+    for (int g = ga; g < gb; g += kMoeChunk)
+      gate_up(gu_phase(p.w_gu + e * eGu, g, min(kMoeChunk, gb - g)), min(kMoeChunk, gb - g),
+              act_r + 8 * (u * Ge + g - m.r0));
   }
-  zero_acc();
-  for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u)
-    down(routed_phase(m, u, true), act_r, 8 * L.max_groups, max(m.r0, u * Ge) - m.r0);
-  flush(true);
+  stamp(6);
+  for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
+    int ga, gb;
+    const int e = seg(m, u, ga, gb);
+    zero_acc();
+    down(dn_phase(p.w_dn + e * eDn, ga, gb - ga), act_r, u * Ge + ga - m.r0);
+    flush(gw + u, true);
+  }
   consumer_sync();
-  (void)nr;
+  stamp(7);
 
   // 5. this CTA's split-K partial into the fixed-point accumulator
   const int nparts = 8 / Q;
   for (int t = tid; t < B * D; t += kConsumerThreads) {
     float v = 0.f;
-    for (int s = 0; s < nparts; ++s) v += dpart[(size_t)s * B * D + t];
+    for (int s2 = 0; s2 < nparts; ++s2) v += dpart[(size_t)s2 * B * D + t];
     red_add_fixed(p.accum + t, v);
   }
-  grid_barrier(p.barrier, tid);
-
-  // 6. finish: out = [resid + attention sum +] MoE sum for this CTA's slice
-  const int n = B * D, o0 = (int)((long long)i * n / G), o1 = (int)((long long)(i + 1) * n / G);
-  for (int t = o0 + tid; t < o1; t += kConsumerThreads) {
-    float v = fixed_to_float(__ldcg(p.accum + t));
-    p.accum[t] = 0ull;
-    if (p.flags & CFB_RESID) {
-      float r = p.resid[t];
-      if (p.accum_in) {
-        r = __fadd_rn(r, fixed_to_float(__ldcg(p.accum_in + t)));
-        p.accum_in[t] = 0ull;
-      }
-      v = __fadd_rn(r, v);
-    }
-    p.out[t] = v;
+  stamp(8);
+  // 6. the last CTA to finish writes out = [resid + attention sum +] MoE sum
+  //    and re-zeroes the accumulators (no grid-wide wait for the others)
+  __threadfence();
+  consumer_sync();
+  int* last = reinterpret_cast<int*>(red);
+  if (tid == 0) {
+    const unsigned long long old = atomicAdd(p.barrier, 1ull);
+    *last = (old + 1ull) % (unsigned long long)G == 0ull;
   }
+  consumer_sync();
+  if (!*last) return;
+  __threadfence();
+  stamp(9);
+  const int n4 = B * D / 4;
+  for (int t = tid; t < n4; t += kConsumerThreads) {
+    const ulonglong2 m0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum) + 2 * t);
+    const ulonglong2 m1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum) + 2 * t + 1);
+    float v[4] = {fixed_to_float(m0.x), fixed_to_float(m0.y), fixed_to_float(m1.x), fixed_to_float(m1.y)};
+    reinterpret_cast<ulonglong2*>(p.accum)[2 * t] = make_ulonglong2(0ull, 0ull);
+    reinterpret_cast<ulonglong2*>(p.accum)[2 * t + 1] = make_ulonglong2(0ull, 0ull);
+    if (p.flags & CFB_RESID) {
+      const float4 r4 = __ldcg(reinterpret_cast<const float4*>(p.resid) + t);
+      float r[4] = {r4.x, r4.y, r4.z, r4.w};
+      if (p.accum_in) {
+        const ulonglong2 a0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum_in) + 2 * t);
+        const ulonglong2 a1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum_in) + 2 * t + 1);
+        r[0] = __fadd_rn(r[0], fixed_to_float(a0.x));
+        r[1] = __fadd_rn(r[1], fixed_to_float(a0.y));
+        r[2] = __fadd_rn(r[2], fixed_to_float(a1.x));
+        r[3] = __fadd_rn(r[3], fixed_to_float(a1.y));
+        reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t] = make_ulonglong2(0ull, 0ull);
+        reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t + 1] = make_ulonglong2(0ull, 0ull);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __fadd_rn(r[k], v[k]);
+    }
+    reinterpret_cast<float4*>(p.out)[t] = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  stamp(10);
 }
 
 template <int QB>
@@ -499,7 +587,7 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
   if (D < 8 || D % 8 || (D > 512 && D % 512) || (D > 512 && 8 % (D / 512)))
     return set_error(CFB_ERR_DIMENSION, "hidden must be a multiple of 8 up to 512, or 512/1024/2048/4096");
   if (!a->w_router || !a->w_gu || !a->w_dn || (Fs && (!a->s_gu || !a->s_dn)) || !a->accum ||
-      !a->out || !a->barrier)
+      !a->out || !a->barrier || !a->logits)
     return set_error(CFB_ERR_ARGUMENT, "null weight / workspace pointer");
   if ((a->flags & CFB_NORM) ? (!a->resid || !a->norm_w) : !a->x)
     return set_error(CFB_ERR_ARGUMENT, "missing activation input");
@@ -511,7 +599,7 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int Ge = Fe / 8;
   int grid = a->grid > 0 ? a->grid : sms;
-  if (grid > sms) grid = sms;         // grid barrier: every CTA co-resident
+  if (grid > sms) grid = sms;         // routing waits on every CTA's router rows: co-resident
   if (grid > K * Ge) grid = K * Ge;   // routed groups >= grid keeps every range non-empty-ordered
   const int Q = moe_segments(D);
   int spw = tuned_spw();
@@ -546,6 +634,8 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
   p.route_idx = a->route_idx;
   p.route_w = a->route_w;
   p.barrier = a->barrier;
+  p.trace = a->trace;
+  p.logits = a->logits;
   const size_t smem = L.total;
   if (p.B == 1) return launch_moe_inst<1>(p, grid, smem, st);
   if (p.B == 2) return launch_moe_inst<2>(p, grid, smem, st);

@@ -116,14 +116,15 @@ class MoeWorkspace:
         import torch
         dev = device or _native.require_cuda()
         self.accum = torch.zeros(batch, mw.hidden, device=dev, dtype=torch.int64)
-        self.barrier = torch.zeros(1, device=dev, dtype=torch.int64)
+        self.barrier = torch.zeros(2, device=dev, dtype=torch.int64)  # grid barrier, route counter
+        self.logits = torch.zeros(batch, mw.n_experts, device=dev, dtype=torch.float32)
         self.route_idx = torch.zeros(batch, mw.top_k, device=dev, dtype=torch.int32)
         self.route_w = torch.zeros(batch, mw.top_k, device=dev, dtype=torch.float32)
 
 
 def moe_launch(mw: MoeWeights, ws: MoeWorkspace, out, *, x=None, resid=None, norm_w=None,
                accum_in=None, eps: float = 1e-6, pdl: bool = False, grid: int = 0,
-               stream=None) -> None:
+               stream=None, trace=None) -> None:
     """Enqueue one fused MoE launch (device tensors; no host sync)."""
     B = out.shape[0]
     flags = (_native.NORM | _native.RESID) if resid is not None else 0
@@ -137,7 +138,7 @@ def moe_launch(mw: MoeWeights, ws: MoeWorkspace, out, *, x=None, resid=None, nor
         w_gu=mw.w_gu.data_ptr(), w_dn=mw.w_dn.data_ptr(), s_gu=_native.ptr(mw.s_gu),
         s_dn=_native.ptr(mw.s_dn), accum=ws.accum.data_ptr(), out=out.data_ptr(),
         route_idx=ws.route_idx.data_ptr(), route_w=ws.route_w.data_ptr(),
-        barrier=ws.barrier.data_ptr())
+        barrier=ws.barrier.data_ptr(), logits=ws.logits.data_ptr(), trace=_native.ptr(trace))
     _native.check(_native.lib().cfb_moe_decode(a, _native.stream_ptr(stream)))
 
 

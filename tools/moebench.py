@@ -53,5 +53,18 @@ idx = ws.route_idx.cpu().tolist()
 # algorithmic bytes: router + union of routed experts + shared
 U = len({e for row in idx for e in row})
 nbytes = 2 * (E * D + 3 * D * (U * F + NS * F))
+tr = torch.zeros(148, 16, device=dev, dtype=torch.int64)
+with torch.cuda.stream(st):
+    moe_launch(ws_[0], ws, out, resid=resid[0], norm_w=g, grid=a.grid, stream=st, trace=tr)
+torch.cuda.synchronize()
+t = tr.cpu().numpy().astype("float64")
+t = t[t[:, 0] > 0]
+import numpy as np  # noqa: E402
+rel = np.where(t[:, :14] > 0, (t[:, :14] - t[:, :1]) / 1965.0, np.nan)  # cycles -> us at max clock
+names = ["start", "norm", "router", "routed", "shared_gu", "shared_dn", "routed_gu", "routed_dn",
+         "atomics", "last_cta", "end", "r_polled", "r_loaded", "r_ranked"]
+print("cta0", [round(float(x), 2) for x in rel[0]], "cta77", [round(float(x), 2) for x in rel[77]])
+print(json.dumps({"trace_us_mean": {n: round(float(np.nanmean(rel[:, k])), 2) for k, n in enumerate(names)},
+                  "trace_us_max": {n: round(float(np.nanmax(rel[:, k])), 2) for k, n in enumerate(names)}}))
 print(json.dumps({"kernel": "moe_kernel", "batch": B, "us": round(us, 2),
                   "GBps": round(nbytes / us / 1e3, 1), "bytes": nbytes, "experts_streamed": U}))
