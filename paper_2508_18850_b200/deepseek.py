@@ -1,0 +1,156 @@
+"""DeepSeek-V2-Lite-shaped decoder block on the GPU (BASELINE.json config #3).
+
+One block = two launches chained with programmatic dependent launch:
+
+  1. fused_mla latent attention (``csrc/attn_mla.cu``, the reference's
+     ``run_fused_mla_decode`` dataflow, ``dataflows.py:316-429``) with the
+     RMSNorm prologue (CFB_NORM): x = f16(rmsnorm(resid) * g_attn); the head
+     sum stays in the 64-bit fixed-point accumulator;
+  2. fused MoE (``csrc/moe.cu``): r = resid + head sum, h = f16(rmsnorm(r) *
+     g_ffn), router + softmax top-k, shared + routed SwiGLU experts,
+     resid <- r + MoE(h).
+
+Dims: the reference preset for MLA (hidden 2048, 16 heads x 128,
+kv_lora_rank 512; ``cli.py:47-54``) and the DeepSeek-V2-Lite MoE (64 routed
+experts, top-6, 2 shared, width 1408).  The CPU restatement is
+``oracle/deepseek_port.block``.  The latent cache is an input (the reference
+never appends to it, ``dataflows.py:393-397``): the new token's latent row
+joins attention on rank N-1 only.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+from types import SimpleNamespace
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError
+from .fused import padded_hidden, pow2_at_least
+from .mla import pack_mla
+from .moe import MoeWeights, MoeWorkspace, moe_launch, pack_moe, random_moe_device
+
+
+@dataclass(frozen=True)
+class DeepSeekDims:
+    hidden: int = 2048
+    n_heads: int = 16
+    head_dim: int = 128
+    kv_rank: int = 512
+    n_experts: int = 64
+    top_k: int = 6
+    inter: int = 1408
+    n_shared: int = 2
+    cluster: int = 4
+    eps: float = 1e-6
+    routed_scale: float = 1.0
+
+    def mla_bytes(self, seq_len: int) -> int:
+        """Algorithmic HBM bytes of the attention half: MLA weights + the
+        latent cache read once + the norm gain (fp16)."""
+        D, nh, H, R = self.hidden, self.n_heads, self.head_dim, self.kv_rank
+        w = nh * D * H + D * R + nh * H * R + nh * R * H + nh * H * D
+        return 2 * (w + seq_len * R + D)
+
+    def moe_bytes(self) -> int:
+        D = self.hidden
+        return 2 * (self.n_experts * D + 3 * D * self.inter * (self.top_k + self.n_shared) + D)
+
+    def block_bytes(self, seq_len: int) -> int:
+        return self.mla_bytes(seq_len) + self.moe_bytes()
+
+
+LITE = DeepSeekDims()
+
+
+class DeepSeekBlock:
+    """Device-resident block: packed MLA + MoE weights, latent cache, norms,
+    and the fixed-point workspaces.  ``launch(resid)`` updates ``resid``
+    ([B][D] fp32, device) in place."""
+
+    def __init__(self, dims: DeepSeekDims, mla: dict, moe: MoeWeights, attn_norm, ffn_norm,
+                 seq_len: int, batch: int = 1):
+        import torch
+        dev = _native.require_cuda()
+        if batch > 4:
+            raise DimensionError("the DeepSeek block supports batch <= 4")
+        if mla["Dp"] != dims.hidden:
+            raise DimensionError("the block's RMSNorm needs hidden % cluster == 0 and 16-byte rows")
+        self.dims, self.mla, self.moe, self.S, self.B = dims, mla, moe, seq_len, batch
+        self.attn_norm, self.ffn_norm = attn_norm, ffn_norm
+        self.accum_attn = torch.zeros(batch, dims.hidden, device=dev, dtype=torch.int64)
+        self.ws = MoeWorkspace(moe, batch, dev)
+
+    # ---------------------------------------------------------------- builders
+    @classmethod
+    def from_arrays(cls, dims: DeepSeekDims, mla_arrays: dict, moe_w: dict, attn_norm, ffn_norm,
+                    batch: int = 1) -> "DeepSeekBlock":
+        """Oracle-format inputs: ``mla_arrays`` holds the reference MLA weights
+        and cache (``w_q``, ``w_up``, ``w_kv``, ``w_down``, ``w_out``,
+        ``kv_cache``; scenarios.py:140-165 layouts), ``moe_w`` the
+        ``oracle.deepseek_port.gen_moe`` dict."""
+        import torch
+        dev = _native.require_cuda()
+        S = mla_arrays["kv_cache"].shape[0]
+        md = SimpleNamespace(batch_size=batch, hidden_dim=dims.hidden, n_heads=dims.n_heads,
+                             head_dim=dims.head_dim, kv_lora_rank=dims.kv_rank, seq_len=S,
+                             dtype_bytes=2)
+        sc = SimpleNamespace(dims=md, cluster=SimpleNamespace(n_blocks=dims.cluster),
+                             hidden=np.zeros((batch, dims.hidden), np.float32), **mla_arrays)
+        mla = pack_mla(sc, dev, torch.float16)
+        moe = pack_moe(moe_w, dims.top_k, dims.routed_scale, dev)
+
+        def g(a):
+            return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).half()
+
+        return cls(dims, mla, moe, g(attn_norm), g(ffn_norm), S, batch)
+
+    @classmethod
+    def random(cls, dims: DeepSeekDims, seq_len: int, seed: int = 0, batch: int = 1) -> "DeepSeekBlock":
+        """Random fp16 weights (scales of scenarios.py:155-162) and latent cache."""
+        from .scenario import ModelDims, random_mla_scenario
+        import torch
+        dev = _native.require_cuda()
+        sc = random_mla_scenario(ModelDims(batch, dims.hidden, dims.n_heads, dims.head_dim, seq_len,
+                                           dims.kv_rank, 2), dims.cluster, seed)
+        mla = pack_mla(sc, dev, torch.float16)
+        moe = random_moe_device(dims.hidden, dims.n_experts, dims.inter, dims.n_shared, dims.top_k,
+                                seed=seed, routed_scale=dims.routed_scale, device=dev)
+        ones = torch.ones(dims.hidden, device=dev, dtype=torch.float16)
+        return cls(dims, mla, moe, ones, ones.clone(), seq_len, batch)
+
+    # ---------------------------------------------------------------- launch
+    def mla_args(self, resid, pdl: bool):
+        d, pk = self.dims, self.mla
+        flags = _native.APPEND | _native.NORM | (_native.PDL if pdl else 0)
+        return _native.MlaArgs(
+            dtype=2, batch=self.B, hidden=pk["Dp"], n_heads=d.n_heads, head_dim=d.head_dim,
+            head_pad=pk["Hp"], kv_rank=d.kv_rank, rank_pad=pk["Rp"], cluster=d.cluster,
+            seq_len=self.S, flags=flags, x=None, w_q=pk["w_q"].data_ptr(),
+            w_kv=pk["w_kv"].data_ptr(), w_up=pk["w_up"].data_ptr(), w_down=pk["w_down"].data_ptr(),
+            w_out=pk["w_out"].data_ptr(), cache=pk["cache"].data_ptr(), out=None,
+            accum=self.accum_attn.data_ptr(), stats=None, traffic=None, resid=resid.data_ptr(),
+            norm_w=self.attn_norm.data_ptr(), eps=d.eps)
+
+    def launch(self, resid, pdl: bool = True, stream=None) -> None:
+        """Enqueue the block on `stream`: resid <- block(resid)."""
+        _native.check(_native.lib().cfb_mla_decode(self.mla_args(resid, pdl),
+                                                   _native.stream_ptr(stream)))
+        moe_launch(self.moe, self.ws, resid, resid=resid, norm_w=self.ffn_norm,
+                   accum_in=self.accum_attn, eps=self.dims.eps, pdl=pdl, stream=stream)
+
+    def run(self, resid_host) -> tuple[np.ndarray, np.ndarray]:
+        """Host convenience: one block on (B, D) fp32 rows.  Returns (new
+        residual rows, routed expert ids in selection order)."""
+        import torch
+        dev = _native.require_cuda()
+        r = torch.from_numpy(np.ascontiguousarray(resid_host, np.float32)).to(dev)
+        self.launch(r, pdl=False)
+        torch.cuda.synchronize()
+        return r.cpu().numpy(), self.ws.route_idx.cpu().numpy().astype(np.int64)
+
+
+def mla_padding_ok(dims: DeepSeekDims) -> bool:
+    return padded_hidden(dims.hidden, dims.cluster, 2) == dims.hidden and \
+        pow2_at_least(dims.head_dim) >= dims.head_dim
