@@ -311,6 +311,33 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
 int cfb_llama_launches_per_step(const cfb_llama* m);
 /* stream-ordered copies between the engine and host memory (either may be NULL) */
 int cfb_llama_read(cfb_llama* m, int* token_host, float* logits_host, void* stream);
+
+/*
+ * Tensor parallelism (north-star (d)): each rank's engine is created with its
+ * shard - n_heads / size heads (W_qkv, W_out, KV cache of those heads), inter /
+ * size FFN columns (gate/up rows, down columns), vocab / size LM-head rows
+ * starting at vocab_offset - and is driven part by part so the caller can put
+ * one all-reduce after each block half:
+ *   EMBED; per layer: ATTN -> allreduce(accum, int64 SUM: the fixed-point head
+ *   sum, exact) -> FFN (rank 0 adds the residual, other ranks write their
+ *   partial) -> allreduce(resid, fp32 SUM); HEAD (local argmax packed into
+ *   argkey) -> allreduce(argkey, int64 MAX) -> TP_TOKEN (global token, pos++).
+ * With size 1 the parts are exactly cfb_llama_step.
+ */
+enum cfb_engine_part {
+  CFB_PART_EMBED = 0,
+  CFB_PART_ATTN = 1,
+  CFB_PART_FFN = 2,
+  CFB_PART_HEAD = 3,
+  CFB_PART_TP_TOKEN = 4
+};
+/* accum [D] u64, resid [D] fp32, argkey one u64: caller-owned, zeroed buffers the
+ * engine then uses instead of its own (so a communicator can address them), or NULL */
+int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigned long long* accum,
+                     float* resid, unsigned long long* argkey);
+int cfb_llama_enqueue(cfb_llama* m, int part, int layer, void* stream);
+int cfb_llama_tp_buffers(cfb_llama* m, unsigned long long** accum, float** resid,
+                         unsigned long long** argkey);
 int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
 
 /* One ClusterReduce (op 0=sum,1=max,2=softmax_merge) or ClusterGather (op 3)

@@ -19,7 +19,9 @@
 // attention module's fixed-point head sum (accum), folded into the RMSNorm
 // prologue; after the grid barrier every CTA re-zeroes accum for the output
 // rows it owns, and writes out = r + FFN for those rows (out may alias
-// resid).  With PDL the producer streams w_gu before griddepcontrol.wait.
+// resid).  Without CFB_RESID (tensor-parallel ranks > 0) it writes the
+// partial FFN only, so a sum over ranks adds r exactly once.  With PDL the
+// producer streams w_gu before griddepcontrol.wait.
 #include <cuda_runtime.h>
 
 #include "common.h"
@@ -147,6 +149,8 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
                                 p.accum[c] = 0ull;  // every CTA read it before the barrier
                               }
                               v = __fadd_rn(r, v);
+                            } else if (p.accum) {
+                              p.accum[c] = 0ull;  // tensor-parallel rank > 0: partial only
                             }
                             p.out[c] = v;
                           });
@@ -185,8 +189,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   if ((a->flags & CFB_NORM) ? (!a->resid || !a->norm_w) : !a->x)
     return set_error(CFB_ERR_ARGUMENT, "missing activation input");
   if ((a->flags & CFB_RESID) && !a->resid) return set_error(CFB_ERR_ARGUMENT, "CFB_RESID needs resid");
-  if (a->accum && (a->flags & (CFB_NORM | CFB_RESID)) != (CFB_NORM | CFB_RESID))
-    return set_error(CFB_ERR_ARGUMENT, "accum needs CFB_NORM | CFB_RESID");
+  if (a->accum && !(a->flags & CFB_NORM))
+    return set_error(CFB_ERR_ARGUMENT, "accum needs CFB_NORM");
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

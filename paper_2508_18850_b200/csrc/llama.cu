@@ -7,6 +7,7 @@
 #include <vector>
 
 #include "common.h"
+#include "ptx.cuh"
 
 struct cfb_llama {
   cfb_llama_config cfg;
@@ -27,6 +28,9 @@ struct cfb_llama {
   unsigned* lm_ticket = nullptr;
   int* token = nullptr;
   int* pos = nullptr;
+  unsigned long long* argkey = nullptr;  // TP: packed (logit, -index) of the local argmax
+  int tp_rank = 0, tp_size = 1, vocab_offset = 0;
+  int ext = 0;  // bit mask: accum / resid / argkey are caller-owned
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -39,50 +43,77 @@ int alloc_zero(void** p, size_t bytes) {
   return CFB_OK;
 }
 
-int enqueue_step(cfb_llama* m, cudaStream_t st) {
+// Tensor-parallel argmax: order-preserving 32-bit key of the local maximum
+// logit in the high word, 0xffffffff - global index in the low word, so an
+// int64 MAX all-reduce yields the largest logit and, among equal logits, the
+// smallest index (numpy argmax semantics across vocabulary shards).
+__global__ void tp_argmax_pack_kernel(const float* logits, const int* token, int vocab_offset,
+                                      unsigned long long* key) {
+  cfb::pdl_wait();
+  const int t = *token;
+  const unsigned u = __float_as_uint(logits[t]);
+  const unsigned ord = (u & 0x80000000u) ? ~u : (u | 0x80000000u);  // unsigned-monotone
+  // high word flipped to signed order: NCCL's int64 MAX compares signed
+  *key = ((unsigned long long)(ord ^ 0x80000000u) << 32) | (0xffffffffu - (unsigned)(t + vocab_offset));
+}
+__global__ void tp_argmax_unpack_kernel(const unsigned long long* key, int* token, int* pos) {
+  *token = (int)(0xffffffffu - (unsigned)(*key & 0xffffffffull));
+  *pos += 1;
+}
+
+int enqueue_embed(cfb_llama* m, cudaStream_t st) {
+  return cfb::embed(m->cfg.dtype, m->embed, m->token, m->resid, 1, m->cfg.hidden, st, true);
+}
+
+int enqueue_attn(cfb_llama* m, int l, cudaStream_t st) {
   const cfb_llama_config& c = m->cfg;
-  int rc = cfb::embed(c.dtype, m->embed, m->token, m->resid, 1, c.hidden, st, true);
-  if (rc) return rc;
-  for (int l = 0; l < c.n_layers; ++l) {
-    cfb_mha_args a = {};
-    a.dtype = c.dtype;
-    a.batch = 1;
-    a.hidden = c.hidden;
-    a.n_heads = c.n_heads;
-    a.head_dim = c.head_dim;
-    a.head_pad = c.head_dim;
-    a.cluster = c.cluster;
-    a.cache_cap = c.cache_cap;
-    a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_ONESHOT | CFB_PDL;
-    a.resid = m->resid;
-    a.norm_w = m->attn_norm[l];
-    a.eps = c.eps;
-    a.w_qkv = m->w_qkv[l];
-    a.w_out = m->w_out[l];
-    a.k_cache = m->k_cache[l];
-    a.v_cache = m->v_cache[l];
-    a.rope_cs = m->rope_cs;
-    a.step_pos = m->pos;
-    a.out = nullptr;  // the head sum stays in accum for the FFN prologue
-    a.accum = m->accum;
-    if ((rc = cfb::mha_decode(&a, st))) return rc;
-    cfb_ffn_args f = {};
-    f.dtype = c.dtype;
-    f.batch = 1;
-    f.hidden = c.hidden;
-    f.inter = c.inter;
-    f.flags = CFB_NORM | CFB_RESID | CFB_PDL;
-    f.eps = c.eps;
-    f.resid = m->resid;
-    f.accum = m->accum;
-    f.norm_w = m->ffn_norm[l];
-    f.w_gu = m->w_gu[l];
-    f.w_dn = m->w_dn[l];
-    f.act = m->act;
-    f.out = m->resid;
-    f.barrier = m->barrier;
-    if ((rc = cfb::ffn_decode(&f, st))) return rc;
-  }
+  cfb_mha_args a = {};
+  a.dtype = c.dtype;
+  a.batch = 1;
+  a.hidden = c.hidden;
+  a.n_heads = c.n_heads;
+  a.head_dim = c.head_dim;
+  a.head_pad = c.head_dim;
+  a.cluster = c.cluster;
+  a.cache_cap = c.cache_cap;
+  a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_ONESHOT | CFB_PDL;
+  a.resid = m->resid;
+  a.norm_w = m->attn_norm[l];
+  a.eps = c.eps;
+  a.w_qkv = m->w_qkv[l];
+  a.w_out = m->w_out[l];
+  a.k_cache = m->k_cache[l];
+  a.v_cache = m->v_cache[l];
+  a.rope_cs = m->rope_cs;
+  a.step_pos = m->pos;
+  a.out = nullptr;  // the head sum stays in accum for the FFN prologue (TP: all-reduced first)
+  a.accum = m->accum;
+  return cfb::mha_decode(&a, st);
+}
+
+int enqueue_ffn(cfb_llama* m, int l, cudaStream_t st) {
+  const cfb_llama_config& c = m->cfg;
+  cfb_ffn_args f = {};
+  f.dtype = c.dtype;
+  f.batch = 1;
+  f.hidden = c.hidden;
+  f.inter = c.inter;
+  // TP: only rank 0 adds the residual, so the all-reduce of resid counts it once
+  f.flags = CFB_NORM | CFB_PDL | (m->tp_rank == 0 ? CFB_RESID : 0);
+  f.eps = c.eps;
+  f.resid = m->resid;
+  f.accum = m->accum;
+  f.norm_w = m->ffn_norm[l];
+  f.w_gu = m->w_gu[l];
+  f.w_dn = m->w_dn[l];
+  f.act = m->act;
+  f.out = m->resid;
+  f.barrier = m->barrier;
+  return cfb::ffn_decode(&f, st);
+}
+
+int enqueue_head(cfb_llama* m, cudaStream_t st) {
+  const cfb_llama_config& c = m->cfg;
   cfb_lm_args h = {};
   h.dtype = c.dtype;
   h.batch = 1;
@@ -98,8 +129,46 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
   h.cand_idx = m->cand_idx;
   h.ticket = m->lm_ticket;
   h.token_out = m->token;
-  h.step_pos = m->pos;
-  return cfb::lm_head_argmax(&h, st);
+  h.step_pos = m->tp_size > 1 ? nullptr : m->pos;  // TP: advanced after the global argmax
+  int rc = cfb::lm_head_argmax(&h, st);
+  if (rc || m->tp_size == 1) return rc;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1);
+  cfg.stream = st;
+  cfb::LaunchAttrs at(0, true);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, tp_argmax_pack_kernel, (const float*)m->logits,
+                              (const int*)m->token, m->vocab_offset, m->argkey));
+  return CFB_OK;
+}
+
+int enqueue_tp_token(cfb_llama* m, cudaStream_t st) {
+  tp_argmax_unpack_kernel<<<1, 1, 0, st>>>(m->argkey, m->token, m->pos);
+  CFB_CUDA(cudaGetLastError());
+  return CFB_OK;
+}
+
+int enqueue_part(cfb_llama* m, int part, int layer, cudaStream_t st) {
+  switch (part) {
+    case CFB_PART_EMBED: return enqueue_embed(m, st);
+    case CFB_PART_ATTN: return enqueue_attn(m, layer, st);
+    case CFB_PART_FFN: return enqueue_ffn(m, layer, st);
+    case CFB_PART_HEAD: return enqueue_head(m, st);
+    case CFB_PART_TP_TOKEN: return enqueue_tp_token(m, st);
+  }
+  return cfb::set_error(CFB_ERR_ARGUMENT, "unknown engine part %d", part);
+}
+
+int enqueue_step(cfb_llama* m, cudaStream_t st) {
+  if (m->tp_size > 1)
+    return cfb::set_error(CFB_ERR_ARGUMENT,
+                          "tensor-parallel engines are driven part by part (collectives between)");
+  int rc = enqueue_embed(m, st);
+  for (int l = 0; !rc && l < m->cfg.n_layers; ++l)
+    if (!(rc = enqueue_attn(m, l, st))) rc = enqueue_ffn(m, l, st);
+  return rc ? rc : enqueue_head(m, st);
 }
 
 }  // namespace
@@ -139,7 +208,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
       (rc = alloc_zero((void**)&m->cand_val, (size_t)sms * 4)) ||
       (rc = alloc_zero((void**)&m->cand_idx, (size_t)sms * 4)) ||
       (rc = alloc_zero((void**)&m->lm_ticket, 4)) || (rc = alloc_zero((void**)&m->token, 4)) ||
-      (rc = alloc_zero((void**)&m->pos, 4))) {
+      (rc = alloc_zero((void**)&m->pos, 4)) || (rc = alloc_zero((void**)&m->argkey, 8))) {
     cfb_llama_destroy(m);
     return rc;
   }
@@ -151,8 +220,9 @@ int cfb_llama_destroy(cfb_llama* m) {
   if (!m) return CFB_OK;
   if (m->exec) cudaGraphExecDestroy(m->exec);
   if (m->graph) cudaGraphDestroy(m->graph);
-  void* bufs[] = {m->resid,  m->accum,    m->act,      m->barrier, m->logits,
-                  m->cand_val, m->cand_idx, m->lm_ticket, m->token,   m->pos};
+  void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
+                  m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
+                  m->pos, (m->ext & 4) ? nullptr : m->argkey};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -219,7 +289,53 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
   return CFB_OK;
 }
 
-int cfb_llama_launches_per_step(const cfb_llama* m) { return m ? 2 + 2 * m->cfg.n_layers : 0; }
+int cfb_llama_launches_per_step(const cfb_llama* m) {
+  return m ? 2 + 2 * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
+}
+
+int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigned long long* accum,
+                     float* resid, unsigned long long* argkey) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (size < 1 || rank < 0 || rank >= size || vocab_offset < 0)
+    return cfb::set_error(CFB_ERR_ARGUMENT, "bad tensor-parallel rank %d / size %d", rank, size);
+  m->tp_rank = rank;
+  m->tp_size = size;
+  m->vocab_offset = vocab_offset;
+  // caller-owned (e.g. torch-allocated, so a communicator can address them) buffers
+  // replace the engine's own; they must be zero-initialised like the originals
+  if (accum) {
+    cudaFree(m->accum);
+    m->accum = accum;
+    m->ext |= 1;
+  }
+  if (resid) {
+    cudaFree(m->resid);
+    m->resid = resid;
+    m->ext |= 2;
+  }
+  if (argkey) {
+    cudaFree(m->argkey);
+    m->argkey = argkey;
+    m->ext |= 4;
+  }
+  return CFB_OK;
+}
+
+int cfb_llama_enqueue(cfb_llama* m, int part, int layer, void* stream) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if ((part == CFB_PART_ATTN || part == CFB_PART_FFN) && (layer < 0 || layer >= m->cfg.n_layers))
+    return cfb::set_error(CFB_ERR_ARGUMENT, "layer %d out of range", layer);
+  return enqueue_part(m, part, layer, static_cast<cudaStream_t>(stream));
+}
+
+int cfb_llama_tp_buffers(cfb_llama* m, unsigned long long** accum, float** resid,
+                         unsigned long long** argkey) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (accum) *accum = m->accum;
+  if (resid) *resid = m->resid;
+  if (argkey) *argkey = m->argkey;
+  return CFB_OK;
+}
 
 int cfb_llama_read(cfb_llama* m, int* token_host, float* logits_host, void* stream) {
   if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");

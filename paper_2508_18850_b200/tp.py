@@ -1,0 +1,211 @@
+"""Tensor-parallel Llama decode (north-star (d), BASELINE.json config #5).
+
+One process per GPU.  Rank r of `world` holds a Megatron shard of every
+layer: heads [r*nh/W, (r+1)*nh/W) (their W_qkv columns, W_out rows and KV
+cache), FFN columns [r*F/W, (r+1)*F/W) (gate/up rows, down columns) and LM
+head rows [r*V/W, (r+1)*V/W); embedding and norms are replicated.  A step is
+the native engine driven part by part with exactly one all-reduce per block
+half (NCCL over NVLink via torch.distributed, captured in the same CUDA
+graph as the kernels):
+
+    EMBED
+    per layer:  ATTN  -> all_reduce(accum, int64 SUM)   attention half: the
+                         64-bit fixed-point head sum - integer, so the sum over
+                         ranks is exact and order-independent
+                FFN   -> all_reduce(resid, fp32 SUM)    FFN half: rank 0 adds
+                         the residual, the others contribute their partial
+    HEAD  -> all_reduce(argkey, int64 MAX)   (logit, -index) of each shard's
+             argmax: the global greedy token (first index of the max)
+    TP_TOKEN
+
+The same schedule is ``tp_step`` below, parameterised by the compute and
+communication operations, so the CPU tests run it with the numpy oracle and
+gloo (world size 2) and the GPU runs it with the kernels and NCCL.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import replace
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError
+from .llama import LlamaConfig, LlamaDecoder
+
+PART_EMBED, PART_ATTN, PART_FFN, PART_HEAD, PART_TP_TOKEN = 0, 1, 2, 3, 4
+
+
+# ------------------------------------------------------------------ sharding
+def check_tp(cfg: LlamaConfig, world: int) -> None:
+    if cfg.n_heads % world or cfg.inter % (8 * world) or cfg.vocab % (4 * world):
+        raise DimensionError(f"tensor-parallel size {world} must divide the heads, inter/8 and vocab/4 "
+                             f"({cfg.n_heads}, {cfg.inter}, {cfg.vocab})")
+
+
+def local_config(cfg: LlamaConfig, world: int, cluster: int | None = None) -> LlamaConfig:
+    """The per-rank model shape; `cluster` defaults to keeping ~128 CTAs per
+    attention launch (4 x heads at TP1, up to 16 CTAs per head)."""
+    check_tp(cfg, world)
+    nh = cfg.n_heads // world
+    if cluster is None:
+        cluster = cfg.cluster
+        while nh * cluster < 128 and cluster < 16 and cfg.head_dim % (2 * cluster) == 0:
+            cluster *= 2
+    return replace(cfg, n_heads=nh, inter=cfg.inter // world, vocab=cfg.vocab // world,
+                   cluster=cluster)
+
+
+def shard_layer(lp: dict, rank: int, world: int) -> dict:
+    """Megatron shard of one logical layer (``random_llama_params`` layout)."""
+    nh = lp["w_qkv"].shape[0] // world
+    F = lp["w1"].shape[0] // world
+    hs, fs = slice(rank * nh, (rank + 1) * nh), slice(rank * F, (rank + 1) * F)
+    return dict(attn_norm=lp["attn_norm"], ffn_norm=lp["ffn_norm"], w_qkv=lp["w_qkv"][hs],
+                w_out=lp["w_out"][hs], k_cache=lp["k_cache"][hs], v_cache=lp["v_cache"][hs],
+                w1=lp["w1"][fs], w2=lp["w2"][fs], w3=lp["w3"][:, fs])
+
+
+def shard_params(params: dict, rank: int, world: int) -> dict:
+    V = params["lm_head"].shape[0] // world
+    return dict(layers=[shard_layer(lp, rank, world) for lp in params["layers"]],
+                embed=params["embed"], final_norm=params["final_norm"],
+                lm_head=params["lm_head"][rank * V:(rank + 1) * V])
+
+
+def pack_argmax_key(value: float, index: int) -> int:
+    """Host twin of the device packing (csrc/llama.cu tp_argmax_pack_kernel):
+    signed-int64 key whose MAX is the largest value, ties to the smallest index."""
+    u = int(np.float32(value).view(np.uint32))
+    ord_ = (~u & 0xFFFFFFFF) if u & 0x80000000 else (u | 0x80000000)
+    key = ((ord_ ^ 0x80000000) << 32) | (0xFFFFFFFF - index)
+    return key - (1 << 64) if key >= (1 << 63) else key
+
+
+def unpack_argmax_key(key: int) -> int:
+    return 0xFFFFFFFF - (key & 0xFFFFFFFF)
+
+
+def tp_step(ops, n_layers: int) -> None:
+    """The tensor-parallel decode schedule (one step).  `ops` supplies
+    embed/attn/ffn/head/token compute and the three collectives."""
+    ops.embed()
+    for l in range(n_layers):
+        ops.attn(l)
+        ops.allreduce_heads()      # int64 SUM of the fixed-point head sum
+        ops.ffn(l)
+        ops.allreduce_resid()      # fp32 SUM (residual added by rank 0 only)
+    ops.head()
+    ops.allreduce_argmax()         # int64 MAX of the packed (logit, -index) keys
+    ops.token()
+
+
+# ------------------------------------------------------------------ GPU driver
+class _EngineOps:
+    """tp_step operations bound to a rank's native engine + NCCL group."""
+
+    def __init__(self, dec: "TPLlamaDecoder"):
+        self.d = dec
+
+    def _enq(self, part, layer=0):
+        _native.check(self.d.lib.cfb_llama_enqueue(self.d.eng._h, part, layer, self.d.sp()))
+
+    def embed(self):
+        self._enq(PART_EMBED)
+
+    def attn(self, l):
+        self._enq(PART_ATTN, l)
+
+    def ffn(self, l):
+        self._enq(PART_FFN, l)
+
+    def head(self):
+        self._enq(PART_HEAD)
+
+    def token(self):
+        if self.d.world > 1:
+            self._enq(PART_TP_TOKEN)
+
+    def _ar(self, t, op):
+        if self.d.world > 1 or self.d.force_collectives:
+            import torch.distributed as dist
+            dist.all_reduce(t, op=op, group=self.d.group)
+
+    def allreduce_heads(self):
+        import torch.distributed as dist
+        self._ar(self.d.accum, dist.ReduceOp.SUM)
+
+    def allreduce_resid(self):
+        import torch.distributed as dist
+        self._ar(self.d.resid, dist.ReduceOp.SUM)
+
+    def allreduce_argmax(self):
+        import torch.distributed as dist
+        if self.d.world > 1:
+            self._ar(self.d.argkey, dist.ReduceOp.MAX)
+
+
+class TPLlamaDecoder:
+    """Rank-local tensor-parallel decoder.  `group` is a torch.distributed
+    NCCL process group (None: the default group)."""
+
+    def __init__(self, cfg: LlamaConfig, rank: int, world: int, cache_cap: int, *, params=None,
+                 seed: int = 0, group=None, cluster: int | None = None,
+                 force_collectives: bool = False):
+        import torch
+        self.cfg, self.rank, self.world, self.group = cfg, rank, world, group
+        self.lcfg = local_config(cfg, world, cluster)
+        self.force_collectives = force_collectives
+        if params is not None:
+            self.eng = LlamaDecoder.from_params(self.lcfg, shard_params(params, rank, world), cache_cap)
+        else:
+            self.eng = LlamaDecoder.random(self.lcfg, cache_cap, seed=seed)
+        dev = self.eng.dev
+        self.accum = torch.zeros(cfg.hidden, device=dev, dtype=torch.int64)
+        self.resid = torch.zeros(cfg.hidden, device=dev, dtype=torch.float32)
+        self.argkey = torch.zeros(1, device=dev, dtype=torch.int64)
+        self.lib = _native.lib()
+        self.lib.cfb_llama_set_tp.argtypes = [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3
+        self.lib.cfb_llama_enqueue.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]
+        _native.check(self.lib.cfb_llama_set_tp(self.eng._h, rank, world, rank * self.lcfg.vocab,
+                                                self.accum.data_ptr(), self.resid.data_ptr(),
+                                                self.argkey.data_ptr()))
+        self.ops = _EngineOps(self)
+        self.graph = None
+
+    @property
+    def stream(self):
+        return self.eng.stream
+
+    def sp(self) -> int:
+        return self.eng.stream.cuda_stream
+
+    @property
+    def launches_per_step(self) -> int:
+        return 2 + 2 * self.cfg.n_layers + (2 if self.world > 1 else 0)
+
+    def set_state(self, pos: int, token: int) -> None:
+        self.eng.set_state(pos, token)
+
+    def step(self) -> None:
+        import torch
+        with torch.cuda.stream(self.eng.stream):
+            tp_step(self.ops, self.cfg.n_layers)
+
+    def capture(self) -> None:
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.eng.stream):
+            tp_step(self.ops, self.cfg.n_layers)
+
+    def replay(self) -> None:
+        import torch
+        with torch.cuda.stream(self.eng.stream):  # stream-ordered with token()/logits reads
+            self.graph.replay()
+
+    def token(self) -> int:
+        return self.eng.token()
+
+    def logits_local(self) -> np.ndarray:
+        return self.eng.logits()
