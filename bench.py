@@ -10,6 +10,12 @@ replayed from a CUDA graph with weights and KV cache resident in HBM.
 numbers are in `sweep`.  Inputs (13.5 GB of weights) are far larger than the
 126 MB L2, so no L2 flush is needed between steps.
 
+Under torchrun (N > 1) each rank holds a tensor-parallel shard (configs[4]:
+heads, FFN columns and LM-head rows split N ways) and a step carries one NCCL
+all-reduce per block half; `value` is then the TP TPOT ("scaling": "strong").
+At N = 1 the line also carries `deepseek_block` (configs[2]: MLA + MoE block
+latency over contexts, CUDA-graph replay of 4 distinct blocks).
+
 --impl reference times the CPU oracle restatement of the reference path
 (oracle/, numpy, all host threads) on a bounded sample: one decoder block per
 context, extrapolated to 32 layers plus the LM head.
@@ -107,17 +113,27 @@ def run_ours(args, rank, world):
     cfg = LLAMA2_7B
     ctxs = [int(c) for c in args.contexts.split(",")]
     cap = max(ctxs) + args.warmup + args.steps + 8
-    model = LlamaDecoder.random(cfg, cache_cap=cap, seed=1234 + rank)
+    if world > 1:
+        # tensor parallel (configs[4]): rank-local shard, one NCCL all-reduce per block half
+        from paper_2508_18850_b200.tp import TPLlamaDecoder
+        tp = TPLlamaDecoder(cfg, rank, world, cap, seed=1234 + rank)
+        model = tp.eng
+        step_fn, capture_fn, replay_fn = tp.step, tp.capture, tp.replay
+        launches_per_step = tp.launches_per_step
+    else:
+        tp = None
+        model = LlamaDecoder.random(cfg, cache_cap=cap, seed=1234 + rank)
+        step_fn, capture_fn, replay_fn = model.step, model.capture, model.replay
+        launches_per_step = model.launches_per_step
     L = _native.lib()
     st = model.stream
 
     # configure kernels outside capture, then capture one step
     model.set_state(ctxs[0], 1)
-    model.step()
+    step_fn()
     torch.cuda.synchronize()
     model.set_state(ctxs[0], 1)
-    model.capture()
-
+    capture_fn()
     pk, pk_kind = peaks()
     sweep = []
     sampler = ClockSampler(dev.index or 0)
@@ -126,7 +142,7 @@ def run_ours(args, rank, world):
         for ctx in ctxs:
             model.set_state(ctx, 1)
             for _ in range(args.warmup):
-                model.replay()
+                replay_fn()
             model.set_state(ctx, 1)
             st.synchronize()
             if world > 1:
@@ -134,7 +150,7 @@ def run_ours(args, rank, world):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
             for _ in range(args.steps):
-                model.replay()
+                replay_fn()
             e1.record(st)
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1)
@@ -142,12 +158,12 @@ def run_ours(args, rank, world):
                 t = torch.tensor([ms], device=dev)
                 torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
                 ms = float(t.item())
-            launches += model.launches_per_step * args.steps
+            launches += launches_per_step * args.steps
             tpot_us = ms * 1e3 / args.steps
             mean_ctx = ctx + (args.steps - 1) / 2
-            gbs = cfg.step_bytes(int(mean_ctx)) / (tpot_us * 1e-6) / 1e9
+            gbs = cfg.step_bytes(int(mean_ctx)) / (tpot_us * 1e-6) / 1e9  # whole job, all ranks
             sweep.append({"ctx": ctx, "tpot_us": round(tpot_us, 2), "hbm_gbs": round(gbs, 1),
-                          "frac_of_peak": round(gbs / pk["hbm_gbs"], 4)})
+                          "frac_of_peak": round(gbs / (world * pk["hbm_gbs"]), 4)})
 
         # e2e: host token -> device (pinned H2D), graph, token -> host (pinned D2H), per step
         host_in = torch.ones(1, dtype=torch.int32).pin_memory()
@@ -160,28 +176,29 @@ def run_ours(args, rank, world):
             for _ in range(args.steps):
                 _native.check(L.cfb_llama_write_token(model._h, ctypes.c_void_p(host_in.data_ptr()),
                                                       model._sp()))
-                model.replay()
+                replay_fn()
                 _native.check(L.cfb_llama_read(model._h, ctypes.c_void_p(host_out.data_ptr()),
                                                None, model._sp()))
                 st.synchronize()
                 host_in[0] = host_out[0]
             dt = time.perf_counter() - t0
             e2e.append(dt * 1e6 / args.steps)
-            launches += model.launches_per_step * args.steps
+            launches += launches_per_step * args.steps
     clocks = sampler.summary()
 
     # dominant kernel (fused FFN, 64% of weight bytes): avg launch duration with
     # CUDA events on its stream, cycling through the 32 layers' weights
-    ffn_bytes = 3 * cfg.hidden * cfg.inter * 2 + cfg.hidden * 2
+    lcfg = tp.lcfg if tp is not None else cfg
+    ffn_bytes = 3 * lcfg.hidden * lcfg.inter * 2 + lcfg.hidden * 2
     resid = torch.randn(1, cfg.hidden, device=dev)
     out = torch.empty(1, cfg.hidden, device=dev)
-    act = torch.empty(cfg.inter, device=dev, dtype=torch.float16)
+    act = torch.empty(lcfg.inter, device=dev, dtype=torch.float16)
     bar = torch.zeros(1, device=dev, dtype=torch.int64)
     accum = torch.zeros(1, cfg.hidden, device=dev, dtype=torch.int64)
     fargs = []
     for lyr in model.layers:
         fargs.append(_native.FfnArgs(
-            dtype=2, batch=1, hidden=cfg.hidden, inter=cfg.inter,
+            dtype=2, batch=1, hidden=cfg.hidden, inter=lcfg.inter,
             flags=_native.NORM | _native.RESID | _native.PDL, grid=0, eps=cfg.eps, x=None,
             resid=resid.data_ptr(), accum=accum.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
             w_dn=lyr["w_dn"].data_ptr(), act=act.data_ptr(), out=out.data_ptr(),
@@ -209,14 +226,14 @@ def run_ours(args, rank, world):
     line = {
         "metric": METRIC, "value": round(tpot, 2), "unit": "us/token", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tpot / 1e3, 4),
-        "higher_is_better": False, "scaling": "replicas" if world > 1 else "weak",
+        "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
         "vs_baseline": None, "dtype": "f16", "data": "synthetic (random fp16 weights + KV cache, device-drawn)",
         "config": {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
                                + "/".join(str(c) for c in ctxs) + ", cluster size 4 (configs[1]); "
                                "value = mean TPOT over the sweep",
-                   "model": "llama2-7b", "global_batch": world, "contexts": ctxs,
-                   "parallelism": f"replicas{world}" if world > 1 else "single",
-                   "cluster_size": cfg.cluster,
+                   "model": "llama2-7b", "global_batch": 1, "contexts": ctxs,
+                   "parallelism": f"tp{world}" if world > 1 else "single",
+                   "cluster_size": lcfg.cluster,
                    "l2": "inputs larger than L2 (13.5 GB weights streamed per token), no flush"},
         "sweep": sweep,
         "achieved_hbm_gbs_mean": round(float(np.mean([s["hbm_gbs"] for s in sweep])), 1),
@@ -232,12 +249,56 @@ def run_ours(args, rank, world):
         "gpu_launches": launches,
         "clocks": clocks,
     }
+    if world == 1 and not args.no_deepseek:
+        del model, fargs
+        torch.cuda.empty_cache()
+        line["deepseek_block"] = deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])
+        line["gpu_launches"] += sum(d["launches"] for d in line["deepseek_block"])
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return line
+
+
+def deepseek_sweep(ctxs, peak_gbs, layers=4, reps=16):
+    """configs[2]: DeepSeek-V2-Lite-shaped block (fused_mla + fused MoE, PDL),
+    CUDA graph of `layers` distinct blocks (nothing reused from L2)."""
+    import torch
+    from paper_2508_18850_b200.deepseek import LITE, DeepSeekBlock
+    out = []
+    for S in ctxs:
+        blocks = [DeepSeekBlock.random(LITE, S, seed=s) for s in range(layers)]
+        st = torch.cuda.Stream()
+        resid = torch.randn(1, LITE.hidden, device="cuda")
+        with torch.cuda.stream(st):
+            for b in blocks:
+                b.launch(resid, stream=st)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for b in blocks:
+                b.launch(resid, stream=st)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        with torch.cuda.stream(st):
+            for _ in range(reps):
+                g.replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / (reps * layers)
+        gbs = LITE.block_bytes(S) / us / 1e3
+        out.append({"ctx": S, "block_us": round(us, 2), "hbm_gbs": round(gbs, 1),
+                    "frac_of_peak": round(gbs / peak_gbs, 4), "bytes": LITE.block_bytes(S),
+                    "launches": 2 * layers * (reps + 4)})
+        del blocks, g
+        torch.cuda.empty_cache()
+    return out
 
 
 # --------------------------------------------------------------------- CPU arm
@@ -363,6 +424,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--contexts", default="1024,2048,4096,8192,16384")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-deepseek", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
