@@ -13,6 +13,7 @@
  *   cfb_mla_decode         <- dataflows.py:316-429  run_fused_mla_decode  (fused_mla, App. B.1)
  *   cfb_splithead_decode   <- dataflows.py:432-502  run_splithead_decode  (split_head, App. B.2)
  *   cfb_ffn_decode         <- oracle.py:112-131     ffn_reference(..., "silu") fused into one launch
+ *   cfb_mla_engine_decode  <- dataflows.py:316-429 math, head-batched for the DeepSeek block
  *   cfb_moe_decode         <- no reference counterpart: DeepSeek-V2 MoE
  *                            (transformers DeepseekV2Moe semantics, oracle/deepseek_port.py)
  *   cfb_cluster_collective <- collectives.py:110-203 cluster_reduce / cluster_gather (DSMEM KAT kernel)
@@ -161,6 +162,44 @@ typedef struct cfb_mla_args {
   float eps;
 } cfb_mla_args;
 int cfb_mla_decode(const cfb_mla_args* args, void* stream);
+
+/*
+ * Head-batched MLA for the DeepSeek block engine (batch 1, 16 heads, kv_lora_rank
+ * 512, head_dim <= 128): same math as cfb_mla_decode (absorbed form, new latent
+ * row attended once) but every weight and cache row crosses HBM once -
+ * three PDL-chained launches: projections (W_q | W_kv, then W_up), split-KV
+ * attention over the S+1 latent rows with tensor-core MMAs (all heads per
+ * cache tile), merge + W_down + W_out into `accum` (fixed point, plain stores:
+ * the block's attention head sum for cfb_moe_decode's accum_in).
+ * Input x = f16(rmsnorm(resid) * norm_w).  Layouts (fp16):
+ *   w_a   row tiles of [W_q^T (n_heads*H rows) ; W_kv^T (512 rows)] x D
+ *   w_up  rows h*512 + j = W_up[h][:, j] (H), chunk-rotated by row index
+ *   w_dn  row tiles of W_down^T: rows h*H + i = W_down[h][:, i] (512)
+ *   w_o   row tiles of W_out^T: row d = [W_out[0][:, d] ; ... ; W_out[15][:, d]]
+ *   cache [seq_len][512]
+ * Workspaces: qc [16*H + 512] fp16, qlat [16][512] fp16, part [min(SMs,
+ * max_parts)][32 + 16*512] fp32, zb [16][512] fp16, ob [16*H] fp16, barrier two
+ * u64 (zero, then monotonic).
+ */
+typedef struct cfb_mla_engine_args {
+  int hidden, n_heads, head_dim, kv_rank, seq_len, flags, max_parts;
+  float eps;
+  const float* resid;
+  const void* norm_w;
+  const void* w_a;
+  const void* w_up;
+  const void* w_dn;
+  const void* w_o;
+  const void* cache;
+  void* qc;
+  void* qlat;
+  float* part;
+  void* zb;
+  void* ob;
+  unsigned long long* accum;
+  unsigned long long* barrier;
+} cfb_mla_engine_args;
+int cfb_mla_engine_decode(const cfb_mla_engine_args* args, void* stream);
 
 /*
  * split_head attention module (dataflows.py:432-502): one cluster of N CTAs

@@ -129,6 +129,16 @@ class LmArgs(ctypes.Structure):
         ("step_pos", _vp)]
 
 
+class MlaEngineArgs(ctypes.Structure):
+    """Mirror of ``cfb_mla_engine_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("hidden", "n_heads", "head_dim", "kv_rank", "seq_len",
+                                             "flags", "max_parts")] + [
+        ("eps", ctypes.c_float)] + [
+        (n, _vp) for n in ("resid", "norm_w", "w_a", "w_up", "w_dn", "w_o", "cache", "qc", "qlat",
+                           "part", "zb", "ob", "accum", "barrier")]
+
+
 class MoeArgs(ctypes.Structure):
     """Mirror of ``cfb_moe_args``."""
 
@@ -140,6 +150,8 @@ class MoeArgs(ctypes.Structure):
 
 
 def bind_extra(L) -> None:
+    L.cfb_mla_engine_decode.argtypes = [ctypes.POINTER(MlaEngineArgs), _vp]
+    L.cfb_mla_engine_decode.restype = ctypes.c_int
     L.cfb_moe_decode.argtypes = [ctypes.POINTER(MoeArgs), _vp]
     L.cfb_moe_decode.restype = ctypes.c_int
     L.cfb_mla_decode.argtypes = [ctypes.POINTER(MlaArgs), _vp]

@@ -43,6 +43,10 @@ int cfb_mla_decode(const cfb_mla_args* args, void* stream) {
   return cfb::mla_decode(args, static_cast<cudaStream_t>(stream));
 }
 
+int cfb_mla_engine_decode(const cfb_mla_engine_args* args, void* stream) {
+  return cfb::mla_engine_decode(args, static_cast<cudaStream_t>(stream));
+}
+
 int cfb_splithead_decode(const cfb_splithead_args* args, void* stream) {
   return cfb::splithead_decode(args, static_cast<cudaStream_t>(stream));
 }

@@ -54,6 +54,7 @@ int tuned_sleep();
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
 int mha_finalize(float* out, const float* resid, unsigned long long* accum, int n, cudaStream_t st);
 int mla_decode(const cfb_mla_args* a, cudaStream_t st);
+int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st);
 int splithead_decode(const cfb_splithead_args* a, cudaStream_t st);
 int ffn_decode(const cfb_ffn_args* a, cudaStream_t st);
 int moe_decode(const cfb_moe_args* a, cudaStream_t st);

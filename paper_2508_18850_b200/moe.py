@@ -120,6 +120,7 @@ class MoeWorkspace:
         self.logits = torch.zeros(batch, mw.n_experts, device=dev, dtype=torch.float32)
         self.route_idx = torch.zeros(batch, mw.top_k, device=dev, dtype=torch.int32)
         self.route_w = torch.zeros(batch, mw.top_k, device=dev, dtype=torch.float32)
+        torch.cuda.synchronize()  # zero counters visible to launches on any stream
 
 
 def moe_launch(mw: MoeWeights, ws: MoeWorkspace, out, *, x=None, resid=None, norm_w=None,

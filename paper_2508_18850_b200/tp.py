@@ -165,6 +165,7 @@ class TPLlamaDecoder:
         self.accum = torch.zeros(cfg.hidden, device=dev, dtype=torch.int64)
         self.resid = torch.zeros(cfg.hidden, device=dev, dtype=torch.float32)
         self.argkey = torch.zeros(1, device=dev, dtype=torch.int64)
+        torch.cuda.synchronize()  # zeroed on the current stream; the engine uses its own
         self.lib = _native.lib()
         self.lib.cfb_llama_set_tp.argtypes = [ctypes.c_void_p] + [ctypes.c_int] * 3 + [ctypes.c_void_p] * 3
         self.lib.cfb_llama_enqueue.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p]

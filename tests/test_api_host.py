@@ -161,7 +161,8 @@ def _struct_fields(text, name):
 @pytest.mark.parametrize("cname,pyname", [("cfb_mha_args", "MhaArgs"), ("cfb_ffn_args", "FfnArgs"),
                                           ("cfb_lm_args", "LmArgs"), ("cfb_mla_args", "MlaArgs"),
                                           ("cfb_splithead_args", "SplitHeadArgs"),
-                                          ("cfb_moe_args", "MoeArgs")])
+                                          ("cfb_moe_args", "MoeArgs"),
+                                          ("cfb_mla_engine_args", "MlaEngineArgs")])
 def test_abi_struct_layout_matches_header(cname, pyname):
     """ctypes mirrors must have the field order of the C structs."""
     text = (ROOT / "include" / "cfb.h").read_text()

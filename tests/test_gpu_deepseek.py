@@ -50,11 +50,15 @@ def test_block_small_dims(B, cluster, S):
     assert float(np.max(np.abs(out - ref))) <= 2e-2 and _rel(out, ref) <= 1e-2
 
 
-@pytest.mark.parametrize("S", [1, 300])
-def test_block_lite_dims(S):
+@pytest.mark.parametrize("S,engine", [(1, False), (300, False), (0, True), (1, True), (300, True),
+                                      (2000, True)])
+def test_block_lite_dims(S, engine):
+    """engine=True: the head-batched MLA engine (csrc/mla_engine.cu);
+    False: the reference-dataflow fused_mla kernel."""
     dims = DeepSeekDims()  # MLA preset dims + DeepSeek-V2-Lite MoE
     mla, moe_w, ga, gf, x = _case(dims, S, 1, seed=7)
-    blk = DeepSeekBlock.from_arrays(dims, mla, moe_w, ga, gf)
+    blk = DeepSeekBlock.from_arrays(dims, mla, moe_w, ga, gf, use_engine=engine)
+    assert (blk.engine is not None) == engine
     out, idx = blk.run(x)
     ref, info = dp.block(x, mla, ga, gf, moe_w, dims.top_k, dims.cluster, dims.eps)
     assert info["margin"][0] > 1e-4
@@ -64,3 +68,22 @@ def test_block_lite_dims(S):
     out2, _ = blk.run(out)
     ref2, _ = dp.block(out, mla, ga, gf, moe_w, dims.top_k, dims.cluster, dims.eps)
     assert float(np.max(np.abs(out2 - ref2))) <= 2e-2 and _rel(out2, ref2) <= 1e-2
+
+
+def test_mla_engine_attention_half_matches_dense_oracle():
+    """The engine's attention half alone (head sum in the fixed-point
+    accumulator) vs the dense fp32 MLA oracle (oracle.py:55-93 absorbed)."""
+    import torch
+    from oracle.llama_port import rmsnorm_f16
+    dims = DeepSeekDims()
+    for S in (5, 700, 5000):
+        mla, moe_w, ga, gf, x = _case(dims, S, 1, seed=S)
+        blk = DeepSeekBlock.from_arrays(dims, mla, moe_w, ga, gf)
+        r = torch.from_numpy(x).cuda()
+        blk.launch_attention(r, pdl=False)
+        torch.cuda.synchronize()
+        got = blk.accum_attn.cpu().numpy().astype(np.float64) * 2.0 ** -32
+        blk.accum_attn.zero_()
+        h = rmsnorm_f16(x, ga, dims.eps)
+        ref = cp.dense_mla(h, *(mla[k] for k in ("w_q", "w_up", "w_kv", "w_down", "w_out", "kv_cache")))
+        assert float(np.max(np.abs(got - ref))) <= 2e-2 and _rel(got, ref) <= 1e-2, S

@@ -20,10 +20,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--contexts", default="1024,4096,16384")
 ap.add_argument("--layers", type=int, default=4)
 ap.add_argument("--reps", type=int, default=32)
+ap.add_argument("--reference-mla", action="store_true", help="reference-dataflow MLA kernel")
 a = ap.parse_args()
 out = []
 for S in [int(c) for c in a.contexts.split(",")]:
-    blocks = [DeepSeekBlock.random(LITE, S, seed=s) for s in range(a.layers)]
+    blocks = [DeepSeekBlock.random(LITE, S, seed=s, use_engine=not a.reference_mla)
+              for s in range(a.layers)]
     st = torch.cuda.Stream()
     resid = torch.randn(1, LITE.hidden, device="cuda")
     with torch.cuda.stream(st):
@@ -63,11 +65,12 @@ for S in [int(c) for c in a.contexts.split(",")]:
     def mla_only():
         b = blocks[k[0] % a.layers]
         k[0] += 1
-        _native.check(_native.lib().cfb_mla_decode(b.mla_args(resid, True), _native.stream_ptr(st)))
+        b.launch_attention(resid, True, stream=st)
     mla_us = time_fn(mla_only)
     out.append({"ctx": S, "block_us": round(us, 2), "GBps": round(nbytes / us / 1e3, 1),
                 "bytes": nbytes, "mla_us": round(mla_us, 2),
                 "mla_GBps": round(LITE.mla_bytes(S) / mla_us / 1e3, 1)})
+    print(json.dumps(out[-1]), flush=True)
     del blocks
     torch.cuda.empty_cache()
 print(json.dumps({"deepseek_block": out}))
