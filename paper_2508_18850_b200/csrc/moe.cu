@@ -109,12 +109,14 @@ struct MoeRange {
   int s0, s1, r0, r1;
 };
 __device__ __forceinline__ MoeRange moe_range(int i, int G, int Gs, int Tr) {
-  const long long Tt = (long long)Gs + Tr;
+  // 32-bit: (G <= 148) x (groups <= 32 * 256 * 16 / 8) stays far below 2^31, and a
+  // 64-bit division is a slow software routine on the GPU
+  const unsigned Tt = (unsigned)(Gs + Tr), g = (unsigned)G, u = (unsigned)i;
   MoeRange m;
-  m.s0 = (int)((long long)i * Gs / G);
-  m.s1 = (int)((long long)(i + 1) * Gs / G);
-  m.r0 = (int)((long long)i * Tt / G) - m.s0;
-  m.r1 = (int)((long long)(i + 1) * Tt / G) - m.s1;
+  m.s0 = (int)(u * (unsigned)Gs / g);
+  m.s1 = (int)((u + 1) * (unsigned)Gs / g);
+  m.r0 = (int)(u * Tt / g) - m.s0;
+  m.r1 = (int)((u + 1) * Tt / g) - m.s1;
   return m;
 }
 
