@@ -398,24 +398,46 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   __half* zs = reinterpret_cast<__half*>(smem + L.zs);
   __half* os = reinterpret_cast<__half*>(smem + L.os);
   float* part = reinterpret_cast<float*>(smem + L.part);
-  // 1. merge the attention partials for this CTA's slice of z (16 x 512)
+  // 1. merge the attention partials for this CTA's slice of z (16 x 512):
+  //    per head (<= 2 per CTA) the weights w_q = 2^(m_q - M) and 1 / sum_q w_q l_q
+  //    once into smem, then per element the sum over q split across a warp's
+  //    lanes, 4 elements per pass so their loads are in flight together
   {
     const int NZ = kMlaHeads * 512;
     const int e0 = (int)((long long)i * NZ / G), e1 = (int)((long long)(i + 1) * NZ / G);
     const int stride = 2 * kMlaHeads + kMlaHeads * 512;
-    for (int e = e0 + tid; e < e1; e += kConsumerThreads) {
-      const int h = e / 512;
+    const int h0 = e0 / 512, h1 = (e1 - 1) / 512;
+    float* wq = reinterpret_cast<float*>(zs);  // [2][G2] weights, then [2] 1/l
+    if (warp < 2 && h0 + warp <= h1) {
+      const int h = h0 + warp;
       float M = -INFINITY;
-      for (int q = 0; q < G2; ++q) M = fmaxf(M, __ldcg(p.part + (size_t)q * stride + h));
-      float l = 0.f, z = 0.f;
-      for (int q = 0; q < G2; ++q) {
-        const float* pq = p.part + (size_t)q * stride;
-        const float mq = __ldcg(pq + h);
+      for (int q = lane; q < G2; q += 32) M = fmaxf(M, __ldcg(p.part + (size_t)q * stride + h));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+      float l = 0.f;
+      for (int q = lane; q < G2; q += 32) {
+        const float mq = __ldcg(p.part + (size_t)q * stride + h);
         const float w = mq == -INFINITY ? 0.f : exp2f(mq - M);
-        l = fmaf(__ldcg(pq + kMlaHeads + h), w, l);
-        z = fmaf(__ldcg(pq + 2 * kMlaHeads + e), w, z);
+        wq[warp * G2 + q] = w;
+        l = fmaf(__ldcg(p.part + (size_t)q * stride + kMlaHeads + h), w, l);
       }
-      p.zb[e] = __float2half_rn(__fdiv_rn(z, l));
+      l = warp_allsum(l);
+      if (lane == 0) wq[2 * G2 + warp] = 1.0f / l;
+    }
+    consumer_sync();
+    for (int eb = e0 + 4 * warp; eb < e1; eb += 4 * kNumConsumerWarps) {
+      float z[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int q = lane; q < G2; q += 32) {
+        const float* zq = p.part + (size_t)q * stride + 2 * kMlaHeads;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (eb + k < e1) z[k] = fmaf(__ldcg(zq + eb + k), wq[((eb + k) / 512 - h0) * G2 + q], z[k]);
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float v = warp_allsum(z[k]);
+        if (lane == 0 && eb + k < e1) p.zb[eb + k] = __float2half_rn(v * wq[2 * G2 + (eb + k) / 512 - h0]);
+      }
     }
   }
   grid_barrier(p.barrier + 1, tid);
