@@ -477,30 +477,50 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   // down, routed gate/up and down
   route();
   stamp(3);
-  for (int g = rs.s0; g < rs.s1; g += kMoeChunk)
-    gate_up(gu_phase(p.s_gu, g, min(kMoeChunk, rs.s1 - g)), min(kMoeChunk, rs.s1 - g),
-            act_s + 8 * (g - rs.s0));
-  stamp(4);
-  zero_acc();
-  down(dn_phase(p.s_dn, rs.s0, rs.s1 - rs.s0), act_s, 0);
-  flush(nullptr, false);
-  stamp(5);
+  // one schedule loop with a single call site per phase kind, so the large
+  // unrolled gate/up and down bodies exist once in the binary (one-shot code
+  // runs from a cold instruction cache every launch):
+  //   pass 0 shared gate/up chunks, 1 shared down, 2 routed gate/up, 3 routed down
   const int U = slot_e[L.umax];
   const MoeRange m = moe_range(i, G, Gs, U * Ge);
-  for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
-    int ga, gb;
-    const int e = seg(m, u, ga, gb);
-    for (int g = ga; g < gb; g += kMoeChunk)
-      gate_up(gu_phase(p.w_gu + e * eGu, g, min(kMoeChunk, gb - g)), min(kMoeChunk, gb - g),
-              act_r + 8 * (u * Ge + g - m.r0));
-  }
-  stamp(6);
-  for (int u = m.r0 / Ge; u < U && u * Ge < m.r1; ++u) {
-    int ga, gb;
-    const int e = seg(m, u, ga, gb);
-    zero_acc();
-    down(dn_phase(p.w_dn + e * eDn, ga, gb - ga), act_r, u * Ge + ga - m.r0);
-    flush(gw + u, true);
+  const int u_first = m.r0 / Ge;
+  for (int pass = 0; pass < 4; ++pass) {
+    const bool routed = pass >= 2, dn = pass & 1;
+    const int nseg = routed ? max(0, min(U, (m.r1 + Ge - 1) / Ge) - u_first) : 1;
+    for (int sg = 0; sg < nseg; ++sg) {
+      int ga, gb, e = 0;
+      const __half *gub, *dnb;
+      __half* act_seg;
+      int g_off;  // local group index = group index within the segment's matrix + g_off
+      if (routed) {
+        const int u = u_first + sg;
+        e = seg(m, u, ga, gb);
+        gub = p.w_gu + e * eGu;
+        dnb = p.w_dn + e * eDn;
+        act_seg = act_r;
+        g_off = u * Ge - m.r0;
+      } else {
+        ga = rs.s0;
+        gb = rs.s1;
+        gub = p.s_gu;
+        dnb = p.s_dn;
+        act_seg = act_s;
+        g_off = -rs.s0;
+      }
+      if (!dn) {
+        for (int g = ga; g < gb; g += kMoeChunk)
+          gate_up(gu_phase(gub, g, min(kMoeChunk, gb - g)), min(kMoeChunk, gb - g),
+                  act_seg + 8 * (g + g_off));
+      } else {
+        zero_acc();
+        down(dn_phase(dnb, ga, gb - ga), act_seg, ga + g_off);
+        flush(routed ? gw + (u_first + sg) : nullptr, routed || sg > 0);
+      }
+    }
+    if (pass == 1 && nseg == 0) {  // no shared experts: the routed flushes add onto zeros
+      zero_acc();
+      flush(nullptr, false);
+    }
   }
   consumer_sync();
   stamp(7);
