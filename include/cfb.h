@@ -16,6 +16,7 @@
  *   cfb_mla_engine_decode  <- dataflows.py:316-429 math, head-batched for the DeepSeek block
  *   cfb_moe_decode         <- no reference counterpart: DeepSeek-V2 MoE
  *                            (transformers DeepseekV2Moe semantics, oracle/deepseek_port.py)
+ *   cfb_tc_gemm_b16        <- no reference counterpart: batch-16 projections on tcgen05 (north star)
  *   cfb_cluster_collective <- collectives.py:110-203 cluster_reduce / cluster_gather (DSMEM KAT kernel)
  *   cfb_lm_head_argmax, cfb_embed, cfb_llama_*  <- no reference counterpart (SPEC.md:298 non-goals);
  *                            the north-star decode loop around the fused modules.
@@ -307,6 +308,19 @@ typedef struct cfb_lm_args {
   int* step_pos;
 } cfb_lm_args;
 int cfb_lm_head_argmax(const cfb_lm_args* args, void* stream);
+
+/*
+ * Batch-16 projection on the tcgen05 tensor cores (swap-AB: weights = MMA M,
+ * batch = N = 16; TMEM accumulators): y[n][m] = sum_k W[m][k] x[n][k].
+ *   w_packed  W (M x K fp16) in UMMA blocks: [M/128][K/64][k-step 4][K half 2]
+ *             [row group 16][8 rows][8]  (K-major, no swizzle; see csrc/tc_gemm.cu)
+ *   x         [16][K] fp16 row-major; x_packed: 16*K fp16 workspace
+ *   y_acc     [16][M] u64 fixed-point workspace, zero before first use
+ *   y         [16][M] fp32 out (= [resid +] y_acc * 2^-32, y_acc re-zeroed), or NULL
+ *             to leave the sum in y_acc.   M % 128 == 0, K % 64 == 0.
+ */
+int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigned long long* y_acc,
+                    float* y, const float* resid, int M, int K, int flags, void* stream);
 
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,

@@ -150,6 +150,8 @@ class MoeArgs(ctypes.Structure):
 
 
 def bind_extra(L) -> None:
+    L.cfb_tc_gemm_b16.argtypes = [_vp] * 6 + [ctypes.c_int] * 3 + [_vp]
+    L.cfb_tc_gemm_b16.restype = ctypes.c_int
     L.cfb_mla_engine_decode.argtypes = [ctypes.POINTER(MlaEngineArgs), _vp]
     L.cfb_mla_engine_decode.restype = ctypes.c_int
     L.cfb_moe_decode.argtypes = [ctypes.POINTER(MoeArgs), _vp]

@@ -1,0 +1,306 @@
+// Batch>1 projections on the 5th-generation tensor cores (tcgen05 + TMEM).
+//
+// At batch 16 a decode projection y = x W^T (W: M x K fp16, x: 16 x K) is a
+// real dense contraction (16 flop/byte - still HBM-bound, but 16 FMAs per
+// weight would saturate the CUDA cores).  Swap-AB: the weights are the MMA's
+// M = 128 operand, the 16 batch rows the N = 16 operand, so one
+// tcgen05.mma.cta_group::1.kind::f16 (M128 N16 K16) consumes 4 KB of weights.
+//
+// Work unit = (128-row weight tile, chunk of K): units are dealt to a
+// persistent grid in contiguous runs (split-K keeps 148 SMs evenly busy even
+// when M/128 is not a multiple of 148).  Per CTA:
+//   warp 0 lane 0   producer: cp.async.bulk of 16 KB weight blocks (128 rows x
+//                   64 K, pre-packed on the host in the UMMA K-major
+//                   no-swizzle "core matrix" order, so a plain bulk copy lands
+//                   in the canonical smem layout - no tensor map needed) and
+//                   the matching 2 KB activation blocks into an S-stage ring
+//   warp 1 lane 0   MMA issuer: 4 x tcgen05.mma per block into a TMEM
+//                   accumulator (128 lanes x 16 fp32 columns, double-buffered
+//                   across units); tcgen05.commit frees ring stages and
+//                   signals the epilogue
+//   warps 2..5      epilogue: tcgen05.ld 32x32b.x16 (one TMEM lane quarter
+//                   per warp) -> 64-bit fixed-point red.add into y_acc[n][m]
+//                   (integer adds: split-K partials sum order-independently)
+//
+// Packed layouts (fp16), "core matrix" = 8 rows x 16 bytes (8 K elements):
+//   W block (tile t, kb): [s = k-step (4)][c = K half (2)][g = row group (16)][8 rows][8]
+//   X block (kb):         [s (4)][c (2)][g = batch group (2)][8 rows][8]
+// UMMA smem descriptors (K-major, SWIZZLE_NONE): SBO = 128 B between row
+// groups, LBO = 2048 B (W) / 256 B (X) between the two K core matrices.
+#include <cuda_runtime.h>
+
+#include "common.h"
+#include "ptx.cuh"
+
+namespace cfb {
+
+constexpr int kTcN = 16;            // batch rows = MMA N
+constexpr int kTcM = 128;           // weight rows per tile = MMA M
+constexpr int kTcKB = 64;           // K elements per block
+constexpr int kTcABytes = kTcM * kTcKB * 2;   // 16 KB
+constexpr int kTcBBytes = kTcN * kTcKB * 2;   // 2 KB
+constexpr int kTcStages = 8;
+constexpr int kTcThreads = 6 * 32;
+
+struct TcParams {
+  const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
+  const __half* x;   // packed activation blocks [K/64][2 KB]
+  unsigned long long* y;  // [16][M] fixed point (2^-32), accumulated
+  int M, K, kchunk, units;  // kchunk: K blocks per unit
+};
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);  // version 1, SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t ad, uint64_t bd, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+      "l"(ad), "l"(bd), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p) {
+  extern __shared__ __align__(1024) char smem[];
+  char* sa = smem;                                   // [S][16 KB]
+  char* sb = smem + kTcStages * kTcABytes;           // [S][2 KB]
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kTcStages * kTcBBytes);
+  uint64_t* empty = full + kTcStages;
+  uint64_t* accf = empty + kTcStages;  // [2] accumulator ready
+  uint64_t* acce = accf + 2;           // [2] accumulator drained
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, i = blockIdx.x;
+  const int u0 = (int)((long long)i * p.units / G), u1 = (int)((long long)(i + 1) * p.units / G);
+  const int KBt = p.K / kTcKB, nkc = (KBt + p.kchunk - 1) / p.kchunk;
+
+  if (tid == 0) {
+    for (int s = 0; s < kTcStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&accf[0], 1);
+    mbar_init(&accf[1], 1);
+    mbar_init(&acce[0], 4);
+    mbar_init(&acce[1], 4);
+    fence_mbar_init();
+  }
+  if (warp == 1) {  // TMEM: 2 accumulators x 16 columns
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+                     smem_u32(tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_launch_dependents();
+
+  auto unit_kb = [&](int u, int& t, int& kb0, int& nkb) {
+    t = u / nkc;
+    const int kc = u % nkc;
+    kb0 = kc * p.kchunk;
+    nkb = min(p.kchunk, KBt - kb0);
+  };
+
+  if (warp == 0) {  // ------------------------------------------------ producer
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      pdl_wait();  // activations come from the previous kernel
+      int it = 0;
+      for (int u = u0; u < u1; ++u) {
+        int t, kb0, nkb;
+        unit_kb(u, t, kb0, nkb);
+        for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
+          const int s = it % kTcStages;
+          if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], kTcABytes + kTcBBytes);
+          bulk_g2s(sa + s * kTcABytes, p.w + ((size_t)t * KBt + kb) * (kTcABytes / 2), kTcABytes,
+                   &full[s], pol);
+          bulk_g2s(sb + s * kTcBBytes, p.x + (size_t)kb * (kTcBBytes / 2), kTcBBytes, &full[s],
+                   policy_evict_last());
+        }
+      }
+    }
+  } else if (warp == 1) {  // ------------------------------------------ MMA issuer
+    if (lane == 0) {
+      // kind::f16, D f32, A/B f16 K-major, N = 16, M = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      int it = 0, n = 0;
+      for (int u = u0; u < u1; ++u, ++n) {
+        int t, kb0, nkb;
+        unit_kb(u, t, kb0, nkb);
+        const int a = n & 1;
+        if (n >= 2) mbar_wait(&acce[a], ((n >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t dt = tmem + (uint32_t)(a * kTcN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kTcStages;
+          mbar_wait(&full[s], (it / kTcStages) & 1);
+          tc_fence_after();
+          const uint32_t abase = smem_u32(sa + s * kTcABytes), bbase = smem_u32(sb + s * kTcBBytes);
+#pragma unroll
+          for (int ks = 0; ks < 4; ++ks)
+            tc_mma(dt, umma_desc(abase + ks * 4096, 2048, 128), umma_desc(bbase + ks * 512, 256, 128),
+                   idesc, (kb | ks) ? 1u : 0u);
+          tc_commit(&empty[s]);  // stage free once these MMAs have read it
+        }
+        tc_commit(&accf[a]);      // accumulator complete
+      }
+    }
+  } else {  // -------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    int n = 0;
+    for (int u = u0; u < u1; ++u, ++n) {
+      int t, kb0, nkb;
+      unit_kb(u, t, kb0, nkb);
+      const int a = n & 1;
+      mbar_wait(&accf[a], (n >> 1) & 1);
+      tc_fence_after();
+      uint32_t r[16];
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15])
+          : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kTcN)));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acce[a]);
+      const int m = t * kTcM + 32 * q + lane;
+#pragma unroll
+      for (int c = 0; c < kTcN; ++c) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+  }
+}
+
+// x [16][K] fp16 row-major -> packed UMMA blocks (see header).
+__global__ void tc_pack_x_kernel(const __half* x, __half* xp, int K) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int nvec = kTcN * K / 8;  // 16-byte vectors
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
+    const int n = v / (K / 8), kv = v % (K / 8);  // row n, elements 8kv..8kv+7
+    const int k = kv * 8, kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
+    const size_t dst = (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8;
+    *reinterpret_cast<uint4*>(xp + dst) = *reinterpret_cast<const uint4*>(x + (size_t)n * K + k);
+  }
+}
+
+// y_acc fixed point [16][M] -> out fp32 [16][M] (optionally + resid), re-zeroes y_acc
+__global__ void tc_finish_kernel(unsigned long long* yacc, float* out, const float* resid, int n) {
+  pdl_wait();
+  pdl_launch_dependents();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    float v = fixed_to_float(yacc[i]);
+    yacc[i] = 0ull;
+    out[i] = resid ? __fadd_rn(resid[i], v) : v;
+  }
+}
+
+int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytes) + (4 * kTcStages + 8) * 8 + 16; }
+
+int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
+            cudaStream_t st, bool pdl) {
+  if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
+  static bool configured = false;
+  if (!configured) {
+    CFB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
+    configured = true;
+  }
+  int dev = 0, sms = 0;
+  CFB_CUDA(cudaGetDevice(&dev));
+  CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (grid <= 0 || grid > sms) grid = sms;
+  const int KBt = K / kTcKB, tiles = M / kTcM;
+  // split K so that units >= ~4 per CTA: even streaming across the grid
+  int kchunk = KBt;
+  while (kchunk > 4 && (long long)tiles * ((KBt + kchunk - 1) / kchunk) < 4LL * grid) kchunk = (kchunk + 1) / 2;
+  TcParams p;
+  p.w = w;
+  p.x = xpacked;
+  p.y = y;
+  p.M = M;
+  p.K = K;
+  p.kchunk = kchunk;
+  p.units = tiles * ((KBt + kchunk - 1) / kchunk);
+  if (grid > p.units) grid = p.units;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(kTcThreads, 1, 1);
+  cfg.dynamicSmemBytes = tc_smem_bytes();
+  cfg.stream = st;
+  LaunchAttrs at(0, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, p));
+  return CFB_OK;
+}
+
+int tc_pack_x(const __half* x, __half* xp, int K, cudaStream_t st, bool pdl) {
+  if (K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_pack_x: K %% 64 must be 0");
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((kTcN * K / 8 + 255) / 256, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = st;
+  LaunchAttrs at(0, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_pack_x_kernel, x, xp, K));
+  return CFB_OK;
+}
+
+int tc_finish(unsigned long long* yacc, float* out, const float* resid, int n, cudaStream_t st, bool pdl) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((n + 255) / 256, 1, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = st;
+  LaunchAttrs at(0, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_finish_kernel, yacc, out, resid, n));
+  return CFB_OK;
+}
+
+}  // namespace cfb
+
+extern "C" {
+
+int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigned long long* y_acc,
+                    float* y, const float* resid, int M, int K, int flags, void* stream) {
+  using namespace cfb;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (!w_packed || !x || !x_packed || !y_acc) return set_error(CFB_ERR_ARGUMENT, "null pointer");
+  const bool pdl = flags & CFB_PDL;
+  int rc = tc_pack_x(static_cast<const __half*>(x), static_cast<__half*>(x_packed), K, st, pdl);
+  if (rc) return rc;
+  if ((rc = tc_gemm(static_cast<const __half*>(w_packed), static_cast<const __half*>(x_packed), y_acc,
+                    M, K, 0, st, true)))
+    return rc;
+  if (!y) return CFB_OK;
+  return tc_finish(y_acc, y, resid, 16 * M, st, true);
+}
+
+}  // extern "C"

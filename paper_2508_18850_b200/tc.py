@@ -1,0 +1,63 @@
+"""Batch-16 projections on the tcgen05 tensor cores (``csrc/tc_gemm.cu``).
+
+y[n][m] = sum_k W[m][k] x[n][k] for 16 batch rows: the weights are the MMA's
+M = 128 operand (swap-AB), accumulators live in TMEM, split-K partials are
+summed in 64-bit fixed point.  ``pack_umma`` lays W out in the UMMA K-major
+no-swizzle core-matrix order so the kernel's plain bulk copies land in the
+canonical shared-memory layout.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError
+
+BATCH = 16
+
+
+def pack_umma(w):
+    """(M, K) fp16 torch tensor -> [M/128][K/64][4][2][16][8][8] (flattened)."""
+    M, K = w.shape
+    if M % 128 or K % 64:
+        raise DimensionError("tcgen05 projection needs M % 128 == 0 and K % 64 == 0")
+    t = w.reshape(M // 128, 16, 8, K // 64, 4, 2, 8)      # (t, g, r, kb, s, c, e)
+    return t.permute(0, 3, 4, 5, 1, 2, 6).contiguous()
+
+
+class TcProjection:
+    """Device-resident packed weight + workspaces for y = x W^T at batch 16."""
+
+    def __init__(self, w, device=None):
+        import torch
+        dev = device or _native.require_cuda()
+        if not isinstance(w, torch.Tensor):
+            w = torch.from_numpy(np.ascontiguousarray(w, np.float32))
+        w = w.to(dev).half()
+        self.M, self.K = w.shape
+        self.wp = pack_umma(w)
+        self.xp = torch.zeros(BATCH * self.K, device=dev, dtype=torch.float16)
+        self.acc = torch.zeros(BATCH, self.M, device=dev, dtype=torch.int64)
+        torch.cuda.synchronize()
+
+    def launch(self, x, y=None, resid=None, pdl=False, stream=None):
+        """x: (16, K) fp16 device tensor; y: (16, M) fp32 or None (sum stays in acc)."""
+        _native.check(_native.lib().cfb_tc_gemm_b16(
+            self.wp.data_ptr(), x.data_ptr(), self.xp.data_ptr(), self.acc.data_ptr(),
+            _native.ptr(y), _native.ptr(resid), self.M, self.K, _native.PDL if pdl else 0,
+            _native.stream_ptr(stream)))
+
+
+def run_projection_b16(w, x) -> np.ndarray:
+    """Host convenience: (M, K) weights, (16, K) activations -> (16, M) fp32."""
+    import torch
+    dev = _native.require_cuda()
+    proj = TcProjection(w, dev)
+    xt = torch.from_numpy(np.ascontiguousarray(x, np.float32)).to(dev).half()
+    if xt.shape != (BATCH, proj.K):
+        raise DimensionError(f"x must be ({BATCH}, {proj.K})")
+    y = torch.empty(BATCH, proj.M, device=dev, dtype=torch.float32)
+    proj.launch(xt, y)
+    torch.cuda.synchronize()
+    return y.cpu().numpy()

@@ -1,0 +1,44 @@
+"""Batch-16 projections on tcgen05 (csrc/tc_gemm.cu) against an fp32 numpy
+reference of the same contraction on identical fp16-valued inputs
+(tolerance: max-abs 2e-2 and max-rel 1e-3 of max|y| - fp32 TMEM accumulation,
+fixed-point split-K sums)."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from oracle.llama_port import f16
+from paper_2508_18850_b200.tc import TcProjection, pack_umma, run_projection_b16
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("M,K", [(128, 64), (256, 128), (384, 1024), (4096, 4096), (4096, 11008)])
+def test_tc_projection_matches_fp32(M, K):
+    rng = np.random.default_rng(M + K)
+    w = f16(rng.standard_normal((M, K)) * K ** -0.5)
+    x = f16(rng.standard_normal((16, K)))
+    y = run_projection_b16(w, x)
+    ref = x @ w.T
+    err = float(np.max(np.abs(y - ref)))
+    assert err <= 2e-2 and err <= 1e-3 * max(1.0, float(np.max(np.abs(ref)))), (M, K, err)
+
+
+def test_tc_projection_repeat_and_layout():
+    """Repeated launches re-zero the accumulator; the packing is a pure permutation."""
+    import torch
+    rng = np.random.default_rng(0)
+    w = f16(rng.standard_normal((256, 128)))
+    x = f16(rng.standard_normal((16, 128)))
+    proj = TcProjection(w)
+    xt = torch.from_numpy(x).cuda().half()
+    y = torch.empty(16, 256, device="cuda")
+    outs = []
+    for _ in range(3):
+        proj.launch(xt, y)
+        torch.cuda.synchronize()
+        outs.append(y.cpu().numpy().copy())
+    assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
+    wp = pack_umma(torch.from_numpy(w).half())
+    assert sorted(wp.flatten().float().tolist()) == sorted(torch.from_numpy(w).half().flatten().float().tolist())
