@@ -322,6 +322,28 @@ int cfb_lm_head_argmax(const cfb_lm_args* args, void* stream);
 int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigned long long* y_acc,
                     float* y, const float* resid, int M, int K, int flags, void* stream);
 
+/*
+ * Batch-16 SwiGLU FFN block on tcgen05: resid[n] += FFN(f16(rmsnorm(resid[n]) * norm_w))
+ * for 16 rows: RMSNorm+pack -> [w1; w2] projection -> SiLU*mul+pack -> w3
+ * projection -> residual add (5 PDL-chained launches).  w_gu = pack of
+ * [w1; w2] (2F x D), w_dn = pack of w3 (D x F) (cfb_tc_gemm_b16 layout).
+ * Workspaces: xp 16*D fp16, gu_acc 16*2F u64 (zero), ap 16*F fp16, out_acc
+ * 16*D u64 (zero).  hidden % 128 == 0, inter % 64 == 0.
+ */
+typedef struct cfb_ffn_b16_args {
+  int hidden, inter, flags;
+  float eps;
+  float* resid;
+  const void* norm_w;
+  const void* w_gu;
+  const void* w_dn;
+  void* xp;
+  unsigned long long* gu_acc;
+  void* ap;
+  unsigned long long* out_acc;
+} cfb_ffn_b16_args;
+int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
+
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,
               void* stream);

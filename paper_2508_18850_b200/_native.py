@@ -139,6 +139,13 @@ class MlaEngineArgs(ctypes.Structure):
                            "part", "zb", "ob", "accum", "barrier")]
 
 
+class FfnB16Args(ctypes.Structure):
+    """Mirror of ``cfb_ffn_b16_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("hidden", "inter", "flags")] + [("eps", ctypes.c_float)] + [
+        (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc")]
+
+
 class MoeArgs(ctypes.Structure):
     """Mirror of ``cfb_moe_args``."""
 
@@ -152,6 +159,8 @@ class MoeArgs(ctypes.Structure):
 def bind_extra(L) -> None:
     L.cfb_tc_gemm_b16.argtypes = [_vp] * 6 + [ctypes.c_int] * 3 + [_vp]
     L.cfb_tc_gemm_b16.restype = ctypes.c_int
+    L.cfb_ffn_b16.argtypes = [ctypes.POINTER(FfnB16Args), _vp]
+    L.cfb_ffn_b16.restype = ctypes.c_int
     L.cfb_mla_engine_decode.argtypes = [ctypes.POINTER(MlaEngineArgs), _vp]
     L.cfb_mla_engine_decode.restype = ctypes.c_int
     L.cfb_moe_decode.argtypes = [ctypes.POINTER(MoeArgs), _vp]

@@ -57,6 +57,7 @@ int mla_decode(const cfb_mla_args* a, cudaStream_t st);
 int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st);
 int splithead_decode(const cfb_splithead_args* a, cudaStream_t st);
 int ffn_decode(const cfb_ffn_args* a, cudaStream_t st);
+int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st);
 int moe_decode(const cfb_moe_args* a, cudaStream_t st);
 int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st);
 int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,

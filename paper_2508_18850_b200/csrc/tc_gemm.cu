@@ -46,7 +46,7 @@ struct TcParams {
   const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
   const __half* x;   // packed activation blocks [K/64][2 KB]
   unsigned long long* y;  // [16][M] fixed point (2^-32), accumulated
-  int M, K, kchunk, units;  // kchunk: K blocks per unit
+  int M, K;
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -85,8 +85,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int G = gridDim.x, i = blockIdx.x;
-  const int u0 = (int)((long long)i * p.units / G), u1 = (int)((long long)(i + 1) * p.units / G);
-  const int KBt = p.K / kTcKB, nkc = (KBt + p.kchunk - 1) / p.kchunk;
+  // CTA i owns weight blocks [b0, b1) of the (tile-major, K-minor) sequence: an
+  // even split at 16 KB granularity; a "segment" is its run inside one tile,
+  // accumulated in TMEM and flushed once (split-K only at tile boundaries)
+  const int KBt = p.K / kTcKB, TB = (p.M / kTcM) * KBt;
+  const int b0 = (int)((long long)i * TB / G), b1 = (int)((long long)(i + 1) * TB / G);
+  const int nseg = b1 > b0 ? (b1 - 1) / KBt - b0 / KBt + 1 : 0;
 
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
@@ -111,11 +115,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   const uint32_t tmem = *tmem_slot;
   pdl_launch_dependents();
 
-  auto unit_kb = [&](int u, int& t, int& kb0, int& nkb) {
-    t = u / nkc;
-    const int kc = u % nkc;
-    kb0 = kc * p.kchunk;
-    nkb = min(p.kchunk, KBt - kb0);
+  auto unit_kb = [&](int u, int& t, int& kb0, int& nkb) {  // segment u of this CTA
+    t = b0 / KBt + u;
+    const int lo = max(b0, t * KBt), hi = min(b1, (t + 1) * KBt);
+    kb0 = lo - t * KBt;
+    nkb = hi - lo;
   };
 
   if (warp == 0) {  // ------------------------------------------------ producer
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       const uint64_t pol = policy_evict_first();
       pdl_wait();  // activations come from the previous kernel
       int it = 0;
-      for (int u = u0; u < u1; ++u) {
+      for (int u = 0; u < nseg; ++u) {
         int t, kb0, nkb;
         unit_kb(u, t, kb0, nkb);
         for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
@@ -142,7 +146,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       // kind::f16, D f32, A/B f16 K-major, N = 16, M = 128
       const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
       int it = 0, n = 0;
-      for (int u = u0; u < u1; ++u, ++n) {
+      for (int u = 0; u < nseg; ++u, ++n) {
         int t, kb0, nkb;
         unit_kb(u, t, kb0, nkb);
         const int a = n & 1;
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   } else {  // -------------------------------------------------------- epilogue
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int n = 0;
-    for (int u = u0; u < u1; ++u, ++n) {
+    for (int u = 0; u < nseg; ++u, ++n) {
       int t, kb0, nkb;
       unit_kb(u, t, kb0, nkb);
       const int a = n & 1;
@@ -234,19 +238,14 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (grid <= 0 || grid > sms) grid = sms;
-  const int KBt = K / kTcKB, tiles = M / kTcM;
-  // split K so that units >= ~4 per CTA: even streaming across the grid
-  int kchunk = KBt;
-  while (kchunk > 4 && (long long)tiles * ((KBt + kchunk - 1) / kchunk) < 4LL * grid) kchunk = (kchunk + 1) / 2;
+  const int TB = (M / kTcM) * (K / kTcKB);
   TcParams p;
   p.w = w;
   p.x = xpacked;
   p.y = y;
   p.M = M;
   p.K = K;
-  p.kchunk = kchunk;
-  p.units = tiles * ((KBt + kchunk - 1) / kchunk);
-  if (grid > p.units) grid = p.units;
+  if (grid > TB) grid = TB;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kTcThreads, 1, 1);
@@ -284,6 +283,95 @@ int tc_finish(unsigned long long* yacc, float* out, const float* resid, int n, c
   return CFB_OK;
 }
 
+// ---------------------------------------------------------------- batch-16 FFN
+// x = f16(rmsnorm(resid[n]) * g) written straight into the packed UMMA layout
+// (one CTA per batch row).
+__global__ void tc_rmsnorm_pack_kernel(const float* resid, const __half* g, __half* xp, int D, float eps) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n = blockIdx.x, tid = threadIdx.x;
+  __shared__ float red[32];
+  const float* r = resid + (size_t)n * D;
+  float ss = 0.f;
+  for (int d = tid; d < D; d += blockDim.x) ss = fmaf(r[d], r[d], ss);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((tid & 31) == 0) red[tid >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
+  for (int k = tid * 8; k < D; k += blockDim.x * 8) {
+    __align__(16) __half h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e)
+      h[e] = __float2half_rn(__fmul_rn(__fmul_rn(r[k + e], inv), __half2float(g[k + e])));
+    const int kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
+    *reinterpret_cast<uint4*>(xp + (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8) =
+        *reinterpret_cast<const uint4*>(h);
+  }
+}
+
+// act = f16(silu(gate) * up) from the fixed-point gate/up sums (rows f and F+f
+// of the [w1; w2] projection), packed for the down projection; re-zeroes gu.
+__global__ void tc_swiglu_pack_kernel(unsigned long long* gu, __half* ap, int F) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int nvec = kTcN * F / 8;
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
+    const int n = v / (F / 8), f0 = (v % (F / 8)) * 8;
+    __align__(16) __half h[8];
+    unsigned long long* gr = gu + (size_t)n * 2 * F;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float gt = fixed_to_float(gr[f0 + e]), up = fixed_to_float(gr[F + f0 + e]);
+      gr[f0 + e] = 0ull;
+      gr[F + f0 + e] = 0ull;
+      h[e] = __float2half_rn(__fmul_rn(__fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt))), up));
+    }
+    const int kb = f0 / kTcKB, kk = f0 % kTcKB, s = kk / 16, c = (kk % 16) / 8;
+    *reinterpret_cast<uint4*>(ap + (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8) =
+        *reinterpret_cast<const uint4*>(h);
+  }
+}
+
+template <class K, class... Args>
+static int launch_simple(K kern, int grid, int block, cudaStream_t st, bool pdl, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.blockDim = dim3(block, 1, 1);
+  cfg.stream = st;
+  LaunchAttrs at(0, pdl);
+  cfg.attrs = at.a;
+  cfg.numAttrs = at.n;
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, args...));
+  return CFB_OK;
+}
+
+int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
+  if (!a || !a->resid || !a->norm_w || !a->w_gu || !a->w_dn || !a->xp || !a->gu_acc || !a->ap ||
+      !a->out_acc)
+    return set_error(CFB_ERR_ARGUMENT, "null pointer");
+  const int D = a->hidden, F = a->inter;
+  if (D % 128 || F % 64 || (2 * F) % 128)
+    return set_error(CFB_ERR_DIMENSION, "ffn_b16: hidden %% 128 and inter %% 64 must be 0");
+  const bool pdl = a->flags & CFB_PDL;
+  int rc;
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, 256, st, pdl, a->resid,
+                          static_cast<const __half*>(a->norm_w), static_cast<__half*>(a->xp), D, a->eps)))
+    return rc;
+  if ((rc = tc_gemm(static_cast<const __half*>(a->w_gu), static_cast<const __half*>(a->xp), a->gu_acc,
+                    2 * F, D, 0, st, true)))
+    return rc;
+  if ((rc = launch_simple(tc_swiglu_pack_kernel, (kTcN * F / 8 + 255) / 256, 256, st, true, a->gu_acc,
+                          static_cast<__half*>(a->ap), F)))
+    return rc;
+  if ((rc = tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc,
+                    D, F, 0, st, true)))
+    return rc;
+  return tc_finish(a->out_acc, a->resid, a->resid, kTcN * D, st, true);
+}
+
 }  // namespace cfb
 
 extern "C" {
@@ -301,6 +389,10 @@ int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigne
     return rc;
   if (!y) return CFB_OK;
   return tc_finish(y_acc, y, resid, 16 * M, st, true);
+}
+
+int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream) {
+  return cfb::ffn_b16(args, static_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

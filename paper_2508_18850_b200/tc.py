@@ -61,3 +61,40 @@ def run_projection_b16(w, x) -> np.ndarray:
     proj.launch(xt, y)
     torch.cuda.synchronize()
     return y.cpu().numpy()
+
+
+class TcFfnB16:
+    """Batch-16 SwiGLU FFN block on tcgen05 (``cfb_ffn_b16``): resid += FFN(rmsnorm(resid))."""
+
+    def __init__(self, w1, w2, w3, norm_w, eps: float = 1e-5, device=None):
+        import torch
+        dev = device or _native.require_cuda()
+
+        def t(a):
+            if not isinstance(a, torch.Tensor):
+                a = torch.from_numpy(np.ascontiguousarray(a, np.float32))
+            return a.to(dev).half()
+
+        w1, w2, w3 = t(w1), t(w2), t(w3)
+        self.F, self.D = w1.shape
+        self.eps = eps
+        self.w_gu = pack_umma(torch.cat([w1, w2], 0))
+        self.w_dn = pack_umma(w3)
+        self.g = t(norm_w)
+        self.xp = torch.zeros(BATCH * self.D, device=dev, dtype=torch.float16)
+        self.gu_acc = torch.zeros(BATCH * 2 * self.F, device=dev, dtype=torch.int64)
+        self.ap = torch.zeros(BATCH * self.F, device=dev, dtype=torch.float16)
+        self.out_acc = torch.zeros(BATCH * self.D, device=dev, dtype=torch.int64)
+        torch.cuda.synchronize()
+
+    @property
+    def weight_bytes(self) -> int:
+        return 3 * self.D * self.F * 2 + self.D * 2
+
+    def launch(self, resid, pdl: bool = False, stream=None) -> None:
+        a = _native.FfnB16Args(hidden=self.D, inter=self.F, flags=_native.PDL if pdl else 0,
+                               eps=self.eps, resid=resid.data_ptr(), norm_w=self.g.data_ptr(),
+                               w_gu=self.w_gu.data_ptr(), w_dn=self.w_dn.data_ptr(),
+                               xp=self.xp.data_ptr(), gu_acc=self.gu_acc.data_ptr(),
+                               ap=self.ap.data_ptr(), out_acc=self.out_acc.data_ptr())
+        _native.check(_native.lib().cfb_ffn_b16(a, _native.stream_ptr(stream)))

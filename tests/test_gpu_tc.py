@@ -42,3 +42,25 @@ def test_tc_projection_repeat_and_layout():
     assert outs[0].tobytes() == outs[1].tobytes() == outs[2].tobytes()
     wp = pack_umma(torch.from_numpy(w).half())
     assert sorted(wp.flatten().float().tolist()) == sorted(torch.from_numpy(w).half().flatten().float().tolist())
+
+
+@pytest.mark.parametrize("D,F", [(512, 1408), (4096, 11008)])
+def test_tc_ffn_b16_matches_oracle(D, F):
+    """Batch-16 FFN block (RMSNorm -> SwiGLU -> residual) vs oracle/llama_port.ffn_block."""
+    import torch
+    from oracle import llama_port as lp
+    from paper_2508_18850_b200.tc import TcFfnB16
+    rng = np.random.default_rng(D)
+    x = rng.standard_normal((16, D)).astype(np.float32)
+    g = f16(1 + 0.1 * rng.standard_normal(D))
+    w1 = f16(rng.standard_normal((F, D)) * D ** -0.5)
+    w2 = f16(rng.standard_normal((F, D)) * D ** -0.5)
+    w3 = f16(rng.standard_normal((D, F)) * F ** -0.5)
+    ffn = TcFfnB16(w1, w2, w3, g, eps=1e-5)
+    r = torch.from_numpy(x).cuda()
+    ffn.launch(r)
+    torch.cuda.synchronize()
+    got = r.cpu().numpy()
+    ref = x + lp.ffn_block(x, g, w1, w2, w3, 1e-5)
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= 2e-2 and err / float(np.max(np.abs(ref))) <= 1e-2, err
