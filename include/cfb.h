@@ -325,10 +325,13 @@ int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigne
 /*
  * Batch-16 SwiGLU FFN block on tcgen05: resid[n] += FFN(f16(rmsnorm(resid[n]) * norm_w))
  * for 16 rows: RMSNorm+pack -> [w1; w2] projection -> SiLU*mul+pack -> w3
- * projection -> residual add (5 PDL-chained launches).  w_gu = pack of
- * [w1; w2] (2F x D), w_dn = pack of w3 (D x F) (cfb_tc_gemm_b16 layout).
+ * projection -> residual add (3 PDL-chained launches; the last CTA to finish
+ * a 128-row tile applies SiLU*mul / the residual add).  w_gu = pack of the
+ * gate/up rows interleaved per 64: [w1[0:64]; w2[0:64]; w1[64:128]; ...]
+ * (2F x D), w_dn = pack of w3 (D x F) (cfb_tc_gemm_b16 layout).
  * Workspaces: xp 16*D fp16, gu_acc 16*2F u64 (zero), ap 16*F fp16, out_acc
- * 16*D u64 (zero).  hidden % 128 == 0, inter % 64 == 0.
+ * 16*D u64 (zero), ticket (2F + D)/128 ints (zero).  hidden % 128 == 0,
+ * inter % 64 == 0.
  */
 typedef struct cfb_ffn_b16_args {
   int hidden, inter, flags;
@@ -341,6 +344,7 @@ typedef struct cfb_ffn_b16_args {
   unsigned long long* gu_acc;
   void* ap;
   unsigned long long* out_acc;
+  int* ticket;
 } cfb_ffn_b16_args;
 int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
 

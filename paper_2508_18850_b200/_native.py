@@ -143,7 +143,7 @@ class FfnB16Args(ctypes.Structure):
     """Mirror of ``cfb_ffn_b16_args``."""
 
     _fields_ = [(n, ctypes.c_int) for n in ("hidden", "inter", "flags")] + [("eps", ctypes.c_float)] + [
-        (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc")]
+        (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc", "ticket")]
 
 
 class MoeArgs(ctypes.Structure):

@@ -42,11 +42,19 @@ constexpr int kTcBBytes = kTcN * kTcKB * 2;   // 2 KB
 constexpr int kTcStages = 8;
 constexpr int kTcThreads = 6 * 32;
 
+// Epilogue modes: the last CTA contributing to a 128-row tile (a per-tile
+// ticket) finishes it, so no separate elementwise launch is needed.
+enum TcMode { kTcAccum = 0, kTcSwiGLU = 1, kTcResidOut = 2 };
+
 struct TcParams {
   const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
   const __half* x;   // packed activation blocks [K/64][2 KB]
   unsigned long long* y;  // [16][M] fixed point (2^-32), accumulated
-  int M, K;
+  int M, K, mode;
+  int* ticket;       // [M/128] zero (re-zeroed by the finishing CTA)
+  __half* act;       // kTcSwiGLU: packed activations for the next projection
+  float* out;        // kTcResidOut: out[n][m] = resid[n][m] + y (out may alias resid)
+  const float* resid;
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -190,6 +198,71 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       const int m = t * kTcM + 32 * q + lane;
 #pragma unroll
       for (int c = 0; c < kTcN; ++c) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
+      if (p.mode == kTcAccum) continue;
+      // ticket: the last contributor to tile t finishes it
+      __threadfence();
+      named_bar_sync(2, 128);
+      int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+      if (warp == 2 && lane == 0) {
+        auto cta_of = [&](long long b) { return (int)(((b + 1) * G - 1) / TB); };
+        const int contrib = cta_of((long long)(t + 1) * KBt - 1) - cta_of((long long)t * KBt) + 1;
+        const int old = atomicAdd(p.ticket + t, 1);
+        *flag = old == contrib - 1;
+        if (old == contrib - 1) p.ticket[t] = 0;
+      }
+      named_bar_sync(2, 128);
+      if (!*flag) continue;
+      __threadfence();
+      const int et = tid - 64;  // 0..127
+      if (p.mode == kTcSwiGLU) {
+        // tile rows: 64 gate rows (f = 64t + j) then the 64 matching up rows;
+        // f-range of tile t = K-block t of the next projection.  All loads of a
+        // thread are issued before any store (no serialised L2 round trips).
+        const int nn = et >> 3, j0 = (et & 7) * 8;  // 16 rows x 8 chunks = 128 threads
+        unsigned long long* yg = p.y + (size_t)nn * p.M + t * kTcM + j0;
+        ulonglong2 gv[4], uv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          gv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yg) + e);
+          uv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yg + 64) + e);
+        }
+        __align__(16) __half h[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float gt = fixed_to_float((e & 1) ? gv[e >> 1].y : gv[e >> 1].x);
+          const float up = fixed_to_float((e & 1) ? uv[e >> 1].y : uv[e >> 1].x);
+          h[e] = __float2half_rn(__fmul_rn(__fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt))), up));
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          reinterpret_cast<ulonglong2*>(yg)[e] = make_ulonglong2(0ull, 0ull);
+          reinterpret_cast<ulonglong2*>(yg + 64)[e] = make_ulonglong2(0ull, 0ull);
+        }
+        const int s2 = j0 / 16, c = (j0 % 16) / 8;
+        *reinterpret_cast<uint4*>(p.act + (size_t)t * (kTcBBytes / 2) + ((s2 * 2 + c) * 2 + nn / 8) * 64 +
+                                  (nn % 8) * 8) = *reinterpret_cast<const uint4*>(h);
+      } else {
+        // 16 rows x 128 columns: thread = (row, 16-column run)
+        const int nn = et >> 3, c0 = (et & 7) * 16;
+        const size_t o = (size_t)nn * p.M + t * kTcM + c0;
+        ulonglong2 yv[8];
+        float4 rv[4];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) yv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(p.y + o) + e);
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          rv[e] = p.resid ? __ldcg(reinterpret_cast<const float4*>(p.resid + o) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) reinterpret_cast<ulonglong2*>(p.y + o)[e] = make_ulonglong2(0ull, 0ull);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float4 r4 = rv[e];
+          reinterpret_cast<float4*>(p.out + o)[e] =
+              make_float4(__fadd_rn(r4.x, fixed_to_float(yv[2 * e].x)), __fadd_rn(r4.y, fixed_to_float(yv[2 * e].y)),
+                          __fadd_rn(r4.z, fixed_to_float(yv[2 * e + 1].x)),
+                          __fadd_rn(r4.w, fixed_to_float(yv[2 * e + 1].y)));
+        }
+      }
     }
   }
   tc_fence_before();
@@ -224,10 +297,12 @@ __global__ void tc_finish_kernel(unsigned long long* yacc, float* out, const flo
   }
 }
 
-int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytes) + (4 * kTcStages + 8) * 8 + 16; }
+int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytes) + (4 * kTcStages + 8) * 8 + 32; }
 
 int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
-            cudaStream_t st, bool pdl) {
+            cudaStream_t st, bool pdl, int mode = kTcAccum, int* ticket = nullptr, __half* act = nullptr,
+            float* out = nullptr, const float* resid = nullptr) {
+  if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
   static bool configured = false;
   if (!configured) {
@@ -245,6 +320,11 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   p.y = y;
   p.M = M;
   p.K = K;
+  p.mode = mode;
+  p.ticket = ticket;
+  p.act = act;
+  p.out = out;
+  p.resid = resid;
   if (grid > TB) grid = TB;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -355,21 +435,19 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
   const int D = a->hidden, F = a->inter;
   if (D % 128 || F % 64 || (2 * F) % 128)
     return set_error(CFB_ERR_DIMENSION, "ffn_b16: hidden %% 128 and inter %% 64 must be 0");
+  if (!a->ticket) return set_error(CFB_ERR_ARGUMENT, "ffn_b16: null ticket workspace");
   const bool pdl = a->flags & CFB_PDL;
   int rc;
   if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, 256, st, pdl, a->resid,
                           static_cast<const __half*>(a->norm_w), static_cast<__half*>(a->xp), D, a->eps)))
     return rc;
+  // gate/up tiles interleave 64 gate + 64 up rows, finished (SwiGLU + pack) by
+  // their last contributor; down tiles finished as resid + sum
   if ((rc = tc_gemm(static_cast<const __half*>(a->w_gu), static_cast<const __half*>(a->xp), a->gu_acc,
-                    2 * F, D, 0, st, true)))
+                    2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap))))
     return rc;
-  if ((rc = launch_simple(tc_swiglu_pack_kernel, (kTcN * F / 8 + 255) / 256, 256, st, true, a->gu_acc,
-                          static_cast<__half*>(a->ap), F)))
-    return rc;
-  if ((rc = tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc,
-                    D, F, 0, st, true)))
-    return rc;
-  return tc_finish(a->out_acc, a->resid, a->resid, kTcN * D, st, true);
+  return tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc, D, F,
+                 0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid, a->resid);
 }
 
 }  // namespace cfb

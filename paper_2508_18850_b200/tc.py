@@ -78,13 +78,16 @@ class TcFfnB16:
         w1, w2, w3 = t(w1), t(w2), t(w3)
         self.F, self.D = w1.shape
         self.eps = eps
-        self.w_gu = pack_umma(torch.cat([w1, w2], 0))
+        # gate/up rows interleaved per 64 (one 128-row tile = 64 gate + their 64 up rows)
+        self.w_gu = pack_umma(torch.stack([w1.reshape(-1, 64, self.D), w2.reshape(-1, 64, self.D)], 1)
+                              .reshape(2 * self.F, self.D))
         self.w_dn = pack_umma(w3)
         self.g = t(norm_w)
         self.xp = torch.zeros(BATCH * self.D, device=dev, dtype=torch.float16)
         self.gu_acc = torch.zeros(BATCH * 2 * self.F, device=dev, dtype=torch.int64)
         self.ap = torch.zeros(BATCH * self.F, device=dev, dtype=torch.float16)
         self.out_acc = torch.zeros(BATCH * self.D, device=dev, dtype=torch.int64)
+        self.ticket = torch.zeros((2 * self.F + self.D) // 128, device=dev, dtype=torch.int32)
         torch.cuda.synchronize()
 
     @property
@@ -96,5 +99,6 @@ class TcFfnB16:
                                eps=self.eps, resid=resid.data_ptr(), norm_w=self.g.data_ptr(),
                                w_gu=self.w_gu.data_ptr(), w_dn=self.w_dn.data_ptr(),
                                xp=self.xp.data_ptr(), gu_acc=self.gu_acc.data_ptr(),
-                               ap=self.ap.data_ptr(), out_acc=self.out_acc.data_ptr())
+                               ap=self.ap.data_ptr(), out_acc=self.out_acc.data_ptr(),
+                               ticket=self.ticket.data_ptr())
         _native.check(_native.lib().cfb_ffn_b16(a, _native.stream_ptr(stream)))
