@@ -254,6 +254,8 @@ def run_ours(args, rank, world):
         torch.cuda.empty_cache()
         line["deepseek_block"] = deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])
         line["gpu_launches"] += sum(d["launches"] for d in line["deepseek_block"])
+        line["batch16_ffn_tcgen05"] = batch16_ffn(cfg, pk["hbm_gbs"])
+        line["gpu_launches"] += line["batch16_ffn_tcgen05"]["launches"]
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
     if world > 1:
@@ -298,6 +300,38 @@ def deepseek_sweep(ctxs, peak_gbs, layers=4, reps=16):
                     "launches": 2 * layers * (reps + 4)})
         del blocks, g
         torch.cuda.empty_cache()
+    return out
+
+
+def batch16_ffn(cfg, peak_gbs, sets=3, reps=30):
+    """Batch-16 Llama2-7B FFN block on tcgen05 (tc.TcFfnB16: RMSNorm -> [w1;w2]
+    projection with SwiGLU epilogue -> w3 projection with residual epilogue)."""
+    import torch
+    from paper_2508_18850_b200.tc import TcFfnB16
+    D, F = cfg.hidden, cfg.inter
+    ffns = [TcFfnB16(torch.randn(F, D, device="cuda") * D ** -0.5,
+                     torch.randn(F, D, device="cuda") * D ** -0.5,
+                     torch.randn(D, F, device="cuda") * F ** -0.5, torch.ones(D, device="cuda"))
+            for _ in range(sets)]
+    resid = torch.randn(16, D, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        for f in ffns:
+            f.launch(resid, pdl=True, stream=st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for r in range(reps):
+            ffns[r % sets].launch(resid, pdl=True, stream=st)
+        e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) * 1e3 / reps
+    gbs = ffns[0].weight_bytes / us / 1e3
+    out = {"batch": 16, "us_per_block": round(us, 2), "hbm_gbs": round(gbs, 1),
+           "frac_of_peak": round(gbs / peak_gbs, 4), "tokens_per_s": round(16e6 / us, 1),
+           "launches": 3 * (reps + sets)}
+    del ffns
+    torch.cuda.empty_cache()
     return out
 
 
