@@ -348,6 +348,48 @@ typedef struct cfb_ffn_b16_args {
 } cfb_ffn_b16_args;
 int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
 
+/*
+ * One Llama decoder layer for 16 INDEPENDENT sequences (own KV caches and
+ * positions), batch>1 path on tcgen05: RMSNorm+pack -> QKV projection whose
+ * finishing epilogue applies RoPE at pos[n] and appends k, v to sequence n's
+ * cache -> split-KV attention over rows 0..pos[n] -> O projection + residual
+ * -> batch-16 FFN block.  resid [16][hidden] fp32 is updated in place.
+ *   w_qkv  packed [q heads ; k heads ; v heads] x 128 rows (3*hidden x hidden)
+ *   w_o    packed W_out^T (hidden x hidden); w_gu / w_dn as cfb_ffn_b16
+ *   k_cache, v_cache [16][n_heads][cache_cap][128] fp16; rope_cs [cap][64][2]
+ *   pos [16] device ints: the new token's position per sequence (not advanced;
+ *   cfb_b16_advance adds 1 to all of them)
+ * Workspaces (zeroed once): xp 16*max(hidden, inter) fp16, q16 16*hidden fp16,
+ * qkv_acc 16*3*hidden u64, part 16*n_heads*ceil(max_len/256)*130 fp32,
+ * o_acc 16*hidden u64, gu_acc 16*2*inter u64, ap 16*inter fp16,
+ * ticket (3*hidden + 2*hidden + 2*inter)/128 ints.  n_heads*128 == hidden.
+ */
+typedef struct cfb_b16_layer_args {
+  int hidden, n_heads, inter, cache_cap, max_len, flags;
+  float eps;
+  float* resid;
+  const void* attn_norm;
+  const void* ffn_norm;
+  const void* w_qkv;
+  const void* w_o;
+  const void* w_gu;
+  const void* w_dn;
+  void* k_cache;
+  void* v_cache;
+  const float* rope_cs;
+  const int* pos;
+  void* xp;
+  void* q16;
+  unsigned long long* qkv_acc;
+  float* part;
+  unsigned long long* o_acc;
+  unsigned long long* gu_acc;
+  void* ap;
+  int* ticket;
+} cfb_b16_layer_args;
+int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);
+int cfb_b16_advance(int* pos, void* stream);
+
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,
               void* stream);

@@ -146,6 +146,16 @@ class FfnB16Args(ctypes.Structure):
         (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc", "ticket")]
 
 
+class B16LayerArgs(ctypes.Structure):
+    """Mirror of ``cfb_b16_layer_args``."""
+
+    _fields_ = [(n, ctypes.c_int) for n in ("hidden", "n_heads", "inter", "cache_cap", "max_len",
+                                             "flags")] + [("eps", ctypes.c_float)] + [
+        (n, _vp) for n in ("resid", "attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gu", "w_dn", "k_cache",
+                           "v_cache", "rope_cs", "pos", "xp", "q16", "qkv_acc", "part", "o_acc",
+                           "gu_acc", "ap", "ticket")]
+
+
 class MoeArgs(ctypes.Structure):
     """Mirror of ``cfb_moe_args``."""
 
@@ -161,6 +171,10 @@ def bind_extra(L) -> None:
     L.cfb_tc_gemm_b16.restype = ctypes.c_int
     L.cfb_ffn_b16.argtypes = [ctypes.POINTER(FfnB16Args), _vp]
     L.cfb_ffn_b16.restype = ctypes.c_int
+    L.cfb_llama_b16_layer.argtypes = [ctypes.POINTER(B16LayerArgs), _vp]
+    L.cfb_llama_b16_layer.restype = ctypes.c_int
+    L.cfb_b16_advance.argtypes = [_vp, _vp]
+    L.cfb_b16_advance.restype = ctypes.c_int
     L.cfb_mla_engine_decode.argtypes = [ctypes.POINTER(MlaEngineArgs), _vp]
     L.cfb_mla_engine_decode.restype = ctypes.c_int
     L.cfb_moe_decode.argtypes = [ctypes.POINTER(MoeArgs), _vp]

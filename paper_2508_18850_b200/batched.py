@@ -1,0 +1,173 @@
+"""Batch-16 decode of 16 independent sequences on tcgen05 (north-star "tensor
+cores for the batch>1 projections"; BASELINE config #5 batch 16).
+
+Each sequence has its own KV cache and position.  One layer is
+``cfb_llama_b16_layer`` (csrc/tc_gemm.cu + csrc/batch_attn.cu): the QKV, O and
+FFN projections run as swap-AB tcgen05 GEMMs (weights = M, the 16 sequences =
+N) whose finishing epilogues apply RoPE + cache append, the residual add and
+SwiGLU; attention is split-KV flash decoding per (sequence, head).  The
+reference's batch semantics (B new tokens of ONE sequence sharing a cache,
+oracle.py:45-50) stay with the cluster kernels (`run_fused_mha_decode`); this
+module is the serving-style batch of the north star.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from .exceptions import DimensionError
+from .llama import LlamaConfig, rope_table
+from .tc import BATCH, pack_umma
+
+
+def pack_layer_b16(lp: dict, dev):
+    """Logical layer (``random_llama_params`` layout) -> packed tcgen05 weights."""
+    import torch
+
+    def t(a):
+        if not isinstance(a, torch.Tensor):
+            a = torch.from_numpy(np.ascontiguousarray(a, np.float32))
+        return a.to(dev).half()
+
+    wqkv = t(lp["w_qkv"])                          # (nh, D, 3H)
+    nh, D, H3 = wqkv.shape
+    H = H3 // 3
+    rows = wqkv.reshape(nh, D, 3, H).permute(2, 0, 3, 1).reshape(3 * nh * H, D)  # [kind][head][i]
+    wo = t(lp["w_out"])                            # (nh, H, D)
+    w1, w2, w3 = t(lp["w1"]), t(lp["w2"]), t(lp["w3"])
+    F = w1.shape[0]
+    gu = torch.stack([w1.reshape(-1, 64, D), w2.reshape(-1, 64, D)], 1).reshape(2 * F, D)
+    return dict(attn_norm=t(lp["attn_norm"]), ffn_norm=t(lp["ffn_norm"]),
+                w_qkv=pack_umma(rows.contiguous()), w_o=pack_umma(wo.reshape(nh * H, D).t().contiguous()),
+                w_gu=pack_umma(gu.contiguous()), w_dn=pack_umma(w3))
+
+
+class BatchedLlama:
+    """16 independent sequences through a Llama layer stack (tcgen05 path)."""
+
+    def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None):
+        import torch
+        if cfg.head_dim != 128 or cfg.n_heads * 128 != cfg.hidden:
+            raise DimensionError("the batch-16 path needs head_dim 128 and n_heads * 128 == hidden")
+        self.cfg, self.cap = cfg, cache_cap
+        self.dev = _native.require_cuda()
+        dev = self.dev
+        self.layers = layers
+        self.max_len = max_len or cache_cap
+        D, nh, F = cfg.hidden, cfg.n_heads, cfg.inter
+        self.rope = torch.from_numpy(rope_table(cache_cap, 128, cfg.rope_theta)).to(dev)
+        self.pos = torch.zeros(BATCH, device=dev, dtype=torch.int32)
+        self.resid = torch.zeros(BATCH, D, device=dev, dtype=torch.float32)
+        nchunks = (self.max_len + 255) // 256
+        self.ws = dict(
+            xp=torch.zeros(BATCH * max(D, F), device=dev, dtype=torch.float16),
+            q16=torch.zeros(BATCH * D, device=dev, dtype=torch.float16),
+            qkv_acc=torch.zeros(BATCH * 3 * D, device=dev, dtype=torch.int64),
+            part=torch.zeros(BATCH * nh * nchunks * 130, device=dev, dtype=torch.float32),
+            o_acc=torch.zeros(BATCH * D, device=dev, dtype=torch.int64),
+            gu_acc=torch.zeros(BATCH * 2 * F, device=dev, dtype=torch.int64),
+            ap=torch.zeros(BATCH * F, device=dev, dtype=torch.float16),
+            ticket=torch.zeros((5 * D + 2 * F) // 128, device=dev, dtype=torch.int32))
+        self.stream = torch.cuda.Stream(device=dev)
+        self.graph = None
+        torch.cuda.synchronize()
+
+    # ---------------------------------------------------------------- builders
+    @classmethod
+    def from_params(cls, cfg: LlamaConfig, layers_params: list, caches: list, cache_cap: int,
+                    max_len: int | None = None) -> "BatchedLlama":
+        """layers_params: logical per-layer weights; caches[l] = list of 16
+        (k (nh, S_n, H), v) numpy prefixes, one per sequence."""
+        import torch
+        dev = _native.require_cuda()
+        layers = []
+        for lp_, cl in zip(layers_params, caches):
+            L = pack_layer_b16(lp_, dev)
+            kc = torch.zeros(BATCH, cfg.n_heads, cache_cap, 128, device=dev, dtype=torch.float16)
+            vc = torch.zeros_like(kc)
+            for n, (k, v) in enumerate(cl):
+                S = k.shape[1]
+                if S:
+                    kc[n, :, :S] = torch.from_numpy(np.ascontiguousarray(k, np.float32)).to(dev).half()
+                    vc[n, :, :S] = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(dev).half()
+            L["k_cache"], L["v_cache"] = kc, vc
+            layers.append(L)
+        return cls(cfg, cache_cap, layers, max_len)
+
+    @classmethod
+    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0) -> "BatchedLlama":
+        """Device-drawn packed weights and full KV caches (benchmarks)."""
+        import torch
+        dev = _native.require_cuda()
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+        D, nh, F = cfg.hidden, cfg.n_heads, cfg.inter
+
+        def rnd(shape, scale, shift=0.0):
+            x = torch.empty(shape, device=dev, dtype=torch.float16)
+            x.normal_(mean=shift, std=scale, generator=g)
+            return x
+
+        layers = []
+        for _ in range(cfg.n_layers):
+            layers.append(dict(
+                attn_norm=rnd((D,), 0.1, 1.0), ffn_norm=rnd((D,), 0.1, 1.0),
+                w_qkv=rnd((3 * D // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
+                w_o=rnd((D // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
+                w_gu=rnd((2 * F // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
+                w_dn=rnd((D // 128, F // 64, 4, 2, 16, 8, 8), F ** -0.5),
+                k_cache=rnd((BATCH, nh, cache_cap, 128), 1.0),
+                v_cache=rnd((BATCH, nh, cache_cap, 128), 1.0)))
+        return cls(cfg, cache_cap, layers)
+
+    # ---------------------------------------------------------------- running
+    def layer_args(self, L: dict):
+        cfg, w = self.cfg, self.ws
+        return _native.B16LayerArgs(
+            hidden=cfg.hidden, n_heads=cfg.n_heads, inter=cfg.inter, cache_cap=self.cap,
+            max_len=self.max_len, flags=_native.PDL, eps=cfg.eps, resid=self.resid.data_ptr(),
+            attn_norm=L["attn_norm"].data_ptr(), ffn_norm=L["ffn_norm"].data_ptr(),
+            w_qkv=L["w_qkv"].data_ptr(), w_o=L["w_o"].data_ptr(), w_gu=L["w_gu"].data_ptr(),
+            w_dn=L["w_dn"].data_ptr(), k_cache=L["k_cache"].data_ptr(),
+            v_cache=L["v_cache"].data_ptr(), rope_cs=self.rope.data_ptr(), pos=self.pos.data_ptr(),
+            xp=w["xp"].data_ptr(), q16=w["q16"].data_ptr(), qkv_acc=w["qkv_acc"].data_ptr(),
+            part=w["part"].data_ptr(), o_acc=w["o_acc"].data_ptr(), gu_acc=w["gu_acc"].data_ptr(),
+            ap=w["ap"].data_ptr(), ticket=w["ticket"].data_ptr())
+
+    def _enqueue(self, advance: bool = True) -> None:
+        L_ = _native.lib()
+        sp = self.stream.cuda_stream
+        for L in self.layers:
+            _native.check(L_.cfb_llama_b16_layer(self.layer_args(L), sp))
+        if advance:
+            _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
+
+    def set_positions(self, pos) -> None:
+        import torch
+        self.pos.copy_(torch.as_tensor(np.asarray(pos, np.int32)))
+        torch.cuda.synchronize()
+
+    def step(self, advance: bool = True) -> None:
+        """resid <- the layer stack applied to resid for all 16 sequences."""
+        self._enqueue(advance)
+
+    def capture(self) -> None:
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._enqueue(True)
+
+    def replay(self) -> None:
+        import torch
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+
+    def step_bytes(self, ctx: int) -> int:
+        """Algorithmic HBM bytes per step: layer weights once + each sequence's
+        KV rows 0..ctx (read) and the new row (written)."""
+        cfg = self.cfg
+        D, F = cfg.hidden, cfg.inter
+        w = cfg.n_layers * (2 * (4 * D * D + 3 * D * F) + 4 * D)
+        kv = cfg.n_layers * BATCH * 2 * D * 2 * (ctx + 2)
+        return w + kv

@@ -44,7 +44,20 @@ constexpr int kTcThreads = 6 * 32;
 
 // Epilogue modes: the last CTA contributing to a 128-row tile (a per-tile
 // ticket) finishes it, so no separate elementwise launch is needed.
-enum TcMode { kTcAccum = 0, kTcSwiGLU = 1, kTcResidOut = 2 };
+enum TcMode { kTcAccum = 0, kTcSwiGLU = 1, kTcResidOut = 2, kTcQKV = 3 };
+
+// kTcQKV: the projection rows are [q heads | k heads | v heads] x 128 (one tile
+// = one head); the finishing CTA rounds to fp16, applies rotate-half RoPE at
+// each sequence's own position (q, k), writes q for the attention kernel and
+// appends k, v to that sequence's cache.
+struct TcQkv {
+  __half* q;              // [16][nh*128]
+  __half* k_cache;        // [16][nh][cap][128]
+  __half* v_cache;
+  const float* rope_cs;   // [cap][64][2]
+  const int* pos;         // [16] position of the new token per sequence
+  int nh, cap;
+};
 
 struct TcParams {
   const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
@@ -55,6 +68,7 @@ struct TcParams {
   __half* act;       // kTcSwiGLU: packed activations for the next projection
   float* out;        // kTcResidOut: out[n][m] = resid[n][m] + y (out may alias resid)
   const float* resid;
+  TcQkv qkv;
 };
 
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -214,7 +228,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       if (!*flag) continue;
       __threadfence();
       const int et = tid - 64;  // 0..127
-      if (p.mode == kTcSwiGLU) {
+      if (p.mode == kTcQKV) {
+        // thread = (sequence nn, 8 rotation pairs (i, i + 64), i in [i0, i0 + 8))
+        const int nn = et >> 3, i0 = (et & 7) * 8;
+        unsigned long long* yr = p.y + (size_t)nn * p.M + t * kTcM;
+        ulonglong2 lo[4], hi[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          lo[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yr + i0) + e);
+          hi[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yr + 64 + i0) + e);
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          reinterpret_cast<ulonglong2*>(yr + i0)[e] = make_ulonglong2(0ull, 0ull);
+          reinterpret_cast<ulonglong2*>(yr + 64 + i0)[e] = make_ulonglong2(0ull, 0ull);
+        }
+        const TcQkv& Q = p.qkv;
+        const int kind = t / Q.nh, hd = t % Q.nh, ps = Q.pos[nn];
+        __align__(16) __half a[8], b[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float x1 = round_to<__half>(fixed_to_float((e & 1) ? lo[e >> 1].y : lo[e >> 1].x));
+          float x2 = round_to<__half>(fixed_to_float((e & 1) ? hi[e >> 1].y : hi[e >> 1].x));
+          if (kind < 2) {  // q, k: rotate-half RoPE at the sequence's position
+            const float c = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2], sn = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2 + 1];
+            const float r1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sn));
+            const float r2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, sn));
+            x1 = r1;
+            x2 = r2;
+          }
+          a[e] = __float2half_rn(x1);
+          b[e] = __float2half_rn(x2);
+        }
+        __half* dst;
+        if (kind == 0) {
+          dst = Q.q + (size_t)nn * Q.nh * 128 + hd * 128;
+        } else {
+          __half* cache = kind == 1 ? Q.k_cache : Q.v_cache;
+          dst = cache + (((size_t)nn * Q.nh + hd) * Q.cap + ps) * 128;
+        }
+        *reinterpret_cast<uint4*>(dst + i0) = *reinterpret_cast<const uint4*>(a);
+        *reinterpret_cast<uint4*>(dst + 64 + i0) = *reinterpret_cast<const uint4*>(b);
+      } else if (p.mode == kTcSwiGLU) {
         // tile rows: 64 gate rows (f = 64t + j) then the 64 matching up rows;
         // f-range of tile t = K-block t of the next projection.  All loads of a
         // thread are issued before any store (no serialised L2 round trips).
@@ -301,7 +356,7 @@ int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytes) + (4 * kTcStage
 
 int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
             cudaStream_t st, bool pdl, int mode = kTcAccum, int* ticket = nullptr, __half* act = nullptr,
-            float* out = nullptr, const float* resid = nullptr) {
+            float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr) {
   if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
   static bool configured = false;
@@ -325,6 +380,9 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   p.act = act;
   p.out = out;
   p.resid = resid;
+  p.qkv = qkv ? *qkv : TcQkv{};
+  if (mode == kTcQKV && (!qkv || M != 3 * qkv->nh * kTcM))
+    return set_error(CFB_ERR_DIMENSION, "tc_gemm QKV mode: M must be 3 * n_heads * 128");
   if (grid > TB) grid = TB;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
@@ -415,6 +473,11 @@ __global__ void tc_swiglu_pack_kernel(unsigned long long* gu, __half* ap, int F)
   }
 }
 
+__global__ void tc_advance_kernel(int* pos) {  // every sequence moves to its next position
+  pdl_wait();
+  if (threadIdx.x < kTcN) pos[threadIdx.x] += 1;
+}
+
 template <class K, class... Args>
 static int launch_simple(K kern, int grid, int block, cudaStream_t st, bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -450,9 +513,70 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
                  0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid, a->resid);
 }
 
+int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
+                    int max_len, float* part, __half* xp, cudaStream_t st, bool pdl);
+
+// One Llama decoder layer for 16 independent sequences (8 PDL-chained launches):
+// RMSNorm+pack -> QKV projection (RoPE + per-sequence cache append in the
+// finishing epilogue) -> split-KV attention + merge (packed) -> O projection
+// (+ residual) -> batch-16 FFN block.
+int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
+  if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
+  const int D = a->hidden, nh = a->n_heads, F = a->inter;
+  if (nh * 128 != D) return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads * 128 must equal hidden");
+  const bool pdl = a->flags & CFB_PDL;
+  int rc;
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, 256, st, pdl, (const float*)a->resid,
+                          static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps)))
+    return rc;
+  TcQkv qkv;
+  qkv.q = static_cast<__half*>(a->q16);
+  qkv.k_cache = static_cast<__half*>(a->k_cache);
+  qkv.v_cache = static_cast<__half*>(a->v_cache);
+  qkv.rope_cs = a->rope_cs;
+  qkv.pos = a->pos;
+  qkv.nh = nh;
+  qkv.cap = a->cache_cap;
+  const int Mq = 3 * nh * 128;
+  if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
+                    0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv)))
+    return rc;
+  if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
+                            static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
+                            a->part, static_cast<__half*>(a->xp), st, true)))
+    return rc;
+  if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, D, 0, st,
+                    true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, a->resid)))
+    return rc;
+  cfb_ffn_b16_args f = {};
+  f.hidden = D;
+  f.inter = F;
+  f.flags = CFB_PDL;
+  f.eps = a->eps;
+  f.resid = a->resid;
+  f.norm_w = a->ffn_norm;
+  f.w_gu = a->w_gu;
+  f.w_dn = a->w_dn;
+  f.xp = a->xp;
+  f.gu_acc = a->gu_acc;
+  f.ap = a->ap;
+  f.out_acc = a->o_acc;
+  f.ticket = a->ticket + (Mq + D) / kTcM;
+  return ffn_b16(&f, st);
+}
+
 }  // namespace cfb
 
 extern "C" {
+
+int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream) {
+  return cfb::llama_b16_layer(args, static_cast<cudaStream_t>(stream));
+}
+
+int cfb_b16_advance(int* pos, void* stream) {
+  return cfb::launch_simple(cfb::tc_advance_kernel, 1, 32, static_cast<cudaStream_t>(stream), true, pos);
+}
+
 
 int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigned long long* y_acc,
                     float* y, const float* resid, int M, int K, int flags, void* stream) {

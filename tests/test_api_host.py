@@ -163,7 +163,8 @@ def _struct_fields(text, name):
                                           ("cfb_splithead_args", "SplitHeadArgs"),
                                           ("cfb_moe_args", "MoeArgs"),
                                           ("cfb_mla_engine_args", "MlaEngineArgs"),
-                                          ("cfb_ffn_b16_args", "FfnB16Args")])
+                                          ("cfb_ffn_b16_args", "FfnB16Args"),
+                                          ("cfb_b16_layer_args", "B16LayerArgs")])
 def test_abi_struct_layout_matches_header(cname, pyname):
     """ctypes mirrors must have the field order of the C structs."""
     text = (ROOT / "include" / "cfb.h").read_text()
