@@ -256,6 +256,8 @@ def run_ours(args, rank, world):
         line["gpu_launches"] += sum(d["launches"] for d in line["deepseek_block"])
         line["batch16_ffn_tcgen05"] = batch16_ffn(cfg, pk["hbm_gbs"])
         line["gpu_launches"] += line["batch16_ffn_tcgen05"]["launches"]
+        line["batch16_llama_tcgen05"] = batch16_stack(cfg, [1024, 4096], pk["hbm_gbs"])
+        line["gpu_launches"] += sum(d["launches"] for d in line["batch16_llama_tcgen05"])
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
     if world > 1:
@@ -332,6 +334,39 @@ def batch16_ffn(cfg, peak_gbs, sets=3, reps=30):
            "launches": 3 * (reps + sets)}
     del ffns
     torch.cuda.empty_cache()
+    return out
+
+
+def batch16_stack(cfg, ctxs, peak_gbs, steps=10):
+    """Batch 16 independent sequences through the 32-layer Llama2-7B stack
+    (batched.BatchedLlama: tcgen05 projections, per-sequence KV caches), CUDA
+    graph per step; LM head excluded."""
+    import torch
+    from paper_2508_18850_b200.batched import BatchedLlama
+    out = []
+    for ctx in ctxs:
+        m = BatchedLlama.random(cfg, cache_cap=ctx + 3 * steps + 8, seed=0)
+        m.set_positions([ctx] * 16)
+        m.step()
+        torch.cuda.synchronize()
+        m.set_positions([ctx] * 16)
+        m.capture()
+        for _ in range(3):
+            m.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(m.stream)
+        for _ in range(steps):
+            m.replay()
+        e1.record(m.stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / steps
+        gbs = m.step_bytes(ctx + 3 + steps // 2) / us / 1e3
+        out.append({"ctx": ctx, "batch": 16, "step_us": round(us, 1), "tokens_per_s": round(16e6 / us, 1),
+                    "hbm_gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak_gbs, 4),
+                    "launches": (8 * cfg.n_layers + 1) * (steps + 4)})
+        del m
+        torch.cuda.empty_cache()
     return out
 
 
