@@ -5,10 +5,12 @@
 // is a pure KV-streaming problem.  Split-KV flash decoding:
 //
 //   batch_attn_kernel  grid (chunk, sequence x head): 4 warps stream a
-//                      256-position chunk of K (one 256 B row per warp load,
-//                      4 positions in flight per warp) into scores, then the
-//                      chunk softmax, then P V with one output dim per thread;
-//                      partial (m, l, acc[128]) per chunk
+//                      256-position chunk of K (a half-warp per 256 B row,
+//                      16 B per lane, 8 rows in flight per warp) into scores,
+//                      then the chunk softmax, then P V with 16 B V loads
+//                      (thread = 8 dims x a row lane, 2 rows in flight),
+//                      summed over the row lanes in smem; partial
+//                      (m, l, acc[128]) per chunk
 //   batch_merge_kernel one CTA per (sequence, head): merges the chunk partials
 //                      and writes the head output as fp16 straight into the
 //                      packed UMMA activation layout of the O-projection
@@ -32,7 +34,7 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   pdl_wait();
   pdl_launch_dependents();
   __shared__ float qs[128];
-  __shared__ float sc[kBaChunk];
+  __shared__ float sc[kBaChunk > 1024 ? kBaChunk : 1024];  // scores, then 8 x 128 PV partials
   __shared__ float red[8];
   const int pair = blockIdx.y, n = pair / nh, h = pair % nh, c = blockIdx.x;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -51,27 +53,41 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   const size_t base = ((size_t)n * nh + h) * cap * 128;
   const __half* K = kc + base;
   const __half* V = vc + base;
-  // scores: lane l covers dims 4l..4l+3 of a row; 4 rows per warp in flight
-  const float q0 = qs[4 * lane], q1 = qs[4 * lane + 1], q2 = qs[4 * lane + 2], q3 = qs[4 * lane + 3];
-  for (int r0 = p0 + 4 * warp; r0 < p1; r0 += 16) {
-    uint2 kv[4];
+  // scores: half-warp per row (lane covers 8 dims = 16 B), 2 rows per warp load,
+  // 4 loads (8 rows) in flight per warp
+  const int hl = lane & 15, ro = lane >> 4;
+  float qv[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) qv[e] = qs[8 * hl + e];
+  for (int r0 = p0 + 8 * warp; r0 < p1; r0 += 32) {
+    uint4 kv[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const int r = min(r0 + j, p1 - 1);
-      kv[j] = __ldg(reinterpret_cast<const uint2*>(K + (size_t)r * 128) + lane);
+      const int r = min(r0 + 2 * j + ro, p1 - 1);
+      kv[j] = __ldg(reinterpret_cast<const uint4*>(K + (size_t)r * 128) + hl);
     }
     float d[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float2 a = __half22float2(*reinterpret_cast<const __half2*>(&kv[j].x));
-      const float2 b = __half22float2(*reinterpret_cast<const __half2*>(&kv[j].y));
-      d[j] = fmaf(q3, b.y, fmaf(q2, b.x, fmaf(q1, a.y, q0 * a.x)));
+      const __half2* hh = reinterpret_cast<const __half2*>(&kv[j]);
+      float t = 0.f;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __half22float2(hh[e]);
+        t = fmaf(qv[2 * e + 1], f.y, fmaf(qv[2 * e], f.x, t));
+      }
+      d[j] = t;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
+    for (int o = 8; o > 0; o >>= 1)
 #pragma unroll
       for (int j = 0; j < 4; ++j) d[j] += __shfl_xor_sync(0xffffffffu, d[j], o);
-    if (lane < 4 && r0 + lane < p1) sc[r0 + lane - p0] = d[lane] * scale;
+    if (hl == 0)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int r = r0 + 2 * j + ro;
+        if (r < p1) sc[r - p0] = d[j] * scale;
+      }
   }
   __syncthreads();
   const int n_rows = p1 - p0;
@@ -92,23 +108,39 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
   __syncthreads();
   if (lane == 0) red[4 + warp] = l;
-  __syncthreads();
-  // P V: thread = output dim, 8 rows in flight
-  float acc = 0.f;
-  int r = 0;
-  for (; r + 8 <= n_rows; r += 8) {
-    __half v[8];
+  // P V: thread = (row lane rl of 8, dim group dg of 16 x 8 dims), 16 B loads,
+  // 2 rows in flight per thread; the 8 row lanes are summed through smem
+  const int dg = tid & 15, rl = tid >> 4;
+  float acc[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) v[j] = V[(size_t)(p0 + r + j) * 128 + tid];
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int r = rl; r < n_rows; r += 16) {
+    const int r2 = min(r + 8, n_rows - 1);
+    const uint4 v0 = __ldg(reinterpret_cast<const uint4*>(V + (size_t)(p0 + r) * 128) + dg);
+    const uint4 v1 = __ldg(reinterpret_cast<const uint4*>(V + (size_t)(p0 + r2) * 128) + dg);
+    const float w0 = sc[r], w1 = r + 8 < n_rows ? sc[r2] : 0.f;
+    const __half2* a0 = reinterpret_cast<const __half2*>(&v0);
+    const __half2* a1 = reinterpret_cast<const __half2*>(&v1);
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = fmaf(sc[r + j], __half2float(v[j]), acc);
+    for (int e = 0; e < 4; ++e) {
+      const float2 f0 = __half22float2(a0[e]), f1 = __half22float2(a1[e]);
+      acc[2 * e] = fmaf(w1, f1.x, fmaf(w0, f0.x, acc[2 * e]));
+      acc[2 * e + 1] = fmaf(w1, f1.y, fmaf(w0, f0.y, acc[2 * e + 1]));
+    }
   }
-  for (; r < n_rows; ++r) acc = fmaf(sc[r], __half2float(V[(size_t)(p0 + r) * 128 + tid]), acc);
+  __syncthreads();  // sc no longer needed: reuse it for the row-lane partials
+#pragma unroll
+  for (int e = 0; e < 8; ++e) sc[rl * 128 + 8 * dg + e] = acc[e];
+  __syncthreads();
+  float accd = 0.f;
+#pragma unroll
+  for (int q2 = 0; q2 < 8; ++q2) accd += sc[q2 * 128 + tid];
+  const float acc_out = accd;
   if (tid == 0) {
     out[0] = m;
     out[1] = red[4] + red[5] + red[6] + red[7];
   }
-  out[2 + tid] = acc;
+  out[2 + tid] = acc_out;
 }
 
 // one CTA (128 threads = head dims) per (sequence, head)

@@ -427,24 +427,40 @@ int tc_finish(unsigned long long* yacc, float* out, const float* resid, int n, c
 __global__ void tc_rmsnorm_pack_kernel(const float* resid, const __half* g, __half* xp, int D, float eps) {
   pdl_wait();
   pdl_launch_dependents();
+  // one CTA per batch row; thread = 16 consecutive elements, loaded once
+  // (4 x 16 B of the residual, 2 x 16 B of the gain) before any arithmetic
   const int n = blockIdx.x, tid = threadIdx.x;
   __shared__ float red[32];
   const float* r = resid + (size_t)n * D;
+  const int k0 = tid * 16;
+  const bool act = k0 < D;
+  float4 rv[4];
+  uint4 gv[2];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) rv[e] = act ? __ldcg(reinterpret_cast<const float4*>(r + k0) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int e = 0; e < 2; ++e) gv[e] = act ? __ldg(reinterpret_cast<const uint4*>(g + k0) + e) : make_uint4(0, 0, 0, 0);
   float ss = 0.f;
-  for (int d = tid; d < D; d += blockDim.x) ss = fmaf(r[d], r[d], ss);
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    ss = fmaf(rv[e].w, rv[e].w, fmaf(rv[e].z, rv[e].z, fmaf(rv[e].y, rv[e].y, fmaf(rv[e].x, rv[e].x, ss))));
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((tid & 31) == 0) red[tid >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
   for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
+  if (!act) return;
   const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
-  for (int k = tid * 8; k < D; k += blockDim.x * 8) {
+  const float* rf = reinterpret_cast<const float*>(rv);
+  const __half* gh = reinterpret_cast<const __half*>(gv);
+#pragma unroll
+  for (int half8 = 0; half8 < 2; ++half8) {
     __align__(16) __half h[8];
 #pragma unroll
     for (int e = 0; e < 8; ++e)
-      h[e] = __float2half_rn(__fmul_rn(__fmul_rn(r[k + e], inv), __half2float(g[k + e])));
-    const int kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
+      h[e] = __float2half_rn(__fmul_rn(__fmul_rn(rf[half8 * 8 + e], inv), __half2float(gh[half8 * 8 + e])));
+    const int k = k0 + half8 * 8, kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
     *reinterpret_cast<uint4*>(xp + (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8) =
         *reinterpret_cast<const uint4*>(h);
   }
@@ -501,7 +517,7 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
   if (!a->ticket) return set_error(CFB_ERR_ARGUMENT, "ffn_b16: null ticket workspace");
   const bool pdl = a->flags & CFB_PDL;
   int rc;
-  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, 256, st, pdl, a->resid,
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, a->resid,
                           static_cast<const __half*>(a->norm_w), static_cast<__half*>(a->xp), D, a->eps)))
     return rc;
   // gate/up tiles interleave 64 gate + 64 up rows, finished (SwiGLU + pack) by
@@ -526,7 +542,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   if (nh * 128 != D) return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads * 128 must equal hidden");
   const bool pdl = a->flags & CFB_PDL;
   int rc;
-  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, 256, st, pdl, (const float*)a->resid,
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, (const float*)a->resid,
                           static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps)))
     return rc;
   TcQkv qkv;
