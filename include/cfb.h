@@ -54,9 +54,12 @@ enum cfb_flags {
   CFB_STATS_MERGED = 1 << 5, /* stats_mode="merged": one SOFTMAX_MERGE pair reduce */
   CFB_PDL = 1 << 6,          /* programmatic dependent launch: the kernel may start while its
                                 stream predecessor finishes (weights stream before the wait) */
-  CFB_ONESHOT = 1 << 7       /* latency-optimal cluster exchange (decode engine): one-round
+  CFB_ONESHOT = 1 << 7,      /* latency-optimal cluster exchange (decode engine): one-round
                                 all-to-all DSMEM gather, and ONE fused softmax-merge reduce of
                                 fp32 (m, l, A) in place of the stats + attn_out reduces */
+  CFB_PARTIAL = 1 << 8       /* batch-16 tensor parallel, ranks > 0: residual-epilogue
+                                projections write their partial sum only (the caller's
+                                all-reduce adds the residual once, from rank 0) */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
@@ -362,10 +365,14 @@ int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
  * Workspaces (zeroed once): xp 16*max(hidden, inter) fp16, q16 16*hidden fp16,
  * qkv_acc 16*3*hidden u64, part 16*n_heads*ceil(max_len/256)*130 fp32,
  * o_acc 16*hidden u64, gu_acc 16*2*inter u64, ap 16*inter fp16,
- * ticket (3*hidden + 2*hidden + 2*inter)/128 ints.  n_heads*128 == hidden.
+ * ticket (3*hidden + 2*hidden + 2*inter)/128 ints.  flags: CFB_PDL, CFB_PARTIAL.
  */
 typedef struct cfb_b16_layer_args {
   int hidden, n_heads, inter, cache_cap, max_len, flags;
+  /* stage: 0 whole layer, 1 attention half only, 2 FFN half only (tensor parallel:
+   * one all-reduce of resid after each half; n_heads / inter are then the rank's
+   * shard: n_heads*128 <= hidden, inter % 64 == 0) */
+  int stage;
   float eps;
   float* resid;
   const void* attn_norm;

@@ -18,6 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcfb.so"
 
 CFB_F16, CFB_F32 = 2, 4
 APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED, PDL, ONESHOT = 1, 2, 4, 8, 16, 32, 64, 128
+PARTIAL = 256
 STAGE_NAMES = ("qkv_gather", "stats_max_reduce", "stats_sum_reduce", "stats_merge_reduce",
                "attn_out_reduce", "q_proj_gather", "latent_kv_gather", "absorbed_q_gather",
                "down_proj_reduce", "score_reduce", "out_proj_reduce")
@@ -150,7 +151,7 @@ class B16LayerArgs(ctypes.Structure):
     """Mirror of ``cfb_b16_layer_args``."""
 
     _fields_ = [(n, ctypes.c_int) for n in ("hidden", "n_heads", "inter", "cache_cap", "max_len",
-                                             "flags")] + [("eps", ctypes.c_float)] + [
+                                             "flags", "stage")] + [("eps", ctypes.c_float)] + [
         (n, _vp) for n in ("resid", "attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gu", "w_dn", "k_cache",
                            "v_cache", "rope_cs", "pos", "xp", "q16", "qkv_acc", "part", "o_acc",
                            "gu_acc", "ap", "ticket")]

@@ -48,8 +48,9 @@ class BatchedLlama:
 
     def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None):
         import torch
-        if cfg.head_dim != 128 or cfg.n_heads * 128 != cfg.hidden:
-            raise DimensionError("the batch-16 path needs head_dim 128 and n_heads * 128 == hidden")
+        if cfg.head_dim != 128 or cfg.n_heads * 128 > cfg.hidden or cfg.inter % 64:
+            raise DimensionError("the batch-16 path needs head_dim 128, n_heads * 128 <= hidden "
+                                 "(== unless tensor-parallel) and inter % 64 == 0")
         self.cfg, self.cap = cfg, cache_cap
         self.dev = _native.require_cuda()
         dev = self.dev
@@ -62,13 +63,13 @@ class BatchedLlama:
         nchunks = (self.max_len + 255) // 256
         self.ws = dict(
             xp=torch.zeros(BATCH * max(D, F), device=dev, dtype=torch.float16),
-            q16=torch.zeros(BATCH * D, device=dev, dtype=torch.float16),
-            qkv_acc=torch.zeros(BATCH * 3 * D, device=dev, dtype=torch.int64),
+            q16=torch.zeros(BATCH * nh * 128, device=dev, dtype=torch.float16),
+            qkv_acc=torch.zeros(BATCH * 3 * nh * 128, device=dev, dtype=torch.int64),
             part=torch.zeros(BATCH * nh * nchunks * 130, device=dev, dtype=torch.float32),
             o_acc=torch.zeros(BATCH * D, device=dev, dtype=torch.int64),
             gu_acc=torch.zeros(BATCH * 2 * F, device=dev, dtype=torch.int64),
             ap=torch.zeros(BATCH * F, device=dev, dtype=torch.float16),
-            ticket=torch.zeros((5 * D + 2 * F) // 128, device=dev, dtype=torch.int32))
+            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128, device=dev, dtype=torch.int32))
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
         torch.cuda.synchronize()
@@ -113,8 +114,8 @@ class BatchedLlama:
         for _ in range(cfg.n_layers):
             layers.append(dict(
                 attn_norm=rnd((D,), 0.1, 1.0), ffn_norm=rnd((D,), 0.1, 1.0),
-                w_qkv=rnd((3 * D // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
-                w_o=rnd((D // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
+                w_qkv=rnd((3 * nh, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
+                w_o=rnd((D // 128, 2 * nh, 4, 2, 16, 8, 8), (nh * 128) ** -0.5),
                 w_gu=rnd((2 * F // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
                 w_dn=rnd((D // 128, F // 64, 4, 2, 16, 8, 8), F ** -0.5),
                 k_cache=rnd((BATCH, nh, cache_cap, 128), 1.0),
@@ -122,11 +123,12 @@ class BatchedLlama:
         return cls(cfg, cache_cap, layers)
 
     # ---------------------------------------------------------------- running
-    def layer_args(self, L: dict):
+    def layer_args(self, L: dict, stage: int = 0, partial: bool = False):
         cfg, w = self.cfg, self.ws
         return _native.B16LayerArgs(
             hidden=cfg.hidden, n_heads=cfg.n_heads, inter=cfg.inter, cache_cap=self.cap,
-            max_len=self.max_len, flags=_native.PDL, eps=cfg.eps, resid=self.resid.data_ptr(),
+            max_len=self.max_len, flags=_native.PDL | (_native.PARTIAL if partial else 0), stage=stage,
+            eps=cfg.eps, resid=self.resid.data_ptr(),
             attn_norm=L["attn_norm"].data_ptr(), ffn_norm=L["ffn_norm"].data_ptr(),
             w_qkv=L["w_qkv"].data_ptr(), w_o=L["w_o"].data_ptr(), w_gu=L["w_gu"].data_ptr(),
             w_dn=L["w_dn"].data_ptr(), k_cache=L["k_cache"].data_ptr(),

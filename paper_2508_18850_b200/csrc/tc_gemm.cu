@@ -526,7 +526,8 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
                     2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap))))
     return rc;
   return tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc, D, F,
-                 0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid, a->resid);
+                 0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid,
+                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid);
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
@@ -538,36 +539,40 @@ int batch_attention(const __half* q, const __half* kc, const __half* vc, const i
 // (+ residual) -> batch-16 FFN block.
 int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
-  const int D = a->hidden, nh = a->n_heads, F = a->inter;
-  if (nh * 128 != D) return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads * 128 must equal hidden");
-  const bool pdl = a->flags & CFB_PDL;
-  int rc;
-  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, (const float*)a->resid,
-                          static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps)))
-    return rc;
-  TcQkv qkv;
-  qkv.q = static_cast<__half*>(a->q16);
-  qkv.k_cache = static_cast<__half*>(a->k_cache);
-  qkv.v_cache = static_cast<__half*>(a->v_cache);
-  qkv.rope_cs = a->rope_cs;
-  qkv.pos = a->pos;
-  qkv.nh = nh;
-  qkv.cap = a->cache_cap;
+  const int D = a->hidden, nh = a->n_heads, F = a->inter, Ka = nh * 128;
+  if (Ka > D || D % 128 || F % 64 || a->stage < 0 || a->stage > 2)
+    return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads*128 <= hidden, hidden %% 128, inter %% 64");
+  const bool pdl = a->flags & CFB_PDL, partial = a->flags & CFB_PARTIAL;
   const int Mq = 3 * nh * 128;
-  if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
-                    0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv)))
-    return rc;
-  if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
-                            static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
-                            a->part, static_cast<__half*>(a->xp), st, true)))
-    return rc;
-  if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, D, 0, st,
-                    true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, a->resid)))
-    return rc;
+  int rc;
+  if (a->stage != 2) {  // attention half
+    if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, (const float*)a->resid,
+                            static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps)))
+      return rc;
+    TcQkv qkv;
+    qkv.q = static_cast<__half*>(a->q16);
+    qkv.k_cache = static_cast<__half*>(a->k_cache);
+    qkv.v_cache = static_cast<__half*>(a->v_cache);
+    qkv.rope_cs = a->rope_cs;
+    qkv.pos = a->pos;
+    qkv.nh = nh;
+    qkv.cap = a->cache_cap;
+    if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
+                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv)))
+      return rc;
+    if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
+                              static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
+                              a->part, static_cast<__half*>(a->xp), st, true)))
+      return rc;
+    if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
+                      st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid)))
+      return rc;
+  }
+  if (a->stage == 1) return CFB_OK;
   cfb_ffn_b16_args f = {};
   f.hidden = D;
   f.inter = F;
-  f.flags = CFB_PDL;
+  f.flags = CFB_PDL | (partial ? CFB_PARTIAL : 0);
   f.eps = a->eps;
   f.resid = a->resid;
   f.norm_w = a->ffn_norm;

@@ -210,3 +210,77 @@ class TPLlamaDecoder:
 
     def logits_local(self) -> np.ndarray:
         return self.eng.logits()
+
+
+# ------------------------------------------------------------------ batch 16
+def shard_layer_b16(lp: dict, rank: int, world: int) -> dict:
+    """Megatron shard of one logical layer for the batch-16 tcgen05 path: the
+    FFN column shard is zero-padded to a multiple of 64 (a zero gate/up row
+    gives silu(0) * 0 = 0, a zero down column adds nothing)."""
+    sh = shard_layer(lp, rank, world)
+    F = sh["w1"].shape[0]
+    Fp = -(-F // 64) * 64
+    if Fp != F:
+        pad = Fp - F
+        D = sh["w1"].shape[1]
+        sh["w1"] = np.concatenate([sh["w1"], np.zeros((pad, D), np.float32)], 0)
+        sh["w2"] = np.concatenate([sh["w2"], np.zeros((pad, D), np.float32)], 0)
+        sh["w3"] = np.concatenate([sh["w3"], np.zeros((sh["w3"].shape[0], pad), np.float32)], 1)
+    return sh
+
+
+class TPBatchedLlama:
+    """Rank-local shard of the batch-16 independent-sequence stack; one
+    all-reduce of the residual stream per block half (rank 0 adds the
+    residual, the others their partial: CFB_PARTIAL)."""
+
+    def __init__(self, cfg: LlamaConfig, rank: int, world: int, cache_cap: int, *, params=None,
+                 caches=None, seed: int = 0, group=None):
+        from .batched import BatchedLlama
+        if cfg.n_heads % world:
+            raise DimensionError(f"tensor-parallel size {world} must divide the heads")
+        self.cfg, self.rank, self.world, self.group = cfg, rank, world, group
+        nh = cfg.n_heads // world
+        Fp = -(-(cfg.inter // world) // 64) * 64
+        self.lcfg = replace(cfg, n_heads=nh, inter=Fp)
+        if params is not None:
+            hs = slice(rank * nh, (rank + 1) * nh)
+            layers = [shard_layer_b16(lp, rank, world) for lp in params["layers"]]
+            cl = [[(k[hs], v[hs]) for k, v in per_layer] for per_layer in caches]
+            self.m = BatchedLlama.from_params(self.lcfg, layers, cl, cache_cap)
+        else:
+            self.m = BatchedLlama.random(self.lcfg, cache_cap, seed=seed)
+
+    def stage(self, layer: int, stage: int) -> None:
+        m = self.m
+        _native.check(_native.lib().cfb_llama_b16_layer(
+            m.layer_args(m.layers[layer], stage=stage, partial=self.rank > 0), m.stream.cuda_stream))
+
+    def allreduce(self) -> None:
+        import torch.distributed as dist
+        if self.world > 1:
+            dist.all_reduce(self.m.resid, group=self.group)
+
+    def _enqueue(self) -> None:
+        for l in range(len(self.m.layers)):
+            self.stage(l, 1)
+            self.allreduce()
+            self.stage(l, 2)
+            self.allreduce()
+        _native.check(_native.lib().cfb_b16_advance(self.m.pos.data_ptr(), self.m.stream.cuda_stream))
+
+    def step(self) -> None:
+        import torch
+        with torch.cuda.stream(self.m.stream):
+            self._enqueue()
+
+    def capture(self) -> None:
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.m.stream):
+            self._enqueue()
+
+    def replay(self) -> None:
+        import torch
+        with torch.cuda.stream(self.m.stream):
+            self.graph.replay()

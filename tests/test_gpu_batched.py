@@ -67,3 +67,38 @@ def test_batched_graph_replay_advances_positions():
     torch.cuda.synchronize()
     assert m.pos.cpu().tolist() == [103 + n for n in range(16)]  # capture does not execute
     assert torch.isfinite(m.resid).all()
+
+
+def test_batched_tensor_parallel_emulated():
+    """TP=2 shards of the batch-16 stack on one device (head / padded FFN-column
+    shards, CFB_PARTIAL on rank 1), the per-half all-reduce done by a device
+    sum: equals the unsharded stack."""
+    import torch
+    from paper_2508_18850_b200.tp import TPBatchedLlama
+    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=576, vocab=64)  # 288/rank -> pad 320
+    params = random_llama_params(cfg, seed=5, prefill=0)
+    rng = np.random.default_rng(2)
+    S = [3 + 11 * n for n in range(16)]
+    cap = max(S) + 4
+    caches = [[(lp.f16(rng.standard_normal((cfg.n_heads, s, 128))),
+                lp.f16(rng.standard_normal((cfg.n_heads, s, 128)))) for s in S]
+              for _ in range(cfg.n_layers)]
+    ref = BatchedLlama.from_params(cfg, params["layers"], caches, cache_cap=cap)
+    ranks = [TPBatchedLlama(cfg, r, 2, cap, params=params, caches=caches) for r in range(2)]
+    x = torch.from_numpy(rng.standard_normal((16, cfg.hidden)).astype(np.float32)).cuda()
+    for m in [ref] + [r.m for r in ranks]:
+        m.resid.copy_(x)
+        m.set_positions(S)
+    ref.step()
+    for l in range(cfg.n_layers):
+        for stage in (1, 2):
+            for r in ranks:
+                r.stage(l, stage)
+            torch.cuda.synchronize()
+            tot = ranks[0].m.resid + ranks[1].m.resid
+            for r in ranks:
+                r.m.resid.copy_(tot)
+    torch.cuda.synchronize()
+    a, b = ref.resid.cpu().numpy(), ranks[0].m.resid.cpu().numpy()
+    err = float(np.max(np.abs(a - b)))
+    assert err <= 2e-2 and err / float(np.max(np.abs(a))) <= 1e-2, err
