@@ -6,9 +6,11 @@
 // M = 128 operand, the 16 batch rows the N = 16 operand, so one
 // tcgen05.mma.cta_group::1.kind::f16 (M128 N16 K16) consumes 4 KB of weights.
 //
-// Work unit = (128-row weight tile, chunk of K): units are dealt to a
-// persistent grid in contiguous runs (split-K keeps 148 SMs evenly busy even
-// when M/128 is not a multiple of 148).  Per CTA:
+// Work split: the (tile-major, K-minor) sequence of 16 KB weight blocks is cut
+// into contiguous equal runs, one per CTA of a persistent grid; a run's part
+// inside one 128-row tile is accumulated in TMEM and flushed once, so split-K
+// partials only appear at tile edges (148 SMs evenly busy whatever M/128).
+// Per CTA:
 //   warp 0 lane 0   producer: cp.async.bulk of 16 KB weight blocks (128 rows x
 //                   64 K, pre-packed on the host in the UMMA K-major
 //                   no-swizzle "core matrix" order, so a plain bulk copy lands
@@ -20,7 +22,10 @@
 //                   signals the epilogue
 //   warps 2..5      epilogue: tcgen05.ld 32x32b.x16 (one TMEM lane quarter
 //                   per warp) -> 64-bit fixed-point red.add into y_acc[n][m]
-//                   (integer adds: split-K partials sum order-independently)
+//                   (integer adds: split-K partials sum order-independently);
+//                   the last CTA to finish a tile (per-tile ticket) may apply a
+//                   finishing epilogue: SwiGLU + pack for the next projection,
+//                   residual add, or RoPE + per-sequence KV-cache append
 //
 // Packed layouts (fp16), "core matrix" = 8 rows x 16 bytes (8 K elements):
 //   W block (tile t, kb): [s = k-step (4)][c = K half (2)][g = row group (16)][8 rows][8]
