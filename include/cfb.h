@@ -57,9 +57,11 @@ enum cfb_flags {
   CFB_ONESHOT = 1 << 7,      /* latency-optimal cluster exchange (decode engine): one-round
                                 all-to-all DSMEM gather, and ONE fused softmax-merge reduce of
                                 fp32 (m, l, A) in place of the stats + attn_out reduces */
-  CFB_PARTIAL = 1 << 8       /* batch-16 tensor parallel, ranks > 0: residual-epilogue
+  CFB_PARTIAL = 1 << 8,      /* batch-16 tensor parallel, ranks > 0: residual-epilogue
                                 projections write their partial sum only (the caller's
                                 all-reduce adds the residual once, from rank 0) */
+  CFB_QKV_IN = 1 << 9        /* attention module: the rank's q|k|v slices come precomputed
+                                from cfb_qkv_proj (qkv_in) instead of its own QKV GEMV */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
@@ -125,7 +127,18 @@ typedef struct cfb_mha_args {
   float* stats;
   unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
   unsigned long long* trace;   /* [grid CTAs][16] %globaltimer phase stamps (profiling), or NULL */
+  const void* qkv_in;          /* CFB_QKV_IN: [B][rows of w_qkv] T from cfb_qkv_proj */
 } cfb_mha_args;
+
+/*
+ * QKV projection of the attention module on ALL SMs (engine split mode): the
+ * cluster kernel occupies n_heads * N SMs only, so its 100 MB QKV stream runs
+ * here on a persistent grid instead: out[b][r] = T(x[b] . w_qkv row r) over the
+ * w_qkv row tiles of the cfb_mha_args layout - rows in [head][rank][q|k|v slice] order;
+ * x = f16(rmsnorm(resid) * norm_w).  flags: CFB_PDL.
+ */
+int cfb_qkv_proj(int dtype, int batch, int hidden, int rows, const float* resid, const void* norm_w,
+                 float eps, const void* w_qkv, void* out, int flags, void* stream);
 
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);
 

@@ -52,6 +52,8 @@ int tuned_sleep();
   } while (0)
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
+int qkv_proj(int dtype, int B, int D, int rows, const float* resid, const void* norm_w, float eps,
+             const void* w, void* out, int flags, cudaStream_t st);
 int mha_finalize(float* out, const float* resid, unsigned long long* accum, int n, cudaStream_t st);
 int mla_decode(const cfb_mla_args* a, cudaStream_t st);
 int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st);

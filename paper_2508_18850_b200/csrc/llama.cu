@@ -29,6 +29,8 @@ struct cfb_llama {
   int* token = nullptr;
   int* pos = nullptr;
   unsigned long long* argkey = nullptr;  // TP: packed (logit, -index) of the local argmax
+  void* qkv = nullptr;                   // split mode: q|k|v slices of the layer [rows]
+  bool split_qkv = false;
   int tp_rank = 0, tp_size = 1, vocab_offset = 0;
   int ext = 0;  // bit mask: accum / resid / argkey are caller-owned
   cudaGraph_t graph = nullptr;
@@ -67,6 +69,12 @@ int enqueue_embed(cfb_llama* m, cudaStream_t st) {
 
 int enqueue_attn(cfb_llama* m, int l, cudaStream_t st) {
   const cfb_llama_config& c = m->cfg;
+  const int qkv_rows = c.n_heads * c.cluster * ((3 * c.head_dim / c.cluster + 3) / 4) * 4;
+  if (m->split_qkv) {  // QKV stream on all SMs, the cluster kernel starts at the gather
+    const int rc = cfb::qkv_proj(c.dtype, 1, c.hidden, qkv_rows, m->resid, m->attn_norm[l], c.eps,
+                                 m->w_qkv[l], m->qkv, CFB_PDL, st);
+    if (rc) return rc;
+  }
   cfb_mha_args a = {};
   a.dtype = c.dtype;
   a.batch = 1;
@@ -76,7 +84,9 @@ int enqueue_attn(cfb_llama* m, int l, cudaStream_t st) {
   a.head_pad = c.head_dim;
   a.cluster = c.cluster;
   a.cache_cap = c.cache_cap;
-  a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_NORM | CFB_ONESHOT | CFB_PDL;
+  a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_ONESHOT | CFB_PDL |
+            (m->split_qkv ? CFB_QKV_IN : CFB_NORM);
+  a.qkv_in = m->qkv;
   a.resid = m->resid;
   a.norm_w = m->attn_norm[l];
   a.eps = c.eps;
@@ -212,6 +222,17 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     cfb_llama_destroy(m);
     return rc;
   }
+  {  // optional engine mode: split QKV projection (CFB_SPLIT_QKV=1); measured slower
+     // than the fused module, kept for the A/B
+    const char* e = getenv("CFB_SPLIT_QKV");
+    m->split_qkv = e ? atoi(e) != 0 : false;
+    const size_t qkv_rows = (size_t)cfg->n_heads * cfg->cluster *
+                            ((3 * cfg->head_dim / cfg->cluster + 3) / 4) * 4;
+    if (m->split_qkv && (rc = alloc_zero(&m->qkv, qkv_rows * cfg->dtype))) {
+      cfb_llama_destroy(m);
+      return rc;
+    }
+  }
   *out = m;
   return CFB_OK;
 }
@@ -222,7 +243,7 @@ int cfb_llama_destroy(cfb_llama* m) {
   if (m->graph) cudaGraphDestroy(m->graph);
   void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
                   m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
-                  m->pos, (m->ext & 4) ? nullptr : m->argkey};
+                  m->pos, (m->ext & 4) ? nullptr : m->argkey, m->qkv};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -290,7 +311,7 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
 }
 
 int cfb_llama_launches_per_step(const cfb_llama* m) {
-  return m ? 2 + 2 * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
+  return m ? 2 + (m->split_qkv ? 3 : 2) * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
 }
 
 int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigned long long* accum,
