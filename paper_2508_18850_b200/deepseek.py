@@ -1,11 +1,15 @@
 """DeepSeek-V2-Lite-shaped decoder block on the GPU (BASELINE.json config #3).
 
-One block = two launches chained with programmatic dependent launch:
+One block = the attention half then the MoE, chained with programmatic
+dependent launch:
 
-  1. fused_mla latent attention (``csrc/attn_mla.cu``, the reference's
-     ``run_fused_mla_decode`` dataflow, ``dataflows.py:316-429``) with the
-     RMSNorm prologue (CFB_NORM): x = f16(rmsnorm(resid) * g_attn); the head
-     sum stays in the 64-bit fixed-point accumulator;
+  1. MLA latent attention with the RMSNorm prologue x = f16(rmsnorm(resid) *
+     g_attn), head sum into the 64-bit fixed-point accumulator.  At batch 1
+     with the DeepSeek shape (16 heads, kv_lora_rank 512) this is the
+     head-batched engine (``csrc/mla_engine.cu``: 3 launches, every weight and
+     latent row read once); otherwise the reference-dataflow kernel
+     (``csrc/attn_mla.cu``, ``run_fused_mla_decode``, ``dataflows.py:316-429``,
+     CFB_NORM);
   2. fused MoE (``csrc/moe.cu``): r = resid + head sum, h = f16(rmsnorm(r) *
      g_ffn), router + softmax top-k, shared + routed SwiGLU experts,
      resid <- r + MoE(h).
@@ -14,8 +18,8 @@ Dims: the reference preset for MLA (hidden 2048, 16 heads x 128,
 kv_lora_rank 512; ``cli.py:47-54``) and the DeepSeek-V2-Lite MoE (64 routed
 experts, top-6, 2 shared, width 1408).  The CPU restatement is
 ``oracle/deepseek_port.block``.  The latent cache is an input (the reference
-never appends to it, ``dataflows.py:393-397``): the new token's latent row
-joins attention on rank N-1 only.
+never appends to it, ``dataflows.py:393-397``): the new token's latent row is
+attended once.
 """
 
 from __future__ import annotations
