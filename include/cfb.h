@@ -60,8 +60,10 @@ enum cfb_flags {
   CFB_PARTIAL = 1 << 8,      /* batch-16 tensor parallel, ranks > 0: residual-epilogue
                                 projections write their partial sum only (the caller's
                                 all-reduce adds the residual once, from rank 0) */
-  CFB_QKV_IN = 1 << 9        /* attention module: the rank's q|k|v slices come precomputed
+  CFB_QKV_IN = 1 << 9,       /* attention module: the rank's q|k|v slices come precomputed
                                 from cfb_qkv_proj (qkv_in) instead of its own QKV GEMV */
+  CFB_DYN_POOL = 1 << 10     /* fused FFN, batch 1: the last ~4 gate/up tiles per CTA are
+                                work-stolen from a pool; barrier must then hold 2 u64 */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */
@@ -248,7 +250,8 @@ int cfb_splithead_decode(const cfb_splithead_args* args, void* stream);
  *   sum, nullable; re-zeroed by this kernel).  out may alias resid.
  *   w_gu  [F][2][D]  T   row 2f = w1[f] (gate), row 2f+1 = w2[f] (up)
  *   w_dn  [D][F]     T   = w3
- *   act   [B][F]     T   workspace;  barrier: one u64, zero before first use
+ *   act   [B][F]     T   workspace;  barrier: one u64 (two with CFB_DYN_POOL), zero
+ *                           before first use, then monotonic (keep the same grid)
  */
 typedef struct cfb_ffn_args {
   int dtype, batch, hidden, inter, flags, grid; /* grid <= 0: one CTA per SM */

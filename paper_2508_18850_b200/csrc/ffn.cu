@@ -40,14 +40,15 @@ struct FfnParams {
   const void* w_dn;       // row-tiled, D/4 tiles of F
   void* act;              // [B][F] T workspace
   float* out;             // [B][D] fp32
-  unsigned long long* barrier;
+  unsigned long long* barrier;  // [0] grid barrier, [1] dynamic tile counter (both monotonic)
   unsigned long long* trace;
+  int pool;                     // gate/up tiles handed out dynamically (0: fully static)
 };
 
 // x (phase 0 input, B x D) and act (phase 1 input, B x F) are never live at
 // the same time and share one fp32 region.
 struct FfnLayout {
-  int bars, x, gu, part, red, total;
+  int bars, x, gu, part, red, tag, total;
 };
 
 __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int spw, bool xh) {
@@ -60,6 +61,7 @@ __host__ __device__ inline FfnLayout ffn_layout(int B, int D, int F, int G, int 
   L.gu = o;    o += ((B * 4 * t1 * 4 + 15) & ~15);
   L.part = o;  o += ((kNumConsumerWarps * B * rows * 4 + 15) & ~15);
   L.red = o;   o += (kNumConsumerWarps * B * 4 + 15) & ~15;
+  L.tag = o;   o += kNumSlots * 4;  // dynamic pool: tile index per ring slot (-1: end)
   L.total = o;
   return L;
 }
@@ -73,8 +75,11 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int T1 = F / 2, T2 = D / 4;
-  const int a0 = (int)((long long)i * T1 / G), a1 = (int)((long long)(i + 1) * T1 / G);
+  // gate/up tiles: a static prefix [0, T1s) split evenly, then a pool of
+  // p.pool tiles grabbed one at a time by the producer lanes (work stealing
+  // absorbs the few-us spread of per-SM HBM throughput before the barrier)
+  const int T1 = F / 2, T2 = D / 4, T1s = T1 - p.pool;
+  const int a0 = (int)((long long)i * T1s / G), a1 = (int)((long long)(i + 1) * T1s / G);
   const int u0 = (int)((long long)i * T2 / G), u1 = (int)((long long)(i + 1) * T2 / G);
   if (tid == 0) {
     ring_init(ring);
@@ -85,10 +90,65 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
                               4 * D * tb, true);
   const Phase P1 = make_phase(static_cast<const T*>(p.w_dn) + (size_t)u0 * 4 * F, nullptr, u1 - u0,
                               4 * F * tb, true);
+  const int tileB = 4 * D * tb, npc = (tileB + kSlotBytes - 1) / kSlotBytes;  // pieces per tile
+  int* tag = reinterpret_cast<int*>(smem + L.tag);
   pdl_launch_dependents();
   if (warp == kNumConsumerWarps) {
-    const Phase ph[2] = {P0, P1};
-    produce_all(ph, ring, lane, policy_evict_first());
+    const uint64_t pol = policy_evict_first();
+    int c = 0;
+    {
+      const Phase ph[1] = {P0};
+      produce_all(ph, ring, lane, pol, c);
+    }
+    if (p.pool > 0) {
+      // launch epoch: completed grid barriers / G; each lane makes exactly one
+      // failing grab, so a launch adds pool + 8 G.  After the PDL wait every
+      // earlier FFN launch has completed (when the grid leaves SMs idle, this
+      // launch's CTAs can otherwise start while the previous FFN still runs)
+      pdl_wait();
+      const unsigned long long per = (unsigned long long)p.pool + 8ull * G;
+      const unsigned long long base = (ld_acquire_u64(p.barrier) / (unsigned long long)G) * per;
+      bool done = lane >= kNumConsumerWarps;
+      int cur = 0, piece = npc, nap = 32;
+      while (true) {
+        bool issued = false;
+        if (!done) {
+          const int sl = lane * ring.spw + (c % ring.spw);
+          if (mbar_test(&ring.empty[sl], ((c / ring.spw) & 1) ^ 1)) {
+            if (piece == npc) {
+              const long long t = (long long)(atomicAdd(p.barrier + 1, 1ull) - base);
+              if (t >= p.pool) {  // pool exhausted: sentinel slot
+                tag[sl] = -1;
+                mbar_arrive(&ring.full[sl]);
+                done = true;
+              } else {
+                cur = T1s + (int)t;
+                piece = 0;
+              }
+            }
+            if (!done) {
+              const int b0 = piece * kSlotBytes, nb = min(kSlotBytes, tileB - b0);
+              tag[sl] = cur;
+              mbar_arrive_expect_tx(&ring.full[sl], (uint32_t)nb);
+              bulk_g2s(ring.slot(sl), static_cast<const char*>(p.w_gu) + (size_t)cur * tileB + b0, nb,
+                       &ring.full[sl], pol);
+              ++piece;
+            }
+            ++c;
+            issued = true;
+          }
+        }
+        if (__all_sync(0xffffffffu, done)) break;
+        if (__any_sync(0xffffffffu, issued)) {
+          nap = 32;
+        } else {
+          __nanosleep(nap);
+          nap = min(2 * nap, ring.sleep_max);
+        }
+      }
+    }
+    const Phase ph[1] = {P1};
+    produce_all(ph, ring, lane, pol, c);
     return;
   }
   pdl_wait();
@@ -131,6 +191,43 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
     const float g = gu[b * rows0 + 4 * t + e], u = gu[b * rows0 + 4 * t + 2 + e];
     const float sl = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
     act_g[(size_t)b * F + 2 * a0 + j] = Elem<T>::from_f(__fmul_rn(sl, u));
+  }
+  if (p.pool > 0) {
+    // dynamic pool: whole tiles (npc pieces in this warp's consecutive slots);
+    // lanes 0..3 accumulate rows (gate 2t, gate 2t+1, up 2t, up 2t+1)
+    while (true) {
+      const int sl = warp * ring.spw + (cnt % ring.spw);
+      mbar_wait(&ring.full[sl], (cnt / ring.spw) & 1);
+      const int t = tag[sl];
+      if (t < 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.empty[sl]);
+        ++cnt;
+        break;
+      }
+      float rowsum = 0.f;
+      for (int pc = 0; pc < npc; ++pc) {
+        const int s2 = warp * ring.spw + (cnt % ring.spw);
+        if (pc > 0) mbar_wait(&ring.full[s2], (cnt / ring.spw) & 1);
+        Item it;
+        it.unit0 = 0;
+        it.nunits = 1;
+        it.piece = pc;
+        it.byte0 = pc * kSlotBytes;
+        it.bytes = min(kSlotBytes, tileB - it.byte0);
+        tile_item<T, QB, XH>(P0, it, ring.slot(s2), xs, D, B, lane,
+                             [&](int row, const float (&sm)[QB]) { rowsum += sm[0]; });
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ring.empty[s2]);
+        ++cnt;
+      }
+      // lane e (0, 1): gate from lane e, up from lane 2 + e
+      const float up = __shfl_sync(0xffffffffu, rowsum, (lane & 1) + 2);
+      if (lane < 2) {
+        const float sl2 = __fdiv_rn(rowsum, __fadd_rn(1.0f, expf(-rowsum)));
+        act_g[2 * t + lane] = Elem<T>::from_f(__fmul_rn(sl2, up));
+      }
+    }
   }
   if (tr && tid == 0) tr[2] = globaltimer();
   grid_barrier(p.barrier, tid);
@@ -224,6 +321,8 @@ int ffn_decode(const cfb_ffn_args* a, cudaStream_t st) {
   p.out = a->out;
   p.barrier = a->barrier;
   p.trace = a->trace;
+  // dynamic gate/up pool (batch 1, engine launches): ~4 tiles per CTA
+  p.pool = (a->batch == 1 && (a->flags & CFB_DYN_POOL)) ? min(4 * grid, a->inter / 2 / 4) : 0;
   const size_t smem = L.total;
   if (tb == 2) {
     if (p.B == 1) return launch_ffn_inst<__half, 1, true>(p, grid, smem, st);

@@ -109,7 +109,11 @@ int enqueue_ffn(cfb_llama* m, int l, cudaStream_t st) {
   f.hidden = c.hidden;
   f.inter = c.inter;
   // TP: only rank 0 adds the residual, so the all-reduce of resid counts it once
-  f.flags = CFB_NORM | CFB_PDL | (m->tp_rank == 0 ? CFB_RESID : 0);
+  static const bool pool = [] {  // work-stolen gate/up tail (CFB_FFN_POOL=0 disables)
+    const char* e = getenv("CFB_FFN_POOL");
+    return e ? atoi(e) != 0 : true;
+  }();
+  f.flags = CFB_NORM | CFB_PDL | (m->tp_rank == 0 ? CFB_RESID : 0) | (pool ? CFB_DYN_POOL : 0);
   f.eps = c.eps;
   f.resid = m->resid;
   f.accum = m->accum;
@@ -213,7 +217,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
   if (sms <= 0) sms = 148;
   if ((rc = alloc_zero((void**)&m->resid, D * 4)) || (rc = alloc_zero((void**)&m->accum, D * 8)) ||
       (rc = alloc_zero(&m->act, (size_t)cfg->inter * cfg->dtype)) ||
-      (rc = alloc_zero((void**)&m->barrier, 8)) ||
+      (rc = alloc_zero((void**)&m->barrier, 16)) ||
       (rc = alloc_zero((void**)&m->logits, (size_t)cfg->vocab * 4)) ||
       (rc = alloc_zero((void**)&m->cand_val, (size_t)sms * 4)) ||
       (rc = alloc_zero((void**)&m->cand_idx, (size_t)sms * 4)) ||

@@ -77,7 +77,12 @@ for l in range(a.layers):
                  "mha_wait_first": round((m[:, 0].min() - t0) / 1e3, 2), "mha_wait_last": round((m[:, 0].max() - t0) / 1e3, 2),
                  "mha_end_first": round((m[:, 7].min() - t0) / 1e3, 2), "mha_end_last": round((m[:, 7].max() - t0) / 1e3, 2),
                  "ffn_wait_first": round((f[:, 0].min() - t0) / 1e3, 2), "ffn_wait_last": round((f[:, 0].max() - t0) / 1e3, 2),
+                 "ffn_norm_done_med": round((np.median(f[:, 1]) - t0) / 1e3, 2),
+                 "ffn_gu_done_min": round((f[:, 2].min() - t0) / 1e3, 2),
+                 "ffn_gu_done_med": round((np.median(f[:, 2]) - t0) / 1e3, 2),
+                 "ffn_gu_done_max": round((f[:, 2].max() - t0) / 1e3, 2),
                  "ffn_barrier_median": round((np.median(f[:, 3]) - t0) / 1e3, 2),
+                 "ffn_actload_med": round((np.median(f[:, 4]) - t0) / 1e3, 2),
                  "ffn_end_first": round((f[:, 5].min() - t0) / 1e3, 2), "ffn_end_last": round((f[:, 5].max() - t0) / 1e3, 2)})
 for r in rows:
     print(json.dumps(r))
