@@ -412,6 +412,13 @@ typedef struct cfb_b16_layer_args {
 } cfb_b16_layer_args;
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);
 int cfb_b16_advance(int* pos, void* stream);
+/* Batch-16 final RMSNorm + LM head (tcgen05, w_lm packed V x hidden) + greedy
+ * argmax per sequence (first index of the max): tokens [16]; logits [16][V]
+ * fp32 or NULL; xp 16*hidden fp16 and y_acc 16*V u64 (zero) workspaces.
+ * vocab % 128 == 0.  Then cfb_embed(batch 16) gathers the next inputs. */
+int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
+                    float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
+                    void* stream);
 
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,

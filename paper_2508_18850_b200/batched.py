@@ -165,11 +165,81 @@ class BatchedLlama:
         with torch.cuda.stream(self.stream):
             self.graph.replay()
 
-    def step_bytes(self, ctx: int) -> int:
+    # ---------------------------------------------------------------- greedy decode
+    def set_head(self, embed, final_norm, lm_head) -> None:
+        """Embedding table (V, D), final norm (D,), LM head (V, D): logical
+        numpy / torch arrays; the LM head is packed for tcgen05."""
+        import torch
+        dev = self.dev
+
+        def t(a):
+            if not isinstance(a, torch.Tensor):
+                a = torch.from_numpy(np.ascontiguousarray(a, np.float32))
+            return a.to(dev).half()
+
+        self.embed, self.final_norm = t(embed), t(final_norm)
+        lm = t(lm_head)
+        self.V = lm.shape[0]
+        self.lm = pack_umma(lm)
+        self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
+        self.logits = torch.zeros(BATCH, self.V, device=dev, dtype=torch.float32)
+        self.lm_acc = torch.zeros(BATCH * self.V, device=dev, dtype=torch.int64)
+        torch.cuda.synchronize()
+
+    def random_head(self, vocab: int, seed: int = 1) -> None:
+        """Device-drawn embedding / final norm / packed LM head (benchmarks)."""
+        import torch
+        dev, D = self.dev, self.cfg.hidden
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed)
+
+        def rnd(shape, scale, shift=0.0):
+            x = torch.empty(shape, device=dev, dtype=torch.float16)
+            x.normal_(mean=shift, std=scale, generator=g)
+            return x
+
+        self.embed, self.final_norm = rnd((vocab, D), 1.0), rnd((D,), 0.1, 1.0)
+        self.V = vocab
+        self.lm = rnd((vocab // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5)
+        self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
+        self.logits = torch.zeros(BATCH, vocab, device=dev, dtype=torch.float32)
+        self.lm_acc = torch.zeros(BATCH * vocab, device=dev, dtype=torch.int64)
+        torch.cuda.synchronize()
+
+    def _enqueue_decode(self, logits: bool) -> None:
+        L_ = _native.lib()
+        sp = self.stream.cuda_stream
+        cfg = self.cfg
+        _native.check(L_.cfb_embed(2, self.embed.data_ptr(), self.tokens.data_ptr(), self.resid.data_ptr(),
+                                   BATCH, cfg.hidden, sp))
+        for L in self.layers:
+            _native.check(L_.cfb_llama_b16_layer(self.layer_args(L), sp))
+        _native.check(L_.cfb_b16_lm_head(
+            self.resid.data_ptr(), self.final_norm.data_ptr(), self.lm.data_ptr(), self.V, cfg.hidden,
+            cfg.eps, self.ws["xp"].data_ptr(), self.lm_acc.data_ptr(), self.tokens.data_ptr(),
+            self.logits.data_ptr() if logits else None, sp))
+        _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
+
+    def decode_step(self, logits: bool = False) -> None:
+        """One greedy step for all 16 sequences: tokens -> embed -> layers ->
+        LM head -> argmax -> tokens; positions advance."""
+        import torch
+        with torch.cuda.stream(self.stream):
+            self._enqueue_decode(logits)
+
+    def capture_decode(self) -> None:
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph, stream=self.stream):
+            self._enqueue_decode(False)
+
+    def step_bytes(self, ctx: int, head: bool = False) -> int:
         """Algorithmic HBM bytes per step: layer weights once + each sequence's
-        KV rows 0..ctx (read) and the new row (written)."""
+        KV rows 0..ctx (read) and the new row (written); with ``head`` also the
+        LM head, final norm and the 16 embedding rows."""
         cfg = self.cfg
         D, F = cfg.hidden, cfg.inter
         w = cfg.n_layers * (2 * (4 * D * D + 3 * D * F) + 4 * D)
         kv = cfg.n_layers * BATCH * 2 * D * 2 * (ctx + 2)
-        return w + kv
+        h = 2 * self.V * D + 2 * D + BATCH * 2 * D if head else 0
+        return w + kv + h

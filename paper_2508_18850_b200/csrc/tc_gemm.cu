@@ -34,6 +34,8 @@
 // groups, LBO = 2048 B (W) / 256 B (X) between the two K core matrices.
 #include <cuda_runtime.h>
 
+#include <climits>
+
 #include "common.h"
 #include "ptx.cuh"
 
@@ -591,9 +593,73 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   return ffn_b16(&f, st);
 }
 
+// greedy argmax per sequence over the fixed-point logits [16][V] (fixed point
+// is monotonic in the value: int64 compare; first index of the max, numpy
+// semantics); re-zeroes the logits accumulator, optionally exports fp32 logits
+__global__ void __launch_bounds__(1024) tc_argmax_kernel(unsigned long long* yacc, int V, int* tokens,
+                                                         float* logits) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int n = blockIdx.x, tid = threadIdx.x;
+  __shared__ long long bv[32];
+  __shared__ int bi[32];
+  unsigned long long* row = yacc + (size_t)n * V;
+  long long best = LLONG_MIN;
+  int besti = 0x7fffffff;
+  for (int v = tid; v < V; v += blockDim.x) {
+    const long long x = (long long)__ldcg(row + v);
+    row[v] = 0ull;
+    if (logits) logits[(size_t)n * V + v] = fixed_to_float((unsigned long long)x);
+    if (x > best) {  // strictly greater: each thread scans ascending v
+      best = x;
+      besti = v;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const long long ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
+    if (ov > best || (ov == best && oi < besti)) {
+      best = ov;
+      besti = oi;
+    }
+  }
+  if ((tid & 31) == 0) {
+    bv[tid >> 5] = best;
+    bi[tid >> 5] = besti;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+      if (bv[w] > best || (bv[w] == best && bi[w] < besti)) {
+        best = bv[w];
+        besti = bi[w];
+      }
+    tokens[n] = besti;
+  }
+}
+
+int b16_lm_head(const float* resid, const __half* g, const __half* w, int V, int D, float eps, __half* xp,
+                unsigned long long* yacc, int* tokens, float* logits, cudaStream_t st) {
+  if (V % kTcM || D % 128) return set_error(CFB_ERR_DIMENSION, "b16 LM head: vocab %% 128, hidden %% 128");
+  int rc;
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, true, resid, g, xp, D, eps)))
+    return rc;
+  if ((rc = tc_gemm(w, xp, yacc, V, D, 0, st, true))) return rc;
+  return launch_simple(tc_argmax_kernel, kTcN, 1024, st, true, yacc, V, tokens, logits);
+}
+
 }  // namespace cfb
 
 extern "C" {
+
+int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
+                    float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
+                    void* stream) {
+  return cfb::b16_lm_head(resid, static_cast<const __half*>(norm_w), static_cast<const __half*>(w_lm), vocab,
+                          hidden, eps, static_cast<__half*>(xp), y_acc, tokens, logits,
+                          static_cast<cudaStream_t>(stream));
+}
 
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream) {
   return cfb::llama_b16_layer(args, static_cast<cudaStream_t>(stream));

@@ -102,3 +102,51 @@ def test_batched_tensor_parallel_emulated():
     a, b = ref.resid.cpu().numpy(), ranks[0].m.resid.cpu().numpy()
     err = float(np.max(np.abs(a - b)))
     assert err <= 2e-2 and err / float(np.max(np.abs(a))) <= 1e-2, err
+
+
+def test_batched_greedy_decode_teacher_forced():
+    """Full batch-16 greedy steps (embed -> layers -> tcgen05 LM head -> argmax)
+    for 16 independent sequences vs the CPU oracle's decode_step per sequence:
+    tokens equal whenever the oracle's top-2 margin is not a near-tie."""
+    import torch
+    cfg = LlamaConfig(n_layers=2, hidden=256, n_heads=2, head_dim=128, inter=384, vocab=512)
+    params = random_llama_params(cfg, seed=9, prefill=0)
+    rng = np.random.default_rng(4)
+    S = [4 + 9 * n for n in range(16)]
+    cap = max(S) + 6
+    caches = [[(lp.f16(rng.standard_normal((cfg.n_heads, s, 128))),
+                lp.f16(rng.standard_normal((cfg.n_heads, s, 128)))) for s in S]
+              for _ in range(cfg.n_layers)]
+    m = BatchedLlama.from_params(cfg, params["layers"], caches, cache_cap=cap)
+    m.set_head(params["embed"], params["final_norm"], params["lm_head"])
+    toks = [int(t) for t in rng.integers(0, cfg.vocab, 16)]
+    m.tokens.copy_(torch.tensor(toks, dtype=torch.int32))
+    m.set_positions(S)
+    # oracle state per sequence
+    ocache = []
+    for n in range(16):
+        per = []
+        for l in range(cfg.n_layers):
+            kc = np.zeros((cfg.n_heads, cap, 128), np.float32)
+            vc = np.zeros_like(kc)
+            kc[:, :S[n]], vc[:, :S[n]] = caches[l][n]
+            per.append((kc, vc))
+        ocache.append(per)
+    oparams = dict(params, rope_cs=rope_table(cap, 128, cfg.rope_theta))
+    checked = 0
+    for step in range(3):
+        m.decode_step(logits=True)
+        torch.cuda.synchronize()
+        got = m.tokens.cpu().tolist()
+        glog = m.logits.cpu().numpy()
+        for n in range(16):
+            ologits, otok = lp.decode_step(oparams, ocache[n], toks[n], S[n] + step, cfg)
+            err = float(np.max(np.abs(glog[n] - ologits)))
+            assert err <= 2e-2 * max(1.0, float(np.max(np.abs(ologits)))), (step, n, err)
+            top2 = np.sort(ologits)[-2:]
+            if top2[1] - top2[0] > 1e-3:
+                assert got[n] == otok, (step, n, got[n], otok)
+                checked += 1
+            toks[n] = otok  # teacher forcing
+        m.tokens.copy_(torch.tensor(toks, dtype=torch.int32))
+    assert checked >= 30
