@@ -379,7 +379,7 @@ def batch16_stack(cfg, ctxs, peak_gbs, steps=10):
             out.append({"ctx": ctx, "batch": 16, "step": "greedy_full" if full else "layers_only",
                         "step_us": round(us, 1), "tokens_per_s": round(16e6 / us, 1),
                         "hbm_gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak_gbs, 4),
-                        "launches": (8 * cfg.n_layers + 1 + (4 if full else 0)) * (steps + 4)})
+                        "launches": (7 * cfg.n_layers + 1 + (4 if full else 0)) * (steps + 4)})
             m.graph = None
         del m
         torch.cuda.empty_cache()

@@ -379,9 +379,10 @@ int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
  *   pos [16] device ints: the new token's position per sequence (not advanced;
  *   cfb_b16_advance adds 1 to all of them)
  * Workspaces (zeroed once): xp 16*max(hidden, inter) fp16, q16 16*hidden fp16,
- * qkv_acc 16*3*hidden u64, part 16*n_heads*ceil(max_len/256)*130 fp32,
+ * qkv_acc 16*3*hidden u64, part 16*n_heads*ceil(max_len/128)*130 fp32,
  * o_acc 16*hidden u64, gu_acc 16*2*inter u64, ap 16*inter fp16,
- * ticket (3*hidden + 2*hidden + 2*inter)/128 ints.  flags: CFB_PDL, CFB_PARTIAL.
+ * ticket (3*n_heads*128 + 2*hidden + 2*inter)/128 + 16*n_heads ints (zero).
+ * flags: CFB_PDL, CFB_PARTIAL.
  */
 typedef struct cfb_b16_layer_args {
   int hidden, n_heads, inter, cache_cap, max_len, flags;
@@ -414,11 +415,13 @@ int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);
 int cfb_b16_advance(int* pos, void* stream);
 /* Batch-16 final RMSNorm + LM head (tcgen05, w_lm packed V x hidden) + greedy
  * argmax per sequence (first index of the max): tokens [16]; logits [16][V]
- * fp32 or NULL; xp 16*hidden fp16 and y_acc 16*V u64 (zero) workspaces.
- * vocab % 128 == 0.  Then cfb_embed(batch 16) gathers the next inputs. */
+ * fp32 or NULL; xp 16*hidden fp16, y_acc 16*V u64 (zero) and scratch
+ * CFB_B16_ARGMAX_SCRATCH u64 (zero) workspaces.  vocab % 128 == 0.  Then
+ * cfb_embed(batch 16) gathers the next inputs. */
+#define CFB_B16_ARGMAX_SCRATCH (33 * 32)
 int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
                     float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
-                    void* stream);
+                    unsigned long long* scratch, void* stream);
 
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,

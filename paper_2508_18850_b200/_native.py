@@ -176,7 +176,7 @@ def bind_extra(L) -> None:
     L.cfb_llama_b16_layer.restype = ctypes.c_int
     L.cfb_b16_advance.argtypes = [_vp, _vp]
     L.cfb_b16_advance.restype = ctypes.c_int
-    L.cfb_b16_lm_head.argtypes = [_vp] * 3 + [ctypes.c_int] * 2 + [ctypes.c_float] + [_vp] * 5
+    L.cfb_b16_lm_head.argtypes = [_vp] * 3 + [ctypes.c_int] * 2 + [ctypes.c_float] + [_vp] * 6
     L.cfb_b16_lm_head.restype = ctypes.c_int
     L.cfb_embed.argtypes = [ctypes.c_int] + [_vp] * 3 + [ctypes.c_int] * 2 + [_vp]
     L.cfb_embed.restype = ctypes.c_int

@@ -60,7 +60,7 @@ class BatchedLlama:
         self.rope = torch.from_numpy(rope_table(cache_cap, 128, cfg.rope_theta)).to(dev)
         self.pos = torch.zeros(BATCH, device=dev, dtype=torch.int32)
         self.resid = torch.zeros(BATCH, D, device=dev, dtype=torch.float32)
-        nchunks = (self.max_len + 255) // 256
+        nchunks = (self.max_len + 127) // 128
         self.ws = dict(
             xp=torch.zeros(BATCH * max(D, F), device=dev, dtype=torch.float16),
             q16=torch.zeros(BATCH * nh * 128, device=dev, dtype=torch.float16),
@@ -69,7 +69,7 @@ class BatchedLlama:
             o_acc=torch.zeros(BATCH * D, device=dev, dtype=torch.int64),
             gu_acc=torch.zeros(BATCH * 2 * F, device=dev, dtype=torch.int64),
             ap=torch.zeros(BATCH * F, device=dev, dtype=torch.float16),
-            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128, device=dev, dtype=torch.int32))
+            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + BATCH * nh, device=dev, dtype=torch.int32))
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
         torch.cuda.synchronize()
@@ -184,6 +184,7 @@ class BatchedLlama:
         self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
         self.logits = torch.zeros(BATCH, self.V, device=dev, dtype=torch.float32)
         self.lm_acc = torch.zeros(BATCH * self.V, device=dev, dtype=torch.int64)
+        self.arg_scratch = torch.zeros(33 * 32, device=dev, dtype=torch.int64)
         torch.cuda.synchronize()
 
     def random_head(self, vocab: int, seed: int = 1) -> None:
@@ -204,6 +205,7 @@ class BatchedLlama:
         self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
         self.logits = torch.zeros(BATCH, vocab, device=dev, dtype=torch.float32)
         self.lm_acc = torch.zeros(BATCH * vocab, device=dev, dtype=torch.int64)
+        self.arg_scratch = torch.zeros(33 * 32, device=dev, dtype=torch.int64)
         torch.cuda.synchronize()
 
     def _enqueue_decode(self, logits: bool) -> None:
@@ -217,7 +219,7 @@ class BatchedLlama:
         _native.check(L_.cfb_b16_lm_head(
             self.resid.data_ptr(), self.final_norm.data_ptr(), self.lm.data_ptr(), self.V, cfg.hidden,
             cfg.eps, self.ws["xp"].data_ptr(), self.lm_acc.data_ptr(), self.tokens.data_ptr(),
-            self.logits.data_ptr() if logits else None, sp))
+            self.logits.data_ptr() if logits else None, self.arg_scratch.data_ptr(), sp))
         _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
 
     def decode_step(self, logits: bool = False) -> None:

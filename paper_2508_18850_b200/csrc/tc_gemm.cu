@@ -154,20 +154,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   if (warp == 0) {  // ------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      pdl_wait();  // activations come from the previous kernel
-      int it = 0;
-      for (int u = 0; u < nseg; ++u) {
-        int t, kb0, nkb;
-        unit_kb(u, t, kb0, nkb);
-        for (int kb = kb0; kb < kb0 + nkb; ++kb, ++it) {
-          const int s = it % kTcStages;
-          if (it >= kTcStages) mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
-          mbar_arrive_expect_tx(&full[s], kTcABytes + kTcBBytes);
-          bulk_g2s(sa + s * kTcABytes, p.w + ((size_t)t * KBt + kb) * (kTcABytes / 2), kTcABytes,
-                   &full[s], pol);
-          bulk_g2s(sb + s * kTcBBytes, p.x + (size_t)kb * (kTcBBytes / 2), kTcBBytes, &full[s],
-                   policy_evict_last());
-        }
+      // blocks b0 .. b1 in order (tile-major, K-minor).  Weights do not depend
+      // on the previous kernel: the first ring's worth streams before
+      // griddepcontrol.wait, overlapping the previous kernel's tail; only the
+      // activation blocks wait for it
+      const int nb = b1 - b0, pre = min(nb, kTcStages);
+      for (int it = 0; it < pre; ++it) {
+        mbar_arrive_expect_tx(&full[it], kTcABytes + kTcBBytes);
+        bulk_g2s(sa + it * kTcABytes, p.w + (size_t)(b0 + it) * (kTcABytes / 2), kTcABytes, &full[it], pol);
+      }
+      pdl_wait();
+      for (int it = 0; it < pre; ++it)
+        bulk_g2s(sb + it * kTcBBytes, p.x + (size_t)((b0 + it) % KBt) * (kTcBBytes / 2), kTcBBytes, &full[it],
+                 policy_evict_last());
+      for (int it = pre; it < nb; ++it) {
+        const int s = it % kTcStages, b = b0 + it;
+        mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], kTcABytes + kTcBBytes);
+        bulk_g2s(sa + s * kTcABytes, p.w + (size_t)b * (kTcABytes / 2), kTcABytes, &full[s], pol);
+        bulk_g2s(sb + s * kTcBBytes, p.x + (size_t)(b % KBt) * (kTcBBytes / 2), kTcBBytes, &full[s],
+                 policy_evict_last());
       }
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
@@ -502,9 +508,9 @@ __global__ void tc_advance_kernel(int* pos) {  // every sequence moves to its ne
 }
 
 template <class K, class... Args>
-static int launch_simple(K kern, int grid, int block, cudaStream_t st, bool pdl, Args... args) {
+static int launch_simple(K kern, dim3 grid, int block, cudaStream_t st, bool pdl, Args... args) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid, 1, 1);
+  cfg.gridDim = grid;
   cfg.blockDim = dim3(block, 1, 1);
   cfg.stream = st;
   LaunchAttrs at(0, pdl);
@@ -538,9 +544,9 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
-                    int max_len, float* part, __half* xp, cudaStream_t st, bool pdl);
+                    int max_len, float* part, int* ticket, __half* xp, cudaStream_t st, bool pdl);
 
-// One Llama decoder layer for 16 independent sequences (8 PDL-chained launches):
+// One Llama decoder layer for 16 independent sequences (7 PDL-chained launches):
 // RMSNorm+pack -> QKV projection (RoPE + per-sequence cache append in the
 // finishing epilogue) -> split-KV attention + merge (packed) -> O projection
 // (+ residual) -> batch-16 FFN block.
@@ -569,7 +575,8 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
       return rc;
     if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
                               static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
-                              a->part, static_cast<__half*>(a->xp), st, true)))
+                              a->part, a->ticket + (Mq + 2 * D + 2 * F) / kTcM, static_cast<__half*>(a->xp), st,
+                              true)))
       return rc;
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
                       st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid)))
@@ -595,58 +602,84 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
 
 // greedy argmax per sequence over the fixed-point logits [16][V] (fixed point
 // is monotonic in the value: int64 compare; first index of the max, numpy
-// semantics); re-zeroes the logits accumulator, optionally exports fp32 logits
-__global__ void __launch_bounds__(1024) tc_argmax_kernel(unsigned long long* yacc, int V, int* tokens,
-                                                         float* logits) {
-  pdl_wait();
-  pdl_launch_dependents();
-  const int n = blockIdx.x, tid = threadIdx.x;
-  __shared__ long long bv[32];
-  __shared__ int bi[32];
-  unsigned long long* row = yacc + (size_t)n * V;
-  long long best = LLONG_MIN;
-  int besti = 0x7fffffff;
-  for (int v = tid; v < V; v += blockDim.x) {
-    const long long x = (long long)__ldcg(row + v);
-    row[v] = 0ull;
-    if (logits) logits[(size_t)n * V + v] = fixed_to_float((unsigned long long)x);
-    if (x > best) {  // strictly greater: each thread scans ascending v
-      best = x;
-      besti = v;
-    }
+// semantics).  Grid (kArgSplit, 16): each CTA scans a V slice (re-zeroing the
+// accumulator, optionally exporting fp32 logits) and publishes its (max, index);
+// the last CTA of a sequence (ticket) reduces the partials.
+constexpr int kArgSplit = 32;
+__device__ __forceinline__ void arg_better(long long& bv, int& bi, long long ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) {
+    bv = ov;
+    bi = oi;
   }
+}
+__device__ __forceinline__ void arg_block_reduce(long long& best, int& besti, long long* bv, int* bi) {
+  const int tid = threadIdx.x;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const long long ov = __shfl_xor_sync(0xffffffffu, best, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, besti, o);
-    if (ov > best || (ov == best && oi < besti)) {
-      best = ov;
-      besti = oi;
-    }
-  }
+  for (int o = 16; o > 0; o >>= 1)
+    arg_better(best, besti, __shfl_xor_sync(0xffffffffu, best, o), __shfl_xor_sync(0xffffffffu, besti, o));
   if ((tid & 31) == 0) {
     bv[tid >> 5] = best;
     bi[tid >> 5] = besti;
   }
   __syncthreads();
-  if (tid == 0) {
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
-      if (bv[w] > best || (bv[w] == best && bi[w] < besti)) {
-        best = bv[w];
-        besti = bi[w];
-      }
-    tokens[n] = besti;
+  if (tid == 0)
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) arg_better(best, besti, bv[w], bi[w]);
+}
+__global__ void __launch_bounds__(256) tc_argmax_kernel(unsigned long long* yacc, int V, int* tokens,
+                                                        float* logits, unsigned long long* scratch) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const int c = blockIdx.x, n = blockIdx.y, tid = threadIdx.x;
+  __shared__ long long bv[8];
+  __shared__ int bi[8];
+  __shared__ int last;
+  const int per = (V / 2 + kArgSplit - 1) / kArgSplit * 2, v0 = c * per, v1 = min(V, v0 + per);
+  unsigned long long* row = yacc + (size_t)n * V;
+  long long best = LLONG_MIN;
+  int besti = 0x7fffffff;
+  for (int v = v0 + 2 * tid; v < v1; v += 512) {  // V even: 16 B per thread
+    const ulonglong2 x = __ldcg(reinterpret_cast<const ulonglong2*>(row + v));
+    *reinterpret_cast<ulonglong2*>(row + v) = make_ulonglong2(0ull, 0ull);
+    if (logits)
+      *reinterpret_cast<float2*>(logits + (size_t)n * V + v) = make_float2(fixed_to_float(x.x), fixed_to_float(x.y));
+    arg_better(best, besti, (long long)x.x, v);
+    arg_better(best, besti, (long long)x.y, v + 1);
   }
+  arg_block_reduce(best, besti, bv, bi);
+  // scratch: [16][kArgSplit] values, [16][kArgSplit] indices, [16] tickets
+  unsigned long long* sv = scratch + (size_t)n * kArgSplit;
+  unsigned long long* si = scratch + 16 * kArgSplit + (size_t)n * kArgSplit;
+  unsigned long long* tk = scratch + 32 * kArgSplit + n;
+  if (tid == 0) {
+    sv[c] = (unsigned long long)best;
+    si[c] = (unsigned long long)besti;
+    __threadfence();
+    const unsigned long long old = atomicAdd(tk, 1ull);
+    last = old == kArgSplit - 1;
+    if (last) *tk = 0ull;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  best = LLONG_MIN;
+  besti = 0x7fffffff;
+  if (tid < kArgSplit) {
+    best = (long long)__ldcg(sv + tid);
+    besti = (int)__ldcg(si + tid);
+  }
+  arg_block_reduce(best, besti, bv, bi);
+  if (tid == 0) tokens[n] = besti;
 }
 
 int b16_lm_head(const float* resid, const __half* g, const __half* w, int V, int D, float eps, __half* xp,
-                unsigned long long* yacc, int* tokens, float* logits, cudaStream_t st) {
+                unsigned long long* yacc, int* tokens, float* logits, unsigned long long* scratch,
+                cudaStream_t st) {
   if (V % kTcM || D % 128) return set_error(CFB_ERR_DIMENSION, "b16 LM head: vocab %% 128, hidden %% 128");
   int rc;
   if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, true, resid, g, xp, D, eps)))
     return rc;
   if ((rc = tc_gemm(w, xp, yacc, V, D, 0, st, true))) return rc;
-  return launch_simple(tc_argmax_kernel, kTcN, 1024, st, true, yacc, V, tokens, logits);
+  return launch_simple(tc_argmax_kernel, dim3(kArgSplit, kTcN), 256, st, true, yacc, V, tokens, logits, scratch);
 }
 
 }  // namespace cfb
@@ -655,9 +688,9 @@ extern "C" {
 
 int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
                     float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
-                    void* stream) {
+                    unsigned long long* scratch, void* stream) {
   return cfb::b16_lm_head(resid, static_cast<const __half*>(norm_w), static_cast<const __half*>(w_lm), vocab,
-                          hidden, eps, static_cast<__half*>(xp), y_acc, tokens, logits,
+                          hidden, eps, static_cast<__half*>(xp), y_acc, tokens, logits, scratch,
                           static_cast<cudaStream_t>(stream));
 }
 

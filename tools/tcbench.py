@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2508_18850_b200.tc import TcProjection  # noqa: E402
 
 res = []
-for M, K in ((22016, 4096), (4096, 11008), (12288, 4096)):
+for M, K in ((22016, 4096), (4096, 11008), (12288, 4096), (4096, 4096)):
     ps = [TcProjection(torch.randn(M, K, device="cuda") * K ** -0.5) for _ in range(3)]
     x = torch.randn(16, K, device="cuda").half()
     st = torch.cuda.Stream()
