@@ -347,42 +347,55 @@ def batch16_ffn(cfg, peak_gbs, sets=3, reps=30):
     return out
 
 
+def _time_b16(m, ctx, full, steps):
+    import torch
+    m.set_positions([ctx] * 16)
+    m.reserve(4 * steps + 8)
+    (m.decode_step if full else m.step)()
+    torch.cuda.synchronize()
+    m.set_positions([ctx] * 16)
+    (m.capture_decode if full else m.capture)()
+    for _ in range(3):
+        m.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(m.stream)
+    for _ in range(steps):
+        m.replay()
+    e1.record(m.stream)
+    torch.cuda.synchronize()
+    m.graph = None
+    return e0.elapsed_time(e1) * 1e3 / steps
+
+
 def batch16_stack(cfg, ctxs, peak_gbs, steps=10):
     """Batch 16 independent sequences through the 32-layer Llama2-7B stack
     (batched.BatchedLlama: tcgen05 projections, per-sequence KV caches), CUDA
-    graph per step.  Two lines per context: the layer stack alone, and the
-    full greedy step (embed -> 32 layers -> final norm + tcgen05 LM head ->
-    argmax -> next tokens)."""
+    graph per step.  Lines per context: the layer stack alone, the full greedy
+    step (embed -> 32 layers -> final norm + tcgen05 LM head -> argmax -> next
+    tokens), and the full step over the paged KV cache (shuffled 128-position
+    pages, block table)."""
     import torch
     from paper_2508_18850_b200.batched import BatchedLlama
     out = []
     for ctx in ctxs:
-        m = BatchedLlama.random(cfg, cache_cap=ctx + 6 * steps + 16, seed=0)
-        m.random_head(cfg.vocab)
-        for full in (False, True):
-            m.set_positions([ctx] * 16)
-            (m.decode_step if full else m.step)()
-            torch.cuda.synchronize()
-            m.set_positions([ctx] * 16)
-            (m.capture_decode if full else m.capture)()
-            for _ in range(3):
-                m.replay()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(m.stream)
-            for _ in range(steps):
-                m.replay()
-            e1.record(m.stream)
-            torch.cuda.synchronize()
-            us = e0.elapsed_time(e1) * 1e3 / steps
+        cap = ctx + 6 * steps + 16
+        for kind in ("layers_only", "greedy_full", "greedy_full_paged"):
+            if kind == "greedy_full_paged":
+                m = BatchedLlama.random_paged(cfg, max_len=cap, seed=0)
+            elif kind == "layers_only":
+                m = BatchedLlama.random(cfg, cache_cap=cap, seed=0)
+            m.random_head(cfg.vocab)
+            full = kind != "layers_only"
+            us = _time_b16(m, ctx, full, steps)
             gbs = m.step_bytes(ctx + 3 + steps // 2, head=full) / us / 1e3
-            out.append({"ctx": ctx, "batch": 16, "step": "greedy_full" if full else "layers_only",
+            out.append({"ctx": ctx, "batch": 16, "step": kind,
                         "step_us": round(us, 1), "tokens_per_s": round(16e6 / us, 1),
                         "hbm_gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak_gbs, 4),
                         "launches": (7 * cfg.n_layers + 1 + (4 if full else 0)) * (steps + 4)})
-            m.graph = None
-        del m
-        torch.cuda.empty_cache()
+            if kind != "layers_only":
+                del m
+                torch.cuda.empty_cache()
     return out
 
 

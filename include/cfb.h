@@ -410,9 +410,23 @@ typedef struct cfb_b16_layer_args {
   unsigned long long* gu_acc;
   void* ap;
   int* ticket;
+  /* paged KV cache (NULL = the contiguous layout above): block_table [16][max_pages]
+   * page ids; k_cache / v_cache are then page pools [n_pages][n_heads][128][128]
+   * fp16 (page = CFB_KV_PAGE positions of all heads); position p of sequence n
+   * lives in page block_table[n][p / CFB_KV_PAGE] at row p % CFB_KV_PAGE */
+  const int* block_table;
+  int max_pages;
 } cfb_b16_layer_args;
+#define CFB_KV_PAGE 128
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);
 int cfb_b16_advance(int* pos, void* stream);
+/* KV writer (prefill / import): rows [start, start + count) of sequence seq
+ * from k_src / v_src [n_heads][count][128] fp16 (device) into the paged pools
+ * (block_table as above; the pages must already be assigned) or, with
+ * block_table NULL, into the contiguous [16][n_heads][cache_cap][128] caches. */
+int cfb_b16_kv_write(void* k_cache, void* v_cache, const int* block_table, int max_pages, int cache_cap,
+                     int n_heads, int seq, int start, int count, const void* k_src, const void* v_src,
+                     void* stream);
 /* Batch-16 final RMSNorm + LM head (tcgen05, w_lm packed V x hidden) + greedy
  * argmax per sequence (first index of the max): tokens [16]; logits [16][V]
  * fp32 or NULL; xp 16*hidden fp16, y_acc 16*V u64 (zero) and scratch

@@ -154,7 +154,7 @@ class B16LayerArgs(ctypes.Structure):
                                              "flags", "stage")] + [("eps", ctypes.c_float)] + [
         (n, _vp) for n in ("resid", "attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gu", "w_dn", "k_cache",
                            "v_cache", "rope_cs", "pos", "xp", "q16", "qkv_acc", "part", "o_acc",
-                           "gu_acc", "ap", "ticket")]
+                           "gu_acc", "ap", "ticket", "block_table")] + [("max_pages", ctypes.c_int)]
 
 
 class MoeArgs(ctypes.Structure):
@@ -178,6 +178,8 @@ def bind_extra(L) -> None:
     L.cfb_b16_advance.restype = ctypes.c_int
     L.cfb_b16_lm_head.argtypes = [_vp] * 3 + [ctypes.c_int] * 2 + [ctypes.c_float] + [_vp] * 6
     L.cfb_b16_lm_head.restype = ctypes.c_int
+    L.cfb_b16_kv_write.argtypes = [_vp] * 3 + [ctypes.c_int] * 6 + [_vp] * 3
+    L.cfb_b16_kv_write.restype = ctypes.c_int
     L.cfb_embed.argtypes = [ctypes.c_int] + [_vp] * 3 + [ctypes.c_int] * 2 + [_vp]
     L.cfb_embed.restype = ctypes.c_int
     L.cfb_mla_engine_decode.argtypes = [ctypes.POINTER(MlaEngineArgs), _vp]

@@ -43,10 +43,97 @@ def pack_layer_b16(lp: dict, dev):
                 w_gu=pack_umma(gu.contiguous()), w_dn=pack_umma(w3))
 
 
+PAGE = 128  # CFB_KV_PAGE: positions per KV page (= one attention chunk)
+
+
+class PagedKVPool:
+    """Paged KV caches for the 16 sequences: per layer a K and a V page pool
+    [n_pages][n_heads][128][128] fp16 and one shared block table [16][max_pages]
+    (page ids, the same for every layer).  Pages are handed out from a free
+    list as sequences grow (``reserve``) and returned by ``release``; the
+    device table is refreshed on every change (host-side, between steps)."""
+
+    def __init__(self, cfg: LlamaConfig, n_pages: int, max_pages: int, dev):
+        import torch
+        self.cfg, self.n_pages, self.max_pages, self.dev = cfg, n_pages, max_pages, dev
+        shape = (n_pages, cfg.n_heads, PAGE, 128)
+        self.k = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
+        self.v = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
+        self.free = list(range(n_pages))[::-1]
+        self.pages = [[] for _ in range(BATCH)]
+        self.host_table = np.zeros((BATCH, max_pages), np.int32)
+        self.table = torch.zeros((BATCH, max_pages), device=dev, dtype=torch.int32)
+
+    def reserve(self, seq: int, length: int) -> None:
+        """Make positions 0 .. length-1 of ``seq`` addressable."""
+        need = (length + PAGE - 1) // PAGE
+        if need > self.max_pages:
+            raise DimensionError(f"sequence {seq}: {length} positions exceed max_pages={self.max_pages}")
+        changed = False
+        while len(self.pages[seq]) < need:
+            if not self.free:
+                raise DimensionError("KV page pool exhausted")
+            pg = self.free.pop()
+            self.host_table[seq, len(self.pages[seq])] = pg
+            self.pages[seq].append(pg)
+            changed = True
+        if changed:
+            self._push()
+
+    def _push(self) -> None:
+        import torch
+        torch.cuda.synchronize()  # no step in flight reads the table
+        self.table.copy_(torch_from(self.host_table))
+        torch.cuda.synchronize()
+
+    def release(self, seq: int) -> None:
+        self.free.extend(reversed(self.pages[seq]))
+        self.pages[seq] = []
+        self.host_table[seq] = 0
+        self._push()
+
+    def write(self, layer: int, seq: int, start: int, k, v, stream=None) -> None:
+        """Prefill writer: rows start .. start+count of ``seq`` from k, v
+        (n_heads, count, 128) into the pages (``cfb_b16_kv_write``)."""
+        import torch
+        k = _half_dev(k, self.dev)
+        v = _half_dev(v, self.dev)
+        count = k.shape[1]
+        self.reserve(seq, start + count)
+        if count == 0:
+            return
+        _native.check(_native.lib().cfb_b16_kv_write(
+            self.k[layer].data_ptr(), self.v[layer].data_ptr(), self.table.data_ptr(), self.max_pages, 0,
+            self.cfg.n_heads, seq, start, count, k.data_ptr(), v.data_ptr(),
+            (stream or torch.cuda.current_stream()).cuda_stream))
+
+    def gather(self, layer: int, seq: int, length: int):
+        """Debug view: (k, v) (n_heads, length, 128) of ``seq`` (torch, device)."""
+        import torch
+        pg = torch.as_tensor(self.pages[seq][:(length + PAGE - 1) // PAGE], device=self.dev, dtype=torch.long)
+
+        def g(pool):
+            return pool[pg].permute(1, 0, 2, 3).reshape(self.cfg.n_heads, -1, 128)[:, :length]
+        return g(self.k[layer]), g(self.v[layer])
+
+
+def torch_from(a):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(a))
+
+
+def _half_dev(a, dev):
+    import torch
+    if not isinstance(a, torch.Tensor):
+        a = torch.from_numpy(np.ascontiguousarray(a, np.float32))
+    return a.to(dev).half().contiguous()
+
+
 class BatchedLlama:
     """16 independent sequences through a Llama layer stack (tcgen05 path)."""
 
-    def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None):
+    def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None,
+                 pool: PagedKVPool | None = None):
         import torch
         if cfg.head_dim != 128 or cfg.n_heads * 128 > cfg.hidden or cfg.inter % 64:
             raise DimensionError("the batch-16 path needs head_dim 128, n_heads * 128 <= hidden "
@@ -72,9 +159,50 @@ class BatchedLlama:
             ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + BATCH * nh, device=dev, dtype=torch.int32))
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
+        self.pool = pool
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- builders
+    @classmethod
+    def paged(cls, cfg: LlamaConfig, layers_params: list, caches: list, max_len: int,
+              n_pages: int | None = None, shuffle_seed: int | None = None) -> "BatchedLlama":
+        """Like ``from_params`` but the KV caches live in a ``PagedKVPool``
+        (prefill written through ``cfb_b16_kv_write``); positions up to
+        ``max_len`` are addressable.  ``n_pages`` defaults to what 16 sequences
+        of ``max_len`` need."""
+        dev = _native.require_cuda()
+        maxp = (max_len + PAGE - 1) // PAGE
+        pool = PagedKVPool(cfg, n_pages or BATCH * maxp, maxp, dev)
+        if shuffle_seed is not None:  # non-monotonic page ids (tests)
+            pool.free = [int(x) for x in np.random.default_rng(shuffle_seed).permutation(pool.n_pages)]
+        layers = [pack_layer_b16(lp_, dev) for lp_ in layers_params]
+        for li, (L, cl) in enumerate(zip(layers, caches)):
+            L["k_cache"], L["v_cache"] = pool.k[li], pool.v[li]
+            for n, (k, v) in enumerate(cl):
+                pool.write(li, n, 0, k, v)
+        return cls(cfg, max_len, layers, max_len, pool=pool)
+
+    @classmethod
+    def random_paged(cls, cfg: LlamaConfig, max_len: int, seed: int = 0, shuffle: bool = True) -> "BatchedLlama":
+        """Device-drawn weights over a paged pool whose pages are fully drawn;
+        every sequence gets max_len positions of pages (shuffled page ids)."""
+        import torch
+        m = cls.random(cfg, cache_cap=1, seed=seed)
+        dev = m.dev
+        maxp = (max_len + PAGE - 1) // PAGE
+        pool = PagedKVPool(cfg, BATCH * maxp, maxp, dev)
+        if shuffle:
+            rng = np.random.default_rng(seed)
+            pool.free = [int(x) for x in rng.permutation(pool.n_pages)]
+        g = torch.Generator(device=dev)
+        g.manual_seed(seed + 7)
+        for li, L in enumerate(m.layers):
+            pool.k[li].normal_(generator=g)
+            pool.v[li].normal_(generator=g)
+            L["k_cache"], L["v_cache"] = pool.k[li], pool.v[li]
+        for n in range(BATCH):
+            pool.reserve(n, max_len)
+        return cls(cfg, max_len, m.layers, max_len, pool=pool)
     @classmethod
     def from_params(cls, cfg: LlamaConfig, layers_params: list, caches: list, cache_cap: int,
                     max_len: int | None = None) -> "BatchedLlama":
@@ -135,7 +263,9 @@ class BatchedLlama:
             v_cache=L["v_cache"].data_ptr(), rope_cs=self.rope.data_ptr(), pos=self.pos.data_ptr(),
             xp=w["xp"].data_ptr(), q16=w["q16"].data_ptr(), qkv_acc=w["qkv_acc"].data_ptr(),
             part=w["part"].data_ptr(), o_acc=w["o_acc"].data_ptr(), gu_acc=w["gu_acc"].data_ptr(),
-            ap=w["ap"].data_ptr(), ticket=w["ticket"].data_ptr())
+            ap=w["ap"].data_ptr(), ticket=w["ticket"].data_ptr(),
+            block_table=self.pool.table.data_ptr() if self.pool else None,
+            max_pages=self.pool.max_pages if self.pool else 0)
 
     def _enqueue(self, advance: bool = True) -> None:
         L_ = _native.lib()
@@ -147,8 +277,19 @@ class BatchedLlama:
 
     def set_positions(self, pos) -> None:
         import torch
+        if self.pool:  # the new token's page must exist
+            for n, p in enumerate(pos):
+                self.pool.reserve(n, int(p) + 1)
         self.pos.copy_(torch.as_tensor(np.asarray(pos, np.int32)))
         torch.cuda.synchronize()
+
+    def reserve(self, steps: int) -> None:
+        """Paged mode: make the next ``steps`` positions of every sequence
+        addressable (call before replaying a captured graph that far)."""
+        if self.pool:
+            pos = self.pos.cpu().numpy()
+            for n in range(BATCH):
+                self.pool.reserve(n, int(pos[n]) + steps)
 
     def step(self, advance: bool = True) -> None:
         """resid <- the layer stack applied to resid for all 16 sequences."""

@@ -21,6 +21,7 @@
 namespace cfb {
 
 constexpr int kBaChunk = 128;
+static_assert(kBaChunk == CFB_KV_PAGE, "a KV page is one attention chunk");
 constexpr int kBaThreads = 128;
 constexpr int kBaSmem = 2 * kBaChunk * 256 + 2 * 128 * 4 + 64;  // K, V chunks, q, scores, bars
 
@@ -34,7 +35,7 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
                                                                 const __half* vc, const int* pos,
                                                                 int nh, int cap, int nchunks,
                                                                 float scale, float* part, int* ticket,
-                                                                __half* xp) {
+                                                                __half* xp, const int* table, int maxp) {
   extern __shared__ __align__(128) char smem[];
   __half* ks = reinterpret_cast<__half*>(smem);
   __half* vs = ks + kBaChunk * 128;
@@ -50,7 +51,9 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   const int L = pos[n] + 1, p0 = c * kBaChunk, p1 = min(L, p0 + kBaChunk);
   if (p0 >= p1) return;  // beyond this sequence: not part of its merge
   const int n_rows = p1 - p0, nused = (L + kBaChunk - 1) / kBaChunk;
-  const size_t base = (((size_t)n * nh + h) * cap + p0) * 128;
+  // paged: chunk c of a sequence is exactly its page c (CFB_KV_PAGE == kBaChunk)
+  const size_t base = table ? ((size_t)table[n * maxp + c] * nh + h) * (size_t)kBaChunk * 128
+                            : (((size_t)n * nh + h) * cap + p0) * 128;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
@@ -166,7 +169,8 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
-                    int max_len, float* part, int* ticket, __half* xp, cudaStream_t st, bool pdl) {
+                    int max_len, float* part, int* ticket, __half* xp, const int* table, int maxp,
+                    cudaStream_t st, bool pdl) {
   static bool attr = false;
   if (!attr) {
     CFB_CUDA(cudaFuncSetAttribute(batch_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBaSmem));
@@ -183,8 +187,39 @@ int batch_attention(const __half* q, const __half* kc, const __half* vc, const i
   cfg.numAttrs = at.n;
   const float scale = (float)(1.0 / std::sqrt(128.0));
   CFB_CUDA(cudaLaunchKernelEx(&cfg, batch_attn_kernel, q, kc, vc, pos, nh, cap, nchunks, scale, part, ticket,
-                              xp));
+                              xp, table, maxp));
+  return CFB_OK;
+}
+
+// KV writer: grid (count, n_heads), 16 threads x 16 B per 256 B row
+__global__ void kv_write_kernel(__half* kc, __half* vc, const int* table, int maxp, int cap, int nh, int seq,
+                                int start, int count, const __half* ks, const __half* vs) {
+  const int r = blockIdx.x, h = blockIdx.y, t = threadIdx.x, p = start + r;
+  const size_t dst = table ? (((size_t)table[seq * maxp + p / kBaChunk] * nh + h) * kBaChunk + p % kBaChunk) * 128
+                           : (((size_t)seq * nh + h) * cap + p) * 128;
+  const size_t src = ((size_t)h * count + r) * 128;
+  reinterpret_cast<uint4*>(kc + dst)[t] = reinterpret_cast<const uint4*>(ks + src)[t];
+  reinterpret_cast<uint4*>(vc + dst)[t] = reinterpret_cast<const uint4*>(vs + src)[t];
+}
+
+int kv_write(__half* kc, __half* vc, const int* table, int maxp, int cap, int nh, int seq, int start, int count,
+             const __half* ks, const __half* vs, cudaStream_t st) {
+  if (!kc || !vc || (count > 0 && (!ks || !vs)) || seq < 0 || seq >= 16 || start < 0 || count < 0 || nh <= 0)
+    return set_error(CFB_ERR_ARGUMENT, "kv_write: bad arguments");
+  if (!table && start + count > cap) return set_error(CFB_ERR_DIMENSION, "kv_write: rows beyond cache_cap");
+  if (table && start + count > maxp * kBaChunk) return set_error(CFB_ERR_DIMENSION, "kv_write: rows beyond the block table");
+  if (!count) return CFB_OK;
+  kv_write_kernel<<<dim3(count, nh), 16, 0, st>>>(kc, vc, table, maxp, cap, nh, seq, start, count, ks, vs);
+  CFB_CUDA(cudaGetLastError());
   return CFB_OK;
 }
 
 }  // namespace cfb
+
+extern "C" int cfb_b16_kv_write(void* k_cache, void* v_cache, const int* block_table, int max_pages, int cache_cap,
+                                int n_heads, int seq, int start, int count, const void* k_src, const void* v_src,
+                                void* stream) {
+  return cfb::kv_write(static_cast<__half*>(k_cache), static_cast<__half*>(v_cache), block_table, max_pages,
+                       cache_cap, n_heads, seq, start, count, static_cast<const __half*>(k_src),
+                       static_cast<const __half*>(v_src), static_cast<cudaStream_t>(stream));
+}

@@ -64,6 +64,8 @@ struct TcQkv {
   const float* rope_cs;   // [cap][64][2]
   const int* pos;         // [16] position of the new token per sequence
   int nh, cap;
+  const int* table;       // paged caches: [16][maxp] page ids (else null)
+  int maxp;
 };
 
 struct TcParams {
@@ -278,7 +280,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
           dst = Q.q + (size_t)nn * Q.nh * 128 + hd * 128;
         } else {
           __half* cache = kind == 1 ? Q.k_cache : Q.v_cache;
-          dst = cache + (((size_t)nn * Q.nh + hd) * Q.cap + ps) * 128;
+          dst = Q.table ? cache + (((size_t)Q.table[nn * Q.maxp + ps / 128] * Q.nh + hd) * 128 + ps % 128) * 128
+                        : cache + (((size_t)nn * Q.nh + hd) * Q.cap + ps) * 128;
         }
         *reinterpret_cast<uint4*>(dst + i0) = *reinterpret_cast<const uint4*>(a);
         *reinterpret_cast<uint4*>(dst + 64 + i0) = *reinterpret_cast<const uint4*>(b);
@@ -544,7 +547,8 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
-                    int max_len, float* part, int* ticket, __half* xp, cudaStream_t st, bool pdl);
+                    int max_len, float* part, int* ticket, __half* xp, const int* table, int maxp,
+                    cudaStream_t st, bool pdl);
 
 // One Llama decoder layer for 16 independent sequences (7 PDL-chained launches):
 // RMSNorm+pack -> QKV projection (RoPE + per-sequence cache append in the
@@ -570,13 +574,17 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
     qkv.pos = a->pos;
     qkv.nh = nh;
     qkv.cap = a->cache_cap;
+    qkv.table = a->block_table;
+    qkv.maxp = a->max_pages;
+    if (a->block_table && a->max_pages * 128 < a->max_len)
+      return set_error(CFB_ERR_DIMENSION, "b16 layer: max_pages * 128 < max_len");
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
                       0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv)))
       return rc;
     if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
                               static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
-                              a->part, a->ticket + (Mq + 2 * D + 2 * F) / kTcM, static_cast<__half*>(a->xp), st,
-                              true)))
+                              a->part, a->ticket + (Mq + 2 * D + 2 * F) / kTcM, static_cast<__half*>(a->xp),
+                              a->block_table, a->max_pages, st, true)))
       return rc;
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
                       st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid)))

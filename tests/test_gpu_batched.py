@@ -150,3 +150,87 @@ def test_batched_greedy_decode_teacher_forced():
             toks[n] = otok  # teacher forcing
         m.tokens.copy_(torch.tensor(toks, dtype=torch.int32))
     assert checked >= 30
+
+
+def _ragged_setup(seed=11, n_layers=2):
+    cfg = LlamaConfig(n_layers=n_layers, hidden=256, n_heads=2, head_dim=128, inter=384, vocab=512)
+    params = random_llama_params(cfg, seed=seed, prefill=0)
+    rng = np.random.default_rng(seed)
+    # ragged lengths hitting page edges: 0, 1, 127, 128, 129, 255, 256, 257 ...
+    S = [0, 1, 127, 128, 129, 255, 256, 257, 3, 40, 200, 300, 383, 384, 385, 90]
+    caches = [[(lp.f16(rng.standard_normal((cfg.n_heads, s, 128))),
+                lp.f16(rng.standard_normal((cfg.n_heads, s, 128)))) for s in S]
+              for _ in range(cfg.n_layers)]
+    return cfg, params, S, caches, rng
+
+
+def test_kv_writer_and_pool_roundtrip():
+    """cfb_b16_kv_write into shuffled pages, read back through the block table:
+    exact, for ragged lengths at every page edge; pages are recycled."""
+    import torch
+    cfg, params, S, caches, _ = _ragged_setup()
+    m = BatchedLlama.paged(cfg, params["layers"], caches, max_len=512, shuffle_seed=5)
+    pool = m.pool
+    for l in range(cfg.n_layers):
+        for n, s in enumerate(S):
+            k, v = pool.gather(l, n, s)
+            assert np.array_equal(k.float().cpu().numpy(), caches[l][n][0]), (l, n)
+            assert np.array_equal(v.float().cpu().numpy(), caches[l][n][1]), (l, n)
+    used = sum(len(p) for p in pool.pages)
+    assert used == sum((s + 127) // 128 for s in S)
+    free0 = len(pool.free)
+    pool.release(5)
+    assert len(pool.free) == free0 + (S[5] + 127) // 128
+    # an appended write at an offset continues the sequence across a page edge
+    extra = lp.f16(np.random.default_rng(1).standard_normal((cfg.n_heads, 5, 128)))
+    pool.write(0, 4, S[4], extra, extra)
+    k, _ = pool.gather(0, 4, S[4] + 5)
+    assert np.array_equal(k.float().cpu().numpy()[:, S[4]:], extra)
+    torch.cuda.synchronize()
+
+
+def test_paged_equals_contiguous_bit_exact():
+    """The paged layout changes addressing only: 3 greedy steps over shuffled
+    pages give bit-identical residuals, logits, tokens and appended K/V rows."""
+    import torch
+    cfg, params, S, caches, rng = _ragged_setup(seed=12)
+    cap = 512
+    a = BatchedLlama.from_params(cfg, params["layers"], caches, cache_cap=cap)
+    b = BatchedLlama.paged(cfg, params["layers"], caches, max_len=cap, shuffle_seed=3)
+    toks = torch.tensor([int(t) for t in rng.integers(0, cfg.vocab, 16)], dtype=torch.int32)
+    for m in (a, b):
+        m.set_head(params["embed"], params["final_norm"], params["lm_head"])
+        m.tokens.copy_(toks)
+        m.set_positions(S)
+        m.reserve(4)
+    for step in range(3):
+        for m in (a, b):
+            m.decode_step(logits=True)
+        torch.cuda.synchronize()
+        assert torch.equal(a.resid, b.resid), step
+        assert torch.equal(a.logits, b.logits), step
+        assert torch.equal(a.tokens, b.tokens), step
+    for l in range(cfg.n_layers):
+        for n, s in enumerate(S):
+            kb, vb = b.pool.gather(l, n, s + 3)
+            assert torch.equal(a.layers[l]["k_cache"][n, :, :s + 3], kb), (l, n)
+            assert torch.equal(a.layers[l]["v_cache"][n, :, :s + 3], vb), (l, n)
+
+
+def test_paged_graph_replay_crosses_pages():
+    """Captured paged decode replayed across a page boundary after reserve()."""
+    import torch
+    cfg = LlamaConfig(n_layers=1, hidden=256, n_heads=2, head_dim=128, inter=384, vocab=256)
+    m = BatchedLlama.random_paged(cfg, max_len=512, seed=2)
+    m.random_head(cfg.vocab)
+    m.set_positions([126 + n for n in range(16)])
+    m.decode_step()
+    torch.cuda.synchronize()
+    m.set_positions([126 + n for n in range(16)])
+    m.capture_decode()
+    m.reserve(8)
+    for _ in range(4):
+        m.replay()
+    torch.cuda.synchronize()
+    assert m.pos.cpu().tolist() == [130 + n for n in range(16)]
+    assert bool(((m.tokens >= 0) & (m.tokens < cfg.vocab)).all())
