@@ -274,7 +274,8 @@ int cfb_ffn_decode(const cfb_ffn_args* args, void* stream);
  *   h = x or f16(rmsnorm(r) * norm_w), r = resid [+ accum_in * 2^-32]
  *   p = softmax(h W_r^T); top_k experts by p (ties: lower id), w = p * routed_scale
  *   y = sum_k w_k down_k(f16(silu(gate_k h) * up_k h)) + shared(h)
- *   out = [r +] y          (CFB_RESID; out may alias resid; accum_in re-zeroed)
+ *   out = [r +] y          (CFB_RESID; out may alias resid; accum_in re-zeroed;
+ *                           CFB_PARTIAL: out = y, the tensor-parallel rank > 0 form)
  * fp16 only, batch <= 4, n_experts <= 256, top_k <= 16, hidden a multiple of 8
  * up to 512 or one of 1024/2048/4096.  Layouts (fp16), Q = max(1, hidden/512):
  *   w_router [E][D]

@@ -35,6 +35,7 @@ constexpr int kRowStride = 1040;       // 1024 B row + 16 B pad: conflict-free l
 
 struct MlaEngParams {
   int D, H, R, S, flags, spw, sleep_max, G2;
+  int NH;                 // real heads (<= 16; tensor-parallel shard): MMA rows >= NH are zero
   float eps, scale_log2;  // scale_log2 = log2(e) / sqrt(R)
   const float* resid;
   const __half* norm_w;
@@ -77,10 +78,10 @@ __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParam
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int TA = (kMlaHeads * H + R) / 4;
+  const int NH = p.NH, TA = (NH * H + R) / 4;
   const int a0 = (int)((long long)i * TA / G), a1 = (int)((long long)(i + 1) * TA / G);
   // W_up rows in 32-row units (keeps each CTA's rows aligned to the chunk rotation)
-  const int UB = kMlaHeads * R / 32;
+  const int UB = NH * R / 32;
   const int b0 = 32 * (int)((long long)i * UB / G), b1 = 32 * (int)((long long)(i + 1) * UB / G);
   const int hb0 = b0 / R, hb1 = b1 > b0 ? (b1 - 1) / R : hb0;  // heads touched (<= 2 segments)
   auto seg = [&](int s, int& r0, int& r1) {
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParam
                                       p.qc[4 * a0 + row] = __float2half_rn(v);
                                     });
   grid_barrier(p.barrier, tid);
-  for (int t = tid; t < kMlaHeads * H / 8; t += kConsumerThreads)
+  for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(qs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.qc) + t);
   consumer_sync();
   for (int s = 0; s < 2; ++s) {
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
     for (int r = 0; r < n; ++r) {
       const int j = r0 + r;
       const void* src = j < S ? (const void*)(p.cache + (size_t)j * 512)
-                              : (const void*)(p.qc + kMlaHeads * p.H);  // new latent row
+                              : (const void*)(p.qc + p.NH * p.H);  // new latent row
       bulk_g2s(stages + s * kAttnStage + r * kRowStride, src, 1024, &full[s], pol);
     }
   };
@@ -203,11 +204,11 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
   if (tid == 0)
     for (int k = 0; k < min(kAttnStages - 1, ntiles); ++k)
       if (j0 + k * kAttnRows + kAttnRows > S) issue(k);  // tiles holding the new row
-  // q_lat (16 x 512 fp16) -> smem rows of kRowStride
+  // q_lat (NH x 512 fp16, zero rows up to 16) -> smem rows of kRowStride
   for (int k = tid; k < kMlaHeads * 64; k += kAttnThreads) {
     const int h = k >> 6, ch = k & 63;
     *reinterpret_cast<uint4*>(qsm + h * kRowStride + ch * 16) =
-        __ldcg(reinterpret_cast<const uint4*>(p.qlat + h * 512) + ch);
+        h < p.NH ? __ldcg(reinterpret_cast<const uint4*>(p.qlat + h * 512) + ch) : make_uint4(0, 0, 0, 0);
   }
   __syncthreads();
   // A fragments of this warp's 128 dims (8 k-steps of 16)
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // W_down^T row tiles of this CTA, split at head boundaries (H/4 tiles per head)
-  const int TD = kMlaHeads * H / 4, tph = H / 4;
+  const int NH = p.NH, TD = NH * H / 4, tph = H / 4;
   const int d0 = (int)((long long)i * TD / G), d1 = (int)((long long)(i + 1) * TD / G);
   const int hd0 = d0 / tph;
   auto dseg = [&](int s, int& t0, int& t1) {
@@ -386,8 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   const Phase PD0 = make_phase(p.w_dn + (size_t)t0 * 4 * R, nullptr, max(t1 - t0, 0), 4 * R * 2, true);
   dseg(1, t0, t1);
   const Phase PD1 = make_phase(p.w_dn + (size_t)t0 * 4 * R, nullptr, max(t1 - t0, 0), 4 * R * 2, true);
-  const Phase PO = make_phase(p.w_o + (size_t)o0 * 4 * kMlaHeads * H, nullptr, o1 - o0,
-                              4 * kMlaHeads * H * 2, true);
+  const Phase PO = make_phase(p.w_o + (size_t)o0 * 4 * NH * H, nullptr, o1 - o0, 4 * NH * H * 2, true);
   pdl_launch_dependents();
   if (warp == kNumConsumerWarps) {
     const Phase ph[3] = {PD0, PD1, PO};
@@ -403,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   //    once into smem, then per element the sum over q split across a warp's
   //    lanes, 4 elements per pass so their loads are in flight together
   {
-    const int NZ = kMlaHeads * 512;
+    const int NZ = NH * 512;
     const int e0 = (int)((long long)i * NZ / G), e1 = (int)((long long)(i + 1) * NZ / G);
     const int stride = 2 * kMlaHeads + kMlaHeads * 512;
     const int h0 = e0 / 512, h1 = (e1 - 1) / 512;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
     }
   }
   grid_barrier(p.barrier + 1, tid);
-  for (int t = tid; t < kMlaHeads * 512 / 8; t += kConsumerThreads)
+  for (int t = tid; t < NH * 512 / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(zs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.zb) + t);
   consumer_sync();
   // 2. o[h] = f16(z[h] W_down[h])
@@ -457,11 +457,11 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
     consumer_sync();
   }
   grid_barrier(p.barrier + 1, tid);
-  for (int t = tid; t < kMlaHeads * H / 8; t += kConsumerThreads)
+  for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(os)[t] = __ldcg(reinterpret_cast<const uint4*>(p.ob) + t);
   consumer_sync();
   // 3. out = sum_h o[h] W_out[h] -> fixed point (each row owned by one CTA)
-  tiled_gemv_phase<__half, 1, true>(PO, ring, warp, lane, tid, cnt, os, kMlaHeads * H, 1,
+  tiled_gemv_phase<__half, 1, true>(PO, ring, warp, lane, tid, cnt, os, NH * H, 1,
                                     4 * (o1 - o0), part, [&](int row, int, float v) {
                                       p.accum[4 * o0 + row] = static_cast<unsigned long long>(
                                           __float2ll_rn(v * 4294967296.0f));
@@ -486,10 +486,10 @@ static int launch_k(K kern, int grid, int block, size_t smem, bool pdl, const Ml
 
 int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
-  if (a->n_heads != kMlaHeads || a->kv_rank != 512 || a->head_dim % 8 || a->head_dim > 128 ||
+  if (a->n_heads < 1 || a->n_heads > kMlaHeads || a->kv_rank != 512 || a->head_dim % 8 || a->head_dim > 128 ||
       a->hidden % 512)
     return set_error(CFB_ERR_DIMENSION,
-                     "head-batched MLA engine: 16 heads, kv_lora_rank 512, head_dim <= 128 (x8), hidden % 512 == 0");
+                     "head-batched MLA engine: 1..16 heads, kv_lora_rank 512, head_dim <= 128 (x8), hidden % 512 == 0");
   if (a->seq_len < 0) return set_error(CFB_ERR_DIMENSION, "seq_len must be >= 0");
   if (!a->resid || !a->norm_w || !a->w_a || !a->w_up || !a->w_dn || !a->w_o || !a->qc || !a->qlat ||
       !a->part || !a->zb || !a->ob || !a->accum || !a->barrier || (a->seq_len && !a->cache))
@@ -507,6 +507,7 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   MlaEngParams p = {};
   p.D = a->hidden;
   p.H = a->head_dim;
+  p.NH = a->n_heads;
   p.R = a->kv_rank;
   p.S = a->seq_len;
   p.flags = a->flags;

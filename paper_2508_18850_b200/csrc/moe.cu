@@ -566,8 +566,9 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
         reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t] = make_ulonglong2(0ull, 0ull);
         reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t + 1] = make_ulonglong2(0ull, 0ull);
       }
+      if (!(p.flags & CFB_PARTIAL))  // tensor-parallel rank > 0: its expert-shard partial only
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] = __fadd_rn(r[k], v[k]);
+        for (int k = 0; k < 4; ++k) v[k] = __fadd_rn(r[k], v[k]);
     }
     reinterpret_cast<float4*>(p.out)[t] = make_float4(v[0], v[1], v[2], v[3]);
   }

@@ -73,7 +73,7 @@ def engine_supported(dims: "DeepSeekDims", batch: int) -> bool:
     """The head-batched MLA engine (csrc/mla_engine.cu) covers the
     DeepSeek-V2-Lite/preset shape at batch 1; other shapes run the reference
     dataflow kernel (csrc/attn_mla.cu)."""
-    return (batch == 1 and dims.n_heads == 16 and dims.kv_rank == 512 and dims.head_dim % 8 == 0
+    return (batch == 1 and 1 <= dims.n_heads <= 16 and dims.kv_rank == 512 and dims.head_dim % 8 == 0
             and dims.head_dim <= 128 and dims.hidden % 512 == 0)
 
 
@@ -114,6 +114,7 @@ class DeepSeekBlock:
         the engine is used when given."""
         import torch
         dev = _native.require_cuda()
+        self.partial = False  # tensor-parallel rank > 0: the MoE writes its partial only
         if batch > 4:
             raise DimensionError("the DeepSeek block supports batch <= 4")
         if engine is None and (mla is None or mla["Dp"] != dims.hidden):
@@ -231,11 +232,16 @@ class DeepSeekBlock:
             _native.check(_native.lib().cfb_mla_decode(self.mla_args(resid, pdl),
                                                        _native.stream_ptr(stream)))
 
-    def launch(self, resid, pdl: bool = True, stream=None) -> None:
-        """Enqueue the block on `stream`: resid <- block(resid)."""
+    def launch(self, resid, pdl: bool = True, stream=None, attn_reduce=None) -> None:
+        """Enqueue the block on `stream`: resid <- block(resid).  Tensor
+        parallel (tp.TPDeepSeekBlock): ``attn_reduce(accum_attn)`` sums the
+        ranks' fixed-point attention partials between the halves."""
         self.launch_attention(resid, pdl, stream)
+        if attn_reduce is not None:
+            attn_reduce(self.accum_attn)
         moe_launch(self.moe, self.ws, resid, resid=resid, norm_w=self.ffn_norm,
-                   accum_in=self.accum_attn, eps=self.dims.eps, pdl=pdl, stream=stream)
+                   accum_in=self.accum_attn, eps=self.dims.eps, pdl=pdl and attn_reduce is None,
+                   stream=stream, partial=self.partial)
 
     def run(self, resid_host) -> tuple[np.ndarray, np.ndarray]:
         """Host convenience: one block on (B, D) fp32 rows.  Returns (new

@@ -125,10 +125,14 @@ class MoeWorkspace:
 
 def moe_launch(mw: MoeWeights, ws: MoeWorkspace, out, *, x=None, resid=None, norm_w=None,
                accum_in=None, eps: float = 1e-6, pdl: bool = False, grid: int = 0,
-               stream=None, trace=None) -> None:
-    """Enqueue one fused MoE launch (device tensors; no host sync)."""
+               stream=None, trace=None, partial: bool = False) -> None:
+    """Enqueue one fused MoE launch (device tensors; no host sync).
+    ``partial`` (tensor-parallel rank > 0): out = this rank's expert-shard
+    partial instead of resid + attention + MoE."""
     B = out.shape[0]
     flags = (_native.NORM | _native.RESID) if resid is not None else 0
+    if partial:
+        flags |= _native.PARTIAL
     if pdl:
         flags |= _native.PDL
     a = _native.MoeArgs(

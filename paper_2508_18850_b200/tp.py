@@ -284,3 +284,93 @@ class TPBatchedLlama:
         import torch
         with torch.cuda.stream(self.m.stream):
             self.graph.replay()
+
+
+# --------------------------------------------------------------------------
+# DeepSeek-V2-Lite block, tensor parallel (SURVEY §8(e) caveats): MLA heads
+# sharded (W_q / W_up / W_down / W_out per head), the latent cache and W_kv
+# replicated (every rank computes the new latent row itself); MoE "TP inside
+# experts": every routed and shared expert's intermediate dimension sharded,
+# the router replicated (identical inputs -> identical routing on all ranks).
+# Exchange steps: one int64 all-reduce of the fixed-point attention head sum
+# (exact), one fp32 all-reduce of the block output (rank 0 carries the
+# residual + attention, ranks > 0 their MoE partial: CFB_PARTIAL).
+# --------------------------------------------------------------------------
+def check_tp_deepseek(dims, world: int) -> None:
+    if world < 1 or dims.n_heads % world:
+        raise DimensionError(f"tensor parallel {world}: n_heads {dims.n_heads} must divide")
+    f = dims.inter // world
+    if dims.inter % world or f % 8 or (dims.n_shared * f) % 8:
+        raise DimensionError(f"tensor parallel {world}: expert width {dims.inter} / {world} must be a multiple of 8")
+
+
+def deepseek_local_dims(dims, world: int):
+    check_tp_deepseek(dims, world)
+    return replace(dims, n_heads=dims.n_heads // world, inter=dims.inter // world)
+
+
+def shard_deepseek(dims, mla_arrays: dict, moe_w: dict, rank: int, world: int):
+    """Oracle-format block weights -> this rank's shard: (local dims, MLA
+    arrays, MoE weights dict).  Heads [rank*nh/TP, (rank+1)*nh/TP); expert
+    intermediate rows [rank*F/TP, (rank+1)*F/TP) of every routed expert and
+    the same fraction of the (concatenated) shared expert."""
+    ld = deepseek_local_dims(dims, world)
+    h0, h1 = rank * ld.n_heads, (rank + 1) * ld.n_heads
+    mla = dict(w_q=mla_arrays["w_q"][h0:h1], w_up=mla_arrays["w_up"][h0:h1], w_kv=mla_arrays["w_kv"],
+               w_down=mla_arrays["w_down"][h0:h1], w_out=mla_arrays["w_out"][h0:h1],
+               kv_cache=mla_arrays["kv_cache"])
+
+    def cut(ex, f):
+        lo, hi = rank * f, (rank + 1) * f
+        return dict(gate=ex["gate"][lo:hi], up=ex["up"][lo:hi], down=ex["down"][:, lo:hi])
+
+    moe = dict(router=moe_w["router"],
+               experts=[cut(moe_w["experts"][e], ld.inter) for e in range(len(moe_w["experts"]))],
+               shared=None if moe_w.get("shared") is None else cut(moe_w["shared"], ld.n_shared * ld.inter))
+    return ld, mla, moe
+
+
+class TPDeepSeekBlock:
+    """One rank of a tensor-parallel DeepSeek block.  ``reduce_int`` /
+    ``reduce_f32`` are the all-reduce(SUM) callables (NCCL in production,
+    a device sum in the emulated single-GPU test)."""
+
+    def __init__(self, dims, rank: int, world: int, block, reduce_int=None, reduce_f32=None):
+        self.dims, self.rank, self.world, self.block = dims, rank, world, block
+        block.partial = rank > 0
+        self.reduce_int, self.reduce_f32 = reduce_int, reduce_f32
+
+    @classmethod
+    def from_arrays(cls, dims, mla_arrays, moe_w, attn_norm, ffn_norm, rank, world, **kw):
+        from .deepseek import DeepSeekBlock
+        ld, mla, moe = shard_deepseek(dims, mla_arrays, moe_w, rank, world)
+        return cls(dims, rank, world, DeepSeekBlock.from_arrays(ld, mla, moe, attn_norm, ffn_norm), **kw)
+
+    @classmethod
+    def random(cls, dims, rank, world, seq_len, seed=0, **kw):
+        from .deepseek import DeepSeekBlock
+        ld = deepseek_local_dims(dims, world)
+        return cls(dims, rank, world, DeepSeekBlock.random(ld, seq_len, seed=seed * 100 + rank), **kw)
+
+    @staticmethod
+    def nccl_reducers():
+        import torch.distributed as dist
+        return (lambda t: dist.all_reduce(t), lambda t: dist.all_reduce(t))
+
+    def launch_attention(self, resid, stream=None) -> None:
+        self.block.launch_attention(resid, pdl=True, stream=stream)
+
+    def launch_moe(self, resid, stream=None) -> None:
+        b = self.block
+        from .moe import moe_launch
+        moe_launch(b.moe, b.ws, resid, resid=resid, norm_w=b.ffn_norm, accum_in=b.accum_attn,
+                   eps=b.dims.eps, pdl=False, stream=stream, partial=b.partial)
+
+    def launch(self, resid, stream=None) -> None:
+        """resid (replicated, [1][D] fp32) <- block(resid) on every rank."""
+        self.launch_attention(resid, stream)
+        if self.world > 1:
+            self.reduce_int(self.block.accum_attn)
+        self.launch_moe(resid, stream)
+        if self.world > 1:
+            self.reduce_f32(resid)

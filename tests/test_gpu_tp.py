@@ -117,3 +117,47 @@ def test_tp_nccl_graph_world1():
         assert got == want
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_tp_deepseek_block_emulated(world):
+    """TP DeepSeek block on one device: per-rank MLA engine on its heads
+    (world 4: one head per rank, the NH = 1 engine path) -> device int64 SUM of
+    the fixed-point attention partials -> per-rank MoE on its expert-row shard
+    (CFB_PARTIAL on ranks > 0) -> device SUM == the unsharded block."""
+    import torch
+    from oracle import clusterdec_port as cp
+    from oracle import deepseek_port as dp
+    from paper_2508_18850_b200.deepseek import DeepSeekBlock, DeepSeekDims
+    from paper_2508_18850_b200.tp import TPDeepSeekBlock
+    dims = DeepSeekDims(hidden=512, n_heads=4, head_dim=64, kv_rank=512, n_experts=8, top_k=2, inter=128,
+                        n_shared=1)
+    mla = cp.gen_mla(1, dims.hidden, dims.n_heads, dims.head_dim, 300, dims.kv_rank, seed=4)
+    mla = {k: mla[k] for k in ("w_q", "w_up", "w_kv", "w_down", "w_out", "kv_cache")}
+    moe_w = dp.gen_moe(dims.hidden, dims.n_experts, dims.inter, dims.n_shared, seed=6)
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, dims.hidden)).astype(np.float32)
+    g1 = dp.f16(1.0 + 0.1 * rng.standard_normal(dims.hidden))
+    g2 = dp.f16(1.0 + 0.1 * rng.standard_normal(dims.hidden))
+    full = DeepSeekBlock.from_arrays(dims, mla, moe_w, g1, g2)
+    assert full.engine is not None
+    want, want_idx = full.run(x)
+    ranks = [TPDeepSeekBlock.from_arrays(dims, mla, moe_w, g1, g2, r, world) for r in range(world)]
+    assert all(t.block.engine is not None for t in ranks)
+    rs = [torch.from_numpy(x).cuda() for _ in range(world)]
+    for t, r in zip(ranks, rs):
+        t.launch_attention(r)
+    acc = sum(t.block.accum_attn for t in ranks)       # int64: exact, as the NCCL SUM
+    for t in ranks:
+        t.block.accum_attn.copy_(acc)
+    for t, r in zip(ranks, rs):
+        t.launch_moe(r)
+    got = sum(rs).cpu().numpy()
+    torch.cuda.synchronize()
+    for t in ranks:
+        assert np.array_equal(t.block.ws.route_idx.cpu().numpy().astype(np.int64), want_idx)
+    np.testing.assert_allclose(got, want, rtol=1e-5, atol=2e-5)
+    # and against the CPU oracle block at the north-star tolerance
+    ref, _ = dp.block(x, mla, g1, g2, moe_w, dims.top_k, dims.cluster, dims.eps, dims.routed_scale)
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= 2e-2 and err / float(np.max(np.abs(ref))) <= 1e-2, err
