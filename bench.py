@@ -268,6 +268,10 @@ def run_ours(args, rank, world):
             line["batch16_tp"] = batch16_tp(cfg, rank, world, 1024, pk["hbm_gbs"])
         except Exception as exc:  # pragma: no cover - multi-GPU only
             line["batch16_tp"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+        try:
+            line["deepseek_tp"] = deepseek_tp(rank, world, [1024, 16384], pk["hbm_gbs"])
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            line["deepseek_tp"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
     if rank == 0 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
     if world > 1:
@@ -428,6 +432,56 @@ def batch16_tp(cfg, rank, world, ctx, peak_gbs, steps=10):
     nbytes = m.m.step_bytes(ctx + 3 + steps // 2) * world  # per-rank bytes x ranks (weights/KV sharded)
     return {"ctx": ctx, "batch": 16, "tp": world, "step_us": round(us, 1),
             "tokens_per_s": round(16e6 / us, 1), "hbm_gbs_all_ranks": round(nbytes / us / 1e3, 1)}
+
+
+def deepseek_tp(rank, world, ctxs, peak_gbs, layers=4, reps=16):
+    """DeepSeek-V2-Lite block, tensor parallel (tp.TPDeepSeekBlock): MLA
+    heads and expert rows sharded, one int64 and one fp32 NCCL all-reduce per
+    block; ``layers`` distinct blocks per CUDA graph; max over ranks."""
+    import torch
+    from paper_2508_18850_b200.deepseek import LITE
+    from paper_2508_18850_b200.tp import TPDeepSeekBlock, deepseek_local_dims
+    red = TPDeepSeekBlock.nccl_reducers() if world > 1 else (None, None)
+    ld = deepseek_local_dims(LITE, world)
+    out = []
+    for ctx in ctxs:
+        blocks = [TPDeepSeekBlock.random(LITE, rank, world, ctx, seed=l, reduce_int=red[0], reduce_f32=red[1])
+                  for l in range(layers)]
+        resid = torch.full((1, LITE.hidden), 0.5, device="cuda")
+        st = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            for b in blocks:
+                b.launch(resid)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            for b in blocks:
+                b.launch(resid)
+        with torch.cuda.stream(st):
+            for _ in range(3):
+                g.replay()
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            e0.record(st)
+            for _ in range(reps):
+                g.replay()
+            e1.record(st)
+        torch.cuda.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e3 / (reps * layers)], device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        us = float(t.item())
+        nbytes = ld.block_bytes(ctx) * world
+        out.append({"ctx": ctx, "tp": world, "block_us": round(us, 2),
+                    "hbm_gbs_all_ranks": round(nbytes / us / 1e3, 1),
+                    "launches": (3 + 1) * layers * (reps + 3)})
+        del g, blocks
+        torch.cuda.empty_cache()
+    return out
 
 
 # --------------------------------------------------------------------- CPU arm

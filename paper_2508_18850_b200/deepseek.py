@@ -130,7 +130,8 @@ class DeepSeekBlock:
             self.eng_ws = dict(
                 qc=torch.zeros(nh * H + R, device=dev, dtype=torch.float16),
                 qlat=torch.zeros(nh * R, device=dev, dtype=torch.float16),
-                part=torch.zeros(sms, 2 * nh + nh * R, device=dev, dtype=torch.float32),
+                # partials keep all 16 MMA head rows whatever nh is (cfb.h)
+                part=torch.zeros(sms, 2 * 16 + 16 * R, device=dev, dtype=torch.float32),
                 zb=torch.zeros(nh * R, device=dev, dtype=torch.float16),
                 ob=torch.zeros(nh * H, device=dev, dtype=torch.float16),
                 barrier=torch.zeros(2, device=dev, dtype=torch.int64))

@@ -119,8 +119,8 @@ def test_tp_nccl_graph_world1():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 4])
-def test_tp_deepseek_block_emulated(world):
+@pytest.mark.parametrize("world,S", [(2, 300), (4, 300), (4, 10000)])  # 10000: 148 attention partials
+def test_tp_deepseek_block_emulated(world, S):
     """TP DeepSeek block on one device: per-rank MLA engine on its heads
     (world 4: one head per rank, the NH = 1 engine path) -> device int64 SUM of
     the fixed-point attention partials -> per-rank MoE on its expert-row shard
@@ -132,7 +132,7 @@ def test_tp_deepseek_block_emulated(world):
     from paper_2508_18850_b200.tp import TPDeepSeekBlock
     dims = DeepSeekDims(hidden=512, n_heads=4, head_dim=64, kv_rank=512, n_experts=8, top_k=2, inter=128,
                         n_shared=1)
-    mla = cp.gen_mla(1, dims.hidden, dims.n_heads, dims.head_dim, 300, dims.kv_rank, seed=4)
+    mla = cp.gen_mla(1, dims.hidden, dims.n_heads, dims.head_dim, S, dims.kv_rank, seed=4)
     mla = {k: mla[k] for k in ("w_q", "w_up", "w_kv", "w_down", "w_out", "kv_cache")}
     moe_w = dp.gen_moe(dims.hidden, dims.n_experts, dims.inter, dims.n_shared, seed=6)
     rng = np.random.default_rng(1)
