@@ -183,7 +183,8 @@ typedef struct cfb_mla_args {
 int cfb_mla_decode(const cfb_mla_args* args, void* stream);
 
 /*
- * Head-batched MLA for the DeepSeek block engine (batch 1, 16 heads, kv_lora_rank
+ * Head-batched MLA for the DeepSeek block engine (batch 1, 1..16 heads - a
+ * tensor-parallel rank passes its head shard; the MMA pads to 16 - kv_lora_rank
  * 512, head_dim <= 128): same math as cfb_mla_decode (absorbed form, new latent
  * row attended once) but every weight and cache row crosses HBM once -
  * three PDL-chained launches: projections (W_q | W_kv, then W_up), split-KV
