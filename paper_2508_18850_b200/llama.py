@@ -37,6 +37,9 @@ class LlamaConfig:
     rope_theta: float = 10000.0
     cluster: int = 4
     dtype_bytes: int = 2
+    # "persistent": one launch per step on every SM (csrc/decode_step.cu);
+    # "layered": split_token cluster kernel + fused FFN per layer (csrc/llama.cu)
+    engine: str = "layered"
 
     def weight_bytes(self) -> int:
         """Bytes of every weight a decode step streams (attention + FFN + norms,
@@ -61,7 +64,10 @@ LLAMA2_7B = LlamaConfig()
 class _LlamaConfigC(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int) for n in ("dtype", "n_layers", "hidden", "n_heads", "head_dim",
                                              "inter", "vocab", "cache_cap", "cluster")] + [
-        ("eps", ctypes.c_float)]
+        ("eps", ctypes.c_float), ("engine", ctypes.c_int)]
+
+
+ENGINES = {"layered": 0, "persistent": 1}
 
 
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -82,6 +88,36 @@ def rope_table(max_pos: int, head_dim: int, theta: float) -> np.ndarray:
     return np.stack([np.cos(ang), np.sin(ang)], axis=-1).astype(np.float32)
 
 
+def _draw(rng, shape, scale, shift=0.0):
+    x = (rng.standard_normal(shape) * scale + shift).astype(np.float32)
+    return x.astype(np.float16).astype(np.float32)
+
+
+def random_llama_layer(cfg: LlamaConfig, seed: int, layer: int, prefill: int = 0) -> dict:
+    """Layer `layer` of ``random_llama_params`` on its own (same draws), so a
+    32-layer model can be generated, uploaded and checked one layer at a time."""
+    D, F, nh, H = cfg.hidden, cfg.inter, cfg.n_heads, cfg.head_dim
+    rng = np.random.default_rng(seed * 1000 + layer)
+    return dict(
+        attn_norm=_draw(rng, (D,), 0.1, 1.0),
+        w_qkv=_draw(rng, (nh, D, 3 * H), D ** -0.5),
+        w_out=_draw(rng, (nh, H, D), H ** -0.5),
+        ffn_norm=_draw(rng, (D,), 0.1, 1.0),
+        w1=_draw(rng, (F, D), D ** -0.5),
+        w2=_draw(rng, (F, D), D ** -0.5),
+        w3=_draw(rng, (D, F), F ** -0.5),
+        k_cache=_draw(rng, (nh, prefill, H), 1.0),
+        v_cache=_draw(rng, (nh, prefill, H), 1.0))
+
+
+def random_llama_globals(cfg: LlamaConfig, seed: int) -> dict:
+    """Embedding, final norm and LM head of ``random_llama_params``."""
+    rng = np.random.default_rng(seed * 1000 + 999)
+    D = cfg.hidden
+    return dict(embed=_draw(rng, (cfg.vocab, D), 1.0), final_norm=_draw(rng, (D,), 0.1, 1.0),
+                lm_head=_draw(rng, (cfg.vocab, D), D ** -0.5))
+
+
 def random_llama_params(cfg: LlamaConfig, seed: int = 0, prefill: int = 0) -> dict:
     """Seeded numpy parameters in the reference's logical layouts.
 
@@ -91,27 +127,8 @@ def random_llama_params(cfg: LlamaConfig, seed: int = 0, prefill: int = 0) -> di
     K and V caches (nh, prefill, H) ~ N(0, 1); globals from seed*1000 + 999:
     embed (V, D) ~ N(0, 1), final_norm, lm_head (V, D)*D^-1/2.  All values are
     rounded to fp16."""
-    def draw(rng, shape, scale, shift=0.0):
-        x = (rng.standard_normal(shape) * scale + shift).astype(np.float32)
-        return x.astype(np.float16).astype(np.float32)
-
-    D, F, nh, H = cfg.hidden, cfg.inter, cfg.n_heads, cfg.head_dim
-    layers = []
-    for l in range(cfg.n_layers):
-        rng = np.random.default_rng(seed * 1000 + l)
-        layers.append(dict(
-            attn_norm=draw(rng, (D,), 0.1, 1.0),
-            w_qkv=draw(rng, (nh, D, 3 * H), D ** -0.5),
-            w_out=draw(rng, (nh, H, D), H ** -0.5),
-            ffn_norm=draw(rng, (D,), 0.1, 1.0),
-            w1=draw(rng, (F, D), D ** -0.5),
-            w2=draw(rng, (F, D), D ** -0.5),
-            w3=draw(rng, (D, F), F ** -0.5),
-            k_cache=draw(rng, (nh, prefill, H), 1.0),
-            v_cache=draw(rng, (nh, prefill, H), 1.0)))
-    rng = np.random.default_rng(seed * 1000 + 999)
-    return dict(layers=layers, embed=draw(rng, (cfg.vocab, D), 1.0),
-                final_norm=draw(rng, (D,), 0.1, 1.0), lm_head=draw(rng, (cfg.vocab, D), D ** -0.5))
+    layers = [random_llama_layer(cfg, seed, l, prefill) for l in range(cfg.n_layers)]
+    return dict(layers=layers, **random_llama_globals(cfg, seed))
 
 
 class LlamaDecoder:
@@ -123,6 +140,8 @@ class LlamaDecoder:
             raise DimensionError("the decode engine runs fp16 storage only")
         if cfg.head_dim % cfg.cluster or cfg.hidden % cfg.cluster:
             raise DimensionError("head_dim and hidden must be divisible by the cluster size")
+        if cfg.engine not in ENGINES:
+            raise DimensionError(f"unknown engine {cfg.engine!r} (one of {sorted(ENGINES)})")
         self.cfg = cfg
         self.cache_cap = cache_cap
         self.dev = _native.require_cuda()
@@ -156,9 +175,20 @@ class LlamaDecoder:
 
     @classmethod
     def from_params(cls, cfg: LlamaConfig, params: dict, cache_cap: int) -> "LlamaDecoder":
+        return cls.from_layers(cfg, params["layers"], params, cache_cap)
+
+    @classmethod
+    def from_layers(cls, cfg: LlamaConfig, layers, globals_: dict, cache_cap: int) -> "LlamaDecoder":
+        """Pack logical layers one at a time (``layers`` may be a generator,
+        so host memory holds one fp32 layer at a time) plus the globals
+        (embed, final_norm, lm_head)."""
         m = cls(cfg, cache_cap)
         torch = m.torch
-        m.layers = [m._pack_layer(lp) for lp in params["layers"]]
+        for lp in layers:
+            m.layers.append(m._pack_layer(lp))
+        if len(m.layers) != cfg.n_layers:
+            raise DimensionError(f"got {len(m.layers)} layers, config has {cfg.n_layers}")
+        params = globals_
 
         def t(a):
             return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(m.dev).half()
@@ -209,7 +239,8 @@ class LlamaDecoder:
 
         c = _LlamaConfigC(dtype=2, n_layers=L, hidden=cfg.hidden, n_heads=cfg.n_heads,
                           head_dim=cfg.head_dim, inter=cfg.inter, vocab=cfg.vocab,
-                          cache_cap=self.cache_cap, cluster=cfg.cluster, eps=cfg.eps)
+                          cache_cap=self.cache_cap, cluster=cfg.cluster, eps=cfg.eps,
+                          engine=ENGINES[cfg.engine])
         w = _LlamaWeightsC(embed=self.embed.data_ptr(), final_norm=self.final_norm.data_ptr(),
                            lm_head=self.lm_head.data_ptr(), rope_cs=self.rope.data_ptr(),
                            attn_norm=arr("attn_norm"), w_qkv=arr("w_qkv"), w_out=arr("w_out"),
@@ -241,6 +272,32 @@ class LlamaDecoder:
     @property
     def launches_per_step(self) -> int:
         return int(self._lib.cfb_llama_launches_per_step(self._h))
+
+    def set_trace(self, enable: bool = True):
+        """Persistent engine: per-CTA globaltimer stamps of every phase boundary
+        ([n_layers][grid][8] int64 on device, filled by each step), or None."""
+        L_ = self._lib
+        L_.cfb_llama_set_trace.argtypes = [ctypes.c_void_p, ctypes.c_void_p,
+                                           ctypes.POINTER(ctypes.c_int)]
+        grid = ctypes.c_int(0)
+        if not enable:
+            _native.check(L_.cfb_llama_set_trace(self._h, None, ctypes.byref(grid)))
+            self.trace = None
+            return None
+        _native.check(L_.cfb_llama_set_trace(self._h, None, ctypes.byref(grid)))
+        self.trace = self.torch.zeros(self.cfg.n_layers, grid.value, 8, dtype=self.torch.int64,
+                                      device=self.dev)
+        _native.check(L_.cfb_llama_set_trace(self._h, self.trace.data_ptr(), ctypes.byref(grid)))
+        return self.trace
+
+    def check(self) -> None:
+        """Raise if a step found the cache full (pos + 1 > cache_cap) and skipped."""
+        L_ = self._lib
+        L_.cfb_llama_check.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_void_p]
+        err = ctypes.c_int(0)
+        _native.check(L_.cfb_llama_check(self._h, ctypes.byref(err), self._sp()))
+        if err.value:
+            raise DimensionError(f"decode position reached the cache capacity {self.cache_cap}")
 
     def set_state(self, pos: int, token: int) -> None:
         _native.check(self._lib.cfb_llama_set_state(self._h, pos, token, self._sp()))
