@@ -452,9 +452,17 @@ int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int b
  * The engine owns its small workspace; the CUDA graph of one step advances
  * the device-side position, so replays decode consecutive tokens.
  */
+enum cfb_engine_kind {
+  CFB_ENGINE_LAYERED = 0,    /* one launch per block half: split_token cluster kernel (DSMEM
+                                exchange) + fused FFN kernel, PDL-chained (2L+2 launches) */
+  CFB_ENGINE_PERSISTENT = 1  /* ONE persistent launch per step on every SM: continuous weight
+                                stream across layers, global-memory flags between phases
+                                (csrc/decode_step.cu); head_dim 128 */
+};
 typedef struct cfb_llama_config {
   int dtype, n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster;
   float eps;
+  int engine; /* cfb_engine_kind */
 } cfb_llama_config;
 typedef struct cfb_llama_weights {
   const void* embed;
@@ -509,6 +517,13 @@ int cfb_llama_enqueue(cfb_llama* m, int part, int layer, void* stream);
 int cfb_llama_tp_buffers(cfb_llama* m, unsigned long long** accum, float** resid,
                          unsigned long long** argkey);
 int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
+/* Persistent engine only: per-CTA globaltimer stamps [n_layers][grid][8] (phase
+ * boundaries of csrc/decode_step.cu) written each step into `trace` (device, or
+ * NULL to stop); returns the grid size through *grid. */
+int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid);
+/* Device-side status of the last steps: *err_host = 1 if a step found pos + 1 >
+ * cache_cap and did nothing (stream-ordered read, then the flag is cleared). */
+int cfb_llama_check(cfb_llama* m, int* err_host, void* stream);
 
 /* One ClusterReduce (op 0=sum,1=max,2=softmax_merge) or ClusterGather (op 3)
  * over N CTAs of one cluster; in/out [N][n] T.  Test kernel for the DSMEM

@@ -51,6 +51,42 @@ int tuned_sleep();
                               cudaGetErrorString(e_), __FILE__, __LINE__);          \
   } while (0)
 
+// Persistent whole-step decode kernel (csrc/decode_step.cu).  Per-layer
+// pointer arrays live in DEVICE memory (the kernel walks all layers).
+struct LlamaStepArgs {
+  int n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster, grid;
+  float eps;
+  const void* const* attn_norm;
+  const void* const* w_qkv;
+  const void* const* w_out;
+  const void* const* ffn_norm;
+  const void* const* w_gu;
+  const void* const* w_dn;
+  void* const* k_cache;
+  void* const* v_cache;
+  const void* embed;
+  const void* final_norm;
+  const void* lm_head;
+  const float* rope_cs;
+  float* resid;
+  unsigned long long* accum;
+  void* qkv;
+  void* act;
+  float* partials;
+  unsigned long long* barrier;
+  unsigned long long* counters;
+  float* logits;
+  float* cand_val;
+  int* cand_idx;
+  unsigned* ticket;
+  int* token;
+  int* pos;
+  int* err;
+  unsigned long long* trace;
+};
+int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st);
+int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out);
+
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
 int qkv_proj(int dtype, int B, int D, int rows, const float* resid, const void* norm_w, float eps,
              const void* w, void* out, int flags, cudaStream_t st);

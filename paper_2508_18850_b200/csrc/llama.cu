@@ -33,6 +33,15 @@ struct cfb_llama {
   bool split_qkv = false;
   int tp_rank = 0, tp_size = 1, vocab_offset = 0;
   int ext = 0;  // bit mask: accum / resid / argkey are caller-owned
+  // persistent engine (csrc/decode_step.cu)
+  void** dev_ptrs = nullptr;            // 8 x n_layers per-layer pointers, device copy
+  void* pqkv = nullptr;                 // q|k|v rows of the current layer
+  float* partials = nullptr;            // attention partials [nh][grid][132]
+  unsigned long long* pbarrier = nullptr;
+  unsigned long long* counters = nullptr;  // [2 nh]
+  int* err = nullptr;
+  unsigned long long* trace = nullptr;
+  int grid = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -175,10 +184,56 @@ int enqueue_part(cfb_llama* m, int part, int layer, cudaStream_t st) {
   return cfb::set_error(CFB_ERR_ARGUMENT, "unknown engine part %d", part);
 }
 
+int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
+  const cfb_llama_config& c = m->cfg;
+  const int L = c.n_layers;
+  cfb::LlamaStepArgs a = {};
+  a.n_layers = L;
+  a.hidden = c.hidden;
+  a.n_heads = c.n_heads;
+  a.head_dim = c.head_dim;
+  a.inter = c.inter;
+  a.vocab = c.vocab;
+  a.cache_cap = c.cache_cap;
+  a.cluster = c.cluster;
+  a.grid = m->grid;
+  a.eps = c.eps;
+  void** d = m->dev_ptrs;
+  a.attn_norm = d;
+  a.w_qkv = d + L;
+  a.w_out = d + 2 * L;
+  a.ffn_norm = d + 3 * L;
+  a.w_gu = d + 4 * L;
+  a.w_dn = d + 5 * L;
+  a.k_cache = d + 6 * L;
+  a.v_cache = d + 7 * L;
+  a.embed = m->embed;
+  a.final_norm = m->final_norm;
+  a.lm_head = m->lm_head;
+  a.rope_cs = m->rope_cs;
+  a.resid = m->resid;
+  a.accum = m->accum;
+  a.qkv = m->pqkv;
+  a.act = m->act;
+  a.partials = m->partials;
+  a.barrier = m->pbarrier;
+  a.counters = m->counters;
+  a.logits = m->logits;
+  a.cand_val = m->cand_val;
+  a.cand_idx = m->cand_idx;
+  a.ticket = m->lm_ticket;
+  a.token = m->token;
+  a.pos = m->pos;
+  a.err = m->err;
+  a.trace = m->trace;
+  return cfb::llama_step_launch(&a, st);
+}
+
 int enqueue_step(cfb_llama* m, cudaStream_t st) {
   if (m->tp_size > 1)
     return cfb::set_error(CFB_ERR_ARGUMENT,
                           "tensor-parallel engines are driven part by part (collectives between)");
+  if (m->cfg.engine == CFB_ENGINE_PERSISTENT) return enqueue_persistent(m, st);
   int rc = enqueue_embed(m, st);
   for (int l = 0; !rc && l < m->cfg.n_layers; ++l)
     if (!(rc = enqueue_attn(m, l, st))) rc = enqueue_ffn(m, l, st);
@@ -237,6 +292,41 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
       return rc;
     }
   }
+  if (cfg->engine == CFB_ENGINE_PERSISTENT) {
+    if (cfg->dtype != CFB_F16 || cfg->head_dim != 128) {
+      cfb_llama_destroy(m);
+      return set_error(CFB_ERR_DIMENSION, "persistent engine: fp16, head_dim 128");
+    }
+    m->grid = sms;
+    const int N = cfg->cluster;
+    const size_t qkv_rows = (size_t)cfg->n_heads * N * ((3 * cfg->head_dim / N + 3) / 4) * 4;
+    std::vector<const void*> host(8 * (size_t)L);
+    for (int l = 0; l < L; ++l) {
+      host[l] = w->attn_norm[l];
+      host[L + l] = w->w_qkv[l];
+      host[2 * L + l] = w->w_out[l];
+      host[3 * L + l] = w->ffn_norm[l];
+      host[4 * L + l] = w->w_gu[l];
+      host[5 * L + l] = w->w_dn[l];
+      host[6 * L + l] = w->k_cache[l];
+      host[7 * L + l] = w->v_cache[l];
+    }
+    if ((rc = alloc_zero((void**)&m->dev_ptrs, host.size() * sizeof(void*))) ||
+        (rc = alloc_zero(&m->pqkv, qkv_rows * 2)) ||
+        (rc = alloc_zero((void**)&m->partials, (size_t)cfg->n_heads * sms * 132 * 4)) ||
+        (rc = alloc_zero((void**)&m->pbarrier, 8)) ||
+        (rc = alloc_zero((void**)&m->counters, (size_t)2 * cfg->n_heads * 8)) ||
+        (rc = alloc_zero((void**)&m->err, 4))) {
+      cfb_llama_destroy(m);
+      return rc;
+    }
+    const cudaError_t e = cudaMemcpy(m->dev_ptrs, host.data(), host.size() * sizeof(void*),
+                                     cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      cfb_llama_destroy(m);
+      return set_error(CFB_ERR_CUDA, "cudaMemcpy: %s", cudaGetErrorString(e));
+    }
+  }
   *out = m;
   return CFB_OK;
 }
@@ -247,7 +337,8 @@ int cfb_llama_destroy(cfb_llama* m) {
   if (m->graph) cudaGraphDestroy(m->graph);
   void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
                   m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
-                  m->pos, (m->ext & 4) ? nullptr : m->argkey, m->qkv};
+                  m->pos, (m->ext & 4) ? nullptr : m->argkey, m->qkv, m->dev_ptrs, m->pqkv,
+                  m->partials, m->pbarrier, m->counters, m->err};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -315,6 +406,7 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
 }
 
 int cfb_llama_launches_per_step(const cfb_llama* m) {
+  if (m && m->cfg.engine == CFB_ENGINE_PERSISTENT && m->tp_size == 1) return 1;
   return m ? 2 + (m->split_qkv ? 3 : 2) * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
 }
 
@@ -375,6 +467,26 @@ int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream) {
   if (!m || !token_host) return cfb::set_error(CFB_ERR_ARGUMENT, "null argument");
   CFB_CUDA(cudaMemcpyAsync(m->token, token_host, 4, cudaMemcpyHostToDevice,
                            static_cast<cudaStream_t>(stream)));
+  return CFB_OK;
+}
+
+int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (m->cfg.engine != CFB_ENGINE_PERSISTENT)
+    return cfb::set_error(CFB_ERR_ARGUMENT, "tracing needs the persistent engine");
+  m->trace = trace;
+  if (grid) *grid = m->grid;
+  return CFB_OK;
+}
+
+int cfb_llama_check(cfb_llama* m, int* err_host, void* stream) {
+  if (!m || !err_host) return cfb::set_error(CFB_ERR_ARGUMENT, "null argument");
+  *err_host = 0;
+  if (!m->err) return CFB_OK;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CFB_CUDA(cudaMemcpyAsync(err_host, m->err, 4, cudaMemcpyDeviceToHost, st));
+  CFB_CUDA(cudaStreamSynchronize(st));
+  CFB_CUDA(cudaMemsetAsync(m->err, 0, 4, st));
   return CFB_OK;
 }
 
