@@ -60,8 +60,6 @@ enum cfb_flags {
   CFB_PARTIAL = 1 << 8,      /* batch-16 tensor parallel, ranks > 0: residual-epilogue
                                 projections write their partial sum only (the caller's
                                 all-reduce adds the residual once, from rank 0) */
-  CFB_QKV_IN = 1 << 9,       /* attention module: the rank's q|k|v slices come precomputed
-                                from cfb_qkv_proj (qkv_in) instead of its own QKV GEMV */
   CFB_DYN_POOL = 1 << 10     /* fused FFN, batch 1: the last ~4 gate/up tiles per CTA are
                                 work-stolen from a pool; barrier must then hold 2 u64 */
 };
@@ -129,18 +127,7 @@ typedef struct cfb_mha_args {
   float* stats;
   unsigned long long* traffic; /* [CFB_STAGE_COUNT] logical DSMEM bytes, or NULL */
   unsigned long long* trace;   /* [grid CTAs][16] %globaltimer phase stamps (profiling), or NULL */
-  const void* qkv_in;          /* CFB_QKV_IN: [B][rows of w_qkv] T from cfb_qkv_proj */
 } cfb_mha_args;
-
-/*
- * QKV projection of the attention module on ALL SMs (engine split mode): the
- * cluster kernel occupies n_heads * N SMs only, so its 100 MB QKV stream runs
- * here on a persistent grid instead: out[b][r] = T(x[b] . w_qkv row r) over the
- * w_qkv row tiles of the cfb_mha_args layout - rows in [head][rank][q|k|v slice] order;
- * x = f16(rmsnorm(resid) * norm_w).  flags: CFB_PDL.
- */
-int cfb_qkv_proj(int dtype, int batch, int hidden, int rows, const float* resid, const void* norm_w,
-                 float eps, const void* w_qkv, void* out, int flags, void* stream);
 
 int cfb_mha_decode(const cfb_mha_args* args, void* stream);
 
@@ -455,9 +442,14 @@ int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int b
 enum cfb_engine_kind {
   CFB_ENGINE_LAYERED = 0,    /* one launch per block half: split_token cluster kernel (DSMEM
                                 exchange) + fused FFN kernel, PDL-chained (2L+2 launches) */
-  CFB_ENGINE_PERSISTENT = 1  /* ONE persistent launch per step on every SM: continuous weight
-                                stream across layers, global-memory flags between phases
-                                (csrc/decode_step.cu); head_dim 128 */
+  CFB_ENGINE_PERSISTENT = 1, /* ONE persistent launch per step (csrc/decode_step.cu): the
+                                producer warps stream every layer's weights without stopping;
+                                the attention module of a head runs on one N-CTA cluster
+                                (split_token, DSMEM gather/exchange), grid barriers between
+                                block halves; head_dim 128 */
+  CFB_ENGINE_PERSISTENT_FLAT = 2 /* as PERSISTENT, but the attention is split over all SMs
+                                and its partials are exchanged through global memory with
+                                per-head flags (the off-chip-exchange ablation) */
 };
 typedef struct cfb_llama_config {
   int dtype, n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster;

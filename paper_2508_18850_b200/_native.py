@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcfb.so"
 
 CFB_F16, CFB_F32 = 2, 4
 APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED, PDL, ONESHOT = 1, 2, 4, 8, 16, 32, 64, 128
-PARTIAL, QKV_IN, DYN_POOL = 256, 512, 1024
+PARTIAL, DYN_POOL = 256, 1024
 STAGE_NAMES = ("qkv_gather", "stats_max_reduce", "stats_sum_reduce", "stats_merge_reduce",
                "attn_out_reduce", "q_proj_gather", "latent_kv_gather", "absorbed_q_gather",
                "down_proj_reduce", "score_reduce", "out_proj_reduce")
@@ -37,7 +37,7 @@ class MhaArgs(ctypes.Structure):
         ("x", _vp), ("resid", _vp), ("norm_w", _vp), ("eps", ctypes.c_float),
         ("w_qkv", _vp), ("w_out", _vp), ("k_cache", _vp), ("v_cache", _vp),
         ("rope_cs", _vp), ("step_pos", _vp), ("out", _vp), ("accum", _vp),
-        ("stats", _vp), ("traffic", _vp), ("trace", _vp), ("qkv_in", _vp),
+        ("stats", _vp), ("traffic", _vp), ("trace", _vp),
     ]
 
 

@@ -2,6 +2,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #include "common.h"
 
@@ -15,21 +18,21 @@ int set_error(int code, const char* fmt, ...) {
   va_end(ap);
   return code;
 }
-int tuned_spw() {
-  static int v = [] {
-    const char* e = getenv("CFB_SPW");
-    const int x = e ? atoi(e) : kMaxSlotsPerWarpHost;
-    return (x < 1 || x > kMaxSlotsPerWarpHost) ? kMaxSlotsPerWarpHost : x;
-  }();
-  return v;
-}
-int tuned_sleep() {
-  static int v = [] {
-    const char* e = getenv("CFB_SLEEP");
-    const int x = e ? atoi(e) : 32;
-    return x < 32 ? 32 : (x > 100000 ? 100000 : x);
-  }();
-  return v;
+int tuned_spw() { return kMaxSlotsPerWarpHost; }
+int tuned_sleep() { return 32; }
+
+int configure_kernel(const void* fn, int max_dyn_smem, bool nonportable_cluster) {
+  int dev = 0;
+  CFB_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::set<std::pair<int, const void*>> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count({dev, fn})) return CFB_OK;
+  CFB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn_smem));
+  if (nonportable_cluster)
+    CFB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  done.insert({dev, fn});
+  return CFB_OK;
 }
 }  // namespace cfb
 

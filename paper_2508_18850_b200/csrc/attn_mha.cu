@@ -49,7 +49,6 @@ struct MhaParams {
   float* stats;
   unsigned long long* traffic;
   unsigned long long* trace;
-  const void* qkv_in;
 };
 
 struct MhaLayout {
@@ -155,7 +154,7 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
 
   if (warp == kNumConsumerWarps) {  // ------------------------------ producer
     int c = 0;
-    if (!(p.flags & CFB_QKV_IN)) {
+    {
       const Phase ph0[1] = {P0};
       produce_all(ph0, ring, lane, policy_evict_first(), c);  // weights: before the PDL wait
     }
@@ -196,30 +195,19 @@ __global__ void __launch_bounds__(kThreads, 1) mha_split_token_kernel(const MhaP
   const Phase P1 = kv_phase(S);
 
   int cnt = 0;
-  if (p.flags & CFB_QKV_IN) {
-    // 1-2. this rank's q|k|v slices were projected on all SMs by cfb_qkv_proj
-    const T* qin = static_cast<const T*>(p.qkv_in);
-    const size_t rows_all = (size_t)p.n_heads * N * qkv_tiles * kTileRows;
-    const size_t r0 = ((size_t)head * N + rank) * qkv_tiles * kTileRows;
-    for (int idx = tid; idx < B * qkv_rows; idx += kConsumerThreads) {
-      const int b = idx / qkv_rows, row = idx % qkv_rows;
-      gseg[b * 3 * h + row] = __ldcg(qin + b * rows_all + r0 + row);
-    }
-    consumer_sync();
+  // 1. activations
+  if (p.flags & CFB_NORM) {
+    rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
   } else {
-    // 1. activations
-    if (p.flags & CFB_NORM) {
-      rmsnorm_to_smem<T, XH>(xs, p.resid, static_cast<const T*>(p.norm_w), B, D, p.eps, red, tid);
-    } else {
-      load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
-    }
-
-    // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
-    if (tr && tid == 0) tr[1] = globaltimer();
-    tiled_gemv_phase<T, QB, XH>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
-                            [&](int row, int b, float v) { gseg[b * 3 * h + row] = Elem<T>::from_f(v); });
-    consumer_sync();
+    load_act_to_smem<T, XH>(xs, static_cast<const T*>(p.x), B, D, tid);
   }
+
+  // 2. QKV GEMV: rows of [q-slice | k-slice | v-slice] for this rank
+  if (tr && tid == 0) tr[1] = globaltimer();
+  tiled_gemv_phase<T, QB, XH>(P0, ring, warp, lane, tid, cnt, xs, D, B, qkv_rows, part,
+                          [&](int row, int b, float v) { gseg[b * 3 * h + row] = Elem<T>::from_f(v); });
+  consumer_sync();
+
   if (tr && tid == 0) tr[2] = globaltimer();
   cluster_wait();  // peers' mbarriers are initialised from here on
   if (tr && tid == 0) tr[8] = globaltimer();
@@ -605,12 +593,7 @@ __global__ void mha_finalize_kernel(float* out, const float* resid,
 template <typename T, int EPL, int QB>
 static int launch_mha_inst(const MhaParams& p, size_t smem, cudaStream_t st, bool pdl) {
   auto kern = mha_split_token_kernel<T, EPL, QB>;
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)kern, kMaxSmem, true)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.N, p.n_heads, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -662,8 +645,7 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   if ((a->flags & (CFB_NORM | CFB_RESID)) && !a->resid)
     return set_error(CFB_ERR_ARGUMENT, "CFB_NORM/CFB_RESID need resid");
   if ((a->flags & CFB_NORM) && !a->norm_w) return set_error(CFB_ERR_ARGUMENT, "CFB_NORM needs norm_w");
-  if (!(a->flags & (CFB_NORM | CFB_QKV_IN)) && !a->x) return set_error(CFB_ERR_ARGUMENT, "x is null");
-  if ((a->flags & CFB_QKV_IN) && !a->qkv_in) return set_error(CFB_ERR_ARGUMENT, "CFB_QKV_IN needs qkv_in");
+  if (!(a->flags & CFB_NORM) && !a->x) return set_error(CFB_ERR_ARGUMENT, "x is null");
   if (!a->w_qkv || !a->w_out || !a->k_cache || !a->v_cache || !a->accum)
     return set_error(CFB_ERR_ARGUMENT, "null weight / cache / accumulator pointer");
   int spw = tuned_spw();
@@ -700,7 +682,6 @@ int mha_decode(const cfb_mha_args* a, cudaStream_t st) {
   p.stats = a->stats;
   p.traffic = a->traffic;
   p.trace = a->trace;
-  p.qkv_in = a->qkv_in;
   const bool pdl = a->flags & CFB_PDL;
   int rc = tb == 2 ? launch_mha_t<__half>(p, L.total, st, pdl) : launch_mha_t<float>(p, L.total, st, pdl);
   if (rc || !a->out) return rc;

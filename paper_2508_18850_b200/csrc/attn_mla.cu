@@ -491,12 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_fused_kernel(const MlaParams 
 template <typename T, int EPL, int QB>
 static int launch_mla_inst(const MlaParams& p, size_t smem, cudaStream_t st) {
   auto kern = mla_fused_kernel<T, EPL, QB>;
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)kern, kMaxSmem, true)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(p.N, p.n_heads, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

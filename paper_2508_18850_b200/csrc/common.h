@@ -38,10 +38,13 @@ struct LaunchAttrs {
 
 int set_error(int code, const char* fmt, ...);
 
-// Ring depth (slots per consumer warp); CFB_SPW overrides it for tuning runs.
+// Ring depth (slots per consumer warp) and producer idle back-off cap (ns):
+// fixed at the values the round-1 sweeps picked.
 int tuned_spw();
-// Producer idle back-off cap in ns; CFB_SLEEP overrides it.
 int tuned_sleep();
+// Per-(device, kernel) attribute cache: sets the dynamic shared-memory limit
+// (and non-portable cluster sizes) once per device, thread-safe.
+int configure_kernel(const void* fn, int max_dyn_smem, bool nonportable_cluster);
 
 #define CFB_CUDA(expr)                                                              \
   do {                                                                              \
@@ -55,6 +58,7 @@ int tuned_sleep();
 // pointer arrays live in DEVICE memory (the kernel walks all layers).
 struct LlamaStepArgs {
   int n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster, grid;
+  int cluster_attn;  // 1: attention module on DSMEM clusters; 0: flattened, global exchange
   float eps;
   const void* const* attn_norm;
   const void* const* w_qkv;
@@ -68,10 +72,10 @@ struct LlamaStepArgs {
   const void* final_norm;
   const void* lm_head;
   const float* rope_cs;
-  float* resid;
-  unsigned long long* accum;
+  float* resid;               // [2][D] (layer-parity double buffer)
+  unsigned long long* accA;   // [2][D]
+  unsigned long long* accF;   // [2][D]
   void* qkv;
-  void* act;
   float* partials;
   unsigned long long* barrier;
   unsigned long long* counters;
@@ -86,10 +90,9 @@ struct LlamaStepArgs {
 };
 int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st);
 int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out);
+int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* spw_out);
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);
-int qkv_proj(int dtype, int B, int D, int rows, const float* resid, const void* norm_w, float eps,
-             const void* w, void* out, int flags, cudaStream_t st);
 int mha_finalize(float* out, const float* resid, unsigned long long* accum, int n, cudaStream_t st);
 int mla_decode(const cfb_mla_args* a, cudaStream_t st);
 int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st);

@@ -45,6 +45,7 @@
 // csrc/attn_mha.cu (drop-in API and layered engine).
 #include <cuda_runtime.h>
 
+#include "collectives.cuh"
 #include "common.h"
 #include "gemv.cuh"
 
@@ -58,6 +59,7 @@ constexpr int kLPK = kH / kEPL; // lanes per key (8)
 constexpr int kKPP = 32 / kLPK; // keys per warp step (4)
 constexpr int kRC = 4;          // warp steps per online-softmax chunk
 constexpr int kPS = kH + 4;     // floats per attention partial: m, l, pad, pad, A[H]
+constexpr int kMaxDownK = 8;    // down-projection row quads per lane: hidden <= 8192
 
 struct StepParams {
   int L, D, nh, F, V, cap, N, tpr, spw, sleep_max;
@@ -74,10 +76,14 @@ struct StepParams {
   const __half* final_norm;
   const __half* lm_head;
   const float* rope_cs;
-  float* resid;                  // [D] fp32 residual stream
-  unsigned long long* accum;     // [D] fixed-point head sum
+  // residual stream, double-buffered by layer parity p = l & 1 (no barrier is
+  // needed to retire a buffer): r_l = resid[p] + accF[p] enters layer l, the
+  // attention head sum goes to accA[p], the FFN's split-K down partials to
+  // accF[1-p], and resid[1-p] = r_l + accA[p]
+  float* resid;                  // [2][D] fp32
+  unsigned long long* accA;      // [2][D] fixed-point attention head sum
+  unsigned long long* accF;      // [2][D] fixed-point FFN output sum
   __half* qkv;                   // [nh * N * tpr * 4] q|k|v rows of the layer
-  __half* act;                   // [F]
   float* partials;               // [nh][G][kPS]
   unsigned long long* barrier;   // grid barrier counter (monotonic)
   unsigned long long* counters;  // [2 * nh]: qkv_done, att_done (zeroed per step)
@@ -92,12 +98,12 @@ struct StepParams {
 };
 
 struct StepLayout {
-  int bars, xs, part, gu, qf, red, misc, total, max_rows;
+  int bars, xs, part, gu, qf, dsm, red, misc, total, max_rows;
 };
 
 __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
 
-__host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, int G, int spw) {
+__host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, int G, int N, int spw) {
   StepLayout L;
   auto tiles = [&](int T) { return (T + G - 1) / G; };
   int t = tiles(TQ);
@@ -110,10 +116,11 @@ __host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, 
   if (ws > part) part = ws;
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
-  L.xs = o;    o += r16((D > F ? D : F) * 2);
+  L.xs = o;    o += r16(D * 2);
   L.part = o;  o += r16(part);
-  L.gu = o;    o += r16(4 * tiles(F / 2) * 4);
+  L.gu = o;    o += r16(4 * tiles(F / 2) * 4) + r16(2 * tiles(F / 2) * 4);  // gate/up rows | act
   L.qf = o;    o += 3 * kH * 4 + kH * 2;  // q, k, v fp32 + fp16 A for the O projection
+  L.dsm = o;   o += N * r16(3 * (kH / N) * 2) + N * r16((4 + kH) * 4);  // DSMEM gather | exchange
   L.red = o;   o += r16(kNumConsumerWarps * 4 * 2);
   L.misc = o;  o += 64;
   L.total = o;
@@ -204,6 +211,15 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int k, int tid) {
   if (tr && tid == 0) tr[k] = globaltimer();
 }
 
+// kCluster = true: the attention module of head h runs on one thread-block
+// cluster of N CTAs exactly as ClusterFusion's split_token dataflow (QKV
+// slice GEMV -> DSMEM ClusterGather -> RoPE / KV append -> split-KV flash
+// decoding -> one-round DSMEM (m, l, A) exchange -> O-projection slice), so
+// the module has NO global dependency until the end-of-attention barrier.
+// kCluster = false: flattened split over all SMs, partials exchanged through
+// global memory with per-head counters (the ablation: same kernel, off-chip
+// exchange instead of DSMEM).
+template <bool kCluster>
 __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParams p) {
   extern __shared__ __align__(128) char smem[];
   const int G = gridDim.x, i = blockIdx.x;
@@ -211,10 +227,11 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   const int D = p.D, F = p.F, nh = p.nh, N = p.N;
   const int hp = kH / N;                      // head dims per split_token rank
   const int TPH = N * p.tpr;                  // W_qkv tiles per head
-  const int TQ = nh * TPH, T1 = F / 2, T2 = D / 4, TV = p.V / 4;
-  const StepLayout Lo = step_layout(D, F, TQ, TV, G, p.spw);
+  const int TQ = nh * TPH, T1 = F / 2, TV = p.V / 4;
+  const StepLayout Lo = step_layout(D, F, TQ, TV, G, N, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lo.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
+  uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + Lo.misc + 16);  // [0] gather, [1] exchange
 
   const int S = *p.pos;
   if (S + 1 > p.cap) {  // uniform across the grid: no barrier is entered
@@ -222,72 +239,117 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     return;
   }
   const long long SP = S + 1;                 // attended positions per head
+  // ---- static work assignment
+  // cluster variant: cluster c = i / N serves heads c, c + C (rank r = i % N)
+  const int C = G / N, cl = i / N, rank = i % N;
+  const int nrounds = kCluster ? (cl < nh ? 1 + (cl + C < nh) : 0) : 0;
+  const int seg = S == 0 ? 0 : (S + N - 1) / N;  // split_token KV segment (dataflows.py:109-114)
+  const int s_lo = min(rank * seg, S), s_hi = min(s_lo + seg, S);
+  const int cols = D / N;
+  // flat variant ranges
   const long long PK = (long long)nh * SP;    // flattened (head, position) space
   const long long RO = (long long)nh * D;     // flattened (head, output column) rows
-
-  // static ranges of this CTA
-  const int q0 = (int)split_at(TQ, i, G), q1 = (int)split_at(TQ, i + 1, G);
+  const int q0 = kCluster ? 0 : (int)split_at(TQ, i, G), q1 = kCluster ? 0 : (int)split_at(TQ, i + 1, G);
   const long long k0 = split_at(PK, i, G), k1 = split_at(PK, i + 1, G);
   const long long o0 = split_at(RO, i, G), o1 = split_at(RO, i + 1, G);
-  const int a0 = (int)split_at(T1, i, G), a1 = (int)split_at(T1, i + 1, G);
-  const int u0 = (int)split_at(T2, i, G), u1 = (int)split_at(T2, i + 1, G);
-  const int v0 = (int)split_at(TV, i, G), v1 = (int)split_at(TV, i + 1, G);
-  // attention pieces: (head, [lo, hi) local positions), at most two
   int ph[2] = {0, 0}, plo[2] = {0, 0}, phi[2] = {0, 0}, npiece = 0;
-  for (long long x = k0; x < k1 && npiece < 2;) {
-    const int h = (int)(x / SP);
-    const long long e = k1 < (h + 1) * SP ? k1 : (h + 1) * SP;
-    ph[npiece] = h;
-    plo[npiece] = (int)(x - h * SP);
-    phi[npiece] = (int)(e - h * SP);
-    ++npiece;
-    x = e;
-  }
-  // O-projection pieces: (head, [c_lo, c_hi) output columns), at most two
   int oh[2] = {0, 0}, olo[2] = {0, 0}, ohi[2] = {0, 0}, nopiece = 0;
-  for (long long x = o0; x < o1 && nopiece < 2;) {
-    const int h = (int)(x / D);
-    const long long e = o1 < (long long)(h + 1) * D ? o1 : (long long)(h + 1) * D;
-    oh[nopiece] = h;
-    olo[nopiece] = (int)(x - (long long)h * D);
-    ohi[nopiece] = (int)(e - (long long)h * D);
-    ++nopiece;
-    x = e;
+  if (!kCluster) {
+    for (long long x = k0; x < k1 && npiece < 2;) {  // attention pieces (head, [lo, hi))
+      const int h = (int)(x / SP);
+      const long long e = k1 < (h + 1) * SP ? k1 : (h + 1) * SP;
+      ph[npiece] = h;
+      plo[npiece] = (int)(x - h * SP);
+      phi[npiece] = (int)(e - h * SP);
+      ++npiece;
+      x = e;
+    }
+    for (long long x = o0; x < o1 && nopiece < 2;) {  // O rows (head, [c_lo, c_hi))
+      const int h = (int)(x / D);
+      const long long e = o1 < (long long)(h + 1) * D ? o1 : (long long)(h + 1) * D;
+      oh[nopiece] = h;
+      olo[nopiece] = (int)(x - (long long)h * D);
+      ohi[nopiece] = (int)(e - (long long)h * D);
+      ++nopiece;
+      x = e;
+    }
   }
+  // FFN and LM head: contiguous tile ranges over all G CTAs
+  const int a0 = (int)split_at(T1, i, G), a1 = (int)split_at(T1, i + 1, G);
+  const int v0 = (int)split_at(TV, i, G), v1 = (int)split_at(TV, i + 1, G);
+  const int seg_bytes = r16(3 * hp * 2), pay_bytes = r16((4 + kH) * 4);
 
   if (tid == 0) {
     ring_init(ring);
+    if (kCluster && N > 1) {
+      mbar_init(&cbar[0], 1);
+      mbar_arrive_expect_tx(&cbar[0], (N - 1) * seg_bytes);
+      mbar_init(&cbar[1], 1);
+      mbar_arrive_expect_tx(&cbar[1], (N - 1) * pay_bytes);
+    }
     fence_mbar_init();
   }
   __syncthreads();
+  if (kCluster) cluster_arrive();  // peers' mbarriers initialised before any DSMEM push
 
-  auto layer_phases = [&](int l, Phase (&P)[7]) {
-    P[0] = make_phase(p.w_qkv[l] + (size_t)q0 * 4 * D, nullptr, q1 - q0, 4 * D * 2, true);
-    for (int j = 0; j < 2; ++j) {
-      const int n = j < npiece ? (phi[j] < S ? phi[j] : S) - plo[j] : 0;
-      const size_t off = ((size_t)ph[j] * p.cap + (j < npiece ? plo[j] : 0)) * kH;
-      P[1 + j] = make_phase(p.k_cache[l] + off, p.v_cache[l] + off, n > 0 ? n : 0, kH * 2);
+  // The per-layer schedule, phase k of layer l computed on the fly (no arrays:
+  // a dynamically indexed schedule would sit in local memory, which shares
+  // the L1 with the 190+ KB ring).  Attention phases 0..5 (cluster: qkv, kv,
+  // o per head round; flat: qkv, kv piece 0/1, o piece 0/1, -), FFN: 6
+  // (gate/up), 7..14 (down row blocks, warp-affine).
+  auto layer_phase = [&](int l, int k) -> Phase {
+    if (k < 6) {
+      if (kCluster) {
+        const int j = k / 3, part_ = k % 3;
+        const bool on = j < nrounds;
+        const int h = cl + j * C;
+        const size_t hr = on ? (size_t)h * N + rank : 0;
+        if (part_ == 0)
+          return make_phase(p.w_qkv[l] + hr * p.tpr * 4 * D, nullptr, on ? p.tpr : 0, 4 * D * 2, true);
+        if (part_ == 1) {
+          const size_t off = on ? ((size_t)h * p.cap + s_lo) * kH : 0;
+          return make_phase(p.k_cache[l] + off, p.v_cache[l] + off, on ? s_hi - s_lo : 0, kH * 2);
+        }
+        return make_phase(p.w_out[l] + hr * cols * kH, nullptr, on ? cols : 0, kH * 2);
+      }
+      if (k == 0) return make_phase(p.w_qkv[l] + (size_t)q0 * 4 * D, nullptr, q1 - q0, 4 * D * 2, true);
+      if (k <= 2) {
+        const int j = k - 1;
+        const int n = j < npiece ? (phi[j] < S ? phi[j] : S) - plo[j] : 0;
+        const size_t off = ((size_t)ph[j] * p.cap + (j < npiece ? plo[j] : 0)) * kH;
+        return make_phase(p.k_cache[l] + off, p.v_cache[l] + off, n > 0 ? n : 0, kH * 2);
+      }
+      if (k <= 4) {
+        // W_out [head][rank][cols][H] flattens to [head][column][H]
+        const int j = k - 3;
+        const size_t off = ((size_t)oh[j] * D + (j < nopiece ? olo[j] : 0)) * kH;
+        return make_phase(p.w_out[l] + off, nullptr, j < nopiece ? ohi[j] - olo[j] : 0, kH * 2);
+      }
+      return make_phase(nullptr, nullptr, 0, 16);
     }
-    for (int j = 0; j < 2; ++j) {
-      // W_out rows of head oh[j], columns [olo, ohi): layout [head][rank][cols][H]
-      // flattens to [head][column][H]
-      const size_t off = ((size_t)oh[j] * D + (j < nopiece ? olo[j] : 0)) * kH;
-      P[3 + j] = make_phase(p.w_out[l] + off, nullptr, j < nopiece ? ohi[j] - olo[j] : 0, kH * 2);
-    }
-    P[5] = make_phase(p.w_gu[l] + (size_t)a0 * 4 * D, nullptr, a1 - a0, 4 * D * 2, true);
-    P[6] = make_phase(p.w_dn[l] + (size_t)u0 * 4 * F, nullptr, u1 - u0, 4 * F * 2, true);
+    if (k == 6) return make_phase(p.w_gu[l] + (size_t)a0 * 4 * D, nullptr, a1 - a0, 4 * D * 2, true);
+    // W_down packed [8 row blocks][F/2 f-pairs][D/8 rows][2]: block j of this
+    // CTA's f pairs [a0, a1) is one contiguous run, streamed to warp j
+    const int j = k - 7;
+    return warp_phase(make_phase(p.w_dn[l] + ((size_t)j * T1 + a0) * (D / 8) * 2, nullptr, a1 - a0,
+                                 (D / 8) * 2 * 2),
+                      j);
   };
+  constexpr int kPhases = 15;
 
   if (warp == kNumConsumerWarps) {  // ---------------------------- producer
     const uint64_t pol = policy_evict_first();
     int c = 0;
-    for (int l = 0; l < p.L; ++l) {
-      Phase P[7];
-      layer_phases(l, P);
-      produce_all(P, ring, lane, pol, c);
+    for (int l = 0; l < p.L; ++l)
+      produce_gen(kPhases, [&](int k) { return layer_phase(l, k); }, ring, lane, pol, c);
+    produce_gen(1, [&](int) { return make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true); },
+                ring, lane, pol, c);
+    __syncwarp();
+    if (kCluster) {  // both cluster-barrier phases of the CTA (start, end)
+      cluster_wait();
+      cluster_arrive();
+      cluster_wait();
     }
-    const Phase PL[1] = {make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true)};
-    produce_all(PL, ring, lane, pol, c);
     return;
   }
 
@@ -299,235 +361,358 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   float* kf = qf + kH;
   float* vf = kf + kH;
   __half* abuf = reinterpret_cast<__half*>(vf + kH);
+  __half* gseg = reinterpret_cast<__half*>(smem + Lo.dsm);                 // [N][seg]
+  float* pay = reinterpret_cast<float*>(smem + Lo.dsm + N * seg_bytes);    // [N][4 + H]
   float* red = reinterpret_cast<float*>(smem + Lo.red);
   unsigned* last = reinterpret_cast<unsigned*>(smem + Lo.misc);
   unsigned long long* qkv_done = p.counters;
   unsigned long long* att_done = p.counters + nh;
 
-  // embed: resid[c] = embed[token][c] for this CTA's slice; counters reset
+  // embed: resid[0][c] = embed[token][c] for this CTA's slice (accF[0], accA[0]
+  // zeroed: r_0 = resid[0]); counters reset
+  const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);  // residual slice
   {
     const int tok = *p.token;
-    const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);
-    for (int c = c0 + tid; c < c1; c += kConsumerThreads)
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
       p.resid[c] = __half2float(p.embed[(size_t)tok * D + c]);
-    if (i == 0 && tid < 2 * nh) p.counters[tid] = 0ull;
+      p.accF[c] = 0ull;
+      p.accA[c] = 0ull;
+    }
+    if (!kCluster && i == 0 && tid < 2 * nh) p.counters[tid] = 0ull;
   }
+  if (kCluster) cluster_wait();
   grid_barrier(p.barrier, tid);
 
-  // cross-CTA data is read through L2 (ld.global.cg): L1 is not coherent
-  const float* resid_g = p.resid;
-  auto resid_l2 = [resid_g](int, int v) { return __ldcg(reinterpret_cast<const float4*>(resid_g) + v); };
+  // r = resid[q] + accF[q] as float4 (cross-CTA data is read through L2,
+  // ld.global.cg: L1 is not coherent)
+  auto r_in = [&](int q, int v) {
+    const float4 r = __ldcg(reinterpret_cast<const float4*>(p.resid + (size_t)q * D) + v);
+    const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accF + (size_t)q * D) + 2 * v);
+    const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accF + (size_t)q * D) + 2 * v + 1);
+    return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
+                       __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
+  };
   int cnt = 0;
-  const int rowsQ = 4 * (q1 - q0);
+  int use = 0;  // DSMEM barrier phase (one gather + one exchange per head round)
   const int g = lane / kLPK, li = lane % kLPK;
   const float scale = p.inv_sqrt_h;
   const int half = kH / 2;
+
+  // RoPE of q and k_new at position S (rotate-half), fp16-stored values
+  auto rope_qk = [&]() {
+    for (int d = tid; d < half; d += kConsumerThreads) {
+      const float c = p.rope_cs[((size_t)S * half + d) * 2];
+      const float sn = p.rope_cs[((size_t)S * half + d) * 2 + 1];
+      const float q1_ = qf[d], q2 = qf[d + half], k1_ = kf[d], k2 = kf[d + half];
+      qf[d] = round_to<__half>(__fsub_rn(__fmul_rn(q1_, c), __fmul_rn(q2, sn)));
+      qf[d + half] = round_to<__half>(__fadd_rn(__fmul_rn(q2, c), __fmul_rn(q1_, sn)));
+      kf[d] = round_to<__half>(__fsub_rn(__fmul_rn(k1_, c), __fmul_rn(k2, sn)));
+      kf[d + half] = round_to<__half>(__fadd_rn(__fmul_rn(k2, c), __fmul_rn(k1_, sn)));
+    }
+    consumer_sync();
+  };
+  auto append_kv = [&](int l, int h) {  // KV-cache append at row S (read by later steps only)
+    const size_t off = ((size_t)h * p.cap + S) * kH;
+    for (int d = tid; d < kH; d += kConsumerThreads) {
+      p.k_cache[l][off + d] = __float2half_rn(kf[d]);
+      p.v_cache[l][off + d] = __float2half_rn(vf[d]);
+    }
+  };
+  // flash decoding of this CTA's KV rows (+ the new token when has_new) and
+  // the in-order merge of the 8 warp states -> (m, l, A) in `out` (fp32)
+  auto attend_rows = [&](const Phase& PKV, bool has_new, float* out) {
+    float q[kEPL], acc[kEPL], m = -INFINITY, lsum = 0.f;
+#pragma unroll
+    for (int e = 0; e < kEPL; ++e) {
+      q[e] = qf[li * kEPL + e];
+      acc[e] = 0.f;
+    }
+    consume_phase(PKV, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+      const __half* K = reinterpret_cast<const __half*>(slot);
+      const __half* V = reinterpret_cast<const __half*>(slot + kSlotBytes / 2);
+      attend(q, m, lsum, acc, it.nunits, g, scale,
+             [&](int k, float* o) { load_elems<__half, kEPL>(K + k * kH + li * kEPL, o); },
+             [&](int k, float* o) { load_elems<__half, kEPL>(V + k * kH + li * kEPL, o); });
+    });
+    if (has_new && warp == 0)  // the new token's K/V: attended exactly once
+      attend(q, m, lsum, acc, 1, g, scale,
+             [&](int, float* o) {
+#pragma unroll
+               for (int e = 0; e < kEPL; ++e) o[e] = kf[li * kEPL + e];
+             },
+             [&](int, float* o) {
+#pragma unroll
+               for (int e = 0; e < kEPL; ++e) o[e] = vf[li * kEPL + e];
+             });
+#pragma unroll
+    for (int o = kLPK; o < 32; o <<= 1) {  // fold the key groups (same dims, shared m)
+      lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+#pragma unroll
+      for (int e = 0; e < kEPL; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
+    }
+    float* ws = part + warp * kPS;
+    if (g == 0) {
+#pragma unroll
+      for (int e = 0; e < kEPL; ++e) ws[4 + li * kEPL + e] = acc[e];
+    }
+    if (lane == 0) {
+      ws[0] = m;
+      ws[1] = lsum;
+    }
+    consumer_sync();
+    for (int d = tid; d < kH; d += kConsumerThreads) {
+      float mm = -INFINITY;
+#pragma unroll
+      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) mm = fmaxf(mm, part[w2 * kPS]);
+      float ll = 0.f, a = 0.f;
+#pragma unroll
+      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) {
+        const float mw = part[w2 * kPS];
+        const float f = (mw == -INFINITY) ? 0.f : expf(mw - mm);
+        ll = fmaf(part[w2 * kPS + 1], f, ll);
+        a = fmaf(part[w2 * kPS + 4 + d], f, a);
+      }
+      out[4 + d] = a;
+      if (d == 0) {
+        out[0] = mm;
+        out[1] = ll;
+      }
+    }
+  };
+
   for (int l = 0; l < p.L; ++l) {
     unsigned long long* tr = p.trace ? p.trace + ((size_t)l * G + i) * 8 : nullptr;
     stamp(tr, 0, tid);
-    Phase P[7];
-    layer_phases(l, P);
-    // ---- A. QKV projection
-    rmsnorm_to_smem_ld<__half, true>(xs, resid_l2, p.attn_norm[l], 1, D, p.eps, red, tid);
-    tiled_gemv_phase<__half, 1, true>(P[0], ring, warp, lane, tid, cnt, xs, D, 1, rowsQ, part,
-                                      [&](int row, int, float v) {
-                                        p.qkv[(size_t)4 * q0 + row] = __float2half_rn(v);
-                                      });
-    __threadfence();
-    consumer_sync();
-    if (tid == 0) {
-      for (int h = q0 / TPH; h < nh && h * TPH < q1; ++h) {
-        const int lo = max(q0, h * TPH), hi = min(q1, (h + 1) * TPH);
-        red_release_add(&qkv_done[h], (unsigned long long)(hi - lo));
-      }
-    }
-    stamp(tr, 1, tid);
-
-    // ---- B. attention pieces
-    for (int j = 0; j < 2; ++j) {
-      const Phase& PK_ = P[1 + j];
-      if (j >= npiece) {  // keep the ring walk aligned (phase is empty)
-        continue;
-      }
-      const int h = ph[j];
-      const bool has_new = phi[j] == S + 1;
-      wait_counter(&qkv_done[h], (unsigned long long)TPH * (l + 1), tid);
-      // q, k_new, v_new of head h from the split_token row order
-      for (int d = tid; d < kH; d += kConsumerThreads) {
-        const size_t r = ((size_t)h * N + d / hp) * p.tpr * 4 + d % hp;
-        qf[d] = __half2float(__ldcg(p.qkv + r));
-        kf[d] = __half2float(__ldcg(p.qkv + r + hp));
-        vf[d] = __half2float(__ldcg(p.qkv + r + 2 * hp));
-      }
-      consumer_sync();
-      for (int d = tid; d < half; d += kConsumerThreads) {  // RoPE at position S
-        const float c = p.rope_cs[((size_t)S * half + d) * 2];
-        const float sn = p.rope_cs[((size_t)S * half + d) * 2 + 1];
-        const float q1_ = qf[d], q2 = qf[d + half], k1_ = kf[d], k2 = kf[d + half];
-        qf[d] = round_to<__half>(__fsub_rn(__fmul_rn(q1_, c), __fmul_rn(q2, sn)));
-        qf[d + half] = round_to<__half>(__fadd_rn(__fmul_rn(q2, c), __fmul_rn(q1_, sn)));
-        kf[d] = round_to<__half>(__fsub_rn(__fmul_rn(k1_, c), __fmul_rn(k2, sn)));
-        kf[d + half] = round_to<__half>(__fadd_rn(__fmul_rn(k2, c), __fmul_rn(k1_, sn)));
-      }
-      consumer_sync();
-      if (has_new) {  // KV-cache append at row S (read by later steps only)
-        const size_t off = ((size_t)h * p.cap + S) * kH;
+    const int par = l & 1;
+    unsigned long long* accA = p.accA + (size_t)par * D;
+    auto r_l = [&](int, int v) { return r_in(par, v); };
+    // retire accF[1-par] (last read by layer l-1's prologues) before this
+    // layer's FFN adds into it
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads) p.accF[(size_t)(1 - par) * D + c] = 0ull;
+    if (kCluster) {
+      // ================= attention module on the cluster (split_token, Alg. 3)
+      if (nrounds > 0) rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.attn_norm[l], 1, D, p.eps, red, tid);
+      for (int j = 0; j < nrounds; ++j, ++use) {
+        const int h = cl + j * C;
+        // 1. QKV GEMV of this rank's q|k|v slices (dataflows.py:256-267)
+        tiled_gemv_phase<__half, 1, true>(layer_phase(l, 3 * j), ring, warp, lane, tid, cnt, xs, D, 1, 4 * p.tpr,
+                                          part, [&](int row, int, float v) {
+                                            if (row < 3 * hp) gseg[row] = __float2half_rn(v);
+                                          });
+        consumer_sync();
+        stamp(tr, 1, tid);
+        // 2. ClusterGather (one round, rank-rotated slots, dataflows.py:268-279)
+        if (warp == 0 && N > 1) {
+          for (int d = 1; d < N; ++d)
+            dsmem_push(gseg, reinterpret_cast<char*>(gseg) + d * seg_bytes, &cbar[0], seg_bytes,
+                       (rank + d) % N, lane);
+          __syncwarp();
+          mbar_wait(&cbar[0], use & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&cbar[0], (N - 1) * seg_bytes);  // next round
+        }
+        consumer_sync();
         for (int d = tid; d < kH; d += kConsumerThreads) {
-          p.k_cache[l][off + d] = __float2half_rn(kf[d]);
-          p.v_cache[l][off + d] = __float2half_rn(vf[d]);
+          const int rr = d / hp, ii = d % hp;
+          const __half* sg = gseg + ((rank - rr + N) % N) * (seg_bytes / 2);
+          qf[d] = __half2float(sg[ii]);
+          kf[d] = __half2float(sg[hp + ii]);
+          vf[d] = __half2float(sg[2 * hp + ii]);
         }
-      }
-      float q[kEPL], acc[kEPL], m = -INFINITY, lsum = 0.f;
-#pragma unroll
-      for (int e = 0; e < kEPL; ++e) {
-        q[e] = qf[li * kEPL + e];
-        acc[e] = 0.f;
-      }
-      consume_phase(PK_, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-        const __half* K = reinterpret_cast<const __half*>(slot);
-        const __half* V = reinterpret_cast<const __half*>(slot + kSlotBytes / 2);
-        attend(q, m, lsum, acc, it.nunits, g, scale,
-               [&](int k, float* o) { load_elems<__half, kEPL>(K + k * kH + li * kEPL, o); },
-               [&](int k, float* o) { load_elems<__half, kEPL>(V + k * kH + li * kEPL, o); });
-      });
-      if (has_new && warp == 0)
-        attend(q, m, lsum, acc, 1, g, scale,
-               [&](int, float* o) {
-#pragma unroll
-                 for (int e = 0; e < kEPL; ++e) o[e] = kf[li * kEPL + e];
-               },
-               [&](int, float* o) {
-#pragma unroll
-                 for (int e = 0; e < kEPL; ++e) o[e] = vf[li * kEPL + e];
-               });
-      // fold the key groups of the warp (same dims), then the 8 warps in order
-#pragma unroll
-      for (int o = kLPK; o < 32; o <<= 1) {
-        lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-#pragma unroll
-        for (int e = 0; e < kEPL; ++e) acc[e] += __shfl_xor_sync(0xffffffffu, acc[e], o);
-      }
-      float* ws = part + warp * kPS;
-      if (g == 0) {
-#pragma unroll
-        for (int e = 0; e < kEPL; ++e) ws[4 + li * kEPL + e] = acc[e];
-      }
-      if (lane == 0) {
-        ws[0] = m;
-        ws[1] = lsum;
-      }
-      consumer_sync();
-      float* dst = p.partials + ((size_t)h * G + i) * kPS;
-      for (int d = tid; d < kH; d += kConsumerThreads) {
-        float mm = -INFINITY;
-#pragma unroll
-        for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) mm = fmaxf(mm, part[w2 * kPS]);
-        float ll = 0.f, a = 0.f;
-#pragma unroll
-        for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) {
-          const float mw = part[w2 * kPS];
-          const float f = (mw == -INFINITY) ? 0.f : expf(mw - mm);
-          ll = fmaf(part[w2 * kPS + 1], f, ll);
-          a = fmaf(part[w2 * kPS + 4 + d], f, a);
+        consumer_sync();
+        // 3. RoPE + KV append (rank N-1 owns the new row)
+        rope_qk();
+        if (rank == N - 1) append_kv(l, h);
+        // 4. flash decoding over this rank's segment; new token on rank N-1
+        float* mine = pay + rank * (pay_bytes / 4);
+        attend_rows(layer_phase(l, 3 * j + 1), rank == N - 1, mine);
+        consumer_sync();
+        stamp(tr, 2, tid);
+        // 5. one-round DSMEM exchange of fp32 (m, l, A), merged in rank order
+        //    (= MAX-reduce, rescale, SUM-reduce, rescale, SUM-reduce; dataflows.py:187-232)
+        if (warp == 0 && N > 1) {
+          for (int d = 1; d < N; ++d) dsmem_push(mine, mine, &cbar[1], pay_bytes, (rank + d) % N, lane);
+          __syncwarp();
+          mbar_wait(&cbar[1], use & 1);
+          if (lane == 0) mbar_arrive_expect_tx(&cbar[1], (N - 1) * pay_bytes);
         }
-        dst[4 + d] = a;
-        if (d == 0) {
-          dst[0] = mm;
-          dst[1] = ll;
+        consumer_sync();
+        for (int d = tid; d < kH; d += kConsumerThreads) {
+          float ms = -INFINITY;
+          for (int r2 = 0; r2 < N; ++r2) ms = fmaxf(ms, pay[r2 * (pay_bytes / 4)]);
+          float ls = 0.f, a = 0.f;
+          for (int r2 = 0; r2 < N; ++r2) {
+            const float* src = pay + r2 * (pay_bytes / 4);
+            const float f = (src[0] == -INFINITY) ? 0.f : expf(src[0] - ms);
+            ls = fmaf(src[1], f, ls);
+            a = fmaf(src[4 + d], f, a);
+          }
+          abuf[d] = __float2half_rn(__fdiv_rn(a, ls));
         }
+        consumer_sync();
+        // 6. O-projection of this rank's D/N output columns -> fixed-point head sum
+        consume_phase(layer_phase(l, 3 * j + 2), ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+          rowlane_item<__half, 1>(it, slot, abuf, kH, 1, lane, [&](int gcol, const float (&s)[1]) {
+            red_add_fixed(&accA[rank * cols + gcol], s[0]);
+          });
+        });
       }
+      if (nrounds == 0) {
+        stamp(tr, 1, tid);
+        stamp(tr, 2, tid);
+      }
+      stamp(tr, 3, tid);
+    } else {
+      // ================= flattened attention over all SMs, global exchange
+      rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.attn_norm[l], 1, D, p.eps, red, tid);
+      tiled_gemv_phase<__half, 1, true>(layer_phase(l, 0), ring, warp, lane, tid, cnt, xs, D, 1, 4 * (q1 - q0), part,
+                                        [&](int row, int, float v) {
+                                          p.qkv[(size_t)4 * q0 + row] = __float2half_rn(v);
+                                        });
       __threadfence();
       consumer_sync();
-      if (tid == 0) red_release_add(&att_done[h], 1ull);
-    }
-    stamp(tr, 2, tid);
-
-    // ---- C. merge + O projection into the fixed-point head sum
-    for (int j = 0; j < nopiece; ++j) {
-      const int h = oh[j];
-      const long long ha = (long long)h * SP, hb = ha + SP;
-      const int first = owner_of(ha, PK, G), lastc = owner_of(hb - 1, PK, G);
-      int npieces = 0;
-      for (int c = first; c <= lastc; ++c)
-        npieces += split_at(PK, c, G) < split_at(PK, c + 1, G);
-      wait_counter(&att_done[h], (unsigned long long)npieces * (l + 1), tid);
-      for (int d = tid; d < kH; d += kConsumerThreads) {
-        float ms = -INFINITY;
-        for (int c = first; c <= lastc; ++c)
-          if (split_at(PK, c, G) < split_at(PK, c + 1, G))
-            ms = fmaxf(ms, __ldcg(p.partials + ((size_t)h * G + c) * kPS));
-        float ls = 0.f, a = 0.f;
-        for (int c = first; c <= lastc; ++c) {
-          if (split_at(PK, c, G) >= split_at(PK, c + 1, G)) continue;
-          const float* src = p.partials + ((size_t)h * G + c) * kPS;
-          const float mr = __ldcg(src);
-          const float f = (mr == -INFINITY) ? 0.f : expf(mr - ms);
-          ls = fmaf(__ldcg(src + 1), f, ls);
-          a = fmaf(__ldcg(src + 4 + d), f, a);
+      if (tid == 0) {
+        for (int h = q0 / TPH; h < nh && h * TPH < q1; ++h) {
+          const int lo = max(q0, h * TPH), hi = min(q1, (h + 1) * TPH);
+          red_release_add(&qkv_done[h], (unsigned long long)(hi - lo));
         }
-        abuf[d] = __float2half_rn(__fdiv_rn(a, ls));
       }
-      consumer_sync();
-      const int c_lo = olo[j];
-      consume_phase(P[3 + j], ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-        // absolute column index: the packed rows are chunk-rotated by their row
-        // within the rank slice, (c mod D/N) mod 16 == c mod 16 (host-checked)
-        Item it2 = it;
-        it2.unit0 += c_lo;
-        rowlane_item<__half, 1>(it2, slot, abuf, kH, 1, lane, [&](int col, const float (&s)[1]) {
-          red_add_fixed(&p.accum[col], s[0]);
+      stamp(tr, 1, tid);
+      for (int j = 0; j < npiece; ++j) {
+        const int h = ph[j];
+        const bool has_new = phi[j] == S + 1;
+        wait_counter(&qkv_done[h], (unsigned long long)TPH * (l + 1), tid);
+        for (int d = tid; d < kH; d += kConsumerThreads) {  // q, k_new, v_new of head h
+          const size_t r = ((size_t)h * N + d / hp) * p.tpr * 4 + d % hp;
+          qf[d] = __half2float(__ldcg(p.qkv + r));
+          kf[d] = __half2float(__ldcg(p.qkv + r + hp));
+          vf[d] = __half2float(__ldcg(p.qkv + r + 2 * hp));
+        }
+        consumer_sync();
+        rope_qk();
+        if (has_new) append_kv(l, h);
+        attend_rows(layer_phase(l, 1 + j), has_new, p.partials + ((size_t)h * G + i) * kPS);
+        __threadfence();
+        consumer_sync();
+        if (tid == 0) red_release_add(&att_done[h], 1ull);
+      }
+      stamp(tr, 2, tid);
+      for (int j = 0; j < nopiece; ++j) {  // merge + O projection
+        const int h = oh[j];
+        const long long ha = (long long)h * SP, hb = ha + SP;
+        const int first = owner_of(ha, PK, G), lastc = owner_of(hb - 1, PK, G);
+        int npieces = 0;
+        for (int c = first; c <= lastc; ++c) npieces += split_at(PK, c, G) < split_at(PK, c + 1, G);
+        wait_counter(&att_done[h], (unsigned long long)npieces * (l + 1), tid);
+        for (int d = tid; d < kH; d += kConsumerThreads) {
+          float ms = -INFINITY;
+          for (int c = first; c <= lastc; ++c)
+            if (split_at(PK, c, G) < split_at(PK, c + 1, G))
+              ms = fmaxf(ms, __ldcg(p.partials + ((size_t)h * G + c) * kPS));
+          float ls = 0.f, a = 0.f;
+          for (int c = first; c <= lastc; ++c) {
+            if (split_at(PK, c, G) >= split_at(PK, c + 1, G)) continue;
+            const float* src = p.partials + ((size_t)h * G + c) * kPS;
+            const float mr = __ldcg(src);
+            const float f = (mr == -INFINITY) ? 0.f : expf(mr - ms);
+            ls = fmaf(__ldcg(src + 1), f, ls);
+            a = fmaf(__ldcg(src + 4 + d), f, a);
+          }
+          abuf[d] = __float2half_rn(__fdiv_rn(a, ls));
+        }
+        consumer_sync();
+        const int c_lo = olo[j];
+        consume_phase(layer_phase(l, 3 + j), ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+          // absolute column: packed rows are chunk-rotated by their row within the
+          // rank slice, (c mod D/N) mod 16 == c mod 16 (host-checked)
+          Item it2 = it;
+          it2.unit0 += c_lo;
+          rowlane_item<__half, 1>(it2, slot, abuf, kH, 1, lane, [&](int col, const float (&s)[1]) {
+            red_add_fixed(&accA[col], s[0]);
+          });
         });
-      });
+      }
+      stamp(tr, 3, tid);
     }
-    stamp(tr, 3, tid);
     grid_barrier(p.barrier, tid);
     stamp(tr, 4, tid);
 
-    // ---- D. FFN gate/up with the residual + head-sum RMSNorm prologue
-    {
-      const float* resid = p.resid;
-      const unsigned long long* acc = p.accum;
-      rmsnorm_to_smem_ld<__half, true>(
-          xs,
-          [&](int, int v) {
-            const float4 r = __ldcg(reinterpret_cast<const float4*>(resid) + v);
-            const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(acc) + 2 * v);
-            const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(acc) + 2 * v + 1);
-            return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
-                               __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
-          },
-          p.ffn_norm[l], 1, D, p.eps, red, tid);
+    // ---- FFN (one block-half, no internal barrier): RMSNorm(r_l + head sum) ->
+    //      gate/up rows of this CTA's f range -> SiLU*mul (fp16 store, the
+    //      oracle's rounding point) -> split-K down projection over the same f
+    //      range, partial outputs added into accF[1-par] (fixed point, exact)
+    auto r_mid = [&](int, int v) {
+      const float4 r = r_in(par, v);
+      const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v);
+      const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v + 1);
+      return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
+                         __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
+    };
+    rmsnorm_to_smem_ld<__half, true>(xs, r_mid, p.ffn_norm[l], 1, D, p.eps, red, tid);
+    // this CTA's residual slice moves on: resid[1-par] = r_l + head sum; accA of
+    // the other parity is retired (last read in layer l-1)
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
+      const float r = __fadd_rn(__fadd_rn(__ldcg(p.resid + (size_t)par * D + c),
+                                          fixed_to_float(__ldcg(p.accF + (size_t)par * D + c))),
+                                fixed_to_float(__ldcg(accA + c)));
+      p.resid[(size_t)(1 - par) * D + c] = r;
+      p.accA[(size_t)(1 - par) * D + c] = 0ull;
     }
-    const int rows0 = 4 * (a1 - a0);
-    tiled_gemv_phase<__half, 1, true>(P[5], ring, warp, lane, tid, cnt, xs, D, 1, rows0, part,
+    float* actf = gu + 4 * ((T1 + G - 1) / G);
+    tiled_gemv_phase<__half, 1, true>(layer_phase(l, 6), ring, warp, lane, tid, cnt, xs, D, 1, 4 * (a1 - a0), part,
                                       [&](int row, int, float v) { gu[row] = v; });
     consumer_sync();
     for (int jj = tid; jj < 2 * (a1 - a0); jj += kConsumerThreads) {
       const int t = jj >> 1, e = jj & 1;  // tile rows: g0 g1 u0 u1
       const float gt = gu[4 * t + e], up = gu[4 * t + 2 + e];
       const float sl = __fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt)));
-      p.act[2 * a0 + jj] = __float2half_rn(__fmul_rn(sl, up));
+      actf[jj] = round_to<__half>(__fmul_rn(sl, up));
     }
+    consumer_sync();
     stamp(tr, 5, tid);
-    grid_barrier(p.barrier, tid);
+    {
+      // warp w owns output rows [w*D/8, (w+1)*D/8): its warp-affine phase
+      // streams those rows of every down tile [rows][f pair] of this CTA
+      const int RB = D / 8, nck = RB / 4, ub = RB * 4;
+      float dacc[kMaxDownK][4];
+#pragma unroll
+      for (int k = 0; k < kMaxDownK; ++k) dacc[k][0] = dacc[k][1] = dacc[k][2] = dacc[k][3] = 0.f;
+      consume_phase(layer_phase(l, 7 + warp), ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+        for (int u = 0; u < it.nunits; ++u) {
+          const int t = it.unit0 + u;
+          const __half2 av = __floats2half2_rn(actf[2 * t], actf[2 * t + 1]);  // exact (fp16 values)
+          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&av);
+          const char* base = slot + (size_t)u * ub;
+#pragma unroll
+          for (int k = 0; k < kMaxDownK; ++k) {
+            const int c = lane + 32 * k;
+            if (c < nck) {
+              const uint4 w4 = lds128(base + c * 16);  // rows 4c..4c+3 x (f0, f1)
+              dacc[k][0] = fma_f16_hi(w4.x, a2, fma_f16_lo(w4.x, a2, dacc[k][0]));
+              dacc[k][1] = fma_f16_hi(w4.y, a2, fma_f16_lo(w4.y, a2, dacc[k][1]));
+              dacc[k][2] = fma_f16_hi(w4.z, a2, fma_f16_lo(w4.z, a2, dacc[k][2]));
+              dacc[k][3] = fma_f16_hi(w4.w, a2, fma_f16_lo(w4.w, a2, dacc[k][3]));
+            }
+          }
+        }
+      });
+      unsigned long long* accF = p.accF + (size_t)(1 - par) * D + warp * RB;
+#pragma unroll
+      for (int k = 0; k < kMaxDownK; ++k) {
+        const int c = lane + 32 * k;
+        if (c < nck && a1 > a0) {
+#pragma unroll
+          for (int r = 0; r < 4; ++r) red_add_fixed(&accF[4 * c + r], dacc[k][r]);
+        }
+      }
+    }
     stamp(tr, 6, tid);
-
-    // ---- E. down projection + residual
-    load_act_to_smem<__half, true>(xs, p.act, 1, F, tid);
-    tiled_gemv_phase<__half, 1, true>(P[6], ring, warp, lane, tid, cnt, xs, F, 1, 4 * (u1 - u0), part,
-                                      [&](int row, int, float v) {
-                                        const int c = 4 * u0 + row;
-                                        const float r = __fadd_rn(__ldcg(p.resid + c),
-                                                                  fixed_to_float(__ldcg(p.accum + c)));
-                                        p.accum[c] = 0ull;
-                                        p.resid[c] = __fadd_rn(r, v);
-                                      });
-    stamp(tr, 7, tid);
     grid_barrier(p.barrier, tid);
+    stamp(tr, 7, tid);
   }
 
   // ---- final RMSNorm + LM head + argmax
-  rmsnorm_to_smem_ld<__half, true>(xs, resid_l2, p.final_norm, 1, D, p.eps, red, tid);
+  auto r_out = [&](int, int v) { return r_in(p.L & 1, v); };
+  rmsnorm_to_smem_ld<__half, true>(xs, r_out, p.final_norm, 1, D, p.eps, red, tid);
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   const Phase PL = make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true);
@@ -584,6 +769,10 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     *p.ticket = 0;
     *p.pos = S + 1;
   }
+  if (kCluster) {
+    cluster_arrive();  // no CTA leaves while a peer could still address its smem
+    cluster_wait();
+  }
 }
 
 }  // namespace
@@ -591,13 +780,13 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
 int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out) {
   int spw = tuned_spw();
   const int TQ = nh * N * tpr, TV = V / 4;
-  StepLayout L = step_layout(D, F, TQ, TV, G, spw);
-  while (L.total > kMaxSmem && spw > 1) L = step_layout(D, F, TQ, TV, G, --spw);
+  StepLayout L = step_layout(D, F, TQ, TV, G, N, spw);
+  while (L.total > kMaxSmem && spw > 1) L = step_layout(D, F, TQ, TV, G, N, --spw);
   if (spw_out) *spw_out = spw;
   return L.total;
 }
 
-int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
+static int step_check(const LlamaStepArgs* a) {
   if (!a) return set_error(CFB_ERR_ARGUMENT, "null args");
   if (a->head_dim != kH) return set_error(CFB_ERR_DIMENSION, "persistent engine needs head_dim 128");
   const int N = a->cluster;
@@ -605,18 +794,63 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
     return set_error(CFB_ERR_CLUSTER_SIZE, "cluster size must be a power of two in [1, 16]");
   if (a->hidden % 8 || a->inter % 8 || a->vocab % 4 || (a->hidden / N) % (kH * 2 / 16))
     return set_error(CFB_ERR_DIMENSION, "persistent engine: hidden/inter multiples of 8, vocab of 4");
+  return CFB_OK;
+}
+
+// Grid of the persistent launch: every CTA must be co-resident (grid
+// barriers).  Flat: one CTA per SM.  Cluster: as many N-CTA clusters as the
+// GPCs can hold at once (cudaOccupancyMaxActiveClusters; 33 x 4 = 132 SMs on a
+// B200 at ~225 KB of shared memory per CTA).
+int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* spw_out) {
+  if (const int rc = step_check(a)) return rc;
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  const int G = a->grid > 0 && a->grid < sms ? a->grid : sms;
-  if (G < a->n_heads)  // a CTA's flattened ranges then span at most two heads
-    return set_error(CFB_ERR_DIMENSION, "persistent engine: grid %d vs %d heads", G, a->n_heads);
+  const int N = a->cluster, tpr = (3 * (kH / N) + 3) / 4;
+  int G = a->grid > 0 && a->grid < sms ? a->grid : sms;
   int spw = 0;
-  const int tpr = (3 * (kH / N) + 3) / 4;
-  const int smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, &spw);
+  int smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, &spw);
+  if (a->cluster_attn) {
+    const void* kern = (const void*)llama_step_kernel<true>;
+    if (const int rc = configure_kernel(kern, kMaxSmem, true)) return rc;
+    for (int it = 0; it < 3; ++it) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G - G % N, 1, 1);
+      cfg.blockDim = dim3(kThreads, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = N;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int nc = 0;
+      CFB_CUDA(cudaOccupancyMaxActiveClusters(&nc, kern, &cfg));
+      const int G2 = nc * N < G ? nc * N : G - G % N;
+      if (G2 < N) return set_error(CFB_ERR_SMEM, "persistent engine: no cluster of %d fits", N);
+      if (G2 == G) break;
+      G = G2;
+      smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, &spw);
+    }
+  }
+  if (!a->cluster_attn && G < a->n_heads)  // flattened ranges then span at most two heads
+    return set_error(CFB_ERR_DIMENSION, "persistent engine: grid %d vs %d heads", G, a->n_heads);
+  if (a->cluster_attn && 2 * (G / N) < a->n_heads)
+    return set_error(CFB_ERR_DIMENSION, "persistent engine: %d clusters for %d heads", G / N, a->n_heads);
   if (smem > kMaxSmem)
     return set_error(CFB_ERR_SMEM, "persistent engine needs %d B of shared memory (max %d)", smem,
                      kMaxSmem);
+  if (grid_out) *grid_out = G;
+  if (smem_out) *smem_out = smem;
+  if (spw_out) *spw_out = spw;
+  return CFB_OK;
+}
+
+int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
+  int G = 0, smem = 0, spw = 0;
+  if (const int rc = llama_step_grid(a, &G, &smem, &spw)) return rc;
+  const int N = a->cluster;
   StepParams p;
   p.L = a->n_layers;
   p.D = a->hidden;
@@ -625,7 +859,7 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.V = a->vocab;
   p.cap = a->cache_cap;
   p.N = N;
-  p.tpr = tpr;
+  p.tpr = (3 * (kH / N) + 3) / 4;
   p.spw = spw;
   p.sleep_max = tuned_sleep();
   p.eps = a->eps;
@@ -643,9 +877,9 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.lm_head = static_cast<const __half*>(a->lm_head);
   p.rope_cs = a->rope_cs;
   p.resid = a->resid;
-  p.accum = a->accum;
+  p.accA = a->accA;
+  p.accF = a->accF;
   p.qkv = static_cast<__half*>(a->qkv);
-  p.act = static_cast<__half*>(a->act);
   p.partials = a->partials;
   p.barrier = a->barrier;
   p.counters = a->counters;
@@ -657,19 +891,29 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.pos = a->pos;
   p.err = a->err;
   p.trace = a->trace;
-  auto kern = llama_step_kernel;
-  CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (grid barriers)
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+  if (a->cluster_attn) {
+    // co-residency: G <= the GPCs' max active clusters (llama_step_grid)
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = N;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true>, p));
+  } else {
+    if (const int rc = configure_kernel((const void*)llama_step_kernel<false>, kMaxSmem, false)) return rc;
+    at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (grid barriers)
+    at[0].val.cooperative = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<false>, p));
+  }
   return CFB_OK;
 }
 

@@ -257,11 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1) ffn_swiglu_kernel(const FfnParams
 template <typename T, int QB, bool XH>
 static int launch_ffn_inst(const FfnParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = ffn_swiglu_kernel<T, QB, XH>;
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)kern, kMaxSmem, false)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

@@ -29,14 +29,15 @@ struct cfb_llama {
   int* token = nullptr;
   int* pos = nullptr;
   unsigned long long* argkey = nullptr;  // TP: packed (logit, -index) of the local argmax
-  void* qkv = nullptr;                   // split mode: q|k|v slices of the layer [rows]
-  bool split_qkv = false;
   int tp_rank = 0, tp_size = 1, vocab_offset = 0;
   int ext = 0;  // bit mask: accum / resid / argkey are caller-owned
   // persistent engine (csrc/decode_step.cu)
   void** dev_ptrs = nullptr;            // 8 x n_layers per-layer pointers, device copy
   void* pqkv = nullptr;                 // q|k|v rows of the current layer
   float* partials = nullptr;            // attention partials [nh][grid][132]
+  float* presid = nullptr;              // [2][D] residual (layer-parity double buffer)
+  unsigned long long* paccA = nullptr;  // [2][D] attention head sums
+  unsigned long long* paccF = nullptr;  // [2][D] FFN output sums
   unsigned long long* pbarrier = nullptr;
   unsigned long long* counters = nullptr;  // [2 nh]
   int* err = nullptr;
@@ -78,12 +79,6 @@ int enqueue_embed(cfb_llama* m, cudaStream_t st) {
 
 int enqueue_attn(cfb_llama* m, int l, cudaStream_t st) {
   const cfb_llama_config& c = m->cfg;
-  const int qkv_rows = c.n_heads * c.cluster * ((3 * c.head_dim / c.cluster + 3) / 4) * 4;
-  if (m->split_qkv) {  // QKV stream on all SMs, the cluster kernel starts at the gather
-    const int rc = cfb::qkv_proj(c.dtype, 1, c.hidden, qkv_rows, m->resid, m->attn_norm[l], c.eps,
-                                 m->w_qkv[l], m->qkv, CFB_PDL, st);
-    if (rc) return rc;
-  }
   cfb_mha_args a = {};
   a.dtype = c.dtype;
   a.batch = 1;
@@ -93,9 +88,7 @@ int enqueue_attn(cfb_llama* m, int l, cudaStream_t st) {
   a.head_pad = c.head_dim;
   a.cluster = c.cluster;
   a.cache_cap = c.cache_cap;
-  a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_ONESHOT | CFB_PDL |
-            (m->split_qkv ? CFB_QKV_IN : CFB_NORM);
-  a.qkv_in = m->qkv;
+  a.flags = CFB_APPEND | CFB_WRITE_KV | CFB_ROPE | CFB_ONESHOT | CFB_PDL | CFB_NORM;
   a.resid = m->resid;
   a.norm_w = m->attn_norm[l];
   a.eps = c.eps;
@@ -117,12 +110,9 @@ int enqueue_ffn(cfb_llama* m, int l, cudaStream_t st) {
   f.batch = 1;
   f.hidden = c.hidden;
   f.inter = c.inter;
-  // TP: only rank 0 adds the residual, so the all-reduce of resid counts it once
-  static const bool pool = [] {  // work-stolen gate/up tail (CFB_FFN_POOL=0 disables)
-    const char* e = getenv("CFB_FFN_POOL");
-    return e ? atoi(e) != 0 : true;
-  }();
-  f.flags = CFB_NORM | CFB_PDL | (m->tp_rank == 0 ? CFB_RESID : 0) | (pool ? CFB_DYN_POOL : 0);
+  // TP: only rank 0 adds the residual, so the all-reduce of resid counts it once;
+  // the last gate/up tiles are work-stolen (CFB_DYN_POOL)
+  f.flags = CFB_NORM | CFB_PDL | CFB_DYN_POOL | (m->tp_rank == 0 ? CFB_RESID : 0);
   f.eps = c.eps;
   f.resid = m->resid;
   f.accum = m->accum;
@@ -197,6 +187,7 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.cache_cap = c.cache_cap;
   a.cluster = c.cluster;
   a.grid = m->grid;
+  a.cluster_attn = c.engine == CFB_ENGINE_PERSISTENT;
   a.eps = c.eps;
   void** d = m->dev_ptrs;
   a.attn_norm = d;
@@ -211,10 +202,10 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.final_norm = m->final_norm;
   a.lm_head = m->lm_head;
   a.rope_cs = m->rope_cs;
-  a.resid = m->resid;
-  a.accum = m->accum;
+  a.resid = m->presid;
+  a.accA = m->paccA;
+  a.accF = m->paccF;
   a.qkv = m->pqkv;
-  a.act = m->act;
   a.partials = m->partials;
   a.barrier = m->pbarrier;
   a.counters = m->counters;
@@ -233,7 +224,7 @@ int enqueue_step(cfb_llama* m, cudaStream_t st) {
   if (m->tp_size > 1)
     return cfb::set_error(CFB_ERR_ARGUMENT,
                           "tensor-parallel engines are driven part by part (collectives between)");
-  if (m->cfg.engine == CFB_ENGINE_PERSISTENT) return enqueue_persistent(m, st);
+  if (m->cfg.engine != CFB_ENGINE_LAYERED) return enqueue_persistent(m, st);
   int rc = enqueue_embed(m, st);
   for (int l = 0; !rc && l < m->cfg.n_layers; ++l)
     if (!(rc = enqueue_attn(m, l, st))) rc = enqueue_ffn(m, l, st);
@@ -281,23 +272,29 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     cfb_llama_destroy(m);
     return rc;
   }
-  {  // optional engine mode: split QKV projection (CFB_SPLIT_QKV=1); measured slower
-     // than the fused module, kept for the A/B
-    const char* e = getenv("CFB_SPLIT_QKV");
-    m->split_qkv = e ? atoi(e) != 0 : false;
-    const size_t qkv_rows = (size_t)cfg->n_heads * cfg->cluster *
-                            ((3 * cfg->head_dim / cfg->cluster + 3) / 4) * 4;
-    if (m->split_qkv && (rc = alloc_zero(&m->qkv, qkv_rows * cfg->dtype))) {
+  if (cfg->engine != CFB_ENGINE_LAYERED) {
+    if (cfg->engine != CFB_ENGINE_PERSISTENT && cfg->engine != CFB_ENGINE_PERSISTENT_FLAT) {
       cfb_llama_destroy(m);
-      return rc;
+      return set_error(CFB_ERR_ARGUMENT, "unknown engine kind %d", cfg->engine);
     }
-  }
-  if (cfg->engine == CFB_ENGINE_PERSISTENT) {
     if (cfg->dtype != CFB_F16 || cfg->head_dim != 128) {
       cfb_llama_destroy(m);
       return set_error(CFB_ERR_DIMENSION, "persistent engine: fp16, head_dim 128");
     }
-    m->grid = sms;
+    cfb::LlamaStepArgs ga = {};
+    ga.n_layers = L;
+    ga.hidden = cfg->hidden;
+    ga.n_heads = cfg->n_heads;
+    ga.head_dim = cfg->head_dim;
+    ga.inter = cfg->inter;
+    ga.vocab = cfg->vocab;
+    ga.cache_cap = cfg->cache_cap;
+    ga.cluster = cfg->cluster;
+    ga.cluster_attn = cfg->engine == CFB_ENGINE_PERSISTENT;
+    if ((rc = cfb::llama_step_grid(&ga, &m->grid, nullptr, nullptr))) {
+      cfb_llama_destroy(m);
+      return rc;
+    }
     const int N = cfg->cluster;
     const size_t qkv_rows = (size_t)cfg->n_heads * N * ((3 * cfg->head_dim / N + 3) / 4) * 4;
     std::vector<const void*> host(8 * (size_t)L);
@@ -314,6 +311,9 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     if ((rc = alloc_zero((void**)&m->dev_ptrs, host.size() * sizeof(void*))) ||
         (rc = alloc_zero(&m->pqkv, qkv_rows * 2)) ||
         (rc = alloc_zero((void**)&m->partials, (size_t)cfg->n_heads * sms * 132 * 4)) ||
+        (rc = alloc_zero((void**)&m->presid, 2 * D * 4)) ||
+        (rc = alloc_zero((void**)&m->paccA, 2 * D * 8)) ||
+        (rc = alloc_zero((void**)&m->paccF, 2 * D * 8)) ||
         (rc = alloc_zero((void**)&m->pbarrier, 8)) ||
         (rc = alloc_zero((void**)&m->counters, (size_t)2 * cfg->n_heads * 8)) ||
         (rc = alloc_zero((void**)&m->err, 4))) {
@@ -337,8 +337,8 @@ int cfb_llama_destroy(cfb_llama* m) {
   if (m->graph) cudaGraphDestroy(m->graph);
   void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
                   m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
-                  m->pos, (m->ext & 4) ? nullptr : m->argkey, m->qkv, m->dev_ptrs, m->pqkv,
-                  m->partials, m->pbarrier, m->counters, m->err};
+                  m->pos, (m->ext & 4) ? nullptr : m->argkey, m->dev_ptrs, m->pqkv,
+                  m->partials, m->pbarrier, m->counters, m->err, m->presid, m->paccA, m->paccF};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -406,8 +406,8 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
 }
 
 int cfb_llama_launches_per_step(const cfb_llama* m) {
-  if (m && m->cfg.engine == CFB_ENGINE_PERSISTENT && m->tp_size == 1) return 1;
-  return m ? 2 + (m->split_qkv ? 3 : 2) * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
+  if (m && m->cfg.engine != CFB_ENGINE_LAYERED && m->tp_size == 1) return 1;
+  return m ? 2 + 2 * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
 }
 
 int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigned long long* accum,
@@ -472,8 +472,8 @@ int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream) {
 
 int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid) {
   if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
-  if (m->cfg.engine != CFB_ENGINE_PERSISTENT)
-    return cfb::set_error(CFB_ERR_ARGUMENT, "tracing needs the persistent engine");
+  if (m->cfg.engine == CFB_ENGINE_LAYERED)
+    return cfb::set_error(CFB_ERR_ARGUMENT, "tracing needs a persistent engine");
   m->trace = trace;
   if (grid) *grid = m->grid;
   return CFB_OK;

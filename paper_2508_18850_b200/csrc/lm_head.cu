@@ -153,11 +153,7 @@ __global__ void embed_kernel(const T* table, const int* tokens, float* out, int 
 template <typename T, int QB>
 static int launch_lm_inst(const LmParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = lm_head_kernel<T, QB>;
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)kern, kMaxSmem, false)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

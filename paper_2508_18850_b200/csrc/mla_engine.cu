@@ -22,6 +22,8 @@
 //                    fixed-point head-sum accumulator the MoE kernel reads.
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #include "common.h"
 #include "gemv.cuh"
 
@@ -497,13 +499,10 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(mla_proj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(mla_out_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(mla_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kAttnSmem));
-    configured = true;
-  }
+  for (const auto& kc : {std::make_pair((const void*)mla_proj_kernel, kMaxSmem),
+                         std::make_pair((const void*)mla_out_kernel, kMaxSmem),
+                         std::make_pair((const void*)mla_attn_kernel, (int)kAttnSmem)})
+    if (const int rc = configure_kernel(kc.first, kc.second, false)) return rc;
   MlaEngParams p = {};
   p.D = a->hidden;
   p.H = a->head_dim;

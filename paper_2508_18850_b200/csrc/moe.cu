@@ -578,11 +578,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
 template <int QB>
 static int launch_moe_inst(const MoeParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = moe_kernel<QB>;
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)kern, kMaxSmem, false)) return rc;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);

@@ -35,7 +35,8 @@ __device__ __forceinline__ void consumer_sync() { named_bar_sync(kConsumerBar, k
 //   tiles mode (tiles == true):  a unit is a 4-row tile of a row-tiled weight
 //              matrix, [chunk][4 rows][16 B] (see gemv.cuh); a tile larger
 //              than a slot is split into column pieces.
-// Items (<= one slot) are dealt round-robin: item i goes to consumer warp i % 8.
+// Items (<= one slot) are dealt round-robin: item i goes to consumer warp i % 8
+// (or all to one warp: warp_phase).
 struct Phase {
   const char* src0;
   const char* src1;
@@ -46,6 +47,7 @@ struct Phase {
   int piece_bytes;
   int n_items;
   bool tiles;
+  int warp;         // >= 0: every item goes to this consumer warp (warp-affine phase)
 };
 
 __device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, int n_units,
@@ -56,6 +58,7 @@ __device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, 
   p.n_units = n_units < 0 ? 0 : n_units;
   p.unit_bytes = unit_bytes;
   p.tiles = tiles;
+  p.warp = -1;
   const int cap = src1 ? kSlotBytes / 2 : kSlotBytes;
   if (unit_bytes <= cap) {
     p.per_item = cap / unit_bytes;
@@ -79,12 +82,20 @@ struct Item {
   int bytes;   // bytes per source
 };
 
+// Warp-affine phase: all items of the phase go to consumer warp `warp` (the
+// warp then owns everything the phase produces, e.g. a block of output rows).
+__device__ __forceinline__ Phase warp_phase(Phase p, int warp) {
+  p.warp = warp;
+  return p;
+}
+
 __device__ __forceinline__ int items_for_warp(const Phase& p, int w) {
+  if (p.warp >= 0) return p.warp == w ? p.n_items : 0;
   return p.n_items > w ? (p.n_items - w + kNumConsumerWarps - 1) / kNumConsumerWarps : 0;
 }
 
 __device__ __forceinline__ Item item_of(const Phase& p, int w, int j) {
-  const int i = j * kNumConsumerWarps + w;
+  const int i = p.warp >= 0 ? j : j * kNumConsumerWarps + w;
   Item it;
   if (p.pieces == 1) {
     it.unit0 = i * p.per_item;
@@ -170,6 +181,46 @@ __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r,
     }
   }
 }
+// Same walk over `np` phases produced on the fly by gen(k) (no phase array:
+// a long schedule indexed dynamically would live in local memory).
+template <class Gen>
+__device__ __forceinline__ void produce_gen(int np, Gen&& gen, const Ring& r, int lane, uint64_t policy,
+                                            int& c) {
+  const int w = lane;
+  int ph = 0, j = 0;
+  Phase cur = gen(0);
+  bool done = w >= kNumConsumerWarps || np == 0;
+  int nap = 32;
+  while (true) {
+    bool issued = false;
+    if (!done) {
+      while (ph < np && j >= items_for_warp(cur, w)) {
+        ++ph;
+        j = 0;
+        if (ph < np) cur = gen(ph);
+      }
+      if (ph == np) {
+        done = true;
+      } else {
+        const int s = w * r.spw + (c % r.spw);
+        if (mbar_test(&r.empty[s], ((c / r.spw) & 1) ^ 1)) {
+          issue_item(cur, item_of(cur, w, j), r, s, policy);
+          ++c;
+          ++j;
+          issued = true;
+        }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (__any_sync(0xffffffffu, issued)) {
+      nap = 32;
+    } else {
+      __nanosleep(nap);
+      nap = min(2 * nap, r.sleep_max);
+    }
+  }
+}
+
 template <int NP>
 __device__ __forceinline__ void produce_all(const Phase (&P)[NP], const Ring& r, int lane,
                                             uint64_t policy) {

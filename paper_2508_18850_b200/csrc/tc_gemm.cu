@@ -375,11 +375,7 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
             float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr) {
   if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
-  static bool configured = false;
-  if (!configured) {
-    CFB_CUDA(cudaFuncSetAttribute(tc_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes()));
-    configured = true;
-  }
+  if (const int rc = configure_kernel((const void*)tc_gemm_kernel, tc_smem_bytes(), false)) return rc;
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -131,12 +131,3 @@ def test_graph_replay_matches_eager():
     m2 = LlamaDecoder.from_params(cfg, params, cache_cap=64)
     graph = m2.generate(first_token=3, pos=20, n_tokens=8, use_graph=True)
     assert eager == graph
-
-
-def test_llama_split_qkv_mode(monkeypatch):
-    """Engine split mode (cfb_qkv_proj on all SMs + CFB_QKV_IN attention module):
-    same greedy tokens / logits as the CPU oracle."""
-    monkeypatch.setenv("CFB_SPLIT_QKV", "1")
-    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      cluster=4)
-    _teacher_forced(cfg, prefill=40, steps=3, seed=8, atol=2e-2)

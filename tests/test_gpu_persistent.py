@@ -44,34 +44,41 @@ def _run(cfg, prefill, steps, seed):
     return m
 
 
+ENGINES = ["persistent", "persistent_flat"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("prefill", [0, 1, 3, 37, 300])
-def test_persistent_small(prefill):
+def test_persistent_small(prefill, engine):
     cfg = LlamaConfig(n_layers=3, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      engine="persistent")
+                      engine=engine)
     _run(cfg, prefill, steps=4, seed=1)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("cluster", [1, 2, 8])
-def test_persistent_reads_any_split_token_layout(cluster):
+def test_persistent_reads_any_split_token_layout(cluster, engine):
     cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=8, head_dim=128, inter=1024, vocab=512,
-                      cluster=cluster, engine="persistent")
+                      cluster=cluster, engine=engine)
     _run(cfg, 100, steps=3, seed=2)
 
 
-def test_persistent_matches_layered_tokens_graph():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_persistent_matches_layered_tokens_graph(engine):
     cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000)
     params = random_llama_params(cfg, seed=5, prefill=20)
     a = LlamaDecoder.from_params(cfg, params, cache_cap=64)
-    b = LlamaDecoder.from_params(dataclasses.replace(cfg, engine="persistent"), params, cache_cap=64)
+    b = LlamaDecoder.from_params(dataclasses.replace(cfg, engine=engine), params, cache_cap=64)
     assert b.launches_per_step == 1
     ta = a.generate(first_token=3, pos=20, n_tokens=8, use_graph=True)
     tb = b.generate(first_token=3, pos=20, n_tokens=8, use_graph=True)
     assert ta == tb
 
 
-def test_persistent_full_cache_is_flagged():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_persistent_full_cache_is_flagged(engine):
     cfg = LlamaConfig(n_layers=1, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      engine="persistent")
+                      engine=engine)
     m = LlamaDecoder.from_params(cfg, random_llama_params(cfg, seed=3, prefill=8), cache_cap=10)
     m.set_state(9, 1)
     m.step()  # pos 9 -> fills row 9 (cap 10)
@@ -82,9 +89,10 @@ def test_persistent_full_cache_is_flagged():
         m.check()
 
 
-def test_persistent_trace_stamps_monotone():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_persistent_trace_stamps_monotone(engine):
     cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      engine="persistent")
+                      engine=engine)
     m = LlamaDecoder.from_params(cfg, random_llama_params(cfg, seed=4, prefill=16), cache_cap=32)
     tr = m.set_trace(True)
     m.set_state(16, 2)
