@@ -72,9 +72,9 @@ struct LlamaStepArgs {
   const void* final_norm;
   const void* lm_head;
   const float* rope_cs;
-  float* resid;               // [2][D] (layer-parity double buffer)
-  unsigned long long* accA;   // [2][D]
-  unsigned long long* accF;   // [2][D]
+  float* resid;               // [D]
+  unsigned long long* accA;   // [D] attention head sum (fixed point)
+  void* act;                  // [F]
   void* qkv;
   float* partials;
   unsigned long long* barrier;

@@ -59,7 +59,6 @@ constexpr int kLPK = kH / kEPL; // lanes per key (8)
 constexpr int kKPP = 32 / kLPK; // keys per warp step (4)
 constexpr int kRC = 4;          // warp steps per online-softmax chunk
 constexpr int kPS = kH + 4;     // floats per attention partial: m, l, pad, pad, A[H]
-constexpr int kMaxDownK = 8;    // down-projection row quads per lane: hidden <= 8192
 
 struct StepParams {
   int L, D, nh, F, V, cap, N, tpr, spw, sleep_max;
@@ -76,13 +75,9 @@ struct StepParams {
   const __half* final_norm;
   const __half* lm_head;
   const float* rope_cs;
-  // residual stream, double-buffered by layer parity p = l & 1 (no barrier is
-  // needed to retire a buffer): r_l = resid[p] + accF[p] enters layer l, the
-  // attention head sum goes to accA[p], the FFN's split-K down partials to
-  // accF[1-p], and resid[1-p] = r_l + accA[p]
-  float* resid;                  // [2][D] fp32
-  unsigned long long* accA;      // [2][D] fixed-point attention head sum
-  unsigned long long* accF;      // [2][D] fixed-point FFN output sum
+  float* resid;                  // [D] fp32 residual stream
+  unsigned long long* accA;      // [D] fixed-point attention head sum
+  __half* act;                   // [F] SwiGLU activations
   __half* qkv;                   // [nh * N * tpr * 4] q|k|v rows of the layer
   float* partials;               // [nh][G][kPS]
   unsigned long long* barrier;   // grid barrier counter (monotonic)
@@ -107,6 +102,8 @@ __host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, 
   StepLayout L;
   auto tiles = [&](int T) { return (T + G - 1) / G; };
   int t = tiles(TQ);
+  const int tpr = (3 * (kH / N) + 3) / 4;  // cluster variant: one rank's W_qkv tiles
+  if (tpr > t) t = tpr;
   if (tiles(F / 2) > t) t = tiles(F / 2);
   if (tiles(D / 4) > t) t = tiles(D / 4);
   if (tiles(TV) > t) t = tiles(TV);
@@ -116,9 +113,9 @@ __host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, 
   if (ws > part) part = ws;
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
-  L.xs = o;    o += r16(D * 2);
+  L.xs = o;    o += r16((D > F ? D : F) * 2);
   L.part = o;  o += r16(part);
-  L.gu = o;    o += r16(4 * tiles(F / 2) * 4) + r16(2 * tiles(F / 2) * 4);  // gate/up rows | act
+  L.gu = o;    o += r16(4 * tiles(F / 2) * 4);
   L.qf = o;    o += 3 * kH * 4 + kH * 2;  // q, k, v fp32 + fp16 A for the O projection
   L.dsm = o;   o += N * r16(3 * (kH / N) * 2) + N * r16((4 + kH) * 4);  // DSMEM gather | exchange
   L.red = o;   o += r16(kNumConsumerWarps * 4 * 2);
@@ -143,6 +140,22 @@ __device__ __forceinline__ int owner_of(long long x, long long total, int G) {
 
 __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Grid barrier with a precomputed target: the monotonic counter is k*G at
+// launch (every earlier barrier completed), so target_n = base + n*G.  The
+// arrival is a posted red.release (no atomic round trip on the critical
+// path); thread 0 then polls with ld.acquire.
+__device__ __forceinline__ void grid_sync(unsigned long long* counter, unsigned long long target,
+                                          int tid) {
+  __threadfence();
+  consumer_sync();
+  if (tid == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
+    while (ld_acquire_u64(counter) < target) {
+    }
+  }
+  consumer_sync();
 }
 
 // thread 0 spins until *p >= target, then the CTA's consumers proceed
@@ -227,7 +240,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   const int D = p.D, F = p.F, nh = p.nh, N = p.N;
   const int hp = kH / N;                      // head dims per split_token rank
   const int TPH = N * p.tpr;                  // W_qkv tiles per head
-  const int TQ = nh * TPH, T1 = F / 2, TV = p.V / 4;
+  const int TQ = nh * TPH, T1 = F / 2, T2 = D / 4, TV = p.V / 4;
   const StepLayout Lo = step_layout(D, F, TQ, TV, G, N, p.spw);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Lo.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
@@ -276,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   }
   // FFN and LM head: contiguous tile ranges over all G CTAs
   const int a0 = (int)split_at(T1, i, G), a1 = (int)split_at(T1, i + 1, G);
+  const int u0 = (int)split_at(T2, i, G), u1 = (int)split_at(T2, i + 1, G);
   const int v0 = (int)split_at(TV, i, G), v1 = (int)split_at(TV, i + 1, G);
   const int seg_bytes = r16(3 * hp * 2), pay_bytes = r16((4 + kH) * 4);
 
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   // a dynamically indexed schedule would sit in local memory, which shares
   // the L1 with the 190+ KB ring).  Attention phases 0..5 (cluster: qkv, kv,
   // o per head round; flat: qkv, kv piece 0/1, o piece 0/1, -), FFN: 6
-  // (gate/up), 7..14 (down row blocks, warp-affine).
+  // (gate/up), 7 (down).
   auto layer_phase = [&](int l, int k) -> Phase {
     if (k < 6) {
       if (kCluster) {
@@ -328,14 +342,9 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       return make_phase(nullptr, nullptr, 0, 16);
     }
     if (k == 6) return make_phase(p.w_gu[l] + (size_t)a0 * 4 * D, nullptr, a1 - a0, 4 * D * 2, true);
-    // W_down packed [8 row blocks][F/2 f-pairs][D/8 rows][2]: block j of this
-    // CTA's f pairs [a0, a1) is one contiguous run, streamed to warp j
-    const int j = k - 7;
-    return warp_phase(make_phase(p.w_dn[l] + ((size_t)j * T1 + a0) * (D / 8) * 2, nullptr, a1 - a0,
-                                 (D / 8) * 2 * 2),
-                      j);
+    return make_phase(p.w_dn[l] + (size_t)u0 * 4 * F, nullptr, u1 - u0, 4 * F * 2, true);
   };
-  constexpr int kPhases = 15;
+  constexpr int kPhases = 8;
 
   if (warp == kNumConsumerWarps) {  // ---------------------------- producer
     const uint64_t pol = policy_evict_first();
@@ -368,30 +377,24 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   unsigned long long* qkv_done = p.counters;
   unsigned long long* att_done = p.counters + nh;
 
-  // embed: resid[0][c] = embed[token][c] for this CTA's slice (accF[0], accA[0]
-  // zeroed: r_0 = resid[0]); counters reset
-  const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);  // residual slice
+  // embed: resid[c] = embed[token][c] for this CTA's slice; counters reset
   {
     const int tok = *p.token;
-    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
+    const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads)
       p.resid[c] = __half2float(p.embed[(size_t)tok * D + c]);
-      p.accF[c] = 0ull;
-      p.accA[c] = 0ull;
-    }
     if (!kCluster && i == 0 && tid < 2 * nh) p.counters[tid] = 0ull;
   }
+  // barrier base: no CTA can pass the first barrier before all have read it
+  unsigned long long bar_target = (ld_acquire_u64(p.barrier) / G) * G;
   if (kCluster) cluster_wait();
-  grid_barrier(p.barrier, tid);
+  bar_target += G;
+  grid_sync(p.barrier, bar_target, tid);
 
-  // r = resid[q] + accF[q] as float4 (cross-CTA data is read through L2,
-  // ld.global.cg: L1 is not coherent)
-  auto r_in = [&](int q, int v) {
-    const float4 r = __ldcg(reinterpret_cast<const float4*>(p.resid + (size_t)q * D) + v);
-    const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accF + (size_t)q * D) + 2 * v);
-    const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accF + (size_t)q * D) + 2 * v + 1);
-    return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
-                       __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
-  };
+  // cross-CTA data is read through L2 (ld.global.cg): L1 is not coherent
+  const float* resid_g = p.resid;
+  auto r_l = [resid_g](int, int v) { return __ldcg(reinterpret_cast<const float4*>(resid_g) + v); };
+  unsigned long long* accA = p.accA;
   int cnt = 0;
   int use = 0;  // DSMEM barrier phase (one gather + one exchange per head round)
   const int g = lane / kLPK, li = lane % kLPK;
@@ -483,12 +486,6 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   for (int l = 0; l < p.L; ++l) {
     unsigned long long* tr = p.trace ? p.trace + ((size_t)l * G + i) * 8 : nullptr;
     stamp(tr, 0, tid);
-    const int par = l & 1;
-    unsigned long long* accA = p.accA + (size_t)par * D;
-    auto r_l = [&](int, int v) { return r_in(par, v); };
-    // retire accF[1-par] (last read by layer l-1's prologues) before this
-    // layer's FFN adds into it
-    for (int c = c0 + tid; c < c1; c += kConsumerThreads) p.accF[(size_t)(1 - par) * D + c] = 0ull;
     if (kCluster) {
       // ================= attention module on the cluster (split_token, Alg. 3)
       if (nrounds > 0) rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.attn_norm[l], 1, D, p.eps, red, tid);
@@ -633,86 +630,52 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       }
       stamp(tr, 3, tid);
     }
-    grid_barrier(p.barrier, tid);
+    bar_target += G;
+    grid_sync(p.barrier, bar_target, tid);
     stamp(tr, 4, tid);
 
-    // ---- FFN (one block-half, no internal barrier): RMSNorm(r_l + head sum) ->
-    //      gate/up rows of this CTA's f range -> SiLU*mul (fp16 store, the
-    //      oracle's rounding point) -> split-K down projection over the same f
-    //      range, partial outputs added into accF[1-par] (fixed point, exact)
-    auto r_mid = [&](int, int v) {
-      const float4 r = r_in(par, v);
-      const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v);
-      const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v + 1);
-      return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
-                         __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
-    };
-    rmsnorm_to_smem_ld<__half, true>(xs, r_mid, p.ffn_norm[l], 1, D, p.eps, red, tid);
-    // this CTA's residual slice moves on: resid[1-par] = r_l + head sum; accA of
-    // the other parity is retired (last read in layer l-1)
-    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
-      const float r = __fadd_rn(__fadd_rn(__ldcg(p.resid + (size_t)par * D + c),
-                                          fixed_to_float(__ldcg(p.accF + (size_t)par * D + c))),
-                                fixed_to_float(__ldcg(accA + c)));
-      p.resid[(size_t)(1 - par) * D + c] = r;
-      p.accA[(size_t)(1 - par) * D + c] = 0ull;
-    }
-    float* actf = gu + 4 * ((T1 + G - 1) / G);
-    tiled_gemv_phase<__half, 1, true>(layer_phase(l, 6), ring, warp, lane, tid, cnt, xs, D, 1, 4 * (a1 - a0), part,
-                                      [&](int row, int, float v) { gu[row] = v; });
+    // ---- FFN gate/up with the residual + head-sum RMSNorm prologue
+    rmsnorm_to_smem_ld<__half, true>(
+        xs,
+        [&](int, int v) {
+          const float4 r = __ldcg(reinterpret_cast<const float4*>(resid_g) + v);
+          const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v);
+          const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v + 1);
+          return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
+                             __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
+        },
+        p.ffn_norm[l], 1, D, p.eps, red, tid);
+    tiled_gemv_phase<__half, 1, true>(layer_phase(l, 6), ring, warp, lane, tid, cnt, xs, D, 1,
+                                      4 * (a1 - a0), part, [&](int row, int, float v) { gu[row] = v; });
     consumer_sync();
     for (int jj = tid; jj < 2 * (a1 - a0); jj += kConsumerThreads) {
       const int t = jj >> 1, e = jj & 1;  // tile rows: g0 g1 u0 u1
       const float gt = gu[4 * t + e], up = gu[4 * t + 2 + e];
       const float sl = __fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt)));
-      actf[jj] = round_to<__half>(__fmul_rn(sl, up));
+      p.act[2 * a0 + jj] = __float2half_rn(__fmul_rn(sl, up));
     }
-    consumer_sync();
     stamp(tr, 5, tid);
-    {
-      // warp w owns output rows [w*D/8, (w+1)*D/8): its warp-affine phase
-      // streams those rows of every down tile [rows][f pair] of this CTA
-      const int RB = D / 8, nck = RB / 4, ub = RB * 4;
-      float dacc[kMaxDownK][4];
-#pragma unroll
-      for (int k = 0; k < kMaxDownK; ++k) dacc[k][0] = dacc[k][1] = dacc[k][2] = dacc[k][3] = 0.f;
-      consume_phase(layer_phase(l, 7 + warp), ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
-        for (int u = 0; u < it.nunits; ++u) {
-          const int t = it.unit0 + u;
-          const __half2 av = __floats2half2_rn(actf[2 * t], actf[2 * t + 1]);  // exact (fp16 values)
-          const uint32_t a2 = *reinterpret_cast<const uint32_t*>(&av);
-          const char* base = slot + (size_t)u * ub;
-#pragma unroll
-          for (int k = 0; k < kMaxDownK; ++k) {
-            const int c = lane + 32 * k;
-            if (c < nck) {
-              const uint4 w4 = lds128(base + c * 16);  // rows 4c..4c+3 x (f0, f1)
-              dacc[k][0] = fma_f16_hi(w4.x, a2, fma_f16_lo(w4.x, a2, dacc[k][0]));
-              dacc[k][1] = fma_f16_hi(w4.y, a2, fma_f16_lo(w4.y, a2, dacc[k][1]));
-              dacc[k][2] = fma_f16_hi(w4.z, a2, fma_f16_lo(w4.z, a2, dacc[k][2]));
-              dacc[k][3] = fma_f16_hi(w4.w, a2, fma_f16_lo(w4.w, a2, dacc[k][3]));
-            }
-          }
-        }
-      });
-      unsigned long long* accF = p.accF + (size_t)(1 - par) * D + warp * RB;
-#pragma unroll
-      for (int k = 0; k < kMaxDownK; ++k) {
-        const int c = lane + 32 * k;
-        if (c < nck && a1 > a0) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) red_add_fixed(&accF[4 * c + r], dacc[k][r]);
-        }
-      }
-    }
+    bar_target += G;
+    grid_sync(p.barrier, bar_target, tid);
+
+    // ---- down projection + residual: resid = resid + head sum + FFN
+    load_act_to_smem<__half, true>(xs, p.act, 1, F, tid);
     stamp(tr, 6, tid);
-    grid_barrier(p.barrier, tid);
+    tiled_gemv_phase<__half, 1, true>(layer_phase(l, 7), ring, warp, lane, tid, cnt, xs, F, 1,
+                                      4 * (u1 - u0), part, [&](int row, int, float v) {
+                                        const int c = 4 * u0 + row;
+                                        const float r = __fadd_rn(__ldcg(p.resid + c),
+                                                                  fixed_to_float(__ldcg(accA + c)));
+                                        accA[c] = 0ull;
+                                        p.resid[c] = __fadd_rn(r, v);
+                                      });
+    bar_target += G;
+    grid_sync(p.barrier, bar_target, tid);
     stamp(tr, 7, tid);
   }
 
   // ---- final RMSNorm + LM head + argmax
-  auto r_out = [&](int, int v) { return r_in(p.L & 1, v); };
-  rmsnorm_to_smem_ld<__half, true>(xs, r_out, p.final_norm, 1, D, p.eps, red, tid);
+  rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.final_norm, 1, D, p.eps, red, tid);
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   const Phase PL = make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true);
@@ -878,7 +841,7 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.rope_cs = a->rope_cs;
   p.resid = a->resid;
   p.accA = a->accA;
-  p.accF = a->accF;
+  p.act = static_cast<__half*>(a->act);
   p.qkv = static_cast<__half*>(a->qkv);
   p.partials = a->partials;
   p.barrier = a->barrier;

@@ -35,9 +35,6 @@ struct cfb_llama {
   void** dev_ptrs = nullptr;            // 8 x n_layers per-layer pointers, device copy
   void* pqkv = nullptr;                 // q|k|v rows of the current layer
   float* partials = nullptr;            // attention partials [nh][grid][132]
-  float* presid = nullptr;              // [2][D] residual (layer-parity double buffer)
-  unsigned long long* paccA = nullptr;  // [2][D] attention head sums
-  unsigned long long* paccF = nullptr;  // [2][D] FFN output sums
   unsigned long long* pbarrier = nullptr;
   unsigned long long* counters = nullptr;  // [2 nh]
   int* err = nullptr;
@@ -202,9 +199,9 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.final_norm = m->final_norm;
   a.lm_head = m->lm_head;
   a.rope_cs = m->rope_cs;
-  a.resid = m->presid;
-  a.accA = m->paccA;
-  a.accF = m->paccF;
+  a.resid = m->resid;
+  a.accA = m->accum;
+  a.act = m->act;
   a.qkv = m->pqkv;
   a.partials = m->partials;
   a.barrier = m->pbarrier;
@@ -311,9 +308,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     if ((rc = alloc_zero((void**)&m->dev_ptrs, host.size() * sizeof(void*))) ||
         (rc = alloc_zero(&m->pqkv, qkv_rows * 2)) ||
         (rc = alloc_zero((void**)&m->partials, (size_t)cfg->n_heads * sms * 132 * 4)) ||
-        (rc = alloc_zero((void**)&m->presid, 2 * D * 4)) ||
-        (rc = alloc_zero((void**)&m->paccA, 2 * D * 8)) ||
-        (rc = alloc_zero((void**)&m->paccF, 2 * D * 8)) ||
+
         (rc = alloc_zero((void**)&m->pbarrier, 8)) ||
         (rc = alloc_zero((void**)&m->counters, (size_t)2 * cfg->n_heads * 8)) ||
         (rc = alloc_zero((void**)&m->err, 4))) {
@@ -338,7 +333,7 @@ int cfb_llama_destroy(cfb_llama* m) {
   void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
                   m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
                   m->pos, (m->ext & 4) ? nullptr : m->argkey, m->dev_ptrs, m->pqkv,
-                  m->partials, m->pbarrier, m->counters, m->err, m->presid, m->paccA, m->paccF};
+                  m->partials, m->pbarrier, m->counters, m->err};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;

@@ -83,11 +83,3 @@ def rotated_rows(t):
     logical = ((p - g) % nch).view(*([1] * len(lead)), rows, nch, 1).expand(*lead, rows, nch, e)
     return torch.gather(w, len(lead) + 1, logical).reshape(*lead, rows, C).contiguous()
 
-
-def down_pair_blocks(w3, blocks: int = 8):
-    """w3 (D, F) -> [blocks][F/2][D/blocks][2]: the persistent engine's split-K
-    down projection (csrc/decode_step.cu).  Row block j of f-pair t holds
-    w3[j*D/blocks + r, 2t + e] at [j][t][r][e], so the f pairs of one CTA's
-    gate/up range are one contiguous run per row block (one consumer warp)."""
-    D, F = w3.shape
-    return w3.reshape(blocks, D // blocks, F // 2, 2).permute(0, 2, 1, 3).contiguous()

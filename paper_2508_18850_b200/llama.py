@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from .exceptions import DimensionError
-from .layouts import down_pair_blocks, gate_up_tiles, qkv_tiles, row_tiles, wo_rows
+from .layouts import gate_up_tiles, qkv_tiles, row_tiles, wo_rows
 
 
 @dataclass(frozen=True)
@@ -176,7 +176,7 @@ class LlamaDecoder:
     def _pack_down(self, w3):
         """W_down in the layout of the engine: row tiles (layered FFN kernel) or
         row-block x f-pair blocks (persistent kernel's split-K down projection)."""
-        return row_tiles(w3) if self.cfg.engine == "layered" else down_pair_blocks(w3)
+        return row_tiles(w3)
 
     @classmethod
     def from_params(cls, cfg: LlamaConfig, params: dict, cache_cap: int) -> "LlamaDecoder":
@@ -224,8 +224,7 @@ class LlamaDecoder:
                 w_qkv=rnd((nh, N, 3 * H // N // 4, D // 8, 4, 8), D ** -0.5),
                 w_out=rnd((nh, N, D // N, H), H ** -0.5), ffn_norm=rnd((D,), 0.1, 1.0),
                 w_gu=rnd((F // 2, D // 8, 4, 8), D ** -0.5),
-                w_dn=rnd((D // 4, F // 8, 4, 8) if cfg.engine == "layered" else (8, F // 2, D // 8, 2),
-                         F ** -0.5),
+                w_dn=rnd((D // 4, F // 8, 4, 8), F ** -0.5),
                 k_cache=rnd((nh, cache_cap, H), 1.0), v_cache=rnd((nh, cache_cap, H), 1.0)))
         m.embed = rnd((cfg.vocab, D), 1.0)
         m.final_norm = rnd((D,), 0.1, 1.0)
