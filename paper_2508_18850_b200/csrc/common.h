@@ -79,6 +79,7 @@ struct LlamaStepArgs {
   float* partials;
   unsigned long long* barrier;
   unsigned long long* counters;
+  unsigned long long* pool_ctr;  // [n_layers] gate/up work-stealing counters, or NULL (static)
   float* logits;
   float* cand_val;
   int* cand_idx;

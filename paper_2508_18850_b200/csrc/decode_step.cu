@@ -82,6 +82,8 @@ struct StepParams {
   float* partials;               // [nh][G][kPS]
   unsigned long long* barrier;   // grid barrier counter (monotonic)
   unsigned long long* counters;  // [2 * nh]: qkv_done, att_done (zeroed per step)
+  unsigned long long* pool_ctr;  // [L] gate/up work-stealing counters (monotonic)
+  int pool;                      // gate/up tiles per layer handed out dynamically
   float* logits;                 // [V]
   float* cand_val;               // [G]
   int* cand_idx;                 // [G]
@@ -93,7 +95,7 @@ struct StepParams {
 };
 
 struct StepLayout {
-  int bars, xs, part, gu, qf, dsm, red, misc, total, max_rows;
+  int bars, xs, part, gu, qf, dsm, red, tag, misc, total, max_rows;
 };
 
 __host__ __device__ inline int r16(int x) { return (x + 15) & ~15; }
@@ -119,6 +121,7 @@ __host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, 
   L.qf = o;    o += 3 * kH * 4 + kH * 2;  // q, k, v fp32 + fp16 A for the O projection
   L.dsm = o;   o += N * r16(3 * (kH / N) * 2) + N * r16((4 + kH) * 4);  // DSMEM gather | exchange
   L.red = o;   o += r16(kNumConsumerWarps * 4 * 2);
+  L.tag = o;   o += r16(kNumSlots * 4);  // gate/up pool: tile index per ring slot (-1: end)
   L.misc = o;  o += 64;
   L.total = o;
   return L;
@@ -220,6 +223,62 @@ __device__ __forceinline__ void attend(const float (&q)[kEPL], float& m, float& 
   }
 }
 
+// Work-stolen gate/up tail (the layered FFN kernel's CFB_DYN_POOL, here per
+// layer inside the persistent step): after its static tiles each producer
+// lane grabs whole tiles [T1s, T1s + pool) from a global counter and streams
+// their pieces into its own consumer warp's sub-ring, tagging each slot with
+// the tile; one failing grab per lane ends its pool (sentinel tag -1).  Each
+// layer has its own counter and a launch adds exactly pool + 8 G to it, so
+// floor(counter / per) * per read before this CTA's own failing grab is the
+// launch's base: the value cannot reach the next multiple of per until every
+// lane of every CTA (this one included) has failed.  (One shared counter is
+// not enough: in a small model a producer can run a whole layer ahead of a
+// CTA still waiting at a barrier.)
+__device__ __forceinline__ void produce_pool(const Ring& ring, int lane, uint64_t pol, int& c,
+                                            unsigned long long* ctr, int pool, int T1s,
+                                            const char* w_gu, int tileB, int* tag) {
+  const unsigned long long per = (unsigned long long)pool + 8ull * gridDim.x;
+  const unsigned long long base = (ld_acquire_u64(ctr) / per) * per;
+  const int npc = (tileB + kSlotBytes - 1) / kSlotBytes;
+  bool done = lane >= kNumConsumerWarps;
+  int cur = 0, piece = npc, nap = 32;
+  while (true) {
+    bool issued = false;
+    if (!done) {
+      const int sl = lane * ring.spw + (c % ring.spw);
+      if (mbar_test(&ring.empty[sl], ((c / ring.spw) & 1) ^ 1)) {
+        if (piece == npc) {
+          const long long t = (long long)(atomicAdd(ctr, 1ull) - base);
+          if (t >= pool) {
+            tag[sl] = -1;
+            mbar_arrive(&ring.full[sl]);
+            done = true;
+          } else {
+            cur = T1s + (int)t;
+            piece = 0;
+          }
+        }
+        if (!done) {
+          const int b0 = piece * kSlotBytes, nb = min(kSlotBytes, tileB - b0);
+          tag[sl] = cur;
+          mbar_arrive_expect_tx(&ring.full[sl], (uint32_t)nb);
+          bulk_g2s(ring.slot(sl), w_gu + (size_t)cur * tileB + b0, nb, &ring.full[sl], pol);
+          ++piece;
+        }
+        ++c;
+        issued = true;
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (__any_sync(0xffffffffu, issued)) {
+      nap = 32;
+    } else {
+      __nanosleep(nap);
+      nap = min(2 * nap, ring.sleep_max);
+    }
+  }
+}
+
 __device__ __forceinline__ void stamp(unsigned long long* tr, int k, int tid) {
   if (tr && tid == 0) tr[k] = globaltimer();
 }
@@ -288,7 +347,8 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     }
   }
   // FFN and LM head: contiguous tile ranges over all G CTAs
-  const int a0 = (int)split_at(T1, i, G), a1 = (int)split_at(T1, i + 1, G);
+  const int T1s = T1 - p.pool;  // gate/up tiles split statically; the rest is work-stolen
+  const int a0 = (int)split_at(T1s, i, G), a1 = (int)split_at(T1s, i + 1, G);
   const int u0 = (int)split_at(T2, i, G), u1 = (int)split_at(T2, i + 1, G);
   const int v0 = (int)split_at(TV, i, G), v1 = (int)split_at(TV, i + 1, G);
   const int seg_bytes = r16(3 * hp * 2), pay_bytes = r16((4 + kH) * 4);
@@ -349,8 +409,14 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   if (warp == kNumConsumerWarps) {  // ---------------------------- producer
     const uint64_t pol = policy_evict_first();
     int c = 0;
-    for (int l = 0; l < p.L; ++l)
-      produce_gen(kPhases, [&](int k) { return layer_phase(l, k); }, ring, lane, pol, c);
+    int* tag = reinterpret_cast<int*>(smem + Lo.tag);
+    for (int l = 0; l < p.L; ++l) {
+      produce_gen(7, [&](int k) { return layer_phase(l, k); }, ring, lane, pol, c);
+      if (p.pool > 0)
+        produce_pool(ring, lane, pol, c, p.pool_ctr + l, p.pool, T1s,
+                     reinterpret_cast<const char*>(p.w_gu[l]), 4 * D * 2, tag);
+      produce_gen(1, [&](int) { return layer_phase(l, 7); }, ring, lane, pol, c);
+    }
     produce_gen(1, [&](int) { return make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true); },
                 ring, lane, pol, c);
     __syncwarp();
@@ -654,6 +720,45 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       const float sl = __fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt)));
       p.act[2 * a0 + jj] = __float2half_rn(__fmul_rn(sl, up));
     }
+    if (p.pool > 0) {
+      // work-stolen tiles: whole tiles (npc pieces in this warp's consecutive
+      // slots); lanes 0..3 accumulate rows (gate 2t, gate 2t+1, up 2t, up 2t+1)
+      const int* tag = reinterpret_cast<const int*>(smem + Lo.tag);
+      const int tileB = 4 * D * 2, npc = (tileB + kSlotBytes - 1) / kSlotBytes;
+      const Phase P6 = layer_phase(l, 6);
+      while (true) {
+        const int sl = warp * ring.spw + (cnt % ring.spw);
+        mbar_wait(&ring.full[sl], (cnt / ring.spw) & 1);
+        const int t = tag[sl];
+        if (t < 0) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ring.empty[sl]);
+          ++cnt;
+          break;
+        }
+        float rowsum = 0.f;
+        for (int pc = 0; pc < npc; ++pc) {
+          const int s2 = warp * ring.spw + (cnt % ring.spw);
+          if (pc > 0) mbar_wait(&ring.full[s2], (cnt / ring.spw) & 1);
+          Item it;
+          it.unit0 = 0;
+          it.nunits = 1;
+          it.piece = pc;
+          it.byte0 = pc * kSlotBytes;
+          it.bytes = min(kSlotBytes, tileB - it.byte0);
+          tile_item<__half, 1, true>(P6, it, ring.slot(s2), xs, D, 1, lane,
+                                     [&](int, const float (&sm)[1]) { rowsum += sm[0]; });
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&ring.empty[s2]);
+          ++cnt;
+        }
+        const float up = __shfl_sync(0xffffffffu, rowsum, (lane & 1) + 2);
+        if (lane < 2) {
+          const float sl2 = __fdiv_rn(rowsum, __fadd_rn(1.0f, expf(-rowsum)));
+          p.act[2 * t + lane] = __float2half_rn(__fmul_rn(sl2, up));
+        }
+      }
+    }
     stamp(tr, 5, tid);
     bar_target += G;
     grid_sync(p.barrier, bar_target, tid);
@@ -846,6 +951,8 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.partials = a->partials;
   p.barrier = a->barrier;
   p.counters = a->counters;
+  p.pool_ctr = a->pool_ctr;
+  p.pool = a->pool_ctr ? (4 * G < a->inter / 8 ? 4 * G : a->inter / 8) : 0;
   p.logits = a->logits;
   p.cand_val = a->cand_val;
   p.cand_idx = a->cand_idx;
@@ -859,15 +966,17 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   cfg.blockDim = dim3(kThreads, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   if (a->cluster_attn) {
     // co-residency: G <= the GPCs' max active clusters (llama_step_grid)
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = N;
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeCooperative;  // all-or-nothing residency
+    at[1].val.cooperative = 1;
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = 2;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true>, p));
   } else {
     if (const int rc = configure_kernel((const void*)llama_step_kernel<false>, kMaxSmem, false)) return rc;

@@ -206,6 +206,7 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.partials = m->partials;
   a.barrier = m->pbarrier;
   a.counters = m->counters;
+  a.pool_ctr = m->pbarrier + 1;
   a.logits = m->logits;
   a.cand_val = m->cand_val;
   a.cand_idx = m->cand_idx;
@@ -309,7 +310,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
         (rc = alloc_zero(&m->pqkv, qkv_rows * 2)) ||
         (rc = alloc_zero((void**)&m->partials, (size_t)cfg->n_heads * sms * 132 * 4)) ||
 
-        (rc = alloc_zero((void**)&m->pbarrier, 8)) ||
+        (rc = alloc_zero((void**)&m->pbarrier, 8 * (1 + (size_t)L))) ||
         (rc = alloc_zero((void**)&m->counters, (size_t)2 * cfg->n_heads * 8)) ||
         (rc = alloc_zero((void**)&m->err, 4))) {
       cfb_llama_destroy(m);
