@@ -5,7 +5,11 @@
 
 One "step" = one decode token through the whole model (embed, 32 x
 [split_token attention module + fused SwiGLU FFN], LM head + argmax),
-replayed from a CUDA graph with weights and KV cache resident in HBM.
+replayed from a CUDA graph with weights and KV cache resident in HBM.  The
+default engine is the persistent whole-step kernel (csrc/decode_step.cu: ONE
+launch per token, the attention module of each head on a 4-CTA DSMEM
+cluster); the line also carries the layered engine (2 launches per layer) and
+the global-memory-exchange ablation at 1K / 16K for comparison.
 `value` is the mean TPOT (µs/token) over the context sweep; the per-context
 numbers are in `sweep`.  Inputs (13.5 GB of weights) are far larger than the
 126 MB L2, so no L2 flush is needed between steps.
@@ -98,19 +102,82 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------------- GPU arm
+def bench_config(ctxs, world, cluster):
+    """`config` of both arms (identical keys and values: the driver compares them)."""
+    return {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
+                        + "/".join(str(c) for c in ctxs) + ", cluster size 4 (configs[1]); "
+                        "value = mean TPOT over the sweep",
+            "model": "llama2-7b", "global_batch": 1, "contexts": list(ctxs),
+            "parallelism": f"tp{world}" if world > 1 else "single",
+            "cluster_size": cluster,
+            "l2": "inputs larger than L2 (13.5 GB weights streamed per token), no flush"}
+
+
+def trace_phases(model, ctx):
+    """Per-phase durations of the persistent step kernel (globaltimer stamps per
+    CTA and layer): median over CTAs, mean over layers, us."""
+    import torch
+    tr = model.set_trace(True)
+    model.set_state(ctx, 1)
+    model.step()
+    torch.cuda.synchronize()
+    t = tr.cpu().numpy().astype(np.float64)
+    model.set_trace(False)
+    names = ["qkv_gemv", "attention", "o_proj", "barrier_attn", "gate_up", "barrier_ffn",
+             "down_and_barrier"]
+    med = np.median(np.diff(t, axis=2), axis=1).mean(axis=0) / 1e3
+    layer = float(np.diff(np.median(t[:, :, 0], axis=1)).mean() / 1e3)
+    return {"ctx": ctx, "layer_us": round(layer, 2),
+            "phase_us": {n: round(float(v), 2) for n, v in zip(names, med)}}
+
+
+def time_engine(model, ctxs, steps, warmup, cfg, world=1, replay=None):
+    """CUDA-graph TPOT per context on the engine's stream (events), max over ranks."""
+    import torch
+    replay = replay or model.replay
+    st = model.stream
+    out = []
+    for ctx in ctxs:
+        model.set_state(ctx, 1)
+        for _ in range(warmup):
+            replay()
+        model.set_state(ctx, 1)
+        st.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(steps):
+            replay()
+        e1.record(st)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            ms = float(t.item())
+        tpot_us = ms * 1e3 / steps
+        mean_ctx = ctx + (steps - 1) / 2
+        out.append({"ctx": ctx, "tpot_us": round(tpot_us, 2),
+                    "bytes": cfg.step_bytes(int(mean_ctx)),
+                    "hbm_gbs": round(cfg.step_bytes(int(mean_ctx)) / (tpot_us * 1e-6) / 1e9, 1)})
+    return out
+
+
 def run_ours(args, rank, world):
     import torch
     import paper_2508_18850_b200 as cfb  # noqa: F401
     from paper_2508_18850_b200 import _native
     from paper_2508_18850_b200.llama import LLAMA2_7B, LlamaDecoder
     import ctypes
+    import dataclasses
 
     dev = torch.device("cuda", rank % max(torch.cuda.device_count(), 1))
     torch.cuda.set_device(dev)
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    cfg = LLAMA2_7B
+    cfg = dataclasses.replace(LLAMA2_7B, engine=args.engine)
     ctxs = [int(c) for c in args.contexts.split(",")]
     cap = max(ctxs) + args.warmup + args.steps + 8
     if world > 1:
@@ -135,36 +202,11 @@ def run_ours(args, rank, world):
     model.set_state(ctxs[0], 1)
     capture_fn()
     pk, pk_kind = peaks()
-    sweep = []
     sampler = ClockSampler(dev.index or 0)
     launches = 0
     with sampler:
-        for ctx in ctxs:
-            model.set_state(ctx, 1)
-            for _ in range(args.warmup):
-                replay_fn()
-            model.set_state(ctx, 1)
-            st.synchronize()
-            if world > 1:
-                torch.distributed.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(st)
-            for _ in range(args.steps):
-                replay_fn()
-            e1.record(st)
-            torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1)
-            if world > 1:
-                t = torch.tensor([ms], device=dev)
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-                ms = float(t.item())
-            launches += launches_per_step * args.steps
-            tpot_us = ms * 1e3 / args.steps
-            mean_ctx = ctx + (args.steps - 1) / 2
-            gbs = cfg.step_bytes(int(mean_ctx)) / (tpot_us * 1e-6) / 1e9  # whole job, all ranks
-            sweep.append({"ctx": ctx, "tpot_us": round(tpot_us, 2), "hbm_gbs": round(gbs, 1),
-                          "frac_of_peak": round(gbs / (world * pk["hbm_gbs"]), 4)})
-
+        sweep = time_engine(model, ctxs, args.steps, args.warmup, cfg, world, replay_fn)
+        launches += launches_per_step * (args.steps + args.warmup) * len(ctxs)
         # e2e: host token -> device (pinned H2D), graph, token -> host (pinned D2H), per step
         host_in = torch.ones(1, dtype=torch.int32).pin_memory()
         host_out = torch.zeros(1, dtype=torch.int32).pin_memory()
@@ -185,74 +227,55 @@ def run_ours(args, rank, world):
             e2e.append(dt * 1e6 / args.steps)
             launches += launches_per_step * args.steps
     clocks = sampler.summary()
+    for s_ in sweep:
+        s_["frac_of_peak"] = round(s_["hbm_gbs"] / (world * pk["hbm_gbs"]), 4)
 
-    # dominant kernel (fused FFN, 64% of weight bytes): avg launch duration with
-    # CUDA events on its stream, cycling through the 32 layers' weights
-    lcfg = tp.lcfg if tp is not None else cfg
-    ffn_bytes = 3 * lcfg.hidden * lcfg.inter * 2 + lcfg.hidden * 2
-    resid = torch.randn(1, cfg.hidden, device=dev)
-    out = torch.empty(1, cfg.hidden, device=dev)
-    act = torch.empty(lcfg.inter, device=dev, dtype=torch.float16)
-    bar = torch.zeros(1, device=dev, dtype=torch.int64)
-    accum = torch.zeros(1, cfg.hidden, device=dev, dtype=torch.int64)
-    fargs = []
-    for lyr in model.layers:
-        fargs.append(_native.FfnArgs(
-            dtype=2, batch=1, hidden=cfg.hidden, inter=lcfg.inter,
-            flags=_native.NORM | _native.RESID | _native.PDL, grid=0, eps=cfg.eps, x=None,
-            resid=resid.data_ptr(), accum=accum.data_ptr(), norm_w=lyr["ffn_norm"].data_ptr(), w_gu=lyr["w_gu"].data_ptr(),
-            w_dn=lyr["w_dn"].data_ptr(), act=act.data_ptr(), out=out.data_ptr(),
-            barrier=bar.data_ptr()))
-    torch.cuda.synchronize()
-    for a in fargs[:4]:
-        _native.check(L.cfb_ffn_decode(a, model._sp()))
-    reps = 4 * len(fargs)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for i in range(reps):
-        _native.check(L.cfb_ffn_decode(fargs[i % len(fargs)], model._sp()))
-    e1.record(st)
-    torch.cuda.synchronize()
-    ffn_us = e0.elapsed_time(e1) * 1e3 / reps
-    launches += reps
-    ffn_gbs = ffn_bytes / (ffn_us * 1e-6) / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "ffn_dram_bytes.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-
-    tpot = float(np.mean([s["tpot_us"] for s in sweep]))
+    tpot = float(np.mean([s_["tpot_us"] for s_ in sweep]))
     e2e_tpot = float(np.mean(e2e))
+    lcfg = tp.lcfg if tp is not None else cfg
     line = {
         "metric": METRIC, "value": round(tpot, 2), "unit": "us/token", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(tpot / 1e3, 4),
         "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "f16", "data": "synthetic (random fp16 weights + KV cache, device-drawn)",
-        "config": {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
-                               + "/".join(str(c) for c in ctxs) + ", cluster size 4 (configs[1]); "
-                               "value = mean TPOT over the sweep",
-                   "model": "llama2-7b", "global_batch": 1, "contexts": ctxs,
-                   "parallelism": f"tp{world}" if world > 1 else "single",
-                   "cluster_size": lcfg.cluster,
-                   "l2": "inputs larger than L2 (13.5 GB weights streamed per token), no flush"},
-        "sweep": sweep,
-        "achieved_hbm_gbs_mean": round(float(np.mean([s["hbm_gbs"] for s in sweep])), 1),
+        "vs_baseline": None, "dtype": "f16",
+        "data": "synthetic (random fp16 weights + KV cache, device-drawn)",
+        "config": bench_config(ctxs, world, lcfg.cluster),
+        "engine": cfg.engine if world == 1 else "layered (tensor parallel, NCCL between block halves)",
+        "sweep": [{k: v for k, v in s_.items() if k != "bytes"} for s_ in sweep],
+        "achieved_hbm_gbs_mean": round(float(np.mean([s_["hbm_gbs"] for s_ in sweep])), 1),
         "e2e": {"value": round(e2e_tpot, 2), "unit": "us/token", "h2d_bytes_per_step": 4,
                 "d2h_bytes_per_step": 4,
                 "path": "cfb_llama_write_token (pinned H2D) + cfb_llama_replay + cfb_llama_read "
                         "(pinned D2H) + stream sync, every step"},
-        "roofline": {"kernel": "ffn_swiglu_kernel (fused gate/up + SiLU*mul + down)",
-                     "bound": "hbm", "achieved": round(ffn_gbs, 1), "peak": pk["hbm_gbs"],
-                     "peak_kind": pk_kind, "unit": "GB/s", "frac": round(ffn_gbs / pk["hbm_gbs"], 4),
-                     "traffic": traffic, "bytes_per_launch": ffn_bytes,
-                     "avg_launch_us": round(ffn_us, 2)},
-        "gpu_launches": launches,
-        "clocks": clocks,
     }
+    traffic = None
+    prof = ROOT / "profiles" / "r02" / "ncu_step_kernel.json"
+    if world == 1 and cfg.engine == "persistent":
+        # dominant kernel = the ONLY kernel of a step: llama_step_kernel<cluster>;
+        # achieved = algorithmic bytes of all timed launches / their total time
+        tot_b = sum(s_["bytes"] * args.steps for s_ in sweep)
+        tot_t = sum(s_["tpot_us"] * 1e-6 * args.steps for s_ in sweep)
+        ach = tot_b / tot_t / 1e9
+        if prof.exists():
+            traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+        line["roofline"] = {
+            "kernel": "llama_step_kernel<true> (whole decode step: 32 x [attention module on "
+                      "4-CTA DSMEM clusters + fused SwiGLU FFN] + LM head + argmax; 1 launch/step)",
+            "bound": "hbm", "achieved": round(ach, 1), "peak": pk["hbm_gbs"], "peak_kind": pk_kind,
+            "unit": "GB/s", "frac": round(ach / pk["hbm_gbs"], 4), "traffic": traffic,
+            "traffic_ctx": 1024 if traffic else None,
+            "bytes_per_launch": {str(s_["ctx"]): s_["bytes"] for s_ in sweep},
+            "avg_launch_us": {str(s_["ctx"]): s_["tpot_us"] for s_ in sweep},
+            "launch_share_of_step": 1.0,
+            "phases": [trace_phases(model, c) for c in (ctxs[0], ctxs[-1])]}
+    line["gpu_launches"] = launches
+    line["clocks"] = clocks
     if world == 1 and not args.no_deepseek:
-        del model, fargs
+        del model
         torch.cuda.empty_cache()
-        for key, fn in (("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
+        for key, fn in (("engine_compare", lambda: engine_compare(cfg, [ctxs[0], ctxs[-1]], args, pk["hbm_gbs"])),
+                        ("dropin_attention_module", lambda: dropin_api(pk["hbm_gbs"])),
+                        ("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch16_ffn_tcgen05", lambda: batch16_ffn(cfg, pk["hbm_gbs"])),
                         ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096], pk["hbm_gbs"]))):
             try:  # secondary configs; never lose the headline line over one of them
@@ -262,7 +285,7 @@ def run_ours(args, rank, world):
             except Exception as exc:
                 line[key] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
     if world > 1 and not args.no_deepseek:
-        del model, fargs
+        del model
         torch.cuda.empty_cache()
         try:  # extra configs[4] line; never lose the TPOT line over it
             line["batch16_tp"] = batch16_tp(cfg, rank, world, 1024, pk["hbm_gbs"])
@@ -273,11 +296,69 @@ def run_ours(args, rank, world):
         except Exception as exc:  # pragma: no cover - multi-GPU only
             line["deepseek_tp"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
     if rank == 0 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(ctxs[:1], cfg, threads=os.cpu_count(), reps=1)
+        line["cpu_baseline"] = cpu_baseline(ctxs, cfg)
     if world > 1:
         torch.distributed.barrier()
         torch.distributed.destroy_process_group()
     return line
+
+
+def dropin_api(peak_gbs, S=1024, reps=10):
+    """configs[0]'s attention module through the reference-facing Python API
+    (run_fused_mha_decode: host numpy scenario in, DecodeResult out): the first
+    call (uploads + packs), a repeated call on the same scenario (device cache,
+    checksum-validated) and calls on a prepare()d handle with a new hidden
+    vector each time (weights resident)."""
+    import paper_2508_18850_b200 as cfb
+    dims = cfb.ModelDims(1, 4096, 32, 128, S, dtype_bytes=2)
+    sc = cfb.random_mha_scenario(dims, n_blocks=4, seed=0)
+    cfb.clear_device_cache()
+    t0 = time.perf_counter()
+    cfb.run_fused_mha_decode(sc)
+    cold = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    for _ in range(3):
+        cfb.run_fused_mha_decode(sc)
+    cached = (time.perf_counter() - t0) / 3
+    prep = cfb.prepare(sc)
+    hs = [np.random.default_rng(i).standard_normal((1, 4096)).astype(np.float16).astype(np.float32)
+          for i in range(reps)]
+    cfb.run_fused_mha_decode(prep.with_hidden(hs[0]))
+    t0 = time.perf_counter()
+    for h in hs:
+        cfb.run_fused_mha_decode(prep.with_hidden(h))
+    warm = (time.perf_counter() - t0) / reps
+    nbytes = 150994944 + 16384 * S  # module weights + one layer of KV at S positions
+    cfb.clear_device_cache()
+    return {"S": S, "cluster": 4, "first_call_ms": round(cold * 1e3, 2),
+            "cached_call_ms": round(cached * 1e3, 2), "prepared_call_ms": round(warm * 1e3, 3),
+            "module_bytes": nbytes, "launches": 2 * (reps + 5)}
+
+
+def engine_compare(cfg, ctxs, args, peak_gbs):
+    """The other B=1 engines on the same workload: the layered engine (split_token
+    cluster kernel + fused FFN kernel, 2 launches per layer) and the persistent
+    kernel with the attention exchange through global memory instead of DSMEM
+    (the paper's on-chip vs off-chip ablation)."""
+    import dataclasses
+    import torch
+    from paper_2508_18850_b200.llama import LlamaDecoder
+    out = []
+    for eng in ("layered", "persistent_flat"):
+        c = dataclasses.replace(cfg, engine=eng)
+        m = LlamaDecoder.random(c, cache_cap=max(ctxs) + args.warmup + args.steps + 8, seed=1234)
+        m.set_state(ctxs[0], 1)
+        m.step()
+        torch.cuda.synchronize()
+        m.set_state(ctxs[0], 1)
+        m.capture()
+        for s_ in time_engine(m, ctxs, args.steps, args.warmup, c):
+            out.append({"engine": eng, "ctx": s_["ctx"], "tpot_us": s_["tpot_us"],
+                        "hbm_gbs": s_["hbm_gbs"], "frac_of_peak": round(s_["hbm_gbs"] / peak_gbs, 4),
+                        "launches": m.launches_per_step * (args.steps + args.warmup)})
+        del m
+        torch.cuda.empty_cache()
+    return out
 
 
 def deepseek_sweep(ctxs, peak_gbs, layers=4, reps=16):
@@ -485,9 +566,8 @@ def deepseek_tp(rank, world, ctxs, peak_gbs, layers=4, reps=16):
 
 
 # --------------------------------------------------------------------- CPU arm
-def _block_sample(cfg, ctx, rng):
-    """fp32 numpy weights of ONE decoder block + a ctx-long cache (oracle inputs)."""
-    from oracle import clusterdec_port as cp  # noqa: F401
+def _block_weights(cfg, rng):
+    """fp32 numpy weights of ONE decoder block (oracle inputs, fp16-valued)."""
     D, F, nh, H = cfg.hidden, cfg.inter, cfg.n_heads, cfg.head_dim
 
     def f16(shape, scale):
@@ -495,16 +575,21 @@ def _block_sample(cfg, ctx, rng):
 
     return dict(x=f16((1, D), 1.0), g1=np.ones(D, np.float32), g2=np.ones(D, np.float32),
                 w_qkv=f16((nh, D, 3 * H), D ** -0.5), w_out=f16((nh, H, D), H ** -0.5),
-                w1=f16((F, D), D ** -0.5), w2=f16((F, D), D ** -0.5), w3=f16((D, F), F ** -0.5),
-                k=f16((nh, ctx, H), 1.0), v=f16((nh, ctx, H), 1.0))
+                w1=f16((F, D), D ** -0.5), w2=f16((F, D), D ** -0.5), w3=f16((D, F), F ** -0.5))
 
 
-def _block_once(cfg, s):
+def _kv(cfg, ctx, rng):
+    def f16(shape):
+        return rng.standard_normal(shape, dtype=np.float32).astype(np.float16).astype(np.float32)
+    return dict(k=f16((cfg.n_heads, ctx, cfg.head_dim)), v=f16((cfg.n_heads, ctx, cfg.head_dim)))
+
+
+def _block_once(cfg, w, kv):
     from oracle import clusterdec_port as cp
     from oracle import llama_port as lp
-    h = lp.rmsnorm_f16(s["x"], s["g1"], cfg.eps)
-    x = s["x"] + cp.dense_mha(h, s["w_qkv"], s["w_out"], s["k"], s["v"])
-    return x + lp.ffn_block(x, s["g2"], s["w1"], s["w2"], s["w3"], cfg.eps)
+    h = lp.rmsnorm_f16(w["x"], w["g1"], cfg.eps)
+    x = w["x"] + cp.dense_mha(h, w["w_qkv"], w["w_out"], kv["k"], kv["v"])
+    return x + lp.ffn_block(x, w["g2"], w["w1"], w["w2"], w["w3"], cfg.eps)
 
 
 def _lm_head_once(cfg, w, x):
@@ -512,37 +597,64 @@ def _lm_head_once(cfg, w, x):
     return int(np.argmax(lp.rmsnorm_f16(x, np.ones(cfg.hidden, np.float32), cfg.eps) @ w.T))
 
 
-def cpu_baseline(ctxs, cfg, threads, reps=1):
-    """Oracle (numpy port of the reference path) timed on the host: one block
-    per context x 32 layers + the LM head = TPOT estimate."""
+def cpu_info():
+    import platform
+    model = platform.processor()
     try:
-        from threadpoolctl import threadpool_limits
+        for l in open("/proc/cpuinfo"):
+            if l.startswith("model name"):
+                model = l.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        blas = [f"{d['internal_api']} {d.get('version')} ({d.get('architecture')}, "
+                f"{d.get('num_threads')} threads)" for d in threadpool_info() if d["user_api"] == "blas"]
     except ImportError:  # pragma: no cover
-        threadpool_limits = None
+        blas = []
+    return {"cpu_model": model, "os_cpu_count": os.cpu_count(), "blas": blas,
+            "numpy": np.__version__}
+
+
+def cpu_baseline(ctxs, cfg, reps=5):
+    """Oracle (numpy port of the reference path, reference oracle.py:30-52 +
+    :112-131 composed into a block) timed on the host: per context one block
+    (best and median of `reps` after a warm run) x 32 layers + the LM head,
+    at 1 thread and at all threads."""
+    from threadpoolctl import threadpool_limits
     rng = np.random.default_rng(0)
+    w = _block_weights(cfg, rng)
     w_lm = (rng.standard_normal((cfg.vocab, cfg.hidden), dtype=np.float32)
             * cfg.hidden ** -0.5).astype(np.float16).astype(np.float32)
-    vals = []
-    ctx_ = contextlib_null() if threadpool_limits is None else threadpool_limits(threads)
-    with ctx_:
-        for ctx in ctxs:
-            s = _block_sample(cfg, ctx, rng)
-            _block_once(cfg, s)  # warm
-            t = []
-            for _ in range(reps):
+    res = {}
+    for threads in (1, os.cpu_count()):
+        per = {}
+        with threadpool_limits(threads):
+            for ctx in ctxs:
+                kv = _kv(cfg, ctx, rng)
+                _block_once(cfg, w, kv)  # warm
+                t = []
+                for _ in range(reps):
+                    t0 = time.perf_counter()
+                    _block_once(cfg, w, kv)
+                    t.append(time.perf_counter() - t0)
                 t0 = time.perf_counter()
-                _block_once(cfg, s)
-                t.append(time.perf_counter() - t0)
-            t0 = time.perf_counter()
-            _lm_head_once(cfg, w_lm, s["x"])
-            lm = time.perf_counter() - t0
-            vals.append((min(t) * cfg.n_layers + lm) * 1e6)
-            del s
-    return {"value": round(float(np.mean(vals)), 1), "unit": "us/token", "cores": threads,
-            "kind": "port",
+                _lm_head_once(cfg, w_lm, w["x"])
+                lm = time.perf_counter() - t0
+                per[str(ctx)] = {"block_best_ms": round(min(t) * 1e3, 2),
+                                 "block_median_ms": round(float(np.median(t)) * 1e3, 2),
+                                 "tpot_us": round((min(t) * cfg.n_layers + lm) * 1e6, 1)}
+                del kv
+        res[threads] = per
+    allt = res[os.cpu_count()]
+    return {"value": round(float(np.mean([v["tpot_us"] for v in allt.values()])), 1),
+            "unit": "us/token", "cores": os.cpu_count(), "kind": "port",
             "sample": f"oracle numpy block (RMSNorm + dense_mha_decode + residual + RMSNorm + "
-                      f"SwiGLU ffn_reference + residual) at ctx {','.join(map(str, ctxs))}, B=1, "
-                      f"best of {reps}, x{cfg.n_layers} layers + LM head; OpenBLAS, {threads} threads"}
+                      f"SwiGLU ffn_reference + residual) at each ctx {ctxs}, B=1, best of {reps} "
+                      f"after a warm run, x{cfg.n_layers} layers + LM head; value = mean over "
+                      f"contexts at {os.cpu_count()} threads",
+            "per_ctx_all_threads": allt, "per_ctx_1_thread": res[1], "host": cpu_info()}
 
 
 class contextlib_null:
@@ -554,6 +666,8 @@ class contextlib_null:
 
 
 def run_reference(args, rank, world):
+    """Reference arm: the oracle port of the reference's CPU path on the host
+    cores, each step = one block per context x 32 layers + the LM head."""
     from paper_2508_18850_b200.llama import LLAMA2_7B
     cfg = LLAMA2_7B
     ctxs = [int(c) for c in args.contexts.split(",")]
@@ -564,7 +678,8 @@ def run_reference(args, rank, world):
     except ImportError:
         lim = contextlib_null()
     rng = np.random.default_rng(0)
-    samples = {c: _block_sample(cfg, c, rng) for c in ctxs}
+    w = _block_weights(cfg, rng)
+    kvs = {c: _kv(cfg, c, rng) for c in ctxs}
     w_lm = (rng.standard_normal((cfg.vocab, cfg.hidden), dtype=np.float32)
             * cfg.hidden ** -0.5).astype(np.float16).astype(np.float32)
     with lim:
@@ -572,10 +687,10 @@ def run_reference(args, rank, world):
             per = []
             for c in ctxs:
                 t0 = time.perf_counter()
-                _block_once(cfg, samples[c])
+                _block_once(cfg, w, kvs[c])
                 blk = time.perf_counter() - t0
                 t0 = time.perf_counter()
-                _lm_head_once(cfg, w_lm, samples[c]["x"])
+                _lm_head_once(cfg, w_lm, w["x"])
                 per.append((blk * cfg.n_layers + (time.perf_counter() - t0)) * 1e6)
             return float(np.mean(per))
         for _ in range(args.warmup):
@@ -587,16 +702,22 @@ def run_reference(args, rank, world):
               f"+ LM head, mean over contexts; {threads} threads")
     return {"metric": METRIC, "impl": "reference", "value": round(tpot, 1), "unit": "us/token",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(tpot / 1e3, 3), "higher_is_better": False, "scaling": "weak",
+            "ms_per_step": round(tpot / 1e3, 3), "higher_is_better": False,
+            "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32 (fp16-valued inputs)", "data": "synthetic",
-            "config": {"workload": "Llama2-7B full 32-layer greedy decode, batch 1, context sweep "
-                                   + "/".join(map(str, ctxs)) + " (configs[1]); value = mean TPOT",
-                       "model": "llama2-7b", "global_batch": 1, "contexts": ctxs,
-                       "parallelism": "cpu"},
+            "config": bench_config(ctxs, world, _local_cluster(cfg, world)),
             "cpu_baseline": {"value": round(tpot, 1), "unit": "us/token", "cores": threads,
-                             "kind": "port", "sample": sample},
+                             "kind": "port", "sample": sample, "host": cpu_info()},
             "e2e": {"value": round(tpot, 1), "unit": "us/token", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+
+
+def _local_cluster(cfg, world):
+    """cluster size the GPU arm reports for this N (tp.local_config)."""
+    if world <= 1:
+        return cfg.cluster
+    from paper_2508_18850_b200.tp import local_config
+    return local_config(cfg, world).cluster
 
 
 def main():
@@ -608,6 +729,7 @@ def main():
     ap.add_argument("--contexts", default="1024,2048,4096,8192,16384")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-deepseek", action="store_true")
+    ap.add_argument("--engine", default="persistent", choices=["persistent", "layered", "persistent_flat"])
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -13,6 +13,7 @@ from .exceptions import (BufferError, DimensionError, FixtureError, InvalidClust
 from .fused import (DATAFLOW_KINDS, FUSED_MLA, MERGED, SPLIT_HEAD, SPLIT_TOKEN,  # noqa: F401
                     TWO_PASS, DecodeResult, cluster_collective, run_dataflow,
                     run_fused_mha_decode, sequence_segments, validate_partitioning)
+from .devcache import PreparedScenario, clear_device_cache, prepare  # noqa: F401
 from .mla import run_fused_mla_decode, run_splithead_decode  # noqa: F401
 from .moe import MoeWeights, pack_moe, run_moe_decode  # noqa: F401
 from .ledger import (CollectiveTrace, StageTrace, TrafficBreakdown, TrafficEntry,  # noqa: F401
@@ -22,4 +23,4 @@ from .scenario import (MHA, MLA, ClusterConfig, DecodeScenario, ModelDims,  # no
                        project_new_kv, random_mha_scenario, random_mla_scenario,
                        with_preappended_cache)
 
-__version__ = "0.1.0"
+__version__ = "0.2.0"

@@ -61,8 +61,10 @@ class PagedKVPool:
         self.v = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
         self.free = list(range(n_pages))[::-1]
         self.pages = [[] for _ in range(BATCH)]
-        self.host_table = np.zeros((BATCH, max_pages), np.int32)
-        self.table = torch.zeros((BATCH, max_pages), device=dev, dtype=torch.int32)
+        # unassigned entries are -1 (never a real page: the kernels drop writes to
+        # them instead of aliasing page 0)
+        self.host_table = np.full((BATCH, max_pages), -1, np.int32)
+        self.table = torch.full((BATCH, max_pages), -1, device=dev, dtype=torch.int32)
 
     def reserve(self, seq: int, length: int) -> None:
         """Make positions 0 .. length-1 of ``seq`` addressable."""
@@ -89,8 +91,12 @@ class PagedKVPool:
     def release(self, seq: int) -> None:
         self.free.extend(reversed(self.pages[seq]))
         self.pages[seq] = []
-        self.host_table[seq] = 0
+        self.host_table[seq] = -1
         self._push()
+
+    def capacity(self, seq: int) -> int:
+        """Positions of ``seq`` currently addressable (reserved pages x 128)."""
+        return len(self.pages[seq]) * PAGE
 
     def write(self, layer: int, seq: int, start: int, k, v, stream=None) -> None:
         """Prefill writer: rows start .. start+count of ``seq`` from k, v
@@ -146,6 +152,9 @@ class BatchedLlama:
         D, nh, F = cfg.hidden, cfg.n_heads, cfg.inter
         self.rope = torch.from_numpy(rope_table(cache_cap, 128, cfg.rope_theta)).to(dev)
         self.pos = torch.zeros(BATCH, device=dev, dtype=torch.int32)
+        # host mirror of the device positions: every step / replay advances it,
+        # and a step is refused before it would write past a sequence's cache
+        self.host_pos = np.zeros(BATCH, np.int64)
         self.resid = torch.zeros(BATCH, D, device=dev, dtype=torch.float32)
         nchunks = (self.max_len + 127) // 128
         self.ws = dict(
@@ -275,25 +284,46 @@ class BatchedLlama:
         if advance:
             _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
 
+    def _limit(self, n: int) -> int:
+        """Positions sequence n can hold now: the contiguous cache / max_len, or
+        its reserved pages."""
+        lim = min(self.cap, self.max_len) if self.pool is None else min(self.max_len, self.pool.capacity(n))
+        return lim
+
+    def _check_room(self, steps: int = 1) -> None:
+        """Raise before a step would append past a sequence's cache."""
+        for n in range(BATCH):
+            if int(self.host_pos[n]) + steps > self._limit(n):
+                raise DimensionError(
+                    f"sequence {n}: position {int(self.host_pos[n])} + {steps} step(s) exceeds its "
+                    f"cache ({self._limit(n)} positions{'; reserve() more pages' if self.pool else ''})")
+
     def set_positions(self, pos) -> None:
         import torch
+        pos = np.asarray(pos, np.int64)
+        if pos.shape != (BATCH,) or (pos < 0).any():
+            raise DimensionError(f"set_positions needs {BATCH} non-negative positions")
         if self.pool:  # the new token's page must exist
             for n, p in enumerate(pos):
                 self.pool.reserve(n, int(p) + 1)
-        self.pos.copy_(torch.as_tensor(np.asarray(pos, np.int32)))
+        self.host_pos = pos.copy()
+        self._check_room(1)
+        self.pos.copy_(torch.as_tensor(pos.astype(np.int32)))
         torch.cuda.synchronize()
 
     def reserve(self, steps: int) -> None:
         """Paged mode: make the next ``steps`` positions of every sequence
         addressable (call before replaying a captured graph that far)."""
         if self.pool:
-            pos = self.pos.cpu().numpy()
             for n in range(BATCH):
-                self.pool.reserve(n, int(pos[n]) + steps)
+                self.pool.reserve(n, int(self.host_pos[n]) + steps)
 
     def step(self, advance: bool = True) -> None:
         """resid <- the layer stack applied to resid for all 16 sequences."""
+        self._check_room(1)
         self._enqueue(advance)
+        if advance:
+            self.host_pos += 1
 
     def capture(self) -> None:
         import torch
@@ -303,8 +333,10 @@ class BatchedLlama:
 
     def replay(self) -> None:
         import torch
+        self._check_room(1)
         with torch.cuda.stream(self.stream):
             self.graph.replay()
+        self.host_pos += 1  # every captured step advances the positions
 
     # ---------------------------------------------------------------- greedy decode
     def set_head(self, embed, final_norm, lm_head) -> None:
@@ -367,8 +399,10 @@ class BatchedLlama:
         """One greedy step for all 16 sequences: tokens -> embed -> layers ->
         LM head -> argmax -> tokens; positions advance."""
         import torch
+        self._check_room(1)
         with torch.cuda.stream(self.stream):
             self._enqueue_decode(logits)
+        self.host_pos += 1
 
     def capture_decode(self) -> None:
         import torch

@@ -50,9 +50,13 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int L = pos[n] + 1, p0 = c * kBaChunk, p1 = min(L, p0 + kBaChunk);
   if (p0 >= p1) return;  // beyond this sequence: not part of its merge
-  const int n_rows = p1 - p0, nused = (L + kBaChunk - 1) / kBaChunk;
-  // paged: chunk c of a sequence is exactly its page c (CFB_KV_PAGE == kBaChunk)
-  const size_t base = table ? ((size_t)table[n * maxp + c] * nh + h) * (size_t)kBaChunk * 128
+  // nused <= the launched chunks even for a position past max_len (the host
+  // rejects that; the clamp keeps the merge ticket consistent regardless)
+  const int n_rows = p1 - p0, nused = min((L + kBaChunk - 1) / kBaChunk, nchunks);
+  // paged: chunk c of a sequence is exactly its page c (CFB_KV_PAGE == kBaChunk);
+  // an unassigned entry (-1) reads page 0 instead of faulting (host-validated)
+  const int pg = table ? max(table[n * maxp + c], 0) : 0;
+  const size_t base = table ? ((size_t)pg * nh + h) * (size_t)kBaChunk * 128
                             : (((size_t)n * nh + h) * cap + p0) * 128;
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -195,6 +199,7 @@ int batch_attention(const __half* q, const __half* kc, const __half* vc, const i
 __global__ void kv_write_kernel(__half* kc, __half* vc, const int* table, int maxp, int cap, int nh, int seq,
                                 int start, int count, const __half* ks, const __half* vs) {
   const int r = blockIdx.x, h = blockIdx.y, t = threadIdx.x, p = start + r;
+  if (table && table[seq * maxp + p / kBaChunk] < 0) return;  // unassigned page
   const size_t dst = table ? (((size_t)table[seq * maxp + p / kBaChunk] * nh + h) * kBaChunk + p % kBaChunk) * 128
                            : (((size_t)seq * nh + h) * cap + p) * 128;
   const size_t src = ((size_t)h * count + r) * 128;

@@ -275,16 +275,24 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
           a[e] = __float2half_rn(x1);
           b[e] = __float2half_rn(x2);
         }
-        __half* dst;
+        __half* dst = nullptr;
         if (kind == 0) {
           dst = Q.q + (size_t)nn * Q.nh * 128 + hd * 128;
         } else {
+          // never write outside the sequence's cache: an unassigned page (-1) or a
+          // position past the capacity drops the row (the host rejects both)
           __half* cache = kind == 1 ? Q.k_cache : Q.v_cache;
-          dst = Q.table ? cache + (((size_t)Q.table[nn * Q.maxp + ps / 128] * Q.nh + hd) * 128 + ps % 128) * 128
-                        : cache + (((size_t)nn * Q.nh + hd) * Q.cap + ps) * 128;
+          if (Q.table) {
+            const int pg = ps / 128 < Q.maxp ? Q.table[nn * Q.maxp + ps / 128] : -1;
+            if (pg >= 0) dst = cache + (((size_t)pg * Q.nh + hd) * 128 + ps % 128) * 128;
+          } else if (ps < Q.cap) {
+            dst = cache + (((size_t)nn * Q.nh + hd) * Q.cap + ps) * 128;
+          }
         }
-        *reinterpret_cast<uint4*>(dst + i0) = *reinterpret_cast<const uint4*>(a);
-        *reinterpret_cast<uint4*>(dst + 64 + i0) = *reinterpret_cast<const uint4*>(b);
+        if (dst) {
+          *reinterpret_cast<uint4*>(dst + i0) = *reinterpret_cast<const uint4*>(a);
+          *reinterpret_cast<uint4*>(dst + 64 + i0) = *reinterpret_cast<const uint4*>(b);
+        }
       } else if (p.mode == kTcSwiGLU) {
         // tile rows: 64 gate rows (f = 64t + j) then the 64 matching up rows;
         // f-range of tile t = K-block t of the next projection.  All loads of a

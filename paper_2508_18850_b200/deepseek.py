@@ -159,7 +159,7 @@ class DeepSeekBlock:
             mla, eng = None, pack_mla_engine(*(mla_arrays[k] for k in ("w_q", "w_up", "w_kv", "w_down",
                                                                        "w_out", "kv_cache")), dev)
         else:
-            mla, eng = pack_mla(sc, dev, torch.float16), None
+            mla, eng = pack_mla(sc, dev, torch.float16, cached=False), None
         moe = pack_moe(moe_w, dims.top_k, dims.routed_scale, dev)
 
         def g(a):
@@ -193,7 +193,7 @@ class DeepSeekBlock:
             sc = SimpleNamespace(dims=md, cluster=SimpleNamespace(n_blocks=dims.cluster),
                                  hidden=np.zeros((batch, D), np.float32),
                                  **{k: v.cpu().numpy() for k, v in arrs.items()})
-            mla, eng = pack_mla(sc, dev, torch.float16), None
+            mla, eng = pack_mla(sc, dev, torch.float16, cached=False), None
         del arrs
         moe = random_moe_device(dims.hidden, dims.n_experts, dims.inter, dims.n_shared, dims.top_k,
                                 seed=seed, routed_scale=dims.routed_scale, device=dev)

@@ -108,11 +108,61 @@ def _finish_output(out: np.ndarray) -> np.ndarray:
     return out
 
 
+def _pack_mha_static(scenario, cached: bool = True) -> dict:
+    """Packed device copies of the scenario's weights and KV cache (the
+    per-call state is only the hidden vector): through the DeviceCache
+    (checksum-validated) or freshly built for ``prepare``."""
+    import torch
+    from .devcache import CACHE
+    dev = _native.require_cuda()
+    d = scenario.dims
+    n, nb = scenario.cluster.n_blocks, d.dtype_bytes
+    D, nh, H, S = d.hidden_dim, d.n_heads, d.head_dim, d.seq_len
+    dt = torch.float16 if nb == 2 else torch.float32
+    Hp = pow2_at_least(H)
+    Dp = padded_hidden(D, n, nb)
+
+    def up(a):
+        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+
+    def get(arr, tag, build):
+        return CACHE.get(arr, tag, build) if cached else build(arr)
+
+    def b_qkv(a):  # w_qkv (nh, D, 3H) -> row tiles [head][rank][q|k|v slice][D']
+        return qkv_tiles(up(a).to(dt), n, Hp, Dp)
+
+    def b_wo(a):
+        wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
+        wo[:, :D, :H] = up(a).transpose(1, 2).to(dt)
+        return wo_rows(wo, n)
+
+    def b_cache(a):
+        c = torch.zeros(nh, max(S, 1), Hp, device=dev, dtype=dt)
+        if S:
+            c[:, :S, :H] = up(a).to(dt)
+        return c
+
+    with torch.no_grad():
+        return dict(w_qkv=get(scenario.w_qkv, ("mha_qkv", n, Hp, Dp, nb), b_qkv),
+                    w_out=get(scenario.w_out, ("mha_wo", n, Hp, Dp, nb), b_wo),
+                    k_cache=get(scenario.k_cache, ("mha_kv", Hp, nb, S), b_cache),
+                    v_cache=get(scenario.v_cache, ("mha_kv", Hp, nb, S), b_cache),
+                    Hp=Hp, Dp=Dp, cap=max(S, 1))
+
+
 def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
                          append_new_token: bool = True) -> DecodeResult:
-    """split_token fused attention module on the GPU (one cluster per head)."""
-    import torch
+    """split_token fused attention module on the GPU (one cluster per head).
 
+    ``scenario`` is a ``DecodeScenario`` (packed weights come from the
+    checksum-validated device cache) or the ``PreparedScenario`` of
+    ``prepare(scenario)`` (device-resident, no per-call re-validation)."""
+    import torch
+    from .devcache import PreparedScenario
+
+    prepared = scenario if isinstance(scenario, PreparedScenario) else None
+    if prepared is not None:
+        scenario = prepared.scenario
     validate_partitioning(scenario, SPLIT_TOKEN, append_new_token)
     validate_scenario(scenario)
     if stats_mode not in (TWO_PASS, MERGED, ONESHOT):
@@ -122,27 +172,12 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
     n, nb = scenario.cluster.n_blocks, d.dtype_bytes
     B, D, nh, H, S = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.seq_len
     dt = torch.float16 if nb == 2 else torch.float32
-    Hp = pow2_at_least(H)
-    Dp = padded_hidden(D, n, nb)
-    hp = Hp // n
-
-    def up(a):
-        return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
+    pk = prepared.packed if prepared is not None else _pack_mha_static(scenario)
+    Hp, Dp, cap = pk["Hp"], pk["Dp"], pk["cap"]
 
     with torch.no_grad():
         x = torch.zeros(B, Dp, device=dev, dtype=dt)
-        x[:, :D] = up(scenario.hidden).to(dt)
-        # w_qkv (nh, D, 3H) -> row tiles [head][rank][q|k|v slice][D']
-        w_qkv = qkv_tiles(up(scenario.w_qkv).to(dt), n, Hp, Dp)
-        wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
-        wo[:, :D, :H] = up(scenario.w_out).transpose(1, 2).to(dt)
-        wo = wo_rows(wo, n)
-        cap = max(S, 1)
-        kc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)
-        vc = torch.zeros(nh, cap, Hp, device=dev, dtype=dt)
-        if S:
-            kc[:, :S, :H] = up(scenario.k_cache).to(dt)
-            vc[:, :S, :H] = up(scenario.v_cache).to(dt)
+        x[:, :D] = torch.from_numpy(np.ascontiguousarray(scenario.hidden, np.float32)).to(dev).to(dt)
         out = torch.empty(B, Dp, device=dev, dtype=torch.float32)
         L = _native.lib()
         accum = torch.zeros(B, Dp, device=dev, dtype=torch.int64)
@@ -153,8 +188,8 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
         args = _native.MhaArgs(
             dtype=nb, batch=B, hidden=Dp, n_heads=nh, head_dim=H, head_pad=Hp, cluster=n,
             seq_len=S, cache_cap=cap, flags=flags, x=x.data_ptr(), eps=0.0,
-            w_qkv=w_qkv.data_ptr(), w_out=wo.data_ptr(), k_cache=kc.data_ptr(),
-            v_cache=vc.data_ptr(), out=out.data_ptr(), accum=accum.data_ptr(),
+            w_qkv=pk["w_qkv"].data_ptr(), w_out=pk["w_out"].data_ptr(), k_cache=pk["k_cache"].data_ptr(),
+            v_cache=pk["v_cache"].data_ptr(), out=out.data_ptr(), accum=accum.data_ptr(),
             stats=stats.data_ptr(), traffic=traffic.data_ptr())
         _native.check(L.cfb_mha_decode(args, _native.stream_ptr()))
         torch.cuda.synchronize()

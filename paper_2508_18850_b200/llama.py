@@ -37,9 +37,11 @@ class LlamaConfig:
     rope_theta: float = 10000.0
     cluster: int = 4
     dtype_bytes: int = 2
-    # "persistent": one launch per step on every SM (csrc/decode_step.cu);
-    # "layered": split_token cluster kernel + fused FFN per layer (csrc/llama.cu)
-    engine: str = "layered"
+    # "persistent": one launch per step on every SM, attention on DSMEM clusters
+    # (csrc/decode_step.cu); "persistent_flat": same, attention exchange through
+    # global memory (ablation); "layered": split_token cluster kernel + fused
+    # FFN kernel per layer, PDL-chained (csrc/llama.cu; the tensor-parallel path)
+    engine: str = "persistent"
 
     def weight_bytes(self) -> int:
         """Bytes of every weight a decode step streams (attention + FFN + norms,
@@ -188,20 +190,24 @@ class LlamaDecoder:
         so host memory holds one fp32 layer at a time) plus the globals
         (embed, final_norm, lm_head)."""
         m = cls(cfg, cache_cap)
-        torch = m.torch
         for lp in layers:
             m.layers.append(m._pack_layer(lp))
-        if len(m.layers) != cfg.n_layers:
-            raise DimensionError(f"got {len(m.layers)} layers, config has {cfg.n_layers}")
-        params = globals_
+        m.adopt_globals(globals_)
+        return m
+
+    def adopt_globals(self, g: dict) -> None:
+        """Upload embed / final_norm / lm_head once every layer is packed, then
+        create the native engine."""
+        if len(self.layers) != self.cfg.n_layers:
+            raise DimensionError(f"got {len(self.layers)} layers, config has {self.cfg.n_layers}")
+        torch = self.torch
 
         def t(a):
-            return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(m.dev).half()
+            return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(self.dev).half()
 
-        m.embed, m.final_norm = t(params["embed"]), t(params["final_norm"])
-        m.lm_head = row_tiles(t(params["lm_head"]))
-        m._finish()
-        return m
+        self.embed, self.final_norm = t(g["embed"]), t(g["final_norm"])
+        self.lm_head = row_tiles(t(g["lm_head"]))
+        self._finish()
 
     @classmethod
     def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0) -> "LlamaDecoder":

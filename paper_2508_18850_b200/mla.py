@@ -23,11 +23,15 @@ from .ledger import StageTrace, TrafficLedger, emit_gather, emit_reduce
 from .scenario import validate_scenario
 
 
-def pack_mla(sc, dev, dt):
-    """DecodeScenario (MLA) -> dict of device tensors in cfb_mla_args layouts."""
+def _pack_mla_static(sc, cached: bool = True) -> dict:
+    """MLA weights + latent cache in cfb_mla_args layouts, through the
+    checksum-validated DeviceCache (or freshly built for ``prepare``)."""
     import torch
+    from .devcache import CACHE
+    dev = _native.require_cuda()
     d = sc.dims
     n, nb = sc.cluster.n_blocks, d.dtype_bytes
+    dt = torch.float16 if nb == 2 else torch.float32
     B, D, nh, H, R = d.batch_size, d.hidden_dim, d.n_heads, d.head_dim, d.kv_lora_rank
     S = d.seq_len
     Hp, Rp = pow2_at_least(H), pow2_at_least(R)
@@ -38,34 +42,69 @@ def pack_mla(sc, dev, dt):
     def up(a):
         return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(dev)
 
-    x = torch.zeros(B, Dp, device=dev, dtype=dt)
-    x[:, :D] = up(sc.hidden).to(dt)
-    wq = torch.zeros(nh, Dp, H, device=dev, dtype=dt)
-    wq[:, :D, :] = up(sc.w_q).to(dt)                        # (nh, Dp, H)
-    wq = wq.reshape(nh, Dp, n, h).permute(0, 2, 3, 1)         # (nh, N, h, Dp)
-    wkv = torch.zeros(Dp, R, device=dev, dtype=dt)
-    wkv[:D] = up(sc.w_kv).to(dt)
-    wkv = wkv.reshape(Dp, n, rs).permute(1, 2, 0)              # (N, rs, Dp)
-    wup = torch.zeros(nh, Hp, R, device=dev, dtype=dt)
-    wup[:, :H] = up(sc.w_up).to(dt)
-    wup = wup.reshape(nh, Hp, n, rs).permute(0, 2, 3, 1)      # (nh, N, rs, Hp)
-    wdn = torch.zeros(nh, n, rsp, Hp, device=dev, dtype=dt)
-    wdn[:, :, :rs, :H] = up(sc.w_down).to(dt).reshape(nh, n, rs, H)
-    wdn = wdn.transpose(2, 3)                                  # (nh, N, Hp, rsp)
-    wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
-    wo[:, :D, :H] = up(sc.w_out).transpose(1, 2).to(dt)
-    cache = torch.zeros(max(S, 1), Rp, device=dev, dtype=dt)
-    if S:
-        cache[:S, :R] = up(sc.kv_cache).to(dt)
-    return dict(x=x, w_q=row_tiles(wq.contiguous()), w_kv=row_tiles(wkv.contiguous()),
-                w_up=rotated_rows(wup.contiguous()), w_down=rotated_rows(wdn.contiguous()),
-                w_out=wo_rows(wo, n), cache=cache, Dp=Dp, Hp=Hp, Rp=Rp)
+    def get(arr, tag, build):
+        return CACHE.get(arr, ("mla",) + tag, build) if cached else build(arr)
+
+    def b_q(a):
+        wq = torch.zeros(nh, Dp, H, device=dev, dtype=dt)
+        wq[:, :D, :] = up(a).to(dt)                              # (nh, Dp, H)
+        return row_tiles(wq.reshape(nh, Dp, n, h).permute(0, 2, 3, 1).contiguous())  # (nh, N, h, Dp)
+
+    def b_kv(a):
+        wkv = torch.zeros(Dp, R, device=dev, dtype=dt)
+        wkv[:D] = up(a).to(dt)
+        return row_tiles(wkv.reshape(Dp, n, rs).permute(1, 2, 0).contiguous())       # (N, rs, Dp)
+
+    def b_up(a):
+        wup = torch.zeros(nh, Hp, R, device=dev, dtype=dt)
+        wup[:, :H] = up(a).to(dt)
+        return rotated_rows(wup.reshape(nh, Hp, n, rs).permute(0, 2, 3, 1).contiguous())
+
+    def b_dn(a):
+        wdn = torch.zeros(nh, n, rsp, Hp, device=dev, dtype=dt)
+        wdn[:, :, :rs, :H] = up(a).to(dt).reshape(nh, n, rs, H)
+        return rotated_rows(wdn.transpose(2, 3).contiguous())     # (nh, N, Hp, rsp)
+
+    def b_out(a):
+        wo = torch.zeros(nh, Dp, Hp, device=dev, dtype=dt)
+        wo[:, :D, :H] = up(a).transpose(1, 2).to(dt)
+        return wo_rows(wo, n)
+
+    def b_cache(a):
+        c = torch.zeros(max(S, 1), Rp, device=dev, dtype=dt)
+        if S:
+            c[:S, :R] = up(a).to(dt)
+        return c
+
+    key = (n, nb, Hp, Rp, Dp)
+    with torch.no_grad():
+        return dict(w_q=get(sc.w_q, ("q",) + key, b_q), w_kv=get(sc.w_kv, ("kv",) + key, b_kv),
+                    w_up=get(sc.w_up, ("up",) + key, b_up), w_down=get(sc.w_down, ("dn",) + key, b_dn),
+                    w_out=get(sc.w_out, ("out",) + key, b_out),
+                    cache=get(sc.kv_cache, ("cache", S) + key, b_cache), Dp=Dp, Hp=Hp, Rp=Rp)
+
+
+def pack_mla(sc, dev, dt, cached: bool = True, packed: dict | None = None):
+    """DecodeScenario (MLA) -> dict of device tensors in cfb_mla_args layouts
+    (static weights from the device cache / a prepared handle + the hidden)."""
+    import torch
+    pk = dict(packed if packed is not None else _pack_mla_static(sc, cached))
+    d = sc.dims
+    x = torch.zeros(d.batch_size, pk["Dp"], device=dev, dtype=dt)
+    x[:, :d.hidden_dim] = torch.from_numpy(np.ascontiguousarray(sc.hidden, np.float32)).to(dev).to(dt)
+    pk["x"] = x
+    return pk
 
 
 def run_fused_mla_decode(scenario, stats_mode: str = TWO_PASS,
                          append_new_token: bool = True) -> DecodeResult:
-    """fused_mla latent attention on the GPU (one cluster per head)."""
+    """fused_mla latent attention on the GPU (one cluster per head); takes a
+    scenario or its ``prepare``d handle (devcache.py)."""
     import torch
+    from .devcache import PreparedScenario
+    prepared = scenario if isinstance(scenario, PreparedScenario) else None
+    if prepared is not None:
+        scenario = prepared.scenario
     validate_partitioning(scenario, FUSED_MLA, append_new_token)
     validate_scenario(scenario)
     if stats_mode not in (TWO_PASS, MERGED):
@@ -78,7 +117,7 @@ def run_fused_mla_decode(scenario, stats_mode: str = TWO_PASS,
         raise DimensionError("the fused_mla kernel supports batch <= 4")
     dt = torch.float16 if nb == 2 else torch.float32
     with torch.no_grad():
-        pk = pack_mla(scenario, dev, dt)
+        pk = pack_mla(scenario, dev, dt, packed=prepared.packed if prepared is not None else None)
         out = torch.empty(B, pk["Dp"], device=dev, dtype=torch.float32)
         accum = torch.zeros(B, pk["Dp"], device=dev, dtype=torch.int64)
         stats = torch.zeros(nh, 2, B, device=dev, dtype=torch.float32)

@@ -53,8 +53,10 @@ def local_config(cfg: LlamaConfig, world: int, cluster: int | None = None) -> Ll
         cluster = cfg.cluster
         while nh * cluster < 128 and cluster < 16 and cfg.head_dim % (2 * cluster) == 0:
             cluster *= 2
+    # ranks are driven part by part with a collective between block halves:
+    # the layered engine (the persistent step kernel has no cross-GPU exchange)
     return replace(cfg, n_heads=nh, inter=cfg.inter // world, vocab=cfg.vocab // world,
-                   cluster=cluster)
+                   cluster=cluster, engine="layered")
 
 
 def shard_layer(lp: dict, rank: int, world: int) -> dict:
@@ -242,7 +244,7 @@ class TPBatchedLlama:
         self.cfg, self.rank, self.world, self.group = cfg, rank, world, group
         nh = cfg.n_heads // world
         Fp = -(-(cfg.inter // world) // 64) * 64
-        self.lcfg = replace(cfg, n_heads=nh, inter=Fp)
+        self.lcfg = replace(cfg, n_heads=nh, inter=Fp, engine="layered")
         if params is not None:
             hs = slice(rank * nh, (rank + 1) * nh)
             layers = [shard_layer_b16(lp, rank, world) for lp in params["layers"]]
@@ -271,8 +273,10 @@ class TPBatchedLlama:
 
     def step(self) -> None:
         import torch
+        self.m._check_room(1)
         with torch.cuda.stream(self.m.stream):
             self._enqueue()
+        self.m.host_pos += 1
 
     def capture(self) -> None:
         import torch
@@ -282,8 +286,10 @@ class TPBatchedLlama:
 
     def replay(self) -> None:
         import torch
+        self.m._check_room(1)
         with torch.cuda.stream(self.m.stream):
             self.graph.replay()
+        self.m.host_pos += 1
 
 
 # --------------------------------------------------------------------------

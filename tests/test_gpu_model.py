@@ -104,27 +104,35 @@ def _teacher_forced(cfg, prefill, steps, seed, atol):
     return m, margins
 
 
-def test_llama_small_teacher_forced_greedy():
+ENGINES = ["persistent", "layered"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_llama_small_teacher_forced_greedy(engine):
     cfg = LlamaConfig(n_layers=3, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      cluster=4)
+                      cluster=4, engine=engine)
     _teacher_forced(cfg, prefill=37, steps=6, seed=1, atol=2e-2)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("cluster", [2, 8, 16])
-def test_llama_small_cluster_sizes(cluster):
+def test_llama_small_cluster_sizes(cluster, engine):
     cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
-                      cluster=cluster)
+                      cluster=cluster, engine=engine)
     _teacher_forced(cfg, prefill=50, steps=3, seed=2, atol=2e-2)
 
 
-def test_llama_full_width_two_layers():
+@pytest.mark.parametrize("engine", ENGINES)
+def test_llama_full_width_two_layers(engine):
     """Llama2-7B widths (D=4096, 32x128 heads, F=11008, V=32000), 2 layers, S=1000."""
-    cfg = LlamaConfig(n_layers=2)
+    cfg = LlamaConfig(n_layers=2, engine=engine)
     _teacher_forced(cfg, prefill=1000, steps=3, seed=3, atol=2e-2)
 
 
-def test_graph_replay_matches_eager():
-    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000)
+@pytest.mark.parametrize("engine", ENGINES)
+def test_graph_replay_matches_eager(engine):
+    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
+                      engine=engine)
     params = random_llama_params(cfg, seed=5, prefill=20)
     m = LlamaDecoder.from_params(cfg, params, cache_cap=64)
     eager = m.generate(first_token=3, pos=20, n_tokens=8, use_graph=False)

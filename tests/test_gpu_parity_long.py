@@ -21,6 +21,8 @@ greedy tokens equal, unconditionally, with the oracle's top-2 margins printed.
 
 from __future__ import annotations
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -66,9 +68,9 @@ def test_split_token_llama_module_long_context(S):
     assert cfb.reconcile_traffic("split_token", res, sc.dims).reconciled
 
 
-def _teacher_forced_layer_major(cfg, prefill, tokens, seed):
+def _teacher_forced_layer_major(cfg, prefill, tokens, seed, engines=("persistent",)):
     """Run the oracle layer by layer over all teacher-forced tokens while the
-    engine is packed from the same layers; returns (engine, oracle logits)."""
+    engines are packed from the same layers; returns (engines, oracle logits)."""
     T = len(tokens)
     cap = prefill + T + 1
     g = random_llama_globals(cfg, seed)
@@ -92,10 +94,21 @@ def _teacher_forced_layer_major(cfg, prefill, tokens, seed):
             yield L
             del L, kc, vc
 
-    m = LlamaDecoder.from_layers(cfg, layers(), g, cache_cap=cap)
+    ms = [LlamaDecoder(dataclasses.replace(cfg, engine=e), cap) for e in engines]
+
+    def pack_all():
+        for L in layers():
+            for m in ms:
+                m.layers.append(m._pack_layer(L))
+            yield L
+
+    for _ in pack_all():
+        pass
+    for m in ms:
+        m.adopt_globals(g)
     hf = lp.rmsnorm_f16(x, g["final_norm"], cfg.eps)
     logits = (hf @ g["lm_head"].T).astype(np.float32)
-    return m, logits
+    return ms, logits
 
 
 def _check_engine(m, tokens, prefill, ref_logits):
@@ -115,11 +128,13 @@ def _check_engine(m, tokens, prefill, ref_logits):
 
 @pytest.mark.parametrize("prefill", [4095, 16383])
 def test_engine_full_width_long_prefill(prefill):
-    """Llama2-7B widths, 2 layers, the benched 4K / 16K contexts."""
+    """Llama2-7B widths, 2 layers, the benched 4K / 16K contexts (both engines)."""
     cfg = LlamaConfig(n_layers=2)
     tokens = [7, 3051, 29999]
-    m, ref = _teacher_forced_layer_major(cfg, prefill, tokens, seed=40 + prefill % 7)
-    _check_engine(m, tokens, prefill, ref)
+    ms, ref = _teacher_forced_layer_major(cfg, prefill, tokens, seed=40 + prefill % 7,
+                                          engines=("persistent", "layered"))
+    for m in ms:
+        _check_engine(m, tokens, prefill, ref)
 
 
 def test_engine_32_layers_1k():
@@ -129,7 +144,7 @@ def test_engine_32_layers_1k():
     cfg = LlamaConfig()
     tokens = [7, 3051, 29999]
     prefill = 1024
-    m, ref = _teacher_forced_layer_major(cfg, prefill, tokens, seed=77)
+    (m,), ref = _teacher_forced_layer_major(cfg, prefill, tokens, seed=77)
     _check_engine(m, tokens, prefill, ref)
     # the CUDA-graph replay path (what bench.py times) gives the same tokens
     got = []

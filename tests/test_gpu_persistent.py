@@ -65,7 +65,8 @@ def test_persistent_reads_any_split_token_layout(cluster, engine):
 
 @pytest.mark.parametrize("engine", ENGINES)
 def test_persistent_matches_layered_tokens_graph(engine):
-    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000)
+    cfg = LlamaConfig(n_layers=2, hidden=512, n_heads=4, head_dim=128, inter=1376, vocab=1000,
+                      engine="layered")
     params = random_llama_params(cfg, seed=5, prefill=20)
     a = LlamaDecoder.from_params(cfg, params, cache_cap=64)
     b = LlamaDecoder.from_params(dataclasses.replace(cfg, engine=engine), params, cache_cap=64)
