@@ -180,8 +180,16 @@ def run_ours(args, rank, world):
     cfg = dataclasses.replace(LLAMA2_7B, engine=args.engine)
     ctxs = [int(c) for c in args.contexts.split(",")]
     cap = max(ctxs) + args.warmup + args.steps + 8
-    if world > 1:
-        # tensor parallel (configs[4]): rank-local shard, one NCCL all-reduce per block half
+    if world > 1 and args.tp_impl == "fused":
+        # tensor parallel (configs[4]): rank-local shard, ONE persistent launch per token,
+        # both all-reduces of every layer inside the kernel over NVLink peer memory
+        from paper_2508_18850_b200.tp_fused import FusedTPLlama
+        tp = FusedTPLlama(cfg, rank, world, cap, seed=1234)
+        model = tp.eng
+        step_fn, capture_fn, replay_fn = tp.step, tp.capture, tp.replay
+        launches_per_step = tp.launches_per_step
+    elif world > 1:
+        # tensor parallel baseline: layered engine, one NCCL all-reduce per block half
         from paper_2508_18850_b200.tp import TPLlamaDecoder
         tp = TPLlamaDecoder(cfg, rank, world, cap, seed=1234 + rank)
         model = tp.eng
@@ -240,7 +248,10 @@ def run_ours(args, rank, world):
         "vs_baseline": None, "dtype": "f16",
         "data": "synthetic (random fp16 weights + KV cache, device-drawn)",
         "config": bench_config(ctxs, world, lcfg.cluster),
-        "engine": cfg.engine if world == 1 else "layered (tensor parallel, NCCL between block halves)",
+        "engine": (cfg.engine if world == 1 else
+                   f"{tp.lcfg.engine} (fused tensor parallel: in-kernel fixed-point all-reduce over "
+                   f"NVLink peer memory, 1 launch/token/rank)" if args.tp_impl == "fused" else
+                   "layered (tensor parallel, NCCL between block halves)"),
         "sweep": [{k: v for k, v in s_.items() if k != "bytes"} for s_ in sweep],
         "achieved_hbm_gbs_mean": round(float(np.mean([s_["hbm_gbs"] for s_ in sweep])), 1),
         "e2e": {"value": round(e2e_tpot, 2), "unit": "us/token", "h2d_bytes_per_step": 4,
@@ -273,7 +284,7 @@ def run_ours(args, rank, world):
     if world == 1 and not args.no_deepseek:
         del model
         torch.cuda.empty_cache()
-        for key, fn in (("engine_compare", lambda: engine_compare(cfg, [ctxs[0], ctxs[-1]], args, pk["hbm_gbs"])),
+        for key, fn in (("engine_compare", lambda: engine_compare(cfg, ctxs, args, pk["hbm_gbs"])),
                         ("dropin_attention_module", lambda: dropin_api(pk["hbm_gbs"])),
                         ("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch16_ffn_tcgen05", lambda: batch16_ffn(cfg, pk["hbm_gbs"])),
@@ -284,6 +295,13 @@ def run_ours(args, rank, world):
                 line["gpu_launches"] += sum(d.get("launches", 0) for d in items)
             except Exception as exc:
                 line[key] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
+    if world > 1 and args.tp_impl == "fused":
+        try:  # the NCCL baseline of the same TP decode (layered engine, 2L+1 collectives)
+            line["tp_nccl_baseline"] = tp_nccl_baseline(cfg, rank, world, [ctxs[0], ctxs[-1]], args,
+                                                        pk["hbm_gbs"])
+            line["gpu_launches"] += sum(d.get("launches", 0) for d in line["tp_nccl_baseline"])
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            line["tp_nccl_baseline"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
     if world > 1 and not args.no_deepseek:
         del model
         torch.cuda.empty_cache()
@@ -335,16 +353,39 @@ def dropin_api(peak_gbs, S=1024, reps=10):
             "module_bytes": nbytes, "launches": 2 * (reps + 5)}
 
 
+def tp_nccl_baseline(cfg, rank, world, ctxs, args, peak_gbs):
+    """TP decode through the layered engine with one NCCL all-reduce per block
+    half (torch.distributed, graph-captured): the baseline the fused in-kernel
+    all-reduce replaces.  Max over ranks."""
+    import torch
+    from paper_2508_18850_b200.tp import TPLlamaDecoder
+    tp = TPLlamaDecoder(cfg, rank, world, max(ctxs) + args.warmup + args.steps + 8, seed=1234)
+    tp.set_state(ctxs[0], 1)
+    tp.step()
+    torch.cuda.synchronize()
+    tp.set_state(ctxs[0], 1)
+    tp.capture()
+    out = []
+    for s_ in time_engine(tp.eng, ctxs, args.steps, args.warmup, cfg, world, tp.replay):
+        out.append({"ctx": s_["ctx"], "tpot_us": s_["tpot_us"], "hbm_gbs": s_["hbm_gbs"],
+                    "frac_of_peak": round(s_["hbm_gbs"] / (world * peak_gbs), 4),
+                    "launches": tp.launches_per_step * (args.steps + args.warmup)})
+    del tp
+    torch.cuda.empty_cache()
+    return out
+
+
 def engine_compare(cfg, ctxs, args, peak_gbs):
     """The other B=1 engines on the same workload: the layered engine (split_token
-    cluster kernel + fused FFN kernel, 2 launches per layer) and the persistent
-    kernel with the attention exchange through global memory instead of DSMEM
-    (the paper's on-chip vs off-chip ablation)."""
+    cluster kernel + fused FFN kernel, 2 launches per layer), the persistent
+    kernel with the cluster gather / exchange through global memory instead of
+    DSMEM (same partitioning: the paper's with/without-DSMEM ablation,
+    PAPER.md:889-891), and the flat variant (attention split over all SMs)."""
     import dataclasses
     import torch
     from paper_2508_18850_b200.llama import LlamaDecoder
     out = []
-    for eng in ("layered", "persistent_flat"):
+    for eng in ("layered", "persistent_nodsmem", "persistent_flat"):
         c = dataclasses.replace(cfg, engine=eng)
         m = LlamaDecoder.random(c, cache_cap=max(ctxs) + args.warmup + args.steps + 8, seed=1234)
         m.set_state(ctxs[0], 1)
@@ -705,16 +746,16 @@ def run_reference(args, rank, world):
             "ms_per_step": round(tpot / 1e3, 3), "higher_is_better": False,
             "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f32 (fp16-valued inputs)", "data": "synthetic",
-            "config": bench_config(ctxs, world, _local_cluster(cfg, world)),
+            "config": bench_config(ctxs, world, _local_cluster(cfg, world, args.tp_impl)),
             "cpu_baseline": {"value": round(tpot, 1), "unit": "us/token", "cores": threads,
                              "kind": "port", "sample": sample, "host": cpu_info()},
             "e2e": {"value": round(tpot, 1), "unit": "us/token", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 
 
-def _local_cluster(cfg, world):
+def _local_cluster(cfg, world, tp_impl="fused"):
     """cluster size the GPU arm reports for this N (tp.local_config)."""
-    if world <= 1:
+    if world <= 1 or tp_impl == "fused":
         return cfg.cluster
     from paper_2508_18850_b200.tp import local_config
     return local_config(cfg, world).cluster
@@ -729,7 +770,10 @@ def main():
     ap.add_argument("--contexts", default="1024,2048,4096,8192,16384")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-deepseek", action="store_true")
-    ap.add_argument("--engine", default="persistent", choices=["persistent", "layered", "persistent_flat"])
+    ap.add_argument("--engine", default="persistent",
+                    choices=["persistent", "layered", "persistent_flat", "persistent_nodsmem"])
+    ap.add_argument("--tp-impl", default="fused", choices=["fused", "nccl"],
+                    help="N>1: in-kernel all-reduce over peer memory (fused) or NCCL between launches")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -18,6 +18,8 @@
  *                            (transformers DeepseekV2Moe semantics, oracle/deepseek_port.py)
  *   cfb_tc_gemm_b16        <- no reference counterpart: batch-16 projections on tcgen05 (north star)
  *   cfb_cluster_collective <- collectives.py:110-203 cluster_reduce / cluster_gather (DSMEM KAT kernel)
+ *   cfb_collective_bench   <- fixtures/table1.csv:4-19 (Table 1): on-chip vs off-chip
+ *                            ClusterReduce / ClusterGather latency harness
  *   cfb_lm_head_argmax, cfb_embed, cfb_llama_*  <- no reference counterpart (SPEC.md:298 non-goals);
  *                            the north-star decode loop around the fused modules.
  */
@@ -447,9 +449,12 @@ enum cfb_engine_kind {
                                 the attention module of a head runs on one N-CTA cluster
                                 (split_token, DSMEM gather/exchange), grid barriers between
                                 block halves; head_dim 128 */
-  CFB_ENGINE_PERSISTENT_FLAT = 2 /* as PERSISTENT, but the attention is split over all SMs
+  CFB_ENGINE_PERSISTENT_FLAT = 2, /* as PERSISTENT, but the attention is split over all SMs
                                 and its partials are exchanged through global memory with
-                                per-head flags (the off-chip-exchange ablation) */
+                                per-head flags (a different partitioning, kept as an A/B) */
+  CFB_ENGINE_PERSISTENT_NODSMEM = 3 /* as PERSISTENT (same clusters, same partitioning), but
+                                the ClusterGather and the (m, l, A) exchange go through global
+                                memory: the paper's "without DSMEM" ablation */
 };
 typedef struct cfb_llama_config {
   int dtype, n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster;
@@ -506,6 +511,36 @@ enum cfb_engine_part {
 int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigned long long* accum,
                      float* resid, unsigned long long* argkey);
 int cfb_llama_enqueue(cfb_llama* m, int part, int layer, void* stream);
+/* Fused tensor parallel (persistent engines only): the step kernel itself does
+ * both all-reduces of every layer and the vocabulary-shard argmax, pushing
+ * 64-bit fixed-point partial sums straight into every rank's exchange block over
+ * NVLink peer memory and meeting the other ranks at a cross-rank counter; one
+ * launch per token, no NCCL call.  xch_peers [size]: each rank's exchange
+ * block (cfb_tp_xch_bytes(hidden), zeroed) as addressable from THIS device -
+ * cfb_ipc_open'ed for remote ranks, the locally allocated one for `rank`.
+ * emulated != 0: all ranks share this GPU (tests): a plain launch on `grid`
+ * CTAs per rank, sized by the caller so every rank is resident.  timeout_ns > 0
+ * bounds each cross-rank wait (cfb_llama_check then reports 2). */
+int cfb_llama_set_tp_fused(cfb_llama* m, int rank, int size, int vocab_offset, void* const* xch_peers,
+                           int emulated, int grid, long long timeout_ns);
+size_t cfb_tp_xch_bytes(int hidden);
+/* Engine options (set before cfb_llama_capture; a captured graph keeps the
+ * values it was captured with). */
+enum cfb_llama_option {
+  CFB_OPT_L2_PREFETCH = 1, /* persistent engines: bytes per CTA of the next phase, past what
+                             the smem ring holds, prefetched into L2 at each grid barrier
+                             (HBM keeps streaming while the CTA waits); 0 = off */
+  CFB_OPT_PLAIN_LAUNCH = 2 /* persistent engines: 1 = launch without the cooperative
+                             attribute (the grid is sized co-resident either way; for
+                             profilers that cannot replay cooperative cluster launches) */
+};
+int cfb_llama_set_option(cfb_llama* m, int option, long long value);
+/* Inter-process peer memory for the exchange blocks: cudaMalloc + zero + IPC
+ * handle (64 bytes) / open a peer's handle (lazy peer access) / close / free. */
+int cfb_ipc_alloc(size_t bytes, void** dev, void* handle);
+int cfb_ipc_open(const void* handle, void** dev);
+int cfb_ipc_close(void* dev);
+int cfb_dev_free(void* dev);
 int cfb_llama_tp_buffers(cfb_llama* m, unsigned long long** accum, float** resid,
                          unsigned long long** argkey);
 int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
@@ -514,7 +549,8 @@ int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
  * NULL to stop); returns the grid size through *grid. */
 int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid);
 /* Device-side status of the last steps: *err_host = 1 if a step found pos + 1 >
- * cache_cap and did nothing (stream-ordered read, then the flag is cleared). */
+ * cache_cap and did nothing, 2 if a fused tensor-parallel step gave up waiting
+ * for its peers (stream-ordered read, then the flag is cleared). */
 int cfb_llama_check(cfb_llama* m, int* err_host, void* stream);
 
 /* One ClusterReduce (op 0=sum,1=max,2=softmax_merge) or ClusterGather (op 3)
@@ -522,6 +558,18 @@ int cfb_llama_check(cfb_llama* m, int* err_host, void* stream);
  * primitives (reference KATs). */
 int cfb_cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
                            unsigned long long* traffic, void* stream);
+
+/* Table-1 latency harness (fixtures/table1.csv:4-19): one
+ * cluster of N CTAs runs `reps` ClusterReduce (op 0, fp16 sum of `bytes` per
+ * rank) or ClusterGather (op 3, bytes/N per rank) collectives on operands in
+ * shared memory, over DSMEM bulk copies (channel 0) or through global memory /
+ * L2 (channel 1).  validate = 1: operands from in [N][bytes] fp16, results to
+ * out [N][bytes]; validate = 0 (timing): synthetic operands, results folded
+ * into a checksum.  scratch (1 MB) and ctr (one u64, zeroed) for channel 1.
+ * *ns_out (device) = mean ns per collective on rank 0. */
+int cfb_collective_bench(int op, int channel, int cluster, int bytes, int reps, int validate,
+                         const void* in, void* out, void* scratch, unsigned long long* ctr,
+                         unsigned long long* ns_out, void* stream);
 
 const char* cfb_last_error(void);
 const char* cfb_version(void);

@@ -168,6 +168,8 @@ class MoeArgs(ctypes.Structure):
 
 
 def bind_extra(L) -> None:
+    L.cfb_collective_bench.argtypes = [ctypes.c_int] * 6 + [_vp] * 6
+    L.cfb_collective_bench.restype = ctypes.c_int
     L.cfb_tc_gemm_b16.argtypes = [_vp] * 6 + [ctypes.c_int] * 3 + [_vp]
     L.cfb_tc_gemm_b16.restype = ctypes.c_int
     L.cfb_ffn_b16.argtypes = [ctypes.POINTER(FfnB16Args), _vp]

@@ -77,6 +77,13 @@ int cfb_cluster_collective(int dtype, int op, int cluster, int n, const void* in
                                  static_cast<cudaStream_t>(stream));
 }
 
+int cfb_collective_bench(int op, int channel, int cluster, int bytes, int reps, int validate,
+                         const void* in, void* out, void* scratch, unsigned long long* ctr,
+                         unsigned long long* ns_out, void* stream) {
+  return cfb::collective_bench(op, channel, cluster, bytes, reps, validate, in, out, scratch, ctr, ns_out,
+                               static_cast<cudaStream_t>(stream));
+}
+
 const char* cfb_last_error(void) { return cfb::g_err; }
 
 const char* cfb_version(void) { return "cfb 0.1.0 sm_100a"; }

@@ -58,7 +58,8 @@ int configure_kernel(const void* fn, int max_dyn_smem, bool nonportable_cluster)
 // pointer arrays live in DEVICE memory (the kernel walks all layers).
 struct LlamaStepArgs {
   int n_layers, hidden, n_heads, head_dim, inter, vocab, cache_cap, cluster, grid;
-  int cluster_attn;  // 1: attention module on DSMEM clusters; 0: flattened, global exchange
+  int cluster_attn;  // 1: attention module on DSMEM clusters; 2: same clusters, exchanges through
+                     // global memory (no-DSMEM ablation); 0: flattened over all SMs, global exchange
   float eps;
   const void* const* attn_norm;
   const void* const* w_qkv;
@@ -88,7 +89,20 @@ struct LlamaStepArgs {
   int* pos;
   int* err;
   unsigned long long* trace;
+  // tensor parallel (tp_size > 1): this rank's shard of heads / FFN columns /
+  // LM-head rows; the all-reduces run inside the kernel over peer memory
+  int tp_size, tp_rank, vocab_offset;
+  int emulated;                  // ranks share one GPU: plain (non-cooperative) launch, grid given
+  unsigned long long* const* xch;  // DEVICE array [tp_size] of the ranks' exchange blocks
+                                   // (tp_xch_bytes(hidden) each, zeroed), as this device sees them
+  float* resid2;                 // [D] second residual buffer (layer-parity rotation)
+  long long timeout_ns;          // cross-rank wait bound (err = 2 on expiry), 0 = none
+  int l2_prefetch;               // bytes/CTA prefetched into L2 past the ring at each barrier
 };
+// Exchange block of one tensor-parallel rank: reduced attention / FFN sums
+// [3][D] u64 each (fixed point), the cross-rank barrier counter, the argmax
+// key and the token counter (each on its own 128-byte line).
+size_t tp_xch_bytes(int hidden);
 int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st);
 int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out);
 int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* spw_out);
@@ -104,6 +118,8 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st);
 int lm_head_argmax(const cfb_lm_args* a, cudaStream_t st);
 int embed(int dtype, const void* table, const int* tokens, float* out, int B, int D,
           cudaStream_t st, bool pdl = false);
+int collective_bench(int op, int channel, int N, int bytes, int reps, int validate, const void* in, void* out,
+                     void* scratch, unsigned long long* ctr, unsigned long long* ns_out, cudaStream_t st);
 int cluster_collective(int dtype, int op, int cluster, int n, const void* in, void* out,
                        unsigned long long* traffic, cudaStream_t st);
 

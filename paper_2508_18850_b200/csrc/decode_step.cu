@@ -92,7 +92,88 @@ struct StepParams {
   int* pos;
   int* err;                      // set to 1 when pos + 1 > cache capacity (step skipped)
   unsigned long long* trace;     // [L][G][8] globaltimer stamps (nullable)
+  // tensor parallel (T > 1): see tp_* below
+  int T, trank, voff;
+  unsigned long long* const* xch;  // [T] exchange blocks (peer-mapped)
+  float* resid2;
+  long long timeout_ns;
+  int l2_prefetch;               // bytes per CTA prefetched into L2 past the ring at each barrier
 };
+
+// ---------------------------------------------------------------- tensor parallel
+// Rank r holds heads [r nh/T ..), FFN columns [r F/T ..) and LM-head rows
+// [r V/T ..) (Megatron), so each block half ends in a SUM all-reduce of a
+// D-vector.  Here the all-reduce is part of the kernel: every CTA owns a
+// D/G slice and red.adds it, as 64-bit fixed point (exact, order-free: the
+// sum is bit-identical whatever the arrival order), straight into every
+// rank's exchange block over NVLink peer memory, then the T x G CTAs meet at
+// a cross-rank counter (red.release.sys / ld.acquire.sys).  Exchange block
+// of a rank (u64 words): XA [3][D] attention sums, XF [3][D] FFN sums, then
+// the barrier counter, argmax key and token counter on separate lines.
+// Layer l uses set l % 3 and residual buffer l & 1; layer l zeroes its slice
+// of set (l + 1) % 3, whose last reader (layer l - 1) is behind the previous
+// cross barrier and whose next writers (layer l + 1) are behind the next one.
+__device__ __forceinline__ unsigned long long* tp_xa(unsigned long long* x, int D, int s) {
+  return x + (size_t)s * D;
+}
+__device__ __forceinline__ unsigned long long* tp_xf(unsigned long long* x, int D, int s) {
+  return x + (size_t)(3 + s) * D;
+}
+__device__ __forceinline__ unsigned long long* tp_bar(unsigned long long* x, int D) { return x + 6 * (size_t)D; }
+__device__ __forceinline__ unsigned long long* tp_key(unsigned long long* x, int D) { return x + 6 * (size_t)D + 16; }
+__device__ __forceinline__ unsigned long long* tp_tok(unsigned long long* x, int D) { return x + 6 * (size_t)D + 32; }
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_sys_add(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.sys.global.max.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// spin (thread 0) until *ctr >= target; on expiry of the bound set err = 2
+// and give up (the step's result is then garbage, but nothing hangs)
+__device__ __forceinline__ void tp_spin(const unsigned long long* ctr, unsigned long long target,
+                                        long long timeout_ns, int* err) {
+  unsigned long long t0 = 0;
+  while (ld_acquire_sys_u64(ctr) < target) {
+    if (timeout_ns > 0) {
+      const unsigned long long t = globaltimer();
+      if (!t0) {
+        t0 = t;
+      } else if ((long long)(t - t0) > timeout_ns) {
+        atomicExch(err, 2);
+        break;
+      }
+    }
+  }
+}
+
+// all T x G CTAs of the tensor-parallel group meet (target = base + k T G)
+__device__ __forceinline__ void cross_sync(const StepParams& p, unsigned long long target, int tid) {
+  __threadfence_system();
+  consumer_sync();
+  if (tid == 0) {
+    for (int t = 0; t < p.T; ++t) red_release_sys_add(tp_bar(p.xch[t], p.D), 1ull);
+    tp_spin(tp_bar(p.xch[p.trank], p.D), target, p.timeout_ns, p.err);
+    __threadfence();
+  }
+  consumer_sync();
+}
+
+// order-preserving key: larger logit wins, equal logits -> smaller index
+__device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
+  const unsigned u = __float_as_uint(v);
+  const unsigned o = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+  return ((unsigned long long)o << 32) | (unsigned long long)(0xFFFFFFFFu - (unsigned)idx);
+}
 
 struct StepLayout {
   int bars, xs, part, gu, qf, dsm, red, tag, misc, total, max_rows;
@@ -279,6 +360,36 @@ __device__ __forceinline__ void produce_pool(const Ring& ring, int lane, uint64_
   }
 }
 
+// Off-chip exchange (no-DSMEM ablation): every rank of the cluster stores its
+// `bytes` from shared memory into its global slot (slot stride `stride`, byte
+// offset `off`), the N ranks meet at a release/acquire counter, then each
+// copies every peer's slot back into its own shared memory at dst(d, peer),
+// d = the rotation distance (rank - peer) mod N, i.e. where the DSMEM push
+// would have put it, so the math that follows is shared by both channels.
+template <class Dst>
+__device__ __forceinline__ void global_exchange(const void* src, int bytes, float* slots, int stride,
+                                                int off, int rank, int N, unsigned long long* ctr,
+                                                unsigned long long target, int tid, Dst&& dst) {
+  char* mine = reinterpret_cast<char*>(slots) + (size_t)rank * stride + off;
+  for (int v = tid; v < bytes / 16; v += kConsumerThreads)
+    __stcg(reinterpret_cast<uint4*>(mine) + v, reinterpret_cast<const uint4*>(src)[v]);
+  __threadfence();
+  consumer_sync();
+  if (tid == 0) {
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
+    while (ld_acquire_u64(ctr) < target) {
+    }
+  }
+  consumer_sync();
+  for (int d = 1; d < N; ++d) {
+    const int peer = (rank - d + N) % N;
+    const uint4* s = reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(slots) +
+                                                    (size_t)peer * stride + off);
+    uint4* o = reinterpret_cast<uint4*>(dst(d, peer));
+    for (int v = tid; v < bytes / 16; v += kConsumerThreads) o[v] = __ldcg(s + v);
+  }
+}
+
 __device__ __forceinline__ void stamp(unsigned long long* tr, int k, int tid) {
   if (tr && tid == 0) tr[k] = globaltimer();
 }
@@ -291,7 +402,12 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int k, int tid) {
 // kCluster = false: flattened split over all SMs, partials exchanged through
 // global memory with per-head counters (the ablation: same kernel, off-chip
 // exchange instead of DSMEM).
-template <bool kCluster>
+//
+// kDsmem = false (cluster variant only): the same cluster partitioning, but
+// the ClusterGather and the (m, l, A) exchange go through global memory (a
+// slot per rank, a per-cluster release/acquire counter) instead of DSMEM -
+// the paper's "without DSMEM" ablation.
+template <bool kCluster, bool kDsmem = true>
 __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParams p) {
   extern __shared__ __align__(128) char smem[];
   const int G = gridDim.x, i = blockIdx.x;
@@ -364,6 +480,11 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     fence_mbar_init();
   }
   __syncthreads();
+  // no-DSMEM ablation: per-cluster exchange counter (monotonic; its launch
+  // base is read before the start cluster barrier, i.e. before any increment)
+  unsigned long long* xctr = p.counters + 2 * nh + cl;
+  unsigned long long xtarget = (!kDsmem && kCluster) ? (ld_acquire_u64(xctr) / N) * N : 0ull;
+  float* xslot = p.partials + (size_t)cl * N * ((seg_bytes + pay_bytes) / 4);  // [N][seg | pay]
   if (kCluster) cluster_arrive();  // peers' mbarriers initialised before any DSMEM push
 
   // The per-layer schedule, phase k of layer l computed on the fly (no arrays:
@@ -404,7 +525,18 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     if (k == 6) return make_phase(p.w_gu[l] + (size_t)a0 * 4 * D, nullptr, a1 - a0, 4 * D * 2, true);
     return make_phase(p.w_dn[l] + (size_t)u0 * 4 * F, nullptr, u1 - u0, 4 * F * 2, true);
   };
-  constexpr int kPhases = 8;
+  // At a barrier the ring (ring_bytes) already holds the head of the next
+  // phase and stalls once full; thread 0 lets HBM keep working on the bytes
+  // after it by prefetching the next `l2_prefetch` bytes of that phase into
+  // L2 (the producer's bulk copies then hit L2).  Rows/tiles are contiguous
+  // from src0, so the ring holds exactly the first ring_bytes of the phase.
+  auto prefetch_next = [&](const Phase& P) {
+    if (tid != 0 || p.l2_prefetch <= 0 || P.src1) return;
+    const long long total = (long long)P.n_units * P.unit_bytes;
+    const long long lo = ring_bytes(p.spw), hi = min(total, lo + (long long)p.l2_prefetch);
+    for (long long o = lo; o < hi; o += 16384)
+      bulk_prefetch_l2(P.src0 + o, (uint32_t)min(16384ll, hi - o) & ~15u);
+  };
 
   if (warp == kNumConsumerWarps) {  // ---------------------------- producer
     const uint64_t pol = policy_evict_first();
@@ -444,22 +576,68 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   unsigned long long* att_done = p.counters + nh;
 
   // embed: resid[c] = embed[token][c] for this CTA's slice; counters reset
+  const bool tp = p.T > 1;
+  const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);  // this CTA's D slice
+  unsigned long long* xown = tp ? p.xch[p.trank] : nullptr;
   {
     const int tok = *p.token;
-    const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);
-    for (int c = c0 + tid; c < c1; c += kConsumerThreads)
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
       p.resid[c] = __half2float(p.embed[(size_t)tok * D + c]);
+      if (tp) {  // set 0 (layer 0's sums) starts at zero; set 1 is zeroed by layer 0
+        tp_xa(xown, D, 0)[c] = 0ull;
+        tp_xf(xown, D, 0)[c] = 0ull;
+      }
+    }
     if (!kCluster && i == 0 && tid < 2 * nh) p.counters[tid] = 0ull;
+    if (tp && i == 0 && tid == 0) *tp_key(xown, D) = 0ull;
   }
-  // barrier base: no CTA can pass the first barrier before all have read it
+  // barrier bases: no CTA can pass the first barrier before all have read them
+  // (cross-rank: the count is below base + T G until this CTA arrives)
   unsigned long long bar_target = (ld_acquire_u64(p.barrier) / G) * G;
+  const unsigned long long TG = (unsigned long long)p.T * G;
+  unsigned long long x_target = tp ? (ld_acquire_sys_u64(tp_bar(xown, D)) / TG) * TG : 0ull;
+  const unsigned long long tok_base =
+      tp ? (ld_acquire_sys_u64(tp_tok(xown, D)) / p.T) * p.T : 0ull;
   if (kCluster) cluster_wait();
-  bar_target += G;
-  grid_sync(p.barrier, bar_target, tid);
+  if (tp) {
+    cross_sync(p, x_target += TG, tid);  // no rank pushes into set 0 before it is zeroed everywhere
+  } else {
+    bar_target += G;
+    grid_sync(p.barrier, bar_target, tid);
+  }
 
   // cross-CTA data is read through L2 (ld.global.cg): L1 is not coherent
   const float* resid_g = p.resid;
-  auto r_l = [resid_g](int, int v) { return __ldcg(reinterpret_cast<const float4*>(resid_g) + v); };
+  // residual stream h_l entering layer l (l == L: the final norm's input).
+  // Single GPU: resid, updated in place by the down-projection epilogue.
+  // TP: H[(l-1) & 1] + XA[(l-1) % 3] + XF[(l-1) % 3] (H[0] = embed for l == 0).
+  auto h_in = [&](int l, int v) -> float4 {
+    if (!tp || l == 0) return __ldcg(reinterpret_cast<const float4*>(resid_g) + v);
+    const float* Hp = ((l - 1) & 1) ? p.resid2 : p.resid;
+    const float4 r = __ldcg(reinterpret_cast<const float4*>(Hp) + v);
+    const ulonglong2* xa = reinterpret_cast<const ulonglong2*>(tp_xa(xown, D, (l - 1) % 3));
+    const ulonglong2* xf = reinterpret_cast<const ulonglong2*>(tp_xf(xown, D, (l - 1) % 3));
+    const ulonglong2 a0 = __ldcg(xa + 2 * v), a1 = __ldcg(xa + 2 * v + 1);
+    const ulonglong2 f0 = __ldcg(xf + 2 * v), f1 = __ldcg(xf + 2 * v + 1);
+    return make_float4(__fadd_rn(__fadd_rn(r.x, fixed_to_float(a0.x)), fixed_to_float(f0.x)),
+                       __fadd_rn(__fadd_rn(r.y, fixed_to_float(a0.y)), fixed_to_float(f0.y)),
+                       __fadd_rn(__fadd_rn(r.z, fixed_to_float(a1.x)), fixed_to_float(f1.x)),
+                       __fadd_rn(__fadd_rn(r.w, fixed_to_float(a1.y)), fixed_to_float(f1.y)));
+  };
+  // TP, layer l >= 1: the slice owner stores h_l into H[l & 1] (read by this
+  // layer's FFN prologue) and zeroes its slice of set (l + 1) % 3
+  auto tp_layer_start = [&](int l) {
+    if (!tp) return;
+    float* Hn = (l & 1) ? p.resid2 : p.resid;
+    const float* Hp = ((l - 1) & 1) ? p.resid2 : p.resid;
+    for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
+      if (l > 0)
+        Hn[c] = __fadd_rn(__fadd_rn(__ldcg(Hp + c), fixed_to_float(__ldcg(tp_xa(xown, D, (l - 1) % 3) + c))),
+                          fixed_to_float(__ldcg(tp_xf(xown, D, (l - 1) % 3) + c)));
+      tp_xa(xown, D, (l + 1) % 3)[c] = 0ull;
+      tp_xf(xown, D, (l + 1) % 3)[c] = 0ull;
+    }
+  };
   unsigned long long* accA = p.accA;
   int cnt = 0;
   int use = 0;  // DSMEM barrier phase (one gather + one exchange per head round)
@@ -554,7 +732,10 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     stamp(tr, 0, tid);
     if (kCluster) {
       // ================= attention module on the cluster (split_token, Alg. 3)
-      if (nrounds > 0) rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.attn_norm[l], 1, D, p.eps, red, tid);
+      tp_layer_start(l);
+      if (nrounds > 0)
+        rmsnorm_to_smem_ld<__half, true>(xs, [&](int, int v) { return h_in(l, v); }, p.attn_norm[l], 1, D,
+                                         p.eps, red, tid);
       for (int j = 0; j < nrounds; ++j, ++use) {
         const int h = cl + j * C;
         // 1. QKV GEMV of this rank's q|k|v slices (dataflows.py:256-267)
@@ -565,13 +746,18 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         consumer_sync();
         stamp(tr, 1, tid);
         // 2. ClusterGather (one round, rank-rotated slots, dataflows.py:268-279)
-        if (warp == 0 && N > 1) {
+        if (kDsmem && warp == 0 && N > 1) {
           for (int d = 1; d < N; ++d)
             dsmem_push(gseg, reinterpret_cast<char*>(gseg) + d * seg_bytes, &cbar[0], seg_bytes,
                        (rank + d) % N, lane);
           __syncwarp();
           mbar_wait(&cbar[0], use & 1);
           if (lane == 0) mbar_arrive_expect_tx(&cbar[0], (N - 1) * seg_bytes);  // next round
+        }
+        if (!kDsmem && N > 1) {  // off-chip: slot store, counter meet, peers' slots back via L2
+          global_exchange(gseg, seg_bytes, xslot, seg_bytes + pay_bytes, 0, rank, N, xctr,
+                          xtarget += N, tid,
+                          [&](int d, int) { return reinterpret_cast<char*>(gseg) + d * seg_bytes; });
         }
         consumer_sync();
         for (int d = tid; d < kH; d += kConsumerThreads) {
@@ -592,11 +778,17 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         stamp(tr, 2, tid);
         // 5. one-round DSMEM exchange of fp32 (m, l, A), merged in rank order
         //    (= MAX-reduce, rescale, SUM-reduce, rescale, SUM-reduce; dataflows.py:187-232)
-        if (warp == 0 && N > 1) {
+        if (kDsmem && warp == 0 && N > 1) {
           for (int d = 1; d < N; ++d) dsmem_push(mine, mine, &cbar[1], pay_bytes, (rank + d) % N, lane);
           __syncwarp();
           mbar_wait(&cbar[1], use & 1);
           if (lane == 0) mbar_arrive_expect_tx(&cbar[1], (N - 1) * pay_bytes);
+        }
+        if (!kDsmem && N > 1) {
+          global_exchange(mine, pay_bytes, xslot, seg_bytes + pay_bytes, seg_bytes, rank, N, xctr,
+                          xtarget += N, tid, [&](int, int r2) {
+                            return reinterpret_cast<char*>(pay + r2 * (pay_bytes / 4));
+                          });
         }
         consumer_sync();
         for (int d = tid; d < kH; d += kConsumerThreads) {
@@ -626,7 +818,9 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       stamp(tr, 3, tid);
     } else {
       // ================= flattened attention over all SMs, global exchange
-      rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.attn_norm[l], 1, D, p.eps, red, tid);
+      tp_layer_start(l);
+      rmsnorm_to_smem_ld<__half, true>(xs, [&](int, int v) { return h_in(l, v); }, p.attn_norm[l], 1, D,
+                                       p.eps, red, tid);
       tiled_gemv_phase<__half, 1, true>(layer_phase(l, 0), ring, warp, lane, tid, cnt, xs, D, 1, 4 * (q1 - q0), part,
                                         [&](int row, int, float v) {
                                           p.qkv[(size_t)4 * q0 + row] = __float2half_rn(v);
@@ -696,17 +890,28 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       }
       stamp(tr, 3, tid);
     }
+    prefetch_next(layer_phase(l, 6));
     bar_target += G;
     grid_sync(p.barrier, bar_target, tid);
+    if (tp) {  // attention all-reduce: this CTA's slice of the local head sum to every rank
+      for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
+        const unsigned long long v = __ldcg(accA + c);
+        for (int t = 0; t < p.T; ++t) red_add_u64(tp_xa(p.xch[t], D, l % 3) + c, v);
+        accA[c] = 0ull;
+      }
+      cross_sync(p, x_target += TG, tid);
+    }
     stamp(tr, 4, tid);
 
     // ---- FFN gate/up with the residual + head-sum RMSNorm prologue
     rmsnorm_to_smem_ld<__half, true>(
         xs,
         [&](int, int v) {
-          const float4 r = __ldcg(reinterpret_cast<const float4*>(resid_g) + v);
-          const ulonglong2 x0 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v);
-          const ulonglong2 x1 = __ldcg(reinterpret_cast<const ulonglong2*>(accA) + 2 * v + 1);
+          const float* Hl = tp && (l & 1) ? p.resid2 : resid_g;  // TP: h_l in H[l & 1]
+          const ulonglong2* acc = reinterpret_cast<const ulonglong2*>(tp ? tp_xa(xown, D, l % 3) : accA);
+          const float4 r = __ldcg(reinterpret_cast<const float4*>(Hl) + v);
+          const ulonglong2 x0 = __ldcg(acc + 2 * v);
+          const ulonglong2 x1 = __ldcg(acc + 2 * v + 1);
           return make_float4(__fadd_rn(r.x, fixed_to_float(x0.x)), __fadd_rn(r.y, fixed_to_float(x0.y)),
                              __fadd_rn(r.z, fixed_to_float(x1.x)), __fadd_rn(r.w, fixed_to_float(x1.y)));
         },
@@ -760,6 +965,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
       }
     }
     stamp(tr, 5, tid);
+    prefetch_next(layer_phase(l, 7));
     bar_target += G;
     grid_sync(p.barrier, bar_target, tid);
 
@@ -769,18 +975,34 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     tiled_gemv_phase<__half, 1, true>(layer_phase(l, 7), ring, warp, lane, tid, cnt, xs, F, 1,
                                       4 * (u1 - u0), part, [&](int row, int, float v) {
                                         const int c = 4 * u0 + row;
+                                        if (tp) {  // FFN all-reduce: partial column sums to every rank
+                                          const unsigned long long q =
+                                              (unsigned long long)__float2ll_rn(v * 4294967296.0f);
+                                          for (int t = 0; t < p.T; ++t)
+                                            red_add_u64(tp_xf(p.xch[t], D, l % 3) + c, q);
+                                          return;
+                                        }
                                         const float r = __fadd_rn(__ldcg(p.resid + c),
                                                                   fixed_to_float(__ldcg(accA + c)));
                                         accA[c] = 0ull;
                                         p.resid[c] = __fadd_rn(r, v);
                                       });
-    bar_target += G;
-    grid_sync(p.barrier, bar_target, tid);
+    if (l + 1 < p.L)
+      prefetch_next(layer_phase(l + 1, 0));
+    else
+      prefetch_next(make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true));
+    if (tp) {
+      cross_sync(p, x_target += TG, tid);
+    } else {
+      bar_target += G;
+      grid_sync(p.barrier, bar_target, tid);
+    }
     stamp(tr, 7, tid);
   }
 
   // ---- final RMSNorm + LM head + argmax
-  rmsnorm_to_smem_ld<__half, true>(xs, r_l, p.final_norm, 1, D, p.eps, red, tid);
+  rmsnorm_to_smem_ld<__half, true>(xs, [&](int, int v) { return h_in(p.L, v); }, p.final_norm, 1, D, p.eps,
+                                   red, tid);
   float bv = -INFINITY;
   int bi = 0x7fffffff;
   const Phase PL = make_phase(p.lm_head + (size_t)v0 * 4 * D, nullptr, v1 - v0, 4 * D * 2, true);
@@ -833,6 +1055,15 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         ix = ci;
       }
     }
+    if (tp) {  // global argmax over the vocabulary shards: MAX of order-preserving keys
+      const unsigned long long key = argmax_key(v, ix + p.voff);
+      for (int t = 0; t < p.T; ++t) red_max_u64(tp_key(p.xch[t], D), key);
+      __threadfence_system();
+      for (int t = 0; t < p.T; ++t) red_release_sys_add(tp_tok(p.xch[t], D), 1ull);
+      tp_spin(tp_tok(xown, D), tok_base + p.T, p.timeout_ns, p.err);
+      const unsigned long long k = ld_acquire_sys_u64(tp_key(xown, D));
+      ix = (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull));
+    }
     *p.token = ix;
     *p.ticket = 0;
     *p.pos = S + 1;
@@ -844,6 +1075,8 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
 }
 
 }  // namespace
+
+size_t tp_xch_bytes(int hidden) { return (6 * (size_t)hidden + 48) * 8; }
 
 int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out) {
   int spw = tuned_spw();
@@ -961,6 +1194,18 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.pos = a->pos;
   p.err = a->err;
   p.trace = a->trace;
+  p.T = a->tp_size > 1 ? a->tp_size : 1;
+  p.trank = a->tp_rank;
+  p.voff = a->vocab_offset;
+  p.xch = a->xch;
+  p.resid2 = a->resid2;
+  p.timeout_ns = a->timeout_ns;
+  p.l2_prefetch = a->l2_prefetch;
+  if (p.T > 1 && (!p.xch || !p.resid2 || p.trank < 0 || p.trank >= p.T))
+    return set_error(CFB_ERR_ARGUMENT, "tensor-parallel step without exchange blocks");
+  // emulated ranks share the GPU: every rank's grid is resident by construction
+  // (the caller sizes it), a cooperative launch could not overlap with the peers'
+  const int coop = a->emulated ? 0 : 1;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G, 1, 1);
   cfg.blockDim = dim3(kThreads, 1, 1);
@@ -974,14 +1219,20 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
     at[0].val.clusterDim.y = 1;
     at[0].val.clusterDim.z = 1;
     at[1].id = cudaLaunchAttributeCooperative;  // all-or-nothing residency
-    at[1].val.cooperative = 1;
+    at[1].val.cooperative = coop;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true>, p));
+    if (a->cluster_attn == 2) {
+      if (const int rc = configure_kernel((const void*)llama_step_kernel<true, false>, kMaxSmem, true))
+        return rc;
+      CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true, false>, p));
+    } else {
+      CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true>, p));
+    }
   } else {
     if (const int rc = configure_kernel((const void*)llama_step_kernel<false>, kMaxSmem, false)) return rc;
     at[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident (grid barriers)
-    at[0].val.cooperative = 1;
+    at[0].val.cooperative = coop;
     cfg.attrs = at;
     cfg.numAttrs = 1;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<false>, p));

@@ -4,6 +4,7 @@
 // step is captured once into a CUDA graph and replayed, and the device-side
 // position/token it advances make consecutive replays decode consecutive
 // tokens without any host work.
+#include <cstring>
 #include <vector>
 
 #include "common.h"
@@ -36,10 +37,17 @@ struct cfb_llama {
   void* pqkv = nullptr;                 // q|k|v rows of the current layer
   float* partials = nullptr;            // attention partials [nh][grid][132]
   unsigned long long* pbarrier = nullptr;
-  unsigned long long* counters = nullptr;  // [2 nh]
+  unsigned long long* counters = nullptr;  // [2 nh] flat per-head flags + [sms] per-cluster
   int* err = nullptr;
   unsigned long long* trace = nullptr;
   int grid = 0;
+  // fused tensor parallel (persistent engine, in-kernel all-reduce over peer memory)
+  int tp_fused = 0, emulated = 0;
+  int l2_prefetch = 0;  // CFB_OPT_L2_PREFETCH
+  int plain_launch = 0; // CFB_OPT_PLAIN_LAUNCH
+  long long timeout_ns = 0;
+  unsigned long long** xch_dev = nullptr;  // [tp_size] exchange blocks as this device sees them
+  float* resid2 = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -184,7 +192,7 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.cache_cap = c.cache_cap;
   a.cluster = c.cluster;
   a.grid = m->grid;
-  a.cluster_attn = c.engine == CFB_ENGINE_PERSISTENT;
+  a.cluster_attn = c.engine == CFB_ENGINE_PERSISTENT ? 1 : c.engine == CFB_ENGINE_PERSISTENT_NODSMEM ? 2 : 0;
   a.eps = c.eps;
   void** d = m->dev_ptrs;
   a.attn_norm = d;
@@ -215,11 +223,22 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.pos = m->pos;
   a.err = m->err;
   a.trace = m->trace;
+  a.l2_prefetch = m->l2_prefetch;
+  a.emulated = m->plain_launch;
+  if (m->tp_fused) {
+    a.tp_size = m->tp_size;
+    a.tp_rank = m->tp_rank;
+    a.vocab_offset = m->vocab_offset;
+    a.emulated = m->emulated || m->plain_launch;
+    a.xch = m->xch_dev;
+    a.resid2 = m->resid2;
+    a.timeout_ns = m->timeout_ns;
+  }
   return cfb::llama_step_launch(&a, st);
 }
 
 int enqueue_step(cfb_llama* m, cudaStream_t st) {
-  if (m->tp_size > 1)
+  if (m->tp_size > 1 && !m->tp_fused)
     return cfb::set_error(CFB_ERR_ARGUMENT,
                           "tensor-parallel engines are driven part by part (collectives between)");
   if (m->cfg.engine != CFB_ENGINE_LAYERED) return enqueue_persistent(m, st);
@@ -271,7 +290,8 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     return rc;
   }
   if (cfg->engine != CFB_ENGINE_LAYERED) {
-    if (cfg->engine != CFB_ENGINE_PERSISTENT && cfg->engine != CFB_ENGINE_PERSISTENT_FLAT) {
+    if (cfg->engine != CFB_ENGINE_PERSISTENT && cfg->engine != CFB_ENGINE_PERSISTENT_FLAT &&
+        cfg->engine != CFB_ENGINE_PERSISTENT_NODSMEM) {
       cfb_llama_destroy(m);
       return set_error(CFB_ERR_ARGUMENT, "unknown engine kind %d", cfg->engine);
     }
@@ -288,7 +308,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
     ga.vocab = cfg->vocab;
     ga.cache_cap = cfg->cache_cap;
     ga.cluster = cfg->cluster;
-    ga.cluster_attn = cfg->engine == CFB_ENGINE_PERSISTENT;
+    ga.cluster_attn = cfg->engine == CFB_ENGINE_PERSISTENT ? 1 : cfg->engine == CFB_ENGINE_PERSISTENT_NODSMEM ? 2 : 0;
     if ((rc = cfb::llama_step_grid(&ga, &m->grid, nullptr, nullptr))) {
       cfb_llama_destroy(m);
       return rc;
@@ -311,7 +331,7 @@ int cfb_llama_create(const cfb_llama_config* cfg, const cfb_llama_weights* w, cf
         (rc = alloc_zero((void**)&m->partials, (size_t)cfg->n_heads * sms * 132 * 4)) ||
 
         (rc = alloc_zero((void**)&m->pbarrier, 8 * (1 + (size_t)L))) ||
-        (rc = alloc_zero((void**)&m->counters, (size_t)2 * cfg->n_heads * 8)) ||
+        (rc = alloc_zero((void**)&m->counters, ((size_t)2 * cfg->n_heads + sms) * 8)) ||
         (rc = alloc_zero((void**)&m->err, 4))) {
       cfb_llama_destroy(m);
       return rc;
@@ -334,7 +354,7 @@ int cfb_llama_destroy(cfb_llama* m) {
   void* bufs[] = {(m->ext & 2) ? nullptr : m->resid, (m->ext & 1) ? nullptr : m->accum,
                   m->act, m->barrier, m->logits, m->cand_val, m->cand_idx, m->lm_ticket, m->token,
                   m->pos, (m->ext & 4) ? nullptr : m->argkey, m->dev_ptrs, m->pqkv,
-                  m->partials, m->pbarrier, m->counters, m->err};
+                  m->partials, m->pbarrier, m->counters, m->err, m->xch_dev, m->resid2};
   for (void* b : bufs)
     if (b) cudaFree(b);
   delete m;
@@ -345,7 +365,9 @@ int cfb_llama_set_state(cfb_llama* m, int pos, int token, void* stream) {
   if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
   if (pos < 0 || pos >= m->cfg.cache_cap)
     return cfb::set_error(CFB_ERR_DIMENSION, "pos %d outside cache capacity %d", pos, m->cfg.cache_cap);
-  if (token < 0 || token >= m->cfg.vocab) return cfb::set_error(CFB_ERR_DIMENSION, "token out of range");
+  // tensor parallel: the local vocabulary is a shard, the token is global
+  if (token < 0 || token >= m->cfg.vocab * m->tp_size)
+    return cfb::set_error(CFB_ERR_DIMENSION, "token out of range");
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   static thread_local int host[2];
   host[0] = pos;
@@ -402,7 +424,7 @@ int cfb_llama_buffers(cfb_llama* m, float** logits, int** token, int** pos, floa
 }
 
 int cfb_llama_launches_per_step(const cfb_llama* m) {
-  if (m && m->cfg.engine != CFB_ENGINE_LAYERED && m->tp_size == 1) return 1;
+  if (m && m->cfg.engine != CFB_ENGINE_LAYERED && (m->tp_size == 1 || m->tp_fused)) return 1;
   return m ? 2 + 2 * m->cfg.n_layers + (m->tp_size > 1 ? 2 : 0) : 0;
 }
 
@@ -431,6 +453,89 @@ int cfb_llama_set_tp(cfb_llama* m, int rank, int size, int vocab_offset, unsigne
     m->argkey = argkey;
     m->ext |= 4;
   }
+  return CFB_OK;
+}
+
+int cfb_llama_set_tp_fused(cfb_llama* m, int rank, int size, int vocab_offset, void* const* xch_peers,
+                           int emulated, int grid, long long timeout_ns) {
+  using cfb::set_error;
+  if (!m || !xch_peers) return set_error(CFB_ERR_ARGUMENT, "null argument");
+  if (m->cfg.engine == CFB_ENGINE_LAYERED)
+    return set_error(CFB_ERR_ARGUMENT, "fused tensor parallel needs a persistent engine");
+  if (size < 2 || size > 64 || rank < 0 || rank >= size || vocab_offset < 0)
+    return set_error(CFB_ERR_ARGUMENT, "bad tensor-parallel rank %d / size %d", rank, size);
+  for (int t = 0; t < size; ++t)
+    if (!xch_peers[t]) return set_error(CFB_ERR_ARGUMENT, "missing exchange block of rank %d", t);
+  if (grid > 0) {  // emulated ranks on one GPU: each gets a share of the SMs
+    cfb::LlamaStepArgs ga = {};
+    ga.n_layers = m->cfg.n_layers;
+    ga.hidden = m->cfg.hidden;
+    ga.n_heads = m->cfg.n_heads;
+    ga.head_dim = m->cfg.head_dim;
+    ga.inter = m->cfg.inter;
+    ga.vocab = m->cfg.vocab;
+    ga.cache_cap = m->cfg.cache_cap;
+    ga.cluster = m->cfg.cluster;
+    ga.grid = grid;
+    ga.cluster_attn = m->cfg.engine == CFB_ENGINE_PERSISTENT ? 1 : m->cfg.engine == CFB_ENGINE_PERSISTENT_NODSMEM ? 2 : 0;
+    if (const int rc = cfb::llama_step_grid(&ga, &m->grid, nullptr, nullptr)) return rc;
+    if (m->grid > grid) return set_error(CFB_ERR_ARGUMENT, "grid %d does not fit %d", grid, m->grid);
+  }
+  if (!m->xch_dev) CFB_CUDA(cudaMalloc((void**)&m->xch_dev, 64 * sizeof(void*)));
+  CFB_CUDA(cudaMemcpy(m->xch_dev, xch_peers, (size_t)size * sizeof(void*), cudaMemcpyHostToDevice));
+  if (!m->resid2) {
+    CFB_CUDA(cudaMalloc((void**)&m->resid2, (size_t)m->cfg.hidden * 4));
+    CFB_CUDA(cudaMemset(m->resid2, 0, (size_t)m->cfg.hidden * 4));
+  }
+  m->tp_rank = rank;
+  m->tp_size = size;
+  m->vocab_offset = vocab_offset;
+  m->tp_fused = 1;
+  m->emulated = emulated ? 1 : 0;
+  m->timeout_ns = timeout_ns;
+  return CFB_OK;
+}
+
+size_t cfb_tp_xch_bytes(int hidden) { return cfb::tp_xch_bytes(hidden); }
+
+int cfb_llama_set_option(cfb_llama* m, int option, long long value) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  switch (option) {
+    case CFB_OPT_L2_PREFETCH:
+      if (value < 0 || value > (64 << 20) || value % 16)
+        return cfb::set_error(CFB_ERR_ARGUMENT, "l2 prefetch bytes must be a multiple of 16 in [0, 64 MB]");
+      m->l2_prefetch = (int)value;
+      return CFB_OK;
+    case CFB_OPT_PLAIN_LAUNCH:
+      m->plain_launch = value ? 1 : 0;
+      return CFB_OK;
+  }
+  return cfb::set_error(CFB_ERR_ARGUMENT, "unknown engine option %d", option);
+}
+
+int cfb_ipc_alloc(size_t bytes, void** dev, void* handle) {
+  if (!dev || !handle || !bytes) return cfb::set_error(CFB_ERR_ARGUMENT, "null argument");
+  CFB_CUDA(cudaMalloc(dev, bytes));
+  CFB_CUDA(cudaMemset(*dev, 0, bytes));
+  CFB_CUDA(cudaIpcGetMemHandle(static_cast<cudaIpcMemHandle_t*>(handle), *dev));
+  return CFB_OK;
+}
+
+int cfb_ipc_open(const void* handle, void** dev) {
+  if (!dev || !handle) return cfb::set_error(CFB_ERR_ARGUMENT, "null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CFB_CUDA(cudaIpcOpenMemHandle(dev, h, cudaIpcMemLazyEnablePeerAccess));
+  return CFB_OK;
+}
+
+int cfb_ipc_close(void* dev) {
+  if (dev) CFB_CUDA(cudaIpcCloseMemHandle(dev));
+  return CFB_OK;
+}
+
+int cfb_dev_free(void* dev) {
+  if (dev) CFB_CUDA(cudaFree(dev));
   return CFB_OK;
 }
 

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _native
-from .exceptions import DimensionError
+from .exceptions import DimensionError, SimulationError
 from .layouts import gate_up_tiles, qkv_tiles, row_tiles, wo_rows
 
 
@@ -38,8 +38,10 @@ class LlamaConfig:
     cluster: int = 4
     dtype_bytes: int = 2
     # "persistent": one launch per step on every SM, attention on DSMEM clusters
-    # (csrc/decode_step.cu); "persistent_flat": same, attention exchange through
-    # global memory (ablation); "layered": split_token cluster kernel + fused
+    # (csrc/decode_step.cu); "persistent_nodsmem": same clusters, gather and
+    # exchange through global memory (the paper's without-DSMEM ablation);
+    # "persistent_flat": attention split over all SMs, exchange through global
+    # memory (A/B); "layered": split_token cluster kernel + fused
     # FFN kernel per layer, PDL-chained (csrc/llama.cu; the tensor-parallel path)
     engine: str = "persistent"
 
@@ -69,7 +71,7 @@ class _LlamaConfigC(ctypes.Structure):
         ("eps", ctypes.c_float), ("engine", ctypes.c_int)]
 
 
-ENGINES = {"layered": 0, "persistent": 1, "persistent_flat": 2}
+ENGINES = {"layered": 0, "persistent": 1, "persistent_flat": 2, "persistent_nodsmem": 3}
 
 
 _PP = ctypes.POINTER(ctypes.c_void_p)
@@ -210,9 +212,11 @@ class LlamaDecoder:
         self._finish()
 
     @classmethod
-    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0) -> "LlamaDecoder":
+    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0,
+               embed_vocab: int | None = None) -> "LlamaDecoder":
         """Weights and a full KV cache drawn on the device (torch Philox), packed
-        layouts directly.  Scales as random_llama_params."""
+        layouts directly.  Scales as random_llama_params.  `embed_vocab`: rows of
+        the embedding table when cfg.vocab is a tensor-parallel LM-head shard."""
         m = cls(cfg, cache_cap)
         torch, dev = m.torch, m.dev
         g = torch.Generator(device=dev)
@@ -232,7 +236,7 @@ class LlamaDecoder:
                 w_gu=rnd((F // 2, D // 8, 4, 8), D ** -0.5),
                 w_dn=rnd((D // 4, F // 8, 4, 8), F ** -0.5),
                 k_cache=rnd((nh, cache_cap, H), 1.0), v_cache=rnd((nh, cache_cap, H), 1.0)))
-        m.embed = rnd((cfg.vocab, D), 1.0)
+        m.embed = rnd((embed_vocab or cfg.vocab, D), 1.0)
         m.final_norm = rnd((D,), 0.1, 1.0)
         m.lm_head = rnd((cfg.vocab // 4, D // 8, 4, 8), D ** -0.5)
         m._finish()
@@ -302,12 +306,27 @@ class LlamaDecoder:
         _native.check(L_.cfb_llama_set_trace(self._h, self.trace.data_ptr(), ctypes.byref(grid)))
         return self.trace
 
+    def set_l2_prefetch(self, nbytes: int) -> None:
+        """Persistent engines: bytes per CTA of the next phase prefetched into L2
+        (past the smem ring) at each grid barrier; capture again afterwards."""
+        L_ = self._lib
+        L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
+        _native.check(L_.cfb_llama_set_option(self._h, 1, int(nbytes)))
+
+    def set_plain_launch(self, on: bool = True) -> None:
+        """Persistent engines: launch without the cooperative attribute (ncu)."""
+        L_ = self._lib
+        L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
+        _native.check(L_.cfb_llama_set_option(self._h, 2, 1 if on else 0))
+
     def check(self) -> None:
         """Raise if a step found the cache full (pos + 1 > cache_cap) and skipped."""
         L_ = self._lib
         L_.cfb_llama_check.argtypes = [ctypes.c_void_p, ctypes.POINTER(ctypes.c_int), ctypes.c_void_p]
         err = ctypes.c_int(0)
         _native.check(L_.cfb_llama_check(self._h, ctypes.byref(err), self._sp()))
+        if err.value == 2:
+            raise SimulationError("fused tensor-parallel step: peers did not arrive in time")
         if err.value:
             raise DimensionError(f"decode position reached the cache capacity {self.cache_cap}")
 

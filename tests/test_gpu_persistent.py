@@ -44,7 +44,7 @@ def _run(cfg, prefill, steps, seed):
     return m
 
 
-ENGINES = ["persistent", "persistent_flat"]
+ENGINES = ["persistent", "persistent_flat", "persistent_nodsmem"]
 
 
 @pytest.mark.parametrize("engine", ENGINES)

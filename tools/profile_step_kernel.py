@@ -13,6 +13,7 @@ from paper_2508_18850_b200.llama import LLAMA2_7B, LlamaDecoder  # noqa: E402
 ctx = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 eng = sys.argv[2] if len(sys.argv) > 2 else "persistent"
 m = LlamaDecoder.random(dataclasses.replace(LLAMA2_7B, engine=eng), cache_cap=ctx + 8, seed=1)
+m.set_plain_launch(True)  # ncu cannot replay cooperative cluster launches
 for _ in range(2):
     m.set_state(ctx, 1)
     m.step()
