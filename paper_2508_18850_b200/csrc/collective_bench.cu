@@ -202,7 +202,7 @@ int collective_bench(int op, int channel, int N, int bytes, int reps, int valida
   const bool g = op == 3, on = channel == 0;
   auto k = g ? (on ? collective_bench_kernel<true, true> : collective_bench_kernel<true, false>)
              : (on ? collective_bench_kernel<false, true> : collective_bench_kernel<false, false>);
-  if (const int rc = configure_kernel((const void*)k, (int)cfg.dynamicSmemBytes, true)) return rc;
+  if (const int rc = configure_kernel((const void*)k, kMaxSmem, true)) return rc;
   CFB_CUDA(cudaLaunchKernelEx(&cfg, k, bytes, chunk, reps, validate, static_cast<const __half*>(in),
                               static_cast<__half*>(out), static_cast<__half*>(scratch), ctr, ns_out));
   return CFB_OK;
