@@ -755,8 +755,11 @@ def run_reference(args, rank, world):
 
 def _local_cluster(cfg, world, tp_impl="fused"):
     """cluster size the GPU arm reports for this N (tp.local_config)."""
-    if world <= 1 or tp_impl == "fused":
+    if world <= 1:
         return cfg.cluster
+    if tp_impl == "fused":
+        from paper_2508_18850_b200.tp_fused import fused_local_config
+        return fused_local_config(cfg, world).cluster
     from paper_2508_18850_b200.tp import local_config
     return local_config(cfg, world).cluster
 

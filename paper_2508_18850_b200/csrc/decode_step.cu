@@ -158,9 +158,9 @@ __device__ __forceinline__ void tp_spin(const unsigned long long* ctr, unsigned 
 
 // all T x G CTAs of the tensor-parallel group meet (target = base + k T G)
 __device__ __forceinline__ void cross_sync(const StepParams& p, unsigned long long target, int tid) {
-  __threadfence_system();
   consumer_sync();
   if (tid == 0) {
+    __threadfence_system();  // cumulative over the CTA's writes ordered by the bar.sync above
     for (int t = 0; t < p.T; ++t) red_release_sys_add(tp_bar(p.xch[t], p.D), 1ull);
     tp_spin(tp_bar(p.xch[p.trank], p.D), target, p.timeout_ns, p.err);
     __threadfence();
@@ -194,6 +194,7 @@ __host__ __device__ inline StepLayout step_layout(int D, int F, int TQ, int TV, 
   int part = kNumConsumerWarps * L.max_rows * 4;
   const int ws = kNumConsumerWarps * kPS * 4;  // attention warp states alias `part`
   if (ws > part) part = ws;
+  if (3 * G * 4 > part) part = 3 * G * 4;  // flat O-phase merge: per-piece m, l, weight
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
   L.xs = o;    o += r16((D > F ? D : F) * 2);
@@ -232,12 +233,12 @@ __device__ __forceinline__ void red_release_add(unsigned long long* p, unsigned 
 // path); thread 0 then polls with ld.acquire.
 __device__ __forceinline__ void grid_sync(unsigned long long* counter, unsigned long long target,
                                           int tid) {
-  __threadfence();
+  // bar.sync orders every consumer's prior writes before thread 0's release
+  // (cumulative), so one fence-carrying arrival per CTA publishes them all
   consumer_sync();
   if (tid == 0) {
     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(counter) : "memory");
-    while (ld_acquire_u64(counter) < target) {
-    }
+    spin_until_geq(counter, target);
   }
   consumer_sync();
 }
@@ -246,8 +247,7 @@ __device__ __forceinline__ void grid_sync(unsigned long long* counter, unsigned 
 __device__ __forceinline__ void wait_counter(const unsigned long long* p, unsigned long long target,
                                              int tid) {
   if (tid == 0) {
-    while (ld_acquire_u64(p) < target) __nanosleep(32);
-    __threadfence();
+    spin_until_geq(p, target);
   }
   consumer_sync();
 }
@@ -373,8 +373,7 @@ __device__ __forceinline__ void global_exchange(const void* src, int bytes, floa
   char* mine = reinterpret_cast<char*>(slots) + (size_t)rank * stride + off;
   for (int v = tid; v < bytes / 16; v += kConsumerThreads)
     __stcg(reinterpret_cast<uint4*>(mine) + v, reinterpret_cast<const uint4*>(src)[v]);
-  __threadfence();
-  consumer_sync();
+  consumer_sync();  // thread 0's release below is cumulative over these stores
   if (tid == 0) {
     asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(ctr) : "memory");
     while (ld_acquire_u64(ctr) < target) {
@@ -825,8 +824,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
                                         [&](int row, int, float v) {
                                           p.qkv[(size_t)4 * q0 + row] = __float2half_rn(v);
                                         });
-      __threadfence();
-      consumer_sync();
+      consumer_sync();  // thread 0's releases are cumulative over the CTA's q|k|v stores
       if (tid == 0) {
         for (int h = q0 / TPH; h < nh && h * TPH < q1; ++h) {
           const int lo = max(q0, h * TPH), hi = min(q1, (h + 1) * TPH);
@@ -848,7 +846,6 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         rope_qk();
         if (has_new) append_kv(l, h);
         attend_rows(layer_phase(l, 1 + j), has_new, p.partials + ((size_t)h * G + i) * kPS);
-        __threadfence();
         consumer_sync();
         if (tid == 0) red_release_add(&att_done[h], 1ull);
       }
@@ -857,22 +854,44 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         const int h = oh[j];
         const long long ha = (long long)h * SP, hb = ha + SP;
         const int first = owner_of(ha, PK, G), lastc = owner_of(hb - 1, PK, G);
+        const int ncand = lastc - first + 1;  // CTAs whose (head, position) range may touch head h
+        // per-piece (m, l) into smem in parallel (a piece = a CTA with a non-empty range),
+        // then every thread merges its dims over the pieces in ascending CTA order
+        float* pm = part;          // [ncand] m
+        float* pl = part + G;      // [ncand] l
+        float* pw = part + 2 * G;  // [ncand] weights e^(m_c - M) (0: empty / -inf piece)
         int npieces = 0;
         for (int c = first; c <= lastc; ++c) npieces += split_at(PK, c, G) < split_at(PK, c + 1, G);
         wait_counter(&att_done[h], (unsigned long long)npieces * (l + 1), tid);
-        for (int d = tid; d < kH; d += kConsumerThreads) {
+        for (int t = tid; t < ncand; t += kConsumerThreads) {
+          const int c = first + t;
+          const bool ne = split_at(PK, c, G) < split_at(PK, c + 1, G);
+          const float* src = p.partials + ((size_t)h * G + c) * kPS;
+          pm[t] = ne ? __ldcg(src) : -INFINITY;
+          pl[t] = ne ? __ldcg(src + 1) : 0.f;
+        }
+        consumer_sync();
+        {
           float ms = -INFINITY;
-          for (int c = first; c <= lastc; ++c)
-            if (split_at(PK, c, G) < split_at(PK, c + 1, G))
-              ms = fmaxf(ms, __ldcg(p.partials + ((size_t)h * G + c) * kPS));
+          for (int t = 0; t < ncand; ++t) ms = fmaxf(ms, pm[t]);
+          for (int t = tid; t < ncand; t += kConsumerThreads) pw[t] = pm[t] == -INFINITY ? 0.f : expf(pm[t] - ms);
+        }
+        consumer_sync();
+        for (int d = tid; d < kH; d += kConsumerThreads) {
           float ls = 0.f, a = 0.f;
-          for (int c = first; c <= lastc; ++c) {
-            if (split_at(PK, c, G) >= split_at(PK, c + 1, G)) continue;
-            const float* src = p.partials + ((size_t)h * G + c) * kPS;
-            const float mr = __ldcg(src);
-            const float f = (mr == -INFINITY) ? 0.f : expf(mr - ms);
-            ls = fmaf(__ldcg(src + 1), f, ls);
-            a = fmaf(__ldcg(src + 4 + d), f, a);
+          for (int t0 = 0; t0 < ncand; t0 += 8) {  // 8 independent L2 loads in flight
+            float v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              v[k] = (t0 + k < ncand && pw[t0 + k] != 0.f)
+                         ? __ldcg(p.partials + ((size_t)h * G + first + t0 + k) * kPS + 4 + d)
+                         : 0.f;
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (t0 + k < ncand && pw[t0 + k] != 0.f) {  // fixed (ascending) order: deterministic
+                ls = fmaf(pl[t0 + k], pw[t0 + k], ls);
+                a = fmaf(v[k], pw[t0 + k], a);
+              }
           }
           abuf[d] = __float2half_rn(__fdiv_rn(a, ls));
         }

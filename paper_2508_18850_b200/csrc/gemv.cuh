@@ -473,9 +473,9 @@ __device__ __forceinline__ void load_act_to_smem(XElem<XH>* xs, const T* x, int 
 // one CTA per SM, so every CTA is resident).  Monotonic 64-bit counter: the
 // n-th use waits for n * gridDim.x arrivals, so it never needs resetting.
 __device__ __forceinline__ void grid_barrier(unsigned long long* counter, int tid) {
-  __threadfence();
   consumer_sync();
   if (tid == 0) {
+    __threadfence();  // cumulative over the CTA's writes ordered by the bar.sync above
     const unsigned long long g = gridDim.x;
     const unsigned long long old = atomicAdd(counter, 1ull);
     const unsigned long long target = (old / g + 1) * g;

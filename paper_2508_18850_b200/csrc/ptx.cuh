@@ -123,6 +123,18 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+// spin with relaxed loads, then ONE acquire load of the same word: the
+// acquire orders every later read after the arrivals it observed
+__device__ __forceinline__ void spin_until_geq(const unsigned long long* p, unsigned long long target) {
+  while (ld_relaxed_u64(p) < target) {
+  }
+  (void)ld_acquire_u64(p);
+}
 __device__ __forceinline__ int ld_acquire_s32(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");

@@ -47,14 +47,26 @@ def _bind(L):
     return L
 
 
-def fused_local_config(cfg: LlamaConfig, world: int) -> LlamaConfig:
-    """Per-rank shape of the fused path: the shard of heads / FFN / vocab,
-    the persistent engine (cluster size kept: the step kernel puts up to two
-    heads on each cluster and the FFN on every SM)."""
+def fused_local_config(cfg: LlamaConfig, world: int, cluster: int | None = None) -> LlamaConfig:
+    """Per-rank shape of the fused path: the shard of heads / FFN / vocab and
+    the persistent engine.  The attention module of a head runs on one
+    cluster, so with nh/T heads per rank the cluster grows until the heads
+    cover ~64 CTAs (TP2: 16 heads x 4, TP4: 8 x 8, TP8: 4 x 16): the step
+    kernel's per-SM stream rate is capped (~50-90 GB/s, tools/ubench/stream_probe),
+    so a head on 4 SMs would take as long at TP8 as at TP1 (DESIGN.md section 5,
+    profiles/r02/tp_shard_trace.json).  Every choice keeps nh/T <= the
+    co-resident clusters of that size (33 / 15 / 7 for N = 4 / 8 / 16).
+    `cluster` overrides (the single-GPU emulation shares one GPU between the
+    ranks and keeps cfg.cluster)."""
     check_tp(cfg, world)
     eng = cfg.engine if cfg.engine != "layered" else "persistent"
-    return replace(cfg, n_heads=cfg.n_heads // world, inter=cfg.inter // world,
-                   vocab=cfg.vocab // world, engine=eng)
+    nh = cfg.n_heads // world
+    if cluster is None:
+        cluster = cfg.cluster
+        while 2 * cluster <= 16 and nh * cluster < 64 and cfg.head_dim % (2 * cluster) == 0:
+            cluster *= 2
+    return replace(cfg, n_heads=nh, inter=cfg.inter // world, vocab=cfg.vocab // world, engine=eng,
+                   cluster=cluster)
 
 
 class XchBlock:
@@ -92,7 +104,7 @@ class FusedTPLlama:
         if world < 2:
             raise DimensionError("fused tensor parallel needs at least 2 ranks")
         self.cfg, self.rank, self.world = cfg, rank, world
-        self.lcfg = fused_local_config(cfg, world)
+        self.lcfg = fused_local_config(cfg, world, cfg.cluster if emulated else None)
         if params is not None:
             self.eng = LlamaDecoder.from_params(self.lcfg, shard_params(params, rank, world), cache_cap)
         else:
@@ -209,7 +221,7 @@ def emulated_grid(cfg: LlamaConfig, world: int) -> int:
     a 1/world share of the SMs (cluster engines: of the 33 co-resident
     4-CTA clusters a ~225 KB CTA allows, ncu launch__cluster_max_active)."""
     sms = int(_native.lib().cfb_device_sm_count())
-    lcfg = fused_local_config(cfg, world)
+    lcfg = fused_local_config(cfg, world, cfg.cluster)
     if lcfg.engine == "persistent_flat":
         return sms // world
     N = cfg.cluster
