@@ -530,9 +530,11 @@ enum cfb_llama_option {
   CFB_OPT_L2_PREFETCH = 1, /* persistent engines: bytes per CTA of the next phase, past what
                              the smem ring holds, prefetched into L2 at each grid barrier
                              (HBM keeps streaming while the CTA waits); 0 = off */
-  CFB_OPT_PLAIN_LAUNCH = 2 /* persistent engines: 1 = launch without the cooperative
+  CFB_OPT_PLAIN_LAUNCH = 2, /* persistent engines: 1 = launch without the cooperative
                              attribute (the grid is sized co-resident either way; for
                              profilers that cannot replay cooperative cluster launches) */
+  CFB_OPT_RING_SLOTS = 3    /* persistent engines: 8 KB ring slots per consumer warp
+                             (1..3: 64 / 128 / 192 KB per CTA); 0 = the deepest that fits */
 };
 int cfb_llama_set_option(cfb_llama* m, int option, long long value);
 /* Inter-process peer memory for the exchange blocks: cudaMalloc + zero + IPC

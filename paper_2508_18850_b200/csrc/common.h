@@ -98,13 +98,14 @@ struct LlamaStepArgs {
   float* resid2;                 // [D] second residual buffer (layer-parity rotation)
   long long timeout_ns;          // cross-rank wait bound (err = 2 on expiry), 0 = none
   int l2_prefetch;               // bytes/CTA prefetched into L2 past the ring at each barrier
+  int ring_spw;                  // ring slots per consumer warp (8 KB each); 0 = the deepest that fits
 };
 // Exchange block of one tensor-parallel rank: reduced attention / FFN sums
 // [3][D] u64 each (fixed point), the cross-rank barrier counter, the argmax
 // key and the token counter (each on its own 128-byte line).
 size_t tp_xch_bytes(int hidden);
 int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st);
-int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out);
+int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int max_spw, int* spw_out);
 int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* spw_out);
 
 int mha_decode(const cfb_mha_args* a, cudaStream_t st);

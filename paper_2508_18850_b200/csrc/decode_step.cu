@@ -1097,8 +1097,9 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
 
 size_t tp_xch_bytes(int hidden) { return (6 * (size_t)hidden + 48) * 8; }
 
-int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int* spw_out) {
+int llama_step_smem(int D, int F, int nh, int N, int tpr, int V, int G, int max_spw, int* spw_out) {
   int spw = tuned_spw();
+  if (max_spw > 0 && max_spw < spw) spw = max_spw;
   const int TQ = nh * N * tpr, TV = V / 4;
   StepLayout L = step_layout(D, F, TQ, TV, G, N, spw);
   while (L.total > kMaxSmem && spw > 1) L = step_layout(D, F, TQ, TV, G, N, --spw);
@@ -1129,7 +1130,7 @@ int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* s
   const int N = a->cluster, tpr = (3 * (kH / N) + 3) / 4;
   int G = a->grid > 0 && a->grid < sms ? a->grid : sms;
   int spw = 0;
-  int smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, &spw);
+  int smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, a->ring_spw, &spw);
   if (a->cluster_attn) {
     const void* kern = (const void*)llama_step_kernel<true>;
     if (const int rc = configure_kernel(kern, kMaxSmem, true)) return rc;
@@ -1151,7 +1152,7 @@ int llama_step_grid(const LlamaStepArgs* a, int* grid_out, int* smem_out, int* s
       if (G2 < N) return set_error(CFB_ERR_SMEM, "persistent engine: no cluster of %d fits", N);
       if (G2 == G) break;
       G = G2;
-      smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, &spw);
+      smem = llama_step_smem(a->hidden, a->inter, a->n_heads, N, tpr, a->vocab, G, a->ring_spw, &spw);
     }
   }
   if (!a->cluster_attn && G < a->n_heads)  // flattened ranges then span at most two heads

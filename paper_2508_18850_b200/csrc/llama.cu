@@ -45,6 +45,7 @@ struct cfb_llama {
   int tp_fused = 0, emulated = 0;
   int l2_prefetch = 0;  // CFB_OPT_L2_PREFETCH
   int plain_launch = 0; // CFB_OPT_PLAIN_LAUNCH
+  int ring_spw = 0;     // CFB_OPT_RING_SLOTS
   long long timeout_ns = 0;
   unsigned long long** xch_dev = nullptr;  // [tp_size] exchange blocks as this device sees them
   float* resid2 = nullptr;
@@ -224,6 +225,7 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.err = m->err;
   a.trace = m->trace;
   a.l2_prefetch = m->l2_prefetch;
+  a.ring_spw = m->ring_spw;
   a.emulated = m->plain_launch;
   if (m->tp_fused) {
     a.tp_size = m->tp_size;
@@ -508,6 +510,11 @@ int cfb_llama_set_option(cfb_llama* m, int option, long long value) {
       return CFB_OK;
     case CFB_OPT_PLAIN_LAUNCH:
       m->plain_launch = value ? 1 : 0;
+      return CFB_OK;
+    case CFB_OPT_RING_SLOTS:
+      if (value < 0 || value > 3)
+        return cfb::set_error(CFB_ERR_ARGUMENT, "ring slots per consumer warp must be in [0, 3]");
+      m->ring_spw = (int)value;
       return CFB_OK;
   }
   return cfb::set_error(CFB_ERR_ARGUMENT, "unknown engine option %d", option);

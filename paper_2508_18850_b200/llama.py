@@ -319,6 +319,13 @@ class LlamaDecoder:
         L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
         _native.check(L_.cfb_llama_set_option(self._h, 2, 1 if on else 0))
 
+    def set_ring_slots(self, spw: int) -> None:
+        """Persistent engines: 8 KB ring slots per consumer warp (1..3; 0 =
+        the deepest ring that fits); capture again afterwards."""
+        L_ = self._lib
+        L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
+        _native.check(L_.cfb_llama_set_option(self._h, 3, int(spw)))
+
     def check(self) -> None:
         """Raise if a step found the cache full (pos + 1 > cache_cap) and skipped."""
         L_ = self._lib
