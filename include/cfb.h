@@ -207,6 +207,7 @@ typedef struct cfb_mla_engine_args {
   void* ob;
   unsigned long long* accum;
   unsigned long long* barrier;
+  unsigned long long* trace; /* nullable: [grid][16] %globaltimer stamps per CTA (profiling) */
 } cfb_mla_engine_args;
 int cfb_mla_engine_decode(const cfb_mla_engine_args* args, void* stream);
 

@@ -53,7 +53,13 @@ struct MlaEngParams {
   __half* ob;            // [nh*H]
   unsigned long long* accum;   // [D] fixed-point head sum (plain stores)
   unsigned long long* barrier; // [2] proj, out grid barriers (monotonic)
+  unsigned long long* trace;   // [grid][16] %globaltimer stamps (profiling) or null
 };
+
+// profiling stamp k of this CTA (thread 0): proj 0-4, attention 5-7, out 8-13
+__device__ __forceinline__ void mla_stamp(const MlaEngParams& p, int k, int tid) {
+  if (p.trace && tid == 0) p.trace[(size_t)blockIdx.x * 16 + k] = globaltimer();
+}
 
 // ------------------------------------------------------------------ kernel 1
 struct MlaProjLayout {
@@ -111,18 +117,22 @@ __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParam
     return;
   }
   pdl_wait();
+  mla_stamp(p, 0, tid);
   __half* xs = reinterpret_cast<__half*>(smem + L.xs);
   float* part = reinterpret_cast<float*>(smem + L.part);
   __half* qs = reinterpret_cast<__half*>(smem + L.qs);
   float* red = reinterpret_cast<float*>(smem + L.red);
   rmsnorm_to_smem<__half, true>(xs, p.resid, p.norm_w, 1, D, p.eps, red, tid);
+  mla_stamp(p, 1, tid);
   int cnt = 0;
   const int rows = 4 * (a1 - a0);
   tiled_gemv_phase<__half, 1, true>(PA, ring, warp, lane, tid, cnt, xs, D, 1, rows, part,
                                     [&](int row, int, float v) {
                                       p.qc[4 * a0 + row] = __float2half_rn(v);
                                     });
+  mla_stamp(p, 2, tid);
   grid_barrier(p.barrier, tid);
+  mla_stamp(p, 3, tid);
   for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(qs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.qc) + t);
   consumer_sync();
@@ -136,6 +146,8 @@ __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParam
                               });
     });
   }
+  consumer_sync();
+  mla_stamp(p, 4, tid);
 }
 
 // ------------------------------------------------------------------ kernel 2
@@ -203,14 +215,24 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
     for (int k = 0; k < min(kAttnStages - 1, ntiles); ++k)
       if (j0 + k * kAttnRows + kAttnRows <= S) issue(k);
   pdl_wait();
+  mla_stamp(p, 5, tid);
   if (tid == 0)
     for (int k = 0; k < min(kAttnStages - 1, ntiles); ++k)
       if (j0 + k * kAttnRows + kAttnRows > S) issue(k);  // tiles holding the new row
   // q_lat (NH x 512 fp16, zero rows up to 16) -> smem rows of kRowStride
-  for (int k = tid; k < kMlaHeads * 64; k += kAttnThreads) {
-    const int h = k >> 6, ch = k & 63;
-    *reinterpret_cast<uint4*>(qsm + h * kRowStride + ch * 16) =
-        h < p.NH ? __ldcg(reinterpret_cast<const uint4*>(p.qlat + h * 512) + ch) : make_uint4(0, 0, 0, 0);
+  {  // all 8 loads of a thread in flight together (one L2 round trip, not 8)
+    constexpr int kPer = kMlaHeads * 64 / kAttnThreads;
+    uint4 v[kPer];
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int k = tid + j * kAttnThreads, h = k >> 6, ch = k & 63;
+      v[j] = h < p.NH ? __ldcg(reinterpret_cast<const uint4*>(p.qlat + h * 512) + ch) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < kPer; ++j) {
+      const int k = tid + j * kAttnThreads, h = k >> 6, ch = k & 63;
+      *reinterpret_cast<uint4*>(qsm + h * kRowStride + ch * 16) = v[j];
+    }
   }
   __syncthreads();
   // A fragments of this warp's 128 dims (8 k-steps of 16)
@@ -224,6 +246,7 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
 #pragma unroll
     for (int e = 0; e < 4; ++e) zacc[nb][e] = 0.f;
   float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};  // rows g, g + 8
+  mla_stamp(p, 6, tid);
 
   for (int tile = 0; tile < ntiles; ++tile) {
     if (tid == 0 && tile + kAttnStages - 1 < ntiles) issue(tile + kAttnStages - 1);
@@ -341,6 +364,7 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
     *reinterpret_cast<float2*>(z + g * 512 + d) = make_float2(zacc[nb][0], zacc[nb][1]);
     *reinterpret_cast<float2*>(z + (g + 8) * 512 + d) = make_float2(zacc[nb][2], zacc[nb][3]);
   }
+  mla_stamp(p, 7, tid);
 }
 
 // ------------------------------------------------------------------ kernel 3
@@ -397,6 +421,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
     return;
   }
   pdl_wait();
+  mla_stamp(p, 8, tid);
   __half* zs = reinterpret_cast<__half*>(smem + L.zs);
   __half* os = reinterpret_cast<__half*>(smem + L.os);
   float* part = reinterpret_cast<float*>(smem + L.part);
@@ -412,37 +437,68 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
     float* wq = reinterpret_cast<float*>(zs);  // [2][G2] weights, then [2] 1/l
     if (warp < 2 && h0 + warp <= h1) {
       const int h = h0 + warp;
+      float mv[5], lv[5];  // G2 <= 160: all of a lane's (m, l) loads in flight together
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const int q = lane + 32 * j;
+        mv[j] = q < G2 ? __ldcg(p.part + (size_t)q * stride + h) : -INFINITY;
+        lv[j] = q < G2 ? __ldcg(p.part + (size_t)q * stride + kMlaHeads + h) : 0.f;
+      }
       float M = -INFINITY;
-      for (int q = lane; q < G2; q += 32) M = fmaxf(M, __ldcg(p.part + (size_t)q * stride + h));
+#pragma unroll
+      for (int j = 0; j < 5; ++j) M = fmaxf(M, mv[j]);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
       float l = 0.f;
-      for (int q = lane; q < G2; q += 32) {
-        const float mq = __ldcg(p.part + (size_t)q * stride + h);
-        const float w = mq == -INFINITY ? 0.f : exp2f(mq - M);
-        wq[warp * G2 + q] = w;
-        l = fmaf(__ldcg(p.part + (size_t)q * stride + kMlaHeads + h), w, l);
+#pragma unroll
+      for (int j = 0; j < 5; ++j) {
+        const int q = lane + 32 * j;
+        if (q < G2) {
+          const float w = mv[j] == -INFINITY ? 0.f : exp2f(mv[j] - M);
+          wq[warp * G2 + q] = w;
+          l = fmaf(lv[j], w, l);
+        }
       }
       l = warp_allsum(l);
       if (lane == 0) wq[2 * G2 + warp] = 1.0f / l;
     }
     consumer_sync();
-    for (int eb = e0 + 4 * warp; eb < e1; eb += 4 * kNumConsumerWarps) {
-      float z[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int q = lane; q < G2; q += 32) {
-        const float* zq = p.part + (size_t)q * stride + 2 * kMlaHeads;
+    mla_stamp(p, 14, tid);
+    // element-parallel: thread (ei, qg) sums partials q = qg (mod 4) of element
+    // e0 + ei, so a warp's load reads 32 consecutive floats of ONE partial
+    // (coalesced; lanes over partials would cost one L2 sector per lane), 8
+    // loads in flight per thread; the 4 q-subsets are added in fixed order
+    float* zred = reinterpret_cast<float*>(zs) + 1024;  // [4][64], past wq
+    const int ei = tid & 63, qg = tid >> 6;
+    for (int eb = e0; eb < e1; eb += 64) {
+      const int e = eb + ei;
+      float acc = 0.f;
+      if (e < e1) {
+        const float* wrow = wq + (e / 512 - h0) * G2;
+        for (int q0 = qg; q0 < G2; q0 += 32) {
+          float v[8];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-          if (eb + k < e1) z[k] = fmaf(__ldcg(zq + eb + k), wq[((eb + k) / 512 - h0) * G2 + q], z[k]);
-      }
+          for (int j = 0; j < 8; ++j) {
+            const int q = q0 + 4 * j;
+            v[j] = q < G2 ? __ldcg(p.part + (size_t)q * stride + 2 * kMlaHeads + e) : 0.f;
+          }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float v = warp_allsum(z[k]);
-        if (lane == 0 && eb + k < e1) p.zb[eb + k] = __float2half_rn(v * wq[2 * G2 + (eb + k) / 512 - h0]);
+          for (int j = 0; j < 8; ++j)
+            if (q0 + 4 * j < G2) acc = fmaf(v[j], wrow[q0 + 4 * j], acc);
+        }
       }
+      zred[qg * 64 + ei] = acc;
+      consumer_sync();
+      if (tid < 64 && eb + tid < e1) {
+        const float v = ((zred[tid] + zred[64 + tid]) + zred[128 + tid]) + zred[192 + tid];
+        p.zb[eb + tid] = __float2half_rn(v * wq[2 * G2 + (eb + tid) / 512 - h0]);
+      }
+      consumer_sync();
     }
   }
+  mla_stamp(p, 9, tid);
   grid_barrier(p.barrier + 1, tid);
+  mla_stamp(p, 10, tid);
   for (int t = tid; t < NH * 512 / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(zs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.zb) + t);
   consumer_sync();
@@ -458,7 +514,9 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
                                       });
     consumer_sync();
   }
+  mla_stamp(p, 11, tid);
   grid_barrier(p.barrier + 1, tid);
+  mla_stamp(p, 12, tid);
   for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(os)[t] = __ldcg(reinterpret_cast<const uint4*>(p.ob) + t);
   consumer_sync();
@@ -468,6 +526,8 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
                                       p.accum[4 * o0 + row] = static_cast<unsigned long long>(
                                           __float2ll_rn(v * 4294967296.0f));
                                     });
+  consumer_sync();
+  mla_stamp(p, 13, tid);
 }
 
 // ------------------------------------------------------------------ host
@@ -527,10 +587,12 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   p.ob = static_cast<__half*>(a->ob);
   p.accum = a->accum;
   p.barrier = a->barrier;
+  p.trace = a->trace;
   const int T = a->seq_len + 1;
   int G2 = (T + 63) / 64;
   if (G2 > sms) G2 = sms;
   if (a->max_parts > 0 && G2 > a->max_parts) G2 = a->max_parts;
+  if (G2 > 160) G2 = 160;  // mla_out_kernel's merge holds <= 5 partials per lane
   p.G2 = G2;
   const bool pdl = a->flags & CFB_PDL;
   int spw = tuned_spw();

@@ -223,7 +223,8 @@ class DeepSeekBlock:
             w_o=e["w_o"].data_ptr(), cache=e["cache"].data_ptr(), qc=w["qc"].data_ptr(),
             qlat=w["qlat"].data_ptr(), part=w["part"].data_ptr(), zb=w["zb"].data_ptr(),
             ob=w["ob"].data_ptr(), accum=self.accum_attn.data_ptr(),
-            barrier=w["barrier"].data_ptr())
+            barrier=w["barrier"].data_ptr(),
+            trace=self.trace.data_ptr() if getattr(self, "trace", None) is not None else None)
 
     def launch_attention(self, resid, pdl: bool = True, stream=None) -> None:
         if self.engine is not None:
