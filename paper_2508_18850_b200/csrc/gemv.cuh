@@ -381,6 +381,15 @@ __device__ void rmsnorm_to_smem_ld(XElem<XH>* xs, Load&& ld, const T* w, int B, 
   const int warp = tid >> 5, lane = tid & 31;
   const int nv = D / 4;
   constexpr int kReg = 4;
+  // the gains do not depend on the reduction: load them with the first batch
+  // (one round trip instead of two - the gain rows are usually cold in L2)
+  using GVec = typename std::conditional<sizeof(T) == 2, uint2, float4>::type;
+  GVec gv[kReg];
+#pragma unroll
+  for (int k = 0; k < kReg; ++k) {
+    const int v = tid + k * kConsumerThreads;
+    if (v < nv) gv[k] = *reinterpret_cast<const GVec*>(w + 4 * v);
+  }
   for (int b = 0; b < B; ++b) {
     float4 c[kReg];
     float ss = 0.f;
@@ -402,15 +411,15 @@ __device__ void rmsnorm_to_smem_ld(XElem<XH>* xs, Load&& ld, const T* w, int B, 
     float tot = 0.f;
     for (int w2 = 0; w2 < kNumConsumerWarps; ++w2) tot += red[b * kNumConsumerWarps + w2];
     const float inv = 1.0f / sqrtf(__fdiv_rn(tot, (float)D) + eps);
-    auto emit = [&](const float4& a, int v) {
+    auto emit = [&](const float4& a, int v, const GVec* pre) {
       float g[4];
       if constexpr (sizeof(T) == 2) {
-        const uint2 wv = *reinterpret_cast<const uint2*>(w + 4 * v);
+        const uint2 wv = pre ? *pre : *reinterpret_cast<const uint2*>(w + 4 * v);
         const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&wv.x));
         const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&wv.y));
         g[0] = g01.x; g[1] = g01.y; g[2] = g23.x; g[3] = g23.y;
       } else {
-        const float4 wv = *reinterpret_cast<const float4*>(w + 4 * v);
+        const float4 wv = pre ? *pre : *reinterpret_cast<const float4*>(w + 4 * v);
         g[0] = wv.x; g[1] = wv.y; g[2] = wv.z; g[3] = wv.w;
       }
       float o[4] = {__fmul_rn(__fmul_rn(a.x, inv), g[0]), __fmul_rn(__fmul_rn(a.y, inv), g[1]),
@@ -429,8 +438,8 @@ __device__ void rmsnorm_to_smem_ld(XElem<XH>* xs, Load&& ld, const T* w, int B, 
     };
 #pragma unroll
     for (int k = 0; k < kReg; ++k)
-      if (tid + k * kConsumerThreads < nv) emit(c[k], tid + k * kConsumerThreads);
-    for (int v = tid + kReg * kConsumerThreads; v < nv; v += kConsumerThreads) emit(ld(b, v), v);
+      if (tid + k * kConsumerThreads < nv) emit(c[k], tid + k * kConsumerThreads, &gv[k]);
+    for (int v = tid + kReg * kConsumerThreads; v < nv; v += kConsumerThreads) emit(ld(b, v), v, nullptr);
   }
   consumer_sync();
 }

@@ -205,14 +205,16 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   // ---------------------------------------------------------------- consumers
   pdl_wait();
   unsigned long long* tr = p.trace ? p.trace + (size_t)i * 16 : nullptr;
-  auto stamp = [&](int k) {  // SM cycle counter (globaltimer is too coarse on B200)
-    if (tr && tid == 0) tr[k] = clock64();
+  auto stamp = [&](int k) {  // %globaltimer ns (comparable across SMs and kernels)
+    if (tr && tid == 0) tr[k] = globaltimer();
   };
   stamp(0);
   // launch epoch: barrier[0] counts finished CTAs (G per launch); no CTA of
   // this launch can finish before every CTA has published its router rows
+  // (relaxed: the previous launch completed before pdl_wait returned; the
+  // load's latency then overlaps the RMSNorm prologue instead of blocking it)
   const unsigned long long epoch =
-      tid == 0 ? ld_acquire_u64(p.barrier) / (unsigned long long)G : 0ull;
+      tid == 0 ? ld_relaxed_u64(p.barrier) / (unsigned long long)G : 0ull;
   __half* xs = reinterpret_cast<__half*>(smem + L.xs);
   float* lg = reinterpret_cast<float*>(smem + L.logit);   // [2][B][E]: logits, gate weights
   float* gw = reinterpret_cast<float*>(smem + L.gw);      // [B][umax]

@@ -243,7 +243,7 @@ class DeepSeekBlock:
             attn_reduce(self.accum_attn)
         moe_launch(self.moe, self.ws, resid, resid=resid, norm_w=self.ffn_norm,
                    accum_in=self.accum_attn, eps=self.dims.eps, pdl=pdl and attn_reduce is None,
-                   stream=stream, partial=self.partial)
+                   stream=stream, partial=self.partial, trace=getattr(self, "moe_trace", None))
 
     def run(self, resid_host) -> tuple[np.ndarray, np.ndarray]:
         """Host convenience: one block on (B, D) fp32 rows.  Returns (new

@@ -60,7 +60,7 @@ torch.cuda.synchronize()
 t = tr.cpu().numpy().astype("float64")
 t = t[t[:, 0] > 0]
 import numpy as np  # noqa: E402
-rel = np.where(t[:, :14] > 0, (t[:, :14] - t[:, :1]) / 1965.0, np.nan)  # cycles -> us at max clock
+rel = np.where(t[:, :14] > 0, (t[:, :14] - t[:, :1]) / 1e3, np.nan)  # globaltimer ns -> us
 names = ["start", "norm", "router", "routed", "shared_gu", "shared_dn", "routed_gu", "routed_dn",
          "atomics", "last_cta", "end", "r_polled", "r_loaded", "r_ranked"]
 print("cta0", [round(float(x), 2) for x in rel[0]], "cta77", [round(float(x), 2) for x in rel[77]])
