@@ -20,7 +20,7 @@ a = ap.parse_args()
 names = {0: "proj_start", 1: "proj_norm", 2: "proj_qc", 3: "proj_barrier", 4: "proj_qlat",
          5: "attn_start", 6: "attn_q", 7: "attn_end", 8: "out_start", 14: "out_weights", 9: "out_merge",
          10: "out_barrier1", 11: "out_wdown", 12: "out_barrier2", 13: "out_end"}
-moe_names = {0: "moe_start", 1: "moe_norm", 2: "moe_router", 11: "moe_polled", 12: "moe_loaded",
+moe_names = {0: "moe_start", 14: "moe_norm1", 1: "moe_norm", 2: "moe_router", 11: "moe_polled", 12: "moe_loaded",
              13: "moe_ranked", 3: "moe_routed", 7: "moe_experts", 8: "moe_atomics", 9: "moe_last",
              10: "moe_end"}
 res = {}
