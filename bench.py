@@ -288,7 +288,7 @@ def run_ours(args, rank, world):
                         ("dropin_attention_module", lambda: dropin_api(pk["hbm_gbs"])),
                         ("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch16_ffn_tcgen05", lambda: batch16_ffn(cfg, pk["hbm_gbs"])),
-                        ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096], pk["hbm_gbs"]))):
+                        ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096, 16384], pk["hbm_gbs"]))):
             try:  # secondary configs; never lose the headline line over one of them
                 line[key] = fn()
                 items = line[key] if isinstance(line[key], list) else [line[key]]
