@@ -102,3 +102,15 @@ def test_persistent_trace_stamps_monotone(engine):
     t = tr.cpu().numpy()
     assert (t > 0).all()
     assert (np.diff(t, axis=2) >= 0).all()
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_persistent_tp_shard_cluster(world):
+    """One rank's shard of the fused tensor-parallel path at Llama2-7B width
+    with the cluster size `fused_local_config` picks for it (TP2: 4, TP4: 8,
+    TP8: 16 - non-portable), against the oracle on the shard's dims."""
+    from paper_2508_18850_b200.tp_fused import fused_local_config
+    full = LlamaConfig(n_layers=2, hidden=4096, n_heads=32, head_dim=128, inter=11008, vocab=32000)
+    cfg = fused_local_config(full, world)
+    assert cfg.cluster == {2: 4, 4: 8, 8: 16}[world]
+    _run(cfg, 700, steps=2, seed=10 + world)
