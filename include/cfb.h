@@ -183,12 +183,12 @@ int cfb_mla_decode(const cfb_mla_args* args, void* stream);
  * Input x = f16(rmsnorm(resid) * norm_w).  Layouts (fp16):
  *   w_a   row tiles of [W_q^T (n_heads*H rows) ; W_kv^T (512 rows)] x D
  *   w_up  rows h*512 + j = W_up[h][:, j] (H), chunk-rotated by row index
- *   w_dn  row tiles of W_down^T: rows h*H + i = W_down[h][:, i] (512)
+ *   w_dn  W_down as given: [n_heads][512][H] (row h*512 + j = W_down[h][j, :])
  *   w_o   row tiles of W_out^T: row d = [W_out[0][:, d] ; ... ; W_out[15][:, d]]
  *   cache [seq_len][512]
  * Workspaces: qc [16*H + 512] fp16, qlat [16][512] fp16, part [min(SMs,
- * max_parts)][32 + 16*512] fp32, zb [16][512] fp16, ob [16*H] fp16, barrier two
- * u64 (zero, then monotonic).
+ * max_parts)][32 + 16*512] fp32, o_acc [16*H] u64 (zero: the attention launch
+ * re-zeroes it every step), barrier two u64 (zero, then monotonic).
  */
 typedef struct cfb_mla_engine_args {
   int hidden, n_heads, head_dim, kv_rank, seq_len, flags, max_parts;
@@ -203,8 +203,7 @@ typedef struct cfb_mla_engine_args {
   void* qc;
   void* qlat;
   float* part;
-  void* zb;
-  void* ob;
+  unsigned long long* o_acc;
   unsigned long long* accum;
   unsigned long long* barrier;
   unsigned long long* trace; /* nullable: [grid][16] %globaltimer stamps per CTA (profiling) */

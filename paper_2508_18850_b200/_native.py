@@ -137,7 +137,7 @@ class MlaEngineArgs(ctypes.Structure):
                                              "flags", "max_parts")] + [
         ("eps", ctypes.c_float)] + [
         (n, _vp) for n in ("resid", "norm_w", "w_a", "w_up", "w_dn", "w_o", "cache", "qc", "qlat",
-                           "part", "zb", "ob", "accum", "barrier", "trace")]
+                           "part", "o_acc", "accum", "barrier", "trace")]
 
 
 class FfnB16Args(ctypes.Structure):

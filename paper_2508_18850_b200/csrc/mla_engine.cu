@@ -16,10 +16,12 @@
 //                    warp-level tensor-core MMAs (mma.sync m16n8k16, heads =
 //                    the M=16 dimension): S = Q_lat L^T, online softmax,
 //                    Z += P L; partial (m, l, Z) per CTA
-//   mla_out_kernel   (persistent grid)  merge the partials -> z (fp16);
-//                    -- grid barrier --  o[h] = f16(z[h] W_down[h]);
-//                    -- grid barrier --  out = sum_h o[h] W_out[h] -> the
-//                    fixed-point head-sum accumulator the MoE kernel reads.
+//   mla_out_kernel   (persistent grid)  merge the partials -> this CTA's z
+//                    elements (fp16), and straight away their split-K share
+//                    of o[h] = z[h] W_down[h] (W_down rows of those elements)
+//                    into a 64-bit fixed-point o accumulator;
+//                    -- grid barrier --  o = f16(o_acc); out = sum_h o[h] W_out[h]
+//                    -> the fixed-point head-sum accumulator the MoE reads.
 #include <cuda_runtime.h>
 
 #include <utility>
@@ -43,14 +45,13 @@ struct MlaEngParams {
   const __half* norm_w;
   const __half* w_a;     // row tiles of [W_q^T (nh*H rows) ; W_kv^T (R rows)] x D
   const __half* w_up;    // rows h*R + j = W_up[h][:, j] (H), chunk-rotated by row
-  const __half* w_dn;    // row tiles of W_down^T: rows h*H + i = W_down[h][:, i] (R)
+  const __half* w_dn;    // W_down [nh][R][H]: row h*R + j = W_down[h][j, :]
   const __half* w_o;     // row tiles of W_out^T: rows d = [W_out[h][:, d]]_h (nh*H)
   const __half* cache;   // [S][R]
   __half* qc;            // [nh*H + R]  q | new latent row
   __half* qlat;          // [nh][R]
   float* part;           // [G2][2*nh + nh*R]  m, l, Z per attention CTA
-  __half* zb;            // [nh][R]
-  __half* ob;            // [nh*H]
+  unsigned long long* o_acc;  // [nh*H] fixed-point o (zeroed by the attention launch)
   unsigned long long* accum;   // [D] fixed-point head sum (plain stores)
   unsigned long long* barrier; // [2] proj, out grid barriers (monotonic)
   unsigned long long* trace;   // [grid][16] %globaltimer stamps (profiling) or null
@@ -216,6 +217,9 @@ __global__ void __launch_bounds__(kAttnThreads) mla_attn_kernel(const MlaEngPara
       if (j0 + k * kAttnRows + kAttnRows <= S) issue(k);
   pdl_wait();
   mla_stamp(p, 5, tid);
+  // o_acc's previous reader (the last step's mla_out) completed long before
+  // this launch; its next writers (this step's mla_out) start after it
+  for (int t = c * kAttnThreads + tid; t < p.NH * p.H; t += G2 * kAttnThreads) p.o_acc[t] = 0ull;
   if (tid == 0)
     for (int k = 0; k < min(kAttnStages - 1, ntiles); ++k)
       if (j0 + k * kAttnRows + kAttnRows > S) issue(k);  // tiles holding the new row
@@ -373,8 +377,8 @@ struct MlaOutLayout {
 };
 __host__ __device__ inline MlaOutLayout mla_out_layout(int D, int H, int G, int spw) {
   MlaOutLayout L;
-  const int tdn = (kMlaHeads * H / 4 + G - 1) / G + 1, to = (D / 4 + G - 1) / G;
-  const int rows = 4 * (tdn > to ? tdn : to);
+  const int to = (D / 4 + G - 1) / G;
+  const int rows = 4 * to;
   int o = ring_bytes(spw);
   L.bars = o;  o += 2 * kNumSlots * 8;
   L.zs = o;    o += kMlaHeads * 512 * 2;
@@ -391,14 +395,16 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // W_down^T row tiles of this CTA, split at head boundaries (H/4 tiles per head)
-  const int NH = p.NH, TD = NH * H / 4, tph = H / 4;
-  const int d0 = (int)((long long)i * TD / G), d1 = (int)((long long)(i + 1) * TD / G);
-  const int hd0 = d0 / tph;
-  auto dseg = [&](int s, int& t0, int& t1) {
-    const int h = hd0 + s;
-    t0 = max(d0, h * tph);
-    t1 = min(d1, (h + 1) * tph);
+  const int NH = p.NH;
+  // z elements [e0, e1) of the NH*R (head-major) merge; their W_down rows
+  // are the same indices of the [NH*R][H] layout, cut at the head boundary
+  const int NZ = NH * R;
+  const int e0 = (int)((long long)i * NZ / G), e1 = (int)((long long)(i + 1) * NZ / G);
+  const int h0 = e0 / R, h1 = (e1 - 1) / R;
+  auto eseg = [&](int s, int& a, int& b) {
+    const int h = h0 + s;
+    a = max(e0, h * R);
+    b = min(e1, (h + 1) * R);
     return h;
   };
   const int TO = D / 4;
@@ -408,11 +414,17 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
     fence_mbar_init();
   }
   __syncthreads();
-  int t0, t1;
-  dseg(0, t0, t1);
-  const Phase PD0 = make_phase(p.w_dn + (size_t)t0 * 4 * R, nullptr, max(t1 - t0, 0), 4 * R * 2, true);
-  dseg(1, t0, t1);
-  const Phase PD1 = make_phase(p.w_dn + (size_t)t0 * 4 * R, nullptr, max(t1 - t0, 0), 4 * R * 2, true);
+  // 8 rows per item (not a full 32-row slot) so the ~56 rows spread over 7 warps
+  auto rows8 = [](Phase P) {
+    P.per_item = 8;
+    P.n_items = (P.n_units + 7) / 8;
+    return P;
+  };
+  int ea, eb;
+  eseg(0, ea, eb);
+  const Phase PD0 = rows8(make_phase(p.w_dn + (size_t)ea * H, nullptr, max(eb - ea, 0), H * 2));
+  eseg(1, ea, eb);
+  const Phase PD1 = rows8(make_phase(p.w_dn + (size_t)ea * H, nullptr, h1 > h0 ? max(eb - ea, 0) : 0, H * 2));
   const Phase PO = make_phase(p.w_o + (size_t)o0 * 4 * NH * H, nullptr, o1 - o0, 4 * NH * H * 2, true);
   pdl_launch_dependents();
   if (warp == kNumConsumerWarps) {
@@ -429,11 +441,9 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
   //    per head (<= 2 per CTA) the weights w_q = 2^(m_q - M) and 1 / sum_q w_q l_q
   //    once into smem, then per element the sum over q split across a warp's
   //    lanes, 4 elements per pass so their loads are in flight together
+  float* zloc = reinterpret_cast<float*>(zs) + 2048;  // [e1 - e0 <= 512] merged z (fp16 values)
   {
-    const int NZ = NH * 512;
-    const int e0 = (int)((long long)i * NZ / G), e1 = (int)((long long)(i + 1) * NZ / G);
     const int stride = 2 * kMlaHeads + kMlaHeads * 512;
-    const int h0 = e0 / 512, h1 = (e1 - 1) / 512;
     float* wq = reinterpret_cast<float*>(zs);  // [2][G2] weights, then [2] 1/l
     if (warp < 2 && h0 + warp <= h1) {
       const int h = h0 + warp;
@@ -491,34 +501,50 @@ __global__ void __launch_bounds__(kThreads, 1) mla_out_kernel(const MlaEngParams
       consumer_sync();
       if (tid < 64 && eb + tid < e1) {
         const float v = ((zred[tid] + zred[64 + tid]) + zred[128 + tid]) + zred[192 + tid];
-        p.zb[eb + tid] = __float2half_rn(v * wq[2 * G2 + (eb + tid) / 512 - h0]);
+        zloc[eb - e0 + tid] = round_to<__half>(v * wq[2 * G2 + (eb + tid) / 512 - h0]);
       }
       consumer_sync();
     }
   }
   mla_stamp(p, 9, tid);
-  grid_barrier(p.barrier + 1, tid);
-  mla_stamp(p, 10, tid);
-  for (int t = tid; t < NH * 512 / 8; t += kConsumerThreads)
-    reinterpret_cast<uint4*>(zs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.zb) + t);
-  consumer_sync();
-  // 2. o[h] = f16(z[h] W_down[h])
+  // 2. split-K share of o[h] = z[h] W_down[h] over this CTA's z elements: a
+  //    warp's lanes own 4 of the H outputs, rows (z elements) come from the
+  //    ring; warps are summed in order, then one fixed-point red.add per output
   int cnt = 0;
+  float* wred = reinterpret_cast<float*>(zs) + 2560;  // [8 warps][H]
   for (int s = 0; s < 2; ++s) {
-    const int h = dseg(s, t0, t1);
-    const int rows = 4 * max(t1 - t0, 0);
-    tiled_gemv_phase<__half, 1, true>(s == 0 ? PD0 : PD1, ring, warp, lane, tid, cnt,
-                                      zs + (size_t)h * 512, 512, 1, rows, part,
-                                      [&](int row, int, float v) {
-                                        p.ob[4 * t0 + row] = __float2half_rn(v);
-                                      });
+    const int h = eseg(s, ea, eb);
+    if (s == 1 && h1 == h0) break;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    const int c4 = 4 * lane;  // this lane's outputs (H <= 128)
+    consume_phase(s == 0 ? PD0 : PD1, ring, warp, lane, cnt, [&](const Item& it, const char* slot) {
+      for (int r = 0; r < it.nunits; ++r) {
+        const float z = zloc[ea + it.unit0 + r - e0];
+        if (c4 < H) {
+          const uint2 wv = *reinterpret_cast<const uint2*>(slot + (size_t)r * H * 2 + c4 * 2);
+          const float2 w01 = __half22float2(*reinterpret_cast<const __half2*>(&wv.x));
+          const float2 w23 = __half22float2(*reinterpret_cast<const __half2*>(&wv.y));
+          acc[0] = fmaf(z, w01.x, acc[0]);
+          acc[1] = fmaf(z, w01.y, acc[1]);
+          acc[2] = fmaf(z, w23.x, acc[2]);
+          acc[3] = fmaf(z, w23.y, acc[3]);
+        }
+      }
+    });
+    if (c4 < H) *reinterpret_cast<float4*>(wred + warp * 128 + c4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    consumer_sync();
+    if (tid < H) {
+      float v = 0.f;
+      for (int w = 0; w < kNumConsumerWarps; ++w) v += wred[w * 128 + tid];
+      red_add_fixed(p.o_acc + (size_t)h * H + tid, v);
+    }
     consumer_sync();
   }
   mla_stamp(p, 11, tid);
   grid_barrier(p.barrier + 1, tid);
   mla_stamp(p, 12, tid);
-  for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
-    reinterpret_cast<uint4*>(os)[t] = __ldcg(reinterpret_cast<const uint4*>(p.ob) + t);
+  for (int t = tid; t < NH * H; t += kConsumerThreads)
+    os[t] = __float2half_rn(fixed_to_float(__ldcg(p.o_acc + t)));
   consumer_sync();
   // 3. out = sum_h o[h] W_out[h] -> fixed point (each row owned by one CTA)
   tiled_gemv_phase<__half, 1, true>(PO, ring, warp, lane, tid, cnt, os, NH * H, 1,
@@ -554,7 +580,7 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
                      "head-batched MLA engine: 1..16 heads, kv_lora_rank 512, head_dim <= 128 (x8), hidden % 512 == 0");
   if (a->seq_len < 0) return set_error(CFB_ERR_DIMENSION, "seq_len must be >= 0");
   if (!a->resid || !a->norm_w || !a->w_a || !a->w_up || !a->w_dn || !a->w_o || !a->qc || !a->qlat ||
-      !a->part || !a->zb || !a->ob || !a->accum || !a->barrier || (a->seq_len && !a->cache))
+      !a->part || !a->o_acc || !a->accum || !a->barrier || (a->seq_len && !a->cache))
     return set_error(CFB_ERR_ARGUMENT, "null pointer");
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
@@ -583,8 +609,7 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   p.qc = static_cast<__half*>(a->qc);
   p.qlat = static_cast<__half*>(a->qlat);
   p.part = a->part;
-  p.zb = static_cast<__half*>(a->zb);
-  p.ob = static_cast<__half*>(a->ob);
+  p.o_acc = a->o_acc;
   p.accum = a->accum;
   p.barrier = a->barrier;
   p.trace = a->trace;

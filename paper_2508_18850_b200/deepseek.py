@@ -94,7 +94,7 @@ def pack_mla_engine(w_q, w_up, w_kv, w_down, w_out, cache, dev):
     w_a = torch.cat([wq.permute(0, 2, 1).reshape(nh * H, D), wkv.t()], 0).contiguous()
     out = dict(w_a=row_tiles(w_a),
                w_up=rotated_rows(wup.permute(0, 2, 1).reshape(nh * R, H).contiguous()),
-               w_dn=row_tiles(wdn.permute(0, 2, 1).reshape(nh * H, R).contiguous()),
+               w_dn=wdn.reshape(nh * R, H).contiguous(),
                w_o=row_tiles(wo.reshape(nh * H, D).t().contiguous()))
     S = cache.shape[0]
     out["cache"] = t(cache).contiguous() if S else torch.zeros(1, R, device=dev, dtype=torch.float16)
@@ -132,8 +132,7 @@ class DeepSeekBlock:
                 qlat=torch.zeros(nh * R, device=dev, dtype=torch.float16),
                 # partials keep all 16 MMA head rows whatever nh is (cfb.h)
                 part=torch.zeros(sms, 2 * 16 + 16 * R, device=dev, dtype=torch.float32),
-                zb=torch.zeros(nh * R, device=dev, dtype=torch.float16),
-                ob=torch.zeros(nh * H, device=dev, dtype=torch.float16),
+                o_acc=torch.zeros(nh * H, device=dev, dtype=torch.int64),
                 barrier=torch.zeros(2, device=dev, dtype=torch.int64))
         # the workspaces were zeroed on torch's current stream; launches may use
         # another stream, and the monotonic counters must read zero there
@@ -221,8 +220,8 @@ class DeepSeekBlock:
             eps=d.eps, resid=resid.data_ptr(), norm_w=self.attn_norm.data_ptr(),
             w_a=e["w_a"].data_ptr(), w_up=e["w_up"].data_ptr(), w_dn=e["w_dn"].data_ptr(),
             w_o=e["w_o"].data_ptr(), cache=e["cache"].data_ptr(), qc=w["qc"].data_ptr(),
-            qlat=w["qlat"].data_ptr(), part=w["part"].data_ptr(), zb=w["zb"].data_ptr(),
-            ob=w["ob"].data_ptr(), accum=self.accum_attn.data_ptr(),
+            qlat=w["qlat"].data_ptr(), part=w["part"].data_ptr(),
+            o_acc=w["o_acc"].data_ptr(), accum=self.accum_attn.data_ptr(),
             barrier=w["barrier"].data_ptr(),
             trace=self.trace.data_ptr() if getattr(self, "trace", None) is not None else None)
 
