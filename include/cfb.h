@@ -290,13 +290,13 @@ typedef struct cfb_moe_args {
   const void* w_dn;
   const void* s_gu;
   const void* s_dn;
-  unsigned long long* accum;
+  float* part;                 /* [grid][batch*hidden] fp32 workspace: per-CTA MoE partial sums */
   float* out;
   int* route_idx;
   float* route_w;
   unsigned long long* barrier;
   float* logits;
-  unsigned long long* trace;   /* [grid CTAs][16] clock64 phase stamps (profiling), or NULL */
+  unsigned long long* trace;   /* [grid CTAs][16] %globaltimer phase stamps (profiling), or NULL */
 } cfb_moe_args;
 int cfb_moe_decode(const cfb_moe_args* args, void* stream);
 

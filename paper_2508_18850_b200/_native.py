@@ -164,7 +164,7 @@ class MoeArgs(ctypes.Structure):
                                              "inter", "shared_inter", "flags", "grid")] + [
         ("eps", ctypes.c_float), ("routed_scale", ctypes.c_float)] + [
         (n, _vp) for n in ("x", "resid", "accum_in", "norm_w", "w_router", "w_gu", "w_dn", "s_gu",
-                           "s_dn", "accum", "out", "route_idx", "route_w", "barrier", "logits", "trace")]
+                           "s_dn", "part", "out", "route_idx", "route_w", "barrier", "logits", "trace")]
 
 
 def bind_extra(L) -> None:

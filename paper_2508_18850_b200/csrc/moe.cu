@@ -60,7 +60,7 @@ struct MoeParams {
   const __half* w_dn;
   const __half* s_gu;
   const __half* s_dn;
-  unsigned long long* accum;  // [B][D] MoE fixed-point sum (zero; re-zeroed)
+  float* part;                // [grid][B*D] per-CTA partial sums (workspace)
   float* out;
   int* route_idx;
   float* route_w;
@@ -527,52 +527,64 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   consumer_sync();
   stamp(7);
 
-  // 5. this CTA's split-K partial into the fixed-point accumulator
-  const int nparts = 8 / Q;
-  for (int t = tid; t < B * D; t += kConsumerThreads) {
+  // 5. this CTA's split-K partial -> its row of the partial buffer (plain
+  //    coalesced stores, no atomics)
+  const int nparts = 8 / Q, BD = B * D;
+  for (int t = tid; t < BD; t += kConsumerThreads) {
     float v = 0.f;
-    for (int s2 = 0; s2 < nparts; ++s2) v += dpart[(size_t)s2 * B * D + t];
-    red_add_fixed(p.accum + t, v);
+    for (int s2 = 0; s2 < nparts; ++s2) v += dpart[(size_t)s2 * BD + t];
+    p.part[(size_t)i * BD + t] = v;
   }
   stamp(8);
-  // 6. the last CTA to finish writes out = [resid + attention sum +] MoE sum
-  //    and re-zeroes the accumulators (no grid-wide wait for the others)
-  __threadfence();
+  // 6. barrier[0] (monotonic, G arrivals per launch; `epoch` read at launch):
+  //    every CTA arrives; only the first NF CTAs wait and finish a column
+  //    slice each, the others leave their SM to the next launch at once.
+  //    out = [resid + attention sum +] sum over the G partial rows, summed as
+  //    8 row-interleaved subsets (coalesced 32-column reads, all <= 20 loads
+  //    of a thread in flight at once) combined in fixed order -
+  //    deterministic, nothing to re-zero
+  const int NF = G < 64 ? G : 64;
   consumer_sync();
-  int* last = reinterpret_cast<int*>(red);
   if (tid == 0) {
-    const unsigned long long old = atomicAdd(p.barrier, 1ull);
-    *last = (old + 1ull) % (unsigned long long)G == 0ull;
+    asm volatile("red.release.gpu.global.add.u64 [%0], 1;" ::"l"(p.barrier) : "memory");
+    if (i < NF) spin_until_geq(p.barrier, (epoch + 1ull) * (unsigned long long)G);
   }
+  if (i >= NF) return;
   consumer_sync();
-  if (!*last) return;
-  __threadfence();
   stamp(9);
-  const int n4 = B * D / 4;
-  for (int t = tid; t < n4; t += kConsumerThreads) {
-    const ulonglong2 m0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum) + 2 * t);
-    const ulonglong2 m1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum) + 2 * t + 1);
-    float v[4] = {fixed_to_float(m0.x), fixed_to_float(m0.y), fixed_to_float(m1.x), fixed_to_float(m1.y)};
-    reinterpret_cast<ulonglong2*>(p.accum)[2 * t] = make_ulonglong2(0ull, 0ull);
-    reinterpret_cast<ulonglong2*>(p.accum)[2 * t + 1] = make_ulonglong2(0ull, 0ull);
-    if (p.flags & CFB_RESID) {
-      const float4 r4 = __ldcg(reinterpret_cast<const float4*>(p.resid) + t);
-      float r[4] = {r4.x, r4.y, r4.z, r4.w};
-      if (p.accum_in) {
-        const ulonglong2 a0 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum_in) + 2 * t);
-        const ulonglong2 a1 = __ldcg(reinterpret_cast<const ulonglong2*>(p.accum_in) + 2 * t + 1);
-        r[0] = __fadd_rn(r[0], fixed_to_float(a0.x));
-        r[1] = __fadd_rn(r[1], fixed_to_float(a0.y));
-        r[2] = __fadd_rn(r[2], fixed_to_float(a1.x));
-        r[3] = __fadd_rn(r[3], fixed_to_float(a1.y));
-        reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t] = make_ulonglong2(0ull, 0ull);
-        reinterpret_cast<ulonglong2*>(p.accum_in)[2 * t + 1] = make_ulonglong2(0ull, 0ull);
-      }
-      if (!(p.flags & CFB_PARTIAL))  // tensor-parallel rank > 0: its expert-shard partial only
+  const int c0 = (int)((long long)i * BD / NF), c1 = (int)((long long)(i + 1) * BD / NF);
+  float* fsum = dpart;  // [8][32] row-subset sums
+  const int ci = tid & 31, rg = tid >> 5;
+  for (int cb = c0; cb < c1; cb += 32) {
+    const int c = cb + ci;
+    float acc = 0.f;
+    if (c < c1) {
+      constexpr int kRows = 20;  // G <= 160 rows / 8 subsets
+      float v[kRows];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) v[k] = __fadd_rn(r[k], v[k]);
+      for (int k = 0; k < kRows; ++k) v[k] = rg + 8 * k < G ? __ldcg(p.part + (size_t)(rg + 8 * k) * BD + c) : 0.f;
+#pragma unroll
+      for (int k = 0; k < kRows; ++k) acc += v[k];
     }
-    reinterpret_cast<float4*>(p.out)[t] = make_float4(v[0], v[1], v[2], v[3]);
+    fsum[rg * 32 + ci] = acc;
+    consumer_sync();
+    if (tid < 32 && cb + tid < c1) {
+      const int cc = cb + tid;
+      float v = 0.f;
+#pragma unroll
+      for (int g2 = 0; g2 < 8; ++g2) v += fsum[g2 * 32 + tid];
+      float o = v;
+      if (p.flags & CFB_RESID) {
+        float r = __ldcg(p.resid + cc);
+        if (p.accum_in) {
+          r = __fadd_rn(r, fixed_to_float(__ldcg(p.accum_in + cc)));
+          p.accum_in[cc] = 0ull;  // its norm readers (every CTA's prologue) are behind the barrier
+        }
+        if (!(p.flags & CFB_PARTIAL)) o = __fadd_rn(r, v);  // TP rank > 0: its expert-shard partial only
+      }
+      p.out[cc] = o;
+    }
+    consumer_sync();
   }
   stamp(10);
 }
@@ -607,7 +619,7 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
     return set_error(CFB_ERR_DIMENSION, "expert widths must be multiples of 8 (inter >= 8)");
   if (D < 8 || D % 8 || (D > 512 && D % 512) || (D > 512 && 8 % (D / 512)))
     return set_error(CFB_ERR_DIMENSION, "hidden must be a multiple of 8 up to 512, or 512/1024/2048/4096");
-  if (!a->w_router || !a->w_gu || !a->w_dn || (Fs && (!a->s_gu || !a->s_dn)) || !a->accum ||
+  if (!a->w_router || !a->w_gu || !a->w_dn || (Fs && (!a->s_gu || !a->s_dn)) || !a->part ||
       !a->out || !a->barrier || !a->logits)
     return set_error(CFB_ERR_ARGUMENT, "null weight / workspace pointer");
   if ((a->flags & CFB_NORM) ? (!a->resid || !a->norm_w) : !a->x)
@@ -621,6 +633,7 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
   const int Ge = Fe / 8;
   int grid = a->grid > 0 ? a->grid : sms;
   if (grid > sms) grid = sms;         // routing waits on every CTA's router rows: co-resident
+  if (grid > 160) grid = 160;         // the finalize holds <= 20 partial rows per thread
   if (grid > K * Ge) grid = K * Ge;   // routed groups >= grid keeps every range non-empty-ordered
   const int Q = moe_segments(D);
   int spw = tuned_spw();
@@ -650,7 +663,7 @@ int moe_decode(const cfb_moe_args* a, cudaStream_t st) {
   p.w_dn = static_cast<const __half*>(a->w_dn);
   p.s_gu = static_cast<const __half*>(a->s_gu);
   p.s_dn = static_cast<const __half*>(a->s_dn);
-  p.accum = a->accum;
+  p.part = a->part;
   p.out = a->out;
   p.route_idx = a->route_idx;
   p.route_w = a->route_w;

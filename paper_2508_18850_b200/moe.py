@@ -109,13 +109,14 @@ def random_moe_device(hidden: int, n_experts: int, inter: int, n_shared: int, to
 
 
 class MoeWorkspace:
-    """Per-stream workspace of the fused MoE launch (fixed-point accumulator,
+    """Per-stream workspace of the fused MoE launch (per-CTA partial sums,
     grid-barrier counter, routing outputs)."""
 
     def __init__(self, mw: MoeWeights, batch: int, device=None):
         import torch
         dev = device or _native.require_cuda()
-        self.accum = torch.zeros(batch, mw.hidden, device=dev, dtype=torch.int64)
+        sms = max(int(_native.lib().cfb_device_sm_count()), 1)
+        self.part = torch.zeros(sms, batch * mw.hidden, device=dev, dtype=torch.float32)
         self.barrier = torch.zeros(2, device=dev, dtype=torch.int64)  # grid barrier, route counter
         self.logits = torch.zeros(batch, mw.n_experts, device=dev, dtype=torch.float32)
         self.route_idx = torch.zeros(batch, mw.top_k, device=dev, dtype=torch.int32)
@@ -141,7 +142,7 @@ def moe_launch(mw: MoeWeights, ws: MoeWorkspace, out, *, x=None, resid=None, nor
         routed_scale=mw.routed_scale, x=_native.ptr(x), resid=_native.ptr(resid),
         accum_in=_native.ptr(accum_in), norm_w=_native.ptr(norm_w), w_router=mw.router.data_ptr(),
         w_gu=mw.w_gu.data_ptr(), w_dn=mw.w_dn.data_ptr(), s_gu=_native.ptr(mw.s_gu),
-        s_dn=_native.ptr(mw.s_dn), accum=ws.accum.data_ptr(), out=out.data_ptr(),
+        s_dn=_native.ptr(mw.s_dn), part=ws.part.data_ptr(), out=out.data_ptr(),
         route_idx=ws.route_idx.data_ptr(), route_w=ws.route_w.data_ptr(),
         barrier=ws.barrier.data_ptr(), logits=ws.logits.data_ptr(), trace=_native.ptr(trace))
     _native.check(_native.lib().cfb_moe_decode(a, _native.stream_ptr(stream)))
