@@ -136,7 +136,12 @@ def _half_dev(a, dev):
 
 
 class BatchedLlama:
-    """16 independent sequences through a Llama layer stack (tcgen05 path)."""
+    """Up to 16 independent sequences through a Llama layer stack (tcgen05
+    path).  The MMA always runs the 16 rows (N = 16); a sequence whose
+    position is -1 is inactive: no RoPE, no KV-cache write, no attention, its
+    position does not advance and its output row is undefined - so any batch
+    of 1..16 sequences runs on the same kernels (``set_positions`` with fewer
+    than 16 entries pads with inactive rows)."""
 
     def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None,
                  pool: PagedKVPool | None = None):
@@ -284,6 +289,14 @@ class BatchedLlama:
         if advance:
             _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
 
+    @property
+    def active(self) -> np.ndarray:
+        """Indices of the active sequences (position >= 0)."""
+        return np.nonzero(self.host_pos >= 0)[0]
+
+    def _advance_host(self) -> None:
+        self.host_pos[self.host_pos >= 0] += 1
+
     def _limit(self, n: int) -> int:
         """Positions sequence n can hold now: the contiguous cache / max_len, or
         its reserved pages."""
@@ -292,7 +305,7 @@ class BatchedLlama:
 
     def _check_room(self, steps: int = 1) -> None:
         """Raise before a step would append past a sequence's cache."""
-        for n in range(BATCH):
+        for n in self.active:
             if int(self.host_pos[n]) + steps > self._limit(n):
                 raise DimensionError(
                     f"sequence {n}: position {int(self.host_pos[n])} + {steps} step(s) exceeds its "
@@ -300,12 +313,15 @@ class BatchedLlama:
 
     def set_positions(self, pos) -> None:
         import torch
-        pos = np.asarray(pos, np.int64)
-        if pos.shape != (BATCH,) or (pos < 0).any():
-            raise DimensionError(f"set_positions needs {BATCH} non-negative positions")
+        pos = np.asarray(pos, np.int64).reshape(-1)
+        if not 1 <= pos.shape[0] <= BATCH or (pos < -1).any() or not (pos >= 0).any():
+            raise DimensionError(f"set_positions needs 1..{BATCH} positions (>= 0, or -1 = inactive), "
+                                 "at least one active")
+        pos = np.concatenate([pos, np.full(BATCH - pos.shape[0], -1, np.int64)])
         if self.pool:  # the new token's page must exist
             for n, p in enumerate(pos):
-                self.pool.reserve(n, int(p) + 1)
+                if p >= 0:
+                    self.pool.reserve(n, int(p) + 1)
         self.host_pos = pos.copy()
         self._check_room(1)
         self.pos.copy_(torch.as_tensor(pos.astype(np.int32)))
@@ -315,7 +331,7 @@ class BatchedLlama:
         """Paged mode: make the next ``steps`` positions of every sequence
         addressable (call before replaying a captured graph that far)."""
         if self.pool:
-            for n in range(BATCH):
+            for n in self.active:
                 self.pool.reserve(n, int(self.host_pos[n]) + steps)
 
     def step(self, advance: bool = True) -> None:
@@ -323,7 +339,7 @@ class BatchedLlama:
         self._check_room(1)
         self._enqueue(advance)
         if advance:
-            self.host_pos += 1
+            self._advance_host()
 
     def capture(self) -> None:
         import torch
@@ -336,7 +352,7 @@ class BatchedLlama:
         self._check_room(1)
         with torch.cuda.stream(self.stream):
             self.graph.replay()
-        self.host_pos += 1  # every captured step advances the positions
+        self._advance_host()  # every captured step advances the active positions
 
     # ---------------------------------------------------------------- greedy decode
     def set_head(self, embed, final_norm, lm_head) -> None:
@@ -402,7 +418,7 @@ class BatchedLlama:
         self._check_room(1)
         with torch.cuda.stream(self.stream):
             self._enqueue_decode(logits)
-        self.host_pos += 1
+        self._advance_host()
 
     def capture_decode(self) -> None:
         import torch
@@ -417,6 +433,7 @@ class BatchedLlama:
         cfg = self.cfg
         D, F = cfg.hidden, cfg.inter
         w = cfg.n_layers * (2 * (4 * D * D + 3 * D * F) + 4 * D)
-        kv = cfg.n_layers * BATCH * 2 * D * 2 * (ctx + 2)
-        h = 2 * self.V * D + 2 * D + BATCH * 2 * D if head else 0
+        nb = len(self.active) or BATCH
+        kv = cfg.n_layers * nb * 2 * D * 2 * (ctx + 2)
+        h = 2 * self.V * D + 2 * D + nb * 2 * D if head else 0
         return w + kv + h

@@ -256,20 +256,10 @@ int splithead_decode(const cfb_splithead_args* a, cudaStream_t st) {
   cfg.attrs = at.a;
   cfg.numAttrs = at.n;
   if (tb == 2) {
-    static bool c16 = false;
-    if (!c16) {
-      CFB_CUDA(cudaFuncSetAttribute(splithead_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-      CFB_CUDA(cudaFuncSetAttribute(splithead_kernel<__half>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      c16 = true;
-    }
+    if (const int rc = configure_kernel((const void*)splithead_kernel<__half>, kMaxSmem, true)) return rc;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, splithead_kernel<__half>, p));
   } else {
-    static bool c32 = false;
-    if (!c32) {
-      CFB_CUDA(cudaFuncSetAttribute(splithead_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-      CFB_CUDA(cudaFuncSetAttribute(splithead_kernel<float>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-      c32 = true;
-    }
+    if (const int rc = configure_kernel((const void*)splithead_kernel<float>, kMaxSmem, true)) return rc;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, splithead_kernel<float>, p));
   }
   if (!a->out) return CFB_OK;

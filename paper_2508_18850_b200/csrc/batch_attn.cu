@@ -175,11 +175,7 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
                     int max_len, float* part, int* ticket, __half* xp, const int* table, int maxp,
                     cudaStream_t st, bool pdl) {
-  static bool attr = false;
-  if (!attr) {
-    CFB_CUDA(cudaFuncSetAttribute(batch_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kBaSmem));
-    attr = true;
-  }
+  if (const int rc = configure_kernel((const void*)batch_attn_kernel, kBaSmem, false)) return rc;
   const int nchunks = (max_len + kBaChunk - 1) / kBaChunk;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nchunks, 16 * nh, 1);

@@ -78,14 +78,12 @@ int cluster_collective(int dtype, int op, int N, int n, const void* in, void* ou
   cfg.numAttrs = 1;
   if (dtype == CFB_F16) {
     auto k = collective_kat_kernel<__half>;
-    CFB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (const int rc = configure_kernel((const void*)k, kMaxSmem, true)) return rc;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, k, op, n, static_cast<const __half*>(in),
                                 static_cast<__half*>(out), traffic));
   } else {
     auto k = collective_kat_kernel<float>;
-    CFB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
-    CFB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    if (const int rc = configure_kernel((const void*)k, kMaxSmem, true)) return rc;
     CFB_CUDA(cudaLaunchKernelEx(&cfg, k, op, n, static_cast<const float*>(in),
                                 static_cast<float*>(out), traffic));
   }

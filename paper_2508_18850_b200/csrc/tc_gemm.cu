@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
           reinterpret_cast<ulonglong2*>(yr + 64 + i0)[e] = make_ulonglong2(0ull, 0ull);
         }
         const TcQkv& Q = p.qkv;
-        const int kind = t / Q.nh, hd = t % Q.nh, ps = Q.pos[nn];
+        const int kind = t / Q.nh, hd = t % Q.nh, ps_ = Q.pos[nn];
+        const int ps = ps_ < 0 ? 0 : ps_;  // inactive sequence (position -1): no RoPE row, no cache write
         __align__(16) __half a[8], b[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
         __half* dst = nullptr;
         if (kind == 0) {
           dst = Q.q + (size_t)nn * Q.nh * 128 + hd * 128;
-        } else {
+        } else if (ps_ >= 0) {
           // never write outside the sequence's cache: an unassigned page (-1) or a
           // position past the capacity drops the row (the host rejects both)
           __half* cache = kind == 1 ? Q.k_cache : Q.v_cache;
@@ -509,9 +510,9 @@ __global__ void tc_swiglu_pack_kernel(unsigned long long* gu, __half* ap, int F)
   }
 }
 
-__global__ void tc_advance_kernel(int* pos) {  // every sequence moves to its next position
+__global__ void tc_advance_kernel(int* pos) {  // every active sequence moves to its next position
   pdl_wait();
-  if (threadIdx.x < kTcN) pos[threadIdx.x] += 1;
+  if (threadIdx.x < kTcN && pos[threadIdx.x] >= 0) pos[threadIdx.x] += 1;
 }
 
 template <class K, class... Args>

@@ -276,7 +276,7 @@ class TPBatchedLlama:
         self.m._check_room(1)
         with torch.cuda.stream(self.m.stream):
             self._enqueue()
-        self.m.host_pos += 1
+        self.m._advance_host()
 
     def capture(self) -> None:
         import torch
@@ -289,7 +289,7 @@ class TPBatchedLlama:
         self.m._check_room(1)
         with torch.cuda.stream(self.m.stream):
             self.graph.replay()
-        self.m.host_pos += 1
+        self.m._advance_host()
 
 
 # --------------------------------------------------------------------------

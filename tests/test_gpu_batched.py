@@ -142,7 +142,7 @@ def test_batched_greedy_decode_teacher_forced():
         for n in range(16):
             ologits, otok = lp.decode_step(oparams, ocache[n], toks[n], S[n] + step, cfg)
             err = float(np.max(np.abs(glog[n] - ologits)))
-            assert err <= 2e-2 * max(1.0, float(np.max(np.abs(ologits)))), (step, n, err)
+            assert err <= 2e-2 and err / float(np.max(np.abs(ologits))) <= 1e-2, (step, n, err)
             top2 = np.sort(ologits)[-2:]
             if top2[1] - top2[0] > 1e-3:
                 assert got[n] == otok, (step, n, got[n], otok)
@@ -234,3 +234,49 @@ def test_paged_graph_replay_crosses_pages():
     torch.cuda.synchronize()
     assert m.pos.cpu().tolist() == [130 + n for n in range(16)]
     assert bool(((m.tokens >= 0) & (m.tokens < cfg.vocab)).all())
+
+
+@pytest.mark.parametrize("nb", [1, 5, 8])
+def test_batched_partial_batch_matches_oracle(nb):
+    """Any batch of 1..16 sequences on the batch-16 kernels: rows >= nb are
+    inactive (position -1) - no KV write, no position advance - and the
+    active rows match the per-sequence oracle over 2 graph-replayed steps."""
+    import torch
+    cfg = LlamaConfig(n_layers=2, hidden=256, n_heads=2, head_dim=128, inter=384, vocab=64)
+    params = random_llama_params(cfg, seed=21, prefill=0)
+    rng = np.random.default_rng(21 + nb)
+    S = [3 + 41 * n for n in range(16)]
+    cap = max(S) + 6
+    caches = [[(lp.f16(rng.standard_normal((cfg.n_heads, s, 128))),
+                lp.f16(rng.standard_normal((cfg.n_heads, s, 128)))) for s in S]
+              for _ in range(cfg.n_layers)]
+    m = BatchedLlama.from_params(cfg, params["layers"], caches, cache_cap=cap)
+    before = [m.layers[l]["k_cache"][nb:].clone() for l in range(cfg.n_layers)]
+    x = rng.standard_normal((16, cfg.hidden)).astype(np.float32)
+    m.resid.copy_(torch.from_numpy(x))
+    m.set_positions(S[:nb])
+    assert list(m.active) == list(range(nb))
+    m.step()
+    m.step()
+    torch.cuda.synchronize()
+    got = m.resid.cpu().numpy()
+    assert m.pos.cpu().tolist() == [s + 2 for s in S[:nb]] + [-1] * (16 - nb)
+    for l in range(cfg.n_layers):  # inactive sequences' caches untouched
+        assert torch.equal(m.layers[l]["k_cache"][nb:], before[l])
+    cs = rope_table(cap, 128, cfg.rope_theta)
+    for n in range(nb):
+        xn = x[n:n + 1].copy()
+        kcs = []
+        for l in range(cfg.n_layers):
+            kc = np.zeros((cfg.n_heads, cap, 128), np.float32)
+            vc = np.zeros_like(kc)
+            kc[:, :S[n]], vc[:, :S[n]] = caches[l][n]
+            kcs.append((kc, vc))
+        for step in range(2):
+            for l, L in enumerate(params["layers"]):
+                kc, vc = kcs[l]
+                h = lp.rmsnorm_f16(xn, L["attn_norm"], cfg.eps)
+                xn = xn + lp.attention_module(h, L["w_qkv"], L["w_out"], kc, vc, S[n] + step, 1, cs)
+                xn = xn + lp.ffn_block(xn, L["ffn_norm"], L["w1"], L["w2"], L["w3"], cfg.eps)
+        err = float(np.max(np.abs(got[n] - xn[0])))
+        assert err <= 2e-2 and err / float(np.max(np.abs(xn))) <= 1e-2, (n, err)
