@@ -260,7 +260,7 @@ def run_ours(args, rank, world):
                         "(pinned D2H) + stream sync, every step"},
     }
     traffic = None
-    prof = ROOT / "profiles" / "r02" / "ncu_step_kernel.json"
+    prof = ROOT / "profiles" / "r02" / "ncu_step_kernel_e.json"
     if world == 1 and cfg.engine == "persistent":
         # dominant kernel = the ONLY kernel of a step: llama_step_kernel<cluster>;
         # achieved = algorithmic bytes of all timed launches / their total time
