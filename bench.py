@@ -306,7 +306,8 @@ def run_ours(args, rank, world):
         del model
         torch.cuda.empty_cache()
         try:  # extra configs[4] line; never lose the TPOT line over it
-            line["batch16_tp"] = batch16_tp(cfg, rank, world, 1024, pk["hbm_gbs"])
+            # configs[4]: batch 16 at 16K context (and 1K), KV sharded by heads over the ranks
+            line["batch16_tp"] = [batch16_tp(cfg, rank, world, c, pk["hbm_gbs"]) for c in (1024, 16384)]
         except Exception as exc:  # pragma: no cover - multi-GPU only
             line["batch16_tp"] = {"error": f"{type(exc).__name__}: {str(exc)[:200]}"}
         try:
@@ -531,6 +532,7 @@ def batch16_tp(cfg, rank, world, ctx, peak_gbs, steps=10):
     CUDA graph per step; max over ranks."""
     import torch
     from paper_2508_18850_b200.tp import TPBatchedLlama
+    torch.cuda.empty_cache()
     m = TPBatchedLlama(cfg, rank, world, ctx + 3 * steps + 8, seed=rank)
     m.m.set_positions([ctx] * 16)
     m.step()
