@@ -288,7 +288,9 @@ def run_ours(args, rank, world):
                         ("dropin_attention_module", lambda: dropin_api(pk["hbm_gbs"])),
                         ("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch16_ffn_tcgen05", lambda: batch16_ffn(cfg, pk["hbm_gbs"])),
-                        ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096, 16384], pk["hbm_gbs"]))):
+                        ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096, 16384], pk["hbm_gbs"])),
+                        ("batch32_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096], pk["hbm_gbs"], batch=32,
+                                                                        kinds=("layers_only", "greedy_full")))):
             try:  # secondary configs; never lose the headline line over one of them
                 line[key] = fn()
                 items = line[key] if isinstance(line[key], list) else [line[key]]
@@ -476,11 +478,11 @@ def batch16_ffn(cfg, peak_gbs, sets=3, reps=30):
 
 def _time_b16(m, ctx, full, steps):
     import torch
-    m.set_positions([ctx] * 16)
+    m.set_positions([ctx] * m.B)
     m.reserve(4 * steps + 8)
     (m.decode_step if full else m.step)()
     torch.cuda.synchronize()
-    m.set_positions([ctx] * 16)
+    m.set_positions([ctx] * m.B)
     (m.capture_decode if full else m.capture)()
     for _ in range(3):
         m.replay()
@@ -495,7 +497,8 @@ def _time_b16(m, ctx, full, steps):
     return e0.elapsed_time(e1) * 1e3 / steps
 
 
-def batch16_stack(cfg, ctxs, peak_gbs, steps=10):
+def batch16_stack(cfg, ctxs, peak_gbs, steps=10, batch=16, kinds=("layers_only", "greedy_full",
+                                                                   "greedy_full_paged")):
     """Batch 16 independent sequences through the 32-layer Llama2-7B stack
     (batched.BatchedLlama: tcgen05 projections, per-sequence KV caches), CUDA
     graph per step.  Lines per context: the layer stack alone, the full greedy
@@ -507,20 +510,20 @@ def batch16_stack(cfg, ctxs, peak_gbs, steps=10):
     out = []
     for ctx in ctxs:
         cap = ctx + 6 * steps + 16
-        for kind in ("layers_only", "greedy_full", "greedy_full_paged"):
+        for kind in kinds:
             if kind == "greedy_full_paged":
-                m = BatchedLlama.random_paged(cfg, max_len=cap, seed=0)
-            elif kind == "layers_only":
-                m = BatchedLlama.random(cfg, cache_cap=cap, seed=0)
+                m = BatchedLlama.random_paged(cfg, max_len=cap, seed=0, batch=batch)
+            elif kind == "layers_only" or "layers_only" not in kinds:
+                m = BatchedLlama.random(cfg, cache_cap=cap, seed=0, batch=batch)
             m.random_head(cfg.vocab)
             full = kind != "layers_only"
             us = _time_b16(m, ctx, full, steps)
             gbs = m.step_bytes(ctx + 3 + steps // 2, head=full) / us / 1e3
-            out.append({"ctx": ctx, "batch": 16, "step": kind,
-                        "step_us": round(us, 1), "tokens_per_s": round(16e6 / us, 1),
+            out.append({"ctx": ctx, "batch": batch, "step": kind,
+                        "step_us": round(us, 1), "tokens_per_s": round(batch * 1e6 / us, 1),
                         "hbm_gbs": round(gbs, 1), "frac_of_peak": round(gbs / peak_gbs, 4),
                         "launches": (7 * cfg.n_layers + 1 + (4 if full else 0)) * (steps + 4)})
-            if kind != "layers_only":
+            if kind != "layers_only" or kind == kinds[-1]:
                 del m
                 torch.cuda.empty_cache()
     return out

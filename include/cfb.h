@@ -355,6 +355,7 @@ typedef struct cfb_ffn_b16_args {
   void* ap;
   unsigned long long* out_acc;
   int* ticket;
+  int batch;  /* rows = MMA N: 16 (or 0) or 32; the workspaces above scale with it */
 } cfb_ffn_b16_args;
 int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
 
@@ -407,10 +408,13 @@ typedef struct cfb_b16_layer_args {
    * lives in page block_table[n][p / CFB_KV_PAGE] at row p % CFB_KV_PAGE */
   const int* block_table;
   int max_pages;
+  /* sequences = MMA N: 16 (or 0) or 32.  Every "16" above is this batch
+   * (caches, pos, table rows, workspaces); a sequence with pos -1 is inactive */
+  int batch;
 } cfb_b16_layer_args;
 #define CFB_KV_PAGE 128
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);
-int cfb_b16_advance(int* pos, void* stream);
+int cfb_b16_advance(int* pos, int batch, void* stream); /* batch 0 = 16; pos -1 stays -1 */
 /* KV writer (prefill / import): rows [start, start + count) of sequence seq
  * from k_src / v_src [n_heads][count][128] fp16 (device) into the paged pools
  * (block_table as above; the pages must already be assigned) or, with
@@ -423,10 +427,10 @@ int cfb_b16_kv_write(void* k_cache, void* v_cache, const int* block_table, int m
  * fp32 or NULL; xp 16*hidden fp16, y_acc 16*V u64 (zero) and scratch
  * CFB_B16_ARGMAX_SCRATCH u64 (zero) workspaces.  vocab % 128 == 0.  Then
  * cfb_embed(batch 16) gathers the next inputs. */
-#define CFB_B16_ARGMAX_SCRATCH (33 * 32)
+#define CFB_B16_ARGMAX_SCRATCH (65 * 32)
 int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
                     float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
-                    unsigned long long* scratch, void* stream);
+                    unsigned long long* scratch, int batch, void* stream); /* batch 0 = 16, or 32 */
 
 /* out[b][:] = float(table[tokens[b]][:]) */
 int cfb_embed(int dtype, const void* table, const int* tokens, float* out, int batch, int hidden,

@@ -144,7 +144,8 @@ class FfnB16Args(ctypes.Structure):
     """Mirror of ``cfb_ffn_b16_args``."""
 
     _fields_ = [(n, ctypes.c_int) for n in ("hidden", "inter", "flags")] + [("eps", ctypes.c_float)] + [
-        (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc", "ticket")]
+        (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc", "ticket")] + [
+        ("batch", ctypes.c_int)]
 
 
 class B16LayerArgs(ctypes.Structure):
@@ -154,7 +155,8 @@ class B16LayerArgs(ctypes.Structure):
                                              "flags", "stage")] + [("eps", ctypes.c_float)] + [
         (n, _vp) for n in ("resid", "attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gu", "w_dn", "k_cache",
                            "v_cache", "rope_cs", "pos", "xp", "q16", "qkv_acc", "part", "o_acc",
-                           "gu_acc", "ap", "ticket", "block_table")] + [("max_pages", ctypes.c_int)]
+                           "gu_acc", "ap", "ticket", "block_table")] + [("max_pages", ctypes.c_int),
+                                                                        ("batch", ctypes.c_int)]
 
 
 class MoeArgs(ctypes.Structure):
@@ -176,9 +178,9 @@ def bind_extra(L) -> None:
     L.cfb_ffn_b16.restype = ctypes.c_int
     L.cfb_llama_b16_layer.argtypes = [ctypes.POINTER(B16LayerArgs), _vp]
     L.cfb_llama_b16_layer.restype = ctypes.c_int
-    L.cfb_b16_advance.argtypes = [_vp, _vp]
+    L.cfb_b16_advance.argtypes = [_vp, ctypes.c_int, _vp]
     L.cfb_b16_advance.restype = ctypes.c_int
-    L.cfb_b16_lm_head.argtypes = [_vp] * 3 + [ctypes.c_int] * 2 + [ctypes.c_float] + [_vp] * 6
+    L.cfb_b16_lm_head.argtypes = [_vp] * 3 + [ctypes.c_int] * 2 + [ctypes.c_float] + [_vp] * 5 + [ctypes.c_int, _vp]
     L.cfb_b16_lm_head.restype = ctypes.c_int
     L.cfb_b16_kv_write.argtypes = [_vp] * 3 + [ctypes.c_int] * 6 + [_vp] * 3
     L.cfb_b16_kv_write.restype = ctypes.c_int

@@ -1,5 +1,7 @@
-"""Batch-16 decode of 16 independent sequences on tcgen05 (north-star "tensor
-cores for the batch>1 projections"; BASELINE config #5 batch 16).
+"""Batched decode of 16 (or 32) independent sequences on tcgen05 (north-star
+"tensor cores for the batch>1 projections"; BASELINE config #5 batch 16).
+The batch B is the MMA N: 16 or 32 rows per weight block (``batch=``); any
+1..B sequences run on it (inactive rows: position -1).
 
 Each sequence has its own KV cache and position.  One layer is
 ``cfb_llama_b16_layer`` (csrc/tc_gemm.cu + csrc/batch_attn.cu): the QKV, O and
@@ -19,6 +21,14 @@ from . import _native
 from .exceptions import DimensionError
 from .llama import LlamaConfig, rope_table
 from .tc import BATCH, pack_umma
+
+BATCHES = (16, 32)  # MMA N of the batched tcgen05 path
+
+
+def _check_batch(batch: int) -> int:
+    if batch not in BATCHES:
+        raise DimensionError(f"the batched tcgen05 path runs batch 16 or 32 (got {batch})")
+    return batch
 
 
 def pack_layer_b16(lp: dict, dev):
@@ -47,24 +57,25 @@ PAGE = 128  # CFB_KV_PAGE: positions per KV page (= one attention chunk)
 
 
 class PagedKVPool:
-    """Paged KV caches for the 16 sequences: per layer a K and a V page pool
-    [n_pages][n_heads][128][128] fp16 and one shared block table [16][max_pages]
+    """Paged KV caches for the n_seq (16 or 32) sequences: per layer a K and a V page pool
+    [n_pages][n_heads][128][128] fp16 and one shared block table [n_seq][max_pages]
     (page ids, the same for every layer).  Pages are handed out from a free
     list as sequences grow (``reserve``) and returned by ``release``; the
     device table is refreshed on every change (host-side, between steps)."""
 
-    def __init__(self, cfg: LlamaConfig, n_pages: int, max_pages: int, dev):
+    def __init__(self, cfg: LlamaConfig, n_pages: int, max_pages: int, dev, n_seq: int = BATCH):
         import torch
         self.cfg, self.n_pages, self.max_pages, self.dev = cfg, n_pages, max_pages, dev
+        self.n_seq = n_seq
         shape = (n_pages, cfg.n_heads, PAGE, 128)
         self.k = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
         self.v = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
         self.free = list(range(n_pages))[::-1]
-        self.pages = [[] for _ in range(BATCH)]
+        self.pages = [[] for _ in range(n_seq)]
         # unassigned entries are -1 (never a real page: the kernels drop writes to
         # them instead of aliasing page 0)
-        self.host_table = np.full((BATCH, max_pages), -1, np.int32)
-        self.table = torch.full((BATCH, max_pages), -1, device=dev, dtype=torch.int32)
+        self.host_table = np.full((n_seq, max_pages), -1, np.int32)
+        self.table = torch.full((n_seq, max_pages), -1, device=dev, dtype=torch.int32)
 
     def reserve(self, seq: int, length: int) -> None:
         """Make positions 0 .. length-1 of ``seq`` addressable."""
@@ -144,8 +155,9 @@ class BatchedLlama:
     than 16 entries pads with inactive rows)."""
 
     def __init__(self, cfg: LlamaConfig, cache_cap: int, layers: list, max_len: int | None = None,
-                 pool: PagedKVPool | None = None):
+                 pool: PagedKVPool | None = None, batch: int = BATCH):
         import torch
+        self.B = B = _check_batch(batch)
         if cfg.head_dim != 128 or cfg.n_heads * 128 > cfg.hidden or cfg.inter % 64:
             raise DimensionError("the batch-16 path needs head_dim 128, n_heads * 128 <= hidden "
                                  "(== unless tensor-parallel) and inter % 64 == 0")
@@ -156,21 +168,21 @@ class BatchedLlama:
         self.max_len = max_len or cache_cap
         D, nh, F = cfg.hidden, cfg.n_heads, cfg.inter
         self.rope = torch.from_numpy(rope_table(cache_cap, 128, cfg.rope_theta)).to(dev)
-        self.pos = torch.zeros(BATCH, device=dev, dtype=torch.int32)
+        self.pos = torch.zeros(B, device=dev, dtype=torch.int32)
         # host mirror of the device positions: every step / replay advances it,
         # and a step is refused before it would write past a sequence's cache
-        self.host_pos = np.zeros(BATCH, np.int64)
-        self.resid = torch.zeros(BATCH, D, device=dev, dtype=torch.float32)
+        self.host_pos = np.zeros(B, np.int64)
+        self.resid = torch.zeros(B, D, device=dev, dtype=torch.float32)
         nchunks = (self.max_len + 127) // 128
         self.ws = dict(
-            xp=torch.zeros(BATCH * max(D, F), device=dev, dtype=torch.float16),
-            q16=torch.zeros(BATCH * nh * 128, device=dev, dtype=torch.float16),
-            qkv_acc=torch.zeros(BATCH * 3 * nh * 128, device=dev, dtype=torch.int64),
-            part=torch.zeros(BATCH * nh * nchunks * 130, device=dev, dtype=torch.float32),
-            o_acc=torch.zeros(BATCH * D, device=dev, dtype=torch.int64),
-            gu_acc=torch.zeros(BATCH * 2 * F, device=dev, dtype=torch.int64),
-            ap=torch.zeros(BATCH * F, device=dev, dtype=torch.float16),
-            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + BATCH * nh, device=dev, dtype=torch.int32))
+            xp=torch.zeros(B * max(D, F), device=dev, dtype=torch.float16),
+            q16=torch.zeros(B * nh * 128, device=dev, dtype=torch.float16),
+            qkv_acc=torch.zeros(B * 3 * nh * 128, device=dev, dtype=torch.int64),
+            part=torch.zeros(B * nh * nchunks * 130, device=dev, dtype=torch.float32),
+            o_acc=torch.zeros(B * D, device=dev, dtype=torch.int64),
+            gu_acc=torch.zeros(B * 2 * F, device=dev, dtype=torch.int64),
+            ap=torch.zeros(B * F, device=dev, dtype=torch.float16),
+            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + B * nh, device=dev, dtype=torch.int32))
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
         self.pool = pool
@@ -179,14 +191,14 @@ class BatchedLlama:
     # ---------------------------------------------------------------- builders
     @classmethod
     def paged(cls, cfg: LlamaConfig, layers_params: list, caches: list, max_len: int,
-              n_pages: int | None = None, shuffle_seed: int | None = None) -> "BatchedLlama":
+              n_pages: int | None = None, shuffle_seed: int | None = None, batch: int = BATCH) -> "BatchedLlama":
         """Like ``from_params`` but the KV caches live in a ``PagedKVPool``
         (prefill written through ``cfb_b16_kv_write``); positions up to
         ``max_len`` are addressable.  ``n_pages`` defaults to what 16 sequences
         of ``max_len`` need."""
         dev = _native.require_cuda()
         maxp = (max_len + PAGE - 1) // PAGE
-        pool = PagedKVPool(cfg, n_pages or BATCH * maxp, maxp, dev)
+        pool = PagedKVPool(cfg, n_pages or batch * maxp, maxp, dev, n_seq=batch)
         if shuffle_seed is not None:  # non-monotonic page ids (tests)
             pool.free = [int(x) for x in np.random.default_rng(shuffle_seed).permutation(pool.n_pages)]
         layers = [pack_layer_b16(lp_, dev) for lp_ in layers_params]
@@ -194,17 +206,18 @@ class BatchedLlama:
             L["k_cache"], L["v_cache"] = pool.k[li], pool.v[li]
             for n, (k, v) in enumerate(cl):
                 pool.write(li, n, 0, k, v)
-        return cls(cfg, max_len, layers, max_len, pool=pool)
+        return cls(cfg, max_len, layers, max_len, pool=pool, batch=batch)
 
     @classmethod
-    def random_paged(cls, cfg: LlamaConfig, max_len: int, seed: int = 0, shuffle: bool = True) -> "BatchedLlama":
+    def random_paged(cls, cfg: LlamaConfig, max_len: int, seed: int = 0, shuffle: bool = True,
+                     batch: int = BATCH) -> "BatchedLlama":
         """Device-drawn weights over a paged pool whose pages are fully drawn;
         every sequence gets max_len positions of pages (shuffled page ids)."""
         import torch
-        m = cls.random(cfg, cache_cap=1, seed=seed)
+        m = cls.random(cfg, cache_cap=1, seed=seed, batch=batch)
         dev = m.dev
         maxp = (max_len + PAGE - 1) // PAGE
-        pool = PagedKVPool(cfg, BATCH * maxp, maxp, dev)
+        pool = PagedKVPool(cfg, batch * maxp, maxp, dev, n_seq=batch)
         if shuffle:
             rng = np.random.default_rng(seed)
             pool.free = [int(x) for x in rng.permutation(pool.n_pages)]
@@ -214,20 +227,20 @@ class BatchedLlama:
             pool.k[li].normal_(generator=g)
             pool.v[li].normal_(generator=g)
             L["k_cache"], L["v_cache"] = pool.k[li], pool.v[li]
-        for n in range(BATCH):
+        for n in range(batch):
             pool.reserve(n, max_len)
-        return cls(cfg, max_len, m.layers, max_len, pool=pool)
+        return cls(cfg, max_len, m.layers, max_len, pool=pool, batch=batch)
     @classmethod
     def from_params(cls, cfg: LlamaConfig, layers_params: list, caches: list, cache_cap: int,
-                    max_len: int | None = None) -> "BatchedLlama":
-        """layers_params: logical per-layer weights; caches[l] = list of 16
+                    max_len: int | None = None, batch: int = BATCH) -> "BatchedLlama":
+        """layers_params: logical per-layer weights; caches[l] = list of <= batch
         (k (nh, S_n, H), v) numpy prefixes, one per sequence."""
         import torch
         dev = _native.require_cuda()
         layers = []
         for lp_, cl in zip(layers_params, caches):
             L = pack_layer_b16(lp_, dev)
-            kc = torch.zeros(BATCH, cfg.n_heads, cache_cap, 128, device=dev, dtype=torch.float16)
+            kc = torch.zeros(batch, cfg.n_heads, cache_cap, 128, device=dev, dtype=torch.float16)
             vc = torch.zeros_like(kc)
             for n, (k, v) in enumerate(cl):
                 S = k.shape[1]
@@ -236,10 +249,10 @@ class BatchedLlama:
                     vc[n, :, :S] = torch.from_numpy(np.ascontiguousarray(v, np.float32)).to(dev).half()
             L["k_cache"], L["v_cache"] = kc, vc
             layers.append(L)
-        return cls(cfg, cache_cap, layers, max_len)
+        return cls(cfg, cache_cap, layers, max_len, batch=batch)
 
     @classmethod
-    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0) -> "BatchedLlama":
+    def random(cls, cfg: LlamaConfig, cache_cap: int, seed: int = 0, batch: int = BATCH) -> "BatchedLlama":
         """Device-drawn packed weights and full KV caches (benchmarks)."""
         import torch
         dev = _native.require_cuda()
@@ -260,9 +273,9 @@ class BatchedLlama:
                 w_o=rnd((D // 128, 2 * nh, 4, 2, 16, 8, 8), (nh * 128) ** -0.5),
                 w_gu=rnd((2 * F // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5),
                 w_dn=rnd((D // 128, F // 64, 4, 2, 16, 8, 8), F ** -0.5),
-                k_cache=rnd((BATCH, nh, cache_cap, 128), 1.0),
-                v_cache=rnd((BATCH, nh, cache_cap, 128), 1.0)))
-        return cls(cfg, cache_cap, layers)
+                k_cache=rnd((batch, nh, cache_cap, 128), 1.0),
+                v_cache=rnd((batch, nh, cache_cap, 128), 1.0)))
+        return cls(cfg, cache_cap, layers, batch=batch)
 
     # ---------------------------------------------------------------- running
     def layer_args(self, L: dict, stage: int = 0, partial: bool = False):
@@ -279,7 +292,7 @@ class BatchedLlama:
             part=w["part"].data_ptr(), o_acc=w["o_acc"].data_ptr(), gu_acc=w["gu_acc"].data_ptr(),
             ap=w["ap"].data_ptr(), ticket=w["ticket"].data_ptr(),
             block_table=self.pool.table.data_ptr() if self.pool else None,
-            max_pages=self.pool.max_pages if self.pool else 0)
+            max_pages=self.pool.max_pages if self.pool else 0, batch=self.B)
 
     def _enqueue(self, advance: bool = True) -> None:
         L_ = _native.lib()
@@ -287,7 +300,7 @@ class BatchedLlama:
         for L in self.layers:
             _native.check(L_.cfb_llama_b16_layer(self.layer_args(L), sp))
         if advance:
-            _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
+            _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), self.B, sp))
 
     @property
     def active(self) -> np.ndarray:
@@ -314,10 +327,10 @@ class BatchedLlama:
     def set_positions(self, pos) -> None:
         import torch
         pos = np.asarray(pos, np.int64).reshape(-1)
-        if not 1 <= pos.shape[0] <= BATCH or (pos < -1).any() or not (pos >= 0).any():
-            raise DimensionError(f"set_positions needs 1..{BATCH} positions (>= 0, or -1 = inactive), "
+        if not 1 <= pos.shape[0] <= self.B or (pos < -1).any() or not (pos >= 0).any():
+            raise DimensionError(f"set_positions needs 1..{self.B} positions (>= 0, or -1 = inactive), "
                                  "at least one active")
-        pos = np.concatenate([pos, np.full(BATCH - pos.shape[0], -1, np.int64)])
+        pos = np.concatenate([pos, np.full(self.B - pos.shape[0], -1, np.int64)])
         if self.pool:  # the new token's page must exist
             for n, p in enumerate(pos):
                 if p >= 0:
@@ -335,7 +348,7 @@ class BatchedLlama:
                 self.pool.reserve(n, int(self.host_pos[n]) + steps)
 
     def step(self, advance: bool = True) -> None:
-        """resid <- the layer stack applied to resid for all 16 sequences."""
+        """resid <- the layer stack applied to resid for all active sequences."""
         self._check_room(1)
         self._enqueue(advance)
         if advance:
@@ -370,10 +383,10 @@ class BatchedLlama:
         lm = t(lm_head)
         self.V = lm.shape[0]
         self.lm = pack_umma(lm)
-        self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
-        self.logits = torch.zeros(BATCH, self.V, device=dev, dtype=torch.float32)
-        self.lm_acc = torch.zeros(BATCH * self.V, device=dev, dtype=torch.int64)
-        self.arg_scratch = torch.zeros(33 * 32, device=dev, dtype=torch.int64)
+        self.tokens = torch.zeros(self.B, device=dev, dtype=torch.int32)
+        self.logits = torch.zeros(self.B, self.V, device=dev, dtype=torch.float32)
+        self.lm_acc = torch.zeros(self.B * self.V, device=dev, dtype=torch.int64)
+        self.arg_scratch = torch.zeros(65 * 32, device=dev, dtype=torch.int64)
         torch.cuda.synchronize()
 
     def random_head(self, vocab: int, seed: int = 1) -> None:
@@ -391,10 +404,10 @@ class BatchedLlama:
         self.embed, self.final_norm = rnd((vocab, D), 1.0), rnd((D,), 0.1, 1.0)
         self.V = vocab
         self.lm = rnd((vocab // 128, D // 64, 4, 2, 16, 8, 8), D ** -0.5)
-        self.tokens = torch.zeros(BATCH, device=dev, dtype=torch.int32)
-        self.logits = torch.zeros(BATCH, vocab, device=dev, dtype=torch.float32)
-        self.lm_acc = torch.zeros(BATCH * vocab, device=dev, dtype=torch.int64)
-        self.arg_scratch = torch.zeros(33 * 32, device=dev, dtype=torch.int64)
+        self.tokens = torch.zeros(self.B, device=dev, dtype=torch.int32)
+        self.logits = torch.zeros(self.B, vocab, device=dev, dtype=torch.float32)
+        self.lm_acc = torch.zeros(self.B * vocab, device=dev, dtype=torch.int64)
+        self.arg_scratch = torch.zeros(65 * 32, device=dev, dtype=torch.int64)
         torch.cuda.synchronize()
 
     def _enqueue_decode(self, logits: bool) -> None:
@@ -402,14 +415,14 @@ class BatchedLlama:
         sp = self.stream.cuda_stream
         cfg = self.cfg
         _native.check(L_.cfb_embed(2, self.embed.data_ptr(), self.tokens.data_ptr(), self.resid.data_ptr(),
-                                   BATCH, cfg.hidden, sp))
+                                   self.B, cfg.hidden, sp))
         for L in self.layers:
             _native.check(L_.cfb_llama_b16_layer(self.layer_args(L), sp))
         _native.check(L_.cfb_b16_lm_head(
             self.resid.data_ptr(), self.final_norm.data_ptr(), self.lm.data_ptr(), self.V, cfg.hidden,
             cfg.eps, self.ws["xp"].data_ptr(), self.lm_acc.data_ptr(), self.tokens.data_ptr(),
-            self.logits.data_ptr() if logits else None, self.arg_scratch.data_ptr(), sp))
-        _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), sp))
+            self.logits.data_ptr() if logits else None, self.arg_scratch.data_ptr(), self.B, sp))
+        _native.check(L_.cfb_b16_advance(self.pos.data_ptr(), self.B, sp))
 
     def decode_step(self, logits: bool = False) -> None:
         """One greedy step for all 16 sequences: tokens -> embed -> layers ->
@@ -433,7 +446,7 @@ class BatchedLlama:
         cfg = self.cfg
         D, F = cfg.hidden, cfg.inter
         w = cfg.n_layers * (2 * (4 * D * D + 3 * D * F) + 4 * D)
-        nb = len(self.active) or BATCH
+        nb = len(self.active) or self.B
         kv = cfg.n_layers * nb * 2 * D * 2 * (ctx + 2)
         h = 2 * self.V * D + 2 * D + nb * 2 * D if head else 0
         return w + kv + h

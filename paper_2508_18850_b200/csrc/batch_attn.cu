@@ -168,17 +168,19 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
     at = fmaf(__ldcg(pp + (size_t)cc * 130 + 2 + tid), w, at);
   }
   // packed UMMA activation layout (csrc/tc_gemm.cu): K index = h*128 + tid, row n
-  const int k = h * 128 + tid, kb = k / 64, kk = k % 64, s = kk / 16, c2 = (kk % 16) / 8;
-  xp[(size_t)kb * 1024 + ((s * 2 + c2) * 2 + n / 8) * 64 + (n % 8) * 8 + (kk % 8)] = __float2half_rn(__fdiv_rn(at, lt));
+  // packed UMMA activation layout of nb rows (csrc/tc_gemm.cu xpack_off): K index h*128 + tid, row n
+  const int nb = gridDim.y / nh, k = h * 128 + tid, kb = k / 64, kk = k % 64, s = kk / 16, c2 = (kk % 16) / 8;
+  xp[(size_t)kb * (nb * 64) + ((s * 2 + c2) * (nb / 8) + n / 8) * 64 + (n % 8) * 8 + (kk % 8)] =
+      __float2half_rn(__fdiv_rn(at, lt));
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
                     int max_len, float* part, int* ticket, __half* xp, const int* table, int maxp,
-                    cudaStream_t st, bool pdl) {
+                    cudaStream_t st, bool pdl, int nb) {
   if (const int rc = configure_kernel((const void*)batch_attn_kernel, kBaSmem, false)) return rc;
   const int nchunks = (max_len + kBaChunk - 1) / kBaChunk;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nchunks, 16 * nh, 1);
+  cfg.gridDim = dim3(nchunks, nb * nh, 1);
   cfg.blockDim = dim3(kBaThreads, 1, 1);
   cfg.dynamicSmemBytes = kBaSmem;
   cfg.stream = st;
@@ -205,7 +207,7 @@ __global__ void kv_write_kernel(__half* kc, __half* vc, const int* table, int ma
 
 int kv_write(__half* kc, __half* vc, const int* table, int maxp, int cap, int nh, int seq, int start, int count,
              const __half* ks, const __half* vs, cudaStream_t st) {
-  if (!kc || !vc || (count > 0 && (!ks || !vs)) || seq < 0 || seq >= 16 || start < 0 || count < 0 || nh <= 0)
+  if (!kc || !vc || (count > 0 && (!ks || !vs)) || seq < 0 || seq >= 32 || start < 0 || count < 0 || nh <= 0)
     return set_error(CFB_ERR_ARGUMENT, "kv_write: bad arguments");
   if (!table && start + count > cap) return set_error(CFB_ERR_DIMENSION, "kv_write: rows beyond cache_cap");
   if (table && start + count > maxp * kBaChunk) return set_error(CFB_ERR_DIMENSION, "kv_write: rows beyond the block table");

@@ -41,11 +41,19 @@
 
 namespace cfb {
 
-constexpr int kTcN = 16;            // batch rows = MMA N
+constexpr int kTcN = 16;            // default batch rows = MMA N (16 or 32 per launch: nb)
+constexpr int kTcNMax = 32;
 constexpr int kTcM = 128;           // weight rows per tile = MMA M
 constexpr int kTcKB = 64;           // K elements per block
 constexpr int kTcABytes = kTcM * kTcKB * 2;   // 16 KB
-constexpr int kTcBBytes = kTcN * kTcKB * 2;   // 2 KB
+constexpr int kTcBBytesMax = kTcNMax * kTcKB * 2;  // 4 KB (nb = 32); nb * 128 B per block
+
+// packed UMMA activation block layout for nb rows: element (row n, k) of
+// K-block kb at [kb][s = k-step (4)][c = K half (2)][g = n / 8 (nb / 8)][n % 8][8]
+__host__ __device__ __forceinline__ size_t xpack_off(int n, int k, int nb) {
+  const int kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
+  return (size_t)kb * (nb * kTcKB) + (size_t)((s * 2 + c) * (nb / 8) + n / 8) * 64 + (n % 8) * 8 + (kk % 8);
+}
 constexpr int kTcStages = 8;
 constexpr int kTcThreads = 6 * 32;
 
@@ -62,7 +70,7 @@ struct TcQkv {
   __half* k_cache;        // [16][nh][cap][128]
   __half* v_cache;
   const float* rope_cs;   // [cap][64][2]
-  const int* pos;         // [16] position of the new token per sequence
+  const int* pos;         // [nb] position of the new token per sequence (-1: inactive)
   int nh, cap;
   const int* table;       // paged caches: [16][maxp] page ids (else null)
   int maxp;
@@ -70,9 +78,9 @@ struct TcQkv {
 
 struct TcParams {
   const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
-  const __half* x;   // packed activation blocks [K/64][2 KB]
+  const __half* x;   // packed activation blocks [K/64][nb * 128 B]
   unsigned long long* y;  // [16][M] fixed point (2^-32), accumulated
-  int M, K, mode;
+  int M, K, mode, nb;  // nb: batch rows = MMA N (16 or 32)
   int* ticket;       // [M/128] zero (re-zeroed by the finishing CTA)
   __half* act;       // kTcSwiGLU: packed activations for the next projection
   float* out;        // kTcResidOut: out[n][m] = resid[n][m] + y (out may alias resid)
@@ -108,8 +116,9 @@ __device__ __forceinline__ void tc_fence_before() {
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p) {
   extern __shared__ __align__(1024) char smem[];
   char* sa = smem;                                   // [S][16 KB]
-  char* sb = smem + kTcStages * kTcABytes;           // [S][2 KB]
-  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kTcStages * kTcBBytes);
+  char* sb = smem + kTcStages * kTcABytes;           // [S][nb * 128 B] (room for nb = 32)
+  uint64_t* full = reinterpret_cast<uint64_t*>(sb + kTcStages * kTcBBytesMax);
+  const int nb = p.nb, xbytes = nb * kTcKB * 2;
   uint64_t* empty = full + kTcStages;
   uint64_t* accf = empty + kTcStages;  // [2] accumulator ready
   uint64_t* acce = accf + 2;           // [2] accumulator drained
@@ -134,8 +143,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
     mbar_init(&acce[1], 4);
     fence_mbar_init();
   }
-  if (warp == 1) {  // TMEM: 2 accumulators x 16 columns
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(
+  if (warp == 1) {  // TMEM: 2 accumulators x nb columns (64 allocated: nb <= 32)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
                      smem_u32(tmem_slot))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -162,26 +171,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       // activation blocks wait for it
       const int nb = b1 - b0, pre = min(nb, kTcStages);
       for (int it = 0; it < pre; ++it) {
-        mbar_arrive_expect_tx(&full[it], kTcABytes + kTcBBytes);
+        mbar_arrive_expect_tx(&full[it], kTcABytes + xbytes);
         bulk_g2s(sa + it * kTcABytes, p.w + (size_t)(b0 + it) * (kTcABytes / 2), kTcABytes, &full[it], pol);
       }
       pdl_wait();
       for (int it = 0; it < pre; ++it)
-        bulk_g2s(sb + it * kTcBBytes, p.x + (size_t)((b0 + it) % KBt) * (kTcBBytes / 2), kTcBBytes, &full[it],
+        bulk_g2s(sb + it * kTcBBytesMax, p.x + (size_t)((b0 + it) % KBt) * (xbytes / 2), xbytes, &full[it],
                  policy_evict_last());
       for (int it = pre; it < nb; ++it) {
         const int s = it % kTcStages, b = b0 + it;
         mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], kTcABytes + kTcBBytes);
+        mbar_arrive_expect_tx(&full[s], kTcABytes + xbytes);
         bulk_g2s(sa + s * kTcABytes, p.w + (size_t)b * (kTcABytes / 2), kTcABytes, &full[s], pol);
-        bulk_g2s(sb + s * kTcBBytes, p.x + (size_t)(b % KBt) * (kTcBBytes / 2), kTcBBytes, &full[s],
+        bulk_g2s(sb + s * kTcBBytesMax, p.x + (size_t)(b % KBt) * (xbytes / 2), xbytes, &full[s],
                  policy_evict_last());
       }
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
     if (lane == 0) {
-      // kind::f16, D f32, A/B f16 K-major, N = 16, M = 128
-      const uint32_t idesc = (1u << 4) | ((uint32_t)(kTcN >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
+      // kind::f16, D f32, A/B f16 K-major, N = nb, M = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(nb >> 3) << 17) | ((uint32_t)(kTcM >> 4) << 24);
       int it = 0, n = 0;
       for (int u = 0; u < nseg; ++u, ++n) {
         int t, kb0, nkb;
@@ -189,16 +198,16 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
         const int a = n & 1;
         if (n >= 2) mbar_wait(&acce[a], ((n >> 1) - 1) & 1);
         tc_fence_after();
-        const uint32_t dt = tmem + (uint32_t)(a * kTcN);
+        const uint32_t dt = tmem + (uint32_t)(a * nb);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = it % kTcStages;
           mbar_wait(&full[s], (it / kTcStages) & 1);
           tc_fence_after();
-          const uint32_t abase = smem_u32(sa + s * kTcABytes), bbase = smem_u32(sb + s * kTcBBytes);
+          const uint32_t abase = smem_u32(sa + s * kTcABytes), bbase = smem_u32(sb + s * kTcBBytesMax);
 #pragma unroll
-          for (int ks = 0; ks < 4; ++ks)
-            tc_mma(dt, umma_desc(abase + ks * 4096, 2048, 128), umma_desc(bbase + ks * 512, 256, 128),
-                   idesc, (kb | ks) ? 1u : 0u);
+          for (int ks = 0; ks < 4; ++ks)  // X: k-step stride nb*32 B, K halves nb*16 B apart
+            tc_mma(dt, umma_desc(abase + ks * 4096, 2048, 128),
+                   umma_desc(bbase + ks * (nb * 32), (uint32_t)(nb * 16), 128), idesc, (kb | ks) ? 1u : 0u);
           tc_commit(&empty[s]);  // stage free once these MMAs have read it
         }
         tc_commit(&accf[a]);      // accumulator complete
@@ -213,20 +222,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       const int a = n & 1;
       mbar_wait(&accf[a], (n >> 1) & 1);
       tc_fence_after();
-      uint32_t r[16];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-            "=r"(r[14]), "=r"(r[15])
-          : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * kTcN)));
+      const int m = t * kTcM + 32 * q + lane;
+      uint32_t r[kTcNMax];  // this lane's row m, batch rows 0..nb-1 (16 columns per tcgen05.ld)
+#pragma unroll
+      for (int h16 = 0; h16 < kTcNMax / 16; ++h16)
+        if (16 * h16 < nb)
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(r[16 * h16 + 0]), "=r"(r[16 * h16 + 1]), "=r"(r[16 * h16 + 2]), "=r"(r[16 * h16 + 3]),
+                "=r"(r[16 * h16 + 4]), "=r"(r[16 * h16 + 5]), "=r"(r[16 * h16 + 6]), "=r"(r[16 * h16 + 7]),
+                "=r"(r[16 * h16 + 8]), "=r"(r[16 * h16 + 9]), "=r"(r[16 * h16 + 10]), "=r"(r[16 * h16 + 11]),
+                "=r"(r[16 * h16 + 12]), "=r"(r[16 * h16 + 13]), "=r"(r[16 * h16 + 14]), "=r"(r[16 * h16 + 15])
+              : "r"(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(a * nb + 16 * h16)));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&acce[a]);
-      const int m = t * kTcM + 32 * q + lane;
+      if (lane == 0) mbar_arrive(&acce[a]);  // accumulator drained: the MMA warp may reuse it
 #pragma unroll
-      for (int c = 0; c < kTcN; ++c) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
+      for (int c = 0; c < kTcNMax; ++c)
+        if (c < nb) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
       if (p.mode == kTcAccum) continue;
       // ticket: the last contributor to tile t finishes it
       __threadfence();
@@ -242,10 +256,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       named_bar_sync(2, 128);
       if (!*flag) continue;
       __threadfence();
-      const int et = tid - 64;  // 0..127
+      const int et = tid - 64;  // 0..127: 16 batch rows per pass
+      for (int hb = 0; hb < nb; hb += 16) {
       if (p.mode == kTcQKV) {
         // thread = (sequence nn, 8 rotation pairs (i, i + 64), i in [i0, i0 + 8))
-        const int nn = et >> 3, i0 = (et & 7) * 8;
+        const int nn = hb + (et >> 3), i0 = (et & 7) * 8;
         unsigned long long* yr = p.y + (size_t)nn * p.M + t * kTcM;
         ulonglong2 lo[4], hi[4];
 #pragma unroll
@@ -298,7 +313,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
         // tile rows: 64 gate rows (f = 64t + j) then the 64 matching up rows;
         // f-range of tile t = K-block t of the next projection.  All loads of a
         // thread are issued before any store (no serialised L2 round trips).
-        const int nn = et >> 3, j0 = (et & 7) * 8;  // 16 rows x 8 chunks = 128 threads
+        const int nn = hb + (et >> 3), j0 = (et & 7) * 8;  // 16 rows x 8 chunks = 128 threads
         unsigned long long* yg = p.y + (size_t)nn * p.M + t * kTcM + j0;
         ulonglong2 gv[4], uv[4];
 #pragma unroll
@@ -318,12 +333,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
           reinterpret_cast<ulonglong2*>(yg)[e] = make_ulonglong2(0ull, 0ull);
           reinterpret_cast<ulonglong2*>(yg + 64)[e] = make_ulonglong2(0ull, 0ull);
         }
-        const int s2 = j0 / 16, c = (j0 % 16) / 8;
-        *reinterpret_cast<uint4*>(p.act + (size_t)t * (kTcBBytes / 2) + ((s2 * 2 + c) * 2 + nn / 8) * 64 +
-                                  (nn % 8) * 8) = *reinterpret_cast<const uint4*>(h);
+        *reinterpret_cast<uint4*>(p.act + xpack_off(nn, t * kTcKB + j0, nb)) = *reinterpret_cast<const uint4*>(h);
       } else {
         // 16 rows x 128 columns: thread = (row, 16-column run)
-        const int nn = et >> 3, c0 = (et & 7) * 16;
+        const int nn = hb + (et >> 3), c0 = (et & 7) * 16;
         const size_t o = (size_t)nn * p.M + t * kTcM + c0;
         ulonglong2 yv[8];
         float4 rv[4];
@@ -343,26 +356,25 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
                           __fadd_rn(r4.w, fixed_to_float(yv[2 * e + 1].y)));
         }
       }
+      }  // row passes
     }
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
   }
 }
 
-// x [16][K] fp16 row-major -> packed UMMA blocks (see header).
-__global__ void tc_pack_x_kernel(const __half* x, __half* xp, int K) {
+// x [nb][K] fp16 row-major -> packed UMMA blocks (see header).
+__global__ void tc_pack_x_kernel(const __half* x, __half* xp, int K, int nb) {
   pdl_wait();
   pdl_launch_dependents();
-  const int nvec = kTcN * K / 8;  // 16-byte vectors
+  const int nvec = nb * K / 8;  // 16-byte vectors
   for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
-    const int n = v / (K / 8), kv = v % (K / 8);  // row n, elements 8kv..8kv+7
-    const int k = kv * 8, kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
-    const size_t dst = (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8;
-    *reinterpret_cast<uint4*>(xp + dst) = *reinterpret_cast<const uint4*>(x + (size_t)n * K + k);
+    const int n = v / (K / 8), k = (v % (K / 8)) * 8;  // row n, elements k..k+7
+    *reinterpret_cast<uint4*>(xp + xpack_off(n, k, nb)) = *reinterpret_cast<const uint4*>(x + (size_t)n * K + k);
   }
 }
 
@@ -377,11 +389,12 @@ __global__ void tc_finish_kernel(unsigned long long* yacc, float* out, const flo
   }
 }
 
-int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytes) + (4 * kTcStages + 8) * 8 + 32; }
+int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytesMax) + (4 * kTcStages + 8) * 8 + 32; }
 
 int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
             cudaStream_t st, bool pdl, int mode = kTcAccum, int* ticket = nullptr, __half* act = nullptr,
-            float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr) {
+            float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr, int nb = kTcN) {
+  if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "tcgen05 batch must be 16 or 32");
   if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
   if (const int rc = configure_kernel((const void*)tc_gemm_kernel, tc_smem_bytes(), false)) return rc;
@@ -397,6 +410,7 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   p.M = M;
   p.K = K;
   p.mode = mode;
+  p.nb = nb;
   p.ticket = ticket;
   p.act = act;
   p.out = out;
@@ -417,16 +431,16 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   return CFB_OK;
 }
 
-int tc_pack_x(const __half* x, __half* xp, int K, cudaStream_t st, bool pdl) {
+int tc_pack_x(const __half* x, __half* xp, int K, cudaStream_t st, bool pdl, int nb = kTcN) {
   if (K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_pack_x: K %% 64 must be 0");
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((kTcN * K / 8 + 255) / 256, 1, 1);
+  cfg.gridDim = dim3((nb * K / 8 + 255) / 256, 1, 1);
   cfg.blockDim = dim3(256, 1, 1);
   cfg.stream = st;
   LaunchAttrs at(0, pdl);
   cfg.attrs = at.a;
   cfg.numAttrs = at.n;
-  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_pack_x_kernel, x, xp, K));
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_pack_x_kernel, x, xp, K, nb));
   return CFB_OK;
 }
 
@@ -445,7 +459,7 @@ int tc_finish(unsigned long long* yacc, float* out, const float* resid, int n, c
 // ---------------------------------------------------------------- batch-16 FFN
 // x = f16(rmsnorm(resid[n]) * g) written straight into the packed UMMA layout
 // (one CTA per batch row).
-__global__ void tc_rmsnorm_pack_kernel(const float* resid, const __half* g, __half* xp, int D, float eps) {
+__global__ void tc_rmsnorm_pack_kernel(const float* resid, const __half* g, __half* xp, int D, float eps, int nb) {
   pdl_wait();
   pdl_launch_dependents();
   // one CTA per batch row; thread = 16 consecutive elements, loaded once
@@ -481,38 +495,13 @@ __global__ void tc_rmsnorm_pack_kernel(const float* resid, const __half* g, __ha
 #pragma unroll
     for (int e = 0; e < 8; ++e)
       h[e] = __float2half_rn(__fmul_rn(__fmul_rn(rf[half8 * 8 + e], inv), __half2float(gh[half8 * 8 + e])));
-    const int k = k0 + half8 * 8, kb = k / kTcKB, kk = k % kTcKB, s = kk / 16, c = (kk % 16) / 8;
-    *reinterpret_cast<uint4*>(xp + (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8) =
-        *reinterpret_cast<const uint4*>(h);
+    *reinterpret_cast<uint4*>(xp + xpack_off(n, k0 + half8 * 8, nb)) = *reinterpret_cast<const uint4*>(h);
   }
 }
 
-// act = f16(silu(gate) * up) from the fixed-point gate/up sums (rows f and F+f
-// of the [w1; w2] projection), packed for the down projection; re-zeroes gu.
-__global__ void tc_swiglu_pack_kernel(unsigned long long* gu, __half* ap, int F) {
+__global__ void tc_advance_kernel(int* pos, int nb) {  // every active sequence moves to its next position
   pdl_wait();
-  pdl_launch_dependents();
-  const int nvec = kTcN * F / 8;
-  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < nvec; v += gridDim.x * blockDim.x) {
-    const int n = v / (F / 8), f0 = (v % (F / 8)) * 8;
-    __align__(16) __half h[8];
-    unsigned long long* gr = gu + (size_t)n * 2 * F;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float gt = fixed_to_float(gr[f0 + e]), up = fixed_to_float(gr[F + f0 + e]);
-      gr[f0 + e] = 0ull;
-      gr[F + f0 + e] = 0ull;
-      h[e] = __float2half_rn(__fmul_rn(__fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt))), up));
-    }
-    const int kb = f0 / kTcKB, kk = f0 % kTcKB, s = kk / 16, c = (kk % 16) / 8;
-    *reinterpret_cast<uint4*>(ap + (size_t)kb * (kTcBBytes / 2) + ((s * 2 + c) * 2 + n / 8) * 64 + (n % 8) * 8) =
-        *reinterpret_cast<const uint4*>(h);
-  }
-}
-
-__global__ void tc_advance_kernel(int* pos) {  // every active sequence moves to its next position
-  pdl_wait();
-  if (threadIdx.x < kTcN && pos[threadIdx.x] >= 0) pos[threadIdx.x] += 1;
+  if ((int)threadIdx.x < nb && pos[threadIdx.x] >= 0) pos[threadIdx.x] += 1;
 }
 
 template <class K, class... Args>
@@ -536,24 +525,27 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
   if (D % 128 || F % 64 || (2 * F) % 128)
     return set_error(CFB_ERR_DIMENSION, "ffn_b16: hidden %% 128 and inter %% 64 must be 0");
   if (!a->ticket) return set_error(CFB_ERR_ARGUMENT, "ffn_b16: null ticket workspace");
+  const int nb = a->batch ? a->batch : kTcN;
+  if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "ffn_b16: batch must be 16 or 32");
   const bool pdl = a->flags & CFB_PDL;
   int rc;
-  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, a->resid,
-                          static_cast<const __half*>(a->norm_w), static_cast<__half*>(a->xp), D, a->eps)))
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, nb, (D / 16 + 31) / 32 * 32, st, pdl, a->resid,
+                          static_cast<const __half*>(a->norm_w), static_cast<__half*>(a->xp), D, a->eps, nb)))
     return rc;
   // gate/up tiles interleave 64 gate + 64 up rows, finished (SwiGLU + pack) by
   // their last contributor; down tiles finished as resid + sum
   if ((rc = tc_gemm(static_cast<const __half*>(a->w_gu), static_cast<const __half*>(a->xp), a->gu_acc,
-                    2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap))))
+                    2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap), nullptr, nullptr,
+                    nullptr, nb)))
     return rc;
   return tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc, D, F,
                  0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid,
-                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid);
+                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid, nullptr, nb);
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
                     int max_len, float* part, int* ticket, __half* xp, const int* table, int maxp,
-                    cudaStream_t st, bool pdl);
+                    cudaStream_t st, bool pdl, int nb);
 
 // One Llama decoder layer for 16 independent sequences (7 PDL-chained launches):
 // RMSNorm+pack -> QKV projection (RoPE + per-sequence cache append in the
@@ -565,11 +557,13 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   if (Ka > D || D % 128 || F % 64 || a->stage < 0 || a->stage > 2)
     return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads*128 <= hidden, hidden %% 128, inter %% 64");
   const bool pdl = a->flags & CFB_PDL, partial = a->flags & CFB_PARTIAL;
+  const int nb = a->batch ? a->batch : kTcN;
+  if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "batched layer: batch must be 16 or 32");
   const int Mq = 3 * nh * 128;
   int rc;
   if (a->stage != 2) {  // attention half
-    if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, pdl, (const float*)a->resid,
-                            static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps)))
+    if ((rc = launch_simple(tc_rmsnorm_pack_kernel, nb, (D / 16 + 31) / 32 * 32, st, pdl, (const float*)a->resid,
+                            static_cast<const __half*>(a->attn_norm), static_cast<__half*>(a->xp), D, a->eps, nb)))
       return rc;
     TcQkv qkv;
     qkv.q = static_cast<__half*>(a->q16);
@@ -584,15 +578,16 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
     if (a->block_table && a->max_pages * 128 < a->max_len)
       return set_error(CFB_ERR_DIMENSION, "b16 layer: max_pages * 128 < max_len");
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
-                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv)))
+                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv, nb)))
       return rc;
     if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
                               static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
                               a->part, a->ticket + (Mq + 2 * D + 2 * F) / kTcM, static_cast<__half*>(a->xp),
-                              a->block_table, a->max_pages, st, true)))
+                              a->block_table, a->max_pages, st, true, nb)))
       return rc;
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
-                      st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid)))
+                      st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid,
+                      nullptr, nb)))
       return rc;
   }
   if (a->stage == 1) return CFB_OK;
@@ -610,6 +605,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   f.ap = a->ap;
   f.out_acc = a->o_acc;
   f.ticket = a->ticket + (Mq + D) / kTcM;
+  f.batch = nb;
   return ffn_b16(&f, st);
 }
 
@@ -659,10 +655,10 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(unsigned long long* yacc
     arg_better(best, besti, (long long)x.y, v + 1);
   }
   arg_block_reduce(best, besti, bv, bi);
-  // scratch: [16][kArgSplit] values, [16][kArgSplit] indices, [16] tickets
+  // scratch: [32][kArgSplit] values, [32][kArgSplit] indices, [32] tickets (up to 32 rows)
   unsigned long long* sv = scratch + (size_t)n * kArgSplit;
-  unsigned long long* si = scratch + 16 * kArgSplit + (size_t)n * kArgSplit;
-  unsigned long long* tk = scratch + 32 * kArgSplit + n;
+  unsigned long long* si = scratch + kTcNMax * kArgSplit + (size_t)n * kArgSplit;
+  unsigned long long* tk = scratch + 2 * kTcNMax * kArgSplit + n;
   if (tid == 0) {
     sv[c] = (unsigned long long)best;
     si[c] = (unsigned long long)besti;
@@ -685,14 +681,16 @@ __global__ void __launch_bounds__(256) tc_argmax_kernel(unsigned long long* yacc
 }
 
 int b16_lm_head(const float* resid, const __half* g, const __half* w, int V, int D, float eps, __half* xp,
-                unsigned long long* yacc, int* tokens, float* logits, unsigned long long* scratch,
+                unsigned long long* yacc, int* tokens, float* logits, unsigned long long* scratch, int nb,
                 cudaStream_t st) {
   if (V % kTcM || D % 128) return set_error(CFB_ERR_DIMENSION, "b16 LM head: vocab %% 128, hidden %% 128");
+  if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "batched LM head: batch must be 16 or 32");
   int rc;
-  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, kTcN, (D / 16 + 31) / 32 * 32, st, true, resid, g, xp, D, eps)))
+  if ((rc = launch_simple(tc_rmsnorm_pack_kernel, nb, (D / 16 + 31) / 32 * 32, st, true, resid, g, xp, D, eps, nb)))
     return rc;
-  if ((rc = tc_gemm(w, xp, yacc, V, D, 0, st, true))) return rc;
-  return launch_simple(tc_argmax_kernel, dim3(kArgSplit, kTcN), 256, st, true, yacc, V, tokens, logits, scratch);
+  if ((rc = tc_gemm(w, xp, yacc, V, D, 0, st, true, kTcAccum, nullptr, nullptr, nullptr, nullptr, nullptr, nb)))
+    return rc;
+  return launch_simple(tc_argmax_kernel, dim3(kArgSplit, nb), 256, st, true, yacc, V, tokens, logits, scratch);
 }
 
 }  // namespace cfb
@@ -701,18 +699,19 @@ extern "C" {
 
 int cfb_b16_lm_head(const float* resid, const void* norm_w, const void* w_lm, int vocab, int hidden,
                     float eps, void* xp, unsigned long long* y_acc, int* tokens, float* logits,
-                    unsigned long long* scratch, void* stream) {
+                    unsigned long long* scratch, int batch, void* stream) {
   return cfb::b16_lm_head(resid, static_cast<const __half*>(norm_w), static_cast<const __half*>(w_lm), vocab,
                           hidden, eps, static_cast<__half*>(xp), y_acc, tokens, logits, scratch,
-                          static_cast<cudaStream_t>(stream));
+                          batch ? batch : cfb::kTcN, static_cast<cudaStream_t>(stream));
 }
 
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream) {
   return cfb::llama_b16_layer(args, static_cast<cudaStream_t>(stream));
 }
 
-int cfb_b16_advance(int* pos, void* stream) {
-  return cfb::launch_simple(cfb::tc_advance_kernel, 1, 32, static_cast<cudaStream_t>(stream), true, pos);
+int cfb_b16_advance(int* pos, int batch, void* stream) {
+  return cfb::launch_simple(cfb::tc_advance_kernel, 1, 32, static_cast<cudaStream_t>(stream), true, pos,
+                            batch ? batch : cfb::kTcN);
 }
 
 

@@ -100,5 +100,5 @@ class TcFfnB16:
                                w_gu=self.w_gu.data_ptr(), w_dn=self.w_dn.data_ptr(),
                                xp=self.xp.data_ptr(), gu_acc=self.gu_acc.data_ptr(),
                                ap=self.ap.data_ptr(), out_acc=self.out_acc.data_ptr(),
-                               ticket=self.ticket.data_ptr())
+                               ticket=self.ticket.data_ptr(), batch=BATCH)
         _native.check(_native.lib().cfb_ffn_b16(a, _native.stream_ptr(stream)))

@@ -269,7 +269,7 @@ class TPBatchedLlama:
             self.allreduce()
             self.stage(l, 2)
             self.allreduce()
-        _native.check(_native.lib().cfb_b16_advance(self.m.pos.data_ptr(), self.m.stream.cuda_stream))
+        _native.check(_native.lib().cfb_b16_advance(self.m.pos.data_ptr(), self.m.B, self.m.stream.cuda_stream))
 
     def step(self) -> None:
         import torch
