@@ -537,8 +537,10 @@ enum cfb_llama_option {
   CFB_OPT_PLAIN_LAUNCH = 2, /* persistent engines: 1 = launch without the cooperative
                              attribute (the grid is sized co-resident either way; for
                              profilers that cannot replay cooperative cluster launches) */
-  CFB_OPT_RING_SLOTS = 3    /* persistent engines: 8 KB ring slots per consumer warp
+  CFB_OPT_RING_SLOTS = 3,   /* persistent engines: 8 KB ring slots per consumer warp
                              (1..3: 64 / 128 / 192 KB per CTA); 0 = the deepest that fits */
+  CFB_OPT_POOL_TILES = 4    /* persistent engines: gate/up tiles per CTA handed out
+                             dynamically at the end of the phase (work stealing); 0 = 4 */
 };
 int cfb_llama_set_option(cfb_llama* m, int option, long long value);
 /* Inter-process peer memory for the exchange blocks: cudaMalloc + zero + IPC

@@ -99,6 +99,7 @@ struct LlamaStepArgs {
   long long timeout_ns;          // cross-rank wait bound (err = 2 on expiry), 0 = none
   int l2_prefetch;               // bytes/CTA prefetched into L2 past the ring at each barrier
   int ring_spw;                  // ring slots per consumer warp (8 KB each); 0 = the deepest that fits
+  int pool_per_cta;              // work-stolen gate/up tiles per CTA; 0 = 4
 };
 // Exchange block of one tensor-parallel rank: reduced attention / FFN sums
 // [3][D] u64 each (fixed point), the cross-rank barrier counter, the argmax

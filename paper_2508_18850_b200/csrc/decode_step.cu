@@ -1205,7 +1205,8 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.barrier = a->barrier;
   p.counters = a->counters;
   p.pool_ctr = a->pool_ctr;
-  p.pool = a->pool_ctr ? (4 * G < a->inter / 8 ? 4 * G : a->inter / 8) : 0;
+  const int ppc = a->pool_per_cta > 0 ? a->pool_per_cta : 4;
+  p.pool = a->pool_ctr ? (ppc * G < a->inter / 8 ? ppc * G : a->inter / 8) : 0;
   p.logits = a->logits;
   p.cand_val = a->cand_val;
   p.cand_idx = a->cand_idx;

@@ -46,6 +46,7 @@ struct cfb_llama {
   int l2_prefetch = 0;  // CFB_OPT_L2_PREFETCH
   int plain_launch = 0; // CFB_OPT_PLAIN_LAUNCH
   int ring_spw = 0;     // CFB_OPT_RING_SLOTS
+  int pool_per_cta = 0; // CFB_OPT_POOL_TILES
   long long timeout_ns = 0;
   unsigned long long** xch_dev = nullptr;  // [tp_size] exchange blocks as this device sees them
   float* resid2 = nullptr;
@@ -226,6 +227,7 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.trace = m->trace;
   a.l2_prefetch = m->l2_prefetch;
   a.ring_spw = m->ring_spw;
+  a.pool_per_cta = m->pool_per_cta;
   a.emulated = m->plain_launch;
   if (m->tp_fused) {
     a.tp_size = m->tp_size;
@@ -510,6 +512,10 @@ int cfb_llama_set_option(cfb_llama* m, int option, long long value) {
       return CFB_OK;
     case CFB_OPT_PLAIN_LAUNCH:
       m->plain_launch = value ? 1 : 0;
+      return CFB_OK;
+    case CFB_OPT_POOL_TILES:
+      if (value < 0 || value > 64) return cfb::set_error(CFB_ERR_ARGUMENT, "pool tiles per CTA must be in [0, 64]");
+      m->pool_per_cta = (int)value;
       return CFB_OK;
     case CFB_OPT_RING_SLOTS:
       if (value < 0 || value > 3)

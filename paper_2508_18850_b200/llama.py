@@ -319,6 +319,12 @@ class LlamaDecoder:
         L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
         _native.check(L_.cfb_llama_set_option(self._h, 2, 1 if on else 0))
 
+    def set_pool_tiles(self, per_cta: int) -> None:
+        """Persistent engines: work-stolen gate/up tiles per CTA (0 = 4)."""
+        L_ = self._lib
+        L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
+        _native.check(L_.cfb_llama_set_option(self._h, 4, int(per_cta)))
+
     def set_ring_slots(self, spw: int) -> None:
         """Persistent engines: 8 KB ring slots per consumer warp (1..3; 0 =
         the deepest ring that fits); capture again afterwards."""

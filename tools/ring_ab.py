@@ -18,14 +18,18 @@ ap.add_argument("--spw", default="3,2")
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--steps", type=int, default=20)
 ap.add_argument("--engine", default="persistent")
+ap.add_argument("--pool", default="", help="A/B pool tiles per CTA instead of ring depth, e.g. 4,8,2")
 a = ap.parse_args()
 ctxs = [int(c) for c in a.ctx.split(",")]
 cfg = dataclasses.replace(LLAMA2_7B, engine=a.engine)
 m = LlamaDecoder.random(cfg, max(ctxs) + 64, seed=1)
 res = {}
 for rep in range(a.reps):
-    for spw in [int(s) for s in a.spw.split(",")]:
-        m.set_ring_slots(spw)
+    for spw in [int(s) for s in (a.pool or a.spw).split(",")]:
+        if a.pool:
+            m.set_pool_tiles(spw)
+        else:
+            m.set_ring_slots(spw)
         m.set_state(ctxs[0], 1)
         m.step()
         torch.cuda.synchronize()
