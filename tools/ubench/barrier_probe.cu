@@ -9,6 +9,8 @@
 //   2  relaxed arrival and polling, no fence at all (NOT a valid barrier:
 //      the lower bound without any memory ordering)
 //   3  atom.add.acq_rel arrival (round trip), relaxed polling + ld.acquire
+//   4  as 0, but only every 4th CTA arrives and polls (G/4 arrivals: the
+//      global part of a hierarchical cluster-then-grid barrier)
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
 //        -I paper_2508_18850_b200/csrc tools/ubench/barrier_probe.cu -o tools/ubench/barrier_probe
 #include <cstdio>
@@ -46,7 +48,9 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const char* src, size_t per
   __syncthreads();
   const int n_items = stream ? items_per_round * rounds * kNumConsumerWarps : 0;
   const Phase P = make_phase(src + per_cta * blockIdx.x, nullptr, n_items, kSlotBytes);
-  unsigned long long target = (ld_acquire_u64(counter) / G) * G;
+  const int per = variant == 4 ? G / 4 : G;  // arrivals per barrier
+  const bool part = variant != 4 || (blockIdx.x % 4 == 0 && blockIdx.x / 4 < per);
+  unsigned long long target = (ld_acquire_u64(counter) / per) * per;
   __syncthreads();
   if (warp == kNumConsumerWarps) {
     const Phase ph[1] = {P};
@@ -68,10 +72,10 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const char* src, size_t per
       }
     }
     consumer_sync();
-    if (tid == 0) {
+    if (tid == 0 && part) {
       const unsigned long long t0 = globaltimer();
-      target += G;
-      arrive_variant(counter, variant);
+      target += per;
+      arrive_variant(counter, variant == 4 ? 0 : variant);
       spin_until_geq(counter, target);
       tot += globaltimer() - t0;
     }
@@ -102,7 +106,7 @@ int main() {
   unsigned long long host[256];
   for (int stream : {0, 1})
     for (int ipr : {1, 4, 16})
-      for (int variant : {0, 1, 2, 3}) {
+      for (int variant : {0, 1, 2, 3, 4}) {
         if (!stream && ipr > 1) continue;
         const int G = sms;
         const size_t per = (total / G) / kSlotBytes * kSlotBytes;
@@ -120,10 +124,12 @@ int main() {
         cudaEventElapsedTime(&ms, e0, e1);
         cudaMemcpy(host, out, G * 8, cudaMemcpyDeviceToHost);
         double s = 0;
-        for (int i = 0; i < G; ++i) s += host[i];
+        int np = 0;
+        for (int i = 0; i < G; ++i)
+          if (variant != 4 || i % 4 == 0) { s += host[i]; ++np; }
         printf("%s {\"stream\": %d, \"kb_per_cta_round\": %d, \"variant\": %d, \"barrier_us\": %.3f, "
                "\"kernel_us_per_round\": %.3f}",
-               first ? "" : ",\n", stream, stream ? ipr * 64 : 0, variant, s / G / rounds / 1e3,
+               first ? "" : ",\n", stream, stream ? ipr * 64 : 0, variant, s / np / rounds / 1e3,
                ms * 1e3 / rounds);
         first = false;
       }
