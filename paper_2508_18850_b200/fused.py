@@ -18,6 +18,8 @@ output, and bit-identical from run to run.
 
 from __future__ import annotations
 
+import functools
+
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -150,6 +152,46 @@ def _pack_mha_static(scenario, cached: bool = True) -> dict:
                     Hp=Hp, Dp=Dp, cap=max(S, 1))
 
 
+@functools.lru_cache(maxsize=64)
+def _mha_schedule_cached(nh, n, B, D, H, nb, stats_mode):
+    """The static collective schedule of one split_token launch, emitted in
+    the reference's event order (pure function of the shapes: memoised, the
+    ~1,300 events of a Llama-dims call cost ~1 ms of Python to build)."""
+    ledger = TrafficLedger()
+    stage_traffic: dict[str, int] = {}
+    traces = []
+    h = H // n
+    for head in range(nh):
+        if stats_mode == ONESHOT:
+            tr = [("qkv_gather", emit_oneshot(ledger, n, B * 3 * h * nb, "gather")),
+                  ("attn_state_merge", emit_oneshot(ledger, n, (2 * B + B * H) * 4, ONESHOT_MERGE))]
+        else:
+            tr = [("qkv_gather", emit_gather(ledger, n, B * 3 * h * nb))]
+        if stats_mode == ONESHOT:
+            pass  # statistics travel inside attn_state_merge
+        elif stats_mode == MERGED:
+            tr.append(("stats_merge_reduce", emit_reduce(ledger, n, 2 * B * nb)))
+        else:
+            tr.append(("stats_max_reduce", emit_reduce(ledger, n, B * nb)))
+            tr.append(("stats_sum_reduce", emit_reduce(ledger, n, B * nb)))
+        if stats_mode != ONESHOT:
+            tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * H * nb)))
+        for stage, t in tr:
+            stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
+            traces.append(StageTrace(stage, head, t))
+        _emit_global(ledger, n, B, D // n, nb)
+    return tuple(ledger.events), tuple(stage_traffic.items()), tuple(traces)
+
+
+def _mha_schedule(nh, n, B, D, H, nb, stats_mode):
+    """Fresh (ledger, stage_traffic, traces) per call: the events and traces
+    are immutable, the containers are new, so callers may extend them."""
+    ev, st, tr = _mha_schedule_cached(nh, n, B, D, H, nb, stats_mode)
+    ledger = TrafficLedger()
+    ledger.events = list(ev)
+    return ledger, dict(st), list(tr)
+
+
 def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
                          append_new_token: bool = True) -> DecodeResult:
     """split_token fused attention module on the GPU (one cluster per head).
@@ -197,32 +239,7 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
         st = stats.cpu().numpy()
         dev_traffic = traffic.cpu().numpy()
 
-    # ledger of the static schedule, in the reference's event order
-    ledger = TrafficLedger()
-    stage_traffic: dict[str, int] = {}
-    traces = []
-    names = ["qkv_gather"] + (["stats_merge_reduce"] if stats_mode == MERGED
-                              else ["stats_max_reduce", "stats_sum_reduce"]) + ["attn_out_reduce"]
-    h = H // n
-    for head in range(nh):
-        if stats_mode == ONESHOT:
-            tr = [("qkv_gather", emit_oneshot(ledger, n, B * 3 * h * nb, "gather")),
-                  ("attn_state_merge", emit_oneshot(ledger, n, (2 * B + B * H) * 4, ONESHOT_MERGE))]
-        else:
-            tr = [("qkv_gather", emit_gather(ledger, n, B * 3 * h * nb))]
-        if stats_mode == ONESHOT:
-            pass  # statistics travel inside attn_state_merge
-        elif stats_mode == MERGED:
-            tr.append(("stats_merge_reduce", emit_reduce(ledger, n, 2 * B * nb)))
-        else:
-            tr.append(("stats_max_reduce", emit_reduce(ledger, n, B * nb)))
-            tr.append(("stats_sum_reduce", emit_reduce(ledger, n, B * nb)))
-        if stats_mode != ONESHOT:
-            tr.append(("attn_out_reduce", emit_reduce(ledger, n, B * H * nb)))
-        for stage, t in tr:
-            stage_traffic[stage] = stage_traffic.get(stage, 0) + t.dsmem_bytes
-            traces.append(StageTrace(stage, head, t))
-        _emit_global(ledger, n, B, D // n, nb)
+    ledger, stage_traffic, traces = _mha_schedule(nh, n, B, D, H, nb, stats_mode)
     if stats_mode == ONESHOT:
         device_traffic = {"qkv_gather": int(dev_traffic[0]), "attn_state_merge": int(dev_traffic[4])}
     else:
