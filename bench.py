@@ -180,11 +180,30 @@ def run_ours(args, rank, world):
     cfg = dataclasses.replace(LLAMA2_7B, engine=args.engine)
     ctxs = [int(c) for c in args.contexts.split(",")]
     cap = max(ctxs) + args.warmup + args.steps + 8
+    fused_error = None
     if world > 1 and args.tp_impl == "fused":
         # tensor parallel (configs[4]): rank-local shard, ONE persistent launch per token,
-        # both all-reduces of every layer inside the kernel over NVLink peer memory
+        # both all-reduces of every layer inside the kernel over NVLink peer memory.
+        # Every rank must take the same path: a failure anywhere (peer mapping,
+        # cross-rank wait timeout flagged by check()) sends ALL ranks to the NCCL path.
         from paper_2508_18850_b200.tp_fused import FusedTPLlama
-        tp = FusedTPLlama(cfg, rank, world, cap, seed=1234)
+        ok = 1
+        try:
+            tp = FusedTPLlama(cfg, rank, world, cap, seed=1234)
+            tp.set_state(ctxs[0], 1)
+            tp.step()
+            torch.cuda.synchronize()
+            tp.check()
+        except Exception as exc:  # pragma: no cover - multi-GPU only
+            ok, fused_error = 0, f"{type(exc).__name__}: {str(exc)[:200]}"
+        flag = torch.tensor([ok], device=dev, dtype=torch.int32)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:  # pragma: no cover - multi-GPU only
+            fused_error = fused_error or "another rank failed"
+            args.tp_impl = "nccl"
+            tp = None
+            torch.cuda.empty_cache()
+    if world > 1 and args.tp_impl == "fused":
         model = tp.eng
         step_fn, capture_fn, replay_fn = tp.step, tp.capture, tp.replay
         launches_per_step = tp.launches_per_step
@@ -281,6 +300,8 @@ def run_ours(args, rank, world):
             "phases": [trace_phases(model, c) for c in (ctxs[0], ctxs[-1])]}
     line["gpu_launches"] = launches
     line["clocks"] = clocks
+    if fused_error:  # pragma: no cover - multi-GPU only
+        line["tp_fused_error"] = fused_error
     if world == 1 and not args.no_deepseek:
         del model
         torch.cuda.empty_cache()
