@@ -240,6 +240,8 @@ def run_fused_mha_decode(scenario, stats_mode: str = TWO_PASS,
         dev_traffic = traffic.cpu().numpy()
 
     ledger, stage_traffic, traces = _mha_schedule(nh, n, B, D, H, nb, stats_mode)
+    names = ["qkv_gather"] + (["stats_merge_reduce"] if stats_mode == MERGED
+                              else ["stats_max_reduce", "stats_sum_reduce"]) + ["attn_out_reduce"]
     if stats_mode == ONESHOT:
         device_traffic = {"qkv_gather": int(dev_traffic[0]), "attn_state_merge": int(dev_traffic[4])}
     else:
