@@ -308,6 +308,7 @@ def run_ours(args, rank, world):
         for key, fn in (("engine_compare", lambda: engine_compare(cfg, ctxs, args, pk["hbm_gbs"])),
                         ("dropin_attention_module", lambda: dropin_api(pk["hbm_gbs"])),
                         ("deepseek_block", lambda: deepseek_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
+                        ("deepseek_model", lambda: deepseek_model_sweep([1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch16_ffn_tcgen05", lambda: batch16_ffn(cfg, pk["hbm_gbs"])),
                         ("batch16_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096, 16384], pk["hbm_gbs"])),
                         ("batch32_llama_tcgen05", lambda: batch16_stack(cfg, [1024, 4096], pk["hbm_gbs"], batch=32,
@@ -461,6 +462,40 @@ def deepseek_sweep(ctxs, peak_gbs, layers=4, reps=16):
                     "frac_of_peak": round(gbs / peak_gbs, 4), "bytes": LITE.block_bytes(S),
                     "launches": 2 * layers * (reps + 4)})
         del blocks, g
+        torch.cuda.empty_cache()
+    return out
+
+
+def deepseek_model_sweep(ctxs, peak_gbs, steps=20):
+    """configs[2] end to end: DeepSeek-V2-Lite-shaped model (27 layers of MLA
+    engine + fused MoE, 102,400-token LM head + argmax), greedy TPOT from ONE
+    CUDA graph per step (deepseek_model.DeepSeekDecoder; the latent caches are
+    attended, not appended - reference dataflows.py:393-397)."""
+    import torch
+    from paper_2508_18850_b200.deepseek_model import LITE_MODEL, DeepSeekDecoder
+    out = []
+    for S in ctxs:
+        m = DeepSeekDecoder.random(LITE_MODEL, S, seed=0)
+        m.set_token(1)
+        m.step()
+        torch.cuda.synchronize()
+        m.capture()
+        for _ in range(3):
+            m.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(m.stream)
+        for _ in range(steps):
+            m.replay()
+        e1.record(m.stream)
+        torch.cuda.synchronize()
+        us = e0.elapsed_time(e1) * 1e3 / steps
+        nbytes = LITE_MODEL.step_bytes(S)
+        out.append({"ctx": S, "layers": LITE_MODEL.n_layers, "vocab": LITE_MODEL.vocab,
+                    "tpot_us": round(us, 1), "hbm_gbs": round(nbytes / us / 1e3, 1),
+                    "frac_of_peak": round(nbytes / us / 1e3 / peak_gbs, 4), "bytes": nbytes,
+                    "launches": (2 + 4 * LITE_MODEL.n_layers) * (steps + 4)})
+        del m
         torch.cuda.empty_cache()
     return out
 
