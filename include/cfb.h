@@ -356,7 +356,12 @@ typedef struct cfb_ffn_b16_args {
   unsigned long long* out_acc;
   int* ticket;
   int batch;  /* rows = MMA N: 16 (or 0) or 32; the workspaces above scale with it */
+  float* slots; /* cfb_b16_slots_floats(hidden, 0, inter, batch) floats: per-contributor partial tiles */
 } cfb_ffn_b16_args;
+/* Floats of the partial-slot workspace (`slots`) the batched projections need:
+ * per 128-row tile, one fp32 [batch][128] partial per contributing CTA, summed
+ * in CTA order by the tile's finishing CTA (deterministic, no atomics). */
+size_t cfb_b16_slots_floats(int hidden, int n_heads, int inter, int batch);
 int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream);
 
 /*
@@ -411,6 +416,7 @@ typedef struct cfb_b16_layer_args {
   /* sequences = MMA N: 16 (or 0) or 32.  Every "16" above is this batch
    * (caches, pos, table rows, workspaces); a sequence with pos -1 is inactive */
   int batch;
+  float* slots; /* cfb_b16_slots_floats(hidden, n_heads, inter, batch) floats */
 } cfb_b16_layer_args;
 #define CFB_KV_PAGE 128
 int cfb_llama_b16_layer(const cfb_b16_layer_args* args, void* stream);

@@ -145,7 +145,7 @@ class FfnB16Args(ctypes.Structure):
 
     _fields_ = [(n, ctypes.c_int) for n in ("hidden", "inter", "flags")] + [("eps", ctypes.c_float)] + [
         (n, _vp) for n in ("resid", "norm_w", "w_gu", "w_dn", "xp", "gu_acc", "ap", "out_acc", "ticket")] + [
-        ("batch", ctypes.c_int)]
+        ("batch", ctypes.c_int), ("slots", _vp)]
 
 
 class B16LayerArgs(ctypes.Structure):
@@ -156,7 +156,8 @@ class B16LayerArgs(ctypes.Structure):
         (n, _vp) for n in ("resid", "attn_norm", "ffn_norm", "w_qkv", "w_o", "w_gu", "w_dn", "k_cache",
                            "v_cache", "rope_cs", "pos", "xp", "q16", "qkv_acc", "part", "o_acc",
                            "gu_acc", "ap", "ticket", "block_table")] + [("max_pages", ctypes.c_int),
-                                                                        ("batch", ctypes.c_int)]
+                                                                        ("batch", ctypes.c_int),
+                                                                        ("slots", _vp)]
 
 
 class MoeArgs(ctypes.Structure):
@@ -175,6 +176,8 @@ def bind_extra(L) -> None:
     L.cfb_tc_gemm_b16.argtypes = [_vp] * 6 + [ctypes.c_int] * 3 + [_vp]
     L.cfb_tc_gemm_b16.restype = ctypes.c_int
     L.cfb_ffn_b16.argtypes = [ctypes.POINTER(FfnB16Args), _vp]
+    L.cfb_b16_slots_floats.argtypes = [ctypes.c_int] * 4
+    L.cfb_b16_slots_floats.restype = ctypes.c_size_t
     L.cfb_ffn_b16.restype = ctypes.c_int
     L.cfb_llama_b16_layer.argtypes = [ctypes.POINTER(B16LayerArgs), _vp]
     L.cfb_llama_b16_layer.restype = ctypes.c_int

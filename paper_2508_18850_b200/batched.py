@@ -182,7 +182,9 @@ class BatchedLlama:
             o_acc=torch.zeros(B * D, device=dev, dtype=torch.int64),
             gu_acc=torch.zeros(B * 2 * F, device=dev, dtype=torch.int64),
             ap=torch.zeros(B * F, device=dev, dtype=torch.float16),
-            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + B * nh, device=dev, dtype=torch.int32))
+            ticket=torch.zeros((3 * nh * 128 + 2 * D + 2 * F) // 128 + B * nh, device=dev, dtype=torch.int32),
+            slots=torch.zeros(int(_native.lib().cfb_b16_slots_floats(D, nh, F, B)), device=dev,
+                              dtype=torch.float32))
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
         self.pool = pool
@@ -292,7 +294,7 @@ class BatchedLlama:
             part=w["part"].data_ptr(), o_acc=w["o_acc"].data_ptr(), gu_acc=w["gu_acc"].data_ptr(),
             ap=w["ap"].data_ptr(), ticket=w["ticket"].data_ptr(),
             block_table=self.pool.table.data_ptr() if self.pool else None,
-            max_pages=self.pool.max_pages if self.pool else 0, batch=self.B)
+            max_pages=self.pool.max_pages if self.pool else 0, batch=self.B, slots=w["slots"].data_ptr())
 
     def _enqueue(self, advance: bool = True) -> None:
         L_ = _native.lib()

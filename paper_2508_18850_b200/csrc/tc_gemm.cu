@@ -79,8 +79,10 @@ struct TcQkv {
 struct TcParams {
   const __half* w;   // packed weight blocks [M/128][K/64][16 KB]
   const __half* x;   // packed activation blocks [K/64][nb * 128 B]
-  unsigned long long* y;  // [16][M] fixed point (2^-32), accumulated
+  unsigned long long* y;  // kTcAccum: [nb][M] fixed point (2^-32), accumulated
+  float* slots;      // finishing modes: [M/128][maxc][nb][128] fp32 per-contributor partials
   int M, K, mode, nb;  // nb: batch rows = MMA N (16 or 32)
+  int maxc;          // contributor slots per tile
   int* ticket;       // [M/128] zero (re-zeroed by the finishing CTA)
   __half* act;       // kTcSwiGLU: packed activations for the next projection
   float* out;        // kTcResidOut: out[n][m] = resid[n][m] + y (out may alias resid)
@@ -111,6 +113,30 @@ __device__ __forceinline__ void tc_fence_after() {
 }
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+// finisher: value of (batch row nn, tile rows r0 .. r0 + V - 1) = sum of the
+// contributors' partial slots in contributor order (deterministic); all loads
+// of one contributor in flight together, everything in registers
+template <int V>
+__device__ __forceinline__ void tc_tile_sum(const float* tslot, int contrib, int nb, int nn, int r0,
+                                            float (&v)[V]) {
+  constexpr int NV = V / 4;
+#pragma unroll
+  for (int e = 0; e < V; ++e) v[e] = 0.f;
+  for (int k = 0; k < contrib; ++k) {
+    const float4* src = reinterpret_cast<const float4*>(tslot + ((size_t)k * nb + nn) * kTcM + r0);
+    float4 w[NV];
+#pragma unroll
+    for (int e = 0; e < NV; ++e) w[e] = __ldcg(src + e);
+#pragma unroll
+    for (int e = 0; e < NV; ++e) {
+      v[4 * e] += w[e].x;
+      v[4 * e + 1] += w[e].y;
+      v[4 * e + 2] += w[e].z;
+      v[4 * e + 3] += w[e].w;
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p) {
@@ -238,17 +264,27 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&acce[a]);  // accumulator drained: the MMA warp may reuse it
+      if (p.mode == kTcAccum) {
+#pragma unroll
+        for (int c = 0; c < kTcNMax; ++c)
+          if (c < nb) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
+        continue;
+      }
+      // finishing modes: this contributor's partial tile -> its own slot (plain,
+      // coalesced stores: lanes = consecutive rows), summed by the finisher in
+      // contributor order - deterministic, and no atomics on the critical tail
+      auto cta_of = [&](long long b) { return (int)(((b + 1) * G - 1) / TB); };
+      const int first = cta_of((long long)t * KBt);
+      float* myslot = p.slots + ((size_t)t * p.maxc + (i - first)) * (size_t)(nb * kTcM);
 #pragma unroll
       for (int c = 0; c < kTcNMax; ++c)
-        if (c < nb) red_add_fixed(p.y + (size_t)c * p.M + m, __uint_as_float(r[c]));
-      if (p.mode == kTcAccum) continue;
+        if (c < nb) myslot[c * kTcM + 32 * q + lane] = __uint_as_float(r[c]);
       // ticket: the last contributor to tile t finishes it
       __threadfence();
       named_bar_sync(2, 128);
       int* flag = reinterpret_cast<int*>(tmem_slot + 1);
+      const int contrib = cta_of((long long)(t + 1) * KBt - 1) - first + 1;
       if (warp == 2 && lane == 0) {
-        auto cta_of = [&](long long b) { return (int)(((b + 1) * G - 1) / TB); };
-        const int contrib = cta_of((long long)(t + 1) * KBt - 1) - cta_of((long long)t * KBt) + 1;
         const int old = atomicAdd(p.ticket + t, 1);
         *flag = old == contrib - 1;
         if (old == contrib - 1) p.ticket[t] = 0;
@@ -256,31 +292,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       named_bar_sync(2, 128);
       if (!*flag) continue;
       __threadfence();
+      // tile value (batch row nn, tile row r0 .. r0 + 4*NV - 1): sum of the
+      // contributors' slots in order; all loads of a contributor in flight together
+      const float* tslot = p.slots + (size_t)t * p.maxc * (nb * kTcM);
+      auto tile_vals = [&](int nn, int r0, auto& v) { tc_tile_sum(tslot, contrib, nb, nn, r0, v); };
       const int et = tid - 64;  // 0..127: 16 batch rows per pass
       for (int hb = 0; hb < nb; hb += 16) {
       if (p.mode == kTcQKV) {
         // thread = (sequence nn, 8 rotation pairs (i, i + 64), i in [i0, i0 + 8))
         const int nn = hb + (et >> 3), i0 = (et & 7) * 8;
-        unsigned long long* yr = p.y + (size_t)nn * p.M + t * kTcM;
-        ulonglong2 lo[4], hi[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          lo[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yr + i0) + e);
-          hi[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yr + 64 + i0) + e);
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          reinterpret_cast<ulonglong2*>(yr + i0)[e] = make_ulonglong2(0ull, 0ull);
-          reinterpret_cast<ulonglong2*>(yr + 64 + i0)[e] = make_ulonglong2(0ull, 0ull);
-        }
+        float lo[8], hi[8];
+        tile_vals(nn, i0, lo);
+        tile_vals(nn, 64 + i0, hi);
         const TcQkv& Q = p.qkv;
         const int kind = t / Q.nh, hd = t % Q.nh, ps_ = Q.pos[nn];
         const int ps = ps_ < 0 ? 0 : ps_;  // inactive sequence (position -1): no RoPE row, no cache write
         __align__(16) __half a[8], b[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float x1 = round_to<__half>(fixed_to_float((e & 1) ? lo[e >> 1].y : lo[e >> 1].x));
-          float x2 = round_to<__half>(fixed_to_float((e & 1) ? hi[e >> 1].y : hi[e >> 1].x));
+          float x1 = round_to<__half>(lo[e]);
+          float x2 = round_to<__half>(hi[e]);
           if (kind < 2) {  // q, k: rotate-half RoPE at the sequence's position
             const float c = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2], sn = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2 + 1];
             const float r1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sn));
@@ -314,46 +345,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
         // f-range of tile t = K-block t of the next projection.  All loads of a
         // thread are issued before any store (no serialised L2 round trips).
         const int nn = hb + (et >> 3), j0 = (et & 7) * 8;  // 16 rows x 8 chunks = 128 threads
-        unsigned long long* yg = p.y + (size_t)nn * p.M + t * kTcM + j0;
-        ulonglong2 gv[4], uv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          gv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yg) + e);
-          uv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(yg + 64) + e);
-        }
+        float gv[8], uv[8];
+        tile_vals(nn, j0, gv);
+        tile_vals(nn, 64 + j0, uv);
         __align__(16) __half h[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const float gt = fixed_to_float((e & 1) ? gv[e >> 1].y : gv[e >> 1].x);
-          const float up = fixed_to_float((e & 1) ? uv[e >> 1].y : uv[e >> 1].x);
-          h[e] = __float2half_rn(__fmul_rn(__fdiv_rn(gt, __fadd_rn(1.0f, expf(-gt))), up));
-        }
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          reinterpret_cast<ulonglong2*>(yg)[e] = make_ulonglong2(0ull, 0ull);
-          reinterpret_cast<ulonglong2*>(yg + 64)[e] = make_ulonglong2(0ull, 0ull);
-        }
+        for (int e = 0; e < 8; ++e)
+          h[e] = __float2half_rn(__fmul_rn(__fdiv_rn(gv[e], __fadd_rn(1.0f, expf(-gv[e]))), uv[e]));
         *reinterpret_cast<uint4*>(p.act + xpack_off(nn, t * kTcKB + j0, nb)) = *reinterpret_cast<const uint4*>(h);
       } else {
         // 16 rows x 128 columns: thread = (row, 16-column run)
         const int nn = hb + (et >> 3), c0 = (et & 7) * 16;
         const size_t o = (size_t)nn * p.M + t * kTcM + c0;
-        ulonglong2 yv[8];
+        float yv[16];
+        tile_vals(nn, c0, yv);
         float4 rv[4];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) yv[e] = __ldcg(reinterpret_cast<const ulonglong2*>(p.y + o) + e);
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           rv[e] = p.resid ? __ldcg(reinterpret_cast<const float4*>(p.resid + o) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) reinterpret_cast<ulonglong2*>(p.y + o)[e] = make_ulonglong2(0ull, 0ull);
-#pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float4 r4 = rv[e];
           reinterpret_cast<float4*>(p.out + o)[e] =
-              make_float4(__fadd_rn(r4.x, fixed_to_float(yv[2 * e].x)), __fadd_rn(r4.y, fixed_to_float(yv[2 * e].y)),
-                          __fadd_rn(r4.z, fixed_to_float(yv[2 * e + 1].x)),
-                          __fadd_rn(r4.w, fixed_to_float(yv[2 * e + 1].y)));
+              make_float4(__fadd_rn(r4.x, yv[4 * e]), __fadd_rn(r4.y, yv[4 * e + 1]),
+                          __fadd_rn(r4.z, yv[4 * e + 2]), __fadd_rn(r4.w, yv[4 * e + 3]));
         }
       }
       }  // row passes
@@ -391,10 +406,31 @@ __global__ void tc_finish_kernel(unsigned long long* yacc, float* out, const flo
 
 int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytesMax) + (4 * kTcStages + 8) * 8 + 32; }
 
+// contributor slots per tile of the even block split: <= ceil(G / tiles) + 1
+static int tc_maxc(int M, int K, int G) {
+  const int tiles = M / kTcM, TB = tiles * (K / kTcKB);
+  if (G > TB) G = TB;
+  return (G + tiles - 1) / tiles + 1;
+}
+static int tc_sms() {
+  int dev = 0, sms = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess)
+    return 0;
+  return sms;
+}
+// floats of the finishing modes' partial-slot workspace for one projection
+size_t tc_slots_floats(int M, int K, int nb) {
+  if (M < kTcM || K < kTcKB) return 0;
+  return (size_t)(M / kTcM) * tc_maxc(M, K, tc_sms()) * nb * kTcM;
+}
+
 int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
             cudaStream_t st, bool pdl, int mode = kTcAccum, int* ticket = nullptr, __half* act = nullptr,
-            float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr, int nb = kTcN) {
+            float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr, int nb = kTcN,
+            float* slots = nullptr) {
   if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "tcgen05 batch must be 16 or 32");
+  if (mode != kTcAccum && !slots) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need the slot workspace");
   if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
   if (const int rc = configure_kernel((const void*)tc_gemm_kernel, tc_smem_bytes(), false)) return rc;
@@ -411,6 +447,8 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   p.K = K;
   p.mode = mode;
   p.nb = nb;
+  p.slots = slots;
+  p.maxc = tc_maxc(M, K, grid);
   p.ticket = ticket;
   p.act = act;
   p.out = out;
@@ -519,7 +557,7 @@ static int launch_simple(K kern, dim3 grid, int block, cudaStream_t st, bool pdl
 
 int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
   if (!a || !a->resid || !a->norm_w || !a->w_gu || !a->w_dn || !a->xp || !a->gu_acc || !a->ap ||
-      !a->out_acc)
+      !a->out_acc || !a->slots)
     return set_error(CFB_ERR_ARGUMENT, "null pointer");
   const int D = a->hidden, F = a->inter;
   if (D % 128 || F % 64 || (2 * F) % 128)
@@ -536,11 +574,11 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
   // their last contributor; down tiles finished as resid + sum
   if ((rc = tc_gemm(static_cast<const __half*>(a->w_gu), static_cast<const __half*>(a->xp), a->gu_acc,
                     2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap), nullptr, nullptr,
-                    nullptr, nb)))
+                    nullptr, nb, a->slots)))
     return rc;
   return tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc, D, F,
                  0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid,
-                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid, nullptr, nb);
+                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid, nullptr, nb, a->slots);
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
@@ -578,7 +616,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
     if (a->block_table && a->max_pages * 128 < a->max_len)
       return set_error(CFB_ERR_DIMENSION, "b16 layer: max_pages * 128 < max_len");
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
-                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv, nb)))
+                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv, nb, a->slots)))
       return rc;
     if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
                               static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
@@ -587,7 +625,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
       return rc;
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
                       st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid,
-                      nullptr, nb)))
+                      nullptr, nb, a->slots)))
       return rc;
   }
   if (a->stage == 1) return CFB_OK;
@@ -606,6 +644,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   f.out_acc = a->o_acc;
   f.ticket = a->ticket + (Mq + D) / kTcM;
   f.batch = nb;
+  f.slots = a->slots;
   return ffn_b16(&f, st);
 }
 
@@ -728,6 +767,16 @@ int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigne
     return rc;
   if (!y) return CFB_OK;
   return tc_finish(y_acc, y, resid, 16 * M, st, true);
+}
+
+size_t cfb_b16_slots_floats(int hidden, int n_heads, int inter, int batch) {
+  using namespace cfb;
+  const int nb = batch ? batch : kTcN, Ka = n_heads * 128;
+  size_t m = tc_slots_floats(3 * Ka, hidden, nb);
+  const size_t c[3] = {tc_slots_floats(hidden, Ka, nb), tc_slots_floats(2 * inter, hidden, nb),
+                       tc_slots_floats(hidden, inter, nb)};
+  for (size_t v : c) m = v > m ? v : m;
+  return m;
 }
 
 int cfb_ffn_b16(const cfb_ffn_b16_args* args, void* stream) {

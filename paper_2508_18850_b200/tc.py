@@ -88,6 +88,8 @@ class TcFfnB16:
         self.ap = torch.zeros(BATCH * self.F, device=dev, dtype=torch.float16)
         self.out_acc = torch.zeros(BATCH * self.D, device=dev, dtype=torch.int64)
         self.ticket = torch.zeros((2 * self.F + self.D) // 128, device=dev, dtype=torch.int32)
+        self.slots = torch.zeros(int(_native.lib().cfb_b16_slots_floats(self.D, 0, self.F, BATCH)),
+                                 device=dev, dtype=torch.float32)
         torch.cuda.synchronize()
 
     @property
@@ -100,5 +102,5 @@ class TcFfnB16:
                                w_gu=self.w_gu.data_ptr(), w_dn=self.w_dn.data_ptr(),
                                xp=self.xp.data_ptr(), gu_acc=self.gu_acc.data_ptr(),
                                ap=self.ap.data_ptr(), out_acc=self.out_acc.data_ptr(),
-                               ticket=self.ticket.data_ptr(), batch=BATCH)
+                               ticket=self.ticket.data_ptr(), batch=BATCH, slots=self.slots.data_ptr())
         _native.check(_native.lib().cfb_ffn_b16(a, _native.stream_ptr(stream)))
