@@ -159,15 +159,33 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   if (!last) return;
   __threadfence();
   const float* pp = part + (size_t)pair * nchunks * 130;
-  float M = -INFINITY;
-  for (int cc = 0; cc < nused; ++cc) M = fmaxf(M, __ldcg(pp + (size_t)cc * 130));
-  float lt = 0.f, at = 0.f;
-  for (int cc = 0; cc < nused; ++cc) {
-    const float w = expf(__ldcg(pp + (size_t)cc * 130) - M);
-    lt = fmaf(__ldcg(pp + (size_t)cc * 130 + 1), w, lt);
-    at = fmaf(__ldcg(pp + (size_t)cc * 130 + 2 + tid), w, at);
+  // chunk (m, l) loaded once, in parallel, into the (now free) K tile; every
+  // thread then merges its dimension over the chunks in chunk order (the
+  // same fmaf sequence as a serial merge), 8 partial loads in flight
+  float* cm = reinterpret_cast<float*>(ks);  // [nused] m, then the weights
+  float* cl = cm + nchunks;                  // [nused] l
+  for (int cc = tid; cc < nused; cc += kBaThreads) {
+    cm[cc] = __ldcg(pp + (size_t)cc * 130);
+    cl[cc] = __ldcg(pp + (size_t)cc * 130 + 1);
   }
-  // packed UMMA activation layout (csrc/tc_gemm.cu): K index = h*128 + tid, row n
+  __syncthreads();
+  float M = -INFINITY;
+  for (int cc = 0; cc < nused; ++cc) M = fmaxf(M, cm[cc]);
+  __syncthreads();
+  for (int cc = tid; cc < nused; cc += kBaThreads) cm[cc] = expf(cm[cc] - M);
+  __syncthreads();
+  float lt = 0.f, at = 0.f;
+  for (int c0 = 0; c0 < nused; c0 += 8) {
+    float a8[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a8[j] = c0 + j < nused ? __ldcg(pp + (size_t)(c0 + j) * 130 + 2 + tid) : 0.f;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (c0 + j < nused) {
+        lt = fmaf(cl[c0 + j], cm[c0 + j], lt);
+        at = fmaf(a8[j], cm[c0 + j], at);
+      }
+  }
   // packed UMMA activation layout of nb rows (csrc/tc_gemm.cu xpack_off): K index h*128 + tid, row n
   const int nb = gridDim.y / nh, k = h * 128 + tid, kb = k / 64, kk = k % 64, s = kk / 16, c2 = (kk % 16) / 8;
   xp[(size_t)kb * (nb * 64) + ((s * 2 + c2) * (nb / 8) + n / 8) * 64 + (n % 8) * 8 + (kk % 8)] =
