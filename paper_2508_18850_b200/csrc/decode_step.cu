@@ -1062,11 +1062,16 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     *last = (atomicAdd(p.ticket, 1u) == (unsigned)G - 1);
   }
   consumer_sync();
-  if (*last && tid == 0) {
-    __threadfence();
+  if (*last) {
+    // the G per-CTA candidates, reduced in parallel: thread c loads
+    // candidate c (one round trip), warp shuffles, then warp 0 folds the
+    // warp winners; `better` is a total order (value, then lower index), so
+    // the winner does not depend on the reduction tree
+    if (tid == 0) __threadfence();
+    consumer_sync();
     float v = -INFINITY;
     int ix = 0x7fffffff;
-    for (int c = 0; c < G; ++c) {
+    for (int c = tid; c < G; c += kConsumerThreads) {
       const float cv = __ldcg(&p.cand_val[c]);
       const int ci = __ldcg(&p.cand_idx[c]);
       if (better(cv, ci, v, ix)) {
@@ -1074,18 +1079,40 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         ix = ci;
       }
     }
-    if (tp) {  // global argmax over the vocabulary shards: MAX of order-preserving keys
-      const unsigned long long key = argmax_key(v, ix + p.voff);
-      for (int t = 0; t < p.T; ++t) red_max_u64(tp_key(p.xch[t], D), key);
-      __threadfence_system();
-      for (int t = 0; t < p.T; ++t) red_release_sys_add(tp_tok(p.xch[t], D), 1ull);
-      tp_spin(tp_tok(xown, D), tok_base + p.T, p.timeout_ns, p.err);
-      const unsigned long long k = ld_acquire_sys_u64(tp_key(xown, D));
-      ix = (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull));
+    for (int o = 16; o > 0; o >>= 1) {
+      const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+      if (better(ov, oi, v, ix)) {
+        v = ov;
+        ix = oi;
+      }
     }
-    *p.token = ix;
-    *p.ticket = 0;
-    *p.pos = S + 1;
+    if (lane == 0) {
+      red[warp] = v;
+      reinterpret_cast<int*>(red)[kNumConsumerWarps + warp] = ix;
+    }
+    consumer_sync();
+    if (tid == 0) {  // fold the warp winners, publish the token
+      v = -INFINITY;
+      ix = 0x7fffffff;
+      for (int w2 = 0; w2 < kNumConsumerWarps; ++w2)
+        if (better(red[w2], reinterpret_cast<int*>(red)[kNumConsumerWarps + w2], v, ix)) {
+          v = red[w2];
+          ix = reinterpret_cast<int*>(red)[kNumConsumerWarps + w2];
+        }
+      if (tp) {  // global argmax over the vocabulary shards: MAX of order-preserving keys
+        const unsigned long long key = argmax_key(v, ix + p.voff);
+        for (int t = 0; t < p.T; ++t) red_max_u64(tp_key(p.xch[t], D), key);
+        __threadfence_system();
+        for (int t = 0; t < p.T; ++t) red_release_sys_add(tp_tok(p.xch[t], D), 1ull);
+        tp_spin(tp_tok(xown, D), tok_base + p.T, p.timeout_ns, p.err);
+        const unsigned long long k = ld_acquire_sys_u64(tp_key(xown, D));
+        ix = (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFull));
+      }
+      *p.token = ix;
+      *p.ticket = 0;
+      *p.pos = S + 1;
+    }
   }
   if (kCluster) {
     cluster_arrive();  // no CTA leaves while a peer could still address its smem

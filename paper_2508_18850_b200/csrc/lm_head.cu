@@ -120,18 +120,29 @@ __global__ void __launch_bounds__(kThreads, 1) lm_head_kernel(const LmParams p) 
   consumer_sync();
   if (last) {
     __threadfence();
-    if (tid < B) {
+    // warp w reduces rows b = w, w + 8, ...: lanes load the candidates in
+    // parallel (one round trip instead of G serial ones), then shuffles;
+    // `better` is a total order, so the tree shape cannot change the winner
+    for (int b = warp; b < B; b += kNumConsumerWarps) {
       float v = -INFINITY;
       int ix = 0x7fffffff;
-      for (int c = 0; c < G; ++c) {
-        const float cv = __ldcg(&p.cand_val[(size_t)c * B + tid]);
-        const int ci = __ldcg(&p.cand_idx[(size_t)c * B + tid]);
+      for (int c = lane; c < G; c += 32) {
+        const float cv = __ldcg(&p.cand_val[(size_t)c * B + b]);
+        const int ci = __ldcg(&p.cand_idx[(size_t)c * B + b]);
         if (better(cv, ci, v, ix)) {
           v = cv;
           ix = ci;
         }
       }
-      p.token_out[tid] = ix;
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (better(ov, oi, v, ix)) {
+          v = ov;
+          ix = oi;
+        }
+      }
+      if (lane == 0) p.token_out[b] = ix;
     }
     if (tid == 0) {
       *p.ticket = 0;
