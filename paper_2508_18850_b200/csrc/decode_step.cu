@@ -645,10 +645,14 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   const int half = kH / 2;
 
   // RoPE of q and k_new at position S (rotate-half), fp16-stored values
+  // the position is fixed for the whole launch: thread d < H/2 keeps its
+  // rotation (cos, sin) in registers instead of re-reading the table in
+  // every layer's attention critical path
+  const float rope_c = tid < half ? p.rope_cs[((size_t)S * half + tid) * 2] : 0.f;
+  const float rope_s = tid < half ? p.rope_cs[((size_t)S * half + tid) * 2 + 1] : 0.f;
   auto rope_qk = [&]() {
-    for (int d = tid; d < half; d += kConsumerThreads) {
-      const float c = p.rope_cs[((size_t)S * half + d) * 2];
-      const float sn = p.rope_cs[((size_t)S * half + d) * 2 + 1];
+    for (int d = tid; d < half; d += kConsumerThreads) {  // half <= kConsumerThreads: d == tid
+      const float c = rope_c, sn = rope_s;
       const float q1_ = qf[d], q2 = qf[d + half], k1_ = kf[d], k2 = kf[d + half];
       qf[d] = round_to<__half>(__fsub_rn(__fmul_rn(q1_, c), __fmul_rn(q2, sn)));
       qf[d + half] = round_to<__half>(__fadd_rn(__fmul_rn(q2, c), __fmul_rn(q1_, sn)));
