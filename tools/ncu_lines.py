@@ -1,6 +1,6 @@
 """Attribute ncu warp-stall samples to CUDA source lines (CPU side).
 
-    python tools/ncu_lines.py <rep.ncu-rep> <lib.so> <mangled-kernel> [N]
+    python tools/ncu_lines.py <rep.ncu-rep> <lib.so> <mangled-kernel> [N] [kernel-regex]
 Extracts the kernel's cubin from the .so, maps SASS offsets to file:line with
 nvdisasm --print-line-info (needs -lineinfo), and sums the per-instruction
 samples of the ncu source page per line.
@@ -16,7 +16,8 @@ import tempfile
 
 rep, lib, kern = sys.argv[1:4]
 n = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+kfilter = ["-k", f"regex:{sys.argv[5]}"] if len(sys.argv) > 5 else []
+out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + kfilter,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
