@@ -11,6 +11,11 @@
 //   3  atom.add.acq_rel arrival (round trip), relaxed polling + ld.acquire
 //   4  as 0, but only every 4th CTA arrives and polls (G/4 arrivals: the
 //      global part of a hierarchical cluster-then-grid barrier)
+//   5  as 0, then every CTA loads a 4096-float vector written by all CTAs
+//      before the barrier (barrier + the dependent data round trip)
+//   6  data-carried epochs: each CTA stores its 4096/G slice as u64 words
+//      (value | epoch << 32, st.relaxed), every CTA loads all 4096 words
+//      (ld.relaxed) and re-reads the stale ones until every epoch is current
 //   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a \
 //        -I paper_2508_18850_b200/csrc tools/ubench/barrier_probe.cu -o tools/ubench/barrier_probe
 #include <cstdio>
@@ -36,7 +41,7 @@ __device__ __forceinline__ void arrive_variant(unsigned long long* c, int v) {
 __global__ void __launch_bounds__(kThreads, 1) probe(const char* src, size_t per_cta, int items_per_round,
                                                      int rounds, int variant, int stream,
                                                      unsigned long long* counter, unsigned long long* out,
-                                                     float* sink) {
+                                                     float* sink, float* vec, unsigned long long* words) {
   extern __shared__ __align__(128) char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + ring_bytes(3));
   const Ring ring{smem, bars, bars + kNumSlots, 3, 32};
@@ -72,7 +77,43 @@ __global__ void __launch_bounds__(kThreads, 1) probe(const char* src, size_t per
       }
     }
     consumer_sync();
-    if (tid == 0 && part) {
+    constexpr int kV = 4096;
+    if (variant == 5 || variant == 6) {
+      const int c0 = (int)((long long)blockIdx.x * kV / G), c1 = (int)((long long)(blockIdx.x + 1) * kV / G);
+      unsigned long long t0 = 0;
+      if (tid == 0) t0 = globaltimer();
+      const unsigned ep = (unsigned)(r + 1) + 1000u * (unsigned)blockIdx.x * 0u;
+      if (variant == 5) {
+        for (int c = c0 + tid; c < c1; c += kConsumerThreads) vec[c] = (float)(r + c);
+        consumer_sync();
+        if (tid == 0) {
+          target += G;
+          arrive_variant(counter, 0);
+          spin_until_geq(counter, target);
+        }
+        consumer_sync();
+        float a = 0.f;
+        for (int c = tid; c < kV; c += kConsumerThreads) a += __ldcg(vec + c);
+        acc += a;
+      } else {
+        for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
+          const unsigned long long w = (unsigned long long)__float_as_uint((float)(r + c)) |
+                                       ((unsigned long long)ep << 32);
+          asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(words + c), "l"(w) : "memory");
+        }
+        float a = 0.f;
+        for (int c = tid; c < kV; c += kConsumerThreads) {
+          unsigned long long w;
+          do {
+            asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w) : "l"(words + c) : "memory");
+          } while ((unsigned)(w >> 32) < ep);
+          a += __uint_as_float((unsigned)w);
+        }
+        acc += a;
+      }
+      consumer_sync();
+      if (tid == 0) tot += globaltimer() - t0;
+    } else if (tid == 0 && part) {
       const unsigned long long t0 = globaltimer();
       target += per;
       arrive_variant(counter, variant == 4 ? 0 : variant);
@@ -94,6 +135,11 @@ int main() {
   cudaMalloc(&counter, 8);
   cudaMalloc(&out, 256 * 8);
   cudaMalloc(&sink, 4);
+  float* vec;
+  unsigned long long* words;
+  cudaMalloc(&vec, 4096 * 4);
+  cudaMalloc(&words, 4096 * 8);
+  cudaMemset(words, 0, 4096 * 8);
   cudaMemset(buf, 1, total);
   cudaMemset(counter, 0, 8);
   int sms;
@@ -106,18 +152,19 @@ int main() {
   unsigned long long host[256];
   for (int stream : {0, 1})
     for (int ipr : {1, 4, 16})
-      for (int variant : {0, 1, 2, 3, 4}) {
+      for (int variant : {0, 1, 2, 3, 4, 5, 6}) {
         if (!stream && ipr > 1) continue;
         const int G = sms;
         const size_t per = (total / G) / kSlotBytes * kSlotBytes;
         if ((size_t)ipr * rounds * kNumConsumerWarps * kSlotBytes > per) continue;
+        cudaMemset(words, 0, 4096 * 8);  // epochs restart at 1 every launch
         for (int rep = 0; rep < 2; ++rep)
-          probe<<<G, kThreads, smem>>>(buf, per, ipr, rounds, variant, stream, counter, out, sink);
+          probe<<<G, kThreads, smem>>>(buf, per, ipr, rounds, variant, stream, counter, out, sink, vec, words);
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
         cudaEventRecord(e0);
-        probe<<<G, kThreads, smem>>>(buf, per, ipr, rounds, variant, stream, counter, out, sink);
+        probe<<<G, kThreads, smem>>>(buf, per, ipr, rounds, variant, stream, counter, out, sink, vec, words);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
