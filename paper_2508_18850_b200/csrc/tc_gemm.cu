@@ -301,19 +301,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       if (p.mode == kTcQKV) {
         // thread = (sequence nn, 8 rotation pairs (i, i + 64), i in [i0, i0 + 8))
         const int nn = hb + (et >> 3), i0 = (et & 7) * 8;
-        float lo[8], hi[8];
-        tile_vals(nn, i0, lo);
-        tile_vals(nn, 64 + i0, hi);
         const TcQkv& Q = p.qkv;
         const int kind = t / Q.nh, hd = t % Q.nh, ps_ = Q.pos[nn];
         const int ps = ps_ < 0 ? 0 : ps_;  // inactive sequence (position -1): no RoPE row, no cache write
+        // the rotation pairs of rows i0..i0+7 are issued before the slot sums,
+        // so their round trip overlaps the partial loads
+        float4 cs4[4];
+        if (kind < 2) {
+          const float4* src = reinterpret_cast<const float4*>(Q.rope_cs + ((size_t)ps * 64 + i0) * 2);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) cs4[e] = __ldg(src + e);
+        }
+        const float* csf = reinterpret_cast<const float*>(cs4);
+        float lo[8], hi[8];
+        tile_vals(nn, i0, lo);
+        tile_vals(nn, 64 + i0, hi);
         __align__(16) __half a[8], b[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float x1 = round_to<__half>(lo[e]);
           float x2 = round_to<__half>(hi[e]);
           if (kind < 2) {  // q, k: rotate-half RoPE at the sequence's position
-            const float c = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2], sn = Q.rope_cs[((size_t)ps * 64 + i0 + e) * 2 + 1];
+            const float c = csf[2 * e], sn = csf[2 * e + 1];
             const float r1 = __fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, sn));
             const float r2 = __fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, sn));
             x1 = r1;
