@@ -366,12 +366,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
         // 16 rows x 128 columns: thread = (row, 16-column run)
         const int nn = hb + (et >> 3), c0 = (et & 7) * 16;
         const size_t o = (size_t)nn * p.M + t * kTcM + c0;
-        float yv[16];
-        tile_vals(nn, c0, yv);
-        float4 rv[4];
+        float4 rv[4];  // the residual does not depend on the slots: its loads go first
 #pragma unroll
         for (int e = 0; e < 4; ++e)
           rv[e] = p.resid ? __ldcg(reinterpret_cast<const float4*>(p.resid + o) + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float yv[16];
+        tile_vals(nn, c0, yv);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float4 r4 = rv[e];
