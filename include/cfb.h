@@ -62,8 +62,12 @@ enum cfb_flags {
   CFB_PARTIAL = 1 << 8,      /* batch-16 tensor parallel, ranks > 0: residual-epilogue
                                 projections write their partial sum only (the caller's
                                 all-reduce adds the residual once, from rank 0) */
-  CFB_DYN_POOL = 1 << 10     /* fused FFN, batch 1: the last ~4 gate/up tiles per CTA are
+  CFB_DYN_POOL = 1 << 10,    /* fused FFN, batch 1: the last ~4 gate/up tiles per CTA are
                                 work-stolen from a pool; barrier must then hold 2 u64 */
+  CFB_TC_PAIR = 1 << 11      /* batched tcgen05 projections: CTA pairs (cluster 2) work on
+                                two row-adjacent tiles over the same K-blocks and fetch each
+                                activation block once, by TMA multicast (even tile counts;
+                                odd ones fall back to single CTAs) */
 };
 
 /* DSMEM traffic counter slots (stage names of analysis.py:212-237) */

@@ -18,7 +18,7 @@ LIB_PATH = Path(__file__).resolve().parent / "libcfb.so"
 
 CFB_F16, CFB_F32 = 2, 4
 APPEND, WRITE_KV, ROPE, NORM, RESID, STATS_MERGED, PDL, ONESHOT = 1, 2, 4, 8, 16, 32, 64, 128
-PARTIAL, DYN_POOL = 256, 1024
+PARTIAL, DYN_POOL, TC_PAIR = 256, 1024, 2048
 STAGE_NAMES = ("qkv_gather", "stats_max_reduce", "stats_sum_reduce", "stats_merge_reduce",
                "attn_out_reduce", "q_proj_gather", "latent_kv_gather", "absorbed_q_gather",
                "down_proj_reduce", "score_reduce", "out_proj_reduce")

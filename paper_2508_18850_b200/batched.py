@@ -56,6 +56,11 @@ def pack_layer_b16(lp: dict, dev):
 PAGE = 128  # CFB_KV_PAGE: positions per KV page (= one attention chunk)
 
 
+# batched projections on CTA pairs sharing each activation block by TMA
+# multicast (CFB_TC_PAIR); False = one CTA per run
+TC_PAIR = False
+
+
 class PagedKVPool:
     """Paged KV caches for the n_seq (16 or 32) sequences: per layer a K and a V page pool
     [n_pages][n_heads][128][128] fp16 and one shared block table [n_seq][max_pages]
@@ -188,6 +193,7 @@ class BatchedLlama:
         self.stream = torch.cuda.Stream(device=dev)
         self.graph = None
         self.pool = pool
+        self.tc_pair = TC_PAIR
         torch.cuda.synchronize()
 
     # ---------------------------------------------------------------- builders
@@ -284,7 +290,8 @@ class BatchedLlama:
         cfg, w = self.cfg, self.ws
         return _native.B16LayerArgs(
             hidden=cfg.hidden, n_heads=cfg.n_heads, inter=cfg.inter, cache_cap=self.cap,
-            max_len=self.max_len, flags=_native.PDL | (_native.PARTIAL if partial else 0), stage=stage,
+            max_len=self.max_len, flags=_native.PDL | (_native.PARTIAL if partial else 0) | (_native.TC_PAIR if self.tc_pair else 0),
+            stage=stage,
             eps=cfg.eps, resid=self.resid.data_ptr(),
             attn_norm=L["attn_norm"].data_ptr(), ffn_norm=L["ffn_norm"].data_ptr(),
             w_qkv=L["w_qkv"].data_ptr(), w_o=L["w_o"].data_ptr(), w_gu=L["w_gu"].data_ptr(),

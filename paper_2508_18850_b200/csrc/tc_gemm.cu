@@ -27,6 +27,9 @@
 //                   finishing epilogue: SwiGLU + pack for the next projection,
 //                   residual add, or RoPE + per-sequence KV-cache append
 //
+// CFB_TC_PAIR runs the same schedule on CTA pairs (cluster 2) that share each
+// activation block by TMA multicast (tc_gemm_kernel<2>).
+//
 // Packed layouts (fp16), "core matrix" = 8 rows x 16 bytes (8 K elements):
 //   W block (tile t, kb): [s = k-step (4)][c = K half (2)][g = row group (16)][8 rows][8]
 //   X block (kb):         [s (4)][c (2)][g = batch group (2)][8 rows][8]
@@ -108,6 +111,23 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
                    smem_u32(bar))
                : "memory");
 }
+// arrive on the barrier at the same offset in every CTA of `mask` once the MMAs complete
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+// global -> the same shared offset in every CTA of `mask`, completing on each one's barrier
+__device__ __forceinline__ void bulk_g2s_mc(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                            uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+      " [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+      : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -139,6 +159,12 @@ __device__ __forceinline__ void tc_tile_sum(const float* tslot, int contrib, int
   }
 }
 
+// kC = 1: one CTA per run.  kC = 2 (CTA pairs, cluster 2): a pair works on
+// two row-adjacent tiles over the SAME K-block run, so each activation block
+// is fetched once per pair - each CTA multicasts half of it into both CTAs'
+// ring slots - and a ring stage is refilled only once both CTAs' MMAs have
+// released it (multicast tcgen05.commit onto both empty barriers).
+template <int kC>
 __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p) {
   extern __shared__ __align__(1024) char smem[];
   char* sa = smem;                                   // [S][16 KB]
@@ -150,18 +176,21 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   uint64_t* acce = accf + 2;           // [2] accumulator drained
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acce + 2);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int G = gridDim.x, i = blockIdx.x;
-  // CTA i owns weight blocks [b0, b1) of the (tile-major, K-minor) sequence: an
-  // even split at 16 KB granularity; a "segment" is its run inside one tile,
-  // accumulated in TMEM and flushed once (split-K only at tile boundaries)
-  const int KBt = p.K / kTcKB, TB = (p.M / kTcM) * KBt;
+  // unit of work = a CTA group (kC CTAs: a cluster) = cluster ci, rank cr
+  const int G = gridDim.x / kC, i = blockIdx.x / kC, cr = blockIdx.x % kC;
+  // group i owns blocks [b0, b1) of the (tile-group-major, K-minor) sequence
+  // of kC x 16 KB blocks: an even split; a "segment" is its run inside one
+  // tile group, accumulated in TMEM and flushed once (split-K only at tile
+  // boundaries).  CTA cr of the group works on tile (group * kC + cr).
+  const int KBt = p.K / kTcKB, TB = (p.M / kTcM / kC) * KBt;
   const int b0 = (int)((long long)i * TB / G), b1 = (int)((long long)(i + 1) * TB / G);
   const int nseg = b1 > b0 ? (b1 - 1) / KBt - b0 / KBt + 1 : 0;
+  constexpr uint16_t kMask = (uint16_t)((1u << kC) - 1u);
 
   if (tid == 0) {
     for (int s = 0; s < kTcStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], kC);  // every CTA of the group releases the stage
     }
     mbar_init(&accf[0], 1);
     mbar_init(&accf[1], 1);
@@ -179,6 +208,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if constexpr (kC > 1) {  // the peer's barriers are initialised before anything lands on them
+    cluster_arrive();
+    cluster_wait();
+  }
   pdl_launch_dependents();
 
   auto unit_kb = [&](int u, int& t, int& kb0, int& nkb) {  // segment u of this CTA
@@ -191,26 +224,41 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   if (warp == 0) {  // ------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      // blocks b0 .. b1 in order (tile-major, K-minor).  Weights do not depend
+      // blocks b0 .. b1 in order (group-major, K-minor).  Weights do not depend
       // on the previous kernel: the first ring's worth streams before
       // griddepcontrol.wait, overlapping the previous kernel's tail; only the
       // activation blocks wait for it
-      const int nb = b1 - b0, pre = min(nb, kTcStages);
+      auto wblk = [&](int b) {  // this CTA's weight block of group block b
+        return p.w + ((size_t)((b / KBt) * kC + cr) * KBt + b % KBt) * (kTcABytes / 2);
+      };
+      const int xs = xbytes / kC;  // this CTA's slice of each activation block
+      auto xload = [&](int s, int b) {
+        if constexpr (kC == 1) {
+          bulk_g2s(sb + s * kTcBBytesMax, p.x + (size_t)(b % KBt) * (xbytes / 2), xbytes, &full[s],
+                   policy_evict_last());
+        } else {
+          bulk_g2s_mc(sb + s * kTcBBytesMax + cr * xs, p.x + (size_t)(b % KBt) * (xbytes / 2) + cr * (xs / 2), xs,
+                      &full[s], kMask, policy_evict_last());
+        }
+      };
+      const int n = b1 - b0, pre = min(n, kTcStages);
       for (int it = 0; it < pre; ++it) {
         mbar_arrive_expect_tx(&full[it], kTcABytes + xbytes);
-        bulk_g2s(sa + it * kTcABytes, p.w + (size_t)(b0 + it) * (kTcABytes / 2), kTcABytes, &full[it], pol);
+        bulk_g2s(sa + it * kTcABytes, wblk(b0 + it), kTcABytes, &full[it], pol);
       }
       pdl_wait();
-      for (int it = 0; it < pre; ++it)
-        bulk_g2s(sb + it * kTcBBytesMax, p.x + (size_t)((b0 + it) % KBt) * (xbytes / 2), xbytes, &full[it],
-                 policy_evict_last());
-      for (int it = pre; it < nb; ++it) {
+      for (int it = 0; it < pre; ++it) xload(it, b0 + it);
+      for (int it = pre; it < n; ++it) {
         const int s = it % kTcStages, b = b0 + it;
         mbar_wait(&empty[s], ((it / kTcStages) - 1) & 1);
         mbar_arrive_expect_tx(&full[s], kTcABytes + xbytes);
-        bulk_g2s(sa + s * kTcABytes, p.w + (size_t)b * (kTcABytes / 2), kTcABytes, &full[s], pol);
-        bulk_g2s(sb + s * kTcBBytesMax, p.x + (size_t)(b % KBt) * (xbytes / 2), xbytes, &full[s],
-                 policy_evict_last());
+        bulk_g2s(sa + s * kTcABytes, wblk(b), kTcABytes, &full[s], pol);
+        xload(s, b);
+      }
+      if constexpr (kC > 1) {
+        // drain: every peer's final release of our stages has arrived before
+        // this CTA may exit (their MMAs arrive on our empty barriers)
+        for (int it = max(n - kTcStages, 0); it < n; ++it) mbar_wait(&empty[it % kTcStages], (it / kTcStages) & 1);
       }
     }
   } else if (warp == 1) {  // ------------------------------------------ MMA issuer
@@ -234,7 +282,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
           for (int ks = 0; ks < 4; ++ks)  // X: k-step stride nb*32 B, K halves nb*16 B apart
             tc_mma(dt, umma_desc(abase + ks * 4096, 2048, 128),
                    umma_desc(bbase + ks * (nb * 32), (uint32_t)(nb * 16), 128), idesc, (kb | ks) ? 1u : 0u);
-          tc_commit(&empty[s]);  // stage free once these MMAs have read it
+          if constexpr (kC == 1)
+            tc_commit(&empty[s]);  // stage free once these MMAs have read it
+          else
+            tc_commit_mc(&empty[s], kMask);  // ... in both CTAs of the pair (each refills half of X)
         }
         tc_commit(&accf[a]);      // accumulator complete
       }
@@ -243,8 +294,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     int n = 0;
     for (int u = 0; u < nseg; ++u, ++n) {
-      int t, kb0, nkb;
-      unit_kb(u, t, kb0, nkb);
+      int g, kb0, nkb;
+      unit_kb(u, g, kb0, nkb);
+      const int t = g * kC + cr;  // this CTA's tile of group g
       const int a = n & 1;
       mbar_wait(&accf[a], (n >> 1) & 1);
       tc_fence_after();
@@ -273,8 +325,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       // finishing modes: this contributor's partial tile -> its own slot (plain,
       // coalesced stores: lanes = consecutive rows), summed by the finisher in
       // contributor order - deterministic, and no atomics on the critical tail
+      // contributors of tile t = the groups whose runs cross tile group g
       auto cta_of = [&](long long b) { return (int)(((b + 1) * G - 1) / TB); };
-      const int first = cta_of((long long)t * KBt);
+      const int first = cta_of((long long)g * KBt);
       float* myslot = p.slots + ((size_t)t * p.maxc + (i - first)) * (size_t)(nb * kTcM);
 #pragma unroll
       for (int c = 0; c < kTcNMax; ++c)
@@ -283,7 +336,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
       __threadfence();
       named_bar_sync(2, 128);
       int* flag = reinterpret_cast<int*>(tmem_slot + 1);
-      const int contrib = cta_of((long long)(t + 1) * KBt - 1) - first + 1;
+      const int contrib = cta_of((long long)(g + 1) * KBt - 1) - first + 1;
       if (warp == 2 && lane == 0) {
         const int old = atomicAdd(p.ticket + t, 1);
         *flag = old == contrib - 1;
@@ -385,6 +438,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) tc_gemm_kernel(const TcParams p
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (kC > 1) {  // no CTA leaves while its peer may still multicast into it
+    cluster_arrive();
+    cluster_wait();
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
@@ -415,9 +472,11 @@ __global__ void tc_finish_kernel(unsigned long long* yacc, float* out, const flo
 
 int tc_smem_bytes() { return kTcStages * (kTcABytes + kTcBBytesMax) + (4 * kTcStages + 8) * 8 + 32; }
 
-// contributor slots per tile of the even block split: <= ceil(G / tiles) + 1
-static int tc_maxc(int M, int K, int G) {
-  const int tiles = M / kTcM, TB = tiles * (K / kTcKB);
+// contributor slots per tile of the even split of G CTAs in groups of kC:
+// <= ceil(groups / tile groups) + 1
+static int tc_maxc(int M, int K, int G, int kC = 1) {
+  const int tiles = M / kTcM / kC, TB = tiles * (K / kTcKB);
+  G /= kC;
   if (G > TB) G = TB;
   return (G + tiles - 1) / tiles + 1;
 }
@@ -431,23 +490,29 @@ static int tc_sms() {
 // floats of the finishing modes' partial-slot workspace for one projection
 size_t tc_slots_floats(int M, int K, int nb) {
   if (M < kTcM || K < kTcKB) return 0;
-  return (size_t)(M / kTcM) * tc_maxc(M, K, tc_sms()) * nb * kTcM;
+  int mc = tc_maxc(M, K, tc_sms());
+  if ((M / kTcM) % 2 == 0 && tc_maxc(M, K, tc_sms(), 2) > mc) mc = tc_maxc(M, K, tc_sms(), 2);  // CTA pairs
+  return (size_t)(M / kTcM) * mc * nb * kTcM;
 }
 
 int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M, int K, int grid,
             cudaStream_t st, bool pdl, int mode = kTcAccum, int* ticket = nullptr, __half* act = nullptr,
             float* out = nullptr, const float* resid = nullptr, const TcQkv* qkv = nullptr, int nb = kTcN,
-            float* slots = nullptr) {
+            float* slots = nullptr, int pair = 0) {
   if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "tcgen05 batch must be 16 or 32");
   if (mode != kTcAccum && !slots) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need the slot workspace");
   if (mode != kTcAccum && !ticket) return set_error(CFB_ERR_ARGUMENT, "tc_gemm: finishing modes need a ticket array");
   if (M % kTcM || K % kTcKB) return set_error(CFB_ERR_DIMENSION, "tc_gemm: M %% 128 and K %% 64 must be 0");
-  if (const int rc = configure_kernel((const void*)tc_gemm_kernel, tc_smem_bytes(), false)) return rc;
+  // CTA pairs need an even tile count (a pair = two row-adjacent tiles)
+  const int kC = (pair && (M / kTcM) % 2 == 0) ? 2 : 1;
+  auto kern = kC == 2 ? tc_gemm_kernel<2> : tc_gemm_kernel<1>;
+  if (const int rc = configure_kernel((const void*)kern, tc_smem_bytes(), false)) return rc;
   int dev = 0, sms = 0;
   CFB_CUDA(cudaGetDevice(&dev));
   CFB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   if (grid <= 0 || grid > sms) grid = sms;
-  const int TB = (M / kTcM) * (K / kTcKB);
+  grid = grid / kC * kC;
+  const int TB = (M / kTcM) * (K / kTcKB);  // blocks; a pair takes two at a time
   TcParams p;
   p.w = w;
   p.x = xpacked;
@@ -457,7 +522,7 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   p.mode = mode;
   p.nb = nb;
   p.slots = slots;
-  p.maxc = tc_maxc(M, K, grid);
+  p.maxc = tc_maxc(M, K, grid, kC);
   p.ticket = ticket;
   p.act = act;
   p.out = out;
@@ -471,10 +536,10 @@ int tc_gemm(const __half* w, const __half* xpacked, unsigned long long* y, int M
   cfg.blockDim = dim3(kTcThreads, 1, 1);
   cfg.dynamicSmemBytes = tc_smem_bytes();
   cfg.stream = st;
-  LaunchAttrs at(0, pdl);
+  LaunchAttrs at(kC > 1 ? kC : 0, pdl);
   cfg.attrs = at.a;
   cfg.numAttrs = at.n;
-  CFB_CUDA(cudaLaunchKernelEx(&cfg, tc_gemm_kernel, p));
+  CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
   return CFB_OK;
 }
 
@@ -581,13 +646,14 @@ int ffn_b16(const cfb_ffn_b16_args* a, cudaStream_t st) {
     return rc;
   // gate/up tiles interleave 64 gate + 64 up rows, finished (SwiGLU + pack) by
   // their last contributor; down tiles finished as resid + sum
+  const int pair = (a->flags & CFB_TC_PAIR) ? 1 : 0;
   if ((rc = tc_gemm(static_cast<const __half*>(a->w_gu), static_cast<const __half*>(a->xp), a->gu_acc,
                     2 * F, D, 0, st, true, kTcSwiGLU, a->ticket, static_cast<__half*>(a->ap), nullptr, nullptr,
-                    nullptr, nb, a->slots)))
+                    nullptr, nb, a->slots, pair)))
     return rc;
   return tc_gemm(static_cast<const __half*>(a->w_dn), static_cast<const __half*>(a->ap), a->out_acc, D, F,
                  0, st, true, kTcResidOut, a->ticket + 2 * F / kTcM, nullptr, a->resid,
-                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid, nullptr, nb, a->slots);
+                 (a->flags & CFB_PARTIAL) ? nullptr : a->resid, nullptr, nb, a->slots, pair);
 }
 
 int batch_attention(const __half* q, const __half* kc, const __half* vc, const int* pos, int nh, int cap,
@@ -604,6 +670,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
   if (Ka > D || D % 128 || F % 64 || a->stage < 0 || a->stage > 2)
     return set_error(CFB_ERR_DIMENSION, "b16 layer: n_heads*128 <= hidden, hidden %% 128, inter %% 64");
   const bool pdl = a->flags & CFB_PDL, partial = a->flags & CFB_PARTIAL;
+  const int pair = (a->flags & CFB_TC_PAIR) ? 1 : 0;
   const int nb = a->batch ? a->batch : kTcN;
   if (nb != 16 && nb != 32) return set_error(CFB_ERR_DIMENSION, "batched layer: batch must be 16 or 32");
   const int Mq = 3 * nh * 128;
@@ -625,7 +692,7 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
     if (a->block_table && a->max_pages * 128 < a->max_len)
       return set_error(CFB_ERR_DIMENSION, "b16 layer: max_pages * 128 < max_len");
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_qkv), static_cast<const __half*>(a->xp), a->qkv_acc, Mq, D,
-                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv, nb, a->slots)))
+                      0, st, true, kTcQKV, a->ticket, nullptr, nullptr, nullptr, &qkv, nb, a->slots, pair)))
       return rc;
     if ((rc = batch_attention(static_cast<const __half*>(a->q16), static_cast<const __half*>(a->k_cache),
                               static_cast<const __half*>(a->v_cache), a->pos, nh, a->cache_cap, a->max_len,
@@ -634,14 +701,14 @@ int llama_b16_layer(const cfb_b16_layer_args* a, cudaStream_t st) {
       return rc;
     if ((rc = tc_gemm(static_cast<const __half*>(a->w_o), static_cast<const __half*>(a->xp), a->o_acc, D, Ka, 0,
                       st, true, kTcResidOut, a->ticket + Mq / kTcM, nullptr, a->resid, partial ? nullptr : a->resid,
-                      nullptr, nb, a->slots)))
+                      nullptr, nb, a->slots, pair)))
       return rc;
   }
   if (a->stage == 1) return CFB_OK;
   cfb_ffn_b16_args f = {};
   f.hidden = D;
   f.inter = F;
-  f.flags = CFB_PDL | (partial ? CFB_PARTIAL : 0);
+  f.flags = CFB_PDL | (partial ? CFB_PARTIAL : 0) | (a->flags & CFB_TC_PAIR);
   f.eps = a->eps;
   f.resid = a->resid;
   f.norm_w = a->ffn_norm;
@@ -772,7 +839,8 @@ int cfb_tc_gemm_b16(const void* w_packed, const void* x, void* x_packed, unsigne
   int rc = tc_pack_x(static_cast<const __half*>(x), static_cast<__half*>(x_packed), K, st, pdl);
   if (rc) return rc;
   if ((rc = tc_gemm(static_cast<const __half*>(w_packed), static_cast<const __half*>(x_packed), y_acc,
-                    M, K, 0, st, true)))
+                    M, K, 0, st, true, kTcAccum, nullptr, nullptr, nullptr, nullptr, nullptr, kTcN, nullptr,
+                    (flags & CFB_TC_PAIR) ? 1 : 0)))
     return rc;
   if (!y) return CFB_OK;
   return tc_finish(y_acc, y, resid, 16 * M, st, true);

@@ -41,15 +41,16 @@ class TcProjection:
         self.acc = torch.zeros(BATCH, self.M, device=dev, dtype=torch.int64)
         torch.cuda.synchronize()
 
-    def launch(self, x, y=None, resid=None, pdl=False, stream=None):
-        """x: (16, K) fp16 device tensor; y: (16, M) fp32 or None (sum stays in acc)."""
+    def launch(self, x, y=None, resid=None, pdl=False, stream=None, pair=False):
+        """x: (16, K) fp16 device tensor; y: (16, M) fp32 or None (sum stays in acc);
+        pair: CTA pairs sharing each activation block by TMA multicast."""
         _native.check(_native.lib().cfb_tc_gemm_b16(
             self.wp.data_ptr(), x.data_ptr(), self.xp.data_ptr(), self.acc.data_ptr(),
-            _native.ptr(y), _native.ptr(resid), self.M, self.K, _native.PDL if pdl else 0,
-            _native.stream_ptr(stream)))
+            _native.ptr(y), _native.ptr(resid), self.M, self.K,
+            (_native.PDL if pdl else 0) | (_native.TC_PAIR if pair else 0), _native.stream_ptr(stream)))
 
 
-def run_projection_b16(w, x) -> np.ndarray:
+def run_projection_b16(w, x, pair: bool = False) -> np.ndarray:
     """Host convenience: (M, K) weights, (16, K) activations -> (16, M) fp32."""
     import torch
     dev = _native.require_cuda()
@@ -58,7 +59,7 @@ def run_projection_b16(w, x) -> np.ndarray:
     if xt.shape != (BATCH, proj.K):
         raise DimensionError(f"x must be ({BATCH}, {proj.K})")
     y = torch.empty(BATCH, proj.M, device=dev, dtype=torch.float32)
-    proj.launch(xt, y)
+    proj.launch(xt, y, pair=pair)
     torch.cuda.synchronize()
     return y.cpu().numpy()
 
@@ -96,8 +97,9 @@ class TcFfnB16:
     def weight_bytes(self) -> int:
         return 3 * self.D * self.F * 2 + self.D * 2
 
-    def launch(self, resid, pdl: bool = False, stream=None) -> None:
-        a = _native.FfnB16Args(hidden=self.D, inter=self.F, flags=_native.PDL if pdl else 0,
+    def launch(self, resid, pdl: bool = False, stream=None, pair: bool = False) -> None:
+        a = _native.FfnB16Args(hidden=self.D, inter=self.F,
+                               flags=(_native.PDL if pdl else 0) | (_native.TC_PAIR if pair else 0),
                                eps=self.eps, resid=resid.data_ptr(), norm_w=self.g.data_ptr(),
                                w_gu=self.w_gu.data_ptr(), w_dn=self.w_dn.data_ptr(),
                                xp=self.xp.data_ptr(), gu_acc=self.gu_acc.data_ptr(),

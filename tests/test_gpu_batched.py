@@ -16,7 +16,9 @@ from paper_2508_18850_b200.llama import LlamaConfig, random_llama_params, rope_t
 pytestmark = pytest.mark.gpu
 
 
-def test_batched_layers_match_per_sequence_oracle():
+@pytest.mark.parametrize("pair", [False, True])
+def test_batched_layers_match_per_sequence_oracle(pair):
+    """pair: every projection on CTA pairs sharing activation blocks (CFB_TC_PAIR)."""
     import torch
     cfg = LlamaConfig(n_layers=2, hidden=256, n_heads=2, head_dim=128, inter=384, vocab=64)
     params = random_llama_params(cfg, seed=3, prefill=0)
@@ -27,6 +29,7 @@ def test_batched_layers_match_per_sequence_oracle():
                 lp.f16(rng.standard_normal((cfg.n_heads, s, 128)))) for s in S]
               for _ in range(cfg.n_layers)]
     m = BatchedLlama.from_params(cfg, params["layers"], caches, cache_cap=cap)
+    m.tc_pair = pair
     x = rng.standard_normal((16, cfg.hidden)).astype(np.float32)
     m.resid.copy_(torch.from_numpy(x))
     m.set_positions(S)

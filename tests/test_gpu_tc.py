@@ -64,3 +64,41 @@ def test_tc_ffn_b16_matches_oracle(D, F):
     ref = x + lp.ffn_block(x, g, w1, w2, w3, 1e-5)
     err = float(np.max(np.abs(got - ref)))
     assert err <= 2e-2 and err / float(np.max(np.abs(ref))) <= 1e-2, err
+
+
+@pytest.mark.parametrize("M,K", [(256, 128), (384, 1024), (4096, 4096), (4096, 11008), (22016, 4096)])
+def test_tc_projection_cta_pairs_match_fp32(M, K):
+    """CFB_TC_PAIR: CTA pairs multicast each activation block into both CTAs
+    (odd tile counts, e.g. M = 384, fall back to single CTAs)."""
+    rng = np.random.default_rng(M * 7 + K)
+    w = f16(rng.standard_normal((M, K)) * K ** -0.5)
+    x = f16(rng.standard_normal((16, K)))
+    y = run_projection_b16(w, x, pair=True)
+    ref = x @ w.T
+    err = float(np.max(np.abs(y - ref)))
+    assert err <= 2e-2 and err <= 1e-3 * max(1.0, float(np.max(np.abs(ref)))), (M, K, err)
+
+
+@pytest.mark.parametrize("D,F", [(512, 1408), (4096, 11008)])
+def test_tc_ffn_b16_cta_pairs_match_oracle(D, F):
+    """The batch-16 FFN on CTA pairs (multicast activations) vs the oracle,
+    repeated launches on the same residual stream."""
+    import torch
+    from oracle import llama_port as lp
+    from paper_2508_18850_b200.tc import TcFfnB16
+    rng = np.random.default_rng(D + 1)
+    x = rng.standard_normal((16, D)).astype(np.float32)
+    g = f16(1 + 0.1 * rng.standard_normal(D))
+    w1 = f16(rng.standard_normal((F, D)) * D ** -0.5)
+    w2 = f16(rng.standard_normal((F, D)) * D ** -0.5)
+    w3 = f16(rng.standard_normal((D, F)) * F ** -0.5)
+    ffn = TcFfnB16(w1, w2, w3, g, eps=1e-5)
+    r = torch.from_numpy(x).cuda()
+    ref = x
+    for _ in range(2):
+        ffn.launch(r, pdl=True, pair=True)
+        ref = ref + lp.ffn_block(ref, g, w1, w2, w3, 1e-5)
+    torch.cuda.synchronize()
+    got = r.cpu().numpy()
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= 2e-2 and err / float(np.max(np.abs(ref))) <= 1e-2, err
