@@ -80,6 +80,22 @@ __host__ __device__ inline MlaProjLayout mla_proj_layout(int D, int H, int G, in
   return L;
 }
 
+// Grid barrier whose counter advances by exactly kProjUnit per launch whatever
+// the grid (CTA 0 arrives with the remainder): the projection's grid shrinks
+// at short contexts (host side), and consecutive launches on one workspace
+// may use different grids.
+constexpr unsigned long long kProjUnit = 1ull << 12;
+__device__ __forceinline__ void proj_barrier(unsigned long long* counter, int tid) {
+  consumer_sync();
+  if (tid == 0) {
+    __threadfence();
+    const unsigned long long inc = blockIdx.x == 0 ? kProjUnit - (gridDim.x - 1) : 1ull;
+    const unsigned long long old = atomicAdd(counter, inc);
+    spin_until_geq(counter, (old / kProjUnit + 1) * kProjUnit);
+  }
+  consumer_sync();
+}
+
 __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParams p) {
   extern __shared__ __align__(128) char smem[];
   const int D = p.D, H = p.H, R = p.R, G = gridDim.x, i = blockIdx.x;
@@ -132,7 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_proj_kernel(const MlaEngParam
                                       p.qc[4 * a0 + row] = __float2half_rn(v);
                                     });
   mla_stamp(p, 2, tid);
-  grid_barrier(p.barrier, tid);
+  proj_barrier(p.barrier, tid);
   mla_stamp(p, 3, tid);
   for (int t = tid; t < NH * H / 8; t += kConsumerThreads)
     reinterpret_cast<uint4*>(qs)[t] = __ldcg(reinterpret_cast<const uint4*>(p.qc) + t);
@@ -622,11 +638,14 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   const bool pdl = a->flags & CFB_PDL;
   int spw = tuned_spw();
   const int G = sms;
-  while (spw > 1 && (mla_proj_layout(p.D, p.H, G, spw).total > kMaxSmem ||
+  // short contexts: the projection leaves the attention CTAs their own SMs, so
+  // they are resident (streaming their cache rows) before the projection ends
+  const int Gp = (G2 <= 72 && sms - G2 >= 64) ? sms - G2 : sms;
+  while (spw > 1 && (mla_proj_layout(p.D, p.H, Gp, spw).total > kMaxSmem ||
                      mla_out_layout(p.D, p.H, G, spw).total > kMaxSmem))
     --spw;
   p.spw = spw;
-  int rc = launch_k(mla_proj_kernel, G, kThreads, mla_proj_layout(p.D, p.H, G, spw).total, pdl, p, st);
+  int rc = launch_k(mla_proj_kernel, Gp, kThreads, mla_proj_layout(p.D, p.H, Gp, spw).total, pdl, p, st);
   if (rc) return rc;
   if ((rc = launch_k(mla_attn_kernel, G2, kAttnThreads, kAttnSmem, true, p, st))) return rc;
   return launch_k(mla_out_kernel, G, kThreads, mla_out_layout(p.D, p.H, G, spw).total, true, p, st);
