@@ -56,8 +56,10 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   uint64_t* bar = reinterpret_cast<uint64_t*>(pv + 8 * 128);
   __shared__ float red[8];
   __shared__ int last;
-  pdl_wait();
-  pdl_launch_dependents();
+  // pos and the block table are set before the step (stable across its
+  // kernels), and cache rows other than the new one were written by earlier
+  // steps: the first chunk streams before griddepcontrol.wait unless it holds
+  // the row the QKV projection is appending
   const int pair = blockIdx.y, n = pair / nh, h = pair % nh, cb = blockIdx.x * kCpc;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int L = pos[n] + 1;
@@ -74,7 +76,7 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
     return (((size_t)n * nh + h) * cap + (size_t)c * kBaChunk) * 128;
   };
   const uint64_t pol = policy_evict_first();
-  if (tid == 0) {
+  auto issue_first = [&]() {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_mbar_init();
@@ -84,7 +86,12 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
     bulk_g2s(ks, kc + b0, r0 * 256, &bar[0], pol);
     mbar_arrive_expect_tx(&bar[1], r0 * 256);
     bulk_g2s(vs, vc + b0, r0 * 256, &bar[1], pol);
-  }
+  };
+  const bool early = (cb + 1) * kBaChunk < L;  // the first chunk ends before the new row L - 1
+  if (tid == 0 && early) issue_first();
+  pdl_wait();
+  pdl_launch_dependents();
+  if (tid == 0 && !early) issue_first();
   qs[tid] = __half2float(q[(size_t)n * nh * 128 + h * 128 + tid]);
   __syncthreads();
   const int hl = lane & 15, ro = lane >> 4;
