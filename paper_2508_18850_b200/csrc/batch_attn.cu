@@ -60,14 +60,17 @@ __global__ void __launch_bounds__(kBaThreads) batch_attn_kernel(const __half* q,
   // kernels), and cache rows other than the new one were written by earlier
   // steps: the first chunk streams before griddepcontrol.wait unless it holds
   // the row the QKV projection is appending
-  const int pair = blockIdx.y, n = pair / nh, h = pair % nh, cb = blockIdx.x * kCpc;
+  const int pair = blockIdx.y, n = pair / nh, h = pair % nh;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int L = pos[n] + 1;
-  if (cb * kBaChunk >= L) return;  // beyond this sequence: not part of its merge
   // nused <= the launched chunks even for a position past max_len (the host
   // rejects that; the clamp keeps the merge ticket consistent regardless)
   const int nused = min((L + kBaChunk - 1) / kBaChunk, nchunks);
-  const int nparts = (nused + kCpc - 1) / kCpc, nj = min(kCpc, nused - cb);
+  // this sequence's chunks split evenly over nparts = ceil(nused / cpc) CTAs
+  const int nparts = (nused + kCpc - 1) / kCpc;
+  if ((int)blockIdx.x >= nparts) return;  // beyond this sequence: not part of its merge
+  const int cb = (int)((long long)blockIdx.x * nused / nparts);
+  const int nj = (int)((long long)(blockIdx.x + 1) * nused / nparts) - cb;
   auto rows_of = [&](int c) { return min(L, (c + 1) * kBaChunk) - c * kBaChunk; };
   // paged: chunk c of a sequence is exactly its page c (CFB_KV_PAGE == kBaChunk);
   // an unassigned entry (-1) reads page 0 instead of faulting (host-validated)
