@@ -631,6 +631,7 @@ int mla_engine_decode(const cfb_mla_engine_args* a, cudaStream_t st) {
   p.trace = a->trace;
   const int T = a->seq_len + 1;
   int G2 = (T + 63) / 64;
+  if (G2 <= 20) G2 = (T + 31) / 32;  // short contexts: 32-row CTAs, the attention is latency-bound
   if (G2 > sms) G2 = sms;
   if (a->max_parts > 0 && G2 > a->max_parts) G2 = a->max_parts;
   if (G2 > 160) G2 = 160;  // mla_out_kernel's merge holds <= 5 partials per lane
