@@ -189,7 +189,7 @@ def run_ours(args, rank, world):
         from paper_2508_18850_b200.tp_fused import FusedTPLlama
         ok = 1
         try:
-            tp = FusedTPLlama(cfg, rank, world, cap, seed=1234)
+            tp = FusedTPLlama(cfg, rank, world, cap, seed=1234, nvls=args.tp_allreduce == "nvls")
             tp.set_state(ctxs[0], 1)
             tp.step()
             torch.cuda.synchronize()
@@ -300,6 +300,8 @@ def run_ours(args, rank, world):
             "phases": [trace_phases(model, c) for c in (ctxs[0], ctxs[-1])]}
     line["gpu_launches"] = launches
     line["clocks"] = clocks
+    if world > 1 and args.tp_impl == "fused":
+        line["tp_allreduce"] = args.tp_allreduce
     if fused_error:  # pragma: no cover - multi-GPU only
         line["tp_fused_error"] = fused_error
     if world == 1 and not args.no_deepseek:
@@ -838,6 +840,9 @@ def main():
                     choices=["persistent", "layered", "persistent_flat", "persistent_nodsmem"])
     ap.add_argument("--tp-impl", default="fused", choices=["fused", "nccl"],
                     help="N>1: in-kernel all-reduce over peer memory (fused) or NCCL between launches")
+    ap.add_argument("--tp-allreduce", default="peer", choices=["peer", "nvls"],
+                    help="fused TP: sums pushed to every peer (peer) or one multimem.red on an NVLS "
+                         "multicast buffer (nvls)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -538,6 +538,31 @@ int cfb_llama_enqueue(cfb_llama* m, int part, int layer, void* stream);
 int cfb_llama_set_tp_fused(cfb_llama* m, int rank, int size, int vocab_offset, void* const* xch_peers,
                            int emulated, int grid, long long timeout_ns);
 size_t cfb_tp_xch_bytes(int hidden);
+/* NVLS (NVLink SHARP multicast) for the fused all-reduce (SURVEY 8(e) next
+ * step): uc_sum / mc_sum are the unicast and multicast mappings of this rank's
+ * copy of a multicast buffer of >= cfb_tp_nvls_bytes(hidden) bytes (zeroed).
+ * The step kernel then adds each sum slice ONCE with multimem.red.add.u64 on
+ * mc_sum (the switch updates every rank's copy) instead of once per peer, and
+ * reads / re-zeroes uc_sum; barriers and the argmax stay on the exchange
+ * blocks.  NULL, NULL = the peer-memory pushes.  Call after
+ * cfb_llama_set_tp_fused. */
+int cfb_llama_set_tp_nvls(cfb_llama* m, void* uc_sum, void* mc_sum);
+size_t cfb_tp_nvls_bytes(int hidden);
+/* Multicast objects (one physical copy per member GPU; nvls.cu):
+ * creator: cfb_nvls_create(bytes, ndev) [+ cfb_nvls_export_fd]; other members:
+ * cfb_nvls_import_fd(creator pid, fd, bytes, ndev) (pidfd_getfd); then every
+ * member cfb_nvls_add_device (all of them before any bind) and
+ * cfb_nvls_bind(device) -> unicast / multicast mappings of its zeroed copy.
+ * An emulated group on one GPU: ndev 1, the ranks share the mappings. */
+typedef struct cfb_nvls cfb_nvls;
+int cfb_nvls_supported(int device, int* supported);
+int cfb_nvls_create(size_t bytes, int ndev, cfb_nvls** out);
+int cfb_nvls_export_fd(cfb_nvls* h, int* fd);
+int cfb_nvls_import_fd(int pid, int fd, size_t bytes, int ndev, cfb_nvls** out);
+int cfb_nvls_add_device(cfb_nvls* h, int device);
+int cfb_nvls_bind(cfb_nvls* h, int device, void** uc, void** mc);
+size_t cfb_nvls_size(const cfb_nvls* h);
+int cfb_nvls_destroy(cfb_nvls* h);
 /* Engine options (set before cfb_llama_capture; a captured graph keeps the
  * values it was captured with). */
 enum cfb_llama_option {

@@ -96,6 +96,8 @@ struct LlamaStepArgs {
   unsigned long long* const* xch;  // DEVICE array [tp_size] of the ranks' exchange blocks
                                    // (tp_xch_bytes(hidden) each, zeroed), as this device sees them
   float* resid2;                 // [D] second residual buffer (layer-parity rotation)
+  unsigned long long* uc_sum;    // NVLS: this rank's copy of the [6][D] sums (or null)
+  unsigned long long* mc_sum;    // NVLS: its multicast mapping (multimem.red target)
   long long timeout_ns;          // cross-rank wait bound (err = 2 on expiry), 0 = none
   int l2_prefetch;               // bytes/CTA prefetched into L2 past the ring at each barrier
   int ring_spw;                  // ring slots per consumer warp (8 KB each); 0 = the deepest that fits

@@ -96,6 +96,8 @@ struct StepParams {
   int T, trank, voff;
   unsigned long long* const* xch;  // [T] exchange blocks (peer-mapped)
   float* resid2;
+  unsigned long long* uc_sum;  // NVLS: this rank's copy of the sums [6][D] (else null)
+  unsigned long long* mc_sum;  // NVLS: multicast mapping of the same buffer
   long long timeout_ns;
   int l2_prefetch;               // bytes per CTA prefetched into L2 past the ring at each barrier
 };
@@ -136,6 +138,19 @@ __device__ __forceinline__ void red_max_u64(unsigned long long* p, unsigned long
 }
 __device__ __forceinline__ void red_add_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+// NVLS: one reduction on the multicast address updates every rank's copy
+__device__ __forceinline__ void multimem_red_add_u64(unsigned long long* mc, unsigned long long v) {
+  asm volatile("multimem.red.relaxed.sys.global.add.u64 [%0], %1;" ::"l"(mc), "l"(v) : "memory");
+}
+// this slice element of the layer's sum to every rank: one multicast
+// reduction (NVLS) or one peer-memory reduction per rank
+__device__ __forceinline__ void tp_push(const StepParams& p, int set, int c, unsigned long long v) {
+  if (p.mc_sum) {
+    multimem_red_add_u64(p.mc_sum + (size_t)set * p.D + c, v);
+  } else {
+    for (int t = 0; t < p.T; ++t) red_add_u64(p.xch[t] + (size_t)set * p.D + c, v);
+  }
 }
 
 // spin (thread 0) until *ctr >= target; on expiry of the bound set err = 2
@@ -577,7 +592,8 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   // embed: resid[c] = embed[token][c] for this CTA's slice; counters reset
   const bool tp = p.T > 1;
   const int c0 = (int)split_at(D, i, G), c1 = (int)split_at(D, i + 1, G);  // this CTA's D slice
-  unsigned long long* xown = tp ? p.xch[p.trank] : nullptr;
+  // this rank's sums: its NVLS copy, or its own exchange block
+  unsigned long long* xown = tp ? (p.uc_sum ? p.uc_sum : p.xch[p.trank]) : nullptr;
   {
     const int tok = *p.token;
     for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
@@ -919,7 +935,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     if (tp) {  // attention all-reduce: this CTA's slice of the local head sum to every rank
       for (int c = c0 + tid; c < c1; c += kConsumerThreads) {
         const unsigned long long v = __ldcg(accA + c);
-        for (int t = 0; t < p.T; ++t) red_add_u64(tp_xa(p.xch[t], D, l % 3) + c, v);
+        tp_push(p, l % 3, c, v);  // tp_xa set l % 3
         accA[c] = 0ull;
       }
       cross_sync(p, x_target += TG, tid);
@@ -1001,8 +1017,7 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
                                         if (tp) {  // FFN all-reduce: partial column sums to every rank
                                           const unsigned long long q =
                                               (unsigned long long)__float2ll_rn(v * 4294967296.0f);
-                                          for (int t = 0; t < p.T; ++t)
-                                            red_add_u64(tp_xf(p.xch[t], D, l % 3) + c, q);
+                                          tp_push(p, 3 + l % 3, c, q);  // tp_xf set l % 3
                                           return;
                                         }
                                         const float r = __fadd_rn(__ldcg(p.resid + c),
@@ -1251,6 +1266,8 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.voff = a->vocab_offset;
   p.xch = a->xch;
   p.resid2 = a->resid2;
+  p.uc_sum = a->uc_sum;
+  p.mc_sum = a->mc_sum;
   p.timeout_ns = a->timeout_ns;
   p.l2_prefetch = a->l2_prefetch;
   if (p.T > 1 && (!p.xch || !p.resid2 || p.trank < 0 || p.trank >= p.T))

@@ -50,6 +50,8 @@ struct cfb_llama {
   long long timeout_ns = 0;
   unsigned long long** xch_dev = nullptr;  // [tp_size] exchange blocks as this device sees them
   float* resid2 = nullptr;
+  unsigned long long* uc_sum = nullptr;  // NVLS sums (cfb_llama_set_tp_nvls) or null
+  unsigned long long* mc_sum = nullptr;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
 };
@@ -236,6 +238,8 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
     a.emulated = m->emulated || m->plain_launch;
     a.xch = m->xch_dev;
     a.resid2 = m->resid2;
+    a.uc_sum = m->uc_sum;
+    a.mc_sum = m->mc_sum;
     a.timeout_ns = m->timeout_ns;
   }
   return cfb::llama_step_launch(&a, st);
@@ -501,6 +505,18 @@ int cfb_llama_set_tp_fused(cfb_llama* m, int rank, int size, int vocab_offset, v
 }
 
 size_t cfb_tp_xch_bytes(int hidden) { return cfb::tp_xch_bytes(hidden); }
+
+size_t cfb_tp_nvls_bytes(int hidden) { return (size_t)6 * hidden * sizeof(unsigned long long); }
+
+int cfb_llama_set_tp_nvls(cfb_llama* m, void* uc_sum, void* mc_sum) {
+  using cfb::set_error;
+  if (!m) return set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (!m->tp_fused) return set_error(CFB_ERR_ARGUMENT, "NVLS sums need cfb_llama_set_tp_fused first");
+  if ((uc_sum == nullptr) != (mc_sum == nullptr)) return set_error(CFB_ERR_ARGUMENT, "uc_sum and mc_sum go together");
+  m->uc_sum = static_cast<unsigned long long*>(uc_sum);
+  m->mc_sum = static_cast<unsigned long long*>(mc_sum);
+  return CFB_OK;
+}
 
 int cfb_llama_set_option(cfb_llama* m, int option, long long value) {
   if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");

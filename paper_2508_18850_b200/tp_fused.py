@@ -17,6 +17,13 @@ Peers' exchange blocks are mapped with CUDA IPC (``cfb_ipc_alloc`` /
 group.  ``emulated_ranks`` builds all T ranks inside one process on one GPU
 (each on its own stream and a 1/T share of the SMs, peers' blocks addressed
 directly): the same kernel code and protocol, used by the single-GPU tests.
+
+``nvls=True`` moves the two sums onto an NVLink SHARP multicast buffer
+(``NvlsSums``, csrc/nvls.cu): each slice element is added ONCE with
+``multimem.red.add.u64`` on the multicast address - the switch updates every
+rank's copy - instead of once per peer; barriers and the argmax stay on the
+exchange blocks.  Emulated on one GPU the ranks share one copy (a multicast
+object with one member), which is the same sum.
 """
 
 from __future__ import annotations
@@ -44,7 +51,102 @@ def _bind(L):
     L.cfb_ipc_open.argtypes = [_vp, ctypes.POINTER(_vp)]
     L.cfb_ipc_close.argtypes = [_vp]
     L.cfb_dev_free.argtypes = [_vp]
+    L.cfb_llama_set_tp_nvls.argtypes = [_vp, _vp, _vp]
+    L.cfb_tp_nvls_bytes.argtypes = [ctypes.c_int]
+    L.cfb_tp_nvls_bytes.restype = ctypes.c_size_t
+    L.cfb_nvls_supported.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+    L.cfb_nvls_create.argtypes = [ctypes.c_size_t, ctypes.c_int, ctypes.POINTER(_vp)]
+    L.cfb_nvls_export_fd.argtypes = [_vp, ctypes.POINTER(ctypes.c_int)]
+    L.cfb_nvls_import_fd.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_size_t, ctypes.c_int,
+                                     ctypes.POINTER(_vp)]
+    L.cfb_nvls_add_device.argtypes = [_vp, ctypes.c_int]
+    L.cfb_nvls_bind.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_vp), ctypes.POINTER(_vp)]
+    L.cfb_nvls_size.argtypes = [_vp]
+    L.cfb_nvls_size.restype = ctypes.c_size_t
+    L.cfb_nvls_destroy.argtypes = [_vp]
     return L
+
+
+def nvls_supported(device: int = 0) -> bool:
+    """Whether the GPU can take part in NVLS multicast (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED)."""
+    L = _bind(_native.lib())
+    v = ctypes.c_int(0)
+    _native.check(L.cfb_nvls_supported(device, ctypes.byref(v)))
+    return bool(v.value)
+
+
+def nvls_usable(device: int = 0) -> bool:
+    """Whether a multicast object can actually be created here (the attribute
+    can be set on a GPU whose fabric slice still refuses cuMulticastCreate,
+    e.g. a single GPU handed to a container)."""
+    if not nvls_supported(device):
+        return False
+    L = _bind(_native.lib())
+    h = _vp()
+    if L.cfb_nvls_create(int(L.cfb_tp_nvls_bytes(4096)), 1, ctypes.byref(h)) != 0:
+        return False
+    L.cfb_nvls_destroy(h)
+    return True
+
+
+class NvlsSums:
+    """This rank's copy of a multicast buffer for the fused all-reduce sums:
+    ``uc`` (unicast: reads, re-zeroing) and ``mc`` (multicast: multimem.red).
+
+    Single process (``group=None``): a multicast object with one member - the
+    emulated ranks share it.  Multi-process: rank 0 creates the object and
+    exports a file descriptor, the others import it from rank 0's process
+    (pidfd_getfd), every rank adds its device, and after a group barrier binds
+    its own zeroed copy."""
+
+    def __init__(self, hidden: int, device: int, *, world: int = 1, rank: int = 0, group=None):
+        L = _bind(_native.lib())
+        self._L = L
+        self.h = _vp()
+        self.uc, self.mc = _vp(), _vp()
+        nbytes = int(L.cfb_tp_nvls_bytes(hidden))
+        if group is None:
+            _native.check(L.cfb_nvls_create(nbytes, 1, ctypes.byref(self.h)))
+            _native.check(L.cfb_nvls_add_device(self.h, device))
+            _native.check(L.cfb_nvls_bind(self.h, device, ctypes.byref(self.uc), ctypes.byref(self.mc)))
+            return
+        import os
+        import torch.distributed as dist
+
+        def agree(status, what, payload=None):
+            # every rank learns every rank's status before anyone goes on, so a
+            # failure anywhere raises everywhere instead of leaving peers in a barrier
+            got = [None] * world
+            dist.all_gather_object(got, (status, payload), group=group)
+            bad = [r for r, (st, _) in enumerate(got) if st != 0]
+            if bad:
+                raise RuntimeError(f"NVLS {what} failed on ranks {bad}: {_native.lib().cfb_last_error()!r}")
+            return got
+
+        st, mine = 0, None
+        if rank == 0:
+            st = L.cfb_nvls_create(nbytes, world, ctypes.byref(self.h))
+            fd = ctypes.c_int(-1)
+            if st == 0:
+                st = L.cfb_nvls_export_fd(self.h, ctypes.byref(fd))
+            mine = (os.getpid(), fd.value)
+        got = agree(st, "create/export", mine)
+        st = 0
+        if rank != 0:
+            pid, fd = got[0][1]
+            st = L.cfb_nvls_import_fd(pid, fd, nbytes, world, ctypes.byref(self.h))
+        agree(st, "import")
+        if rank == 0 and mine[1] >= 0:
+            os.close(mine[1])  # every member holds its own reference now
+        agree(L.cfb_nvls_add_device(self.h, device), "add_device")  # all adds before any bind
+        agree(L.cfb_nvls_bind(self.h, device, ctypes.byref(self.uc), ctypes.byref(self.mc)), "bind")
+
+    def __del__(self):
+        if getattr(self, "h", None) and self.h.value:
+            try:
+                self._L.cfb_nvls_destroy(self.h)
+            except Exception:
+                pass
 
 
 def fused_local_config(cfg: LlamaConfig, world: int, cluster: int | None = None) -> LlamaConfig:
@@ -100,7 +202,7 @@ class FusedTPLlama:
 
     def __init__(self, cfg: LlamaConfig, rank: int, world: int, cache_cap: int, *, params=None,
                  seed: int = 0, group=None, peers=None, emulated: bool = False, grid: int = 0,
-                 timeout_s: float = 10.0):
+                 timeout_s: float = 10.0, nvls: bool = False):
         if world < 2:
             raise DimensionError("fused tensor parallel needs at least 2 ranks")
         self.cfg, self.rank, self.world = cfg, rank, world
@@ -128,7 +230,18 @@ class FusedTPLlama:
                 self._opened.append(p)
                 ptrs.append(p.value)
             self._attach(ptrs, emulated=False, grid=grid, timeout_s=timeout_s)
+            if nvls:
+                import torch
+                self.nvls = NvlsSums(cfg.hidden, torch.cuda.current_device(), world=world, rank=rank,
+                                     group=group)
+                self.use_nvls(self.nvls)
         self._pending = (emulated, grid, timeout_s)
+
+    def use_nvls(self, sums) -> None:
+        """Route the sums through `sums` (an ``NvlsSums``) or back to the
+        peer-memory pushes (None)."""
+        _native.check(self._L.cfb_llama_set_tp_nvls(self.eng._h, sums.uc if sums else None,
+                                                    sums.mc if sums else None))
 
     def _attach(self, ptrs, emulated, grid, timeout_s):
         arr = (_vp * self.world)(*ptrs)
@@ -230,11 +343,17 @@ def emulated_grid(cfg: LlamaConfig, world: int) -> int:
 
 
 def emulated_ranks(cfg: LlamaConfig, world: int, cache_cap: int, *, params=None, seed: int = 0,
-                   timeout_s: float = 10.0) -> EmulatedTP:
+                   timeout_s: float = 10.0, nvls: bool = False) -> EmulatedTP:
     grid = emulated_grid(cfg, world)
     ranks = [FusedTPLlama(cfg, r, world, cache_cap, params=params, seed=seed, peers=True,
                           emulated=True, grid=grid, timeout_s=timeout_s) for r in range(world)]
     ptrs = [r.xch.ptr.value for r in ranks]
     for r in ranks:
         r._attach(ptrs, emulated=True, grid=grid, timeout_s=timeout_s)
-    return EmulatedTP(ranks)
+    tp = EmulatedTP(ranks)
+    if nvls:  # one multicast copy on this GPU, shared by every emulated rank
+        import torch
+        tp.nvls = NvlsSums(cfg.hidden, torch.cuda.current_device())
+        for r in ranks:
+            r.use_nvls(tp.nvls)
+    return tp

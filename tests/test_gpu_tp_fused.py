@@ -28,11 +28,11 @@ def _oracle_caches(params, cfg, steps):
             for l in params["layers"]]
 
 
-def _run(cfg, world, prefill, steps, seed, graph=False):
+def _run(cfg, world, prefill, steps, seed, graph=False, nvls=False):
     params = random_llama_params(cfg, seed=seed, prefill=prefill)
     params["rope_cs"] = lp.rope_table(prefill + steps + 1, cfg.head_dim, cfg.rope_theta)
     caches = _oracle_caches(params, cfg, steps)
-    tp = emulated_ranks(cfg, world, prefill + steps + 1, params=params, timeout_s=5.0)
+    tp = emulated_ranks(cfg, world, prefill + steps + 1, params=params, timeout_s=5.0, nvls=nvls)
     tok, pos = 7, prefill
     seen = []
     for s in range(steps):
@@ -80,3 +80,40 @@ def test_fused_tp_llama_width(world):
     shards of 16 / 8 / 4 heads per rank."""
     cfg = LlamaConfig(n_layers=2)
     _run(cfg, world, 300, steps=2, seed=3)
+
+
+def _need_nvls():
+    from paper_2508_18850_b200.tp_fused import nvls_usable
+    if not nvls_usable(0):
+        pytest.skip("no usable NVLS multicast on this GPU (cuMulticastCreate refused)")
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_fused_tp_nvls_sums_match_oracle_and_peer_path(world):
+    """The sums on an NVLS multicast buffer (multimem.red.add.u64 on the
+    multicast mapping, csrc/nvls.cu; emulated ranks share the one-member
+    object's copy): oracle parity, and bit-identical to the peer-memory
+    pushes (fixed-point sums are order-free)."""
+    _need_nvls()
+    cfg = LlamaConfig(**SMALL)
+    _, a = _run(cfg, world, 64, steps=3, seed=11)
+    tp, b = _run(cfg, world, 64, steps=3, seed=11, nvls=True)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    _, c = _run(cfg, world, 64, steps=3, seed=11, graph=True, nvls=True)
+    for x, y in zip(a, c):
+        assert np.array_equal(x, y)
+
+
+def test_nvls_setup_path_single_member():
+    """The multicast-object setup a multi-GPU group runs (create, add device,
+    bind: a zeroed physical copy with unicast + multicast mappings), with one
+    member; the reductions through it are checked by the test above."""
+    import torch
+    _need_nvls()
+    from paper_2508_18850_b200.tp_fused import NvlsSums
+    s = NvlsSums(4096, torch.cuda.current_device())
+    assert s.uc.value and s.mc.value and s.uc.value != s.mc.value
+    assert int(s._L.cfb_nvls_size(s.h)) >= 6 * 4096 * 8
+    del s
+    torch.cuda.synchronize()
