@@ -84,7 +84,7 @@ __host__ __device__ inline MoeLayout moe_layout(int B, int D, int E, int K, int 
   const int Tt = Gs + L.umax * Ge;
   L.max_groups = (Tt + G - 1) / G + 1;
   int o = ring_bytes(spw);
-  L.bars = o;  o += moe_r16((2 * kNumSlots + 2) * 8);
+  L.bars = o;  o += moe_r16((2 * kNumSlots + 3) * 8);
   const int rows = (E + G - 1) / G;
   L.rrows = rows * D * 2 <= 16384 ? rows : 0;
   L.rrow = o;  o += moe_r16(L.rrows * D * 2);
@@ -128,6 +128,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L.bars);
   uint64_t* route_bar = bars + 2 * kNumSlots;
   uint64_t* rrow_bar = route_bar + 1;  // router rows landed in smem
+  uint64_t* go_bar = rrow_bar + 1;     // consumers past griddepcontrol.wait: experts may stream
   const Ring ring{smem, bars, bars + kNumSlots, p.spw, p.sleep_max};
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int Gs = p.Fs / 8, Ge = p.Fe / 8;
@@ -140,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
     ring_init(ring);
     mbar_init(route_bar, 1);
     mbar_init(rrow_bar, 1);
+    mbar_init(go_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -172,6 +174,11 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
         bulk_g2s(smem + L.rrow + (size_t)n * D * 2, p.w_router + (size_t)e * D, D * 2, rrow_bar,
                  policy_evict_last());  // router rows stay L2-resident across steps
     }
+    // the expert stream starts once the consumers have issued their RMSNorm
+    // loads: a 28 MB burst issued first would queue ahead of those loads
+    if (lane == 0)
+      while (!mbar_test(go_bar, 0)) __nanosleep(32);
+    __syncwarp();
     for (int g = rs.s0; g < rs.s1; g += kMoeChunk) {
       const Phase ph[1] = {gu_phase(p.s_gu, g, min(kMoeChunk, rs.s1 - g))};
       produce_all(ph, ring, lane, pol, c);
@@ -204,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 1) moe_kernel(const MoeParams p) {
 
   // ---------------------------------------------------------------- consumers
   pdl_wait();
+  if (tid == 0) mbar_arrive(go_bar);
   unsigned long long* tr = p.trace ? p.trace + (size_t)i * 16 : nullptr;
   auto stamp = [&](int k) {  // %globaltimer ns (comparable across SMs and kernels)
     if (tr && tid == 0) tr[k] = globaltimer();
