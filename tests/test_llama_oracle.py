@@ -35,8 +35,8 @@ def test_rope_is_rotation_and_identity_at_zero():
     # relative-position property of q.k after rotation
     q = lp.f16(np.random.default_rng(2).standard_normal((1, 8)))
     k = lp.f16(np.random.default_rng(3).standard_normal((1, 8)))
-    d1 = float(lp.apply_rope(q, 10, cs) @ lp.apply_rope(k, 7, cs).T)
-    d2 = float(lp.apply_rope(q, 20, cs) @ lp.apply_rope(k, 17, cs).T)
+    d1 = float((lp.apply_rope(q, 10, cs) @ lp.apply_rope(k, 7, cs).T)[0, 0])
+    d2 = float((lp.apply_rope(q, 20, cs) @ lp.apply_rope(k, 17, cs).T)[0, 0])
     assert abs(d1 - d2) < 2e-2
 
 
