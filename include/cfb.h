@@ -591,6 +591,22 @@ int cfb_llama_write_token(cfb_llama* m, const int* token_host, void* stream);
  * boundaries of csrc/decode_step.cu) written each step into `trace` (device, or
  * NULL to stop); returns the grid size through *grid. */
 int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid);
+/* Persistent cluster engines (PERSISTENT / PERSISTENT_NODSMEM) only: paged KV
+ * cache (SURVEY §8(f) rank 4 at batch 1).  k_cache / v_cache of the weights
+ * are then per-layer page pools of 128-position pages: row r of head h sits at
+ * element h * head_stride + block_table[r / 128] * page_stride + (r % 128) *
+ * head_dim.  Page-major pools [n_pages][n_heads][128][head_dim] (the batched
+ * path's layout: page_stride = n_heads * 128 * head_dim, head_stride = 128 *
+ * head_dim) and head-major pools [n_heads][n_pages][128][head_dim]
+ * (page_stride = 128 * head_dim, head_stride = n_pages * 128 * head_dim) are
+ * both expressible.  `block_table` [max_pages] (device, int32, -1 = not
+ * reserved), max_pages * 128 >= cache_cap.  A step whose new row lands on an
+ * unreserved page does nothing and reports err 1 (cfb_llama_check).  NULL
+ * returns to the contiguous caches.  Set before cfb_llama_capture (a captured
+ * graph keeps the table pointer; the table's CONTENTS may change between
+ * replays). */
+int cfb_llama_set_kv_pages(cfb_llama* m, const int* block_table, int max_pages, long long page_stride,
+                           long long head_stride);
 /* Device-side status of the last steps: *err_host = 1 if a step found pos + 1 >
  * cache_cap and did nothing, 2 if a fused tensor-parallel step gave up waiting
  * for its peers (stream-ordered read, then the flag is cleared). */

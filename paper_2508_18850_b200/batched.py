@@ -139,6 +139,44 @@ class PagedKVPool:
         return g(self.k[layer]), g(self.v[layer])
 
 
+class HeadMajorKVPool(PagedKVPool):
+    """Paged KV for the B=1 persistent engine with per-layer pools
+    [n_heads][n_pages][128][128] fp16 (head-major: a head's pages share one
+    region).  Page bookkeeping (free list, block table, reserve / release) is
+    the batched ``PagedKVPool``'s; only the pool layout and the writer differ."""
+
+    def __init__(self, cfg: LlamaConfig, n_pages: int, max_pages: int, dev, n_seq: int = 1):
+        import torch
+        self.cfg, self.n_pages, self.max_pages, self.dev, self.n_seq = cfg, n_pages, max_pages, dev, n_seq
+        shape = (cfg.n_heads, n_pages, PAGE, cfg.head_dim)
+        self.k = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
+        self.v = [torch.zeros(shape, device=dev, dtype=torch.float16) for _ in range(cfg.n_layers)]
+        self.free = list(range(n_pages))[::-1]
+        self.pages = [[] for _ in range(n_seq)]
+        self.host_table = np.full((n_seq, max_pages), -1, np.int32)
+        self.table = torch.full((n_seq, max_pages), -1, device=dev, dtype=torch.int32)
+
+    def write(self, layer: int, seq: int, start: int, k, v, stream=None) -> None:
+        """Prefill writer: rows start .. start+count of ``seq`` from k, v
+        (n_heads, count, 128) device fp16 into their pages (page-sized copies)."""
+        k, v = _half_dev(k, self.dev), _half_dev(v, self.dev)
+        count = k.shape[1]
+        self.reserve(seq, start + count)
+        r = 0
+        while r < count:
+            pos = start + r
+            pg, off = int(self.host_table[seq, pos // PAGE]), pos % PAGE
+            n = min(PAGE - off, count - r)
+            self.k[layer][:, pg, off:off + n] = k[:, r:r + n]
+            self.v[layer][:, pg, off:off + n] = v[:, r:r + n]
+            r += n
+
+    def gather(self, layer: int, seq: int, length: int):
+        import torch
+        pg = torch.as_tensor(self.pages[seq][:(length + PAGE - 1) // PAGE], device=self.dev, dtype=torch.long)
+        return (self.k[layer][:, pg].reshape(self.cfg.n_heads, -1, self.cfg.head_dim)[:, :length],
+                self.v[layer][:, pg].reshape(self.cfg.n_heads, -1, self.cfg.head_dim)[:, :length])
+
 def torch_from(a):
     import torch
     return torch.from_numpy(np.ascontiguousarray(a))

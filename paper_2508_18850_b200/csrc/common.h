@@ -69,6 +69,8 @@ struct LlamaStepArgs {
   const void* const* w_dn;
   void* const* k_cache;
   void* const* v_cache;
+  const int* kv_pages;        // paged KV block table [cache_cap / 128] or NULL (contiguous)
+  long long kv_pstride, kv_hstride;  // paged: elements between pages / between heads
   const void* embed;
   const void* final_norm;
   const void* lm_head;

@@ -71,6 +71,10 @@ struct StepParams {
   const __half* const* w_dn;
   __half* const* k_cache;
   __half* const* v_cache;
+  const int* kv_pages;           // paged KV: block table [cap / 128] (page ids, -1 = none), or null;
+                                 // the caches are then page pools: row r of head h at element
+                                 // h * kv_hstride + pages[r / 128] * kv_pstride + (r % 128) * H
+  long long kv_pstride, kv_hstride;
   const __half* embed;
   const __half* final_norm;
   const __half* lm_head;
@@ -421,7 +425,7 @@ __device__ __forceinline__ void stamp(unsigned long long* tr, int k, int tid) {
 // the ClusterGather and the (m, l, A) exchange go through global memory (a
 // slot per rank, a per-cluster release/acquire counter) instead of DSMEM -
 // the paper's "without DSMEM" ablation.
-template <bool kCluster, bool kDsmem = true>
+template <bool kCluster, bool kDsmem = true, bool kPaged = false>
 __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParams p) {
   extern __shared__ __align__(128) char smem[];
   const int G = gridDim.x, i = blockIdx.x;
@@ -436,7 +440,9 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
   uint64_t* cbar = reinterpret_cast<uint64_t*>(smem + Lo.misc + 16);  // [0] gather, [1] exchange
 
   const int S = *p.pos;
-  if (S + 1 > p.cap) {  // uniform across the grid: no barrier is entered
+  // uniform across the grid: no barrier is entered.  Paged: the page that
+  // receives row S must be reserved (rows < S were written by earlier steps)
+  if (S + 1 > p.cap || (kPaged && __ldg(p.kv_pages + S / kPageRows) < 0)) {
     if (i == 0 && tid == 0) *p.err = 1;
     return;
   }
@@ -516,6 +522,10 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
         if (part_ == 0)
           return make_phase(p.w_qkv[l] + hr * p.tpr * 4 * D, nullptr, on ? p.tpr : 0, 4 * D * 2, true);
         if (part_ == 1) {
+          if (kPaged) {  // this head's rows of page 0 (layer_pphase adds the pages)
+            const size_t hoff = on ? (size_t)h * p.kv_hstride : 0;
+            return make_phase(p.k_cache[l] + hoff, p.v_cache[l] + hoff, on ? s_hi - s_lo : 0, kH * 2);
+          }
           const size_t off = on ? ((size_t)h * p.cap + s_lo) * kH : 0;
           return make_phase(p.k_cache[l] + off, p.v_cache[l] + off, on ? s_hi - s_lo : 0, kH * 2);
         }
@@ -539,6 +549,14 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     if (k == 6) return make_phase(p.w_gu[l] + (size_t)a0 * 4 * D, nullptr, a1 - a0, 4 * D * 2, true);
     return make_phase(p.w_dn[l] + (size_t)u0 * 4 * F, nullptr, u1 - u0, 4 * F * 2, true);
   };
+  // the producer's view: the KV phases (cluster variant, k % 3 == 1) read the
+  // page pool through the block table when the cache is paged
+  auto layer_pphase = [&](int l, int k) -> PagedPhase {
+    const Phase ph_ = layer_phase(l, k);
+    if (kPaged && k < 6 && k % 3 == 1)
+      return paged_phase(ph_, p.kv_pages, s_lo, p.kv_pstride * 2);
+    return paged_phase(ph_);
+  };
   // At a barrier the ring (ring_bytes) already holds the head of the next
   // phase and stalls once full; thread 0 lets HBM keep working on the bytes
   // after it by prefetching the next `l2_prefetch` bytes of that phase into
@@ -556,8 +574,18 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     const uint64_t pol = policy_evict_first();
     int c = 0;
     int* tag = reinterpret_cast<int*>(smem + Lo.tag);
+    // paged KV: the block-table entries of this CTA's segment pages, in the
+    // producer lanes' registers for the whole launch (produce_gen_paged)
+    int pgr[kPageRegs];
+    const int p0 = s_lo / kPageRows;
+#pragma unroll
+    for (int k = 0; k < kPageRegs; ++k)
+      pgr[k] = kPaged && (p0 + 32 * k + lane) * kPageRows < p.cap ? __ldg(p.kv_pages + p0 + 32 * k + lane) : 0;
     for (int l = 0; l < p.L; ++l) {
-      produce_gen(7, [&](int k) { return layer_phase(l, k); }, ring, lane, pol, c);
+      if constexpr (kPaged)
+        produce_gen_paged(7, [&](int k) { return layer_pphase(l, k); }, ring, lane, pol, c, pgr, p0);
+      else
+        produce_gen(7, [&](int k) { return layer_phase(l, k); }, ring, lane, pol, c);
       if (p.pool > 0)
         produce_pool(ring, lane, pol, c, p.pool_ctr + l, p.pool, T1s,
                      reinterpret_cast<const char*>(p.w_gu[l]), 4 * D * 2, tag);
@@ -678,7 +706,10 @@ __global__ void __launch_bounds__(kThreads, 1) llama_step_kernel(const StepParam
     consumer_sync();
   };
   auto append_kv = [&](int l, int h) {  // KV-cache append at row S (read by later steps only)
-    const size_t off = ((size_t)h * p.cap + S) * kH;
+    const size_t off = kPaged
+        ? (size_t)h * p.kv_hstride + (size_t)__ldg(p.kv_pages + S / kPageRows) * p.kv_pstride +
+              (size_t)(S % kPageRows) * kH
+        : ((size_t)h * p.cap + S) * kH;
     for (int d = tid; d < kH; d += kConsumerThreads) {
       p.k_cache[l][off + d] = __float2half_rn(kf[d]);
       p.v_cache[l][off + d] = __float2half_rn(vf[d]);
@@ -1239,6 +1270,15 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
   p.w_dn = reinterpret_cast<const __half* const*>(a->w_dn);
   p.k_cache = reinterpret_cast<__half* const*>(a->k_cache);
   p.v_cache = reinterpret_cast<__half* const*>(a->v_cache);
+  p.kv_pages = a->kv_pages;
+  p.kv_pstride = a->kv_pstride;
+  p.kv_hstride = a->kv_hstride;
+  if (p.kv_pages && !a->cluster_attn)
+    return set_error(CFB_ERR_ARGUMENT, "paged KV needs the cluster attention (persistent / nodsmem engine)");
+  // a CTA's segment (ceil(cap / N) rows, any offset) must fit the producer's page registers
+  if (p.kv_pages && ((a->cache_cap + N - 1) / N + kPageRows - 1) / kPageRows + 1 >= 32 * kPageRegs)
+    return set_error(CFB_ERR_DIMENSION, "paged KV: %d positions over clusters of %d exceed %d pages per CTA",
+                     a->cache_cap, N, 32 * kPageRegs - 2);
   p.embed = static_cast<const __half*>(a->embed);
   p.final_norm = static_cast<const __half*>(a->final_norm);
   p.lm_head = static_cast<const __half*>(a->lm_head);
@@ -1291,7 +1331,11 @@ int llama_step_launch(const LlamaStepArgs* a, cudaStream_t st) {
     at[1].val.cooperative = coop;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    if (a->cluster_attn == 2) {
+    if (p.kv_pages) {
+      auto kern = a->cluster_attn == 2 ? llama_step_kernel<true, false, true> : llama_step_kernel<true, true, true>;
+      if (const int rc = configure_kernel((const void*)kern, kMaxSmem, true)) return rc;
+      CFB_CUDA(cudaLaunchKernelEx(&cfg, kern, p));
+    } else if (a->cluster_attn == 2) {
       if (const int rc = configure_kernel((const void*)llama_step_kernel<true, false>, kMaxSmem, true))
         return rc;
       CFB_CUDA(cudaLaunchKernelEx(&cfg, llama_step_kernel<true, false>, p));

@@ -47,6 +47,8 @@ struct cfb_llama {
   int plain_launch = 0; // CFB_OPT_PLAIN_LAUNCH
   int ring_spw = 0;     // CFB_OPT_RING_SLOTS
   int pool_per_cta = 0; // CFB_OPT_POOL_TILES
+  const int* kv_pages = nullptr;  // cfb_llama_set_kv_pages: block table, or null (contiguous)
+  long long kv_pstride = 0, kv_hstride = 0;
   long long timeout_ns = 0;
   unsigned long long** xch_dev = nullptr;  // [tp_size] exchange blocks as this device sees them
   float* resid2 = nullptr;
@@ -207,6 +209,9 @@ int enqueue_persistent(cfb_llama* m, cudaStream_t st) {
   a.w_dn = d + 5 * L;
   a.k_cache = d + 6 * L;
   a.v_cache = d + 7 * L;
+  a.kv_pages = m->kv_pages;
+  a.kv_pstride = m->kv_pstride;
+  a.kv_hstride = m->kv_hstride;
   a.embed = m->embed;
   a.final_norm = m->final_norm;
   a.lm_head = m->lm_head;
@@ -606,6 +611,23 @@ int cfb_llama_set_trace(cfb_llama* m, unsigned long long* trace, int* grid) {
     return cfb::set_error(CFB_ERR_ARGUMENT, "tracing needs a persistent engine");
   m->trace = trace;
   if (grid) *grid = m->grid;
+  return CFB_OK;
+}
+
+int cfb_llama_set_kv_pages(cfb_llama* m, const int* block_table, int max_pages, long long page_stride,
+                           long long head_stride) {
+  if (!m) return cfb::set_error(CFB_ERR_ARGUMENT, "null engine");
+  if (m->cfg.engine != CFB_ENGINE_PERSISTENT && m->cfg.engine != CFB_ENGINE_PERSISTENT_NODSMEM)
+    return cfb::set_error(CFB_ERR_ARGUMENT, "paged KV needs a persistent cluster engine");
+  if (m->cfg.head_dim != 128) return cfb::set_error(CFB_ERR_DIMENSION, "paged KV needs head_dim 128");
+  if (block_table && (long long)max_pages * 128 < m->cfg.cache_cap)
+    return cfb::set_error(CFB_ERR_DIMENSION, "block table of %d pages < cache_cap %d positions", max_pages,
+                          m->cfg.cache_cap);
+  if (block_table && (page_stride <= 0 || head_stride < 0 || page_stride % 8 || head_stride % 8))
+    return cfb::set_error(CFB_ERR_ARGUMENT, "paged KV strides must be positive multiples of 8 elements");
+  m->kv_pages = block_table;
+  m->kv_pstride = page_stride;
+  m->kv_hstride = head_stride;
   return CFB_OK;
 }
 

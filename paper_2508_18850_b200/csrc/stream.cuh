@@ -49,6 +49,16 @@ struct Phase {
   bool tiles;
   int warp;         // >= 0: every item goes to this consumer warp (warp-affine phase)
 };
+// A phase whose rows may live in a paged pool (rows mode only; pages == nullptr:
+// contiguous).  Unit u is logical row row0 + u of 128-row pages; page g starts
+// pages[g] * pstride bytes past src0/src1.  A separate type, so the kernels
+// that never page keep the plain Phase (and its stack footprint).
+constexpr int kPageRows = 128;
+struct PagedPhase : Phase {
+  const int* pages;
+  int row0;
+  long long pstride;
+};
 
 __device__ __forceinline__ Phase make_phase(const void* src0, const void* src1, int n_units,
                                             int unit_bytes, bool tiles = false) {
@@ -81,6 +91,19 @@ struct Item {
   int byte0;   // byte offset of the piece within its unit
   int bytes;   // bytes per source
 };
+
+// Paged rows phase: the same units as `p`, unit u read from logical row
+// row0 + u of the page pool (src0/src1 = the pool base of this head's rows);
+// pages == nullptr keeps `p` contiguous.
+__device__ __forceinline__ PagedPhase paged_phase(const Phase& p, const int* pages = nullptr, int row0 = 0,
+                                                  long long pstride = 0) {
+  PagedPhase q;
+  static_cast<Phase&>(q) = p;
+  q.pages = pages;
+  q.row0 = row0;
+  q.pstride = pstride;
+  return q;
+}
 
 // Warp-affine phase: all items of the phase go to consumer warp `warp` (the
 // warp then owns everything the phase produces, e.g. a block of output rows).
@@ -135,6 +158,25 @@ __device__ __forceinline__ void issue_item(const Phase& p, const Item& it, const
   mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
   bulk_g2s(r.slot(s), p.src0 + off, it.bytes, &r.full[s], policy);
   if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + off, it.bytes, &r.full[s], policy);
+}
+
+// Paged rows: `pga` / `pgb` are the page ids of the item's first row and of the
+// next page (an item of <= 16 rows spans at most two 128-row pages).
+__device__ __forceinline__ void issue_item_paged(const PagedPhase& p, const Item& it, const Ring& r, int s,
+                                                 uint64_t policy, int pga, int pgb) {
+  mbar_arrive_expect_tx(&r.full[s], p.src1 ? 2u * it.bytes : static_cast<uint32_t>(it.bytes));
+  const int r0 = p.row0 + it.unit0;
+  const int n0 = min(it.nunits, kPageRows - (r0 & (kPageRows - 1)));
+  const size_t o0 = (size_t)pga * p.pstride + (size_t)(r0 & (kPageRows - 1)) * p.unit_bytes;
+  const int b0 = n0 * p.unit_bytes;
+  bulk_g2s(r.slot(s), p.src0 + o0, b0, &r.full[s], policy);
+  if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2, p.src1 + o0, b0, &r.full[s], policy);
+  if (n0 < it.nunits) {
+    const size_t o1 = (size_t)pgb * p.pstride;
+    const int b1 = it.bytes - b0;
+    bulk_g2s(r.slot(s) + b0, p.src0 + o1, b1, &r.full[s], policy);
+    if (p.src1) bulk_g2s(r.slot(s) + kSlotBytes / 2 + b0, p.src1 + o1, b1, &r.full[s], policy);
+  }
 }
 
 // Producer warp: lane w < kNumConsumerWarps feeds consumer warp w through
@@ -209,6 +251,69 @@ __device__ __forceinline__ void produce_gen(int np, Gen&& gen, const Ring& r, in
           ++j;
           issued = true;
         }
+      }
+    }
+    if (__all_sync(0xffffffffu, done)) break;
+    if (__any_sync(0xffffffffu, issued)) {
+      nap = 32;
+    } else {
+      __nanosleep(nap);
+      nap = min(2 * nap, r.sleep_max);
+    }
+  }
+}
+
+// produce_gen for a schedule whose phases may read paged rows (gen returns
+// PagedPhase).  The page ids of the CTA's rows are held in the producer
+// warp's registers - lane l keeps page p0 + 32 k + l in pg[k] (loaded once per
+// launch: the rows of a CTA's segment sit on the same pages in every layer and
+// head) - and read with shuffles in the convergent part of every loop trip, so
+// no bulk copy waits on a dependent global load of the block table.
+constexpr int kPageRegs = 4;  // <= 128 pages per CTA segment
+template <class Gen>
+__device__ __forceinline__ void produce_gen_paged(int np, Gen&& gen, const Ring& r, int lane, uint64_t policy,
+                                                  int& c, const int (&pg)[kPageRegs], int p0) {
+  const int w = lane;
+  int ph = 0, j = 0;
+  PagedPhase cur = gen(0);
+  bool done = w >= kNumConsumerWarps || np == 0;
+  int nap = 32;
+  while (true) {
+    bool issued = false, cand = false;
+    Item it{};
+    int rel = 0;
+    if (!done) {
+      while (ph < np && j >= items_for_warp(cur, w)) {
+        ++ph;
+        j = 0;
+        if (ph < np) cur = gen(ph);
+      }
+      if (ph == np) {
+        done = true;
+      } else {
+        cand = true;
+        it = item_of(cur, w, j);
+        if (cur.pages) rel = (cur.row0 + it.unit0) / kPageRows - p0;
+      }
+    }
+    int pga = 0, pgb = 0;
+#pragma unroll
+    for (int k = 0; k < kPageRegs; ++k) {  // every lane: convergent shuffles
+      const int va = __shfl_sync(0xffffffffu, pg[k], rel & 31);
+      const int vb = __shfl_sync(0xffffffffu, pg[k], (rel + 1) & 31);
+      if ((rel >> 5) == k) pga = va;
+      if (((rel + 1) >> 5) == k) pgb = vb;
+    }
+    if (cand) {
+      const int s = w * r.spw + (c % r.spw);
+      if (mbar_test(&r.empty[s], ((c / r.spw) & 1) ^ 1)) {
+        if (cur.pages)
+          issue_item_paged(cur, it, r, s, policy, pga, pgb);
+        else
+          issue_item(cur, it, r, s, policy);
+        ++c;
+        ++j;
+        issued = true;
       }
     }
     if (__all_sync(0xffffffffu, done)) break;

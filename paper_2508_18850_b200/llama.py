@@ -332,6 +332,71 @@ class LlamaDecoder:
         L_.cfb_llama_set_option.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_longlong]
         _native.check(L_.cfb_llama_set_option(self._h, 3, int(spw)))
 
+    def page_kv(self, reserve: int | None = None, n_pages: int | None = None, shuffle: bool = True,
+                seed: int = 0, layout: str = "head_major"):
+        """Move the KV caches into a paged pool and re-create the engine on it
+        (persistent cluster engines; SURVEY §8(f) rank 4 at batch 1).
+
+        Pages hold 128 positions; a block table [max_pages] (-1 = not
+        reserved) maps logical to physical pages.  ``layout``:
+        "page_major" is the batched path's ``PagedKVPool`` ([n_pages][n_heads]
+        [128][128] per layer, prefill writer ``cfb_b16_kv_write``);
+        "head_major" (``HeadMajorKVPool``, [n_heads][n_pages][128][128]) keeps
+        each head's pages in one region, so a CTA's rows stay within a few
+        GPU memory pages whatever the page order.  Positions 0 .. reserve-1
+        (default: the whole cache_cap) get pages, taken in a shuffled order when
+        ``shuffle`` so logical and physical pages differ; ``pool.reserve(0, n)``
+        adds more between steps.  A step whose new row lands on an unreserved
+        page does nothing and ``check()`` raises.  Call before ``capture``."""
+        from .batched import PAGE, HeadMajorKVPool, PagedKVPool
+        torch, cfg = self.torch, self.cfg
+        if cfg.engine not in ("persistent", "persistent_nodsmem"):
+            raise DimensionError("paged KV needs a persistent cluster engine")
+        if layout not in ("head_major", "page_major"):
+            raise DimensionError(f"unknown KV page layout {layout!r}")
+        max_pages = -(-self.cache_cap // PAGE)
+        cls = HeadMajorKVPool if layout == "head_major" else PagedKVPool
+        pool = cls(cfg, n_pages or max_pages, max_pages, self.dev, n_seq=1)
+        if shuffle:
+            rng = np.random.default_rng(seed)
+            pool.free = [int(x) for x in rng.permutation(pool.n_pages)]
+        n = self.cache_cap if reserve is None else reserve
+        pool.reserve(0, n)
+        cur = torch.cuda.current_stream(self.dev)
+        cur.wait_stream(self.stream)
+        rows = min(n, self.cache_cap)
+        for l, lay in enumerate(self.layers):
+            pool.write(l, 0, 0, lay["k_cache"][:, :rows], lay["v_cache"][:, :rows], stream=cur)
+            lay["k_cache"], lay["v_cache"] = pool.k[l], pool.v[l]
+        torch.cuda.synchronize()
+        if self._h is not None:
+            self._lib.cfb_llama_destroy(self._h)
+            self._h = None
+        self._finish()
+        H = cfg.head_dim
+        if layout == "head_major":
+            pstride, hstride = PAGE * H, pool.n_pages * PAGE * H
+        else:
+            pstride, hstride = cfg.n_heads * PAGE * H, PAGE * H
+        L_ = self._lib
+        L_.cfb_llama_set_kv_pages.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
+                                              ctypes.c_longlong, ctypes.c_longlong]
+        _native.check(L_.cfb_llama_set_kv_pages(self._h, pool.table.data_ptr(), max_pages, pstride, hstride))
+        self.kv_pool = pool
+        return pool
+
+    def kv_rows(self, layer: int, pos: int):
+        """(k, v) rows at position ``pos`` of every head, (n_heads, head_dim) fp16
+        on the device, whichever layout the cache has."""
+        pool = getattr(self, "kv_pool", None)
+        if pool is None:
+            return self.layers[layer]["k_cache"][:, pos], self.layers[layer]["v_cache"][:, pos]
+        from .batched import HeadMajorKVPool
+        pg = int(pool.host_table[0, pos // 128])
+        if isinstance(pool, HeadMajorKVPool):
+            return pool.k[layer][:, pg, pos % 128], pool.v[layer][:, pg, pos % 128]
+        return pool.k[layer][pg, :, pos % 128], pool.v[layer][pg, :, pos % 128]
+
     def check(self) -> None:
         """Raise if a step found the cache full (pos + 1 > cache_cap) and skipped."""
         L_ = self._lib
@@ -341,7 +406,8 @@ class LlamaDecoder:
         if err.value == 2:
             raise SimulationError("fused tensor-parallel step: peers did not arrive in time")
         if err.value:
-            raise DimensionError(f"decode position reached the cache capacity {self.cache_cap}")
+            raise DimensionError(f"decode position reached the cache capacity {self.cache_cap} "
+                                 "(or, paged, a page that is not reserved)")
 
     def set_state(self, pos: int, token: int) -> None:
         _native.check(self._lib.cfb_llama_set_state(self._h, pos, token, self._sp()))
@@ -401,3 +467,4 @@ class LlamaDecoder:
             except Exception:
                 pass
             self._h = None
+

@@ -23,8 +23,16 @@ ctxs = [int(c) for c in args.ctx.split(",")]
 cap = max(ctxs) + 64
 res = {}
 for eng in args.engines.split(","):
-    cfg = dataclasses.replace(LLAMA2_7B, engine=eng)
+    # "persistent_paged" / "persistent_pagedpm": the persistent engine on a shuffled
+    # 128-position page pool, head-major / page-major
+    paged = "_paged" in eng
+    cfg = dataclasses.replace(LLAMA2_7B, engine=eng.split("_paged")[0])
     m = LlamaDecoder.random(cfg, cache_cap=cap, seed=1)
+    if paged:
+        # "..._pagedseq": pages in logical order (an allocator's best case)
+        m.page_kv(seed=1, layout="page_major" if eng.endswith("pm") else "head_major",
+                  shuffle=not eng.endswith("seq"))
+        torch.cuda.empty_cache()
     m.set_state(ctxs[0], 1)
     m.step()
     torch.cuda.synchronize()
@@ -46,7 +54,7 @@ for eng in args.engines.split(","):
         b = cfg.step_bytes(ctx + args.steps // 2)
         res[f"{eng}@{ctx}"] = {"tpot_us": round(us, 1), "tb_s": round(b / us / 1e6, 3)}
         print(eng, ctx, res[f"{eng}@{ctx}"], flush=True)
-        if args.trace and eng != "layered":
+        if args.trace and cfg.engine != "layered":
             tr = m.set_trace(True)
             m.set_state(ctx, 1)
             m.step()
