@@ -407,14 +407,19 @@ def engine_compare(cfg, ctxs, args, peak_gbs):
     cluster kernel + fused FFN kernel, 2 launches per layer), the persistent
     kernel with the cluster gather / exchange through global memory instead of
     DSMEM (same partitioning: the paper's with/without-DSMEM ablation,
-    PAPER.md:889-891), and the flat variant (attention split over all SMs)."""
+    PAPER.md:889-891), the flat variant (attention split over all SMs), and the
+    persistent engine on a paged KV cache (shuffled 128-position pages,
+    head-major pools, `LlamaDecoder.page_kv`)."""
     import dataclasses
     import torch
     from paper_2508_18850_b200.llama import LlamaDecoder
     out = []
-    for eng in ("layered", "persistent_nodsmem", "persistent_flat"):
-        c = dataclasses.replace(cfg, engine=eng)
+    for eng in ("layered", "persistent_nodsmem", "persistent_flat", "persistent_paged"):
+        c = dataclasses.replace(cfg, engine=eng.replace("_paged", ""))
         m = LlamaDecoder.random(c, cache_cap=max(ctxs) + args.warmup + args.steps + 8, seed=1234)
+        if eng.endswith("_paged"):
+            m.page_kv(seed=1)
+            torch.cuda.empty_cache()
         m.set_state(ctxs[0], 1)
         m.step()
         torch.cuda.synchronize()
