@@ -296,13 +296,17 @@ __device__ __forceinline__ void produce_gen_paged(int np, Gen&& gen, const Ring&
         if (cur.pages) rel = (cur.row0 + it.unit0) / kPageRows - p0;
       }
     }
-    int pga = 0, pgb = 0;
+    // pages of this item (rel, rel + 1) and of the lane's next item, 128 rows
+    // further (rel + 1, rel + 2); every lane: convergent shuffles
+    int pga = 0, pgb = 0, pgc = 0;
 #pragma unroll
-    for (int k = 0; k < kPageRegs; ++k) {  // every lane: convergent shuffles
+    for (int k = 0; k < kPageRegs; ++k) {
       const int va = __shfl_sync(0xffffffffu, pg[k], rel & 31);
       const int vb = __shfl_sync(0xffffffffu, pg[k], (rel + 1) & 31);
+      const int vc = __shfl_sync(0xffffffffu, pg[k], (rel + 2) & 31);
       if ((rel >> 5) == k) pga = va;
       if (((rel + 1) >> 5) == k) pgb = vb;
+      if (((rel + 2) >> 5) == k) pgc = vc;
     }
     if (cand) {
       const int s = w * r.spw + (c % r.spw);
@@ -314,6 +318,19 @@ __device__ __forceinline__ void produce_gen_paged(int np, Gen&& gen, const Ring&
         ++c;
         ++j;
         issued = true;
+        // paged rows: a producer that fell behind refills two slots per trip
+        // (the paged trip is longer); the lane's next item of the phase sits
+        // one page further (rows + 128)
+        if (cur.pages && j < items_for_warp(cur, w)) {
+          const int s2 = w * r.spw + (c % r.spw);
+          const Item it2 = item_of(cur, w, j);
+          if ((cur.row0 + it2.unit0) / kPageRows - p0 == rel + 1 &&
+              mbar_test(&r.empty[s2], ((c / r.spw) & 1) ^ 1)) {
+            issue_item_paged(cur, it2, r, s2, policy, pgb, pgc);
+            ++c;
+            ++j;
+          }
+        }
       }
     }
     if (__all_sync(0xffffffffu, done)) break;
