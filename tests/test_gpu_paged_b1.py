@@ -132,3 +132,27 @@ def test_paged_rejects_flat_engine_and_oversized_segments():
     m1.set_state(5, 1)
     with pytest.raises(DimensionError):
         m1.step()
+
+
+def test_paged_graph_replay_with_incremental_reserve():
+    """The INTEGRATION.md loop: the captured graph keeps the table pointer and
+    sees pages reserved between replays (a new page every 128 positions)."""
+    cfg = dataclasses.replace(SMALL, engine="persistent")
+    params = random_llama_params(cfg, seed=15, prefill=120)
+    a = LlamaDecoder.from_params(cfg, params, cache_cap=400)
+    b = LlamaDecoder.from_params(cfg, params, cache_cap=400)
+    pool = b.page_kv(reserve=121)
+    ref = a.generate(first_token=6, pos=120, n_tokens=20, use_graph=True)
+    b.set_state(120, 6)
+    b.step()
+    b.set_state(120, 6)
+    b.capture()
+    got, pos = [], 120
+    for _ in range(20):
+        pool.reserve(0, pos + 1)
+        b.replay()
+        got.append(b.token())
+        pos += 1
+    b.check()
+    assert got == ref
+    assert len(pool.pages[0]) == 2  # positions 0..139: pages 0 and 1
