@@ -354,6 +354,8 @@ class LlamaDecoder:
             raise DimensionError("paged KV needs a persistent cluster engine")
         if layout not in ("head_major", "page_major"):
             raise DimensionError(f"unknown KV page layout {layout!r}")
+        if getattr(self, "kv_pool", None) is not None:
+            raise DimensionError("the KV cache is already paged")
         max_pages = -(-self.cache_cap // PAGE)
         cls = HeadMajorKVPool if layout == "head_major" else PagedKVPool
         pool = cls(cfg, n_pages or max_pages, max_pages, self.dev, n_seq=1)

@@ -125,6 +125,10 @@ def test_paged_rejects_flat_engine_and_oversized_segments():
     m = LlamaDecoder.from_params(cfg, random_llama_params(cfg, seed=1, prefill=4), cache_cap=16)
     with pytest.raises(DimensionError):
         m.page_kv()
+    m2 = LlamaDecoder.from_params(SMALL, random_llama_params(SMALL, seed=1, prefill=4), cache_cap=16)
+    m2.page_kv()
+    with pytest.raises(DimensionError):  # already paged
+        m2.page_kv()
     # cluster 1 keeps a whole 32K-position sequence on one CTA: more pages than the producer holds
     cfg1 = LlamaConfig(n_layers=1, hidden=512, n_heads=4, head_dim=128, inter=1024, vocab=512, cluster=1)
     m1 = LlamaDecoder.random(cfg1, cache_cap=32768, seed=2)
